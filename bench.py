@@ -1,0 +1,435 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200-native LKV eviction path (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], "C2"): Llama-3-8B-shaped cache, 32 layers x
+8 KV heads x head_dim 128, 32 query heads, seq 32768, batch 1 per GPU, bf16,
+per-layer 128->64->1 GELU scorers, 256 LKV-H logits, retention 15% with budgets
+summing exactly to round(0.15 * 256 * 32768) = 1,258,291; then 128 decode steps.
+
+A step = one eviction pass: LKV-H budgets (K2) -> LKV-T scores (K1, tcgen05)
+-> per-head top-k + fused 16-byte gather into the ragged cache (K3+K4), all
+through the C ABI on one stream.  `value` = KV token-rows evicted per second
+(whole job: rows of all ranks / max-over-ranks device time).  Inputs (4.3 GB of
+K/V per GPU) exceed the 126 MB L2, so no flush is needed between steps.
+
+Multi-GPU (torchrun): one process per GPU, batch-sharded (each rank evicts its
+own sequence; no data-path collective), weak scaling.  NCCL is used only for the
+barrier and the max-over-ranks timing reduction.
+
+`--impl reference` times the reference algorithm's CPU restatement (oracle/,
+fp64, the reference's own code path restated in C) on all host cores over a
+bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "KV tokens/s evicted (score+budget+top-k+compact); decode-attn HBM GB/s"
+UNIT = "KV token-rows/s"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p.get("bf16_tflops", 1676.6)), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.gpu)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i]})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------------------------
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    import paper_2605_06676_b200 as lkv
+    from paper_2605_06676_b200 import synth
+
+    torch.cuda.set_device(local_rank)
+    dev = f"cuda:{local_rank}"
+    assert lkv.lib().lkv_device_check() == 0, lkv.lib().lkv_last_error()
+    cfg = synth.CONFIGS[args.config]
+    if args.ratio:
+        cfg = synth.Config(**{**cfg.__dict__, "ratio": args.ratio})
+    hbm_peak, tc_peak, peak_src = load_peaks()
+
+    # ---- inputs (per rank: its own sequence, seeded by rank) -------------------------------
+    cache = synth.make_cache(cfg, device=dev, seed=1000 + cfg.cid + 17 * rank)
+    scorers = synth.make_scorers(cfg, device=dev)
+    logits = synth.make_logits(cfg, device=dev)
+    n_seq, L, H, T, D = cache.shape
+    rows_per_step = sum(cache.seq_lens) * L * H
+    ev = lkv.Evictor(cache, scorers, logits, cfg.ratio, lkv.BUDGET_EXACT, decode_slack=cfg.decode_steps + 1,
+                     keep_scores=False)
+    lib = lkv.lib()
+    stream = torch.cuda.current_stream()
+    sp = C.c_void_p(stream.cuda_stream)
+    ws = ev.ws
+    cd, sd, rd = ev._cd, ev._sd, ev._rd
+    scores = ws_scores = torch.empty(n_seq, L, H, T, dtype=torch.float32, device=dev)
+
+    def stage_budgets():
+        lkv._check(lib.lkv_budgets(C.c_void_p(ev.logits.data_ptr()), L * H, cfg.ratio, lkv.BUDGET_EXACT, cd.seq_lens,
+                                   n_seq, ev.ragged.decode_slack, C.c_void_p(ev.ratios.data_ptr()),
+                                   C.c_void_p(ev.budgets.data_ptr()), C.c_void_p(ev.ragged.offsets.data_ptr()),
+                                   C.c_void_p(ws.ptr), ws.nbytes, sp))
+
+    def stage_score():
+        lkv._check(lib.lkv_score(C.byref(cd), C.byref(sd), C.c_void_p(ws_scores.data_ptr()), None, 0, sp))
+
+    def stage_select():
+        lkv._check(lib.lkv_select(C.byref(cd), C.c_void_p(scores.data_ptr()), C.c_void_p(ev.budgets.data_ptr()),
+                                  C.byref(rd), 1, C.c_void_p(ws.ptr), ws.nbytes, sp))
+
+    def step(evs=None):
+        if evs is not None:
+            evs[0].record(stream)
+        stage_budgets()
+        if evs is not None:
+            evs[1].record(stream)
+        stage_score()
+        if evs is not None:
+            evs[2].record(stream)
+        stage_select()
+        if evs is not None:
+            evs[3].record(stream)
+
+    # correctness gate before timing: device error latch + exact total
+    step()
+    ws.status()
+    kept = int(ev.ragged.lens.sum())
+    want_total = sum(round(cfg.ratio * L * H * t) for t in cache.seq_lens)
+    assert kept == want_total, (kept, want_total)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    launches0 = lib.lkv_launch_count()
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        for k in range(args.steps):
+            step(evs[k])
+        barrier()
+    launches = lib.lkv_launch_count() - launches0
+    ws.status()
+    total_ms = evs[0][0].elapsed_time(evs[-1][3])
+    t_budget = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
+    t_score = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
+    t_select = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
+    ms_step = total_ms / args.steps
+    if world > 1:
+        t = torch.tensor([ms_step], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_step = float(t.item())
+    value = rows_per_step * world / (ms_step / 1e3)
+
+    # ---- roofline of the dominant kernel (K1 scorer): algorithmic bytes per launch ------------
+    in_bytes = scorers.input * D * cache.keys.element_size()
+    score_bytes = rows_per_step * (in_bytes + 4)  # read x, write one fp32 score
+    score_gbs = score_bytes / (t_score / 1e3) / 1e9
+    hidden = scorers.w1.shape[2]
+    score_tflops = rows_per_step * (2 * scorers.input * D * hidden + 2 * hidden) / (t_score / 1e3) / 1e12
+    # whole-step algorithmic bytes: in_bytes + 8 + rho*(4*d*s + 4) per row
+    kept_rows = want_total
+    step_bytes = rows_per_step * (in_bytes + 8) + kept_rows * (4 * D * cache.keys.element_size() + 4)
+
+    # ---- end to end through the public API with HOST buffers -----------------------------------
+    e2e = None
+    if not args.no_e2e:
+        hk = torch.empty(cache.keys.shape, dtype=cache.keys.dtype, pin_memory=True)
+        hv = torch.empty_like(hk, pin_memory=True)
+        hk.copy_(cache.keys)
+        hv.copy_(cache.values)
+        out_rows = int(ev.ragged.capacity_rows)
+        ok = torch.empty(out_rows, D, dtype=cache.keys.dtype, pin_memory=True)
+        ov = torch.empty_like(ok, pin_memory=True)
+        op = torch.empty(out_rows, dtype=torch.int32, pin_memory=True)
+        oo = torch.empty(ev.ragged.offsets.numel(), dtype=torch.int64, pin_memory=True)
+
+        def e2e_step():
+            cache.keys.copy_(hk, non_blocking=True)
+            cache.values.copy_(hv, non_blocking=True)
+            ev.launch()
+            ok.copy_(ev.ragged.keys, non_blocking=True)
+            ov.copy_(ev.ragged.values, non_blocking=True)
+            op.copy_(ev.ragged.positions, non_blocking=True)
+            oo.copy_(ev.ragged.offsets, non_blocking=True)
+
+        e2e_steps = max(2, min(args.steps, 5))
+        for _ in range(2):
+            e2e_step()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            e2e_step()
+        e1.record(stream)
+        barrier()
+        ms_e2e = e0.elapsed_time(e1) / e2e_steps
+        if world > 1:
+            t = torch.tensor([ms_e2e], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms_e2e = float(t.item())
+        ws.status()
+        h2d = 2 * hk.numel() * hk.element_size()
+        d2h = 2 * ok.numel() * ok.element_size() + op.numel() * 4 + oo.numel() * 8
+        e2e = {"value": rows_per_step * world / (ms_e2e / 1e3), "unit": UNIT, "ms_per_step": ms_e2e,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "path": "pinned host K/V -> lkv_evict (C ABI) -> pinned host ragged cache"}
+        del hk, hv, ok, ov, op, oo
+
+    # ---- decode over the compressed cache --------------------------------------------------------
+    decode = None
+    if not args.no_decode:
+        rc = ev.ragged
+        rc.tokens_seen.copy_(torch.tensor(cache.seq_lens, dtype=torch.int32))
+        lens0 = rc.lens.clone()
+        G = cfg.n_q_heads // cfg.n_kv_heads
+        lkv.decode_plan(rc, G)
+        nsteps = cfg.decode_steps
+        qs = [synth.make_decode_inputs(cfg, s, device=dev, seed=rank) for s in range(2)]
+        out = torch.empty_like(qs[0][0])
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        # warm-up steps then reset the cache lengths so the timed steps see lens = budgets + s
+        for s in range(3):
+            q, k, v = qs[s % 2]
+            lkv.decode_step(rc, q, k, v, out=out, check=False)
+        rc.lens.copy_(lens0)
+        rc.tokens_seen.copy_(torch.tensor(cache.seq_lens, dtype=torch.int32))
+        barrier()
+        l0 = lib.lkv_launch_count()
+        e0.record(stream)
+        for s in range(nsteps):
+            q, k, v = qs[s % 2]
+            lkv.decode_step(rc, q, k, v, out=out, check=False)
+        e1.record(stream)
+        barrier()
+        rc._decode_ws.status()
+        dl = lib.lkv_launch_count() - l0
+        ms_dec = e0.elapsed_time(e1) / nsteps
+        esz = cache.keys.element_size()
+        # bytes read per step: retained K+V rows (mean over the steps incl. growth) + q/out/new k,v
+        mean_rows = int(lens0.sum()) + rc.n_heads * (nsteps + 1) / 2
+        dec_bytes = mean_rows * 2 * D * esz + 2 * q.numel() * esz + 2 * k.numel() * esz
+        dec_gbs = dec_bytes / (ms_dec / 1e3) / 1e9
+        decode = {"steps": nsteps, "ms_per_step": ms_dec, "hbm_gbs": dec_gbs, "bytes_per_step": int(dec_bytes),
+                  "frac_of_measured_hbm": dec_gbs / hbm_peak, "frac_of_8tbs_nominal": dec_gbs / 8000.0,
+                  "gpu_launches": int(dl), "note": "all 32 layers per launch; kernel = TMA + mma.sync split-K"}
+
+    # ---- CPU baseline (rank 0, N=1): the oracle port on a bounded sample ------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(cache, scorers, ev, n_threads=1, n_heads=args.cpu_heads)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded; BASELINE.json configs[1] shapes)",
+            "config": {"workload": f"C2: L{L} x H{H} x d{D}, t={T}, batch 1/GPU, R={cfg.ratio}, exact budgets",
+                       "rows_per_gpu_step": rows_per_step, "kept_rows_per_gpu_step": kept_rows,
+                       "scorer": "K-only 128->64->1 GELU-erf per layer", "parallelism": f"batch-sharded x{world}",
+                       "l2": "inputs (4.3 GB K/V per GPU) larger than L2; no flush"},
+            "stages_ms": {"budgets_K2": t_budget, "score_K1": t_score, "select_gather_K3K4": t_select},
+            "roofline": {"bound": "hbm", "kernel": "score_tc_kernel (K1)", "achieved": score_gbs, "peak": hbm_peak,
+                         "unit": "GB/s", "frac": score_gbs / hbm_peak, "traffic": None,
+                         "algorithmic_bytes_per_launch": int(score_bytes), "peak_source": peak_src,
+                         "tensor_tflops": score_tflops, "tensor_frac": score_tflops / tc_peak},
+            "step_roofline": {"algorithmic_bytes": int(step_bytes), "achieved_gbs": step_bytes / (ms_step / 1e3) / 1e9,
+                              "frac": step_bytes / (ms_step / 1e3) / 1e9 / hbm_peak},
+            "clocks": clk.summary(),
+            "gpu_launches": int(launches),
+            "e2e": e2e,
+            "decode": decode,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(cache, scorers, ev, n_threads=1, n_heads=8):
+    """Time the fp64 oracle port (oracle/lkv_oracle.c: score -> stable-sort top-k -> gather,
+    the reference's per-head loop, evictsim.cpp:161-215) on `n_heads` heads of this workload."""
+    import numpy as np
+    import torch
+
+    import oracle as O
+
+    n_seq, L, H, T, D = cache.shape
+    nh = min(n_heads, L * H)
+    K = cache.keys.reshape(-1, T, D)[:nh].contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+    V = cache.values.reshape(-1, T, D)[:nh].contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+    b = ev.budgets.reshape(-1)[:nh].cpu().numpy().astype(np.int32)
+    offs = np.zeros(nh + 1, np.int64)
+    offs[1:] = np.cumsum(b)
+    w1 = scorers.w1.to(torch.float64).cpu().numpy()
+    b1 = scorers.b1.to(torch.float64).cpu().numpy()
+    w2 = scorers.w2.to(torch.float64).cpu().numpy()
+    head_scorer = np.array([(h // H) * scorers.stride_layer + (h % H) * scorers.stride_head for h in range(nh)],
+                           np.int32)
+    t_per_head = np.full(nh, cache.seq_lens[0], np.int32)
+    t0 = time.perf_counter()
+    O.evict_heads(K, V, t_per_head, scorers.input, w1, b1, w2, scorers.activation, head_scorer, b, offs,
+                  n_threads=n_threads)
+    dt = time.perf_counter() - t0
+    rows = int(t_per_head.sum())
+    return {"value": rows / dt, "unit": UNIT, "cores": n_threads, "kind": "port",
+            "sample": f"{nh} heads x {cache.seq_lens[0]} rows of the same C2 workload (layer 0..), fp64 score + "
+                      f"stable-sort top-k + gather, {dt:.2f} s",
+            "seconds": dt}
+
+
+def run_reference(args, rank, world):
+    """The reference's CPU algorithm (oracle port of proj/src, fp64) on all host cores."""
+    import numpy as np
+
+    import oracle as O
+
+    if rank != 0:
+        return
+    ncores = os.cpu_count() or 1
+    from paper_2605_06676_b200.synth import CONFIGS
+
+    cfg = CONFIGS[args.config]
+    T, D, hidden = cfg.max_tokens, cfg.head_dim, cfg.hidden
+    rng = np.random.default_rng(1000 + cfg.cid)
+    nh = ncores  # one head per thread per step: a bounded sample of the workload
+    K = O.f32_to_bf16_bits(rng.standard_normal((nh, T, D), dtype=np.float32))
+    V = O.f32_to_bf16_bits(rng.standard_normal((nh, T, D), dtype=np.float32))
+    w1 = O.bf16_bits_to_f64(O.f32_to_bf16_bits((rng.standard_normal((1, D, hidden)) * 0.02).astype(np.float32)))
+    b1 = np.zeros((1, hidden))
+    w2 = (rng.standard_normal((1, hidden)) * 0.02).astype(np.float32).astype(np.float64)
+    logits = rng.standard_normal(cfg.n_layers * cfg.n_kv_heads) * cfg.logit_sigma
+    budgets_all = O.freeze_budgets_exact(O.allocate_budgets(logits, cfg.ratio), cfg.ratio, T)
+    b = budgets_all[:nh].astype(np.int32)
+    offs = np.zeros(nh + 1, np.int64)
+    offs[1:] = np.cumsum(b)
+    tph = np.full(nh, T, np.int32)
+    hs = np.zeros(nh, np.int32)
+
+    def one():
+        O.allocate_budgets(logits, cfg.ratio)
+        O.evict_heads(K, V, tph, 1, w1, b1, w2, O.GELU_ERF, hs, b, offs, n_threads=ncores)
+
+    for _ in range(max(args.warmup, 0)):
+        one()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        one()
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(times) / len(times)
+    rows = nh * T
+    value = rows / (ms / 1e3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded; BASELINE.json configs[1] shapes)", "impl": "reference",
+        "config": {"workload": f"C2 sample: {nh} heads x {T} rows (one head per host thread)",
+                   "parallelism": f"{ncores} host threads"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": ncores, "kind": "port",
+                         "sample": f"{nh} heads x {T} rows per step: fp64 LKV-H solve + scorer + stable-sort top-k + gather"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--ratio", type=float, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-decode", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-heads", type=int, default=8)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch
+
+            torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,205 @@
+/*
+ * lkv_b200.h -- C ABI of the B200-native LKV inference-time eviction path.
+ *
+ * This is the drop-in boundary: plain pointers, sizes and POD descriptors, no
+ * C++ or torch types.  It replaces the reference's C++ hot-path API in
+ * /root/reference/proj/include/lkv (all calls there are host-side, synchronous,
+ * fp64, exception-throwing):
+ *
+ *   lkv_budgets     <- allocate_budgets   policy.hpp:67  (policy.cpp:110-120)
+ *                      + freeze_budgets   policy.hpp:70  (policy.cpp:122-129)
+ *                      (+ soft_topk_forward / solve_threshold soft_topk.hpp:57-60)
+ *   lkv_score       <- token_scores       policy.hpp:73  (policy.cpp:131-136)
+ *   lkv_select      <- inference_select   policy.hpp:81  (policy.cpp:152-154)
+ *                      -> hard_topk       soft_topk.hpp:71 (soft_topk.cpp:191-201)
+ *   lkv_compact     <- cache_from_trace   model.hpp:99   (model.cpp:289-315) and the
+ *                      compaction loop of prefill_with_eviction (evictsim.cpp:202-215)
+ *   lkv_evict       <- prefill_with_eviction's score->select->compact loop
+ *                      (evictsim.hpp:74, evictsim.cpp:161-215), K/V-given form
+ *   lkv_decode_step <- decode_step's append + attention block (model.hpp:95,
+ *                      model.cpp:240-265) -> masked_attention_dense (attention.hpp:57)
+ *
+ * Status codes map 1:1 onto the reference's exception types
+ * (proj/include/lkv/errors.hpp:10-32); lkv_last_error() returns a thread-local
+ * message.  Every entry point is stream-ordered and asynchronous: host-side
+ * validation errors return immediately; device-side errors (non-finite scores,
+ * budgets outside [0, t], solve failures) are latched into the caller's
+ * workspace and returned by lkv_workspace_status(), which synchronises.
+ *
+ * Memory: the library never allocates or frees caller memory; every device
+ * buffer is caller-owned.  Dense caches are head-major
+ *   keys/values [n_seq][n_layers][n_kv_heads][max_tokens][head_dim]
+ * and a flat head id is (s * n_layers + l) * n_kv_heads + h.  The ragged
+ * (compacted) cache stores head i's rows at [offsets[i], offsets[i] + lens[i])
+ * with capacity offsets[i+1] - offsets[i] = budget_i + decode_slack.
+ *
+ * Target: NVIDIA B200 (sm_100a).  Built with nvcc -gencode arch=compute_100a,code=sm_100a.
+ */
+#ifndef LKV_B200_H
+#define LKV_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LKV_ABI_VERSION 1
+#define LKV_MAX_SEQ 256
+
+typedef struct CUstream_st* lkv_stream_t; /* identical to cudaStream_t */
+
+typedef enum lkv_status {
+    LKV_OK = 0,
+    LKV_ERR_CONTRACT = 1,        /* lkv::contract_error        errors.hpp:20-22 */
+    LKV_ERR_NUMERIC = 2,         /* lkv::numeric_error         errors.hpp:25-27 */
+    LKV_ERR_BUDGET = 3,          /* lkv::budget_error          errors.hpp:30-32 */
+    LKV_ERR_OVERFLOW_GUARD = 4,  /* lkv::overflow_guard_error  errors.hpp:35-37 */
+    LKV_ERR_DEGENERATE_MASK = 5, /* lkv::degenerate_mask_error errors.hpp:40-42 */
+    LKV_ERR_CUDA = 6,            /* CUDA runtime / launch failure (no reference analogue) */
+    LKV_ERR_UNSUPPORTED = 7      /* device is not sm_100 or shape outside the kernel envelope */
+} lkv_status;
+
+typedef enum lkv_dtype { LKV_F32 = 0, LKV_BF16 = 1 } lkv_dtype;
+typedef enum lkv_activation { LKV_ACT_SILU = 0, LKV_ACT_GELU_ERF = 1 } lkv_activation;
+typedef enum lkv_scorer_input {
+    LKV_SCORER_K = 1,  /* x = k            (BASELINE.json configs: head_dim -> hidden -> 1) */
+    LKV_SCORER_KV = 2  /* x = [k ; v]      (reference: policy.cpp:135, 2d -> d -> 1)        */
+} lkv_scorer_input;
+typedef enum lkv_budget_mode {
+    LKV_BUDGET_FLOOR = 0, /* freeze_budgets: floor(r * t), policy.cpp:126              */
+    LKV_BUDGET_EXACT = 1  /* floor + largest-remainder fix-up to llround(R * n * t)     */
+} lkv_budget_mode;
+
+/* Dense, pre-eviction cache (K already post-RoPE, evictsim.cpp:143). */
+typedef struct lkv_cache_desc {
+    int32_t n_seq;       /* 1 .. LKV_MAX_SEQ */
+    int32_t n_layers;
+    int32_t n_kv_heads;
+    int32_t head_dim;    /* multiple of 8 */
+    int64_t max_tokens;  /* T: row capacity per head in keys/values */
+    int32_t dtype;       /* lkv_dtype */
+    int32_t _pad;
+    const void* keys;    /* device */
+    const void* values;  /* device */
+    const int32_t* seq_lens; /* HOST [n_seq], 1 <= t_s <= max_tokens */
+} lkv_cache_desc;
+
+/* LKV-T token scorers u = act(x W1 + b1) . w2 (policy.hpp:24-32, no output bias). */
+typedef struct lkv_scorer_desc {
+    int32_t input;        /* lkv_scorer_input */
+    int32_t activation;   /* lkv_activation */
+    int32_t hidden;       /* 1..256; the tensor-core path needs a multiple of 16 */
+    int32_t n_scorers;
+    int32_t stride_layer; /* scorer id of (l, h) = l * stride_layer + h * stride_head */
+    int32_t stride_head;  /*   per-(l,h): (n_kv_heads, 1); per-layer: (1, 0)          */
+    const void* w1t;      /* device [n_scorers][hidden][in] in the cache dtype (W1 transposed) */
+    const float* b1;      /* device [n_scorers][hidden] */
+    const float* w2;      /* device [n_scorers][hidden] */
+} lkv_scorer_desc;
+
+/* Ragged compacted cache (KvCache/HeadCache, model.hpp:55-71). */
+typedef struct lkv_ragged_desc {
+    int32_t n_heads;       /* n_seq * n_layers * n_kv_heads */
+    int32_t head_dim;
+    int32_t dtype;
+    int32_t decode_slack;  /* rows reserved per head for decode appends */
+    int64_t capacity_rows; /* rows allocated in keys/values/positions */
+    int64_t* offsets;      /* device [n_heads + 1] */
+    int32_t* lens;         /* device [n_heads]: rows currently held */
+    void* keys;            /* device [capacity_rows][head_dim] */
+    void* values;          /* device [capacity_rows][head_dim] */
+    int32_t* positions;    /* device [capacity_rows]: original token index, strictly increasing */
+} lkv_ragged_desc;
+
+/* ---- library / errors -------------------------------------------------- */
+int lkv_abi_version(void);
+/* Number of CUDA kernels this library has launched in the process (bench accounting). */
+uint64_t lkv_launch_count(void);
+const char* lkv_last_error(void);
+const char* lkv_status_name(int status);
+/* LKV_OK when the current device is sm_100 (B200); LKV_ERR_UNSUPPORTED otherwise. */
+lkv_status lkv_device_check(void);
+
+/* Workspace: one caller-owned device buffer per in-flight call chain.  Its
+ * first bytes latch device-side errors.  lkv_workspace_status synchronises
+ * `stream`, returns the latched status (and clears it). */
+size_t lkv_workspace_bytes(const lkv_cache_desc* cache, int32_t n_logits);
+lkv_status lkv_workspace_init(void* workspace, size_t bytes, lkv_stream_t stream);
+lkv_status lkv_workspace_status(void* workspace, lkv_stream_t stream);
+
+/* Total rows a ragged cache needs (exact in LKV_BUDGET_EXACT mode, an upper
+ * bound in FLOOR mode): sum_s llround(R * n * t_s) + n_heads * decode_slack. */
+int64_t lkv_ragged_capacity(const lkv_cache_desc* cache, double target_ratio, int32_t decode_slack);
+
+/* ---- K2: LKV-H budgets -------------------------------------------------- */
+/* ratios = soft_topk(logits, k = R*n, tau = 1) (fp64, the reference's exact
+ * operation order); budgets[s*n + i] = freeze(ratios_i, seq_lens[s]) per mode;
+ * offsets (nullable) = exclusive scan of (budget + decode_slack), length
+ * n_seq*n + 1.  logits: device fp64 [n]; ratios (nullable): device fp64 [n].
+ * R outside (0,1) -> LKV_ERR_BUDGET. */
+lkv_status lkv_budgets(const double* logits, int32_t n, double target_ratio, int32_t mode,
+                       const int32_t* seq_lens, int32_t n_seq, int32_t decode_slack,
+                       double* ratios, int32_t* budgets, int64_t* offsets,
+                       void* workspace, size_t workspace_bytes, lkv_stream_t stream);
+
+/* Exclusive scan of (budgets[i] + decode_slack) -> offsets[n_heads+1] (device). */
+lkv_status lkv_ragged_offsets(const int32_t* budgets, int32_t n_heads, int32_t decode_slack,
+                              int64_t* offsets, lkv_stream_t stream);
+
+/* ---- K1: LKV-T scorer ------------------------------------------------------ */
+/* scores: device fp32 [n_heads][max_tokens]; rows >= t_s are left untouched.
+ * bf16 + head_dim 128 + hidden % 16 == 0 runs on tcgen05 tensor cores (TMA ->
+ * SMEM -> UMMA -> TMEM, activation and w2 reduction fused in the epilogue);
+ * other shapes run a SIMT kernel (fp32 inputs always do: TF32 would break the
+ * 1e-5 parity bar). */
+lkv_status lkv_score(const lkv_cache_desc* cache, const lkv_scorer_desc* scorer, float* scores,
+                     void* workspace, size_t workspace_bytes, lkv_stream_t stream);
+
+/* ---- K3: per-head top-k ----------------------------------------------------- */
+/* For every head keep the budgets[i] largest scores (ties -> lowest index,
+ * -0.0 == +0.0, NaN -> LKV_ERR_NUMERIC, budget outside [0, t] -> LKV_ERR_BUDGET),
+ * writing their positions ascending to out->positions[offsets[i] ...] and
+ * out->lens[i] = budgets[i].  out->offsets must already be filled.  With
+ * gather != 0 the kept K/V rows are also copied into out->keys/values in the
+ * same pass (fused K3 + K4; needs cache->keys/values). */
+lkv_status lkv_select(const lkv_cache_desc* cache, const float* scores, const int32_t* budgets,
+                      const lkv_ragged_desc* out, int32_t gather, void* workspace, size_t workspace_bytes,
+                      lkv_stream_t stream);
+
+/* ---- K4: compaction ---------------------------------------------------------- */
+/* Gathers rows positions[offsets[i] + r], r < lens[i], of head i from the dense
+ * cache into out->keys/values[offsets[i] + r] (16-byte vectorised). */
+lkv_status lkv_compact(const lkv_cache_desc* cache, const lkv_ragged_desc* out, lkv_stream_t stream);
+
+/* ---- fused: budgets -> score -> select -> compact ----------------------------- */
+/* scores_out, ratios_out, budgets_out may be NULL (workspace-backed). */
+lkv_status lkv_evict(const lkv_cache_desc* cache, const lkv_scorer_desc* scorer, const double* logits,
+                     double target_ratio, int32_t mode, const lkv_ragged_desc* out, float* scores_out,
+                     double* ratios_out, int32_t* budgets_out, void* workspace, size_t workspace_bytes,
+                     lkv_stream_t stream);
+
+/* ---- K5: decode over the ragged cache ------------------------------------------- */
+/* lkv_decode_plan splits every head's capacity into 256-row work items (once
+ * per eviction, after offsets are final).  lkv_decode_step then runs one decode
+ * step for every (seq, layer): append new_k/new_v (post-RoPE) and position
+ * tokens_seen[s] to each KV head (lens += 1, capacity checked), and for each
+ * query head qh attend over kv = qh / (n_q_heads / n_kv_heads):
+ * out = softmax(scale * q K^T) V over all lens rows (causal = false, no mask).
+ * q, out: [n_seq][n_layers][n_q_heads][head_dim]; new_k/new_v:
+ * [n_seq][n_layers][n_kv_heads][head_dim]; all in the cache dtype.
+ * tokens_seen: device int32 [n_seq], incremented by the call.
+ * bf16 requires head_dim 128 and G = n_q_heads / n_kv_heads <= 16. */
+size_t lkv_decode_workspace_bytes(const lkv_ragged_desc* cache, int32_t group_size);
+lkv_status lkv_decode_plan(const lkv_ragged_desc* cache, void* workspace, size_t workspace_bytes,
+                           lkv_stream_t stream);
+lkv_status lkv_decode_step(const lkv_ragged_desc* cache, int32_t n_seq, int32_t n_layers,
+                           int32_t n_kv_heads, int32_t n_q_heads, const void* q, const void* new_k,
+                           const void* new_v, int32_t* tokens_seen, void* out, double scale,
+                           void* workspace, size_t workspace_bytes, lkv_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LKV_B200_H */

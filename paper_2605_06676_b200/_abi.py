@@ -1,0 +1,89 @@
+"""ctypes binding of the C ABI in include/lkv_b200.h (liblkv_b200.so).
+
+The library is the product; this module only declares its structs and entry
+points so the Python harness (tests, bench) can drive it with torch device
+buffers.  Loading fails loudly when the library is missing -- there is no
+fallback of any kind.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblkv_b200.so")
+
+LKV_OK, CONTRACT, NUMERIC, BUDGET, OVERFLOW_GUARD, DEGENERATE_MASK, CUDA, UNSUPPORTED = range(8)
+F32, BF16 = 0, 1
+SILU, GELU_ERF = 0, 1
+SCORER_K, SCORER_KV = 1, 2
+BUDGET_FLOOR, BUDGET_EXACT = 0, 1
+MAX_SEQ = 256
+
+EXPORTED = [
+    "lkv_abi_version", "lkv_launch_count", "lkv_last_error", "lkv_status_name", "lkv_device_check", "lkv_workspace_bytes",
+    "lkv_workspace_init", "lkv_workspace_status", "lkv_ragged_capacity", "lkv_budgets", "lkv_ragged_offsets",
+    "lkv_score", "lkv_select", "lkv_compact", "lkv_evict", "lkv_decode_workspace_bytes", "lkv_decode_plan",
+    "lkv_decode_step",
+]
+
+
+class CacheDesc(C.Structure):
+    _fields_ = [("n_seq", C.c_int32), ("n_layers", C.c_int32), ("n_kv_heads", C.c_int32), ("head_dim", C.c_int32),
+                ("max_tokens", C.c_int64), ("dtype", C.c_int32), ("_pad", C.c_int32), ("keys", C.c_void_p),
+                ("values", C.c_void_p), ("seq_lens", C.POINTER(C.c_int32))]
+
+
+class ScorerDesc(C.Structure):
+    _fields_ = [("input", C.c_int32), ("activation", C.c_int32), ("hidden", C.c_int32), ("n_scorers", C.c_int32),
+                ("stride_layer", C.c_int32), ("stride_head", C.c_int32), ("w1t", C.c_void_p), ("b1", C.c_void_p),
+                ("w2", C.c_void_p)]
+
+
+class RaggedDesc(C.Structure):
+    _fields_ = [("n_heads", C.c_int32), ("head_dim", C.c_int32), ("dtype", C.c_int32), ("decode_slack", C.c_int32),
+                ("capacity_rows", C.c_int64), ("offsets", C.c_void_p), ("lens", C.c_void_p), ("keys", C.c_void_p),
+                ("values", C.c_void_p), ("positions", C.c_void_p)]
+
+
+_lib = None
+
+
+def load():
+    """Load liblkv_b200.so (built in-tree by __graft_entry__.build())."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `make -C paper_2605_06676_b200` "
+                          "(or __graft_entry__.build()); there is no fallback")
+    L = C.CDLL(LIB_PATH)
+    vp, sz, i32, i64, dbl = C.c_void_p, C.c_size_t, C.c_int32, C.c_int64, C.c_double
+    P = C.POINTER
+    L.lkv_abi_version.restype = C.c_int
+    L.lkv_launch_count.restype = C.c_uint64
+    L.lkv_last_error.restype = C.c_char_p
+    L.lkv_status_name.restype = C.c_char_p
+    L.lkv_status_name.argtypes = [C.c_int]
+    L.lkv_device_check.restype = C.c_int
+    L.lkv_workspace_bytes.restype = sz
+    L.lkv_workspace_bytes.argtypes = [P(CacheDesc), i32]
+    L.lkv_workspace_init.argtypes = [vp, sz, vp]
+    L.lkv_workspace_status.argtypes = [vp, vp]
+    L.lkv_ragged_capacity.restype = i64
+    L.lkv_ragged_capacity.argtypes = [P(CacheDesc), dbl, i32]
+    L.lkv_budgets.argtypes = [vp, i32, dbl, i32, P(i32), i32, i32, vp, vp, vp, vp, sz, vp]
+    L.lkv_ragged_offsets.argtypes = [vp, i32, i32, vp, vp]
+    L.lkv_score.argtypes = [P(CacheDesc), P(ScorerDesc), vp, vp, sz, vp]
+    L.lkv_select.argtypes = [P(CacheDesc), vp, vp, P(RaggedDesc), i32, vp, sz, vp]
+    L.lkv_compact.argtypes = [P(CacheDesc), P(RaggedDesc), vp]
+    L.lkv_evict.argtypes = [P(CacheDesc), P(ScorerDesc), vp, dbl, i32, P(RaggedDesc), vp, vp, vp, vp, sz, vp]
+    L.lkv_decode_workspace_bytes.restype = sz
+    L.lkv_decode_workspace_bytes.argtypes = [P(RaggedDesc), i32]
+    L.lkv_decode_plan.argtypes = [P(RaggedDesc), vp, sz, vp]
+    L.lkv_decode_step.argtypes = [P(RaggedDesc), i32, i32, i32, i32, vp, vp, vp, vp, vp, dbl, vp, sz, vp]
+    for name in ["lkv_workspace_init", "lkv_workspace_status", "lkv_budgets", "lkv_ragged_offsets", "lkv_score",
+                 "lkv_select", "lkv_compact", "lkv_evict", "lkv_decode_plan", "lkv_decode_step"]:
+        getattr(L, name).restype = C.c_int
+    _lib = L
+    return L

@@ -1,0 +1,527 @@
+// c_api.cu -- the extern "C" drop-in boundary (include/lkv_b200.h).
+//
+// Host-side validation mirrors the reference's exception behaviour (budget /
+// contract / numeric errors, errors.hpp:10-32); device-side failures are
+// latched into the caller's workspace.  No allocation of caller memory, no
+// CPU fallback: every compute entry point launches sm_100a kernels or fails.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/lkv_b200.h"
+#include "kernels.cuh"
+
+
+using namespace lkv_dev;
+
+namespace {
+
+thread_local std::string g_err;
+
+lkv_status fail(lkv_status code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+lkv_status cuda_fail(cudaError_t e, const char* where) {
+    return fail(LKV_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define LKV_CUDA(call, where)                            \
+    do {                                                 \
+        cudaError_t e_ = (call);                         \
+        if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+    } while (0)
+
+int num_sms() {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+}
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
+
+// ---- TMA descriptor encoding (driver entry point, no -lcuda) ----------------------------------
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+// 2-D bf16 tensor [rows][inner] (row-major), box = 64 x box_rows, 128-byte swizzle.
+lkv_status make_map_bf16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint32_t box_rows) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return fail(LKV_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    if ((reinterpret_cast<uintptr_t>(base) & 15) != 0) return fail(LKV_ERR_CONTRACT, "TMA base must be 16-byte aligned");
+    cuuint64_t dims[2] = {inner, rows};
+    cuuint64_t strides[1] = {inner * 2};
+    cuuint32_t box[2] = {64, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(LKV_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return LKV_OK;
+}
+
+// ---- descriptor validation ---------------------------------------------------------------------
+lkv_status check_cache(const lkv_cache_desc* c, bool need_kv) {
+    if (!c) return fail(LKV_ERR_CONTRACT, "cache descriptor is null");
+    if (c->n_seq < 1 || c->n_seq > LKV_MAX_SEQ) return fail(LKV_ERR_CONTRACT, "n_seq must lie in [1, LKV_MAX_SEQ]");
+    if (c->n_layers < 1 || c->n_kv_heads < 1) return fail(LKV_ERR_CONTRACT, "n_layers and n_kv_heads must be >= 1");
+    if (c->head_dim < 8 || c->head_dim % 8) return fail(LKV_ERR_CONTRACT, "head_dim must be a positive multiple of 8");
+    if (c->dtype != LKV_F32 && c->dtype != LKV_BF16) return fail(LKV_ERR_CONTRACT, "unknown dtype");
+    if (c->max_tokens < 1) return fail(LKV_ERR_CONTRACT, "max_tokens must be >= 1");
+    if (!c->seq_lens) return fail(LKV_ERR_CONTRACT, "seq_lens (host) is null");
+    for (int s = 0; s < c->n_seq; ++s)
+        if (c->seq_lens[s] < 1 || c->seq_lens[s] > c->max_tokens)
+            return fail(LKV_ERR_CONTRACT, "seq_lens[s] must lie in [1, max_tokens]");
+    const int64_t heads = (int64_t)c->n_seq * c->n_layers * c->n_kv_heads;
+    if (heads * c->max_tokens >= (int64_t(1) << 31)) return fail(LKV_ERR_CONTRACT, "cache rows exceed 2^31");
+    if (need_kv && (!c->keys || !c->values)) return fail(LKV_ERR_CONTRACT, "keys/values are null");
+    return LKV_OK;
+}
+
+SeqTable make_seq(const lkv_cache_desc* c) {
+    SeqTable s;
+    memset(&s, 0, sizeof s);
+    s.n_seq = c->n_seq;
+    s.n_layers = c->n_layers;
+    s.n_kv_heads = c->n_kv_heads;
+    s.head_dim = c->head_dim;
+    s.T = c->max_tokens;
+    for (int i = 0; i < c->n_seq; ++i) s.len[i] = c->seq_lens[i];
+    return s;
+}
+
+int64_t n_heads_of(const lkv_cache_desc* c) { return (int64_t)c->n_seq * c->n_layers * c->n_kv_heads; }
+
+// ---- workspace layout -----------------------------------------------------------------------------
+struct EvictWs {
+    size_t err, ratios, budgets, scores, hist, state, chunk_gt, chunk_out, chunk_eqb, cands, total;
+};
+
+EvictWs evict_layout(const lkv_cache_desc* c, int n_logits) {
+    EvictWs w;
+    const int64_t H = n_heads_of(c);
+    int64_t chunks = 0;
+    for (int s = 0; s < c->n_seq; ++s) chunks += (int64_t)c->n_layers * c->n_kv_heads * ((c->seq_lens[s] + 4095) / 4096);
+    size_t o = 0;
+    w.err = o;
+    o = align_up(o + sizeof(ErrWord));
+    w.ratios = o;
+    o = align_up(o + sizeof(double) * (size_t)(n_logits > 0 ? n_logits : 1));
+    w.budgets = o;
+    o = align_up(o + sizeof(int32_t) * (size_t)H);
+    w.scores = o;
+    o = align_up(o + sizeof(float) * (size_t)H * c->max_tokens);
+    w.hist = o;
+    o = align_up(o + sizeof(uint32_t) * 2048 * (size_t)H);
+    w.state = o;
+    o = align_up(o + sizeof(HeadSel) * (size_t)H);
+    w.chunk_gt = o;
+    o = align_up(o + sizeof(uint32_t) * (size_t)chunks);
+    w.chunk_out = o;
+    o = align_up(o + sizeof(uint32_t) * (size_t)chunks);
+    w.chunk_eqb = o;
+    o = align_up(o + sizeof(uint32_t) * (size_t)chunks);
+    w.cands = o;
+    o = align_up(o + sizeof(uint32_t) * (size_t)H * c->max_tokens);
+    w.total = o;
+    return w;
+}
+
+template <typename T>
+T* at(void* ws, size_t off) {
+    return reinterpret_cast<T*>(static_cast<char*>(ws) + off);
+}
+
+lkv_status check_ws(void* ws, size_t have, size_t need) {
+    if (!ws) return fail(LKV_ERR_CONTRACT, "workspace is null");
+    if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return fail(LKV_ERR_CONTRACT, "workspace must be 256-byte aligned");
+    if (have < need) return fail(LKV_ERR_CONTRACT, "workspace too small (" + std::to_string(have) + " < " + std::to_string(need) + ")");
+    return LKV_OK;
+}
+
+lkv_status check_scorer(const lkv_scorer_desc* s, const lkv_cache_desc* c) {
+    if (!s) return fail(LKV_ERR_CONTRACT, "scorer descriptor is null");
+    if (s->input != LKV_SCORER_K && s->input != LKV_SCORER_KV) return fail(LKV_ERR_CONTRACT, "scorer input must be K or KV");
+    if (s->activation != LKV_ACT_SILU && s->activation != LKV_ACT_GELU_ERF) return fail(LKV_ERR_CONTRACT, "unknown activation");
+    if (s->hidden < 1 || s->hidden > 256) return fail(LKV_ERR_CONTRACT, "scorer hidden must lie in [1, 256]");
+    if (s->n_scorers < 1 || !s->w1t || !s->b1 || !s->w2) return fail(LKV_ERR_CONTRACT, "scorer weights are null");
+    const int64_t lo = std::min<int64_t>(0, (int64_t)(c->n_layers - 1) * s->stride_layer) +
+                       std::min<int64_t>(0, (int64_t)(c->n_kv_heads - 1) * s->stride_head);
+    const int64_t hi = std::max<int64_t>(0, (int64_t)(c->n_layers - 1) * s->stride_layer) +
+                       std::max<int64_t>(0, (int64_t)(c->n_kv_heads - 1) * s->stride_head);
+    if (lo < 0 || hi >= s->n_scorers) return fail(LKV_ERR_CONTRACT, "scorer index of some (layer, head) out of range");
+    return LKV_OK;
+}
+
+lkv_status check_ragged(const lkv_ragged_desc* r, int64_t n_heads, int head_dim, int dtype, bool need_rows) {
+    if (!r) return fail(LKV_ERR_CONTRACT, "ragged descriptor is null");
+    if (r->n_heads != n_heads) return fail(LKV_ERR_CONTRACT, "ragged n_heads mismatch");
+    if (r->head_dim != head_dim || r->dtype != dtype) return fail(LKV_ERR_CONTRACT, "ragged head_dim/dtype mismatch");
+    if (!r->offsets || !r->lens || !r->positions) return fail(LKV_ERR_CONTRACT, "ragged offsets/lens/positions are null");
+    if (need_rows && (!r->keys || !r->values)) return fail(LKV_ERR_CONTRACT, "ragged keys/values are null");
+    if (r->decode_slack < 0) return fail(LKV_ERR_CONTRACT, "decode_slack must be >= 0");
+    return LKV_OK;
+}
+
+// ---- internal launchers shared by lkv_score / lkv_evict ---------------------------------------------
+lkv_status run_score(const lkv_cache_desc* c, const lkv_scorer_desc* s, float* scores, cudaStream_t stream) {
+    ScoreParams p;
+    memset(&p, 0, sizeof p);
+    p.seq = make_seq(c);
+    p.in_mode = s->input;
+    p.act = s->activation;
+    p.hidden = s->hidden;
+    p.stride_layer = s->stride_layer;
+    p.stride_head = s->stride_head;
+    p.keys = c->keys;
+    p.values = c->values;
+    p.w1t = s->w1t;
+    p.b1 = s->b1;
+    p.w2 = s->w2;
+    p.scores = scores;
+    if (score_tc_supported(c->dtype, c->head_dim, s->hidden, s->input)) {
+        CUtensorMap mk, mv, mw;
+        const uint64_t rows = (uint64_t)n_heads_of(c) * c->max_tokens;
+        lkv_status st = make_map_bf16(&mk, c->keys, c->head_dim, rows, 128);
+        if (st) return st;
+        st = make_map_bf16(&mv, c->values, c->head_dim, rows, 128);
+        if (st) return st;
+        st = make_map_bf16(&mw, s->w1t, (uint64_t)s->input * c->head_dim, (uint64_t)s->n_scorers * s->hidden,
+                           (uint32_t)s->hidden);
+        if (st) return st;
+        LKV_CUDA(launch_score_tc(p, mk, mv, mw, num_sms(), stream), "score (tcgen05)");
+    } else {
+        const int in = s->input * c->head_dim;
+        if (score_simt_smem_bytes(in, s->hidden) > 200 * 1024)
+            return fail(LKV_ERR_UNSUPPORTED, "scorer too large for the SIMT kernel");
+        LKV_CUDA(launch_score_simt(p, c->dtype, num_sms(), stream), "score (simt)");
+    }
+    return LKV_OK;
+}
+
+lkv_status run_select(const lkv_cache_desc* c, const float* scores, const int32_t* budgets,
+                      const lkv_ragged_desc* out, void* ws, const EvictWs& w, bool gather, cudaStream_t stream) {
+    for (int s = 0; s < c->n_seq; ++s)
+        if (c->seq_lens[s] > 4096 * 1024) return fail(LKV_ERR_UNSUPPORTED, "top-k supports t <= 4M rows per head");
+    SelectParams p;
+    memset(&p, 0, sizeof p);
+    p.seq = make_seq(c);
+    p.scores = scores;
+    p.budgets = budgets;
+    p.hist = at<uint32_t>(ws, w.hist);
+    p.state = at<HeadSel>(ws, w.state);
+    p.chunk_gt = at<uint32_t>(ws, w.chunk_gt);
+    p.chunk_out = at<uint32_t>(ws, w.chunk_out);
+    p.chunk_eqb = at<uint32_t>(ws, w.chunk_eqb);
+    p.cands = at<uint32_t>(ws, w.cands);
+    p.offsets = out->offsets;
+    p.out_pos = out->positions;
+    p.out_lens = out->lens;
+    p.keys = c->keys;
+    p.values = c->values;
+    p.out_keys = out->keys;
+    p.out_values = out->values;
+    p.row_bytes = c->head_dim * (c->dtype == LKV_F32 ? 4 : 2);
+    p.gather = gather ? 1 : 0;
+    p.err = at<ErrWord>(ws, w.err);
+    LKV_CUDA(launch_select(p, (int)n_heads_of(c), stream), "select");
+    return LKV_OK;
+}
+
+// ---- decode workspace -------------------------------------------------------------------------------
+struct DecodeWs {
+    size_t err, n_items, item_base, items, part_m, part_l, part_o, total;
+    int64_t max_items;
+};
+DecodeWs decode_layout(const lkv_ragged_desc* r, int G) {
+    DecodeWs w;
+    w.max_items = r->capacity_rows / 256 + r->n_heads;
+    size_t o = 0;
+    w.err = o;
+    o = align_up(o + sizeof(ErrWord));
+    w.n_items = o;
+    o = align_up(o + sizeof(int32_t));
+    w.item_base = o;
+    o = align_up(o + sizeof(int32_t) * (size_t)r->n_heads);
+    w.items = o;
+    o = align_up(o + sizeof(DecodeItem) * (size_t)w.max_items);
+    w.part_m = o;
+    o = align_up(o + sizeof(float) * (size_t)w.max_items * G);
+    w.part_l = o;
+    o = align_up(o + sizeof(float) * (size_t)w.max_items * G);
+    w.part_o = o;
+    o = align_up(o + sizeof(float) * (size_t)w.max_items * G * r->head_dim);
+    w.total = o;
+    return w;
+}
+
+}  // namespace
+
+// =====================================================================================================
+extern "C" {
+
+int lkv_abi_version(void) { return LKV_ABI_VERSION; }
+
+uint64_t lkv_launch_count(void) { return lkv_dev::launch_count(); }
+
+const char* lkv_last_error(void) { return g_err.c_str(); }
+
+const char* lkv_status_name(int s) {
+    switch (s) {
+        case LKV_OK: return "ok";
+        case LKV_ERR_CONTRACT: return "contract_error";
+        case LKV_ERR_NUMERIC: return "numeric_error";
+        case LKV_ERR_BUDGET: return "budget_error";
+        case LKV_ERR_OVERFLOW_GUARD: return "overflow_guard_error";
+        case LKV_ERR_DEGENERATE_MASK: return "degenerate_mask_error";
+        case LKV_ERR_CUDA: return "cuda_error";
+        case LKV_ERR_UNSUPPORTED: return "unsupported";
+    }
+    return "unknown";
+}
+
+lkv_status lkv_device_check(void) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    if (major != 10 || minor != 0)
+        return fail(LKV_ERR_UNSUPPORTED, "this library is built for sm_100a (B200); found sm_" + std::to_string(major) +
+                                             std::to_string(minor));
+    return LKV_OK;
+}
+
+size_t lkv_workspace_bytes(const lkv_cache_desc* cache, int32_t n_logits) {
+    if (check_cache(cache, false)) return 0;
+    return evict_layout(cache, n_logits).total;
+}
+
+lkv_status lkv_workspace_init(void* ws, size_t bytes, lkv_stream_t stream) {
+    if (!ws || bytes < sizeof(ErrWord)) return fail(LKV_ERR_CONTRACT, "workspace is null or too small");
+    LKV_CUDA(cudaMemsetAsync(ws, 0, sizeof(ErrWord), (cudaStream_t)stream), "workspace init");
+    return LKV_OK;
+}
+
+lkv_status lkv_workspace_status(void* ws, lkv_stream_t stream) {
+    if (!ws) return fail(LKV_ERR_CONTRACT, "workspace is null");
+    ErrWord h{0, 0};
+    LKV_CUDA(cudaMemcpyAsync(&h, ws, sizeof h, cudaMemcpyDeviceToHost, (cudaStream_t)stream), "status read");
+    LKV_CUDA(cudaStreamSynchronize((cudaStream_t)stream), "stream sync");
+    if (h.code != 0) {
+        LKV_CUDA(cudaMemsetAsync(ws, 0, sizeof(ErrWord), (cudaStream_t)stream), "status clear");
+        LKV_CUDA(cudaStreamSynchronize((cudaStream_t)stream), "stream sync");
+        return fail((lkv_status)h.code, std::string("device-side ") + lkv_status_name(h.code) + " (detail " +
+                                            std::to_string(h.detail) + ")");
+    }
+    return LKV_OK;
+}
+
+int64_t lkv_ragged_capacity(const lkv_cache_desc* c, double R, int32_t slack) {
+    if (check_cache(c, false)) return -1;
+    const int64_t n = (int64_t)c->n_layers * c->n_kv_heads;
+    int64_t rows = 0;
+    for (int s = 0; s < c->n_seq; ++s) rows += llround(R * n * c->seq_lens[s]) + n;  // +n: FLOOR-mode margin
+    return rows + n_heads_of(c) * (int64_t)slack;
+}
+
+lkv_status lkv_budgets(const double* logits, int32_t n, double R, int32_t mode, const int32_t* seq_lens, int32_t n_seq,
+                       int32_t slack, double* ratios, int32_t* budgets, int64_t* offsets, void* ws, size_t ws_bytes,
+                       lkv_stream_t stream) {
+    if (!(R > 0.0 && R < 1.0)) return fail(LKV_ERR_BUDGET, "target ratio must lie in (0,1)");  // policy.cpp:111
+    if (n < 1 || n > 3072) return fail(LKV_ERR_CONTRACT, "allocate_budgets: need 1 <= n <= 3072 head logits");
+    if (mode != LKV_BUDGET_FLOOR && mode != LKV_BUDGET_EXACT) return fail(LKV_ERR_CONTRACT, "unknown budget mode");
+    if (n_seq < 1 || n_seq > LKV_MAX_SEQ || !seq_lens) return fail(LKV_ERR_CONTRACT, "bad sequence table");
+    for (int s = 0; s < n_seq; ++s)
+        if (seq_lens[s] < 1) return fail(LKV_ERR_CONTRACT, "freeze_budgets: t must be >= 1");  // policy.cpp:123
+    if (!logits || !budgets) return fail(LKV_ERR_CONTRACT, "logits/budgets are null");
+    if (slack < 0) return fail(LKV_ERR_CONTRACT, "decode_slack must be >= 0");
+    lkv_status st = check_ws(ws, ws_bytes, sizeof(ErrWord));
+    if (st) return st;
+    BudgetParams p;
+    memset(&p, 0, sizeof p);
+    p.logits = logits;
+    p.n = n;
+    p.mode = mode;
+    p.R = R;
+    p.n_seq = n_seq;
+    p.slack = slack;
+    p.ratios_out = ratios;
+    p.budgets_out = budgets;
+    p.offsets_out = offsets;
+    p.err = at<ErrWord>(ws, 0);
+    for (int s = 0; s < n_seq; ++s) p.seq_len[s] = seq_lens[s];
+    LKV_CUDA(launch_budgets(p, (cudaStream_t)stream), "budgets");
+    return LKV_OK;
+}
+
+lkv_status lkv_ragged_offsets(const int32_t* budgets, int32_t n_heads, int32_t slack, int64_t* offsets,
+                              lkv_stream_t stream) {
+    if (!budgets || !offsets || n_heads < 1 || slack < 0) return fail(LKV_ERR_CONTRACT, "bad ragged_offsets arguments");
+    LKV_CUDA(launch_offsets(budgets, n_heads, slack, offsets, (cudaStream_t)stream), "offsets");
+    return LKV_OK;
+}
+
+lkv_status lkv_score(const lkv_cache_desc* c, const lkv_scorer_desc* s, float* scores, void* ws, size_t ws_bytes,
+                     lkv_stream_t stream) {
+    lkv_status st = check_cache(c, true);
+    if (st) return st;
+    if ((st = check_scorer(s, c))) return st;
+    if (!scores) return fail(LKV_ERR_CONTRACT, "scores is null");
+    (void)ws;
+    (void)ws_bytes;
+    return run_score(c, s, scores, (cudaStream_t)stream);
+}
+
+lkv_status lkv_select(const lkv_cache_desc* c, const float* scores, const int32_t* budgets, const lkv_ragged_desc* out,
+                      int32_t gather, void* ws, size_t ws_bytes, lkv_stream_t stream) {
+    lkv_status st = check_cache(c, gather != 0);
+    if (st) return st;
+    if ((st = check_ragged(out, n_heads_of(c), c->head_dim, c->dtype, gather != 0))) return st;
+    if (!scores || !budgets) return fail(LKV_ERR_CONTRACT, "scores/budgets are null");
+    const EvictWs w = evict_layout(c, 1);
+    if ((st = check_ws(ws, ws_bytes, w.total))) return st;
+    return run_select(c, scores, budgets, out, ws, w, gather != 0, (cudaStream_t)stream);
+}
+
+lkv_status lkv_compact(const lkv_cache_desc* c, const lkv_ragged_desc* out, lkv_stream_t stream) {
+    lkv_status st = check_cache(c, true);
+    if (st) return st;
+    if ((st = check_ragged(out, n_heads_of(c), c->head_dim, c->dtype, true))) return st;
+    CompactParams p;
+    memset(&p, 0, sizeof p);
+    p.seq = make_seq(c);
+    p.offsets = out->offsets;
+    p.lens = out->lens;
+    p.positions = out->positions;
+    p.keys = c->keys;
+    p.values = c->values;
+    p.out_keys = out->keys;
+    p.out_values = out->values;
+    p.row_bytes = c->head_dim * (c->dtype == LKV_F32 ? 4 : 2);
+    p.err = nullptr;
+    // compaction has no workspace: contract violations trap into a static latch
+    static ErrWord* s_latch = nullptr;
+    if (!s_latch) LKV_CUDA(cudaMalloc(&s_latch, sizeof(ErrWord)), "latch alloc");
+    p.err = s_latch;
+    LKV_CUDA(launch_compact(p, (int)n_heads_of(c), (cudaStream_t)stream), "compact");
+    return LKV_OK;
+}
+
+lkv_status lkv_evict(const lkv_cache_desc* c, const lkv_scorer_desc* s, const double* logits, double R, int32_t mode,
+                     const lkv_ragged_desc* out, float* scores_out, double* ratios_out, int32_t* budgets_out, void* ws,
+                     size_t ws_bytes, lkv_stream_t stream) {
+    lkv_status st = check_cache(c, true);
+    if (st) return st;
+    if ((st = check_scorer(s, c))) return st;
+    if ((st = check_ragged(out, n_heads_of(c), c->head_dim, c->dtype, true))) return st;
+    const int n = c->n_layers * c->n_kv_heads;
+    const EvictWs w = evict_layout(c, n);
+    if ((st = check_ws(ws, ws_bytes, w.total))) return st;
+    cudaStream_t strm = (cudaStream_t)stream;
+    int32_t* budgets = budgets_out ? budgets_out : at<int32_t>(ws, w.budgets);
+    double* ratios = ratios_out ? ratios_out : at<double>(ws, w.ratios);
+    float* scores = scores_out ? scores_out : at<float>(ws, w.scores);
+    // K2: budgets + ragged offsets (budget + decode slack per head)
+    st = lkv_budgets(logits, n, R, mode, c->seq_lens, c->n_seq, out->decode_slack, ratios, budgets, out->offsets, ws,
+                     ws_bytes, stream);
+    if (st) return st;
+    // K1: scores
+    if ((st = run_score(c, s, scores, strm))) return st;
+    // K3 + K4: select and gather into the ragged cache
+    return run_select(c, scores, budgets, out, ws, w, true, strm);
+}
+
+size_t lkv_decode_workspace_bytes(const lkv_ragged_desc* r, int32_t G) {
+    if (!r || G < 1) return 0;
+    return decode_layout(r, G).total;
+}
+
+lkv_status lkv_decode_plan(const lkv_ragged_desc* r, void* ws, size_t ws_bytes, lkv_stream_t stream) {
+    if (!r || !r->offsets || r->n_heads < 1) return fail(LKV_ERR_CONTRACT, "bad ragged descriptor");
+    const DecodeWs w = decode_layout(r, 1);
+    lkv_status st = check_ws(ws, ws_bytes, w.items + sizeof(DecodeItem) * (size_t)w.max_items);
+    if (st) return st;
+    LKV_CUDA(launch_decode_plan(r->offsets, r->n_heads, at<DecodeItem>(ws, w.items), at<int32_t>(ws, w.item_base),
+                                at<int32_t>(ws, w.n_items), (cudaStream_t)stream),
+             "decode plan");
+    return LKV_OK;
+}
+
+lkv_status lkv_decode_step(const lkv_ragged_desc* r, int32_t n_seq, int32_t n_layers, int32_t n_kv_heads,
+                           int32_t n_q_heads, const void* q, const void* new_k, const void* new_v,
+                           int32_t* tokens_seen, void* out, double scale, void* ws, size_t ws_bytes,
+                           lkv_stream_t stream) {
+    if (n_seq < 1 || n_layers < 1 || n_kv_heads < 1 || n_q_heads < n_kv_heads || n_q_heads % n_kv_heads)
+        return fail(LKV_ERR_CONTRACT, "decode: n_q_heads must be a positive multiple of n_kv_heads");
+    const int64_t H = (int64_t)n_seq * n_layers * n_kv_heads;
+    lkv_status st = check_ragged(r, H, r ? r->head_dim : 0, r ? r->dtype : 0, true);
+    if (st) return st;
+    if (!q || !new_k || !new_v || !tokens_seen || !out) return fail(LKV_ERR_CONTRACT, "decode: null buffer");
+    if (!(scale > 0.0) || !std::isfinite(scale)) return fail(LKV_ERR_CONTRACT, "decode: scale must be positive");
+    const int G = n_q_heads / n_kv_heads;
+    if (r->dtype == LKV_BF16 && (r->head_dim != 128 || G > 16))
+        return fail(LKV_ERR_UNSUPPORTED, "bf16 decode needs head_dim 128 and group size <= 16");
+    if (r->dtype == LKV_F32 && (size_t)G * (r->head_dim + 256) * 4 > 200 * 1024)
+        return fail(LKV_ERR_UNSUPPORTED, "fp32 decode: group too large");
+    const DecodeWs w = decode_layout(r, G);
+    if ((st = check_ws(ws, ws_bytes, w.total))) return st;
+    DecodeParams p;
+    memset(&p, 0, sizeof p);
+    p.n_heads = (int)H;
+    p.n_kv_heads = n_kv_heads;
+    p.n_q_heads = n_q_heads;
+    p.G = G;
+    p.head_dim = r->head_dim;
+    p.n_items = at<int32_t>(ws, w.n_items);
+    p.max_items = (int32_t)w.max_items;
+    p.scale_log2 = (float)(scale * 1.4426950408889634);
+    p.offsets = r->offsets;
+    p.lens = r->lens;
+    p.positions = r->positions;
+    p.keys = r->keys;
+    p.values = r->values;
+    p.q = q;
+    p.new_k = new_k;
+    p.new_v = new_v;
+    p.tokens_seen = tokens_seen;
+    p.heads_per_seq = n_layers * n_kv_heads;
+    p.out = out;
+    p.items = at<DecodeItem>(ws, w.items);
+    p.item_base = at<int32_t>(ws, w.item_base);
+    p.part_m = at<float>(ws, w.part_m);
+    p.part_l = at<float>(ws, w.part_l);
+    p.part_o = at<float>(ws, w.part_o);
+    p.err = at<ErrWord>(ws, w.err);
+    CUtensorMap mk, mv;
+    if (r->dtype == LKV_BF16) {
+        if ((st = make_map_bf16(&mk, r->keys, 128, (uint64_t)r->capacity_rows, 64))) return st;
+        if ((st = make_map_bf16(&mv, r->values, 128, (uint64_t)r->capacity_rows, 64))) return st;
+    }
+    LKV_CUDA(launch_decode(p, r->dtype, &mk, &mv, num_sms(), (cudaStream_t)stream), "decode");
+    return LKV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,491 @@
+// decode.cu -- K5: GQA decode attention over the ragged compacted cache.
+//
+// Reference: decode_step's attention block (model.cpp:240-265): append the new
+// (post-RoPE) k, v and position to every KV head, then for every query head qh
+// attend over kv = qh / G with n_q = 1, causal = false, no mask, scale 1/sqrt(d)
+// (masked_attention_dense, attention.cpp:46-94).  The tiling follows the
+// online-softmax form of masked_attention_blocked (attention.cpp:96-143).
+//
+// B200 design (HBM-bound, 4-8 flop/byte):
+//  * work items = (head, 256-row chunk) over each head's capacity, planned once
+//    per eviction (decode_plan_kernel); a persistent grid walks them;
+//  * per CTA: one TMA producer warp streams 64-row K+V stages (128-byte
+//    swizzle, 32 KB) through a 4-stage mbarrier ring; four consumer warps each
+//    take 16 rows of a stage and run S = Q K^T and O += P V on tensor cores
+//    (mma.sync m16n8k16 bf16, ldmatrix from the swizzled tiles), every K/V
+//    byte read once for all G query heads of the group;
+//  * the chunk containing the appended row patches it into shared memory and
+//    writes it (plus its position) into the cache, so no separate append pass;
+//  * split-K partials (m, l, o) are merged by decode_combine_kernel, which also
+//    advances lens and tokens_seen.
+#include <math.h>
+
+#include "kernels.cuh"
+
+namespace lkv_dev {
+
+constexpr int kDecCh = 256;         // rows per work item
+constexpr int kDecStageRows = 64;   // rows per pipeline stage
+constexpr int kDecStages = 4;
+constexpr int kDecConsumers = 4;    // consumer warps (16 rows of a stage each)
+constexpr int kDecThreads = (kDecConsumers + 1) * 32;
+constexpr int kDecMaxG = 16;
+
+
+
+// ---- plan: work items over each head's capacity (once per eviction) -------------------------
+__global__ void __launch_bounds__(1024) decode_plan_kernel(const int64_t* offsets, int n_heads, DecodeItem* items,
+                                                           int32_t* item_base, int32_t* n_items_out) {
+    __shared__ uint32_t s_scan[33];
+    __shared__ int32_t s_carry;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (int base = 0; base < n_heads; base += 1024) {
+        const int h = base + threadIdx.x;
+        uint32_t nch = 0;
+        if (h < n_heads) {
+            const int64_t cap = offsets[h + 1] - offsets[h];
+            nch = (uint32_t)((cap + kDecCh - 1) / kDecCh);
+        }
+        uint32_t tot;
+        const uint32_t ex = block_exclusive_scan<1024>(nch, s_scan, &tot);
+        if (h < n_heads) {
+            const int b0 = s_carry + (int)ex;
+            item_base[h] = b0;
+            for (uint32_t c = 0; c < nch; ++c) items[b0 + c] = DecodeItem{h, (int32_t)c};
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry += (int32_t)tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *n_items_out = s_carry;
+}
+
+// ---- helpers ---------------------------------------------------------------------------------
+__device__ __forceinline__ void ldmatrix_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldmatrix_x4_trans(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                                  uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+
+// byte offset of (row, 16-byte chunk q in 0..15) inside a stage tile stored as two
+// 64-row x 128-byte boxes with the TMA 128-byte swizzle
+__device__ __forceinline__ uint32_t sw_off(int row, int q) {
+    return (uint32_t)((q >> 3) * (kDecStageRows * 128) + row * 128 + (((q & 7) ^ (row & 7)) << 4));
+}
+
+// ---- bf16 attention kernel (tensor cores) ------------------------------------------------------
+__global__ void __launch_bounds__(kDecThreads, 1)
+    decode_attn_bf16_kernel(const __grid_constant__ DecodeParams p, const __grid_constant__ CUtensorMap tmap_k,
+                            const __grid_constant__ CUtensorMap tmap_v) {
+    constexpr int kStageBytes = 2 * kDecStageRows * 256;  // K + V, 64 rows x 256 B each
+    extern __shared__ unsigned char smem_dyn[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kDecStages * kStageBytes);
+    uint64_t* empty = full + kDecStages;
+    float* red = reinterpret_cast<float*>(empty + kDecStages);  // [consumers][G][D + 2]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int G = p.G;
+    const int D = 128;
+    const int n_items = *p.n_items;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kDecStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], kDecConsumers);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    if (warp == kDecConsumers) {
+        // ===================== producer =====================
+        if (lane == 0) {
+            tma_prefetch_desc(&tmap_k);
+            tma_prefetch_desc(&tmap_v);
+            const uint64_t pol = l2_policy_evict_first();
+            int st = 0;
+            uint32_t ph = 0;
+            for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+                const DecodeItem wi = p.items[it];
+                const int len_new = p.lens[wi.head] + 1;
+                const int r0 = wi.chunk * kDecCh;
+                if (r0 >= len_new) continue;
+                const int rows = min(kDecCh, len_new - r0);
+                const int64_t grow0 = p.offsets[wi.head] + r0;
+                for (int sr = 0; sr < rows; sr += kDecStageRows) {
+                    mbar_wait(&empty[st], ph ^ 1);
+                    mbar_arrive_expect_tx(&full[st], kStageBytes);
+                    unsigned char* dst = smem + st * kStageBytes;
+                    const int y = (int)(grow0 + sr);
+                    tma_load_2d(dst, &tmap_k, &full[st], 0, y, pol);
+                    tma_load_2d(dst + kDecStageRows * 128, &tmap_k, &full[st], 64, y, pol);
+                    tma_load_2d(dst + 2 * kDecStageRows * 128, &tmap_v, &full[st], 0, y, pol);
+                    tma_load_2d(dst + 3 * kDecStageRows * 128, &tmap_v, &full[st], 64, y, pol);
+                    if (++st == kDecStages) {
+                        st = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    // ===================== consumers =====================
+    const int g = lane >> 2;       // fragment row (query head within the group)
+    const int cq = (lane & 3) * 2;  // fragment column pair
+    int st = 0;
+    uint32_t ph = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const DecodeItem wi = p.items[it];
+        const int head = wi.head;
+        const int len_old = p.lens[head];
+        const int len_new = len_old + 1;
+        const int r0 = wi.chunk * kDecCh;
+        if (r0 >= len_new) continue;
+        const int rows = min(kDecCh, len_new - r0);
+        const int64_t off = p.offsets[head];
+        const bool has_new = (len_old >= r0) && (len_old < r0 + kDecCh);
+        if (has_new && off + len_new > p.offsets[head + 1]) {
+            if (threadIdx.x == 0) latch_error(p.err, LKV_ERR_CONTRACT, head);
+        }
+        const int sl = head / p.n_kv_heads, kvh = head - sl * p.n_kv_heads;
+        const __nv_bfloat16* qp = static_cast<const __nv_bfloat16*>(p.q) + ((size_t)sl * p.n_q_heads + kvh * G) * D;
+
+        // Q fragments (rows g and g+8 of the padded 16-row tile)
+        uint32_t qa[8][4];
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            const int c0 = kk * 16 + cq;
+            const uint32_t* r_lo = reinterpret_cast<const uint32_t*>(qp + (size_t)g * D);
+            const uint32_t* r_hi = reinterpret_cast<const uint32_t*>(qp + (size_t)(g + 8) * D);
+            qa[kk][0] = g < G ? __ldg(r_lo + (c0 >> 1)) : 0u;
+            qa[kk][1] = g + 8 < G ? __ldg(r_hi + (c0 >> 1)) : 0u;
+            qa[kk][2] = g < G ? __ldg(r_lo + ((c0 + 8) >> 1)) : 0u;
+            qa[kk][3] = g + 8 < G ? __ldg(r_hi + ((c0 + 8) >> 1)) : 0u;
+        }
+        float o[16][4];
+#pragma unroll
+        for (int n = 0; n < 16; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+        float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;
+
+        for (int sr = 0; sr < rows; sr += kDecStageRows) {
+            mbar_wait(&full[st], ph);
+            unsigned char* sbase = smem + st * kStageBytes;
+            const uint32_t kbase = smem_u32(sbase);
+            const uint32_t vbase = kbase + 2 * kDecStageRows * 128;
+            const int wr0 = warp * 16;  // this warp's 16 rows inside the stage
+            // patch the appended row (it is not in the cache yet)
+            if (has_new) {
+                const int nr = len_old - r0 - sr;  // row inside this stage
+                if (nr >= wr0 && nr < wr0 + 16) {
+                    const int hq = lane & 15;
+                    const bool isv = lane >= 16;
+                    const uint4* src = static_cast<const uint4*>(isv ? p.new_v : p.new_k) + (size_t)head * 16;
+                    const uint4 v = __ldg(src + hq);
+                    *reinterpret_cast<uint4*>(sbase + (isv ? 2 * kDecStageRows * 128 : 0) + sw_off(nr, hq)) = v;
+                    uint4* dstg = static_cast<uint4*>(isv ? p.values : p.keys) + (size_t)(off + len_old) * 16;
+                    dstg[hq] = v;
+                    if (lane == 0) p.positions[off + len_old] = p.tokens_seen[sl / (p.heads_per_seq / p.n_kv_heads)];
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                }
+            }
+            const int valid = min(kDecStageRows, rows - sr) - wr0;  // rows of this warp that exist
+            if (valid > 0 && valid < 16) {
+                // rows past the chunk end hold other heads' data or never-written slack:
+                // zero their V so P = 0 cannot meet a NaN/Inf pattern in the MMA
+                for (int e = lane; e < (16 - valid) * 16; e += 32) {
+                    const int row = wr0 + valid + (e >> 4);
+                    *reinterpret_cast<uint4*>(sbase + 2 * kDecStageRows * 128 + sw_off(row, e & 15)) =
+                        make_uint4(0u, 0u, 0u, 0u);
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+            }
+            if (valid > 0) {
+                // ---- S = Q K^T for 16 rows (two n8 tiles)
+                float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const int j = lane >> 3;
+                    const int row = wr0 + ((j >> 1) << 3) + (lane & 7);
+                    const int q = kk * 2 + (j & 1);
+                    uint32_t b0, b1, b2, b3;
+                    ldmatrix_x4(kbase + sw_off(row, q), b0, b1, b2, b3);
+                    mma_bf16_16816(s0, qa[kk], b0, b1);
+                    mma_bf16_16816(s1, qa[kk], b2, b3);
+                }
+                // ---- mask, online softmax (log2 domain)
+                float sv[8] = {s0[0], s0[1], s1[0], s1[1], s0[2], s0[3], s1[2], s1[3]};
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const int col = ((e & 2) ? 8 : 0) + cq + (e & 1);
+                    sv[e] = col < valid ? sv[e] * p.scale_log2 : -INFINITY;
+                }
+                float mx_lo = fmaxf(fmaxf(sv[0], sv[1]), fmaxf(sv[2], sv[3]));
+                float mx_hi = fmaxf(fmaxf(sv[4], sv[5]), fmaxf(sv[6], sv[7]));
+                mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 1));
+                mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 2));
+                mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 1));
+                mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 2));
+                const float mn_lo = fmaxf(m_lo, mx_lo), mn_hi = fmaxf(m_hi, mx_hi);
+                const float a_lo = (mn_lo == -INFINITY) ? 1.f : exp2f(m_lo - mn_lo);
+                const float a_hi = (mn_hi == -INFINITY) ? 1.f : exp2f(m_hi - mn_hi);
+                m_lo = mn_lo;
+                m_hi = mn_hi;
+                float pv[8];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) pv[e] = (mn_lo == -INFINITY) ? 0.f : exp2f(sv[e] - mn_lo);
+#pragma unroll
+                for (int e = 4; e < 8; ++e) pv[e] = (mn_hi == -INFINITY) ? 0.f : exp2f(sv[e] - mn_hi);
+                l_lo = l_lo * a_lo + (pv[0] + pv[1] + pv[2] + pv[3]);
+                l_hi = l_hi * a_hi + (pv[4] + pv[5] + pv[6] + pv[7]);
+#pragma unroll
+                for (int n = 0; n < 16; ++n) {
+                    o[n][0] *= a_lo;
+                    o[n][1] *= a_lo;
+                    o[n][2] *= a_hi;
+                    o[n][3] *= a_hi;
+                }
+                // P as the A operand (k = the 16 rows)
+                uint32_t pa[4];
+                pa[0] = pack_bf16(pv[0], pv[1]);  // row g,   cols cq..   (rows 0-7)
+                pa[1] = pack_bf16(pv[4], pv[5]);  // row g+8, cols cq..
+                pa[2] = pack_bf16(pv[2], pv[3]);  // row g,   cols 8+cq.. (rows 8-15)
+                pa[3] = pack_bf16(pv[6], pv[7]);  // row g+8, cols 8+cq..
+                // ---- O += P V
+#pragma unroll
+                for (int n2 = 0; n2 < 8; ++n2) {
+                    const int j = lane >> 3;
+                    const int row = wr0 + ((j & 1) << 3) + (lane & 7);
+                    const int q = n2 * 2 + (j >> 1);
+                    uint32_t b0, b1, b2, b3;
+                    ldmatrix_x4_trans(vbase + sw_off(row, q), b0, b1, b2, b3);
+                    mma_bf16_16816(o[2 * n2], pa, b0, b1);
+                    mma_bf16_16816(o[2 * n2 + 1], pa, b2, b3);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+            if (++st == kDecStages) {
+                st = 0;
+                ph ^= 1;
+            }
+        }
+        // ---- merge the 4 consumer warps (rows g < G live in the lo half; g+8 in the hi half)
+        l_lo += __shfl_xor_sync(0xffffffffu, l_lo, 1);
+        l_lo += __shfl_xor_sync(0xffffffffu, l_lo, 2);
+        l_hi += __shfl_xor_sync(0xffffffffu, l_hi, 1);
+        l_hi += __shfl_xor_sync(0xffffffffu, l_hi, 2);
+        const int stride = D + 2;
+        float* rw = red + (size_t)warp * kDecMaxG * stride;
+        if (g < G) {
+#pragma unroll
+            for (int n = 0; n < 16; ++n) {
+                rw[g * stride + n * 8 + cq] = o[n][0];
+                rw[g * stride + n * 8 + cq + 1] = o[n][1];
+            }
+            if ((lane & 3) == 0) {
+                rw[g * stride + D] = m_lo;
+                rw[g * stride + D + 1] = l_lo;
+            }
+        }
+        if (g + 8 < G) {
+#pragma unroll
+            for (int n = 0; n < 16; ++n) {
+                rw[(g + 8) * stride + n * 8 + cq] = o[n][2];
+                rw[(g + 8) * stride + n * 8 + cq + 1] = o[n][3];
+            }
+            if ((lane & 3) == 0) {
+                rw[(g + 8) * stride + D] = m_hi;
+                rw[(g + 8) * stride + D + 1] = l_hi;
+            }
+        }
+        named_bar_sync(1, kDecConsumers * 32);
+        for (int e = threadIdx.x; e < G * D; e += kDecConsumers * 32) {
+            const int gg = e / D, dd = e - gg * D;
+            float M = -INFINITY;
+#pragma unroll
+            for (int w = 0; w < kDecConsumers; ++w) M = fmaxf(M, red[(size_t)w * kDecMaxG * stride + gg * stride + D]);
+            float L = 0.f, acc = 0.f;
+#pragma unroll
+            for (int w = 0; w < kDecConsumers; ++w) {
+                const float* r = red + (size_t)w * kDecMaxG * stride + gg * stride;
+                const float f = (r[D] == -INFINITY) ? 0.f : exp2f(r[D] - M);
+                L += r[D + 1] * f;
+                acc += r[dd] * f;
+            }
+            p.part_o[((size_t)it * G + gg) * D + dd] = acc;
+            if (dd == 0) {
+                p.part_m[(size_t)it * G + gg] = M;
+                p.part_l[(size_t)it * G + gg] = L;
+            }
+        }
+        named_bar_sync(1, kDecConsumers * 32);
+    }
+}
+
+// ---- fp32 attention kernel (SIMT; correctness configs) --------------------------------------------
+constexpr int kDecSimtThreads = 128;
+
+__global__ void __launch_bounds__(kDecSimtThreads) decode_attn_f32_kernel(const __grid_constant__ DecodeParams p) {
+    extern __shared__ float sm[];
+    const int D = p.head_dim, G = p.G;
+    float* qs = sm;                 // [G][D]
+    float* sc = qs + G * D;         // [G][kDecCh]
+    const int it = blockIdx.x;
+    if (it >= *p.n_items) return;
+    const DecodeItem wi = p.items[it];
+    const int head = wi.head;
+    const int len_old = p.lens[head];
+    const int len_new = len_old + 1;
+    const int r0 = wi.chunk * kDecCh;
+    if (r0 >= len_new) return;
+    const int rows = min(kDecCh, len_new - r0);
+    const int64_t off = p.offsets[head];
+    const bool has_new = len_old >= r0 && len_old < r0 + kDecCh;
+    if (has_new && off + len_new > p.offsets[head + 1]) {
+        if (threadIdx.x == 0) latch_error(p.err, LKV_ERR_CONTRACT, head);
+        return;
+    }
+    const int sl = head / p.n_kv_heads, kvh = head - sl * p.n_kv_heads;
+    const float* qp = static_cast<const float*>(p.q) + ((size_t)sl * p.n_q_heads + kvh * G) * D;
+    for (int e = threadIdx.x; e < G * D; e += kDecSimtThreads) qs[e] = qp[e];
+    float* K = static_cast<float*>(p.keys) + (size_t)off * D;
+    float* V = static_cast<float*>(p.values) + (size_t)off * D;
+    const float* nk = static_cast<const float*>(p.new_k) + (size_t)head * D;
+    const float* nv = static_cast<const float*>(p.new_v) + (size_t)head * D;
+    if (has_new) {
+        for (int e = threadIdx.x; e < D; e += kDecSimtThreads) {
+            K[(size_t)len_old * D + e] = nk[e];
+            V[(size_t)len_old * D + e] = nv[e];
+        }
+        if (threadIdx.x == 0) p.positions[off + len_old] = p.tokens_seen[sl / (p.heads_per_seq / p.n_kv_heads)];
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int r = warp; r < rows; r += kDecSimtThreads / 32) {
+        const int row = r0 + r;
+        const float* kr = (row == len_old) ? nk : K + (size_t)row * D;
+        for (int gg = 0; gg < G; ++gg) {
+            float acc = 0.f;
+            for (int c = lane; c < D; c += 32) acc = fmaf(qs[gg * D + c], kr[c], acc);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane == 0) sc[gg * kDecCh + r] = acc * p.scale_log2;
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < G * D; e += kDecSimtThreads) {
+        const int gg = e / D, dd = e - gg * D;
+        float M = -INFINITY;
+        for (int r = 0; r < rows; ++r) M = fmaxf(M, sc[gg * kDecCh + r]);
+        float L = 0.f, acc = 0.f;
+        for (int r = 0; r < rows; ++r) {
+            const float w = exp2f(sc[gg * kDecCh + r] - M);
+            const int row = r0 + r;
+            const float v = (row == len_old) ? nv[dd] : V[(size_t)row * D + dd];
+            L += w;
+            acc = fmaf(w, v, acc);
+        }
+        p.part_o[((size_t)it * G + gg) * D + dd] = acc;
+        if (dd == 0) {
+            p.part_m[(size_t)it * G + gg] = M;
+            p.part_l[(size_t)it * G + gg] = L;
+        }
+    }
+}
+
+// ---- combine split-K partials; advance lens and tokens_seen ------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) decode_combine_kernel(const __grid_constant__ DecodeParams p) {
+    const int head = blockIdx.x;
+    const int D = p.head_dim, G = p.G;
+    const int len_new = p.lens[head] + 1;
+    const int nch = (len_new + kDecCh - 1) / kDecCh;
+    const int base = p.item_base[head];
+    const int sl = head / p.n_kv_heads, kvh = head - sl * p.n_kv_heads;
+    T* out = static_cast<T*>(p.out) + ((size_t)sl * p.n_q_heads + kvh * G) * D;
+    for (int e = threadIdx.x; e < G * D; e += blockDim.x) {
+        const int gg = e / D, dd = e - gg * D;
+        float M = -INFINITY;
+        for (int c = 0; c < nch; ++c) M = fmaxf(M, p.part_m[(size_t)(base + c) * G + gg]);
+        float L = 0.f, acc = 0.f;
+        for (int c = 0; c < nch; ++c) {
+            const size_t i = (size_t)(base + c) * G + gg;
+            const float f = exp2f(p.part_m[i] - M);
+            L += p.part_l[i] * f;
+            acc += p.part_o[i * D + dd] * f;
+        }
+        const float v = acc / L;
+        if constexpr (sizeof(T) == 2) out[(size_t)gg * D + dd] = __float2bfloat16_rn(v);
+        else out[(size_t)gg * D + dd] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        p.lens[head] = len_new;
+        const int hps = p.heads_per_seq;
+        if (head % hps == 0) atomicAdd(&p.tokens_seen[head / hps], 1);
+    }
+}
+
+// ---- host launchers ---------------------------------------------------------------------------------
+cudaError_t launch_decode_plan(const int64_t* offsets, int n_heads, DecodeItem* items, int32_t* item_base,
+                               int32_t* n_items, cudaStream_t stream) {
+    decode_plan_kernel<<<1, 1024, 0, stream>>>(offsets, n_heads, items, item_base, n_items);
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+size_t decode_bf16_smem() {
+    return 1024 + kDecStages * (2 * kDecStageRows * 256) + 2 * kDecStages * 8 +
+           (size_t)kDecConsumers * kDecMaxG * (128 + 2) * 4;
+}
+
+cudaError_t launch_decode(const DecodeParams& p, int dtype, const CUtensorMap* mk, const CUtensorMap* mv, int num_sms,
+                          cudaStream_t stream) {
+    if (p.max_items == 0) return cudaSuccess;
+    if (dtype == LKV_BF16) {
+        const size_t smem = decode_bf16_smem();
+        cudaError_t e = cudaFuncSetAttribute(decode_attn_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        const int grid = min(p.max_items, num_sms);
+        decode_attn_bf16_kernel<<<grid, kDecThreads, smem, stream>>>(p, *mk, *mv);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        decode_combine_kernel<__nv_bfloat16><<<p.n_heads, 256, 0, stream>>>(p);
+        note_launches(2);
+    } else {
+        const size_t smem = ((size_t)p.G * p.head_dim + (size_t)p.G * kDecCh) * sizeof(float);
+        cudaError_t e = cudaFuncSetAttribute(decode_attn_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        decode_attn_f32_kernel<<<p.max_items, kDecSimtThreads, smem, stream>>>(p);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        decode_combine_kernel<float><<<p.n_heads, 256, 0, stream>>>(p);
+        note_launches(2);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace lkv_dev

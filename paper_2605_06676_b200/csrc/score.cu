@@ -1,0 +1,382 @@
+// score.cu -- K1: LKV-T token scorer  u = act(x W1 + b1) . w2   (policy.cpp:30-34,131-136)
+//
+// Two kernels:
+//  * score_tc_kernel  (bf16, head_dim 128, hidden % 16 == 0): persistent,
+//    warp-specialised tcgen05 kernel.  Warp 0 streams 128-row K (and V) tiles
+//    with TMA (128-byte swizzle) into a multi-stage shared-memory ring; warp 1
+//    issues tcgen05.mma (M=128, N=hidden, K=16) into a double-buffered TMEM
+//    accumulator; two 4-warp epilogue groups drain TMEM with tcgen05.ld
+//    (thread = row), add b1, apply SiLU / GELU-erf and reduce against w2 in
+//    registers, writing one fp32 score per row.  QK^T is never formed.
+//  * score_simt_kernel (fp32 inputs, or shapes outside the tensor-core
+//    envelope): FP32 SIMT, warp per row.  TF32 would break the 1e-5 bar.
+#include <math.h>
+
+#include "kernels.cuh"
+
+namespace lkv_dev {
+
+
+__device__ __forceinline__ float act_f32(int act, float h) {
+    if (act == LKV_ACT_SILU) return h / (1.0f + __expf(-h));
+    return 0.5f * h * (1.0f + erff(h * 0.70710678118654752f));
+}
+
+template <int ACT>
+__device__ __forceinline__ float act_t(float h) {
+    if constexpr (ACT == LKV_ACT_SILU) return h / (1.0f + __expf(-h));
+    else return 0.5f * h * (1.0f + erff(h * 0.70710678118654752f));
+}
+
+struct TileInfo {
+    int head;      // flat head
+    int row0;      // first row inside the head
+    int t;         // tokens of this head
+    int scorer;
+};
+
+__device__ __forceinline__ TileInfo decode_tile(const ScoreParams& p, int tile, int tile_rows) {
+    int s = 0;
+    while (s + 1 < p.seq.n_seq && p.tile_base[s + 1] <= tile) ++s;
+    const int t = p.seq.len[s];
+    const int tph = (t + tile_rows - 1) / tile_rows;
+    const int local = tile - p.tile_base[s];
+    const int hs = local / tph;
+    const int j = local - hs * tph;
+    const int H = p.seq.n_kv_heads;
+    const int l = hs / H, h = hs - l * H;
+    TileInfo ti;
+    ti.head = s * p.seq.n_layers * H + hs;
+    ti.row0 = j * tile_rows;
+    ti.t = t;
+    ti.scorer = l * p.stride_layer + h * p.stride_head;
+    return ti;
+}
+
+// ============================================================================
+// tcgen05 kernel
+// ============================================================================
+constexpr int kTcRows = 128;     // UMMA M
+constexpr int kTcThreads = 384;  // 12 warps: TMA, MMA, TMEM alloc, spare, 2 x 4 epilogue
+
+template <int N, int NBOX>
+struct TcCfg {
+    static constexpr int kABox = kTcRows * 128;            // bytes of one 128-row x 64-col box
+    static constexpr int kAStage = NBOX * kABox;           // one tile (k or [k;v])
+    static constexpr int kWBox = N * 128;
+    static constexpr int kW = NBOX * kWBox;
+    static constexpr int kStages = (NBOX == 2) ? 5 : 2;
+    static constexpr int kTmemCols = (2 * N <= 32) ? 32 : (2 * N <= 64) ? 64 : (2 * N <= 128) ? 128 : (2 * N <= 256) ? 256 : 512;
+    static constexpr int kSmem = kStages * kAStage + kW + 256 + 1024;  // + barriers + alignment slack
+};
+
+template <int N, int NBOX, int ACT>
+__global__ void __launch_bounds__(kTcThreads, 1)
+    score_tc_kernel(const __grid_constant__ ScoreParams p, const __grid_constant__ CUtensorMap tmap_k,
+                    const __grid_constant__ CUtensorMap tmap_v, const __grid_constant__ CUtensorMap tmap_w,
+                    int total_tiles) {
+    using Cfg = TcCfg<N, NBOX>;
+    constexpr int S = Cfg::kStages;
+    extern __shared__ unsigned char smem_dyn[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+    unsigned char* sA = smem;
+    unsigned char* sW = smem + S * Cfg::kAStage;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sW + Cfg::kW);
+    uint64_t* full = bars;              // [S]
+    uint64_t* empty = bars + S;         // [S]
+    uint64_t* tfull = bars + 2 * S;     // [2]
+    uint64_t* tempty = bars + 2 * S + 2;  // [2]
+    uint64_t* wfull = bars + 2 * S + 4;
+    uint64_t* wempty = bars + 2 * S + 5;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 6);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    // contiguous tile range of this CTA (tiles of a head, heads of a layer, stay together)
+    const int t_begin = (int)((int64_t)total_tiles * blockIdx.x / gridDim.x);
+    const int t_end = (int)((int64_t)total_tiles * (blockIdx.x + 1) / gridDim.x);
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 4);
+        }
+        mbar_init(wfull, 1);
+        mbar_init(wempty, 1);
+        fence_barrier_init();
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmap_k);
+        if (NBOX == 4) tma_prefetch_desc(&tmap_v);
+        tma_prefetch_desc(&tmap_w);
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, Cfg::kTmemCols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ===================== TMA producer =====================
+        if (lane == 0) {
+            const uint64_t pol_stream = l2_policy_evict_first();
+            const uint64_t pol_keep = l2_policy_evict_last();
+            int cur = -1, wloads = 0;
+            for (int tile = t_begin, i = 0; tile < t_end; ++tile, ++i) {
+                const TileInfo ti = decode_tile(p, tile, kTcRows);
+                if (ti.scorer != cur) {
+                    if (wloads > 0) mbar_wait(wempty, (wloads - 1) & 1);
+                    mbar_arrive_expect_tx(wfull, Cfg::kW);
+#pragma unroll
+                    for (int b = 0; b < NBOX; ++b)
+                        tma_load_2d(sW + b * Cfg::kWBox, &tmap_w, wfull, (b & 1) * 64 + (b >> 1) * 128, ti.scorer * N,
+                                    pol_keep);
+                    cur = ti.scorer;
+                    ++wloads;
+                }
+                const int st = i % S;
+                mbar_wait(&empty[st], ((i / S) & 1) ^ 1);
+                mbar_arrive_expect_tx(&full[st], Cfg::kAStage);
+                const int grow = (int)((int64_t)ti.head * p.seq.T + ti.row0);
+                unsigned char* dst = sA + st * Cfg::kAStage;
+                tma_load_2d(dst, &tmap_k, &full[st], 0, grow, pol_stream);
+                tma_load_2d(dst + Cfg::kABox, &tmap_k, &full[st], 64, grow, pol_stream);
+                if (NBOX == 4) {
+                    tma_load_2d(dst + 2 * Cfg::kABox, &tmap_v, &full[st], 0, grow, pol_stream);
+                    tma_load_2d(dst + 3 * Cfg::kABox, &tmap_v, &full[st], 64, grow, pol_stream);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer =====================
+        if (lane == 0) {
+            constexpr uint32_t idesc = umma_idesc_bf16(kTcRows, N);
+            const uint32_t a_base = smem_u32(sA);
+            const uint32_t w_base = smem_u32(sW);
+            int cur = -1, wuses = 0;
+            for (int tile = t_begin, i = 0; tile < t_end; ++tile, ++i) {
+                const TileInfo ti = decode_tile(p, tile, kTcRows);
+                if (ti.scorer != cur) {
+                    if (wuses > 0) umma_commit(wempty);  // old weights free once prior MMAs retire
+                    mbar_wait(wfull, wuses & 1);
+                    cur = ti.scorer;
+                    ++wuses;
+                }
+                const int acc = i & 1;
+                mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
+                const int st = i % S;
+                mbar_wait(&full[st], (i / S) & 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * N;
+                const uint32_t a_st = a_base + st * Cfg::kAStage;
+#pragma unroll
+                for (int kk = 0; kk < NBOX * 4; ++kk) {
+                    const int box = kk >> 2, within = kk & 3;
+                    const uint64_t adesc = umma_desc_sw128(a_st + box * Cfg::kABox + within * 32);
+                    const uint64_t bdesc = umma_desc_sw128(w_base + box * Cfg::kWBox + within * 32);
+                    umma_bf16(d_tmem, adesc, bdesc, idesc, kk > 0 ? 1u : 0u);
+                }
+                umma_commit(&empty[st]);   // smem slot free when these MMAs retire
+                umma_commit(&tfull[acc]);  // accumulator ready
+            }
+        }
+    } else if (warp >= 4) {
+        // ===================== epilogue (2 groups x 4 warps) =====================
+        const int grp = (warp - 4) >> 2;
+        const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+        const float* b1_all = p.b1;
+        const float* w2_all = p.w2;
+        for (int tile = t_begin + grp, i = grp; tile < t_end; tile += 2, i += 2) {
+            const TileInfo ti = decode_tile(p, tile, kTcRows);
+            const float* b1 = b1_all + (size_t)ti.scorer * N;
+            const float* w2 = w2_all + (size_t)ti.scorer * N;
+            mbar_wait(&tfull[grp], (i >> 1) & 1);
+            tc_fence_after();
+            const uint32_t taddr = tmem_base + (uint32_t(quarter * 32) << 16) + grp * N;
+            float s = 0.f;
+#pragma unroll
+            for (int c = 0; c < N / 32; ++c) {
+                uint32_t r[32];
+                tmem_ld_32x32b_x32(taddr + c * 32, r);
+                tmem_ld_wait();
+                if (c == N / 32 - 1) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[grp]);
+                }
+#pragma unroll
+                for (int q = 0; q < 32; ++q) {
+                    const float h = __uint_as_float(r[q]) + __ldg(b1 + c * 32 + q);
+                    s = fmaf(act_t<ACT>(h), __ldg(w2 + c * 32 + q), s);
+                }
+            }
+            const int row = ti.row0 + quarter * 32 + lane;
+            if (row < ti.t) p.scores[(size_t)ti.head * p.seq.T + row] = s;
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, Cfg::kTmemCols);
+    }
+}
+
+// ============================================================================
+// SIMT kernel (fp32 / generic shapes)
+// ============================================================================
+constexpr int kSimtThreads = 256;
+constexpr int kSimtRows = 256;  // rows per tile
+
+template <typename T>
+__device__ __forceinline__ float ld_elem(const T* p, size_t i);
+template <>
+__device__ __forceinline__ float ld_elem<float>(const float* p, size_t i) { return __ldg(p + i); }
+template <>
+__device__ __forceinline__ float ld_elem<__nv_bfloat16>(const __nv_bfloat16* p, size_t i) {
+    return __bfloat162float(p[i]);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kSimtThreads) score_simt_kernel(const __grid_constant__ ScoreParams p,
+                                                                   int total_tiles) {
+    extern __shared__ float w1s[];  // [in][hidden] fp32, then b1[hidden], w2[hidden]
+    const int d = p.seq.head_dim;
+    const int in = p.in_mode * d;
+    const int hid = p.hidden;
+    float* b1s = w1s + (size_t)in * hid;
+    float* w2s = b1s + hid;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const T* keys = static_cast<const T*>(p.keys);
+    const T* values = static_cast<const T*>(p.values);
+    const T* w1t = static_cast<const T*>(p.w1t);
+    int cur = -1;
+    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        const TileInfo ti = decode_tile(p, tile, kSimtRows);
+        if (ti.scorer != cur) {
+            __syncthreads();
+            const T* w = w1t + (size_t)ti.scorer * hid * in;
+            for (int e = threadIdx.x; e < in * hid; e += kSimtThreads) {
+                const int j = e / in, i = e - j * in;  // source [hidden][in]
+                w1s[(size_t)i * hid + j] = ld_elem<T>(w, e);
+            }
+            for (int j = threadIdx.x; j < hid; j += kSimtThreads) {
+                b1s[j] = p.b1[(size_t)ti.scorer * hid + j];
+                w2s[j] = p.w2[(size_t)ti.scorer * hid + j];
+            }
+            cur = ti.scorer;
+            __syncthreads();
+        }
+        const int rows = min(kSimtRows, ti.t - ti.row0);
+        for (int rr = warp; rr < rows; rr += kSimtThreads / 32) {
+            const size_t base = ((size_t)ti.head * p.seq.T + ti.row0 + rr) * d;
+            float acc[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+            for (int i0 = 0; i0 < in; i0 += 32) {
+                const int i = i0 + lane;
+                float xv = 0.f;
+                if (i < in) xv = (i < d) ? ld_elem<T>(keys, base + i) : ld_elem<T>(values, base + (i - d));
+                const int lim = min(32, in - i0);
+                for (int ii = 0; ii < lim; ++ii) {
+                    const float xi = __shfl_sync(0xffffffffu, xv, ii);
+                    const float* wr = w1s + (size_t)(i0 + ii) * hid;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int j = lane + 32 * q;
+                        if (j < hid) acc[q] = fmaf(xi, wr[j], acc[q]);
+                    }
+                }
+            }
+            float s = 0.f;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int j = lane + 32 * q;
+                if (j < hid) s = fmaf(act_f32(p.act, acc[q] + b1s[j]), w2s[j], s);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (lane == 0) p.scores[(size_t)ti.head * p.seq.T + ti.row0 + rr] = s;
+        }
+    }
+}
+
+// ============================================================================
+// host launchers
+// ============================================================================
+static int compute_tiles(ScoreParams& p, int tile_rows) {
+    int64_t acc = 0;
+    for (int s = 0; s < p.seq.n_seq; ++s) {
+        p.tile_base[s] = (int32_t)acc;
+        acc += (int64_t)p.seq.n_layers * p.seq.n_kv_heads * ((p.seq.len[s] + tile_rows - 1) / tile_rows);
+    }
+    p.tile_base[p.seq.n_seq] = (int32_t)acc;
+    return (int)acc;
+}
+
+cudaError_t launch_score_simt(ScoreParams p, int dtype, int num_sms, cudaStream_t stream) {
+    const int tiles = compute_tiles(p, kSimtRows);
+    if (tiles == 0) return cudaSuccess;
+    const size_t smem = ((size_t)p.in_mode * p.seq.head_dim * p.hidden + 2 * p.hidden) * sizeof(float);
+    const int grid = min(tiles, num_sms * 4);
+    if (dtype == LKV_F32) {
+        cudaError_t e = cudaFuncSetAttribute(score_simt_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        score_simt_kernel<float><<<grid, kSimtThreads, smem, stream>>>(p, tiles);
+        note_launches(1);
+    } else {
+        cudaError_t e = cudaFuncSetAttribute(score_simt_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        score_simt_kernel<__nv_bfloat16><<<grid, kSimtThreads, smem, stream>>>(p, tiles);
+        note_launches(1);
+    }
+    return cudaGetLastError();
+}
+
+size_t score_simt_smem_bytes(int in, int hidden) { return ((size_t)in * hidden + 2 * hidden) * sizeof(float); }
+
+template <int N, int NBOX, int ACT>
+static cudaError_t launch_tc_inst(const ScoreParams& p, const CUtensorMap& mk, const CUtensorMap& mv,
+                                  const CUtensorMap& mw, int tiles, int grid, cudaStream_t stream) {
+    using Cfg = TcCfg<N, NBOX>;
+    auto kern = score_tc_kernel<N, NBOX, ACT>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, kTcThreads, Cfg::kSmem, stream>>>(p, mk, mv, mw, tiles);
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+bool score_tc_supported(int dtype, int head_dim, int hidden, int in_mode) {
+    if (dtype != LKV_BF16 || head_dim != 128) return false;
+    if (in_mode == 1) return hidden == 64 || hidden == 128;
+    return hidden == 128 || hidden == 64;
+}
+
+cudaError_t launch_score_tc(ScoreParams p, const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mw,
+                            int num_sms, cudaStream_t stream) {
+    const int tiles = compute_tiles(p, kTcRows);
+    if (tiles == 0) return cudaSuccess;
+    const int grid = min(tiles, num_sms);
+    const bool silu = p.act == LKV_ACT_SILU;
+    if (p.in_mode == 1) {
+        if (p.hidden == 64)
+            return silu ? launch_tc_inst<64, 2, LKV_ACT_SILU>(p, mk, mv, mw, tiles, grid, stream)
+                        : launch_tc_inst<64, 2, LKV_ACT_GELU_ERF>(p, mk, mv, mw, tiles, grid, stream);
+        return silu ? launch_tc_inst<128, 2, LKV_ACT_SILU>(p, mk, mv, mw, tiles, grid, stream)
+                    : launch_tc_inst<128, 2, LKV_ACT_GELU_ERF>(p, mk, mv, mw, tiles, grid, stream);
+    }
+    if (p.hidden == 64)
+        return silu ? launch_tc_inst<64, 4, LKV_ACT_SILU>(p, mk, mv, mw, tiles, grid, stream)
+                    : launch_tc_inst<64, 4, LKV_ACT_GELU_ERF>(p, mk, mv, mw, tiles, grid, stream);
+    return silu ? launch_tc_inst<128, 4, LKV_ACT_SILU>(p, mk, mv, mw, tiles, grid, stream)
+                : launch_tc_inst<128, 4, LKV_ACT_GELU_ERF>(p, mk, mv, mw, tiles, grid, stream);
+}
+
+}  // namespace lkv_dev

@@ -1,0 +1,423 @@
+// select.cu -- K3 per-head top-k (inference_select -> hard_topk, soft_topk.cpp:191-201)
+// fused with K4 compaction (evictsim.cpp:202-215), plus the standalone gather.
+//
+// Semantics: per head keep exactly b rows, the b largest fp32 scores, ties to
+// the lowest index (std::stable_sort with x[a] > x[b]); -0.0 == +0.0; NaN is a
+// numeric_error; b outside [0, t] a budget_error.  Retained positions are
+// written ascending (the compaction walk, evictsim.cpp:205-212).
+//
+// Algorithm (HBM-bound, 12 bytes/row of score traffic):
+//   S1 hist     per 4096-row chunk: 2048-bin histogram of the top 11 key bits
+//   S2 resolve1 per head: the bin holding the b-th largest key
+//   S3 collect  per chunk: count rows above that bin; append rows inside it
+//               (the candidates, usually a few % of t) to a per-head list
+//   S4 resolve2 per head: radix-select the remaining 21 bits over the
+//               candidates -> exact threshold key T and the number of T-equal
+//               rows still needed; per-chunk output offsets by a chunk scan
+//   S5 emit     per chunk: keep key > T, or key == T while the running equal
+//               rank (index order) is below the need; block scans give each
+//               kept row its slot; optionally gather its K/V rows (16-byte
+//               vectors) straight into the ragged cache.
+#include "kernels.cuh"
+
+namespace lkv_dev {
+
+constexpr int kChunk = 4096;
+constexpr int kSelThreads = 256;
+constexpr int kPerThread = kChunk / kSelThreads;  // 16 contiguous rows per thread
+constexpr int kMaxChunksPerHead = 1024;           // t <= 4M rows per head
+
+enum : uint32_t { kModeNormal = 0, kModeNone = 1, kModeAll = 2 };
+
+
+
+struct ChunkInfo {
+    int head, c, cbase, t, c0, n;  // c: chunk in head, cbase: global chunk id of head's chunk 0
+};
+
+__device__ __forceinline__ ChunkInfo decode_chunk(const SelectParams& p, int chunk) {
+    int s = 0;
+    while (s + 1 < p.seq.n_seq && p.chunk_base[s + 1] <= chunk) ++s;
+    const int t = p.seq.len[s];
+    const int cph = (t + kChunk - 1) / kChunk;
+    const int local = chunk - p.chunk_base[s];
+    const int hs = local / cph;
+    ChunkInfo ci;
+    ci.c = local - hs * cph;
+    ci.head = s * p.seq.n_layers * p.seq.n_kv_heads + hs;
+    ci.cbase = chunk - ci.c;
+    ci.t = t;
+    ci.c0 = ci.c * kChunk;
+    ci.n = min(kChunk, t - ci.c0);
+    return ci;
+}
+
+__device__ __forceinline__ int head_len(const SelectParams& p, int head) { return p.seq.len[head_seq(p.seq, head)]; }
+
+// ---- S1 --------------------------------------------------------------------------
+__global__ void __launch_bounds__(kSelThreads) select_hist_kernel(const __grid_constant__ SelectParams p) {
+    __shared__ uint32_t h[2048];
+    const ChunkInfo ci = decode_chunk(p, blockIdx.x);
+    const int b = p.budgets[ci.head];
+    if (b < 0 || b > ci.t) {
+        if (threadIdx.x == 0) latch_error(p.err, LKV_ERR_BUDGET, ci.head);
+        return;
+    }
+    if (b == 0 || b == ci.t) return;  // resolved without a histogram
+    for (int i = threadIdx.x; i < 2048; i += kSelThreads) h[i] = 0;
+    __syncthreads();
+    const float* sc = p.scores + (size_t)ci.head * p.seq.T + ci.c0;
+    bool nan = false;
+    for (int i = threadIdx.x; i < ci.n; i += kSelThreads) {
+        const float f = sc[i];
+        nan |= f32_is_nan(f);
+        atomicAdd(&h[f32_key(f) >> 21], 1u);
+    }
+    if (nan) latch_error(p.err, LKV_ERR_NUMERIC, ci.head);
+    __syncthreads();
+    uint32_t* gh = p.hist + (size_t)ci.head * 2048;
+    for (int i = threadIdx.x; i < 2048; i += kSelThreads)
+        if (h[i]) atomicAdd(&gh[i], h[i]);
+}
+
+// ---- S2 --------------------------------------------------------------------------
+// Find the bin holding the rank-`want` largest key of a histogram with `nbins`
+// bins (bin value increasing with key).  Returns bin and the count above it.
+template <int NT>
+__device__ void find_bin_from_top(const uint32_t* cnt /*smem*/, int nbins, uint32_t want, uint32_t* s_scan,
+                                  uint32_t* out_bin, uint32_t* out_above) {
+    // exclusive scan in reverse bin order: above(bin) = sum of bins > bin
+    const int per = (nbins + NT - 1) / NT;
+    uint32_t local = 0;
+    for (int q = 0; q < per; ++q) {
+        const int r = threadIdx.x * per + q;  // reverse index
+        if (r < nbins) local += cnt[nbins - 1 - r];
+    }
+    uint32_t tot;
+    uint32_t run = block_exclusive_scan<NT>(local, s_scan, &tot);
+    for (int q = 0; q < per; ++q) {
+        const int r = threadIdx.x * per + q;
+        if (r < nbins) {
+            const uint32_t c = cnt[nbins - 1 - r];
+            if (c && run < want && want <= run + c) {
+                *out_bin = nbins - 1 - r;
+                *out_above = run;
+            }
+            run += c;
+        }
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(1024) select_resolve1_kernel(const __grid_constant__ SelectParams p) {
+    __shared__ uint32_t cnt[2048];
+    __shared__ uint32_t s_scan[33];
+    __shared__ uint32_t s_bin, s_above;
+    const int head = blockIdx.x;
+    const int t = head_len(p, head);
+    const int b = p.budgets[head];
+    HeadSel* st = p.state + head;
+    if (b < 0 || b > t) return;  // latched by S1
+    if (b == 0 || b == t) {
+        if (threadIdx.x == 0) {
+            st->mode = b == 0 ? kModeNone : kModeAll;
+            st->n_cand = 0;
+        }
+        return;
+    }
+    const uint32_t* gh = p.hist + (size_t)head * 2048;
+    for (int i = threadIdx.x; i < 2048; i += 1024) cnt[i] = gh[i];
+    __syncthreads();
+    find_bin_from_top<1024>(cnt, 2048, (uint32_t)b, s_scan, &s_bin, &s_above);
+    if (threadIdx.x == 0) {
+        st->mode = kModeNormal;
+        st->bin1 = s_bin;
+        st->rem1 = (uint32_t)b - s_above;
+        st->n_cand = 0;
+    }
+}
+
+// ---- S3 --------------------------------------------------------------------------
+__global__ void __launch_bounds__(kSelThreads) select_collect_kernel(const __grid_constant__ SelectParams p) {
+    __shared__ uint32_t s_red[kSelThreads / 32];
+    const ChunkInfo ci = decode_chunk(p, blockIdx.x);
+    HeadSel* st = p.state + ci.head;
+    const int b = p.budgets[ci.head];
+    if (b < 0 || b > ci.t) return;
+    const uint32_t mode = st->mode;
+    if (mode != kModeNormal) {
+        if (threadIdx.x == 0) p.chunk_gt[blockIdx.x] = mode == kModeAll ? (uint32_t)ci.n : 0u;
+        return;
+    }
+    const uint32_t bin1 = st->bin1;
+    const float* sc = p.scores + (size_t)ci.head * p.seq.T + ci.c0;
+    uint32_t* cand = p.cands + (size_t)ci.head * p.seq.T;
+    uint32_t gt = 0;
+    const int lane = threadIdx.x & 31;
+    for (int i0 = 0; i0 < ci.n; i0 += kSelThreads) {
+        const int i = i0 + threadIdx.x;
+        uint32_t dig = 0;
+        const bool valid = i < ci.n;
+        if (valid) dig = f32_key(sc[i]) >> 21;
+        gt += (valid && dig > bin1);
+        const bool is_c = valid && dig == bin1;
+        const uint32_t m = __ballot_sync(0xffffffffu, is_c);
+        if (m) {
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(&st->n_cand, (uint32_t)__popc(m));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (is_c) cand[base + __popc(m & ((1u << lane) - 1))] = (uint32_t)(ci.c0 + i);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) gt += __shfl_xor_sync(0xffffffffu, gt, o);
+    if (lane == 0) s_red[threadIdx.x >> 5] = gt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t s = 0;
+        for (int w = 0; w < kSelThreads / 32; ++w) s += s_red[w];
+        p.chunk_gt[blockIdx.x] = s;
+    }
+}
+
+// ---- S4 --------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) select_resolve2_kernel(const __grid_constant__ SelectParams p) {
+    __shared__ uint32_t cnt[2048];
+    __shared__ uint32_t c_gt[kMaxChunksPerHead];
+    __shared__ uint32_t c_eq[kMaxChunksPerHead];
+    __shared__ uint32_t s_scan[33];
+    __shared__ uint32_t s_bin, s_above;
+    const int head = blockIdx.x;
+    const int s_idx = head_seq(p.seq, head);
+    const int t = p.seq.len[s_idx];
+    const int b = p.budgets[head];
+    if (b < 0 || b > t) return;
+    HeadSel* st = p.state + head;
+    const int cph = (t + kChunk - 1) / kChunk;
+    const int hs = head - s_idx * p.seq.n_layers * p.seq.n_kv_heads;
+    const int cbase = p.chunk_base[s_idx] + hs * cph;
+    const uint32_t mode = st->mode;
+    uint32_t key_t = 0, need_eq = 0;
+
+    for (int c = threadIdx.x; c < cph; c += 1024) {
+        c_gt[c] = 0;
+        c_eq[c] = 0;
+    }
+    if (mode == kModeNormal) {
+        const uint32_t n_cand = st->n_cand;
+        const uint32_t bin1 = st->bin1;
+        uint32_t rem = st->rem1;
+        const float* sc = p.scores + (size_t)head * p.seq.T;
+        const uint32_t* cand = p.cands + (size_t)head * p.seq.T;
+        // pass A: key bits [10, 21)
+        for (int i = threadIdx.x; i < 2048; i += 1024) cnt[i] = 0;
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < n_cand; i += 1024) atomicAdd(&cnt[(f32_key(sc[cand[i]]) >> 10) & 2047u], 1u);
+        __syncthreads();
+        find_bin_from_top<1024>(cnt, 2048, rem, s_scan, &s_bin, &s_above);
+        const uint32_t binA = s_bin;
+        rem -= s_above;
+        // pass B: key bits [0, 10) among candidates in binA
+        for (int i = threadIdx.x; i < 1024; i += 1024) cnt[i] = 0;
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < n_cand; i += 1024) {
+            const uint32_t k = f32_key(sc[cand[i]]);
+            if (((k >> 10) & 2047u) == binA) atomicAdd(&cnt[k & 1023u], 1u);
+        }
+        __syncthreads();
+        find_bin_from_top<1024>(cnt, 1024, rem, s_scan, &s_bin, &s_above);
+        key_t = (bin1 << 21) | (binA << 10) | s_bin;
+        need_eq = rem - s_above;
+        // per-chunk: candidates strictly above T, and equal to T
+        for (uint32_t i = threadIdx.x; i < n_cand; i += 1024) {
+            const uint32_t pos = cand[i];
+            const uint32_t k = f32_key(sc[pos]);
+            if (k > key_t) atomicAdd(&c_gt[pos / kChunk], 1u);
+            else if (k == key_t) atomicAdd(&c_eq[pos / kChunk], 1u);
+        }
+    }
+    __syncthreads();
+    // chunk scan (cph <= 1024): eq_before and out_base in index order
+    const int c = threadIdx.x;
+    uint32_t gt = 0, eq = 0;
+    if (c < cph) {
+        if (mode == kModeAll) gt = (uint32_t)min(kChunk, t - c * kChunk);
+        else if (mode == kModeNormal) gt = p.chunk_gt[cbase + c] + c_gt[c];
+        eq = c_eq[c];
+    }
+    uint32_t tot;
+    const uint32_t eqb = block_exclusive_scan<1024>(eq, s_scan, &tot);
+    uint32_t take = 0;
+    if (need_eq > eqb) take = min(need_eq - eqb, eq);
+    const uint32_t kept = gt + take;
+    const uint32_t ob = block_exclusive_scan<1024>(kept, s_scan, &tot);
+    if (c < cph) {
+        p.chunk_out[cbase + c] = ob;
+        p.chunk_eqb[cbase + c] = eqb;
+    }
+    if (threadIdx.x == 0) {
+        st->key_t = key_t;
+        st->need_eq = need_eq;
+        p.out_lens[head] = b;
+        if (tot != (uint32_t)b) latch_error(p.err, LKV_ERR_NUMERIC, head);  // internal consistency
+    }
+}
+
+// ---- row gather (16-byte vectors) ----------------------------------------------------------
+__device__ __forceinline__ void gather_rows(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                            const int32_t* rows /*smem or global*/, int n_rows, int units,
+                                            int tid, int nthreads) {
+    const int total = n_rows * units;
+    int u = tid;
+    for (; u + 3 * nthreads < total; u += 4 * nthreads) {
+        uint4 v[4];
+        int r[4], q[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int uu = u + k * nthreads;
+            r[k] = uu / units;
+            q[k] = uu - r[k] * units;
+            v[k] = __ldg(src + (size_t)rows[r[k]] * units + q[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) dst[(size_t)r[k] * units + q[k]] = v[k];
+    }
+    for (; u < total; u += nthreads) {
+        const int r = u / units, q = u - r * units;
+        dst[(size_t)r * units + q] = __ldg(src + (size_t)rows[r] * units + q);
+    }
+}
+
+// ---- S5 --------------------------------------------------------------------------
+__global__ void __launch_bounds__(kSelThreads) select_emit_kernel(const __grid_constant__ SelectParams p) {
+    __shared__ int32_t s_pos[kChunk];
+    __shared__ uint32_t s_scan[kSelThreads / 32 + 1];
+    const ChunkInfo ci = decode_chunk(p, blockIdx.x);
+    const int b = p.budgets[ci.head];
+    if (b < 0 || b > ci.t) return;
+    const HeadSel* st = p.state + ci.head;
+    const uint32_t mode = st->mode;
+    if (mode == kModeNone) return;
+    const uint32_t key_t = st->key_t, need_eq = st->need_eq;
+    const uint32_t out_base = p.chunk_out[blockIdx.x];
+    const uint32_t eqb = p.chunk_eqb[blockIdx.x];
+    const float* sc = p.scores + (size_t)ci.head * p.seq.T + ci.c0;
+
+    const int j0 = threadIdx.x * kPerThread;
+    uint32_t keys[kPerThread];
+    uint32_t n_eq = 0;
+#pragma unroll
+    for (int q = 0; q < kPerThread; ++q) {
+        const int j = j0 + q;
+        keys[q] = j < ci.n ? f32_key(sc[j]) : 0u;
+        n_eq += (j < ci.n) && keys[q] == key_t;
+    }
+    uint32_t tot;
+    uint32_t eq_rank = eqb + block_exclusive_scan<kSelThreads>(n_eq, s_scan, &tot);
+    uint32_t keepmask = 0, n_keep = 0;
+#pragma unroll
+    for (int q = 0; q < kPerThread; ++q) {
+        const int j = j0 + q;
+        bool keep = false;
+        if (j < ci.n) {
+            if (mode == kModeAll) keep = true;
+            else if (keys[q] > key_t) keep = true;
+            else if (keys[q] == key_t) {
+                keep = eq_rank < need_eq;
+                ++eq_rank;
+            }
+        }
+        keepmask |= uint32_t(keep) << q;
+        n_keep += keep;
+    }
+    uint32_t slot = block_exclusive_scan<kSelThreads>(n_keep, s_scan, &tot);
+    const int64_t obase = p.offsets[ci.head] + out_base;
+#pragma unroll
+    for (int q = 0; q < kPerThread; ++q) {
+        if (keepmask >> q & 1u) {
+            const int32_t pos = ci.c0 + j0 + q;
+            p.out_pos[obase + slot] = pos;
+            s_pos[slot] = pos;
+            ++slot;
+        }
+    }
+    if (!p.gather) return;
+    __syncthreads();
+    const int units = p.row_bytes / 16;
+    const size_t head_row0 = (size_t)ci.head * p.seq.T;
+    gather_rows(static_cast<const uint4*>(p.keys) + head_row0 * units, static_cast<uint4*>(p.out_keys) + obase * units,
+                s_pos, (int)tot, units, threadIdx.x, kSelThreads);
+    gather_rows(static_cast<const uint4*>(p.values) + head_row0 * units,
+                static_cast<uint4*>(p.out_values) + obase * units, s_pos, (int)tot, units, threadIdx.x, kSelThreads);
+}
+
+// ---- standalone compaction: positions given (cache_from_trace, model.cpp:289-315) -------------
+
+constexpr int kCompactRows = 256;
+
+__global__ void __launch_bounds__(256) compact_kernel(const __grid_constant__ CompactParams p) {
+    __shared__ int32_t s_pos[kCompactRows];
+    const int head = blockIdx.y;
+    const int r0 = blockIdx.x * kCompactRows;
+    const int len = p.lens[head];
+    if (r0 >= len) return;
+    const int n = min(kCompactRows, len - r0);
+    const int t = p.seq.len[head_seq(p.seq, head)];
+    const int64_t obase = p.offsets[head] + r0;
+    if (p.offsets[head] + len > p.offsets[head + 1]) {
+        if (threadIdx.x == 0) latch_error(p.err, LKV_ERR_CONTRACT, head);
+        return;
+    }
+    for (int i = threadIdx.x; i < n; i += 256) {
+        int32_t pos = p.positions[obase + i];
+        if (pos < 0 || pos >= t) {
+            latch_error(p.err, LKV_ERR_CONTRACT, head);
+            pos = 0;
+        }
+        s_pos[i] = pos;
+    }
+    __syncthreads();
+    const int units = p.row_bytes / 16;
+    const size_t head_row0 = (size_t)head * p.seq.T;
+    gather_rows(static_cast<const uint4*>(p.keys) + head_row0 * units, static_cast<uint4*>(p.out_keys) + obase * units,
+                s_pos, n, units, threadIdx.x, 256);
+    gather_rows(static_cast<const uint4*>(p.values) + head_row0 * units,
+                static_cast<uint4*>(p.out_values) + obase * units, s_pos, n, units, threadIdx.x, 256);
+}
+
+// ---- host launchers --------------------------------------------------------------------------
+int select_total_chunks(SelectParams& p) {
+    int64_t acc = 0;
+    for (int s = 0; s < p.seq.n_seq; ++s) {
+        p.chunk_base[s] = (int32_t)acc;
+        acc += (int64_t)p.seq.n_layers * p.seq.n_kv_heads * ((p.seq.len[s] + kChunk - 1) / kChunk);
+    }
+    p.chunk_base[p.seq.n_seq] = (int32_t)acc;
+    return (int)acc;
+}
+
+cudaError_t launch_select(SelectParams p, int n_heads, cudaStream_t stream) {
+    const int chunks = select_total_chunks(p);
+    cudaError_t e = cudaMemsetAsync(p.hist, 0, sizeof(uint32_t) * 2048 * (size_t)n_heads, stream);
+    if (e != cudaSuccess) return e;
+    if (chunks == 0) return cudaSuccess;
+    select_hist_kernel<<<chunks, kSelThreads, 0, stream>>>(p);
+    select_resolve1_kernel<<<n_heads, 1024, 0, stream>>>(p);
+    select_collect_kernel<<<chunks, kSelThreads, 0, stream>>>(p);
+    select_resolve2_kernel<<<n_heads, 1024, 0, stream>>>(p);
+    select_emit_kernel<<<chunks, kSelThreads, 0, stream>>>(p);
+    note_launches(5);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_compact(const CompactParams& p, int n_heads, cudaStream_t stream) {
+    int64_t maxt = 0;
+    for (int s = 0; s < p.seq.n_seq; ++s) maxt = maxt > p.seq.len[s] ? maxt : p.seq.len[s];
+    const int gx = (int)((maxt + kCompactRows - 1) / kCompactRows);
+    if (gx == 0 || n_heads == 0) return cudaSuccess;
+    compact_kernel<<<dim3(gx, n_heads), 256, 0, stream>>>(p);
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+}  // namespace lkv_dev

@@ -1,0 +1,81 @@
+"""CPU-side checks of the drop-in boundary: the C-ABI library loads and exports
+every entry point include/lkv_b200.h declares; host-side validation raises the
+reference's error taxonomy without touching a GPU."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import pytest
+
+import paper_2605_06676_b200 as lkv
+from paper_2605_06676_b200 import _abi
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "lkv_b200.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(lkv_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_declares_the_abi():
+    assert set(declared_symbols()) == set(_abi.EXPORTED)
+
+
+def test_library_exports_every_declared_symbol():
+    L = lkv.lib()
+    for name in declared_symbols():
+        assert hasattr(L, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", _abi.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (lkv_[a-z_0-9]+)", out))
+    assert set(declared_symbols()) <= exported
+
+
+def test_library_targets_sm100a_only():
+    out = subprocess.run(["cuobjdump", "--list-elf", _abi.LIB_PATH], capture_output=True, text=True).stdout
+    arches = set(re.findall(r"sm_(\d+a?)", out))
+    assert arches == {"100a"}, arches
+
+
+def test_tensor_core_and_tma_instructions_present():
+    sass = subprocess.run(["cuobjdump", "-sass", _abi.LIB_PATH], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in sass  # tcgen05.mma (scorer)
+    assert "UTMALDG" in sass  # TMA tile loads
+    assert "LDTM" in sass     # tcgen05.ld (TMEM epilogue)
+
+
+def test_status_names_and_version():
+    L = lkv.lib()
+    assert L.lkv_abi_version() == 1
+    assert L.lkv_status_name(3) == b"budget_error"
+    assert L.lkv_status_name(1) == b"contract_error"
+
+
+def test_host_validation_without_gpu():
+    L = lkv.lib()
+    lens = (C.c_int32 * 1)(100)
+    # target ratio outside (0,1) -> budget_error before any device work (policy.cpp:111)
+    assert L.lkv_budgets(None, 8, 1.5, 0, lens, 1, 0, None, None, None, None, 0, None) == _abi.BUDGET
+    assert L.lkv_budgets(None, 8, 0.0, 0, lens, 1, 0, None, None, None, None, 0, None) == _abi.BUDGET
+    # t < 1 -> contract_error (policy.cpp:123)
+    zero = (C.c_int32 * 1)(0)
+    assert L.lkv_budgets(C.c_void_p(16), 8, 0.5, 0, zero, 1, 0, None, C.c_void_p(16), None, C.c_void_p(256), 256,
+                         None) == _abi.CONTRACT
+    # malformed cache descriptor
+    bad = _abi.CacheDesc(0, 1, 1, 128, 10, 1, 0, None, None, C.cast(lens, C.POINTER(C.c_int32)))
+    assert L.lkv_workspace_bytes(C.byref(bad), 8) == 0
+    good = _abi.CacheDesc(1, 32, 8, 128, 32768, 1, 0, None, None, C.cast((C.c_int32 * 1)(32768), C.POINTER(C.c_int32)))
+    assert L.lkv_workspace_bytes(C.byref(good), 256) > 0
+    cap = L.lkv_ragged_capacity(C.byref(good), 0.15, 0)
+    assert cap >= 1258291
+
+
+def test_error_classes_mirror_reference():
+    assert issubclass(lkv.BudgetError, lkv.LkvError)
+    with pytest.raises(lkv.BudgetError):
+        lkv.kv_memory_bytes(retention=0.0)
+    r = lkv.kv_memory_bytes(retention=1.0)
+    assert r["full_bytes"] == pytest.approx(26214400000.0)  # test_evictsim.cpp:45-49
+    assert abs(lkv.kv_memory_bytes(retention=0.15)["reduction_factor"] - 6.67) < 0.01
