@@ -45,6 +45,16 @@ int num_sms() {
     return n > 0 ? n : 148;
 }
 
+// One non-blocking helper stream per (host thread, device) for fork/join inside a call.
+cudaStream_t side_stream() {
+    thread_local cudaStream_t streams[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return nullptr;
+    if (!streams[dev] && cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    return streams[dev];
+}
+
 constexpr size_t kAlign = 256;
 size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
 
@@ -87,6 +97,10 @@ lkv_status check_cache(const lkv_cache_desc* c, bool need_kv) {
     if (c->n_seq < 1 || c->n_seq > LKV_MAX_SEQ) return fail(LKV_ERR_CONTRACT, "n_seq must lie in [1, LKV_MAX_SEQ]");
     if (c->n_layers < 1 || c->n_kv_heads < 1) return fail(LKV_ERR_CONTRACT, "n_layers and n_kv_heads must be >= 1");
     if (c->head_dim < 8 || c->head_dim % 8) return fail(LKV_ERR_CONTRACT, "head_dim must be a positive multiple of 8");
+    {
+        const int units = c->head_dim * (c->dtype == LKV_F32 ? 4 : 2) / 16;
+        if (units & (units - 1)) return fail(LKV_ERR_UNSUPPORTED, "row bytes must be a power-of-two multiple of 16");
+    }
     if (c->dtype != LKV_F32 && c->dtype != LKV_BF16) return fail(LKV_ERR_CONTRACT, "unknown dtype");
     if (c->max_tokens < 1) return fail(LKV_ERR_CONTRACT, "max_tokens must be >= 1");
     if (!c->seq_lens) return fail(LKV_ERR_CONTRACT, "seq_lens (host) is null");
@@ -185,7 +199,8 @@ lkv_status check_ragged(const lkv_ragged_desc* r, int64_t n_heads, int head_dim,
 }
 
 // ---- internal launchers shared by lkv_score / lkv_evict ---------------------------------------------
-lkv_status run_score(const lkv_cache_desc* c, const lkv_scorer_desc* s, float* scores, cudaStream_t stream) {
+lkv_status run_score(const lkv_cache_desc* c, const lkv_scorer_desc* s, float* scores, cudaStream_t stream,
+                     int sms_reserved = 0) {
     ScoreParams p;
     memset(&p, 0, sizeof p);
     p.seq = make_seq(c);
@@ -210,7 +225,7 @@ lkv_status run_score(const lkv_cache_desc* c, const lkv_scorer_desc* s, float* s
         st = make_map_bf16(&mw, s->w1t, (uint64_t)s->input * c->head_dim, (uint64_t)s->n_scorers * s->hidden,
                            (uint32_t)s->hidden);
         if (st) return st;
-        LKV_CUDA(launch_score_tc(p, mk, mv, mw, num_sms(), stream), "score (tcgen05)");
+        LKV_CUDA(launch_score_tc(p, mk, mv, mw, num_sms() - sms_reserved, stream), "score (tcgen05)");
     } else {
         const int in = s->input * c->head_dim;
         if (score_simt_smem_bytes(in, s->hidden) > 200 * 1024)
@@ -251,7 +266,7 @@ lkv_status run_select(const lkv_cache_desc* c, const float* scores, const int32_
 
 // ---- decode workspace -------------------------------------------------------------------------------
 struct DecodeWs {
-    size_t err, n_items, item_base, items, part_m, part_l, part_o, total;
+    size_t err, n_items, item_base, head_done, seq_done, items, part_m, part_l, part_o, total;
     int64_t max_items;
 };
 DecodeWs decode_layout(const lkv_ragged_desc* r, int G) {
@@ -263,6 +278,10 @@ DecodeWs decode_layout(const lkv_ragged_desc* r, int G) {
     w.n_items = o;
     o = align_up(o + sizeof(int32_t));
     w.item_base = o;
+    o = align_up(o + sizeof(int32_t) * (size_t)r->n_heads);
+    w.head_done = o;
+    o = align_up(o + sizeof(int32_t) * (size_t)r->n_heads);
+    w.seq_done = o;  // indexed by sequence; n_heads >= n_seq entries
     o = align_up(o + sizeof(int32_t) * (size_t)r->n_heads);
     w.items = o;
     o = align_up(o + sizeof(DecodeItem) * (size_t)w.max_items);
@@ -444,13 +463,28 @@ lkv_status lkv_evict(const lkv_cache_desc* c, const lkv_scorer_desc* s, const do
     int32_t* budgets = budgets_out ? budgets_out : at<int32_t>(ws, w.budgets);
     double* ratios = ratios_out ? ratios_out : at<double>(ws, w.ratios);
     float* scores = scores_out ? scores_out : at<float>(ws, w.scores);
-    // K2: budgets + ragged offsets (budget + decode slack per head)
+    // K2 (one CTA, latency-bound fp64) runs on a side stream concurrently with K1,
+    // which leaves one SM free for it; K3 waits for both.
+    cudaStream_t side = side_stream();
+    if (!side) return fail(LKV_ERR_CUDA, "side stream creation failed");
+    cudaEvent_t fork = nullptr, join = nullptr;
+    LKV_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming), "event");
+    LKV_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming), "event");
+    struct Ev {
+        cudaEvent_t a, b;
+        ~Ev() {
+            cudaEventDestroy(a);
+            cudaEventDestroy(b);
+        }
+    } guard{fork, join};
+    LKV_CUDA(cudaEventRecord(fork, strm), "event record");
+    LKV_CUDA(cudaStreamWaitEvent(side, fork, 0), "stream wait");
     st = lkv_budgets(logits, n, R, mode, c->seq_lens, c->n_seq, out->decode_slack, ratios, budgets, out->offsets, ws,
-                     ws_bytes, stream);
+                     ws_bytes, (lkv_stream_t)side);
     if (st) return st;
-    // K1: scores
-    if ((st = run_score(c, s, scores, strm))) return st;
-    // K3 + K4: select and gather into the ragged cache
+    LKV_CUDA(cudaEventRecord(join, side), "event record");
+    if ((st = run_score(c, s, scores, strm, /*sms_reserved=*/1))) return st;
+    LKV_CUDA(cudaStreamWaitEvent(strm, join, 0), "stream wait");
     return run_select(c, scores, budgets, out, ws, w, true, strm);
 }
 
@@ -464,8 +498,9 @@ lkv_status lkv_decode_plan(const lkv_ragged_desc* r, void* ws, size_t ws_bytes, 
     const DecodeWs w = decode_layout(r, 1);
     lkv_status st = check_ws(ws, ws_bytes, w.items + sizeof(DecodeItem) * (size_t)w.max_items);
     if (st) return st;
-    LKV_CUDA(launch_decode_plan(r->offsets, r->n_heads, at<DecodeItem>(ws, w.items), at<int32_t>(ws, w.item_base),
-                                at<int32_t>(ws, w.n_items), (cudaStream_t)stream),
+    LKV_CUDA(launch_decode_plan(r->offsets, r->n_heads, r->n_heads, at<DecodeItem>(ws, w.items),
+                                at<int32_t>(ws, w.item_base), at<int32_t>(ws, w.n_items), at<int32_t>(ws, w.head_done),
+                                at<int32_t>(ws, w.seq_done), (cudaStream_t)stream),
              "decode plan");
     return LKV_OK;
 }
@@ -514,6 +549,8 @@ lkv_status lkv_decode_step(const lkv_ragged_desc* r, int32_t n_seq, int32_t n_la
     p.part_m = at<float>(ws, w.part_m);
     p.part_l = at<float>(ws, w.part_l);
     p.part_o = at<float>(ws, w.part_o);
+    p.head_done = at<int32_t>(ws, w.head_done);
+    p.seq_done = at<int32_t>(ws, w.seq_done);
     p.err = at<ErrWord>(ws, w.err);
     CUtensorMap mk, mv;
     if (r->dtype == LKV_BF16) {

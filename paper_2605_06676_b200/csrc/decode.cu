@@ -26,19 +26,21 @@ namespace lkv_dev {
 
 constexpr int kDecCh = 256;         // rows per work item
 constexpr int kDecStageRows = 64;   // rows per pipeline stage
-constexpr int kDecStages = 4;
+constexpr int kDecStages = 3;  // x 32 KB; two CTAs per SM
 constexpr int kDecConsumers = 4;    // consumer warps (16 rows of a stage each)
 constexpr int kDecThreads = (kDecConsumers + 1) * 32;
-constexpr int kDecMaxG = 16;
 
 
 
 // ---- plan: work items over each head's capacity (once per eviction) -------------------------
-__global__ void __launch_bounds__(1024) decode_plan_kernel(const int64_t* offsets, int n_heads, DecodeItem* items,
-                                                           int32_t* item_base, int32_t* n_items_out) {
+__global__ void __launch_bounds__(1024) decode_plan_kernel(const int64_t* offsets, int n_heads, int n_seq,
+                                                           DecodeItem* items, int32_t* item_base, int32_t* n_items_out,
+                                                           int32_t* head_done, int32_t* seq_done) {
     __shared__ uint32_t s_scan[33];
     __shared__ int32_t s_carry;
     if (threadIdx.x == 0) s_carry = 0;
+    for (int h = threadIdx.x; h < n_heads; h += 1024) head_done[h] = 0;
+    for (int q = threadIdx.x; q < n_seq; q += 1024) seq_done[q] = 0;
     __syncthreads();
     for (int base = 0; base < n_heads; base += 1024) {
         const int h = base + threadIdx.x;
@@ -93,7 +95,7 @@ __device__ __forceinline__ uint32_t sw_off(int row, int q) {
 }
 
 // ---- bf16 attention kernel (tensor cores) ------------------------------------------------------
-__global__ void __launch_bounds__(kDecThreads, 1)
+__global__ void __launch_bounds__(kDecThreads, 2)
     decode_attn_bf16_kernel(const __grid_constant__ DecodeParams p, const __grid_constant__ CUtensorMap tmap_k,
                             const __grid_constant__ CUtensorMap tmap_v) {
     constexpr int kStageBytes = 2 * kDecStageRows * 256;  // K + V, 64 rows x 256 B each
@@ -102,6 +104,7 @@ __global__ void __launch_bounds__(kDecThreads, 1)
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kDecStages * kStageBytes);
     uint64_t* empty = full + kDecStages;
     float* red = reinterpret_cast<float*>(empty + kDecStages);  // [consumers][G][D + 2]
+    __shared__ int s_last;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int G = p.G;
@@ -298,7 +301,7 @@ __global__ void __launch_bounds__(kDecThreads, 1)
         l_hi += __shfl_xor_sync(0xffffffffu, l_hi, 1);
         l_hi += __shfl_xor_sync(0xffffffffu, l_hi, 2);
         const int stride = D + 2;
-        float* rw = red + (size_t)warp * kDecMaxG * stride;
+        float* rw = red + (size_t)warp * G * stride;
         if (g < G) {
 #pragma unroll
             for (int n = 0; n < 16; ++n) {
@@ -322,23 +325,64 @@ __global__ void __launch_bounds__(kDecThreads, 1)
             }
         }
         named_bar_sync(1, kDecConsumers * 32);
+        const int nch = (len_new + kDecCh - 1) / kDecCh;
+        __nv_bfloat16* outp = static_cast<__nv_bfloat16*>(p.out) + ((size_t)sl * p.n_q_heads + kvh * G) * D;
         for (int e = threadIdx.x; e < G * D; e += kDecConsumers * 32) {
             const int gg = e / D, dd = e - gg * D;
             float M = -INFINITY;
 #pragma unroll
-            for (int w = 0; w < kDecConsumers; ++w) M = fmaxf(M, red[(size_t)w * kDecMaxG * stride + gg * stride + D]);
+            for (int w = 0; w < kDecConsumers; ++w) M = fmaxf(M, red[((size_t)w * G + gg) * stride + D]);
             float L = 0.f, acc = 0.f;
 #pragma unroll
             for (int w = 0; w < kDecConsumers; ++w) {
-                const float* r = red + (size_t)w * kDecMaxG * stride + gg * stride;
+                const float* r = red + ((size_t)w * G + gg) * stride;
                 const float f = (r[D] == -INFINITY) ? 0.f : exp2f(r[D] - M);
                 L += r[D + 1] * f;
                 acc += r[dd] * f;
             }
-            p.part_o[((size_t)it * G + gg) * D + dd] = acc;
-            if (dd == 0) {
-                p.part_m[(size_t)it * G + gg] = M;
-                p.part_l[(size_t)it * G + gg] = L;
+            if (nch == 1) {
+                outp[e] = __float2bfloat16_rn(acc / L);
+            } else {
+                p.part_o[((size_t)it * G + gg) * D + dd] = acc;
+                if (dd == 0) {
+                    p.part_m[(size_t)it * G + gg] = M;
+                    p.part_l[(size_t)it * G + gg] = L;
+                }
+            }
+        }
+        // split-K: the last chunk of a head to finish merges the head's partials (no combine pass)
+        bool finalize = nch == 1;
+        if (nch > 1) {
+            __threadfence();
+            named_bar_sync(1, kDecConsumers * 32);
+            if (threadIdx.x == 0) s_last = atomicAdd(&p.head_done[head], 1) == nch - 1;
+            named_bar_sync(1, kDecConsumers * 32);
+            finalize = s_last;
+            if (finalize) {
+                __threadfence();
+                const int base = p.item_base[head];
+                for (int e = threadIdx.x; e < G * D; e += kDecConsumers * 32) {
+                    const int gg = e / D, dd = e - gg * D;
+                    float M = -INFINITY;
+                    for (int c = 0; c < nch; ++c) M = fmaxf(M, __ldcg(p.part_m + (size_t)(base + c) * G + gg));
+                    float L = 0.f, acc = 0.f;
+                    for (int c = 0; c < nch; ++c) {
+                        const size_t i2 = (size_t)(base + c) * G + gg;
+                        const float f = exp2f(__ldcg(p.part_m + i2) - M);
+                        L += __ldcg(p.part_l + i2) * f;
+                        acc += __ldcg(p.part_o + i2 * D + dd) * f;
+                    }
+                    outp[e] = __float2bfloat16_rn(acc / L);
+                }
+                if (threadIdx.x == 0) p.head_done[head] = 0;
+            }
+        }
+        if (finalize && threadIdx.x == 0) {
+            p.lens[head] = len_new;
+            const int sq = sl / (p.heads_per_seq / p.n_kv_heads);
+            if (atomicAdd(&p.seq_done[sq], 1) == p.heads_per_seq - 1) {
+                p.seq_done[sq] = 0;
+                atomicAdd(&p.tokens_seen[sq], 1);  // every head of the sequence has its new row
             }
         }
         named_bar_sync(1, kDecConsumers * 32);
@@ -450,31 +494,29 @@ __global__ void __launch_bounds__(256) decode_combine_kernel(const __grid_consta
 }
 
 // ---- host launchers ---------------------------------------------------------------------------------
-cudaError_t launch_decode_plan(const int64_t* offsets, int n_heads, DecodeItem* items, int32_t* item_base,
-                               int32_t* n_items, cudaStream_t stream) {
-    decode_plan_kernel<<<1, 1024, 0, stream>>>(offsets, n_heads, items, item_base, n_items);
+cudaError_t launch_decode_plan(const int64_t* offsets, int n_heads, int n_seq, DecodeItem* items, int32_t* item_base,
+                               int32_t* n_items, int32_t* head_done, int32_t* seq_done, cudaStream_t stream) {
+    decode_plan_kernel<<<1, 1024, 0, stream>>>(offsets, n_heads, n_seq, items, item_base, n_items, head_done,
+                                               seq_done);
     note_launches(1);
     return cudaGetLastError();
 }
 
-size_t decode_bf16_smem() {
-    return 1024 + kDecStages * (2 * kDecStageRows * 256) + 2 * kDecStages * 8 +
-           (size_t)kDecConsumers * kDecMaxG * (128 + 2) * 4;
+size_t decode_bf16_smem(int G) {
+    return 1024 + kDecStages * (2 * kDecStageRows * 256) + 2 * kDecStages * 8 + (size_t)kDecConsumers * G * (128 + 2) * 4;
 }
 
 cudaError_t launch_decode(const DecodeParams& p, int dtype, const CUtensorMap* mk, const CUtensorMap* mv, int num_sms,
                           cudaStream_t stream) {
     if (p.max_items == 0) return cudaSuccess;
     if (dtype == LKV_BF16) {
-        const size_t smem = decode_bf16_smem();
+        const size_t smem = decode_bf16_smem(p.G);
         cudaError_t e = cudaFuncSetAttribute(decode_attn_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        const int grid = min(p.max_items, num_sms);
+        const int per_sm = smem * 2 <= 220 * 1024 ? 2 : 1;
+        const int grid = min(p.max_items, per_sm * num_sms);
         decode_attn_bf16_kernel<<<grid, kDecThreads, smem, stream>>>(p, *mk, *mv);
-        e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
-        decode_combine_kernel<__nv_bfloat16><<<p.n_heads, 256, 0, stream>>>(p);
-        note_launches(2);
+        note_launches(1);
     } else {
         const size_t smem = ((size_t)p.G * p.head_dim + (size_t)p.G * kDecCh) * sizeof(float);
         cudaError_t e = cudaFuncSetAttribute(decode_attn_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

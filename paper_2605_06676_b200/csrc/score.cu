@@ -22,11 +22,47 @@ __device__ __forceinline__ float act_f32(int act, float h) {
     return 0.5f * h * (1.0f + erff(h * 0.70710678118654752f));
 }
 
-template <int ACT>
-__device__ __forceinline__ float act_t(float h) {
-    if constexpr (ACT == LKV_ACT_SILU) return h / (1.0f + __expf(-h));
-    else return 0.5f * h * (1.0f + erff(h * 0.70710678118654752f));
+// Epilogue activations on the MUFU path (approximations far inside the 1e-2 bf16 bar):
+//  GELU-erf: gelu(h) = h * Phi(h) = 0.5 (h + |h| erf(|h|/sqrt2)), erf by Abramowitz-Stegun 7.1.26
+//            (|error| <= 1.5e-7): erf(u) = 1 - t (a1 + t (a2 + t (a3 + t (a4 + t a5)))) e^{-u^2},
+//            t = 1 / (1 + p u); one rcp + one ex2.  f() returns 2*gelu; w2 is pre-scaled by 0.5.
+//  SiLU:     h / (1 + e^{-h}) (tensor.cpp:371-378) with ex2 + rcp.
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
 }
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+template <int ACT>
+struct EpiAct;
+template <>
+struct EpiAct<LKV_ACT_GELU_ERF> {
+    static constexpr float kW2Scale = 0.5f;
+    __device__ __forceinline__ static float f(float h) {
+        const float ah = fabsf(h);
+        const float t = rcp_approx(fmaf(0.3275911f * 0.70710678118654752f, ah, 1.0f));
+        float p = fmaf(1.061405429f, t, -1.453152027f);
+        p = fmaf(p, t, 1.421413741f);
+        p = fmaf(p, t, -0.284496736f);
+        p = fmaf(p, t, 0.254829592f);
+        p *= t;
+        const float e = ex2_approx(h * h * -0.72134752044448170f);  // e^{-h^2/2}
+        const float erf_abs = fmaf(-p, e, 1.0f);
+        return fmaf(ah, erf_abs, h);
+    }
+};
+template <>
+struct EpiAct<LKV_ACT_SILU> {
+    static constexpr float kW2Scale = 1.0f;
+    __device__ __forceinline__ static float f(float h) {
+        return h * rcp_approx(1.0f + ex2_approx(h * -1.4426950408889634f));
+    }
+};
+__device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
 struct TileInfo {
     int head;      // flat head
@@ -67,7 +103,7 @@ struct TcCfg {
     static constexpr int kW = NBOX * kWBox;
     static constexpr int kStages = (NBOX == 2) ? 5 : 2;
     static constexpr int kTmemCols = (2 * N <= 32) ? 32 : (2 * N <= 64) ? 64 : (2 * N <= 128) ? 128 : (2 * N <= 256) ? 256 : 512;
-    static constexpr int kSmem = kStages * kAStage + kW + 256 + 1024;  // + barriers + alignment slack
+    static constexpr int kSmem = kStages * kAStage + kW + 256 + 4 * N * 4 + 1024;  // + barriers, b1/w2, align
 };
 
 template <int N, int NBOX, int ACT>
@@ -89,6 +125,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     uint64_t* wfull = bars + 2 * S + 4;
     uint64_t* wempty = bars + 2 * S + 5;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 6);
+    float* sEpi = reinterpret_cast<float*>(sW + Cfg::kW + 256);  // [2 groups][b1 | w2][N]
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -189,12 +226,21 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         // ===================== epilogue (2 groups x 4 warps) =====================
         const int grp = (warp - 4) >> 2;
         const int quarter = warp & 3;  // TMEM lane quarter this warp may access
-        const float* b1_all = p.b1;
-        const float* w2_all = p.w2;
+        float* s_b1 = sEpi + grp * 2 * N;  // this group's copy of b1 and the pre-scaled w2
+        float* s_w2 = s_b1 + N;
+        int cur = -1;
         for (int tile = t_begin + grp, i = grp; tile < t_end; tile += 2, i += 2) {
             const TileInfo ti = decode_tile(p, tile, kTcRows);
-            const float* b1 = b1_all + (size_t)ti.scorer * N;
-            const float* w2 = w2_all + (size_t)ti.scorer * N;
+            if (ti.scorer != cur) {  // stage this scorer's b1 / w2 once (group-local barrier)
+                named_bar_sync(1 + grp, 128);
+                const int j = threadIdx.x & 127;
+                if (j < N) {
+                    s_b1[j] = p.b1[(size_t)ti.scorer * N + j];
+                    s_w2[j] = p.w2[(size_t)ti.scorer * N + j] * EpiAct<ACT>::kW2Scale;
+                }
+                named_bar_sync(1 + grp, 128);
+                cur = ti.scorer;
+            }
             mbar_wait(&tfull[grp], (i >> 1) & 1);
             tc_fence_after();
             const uint32_t taddr = tmem_base + (uint32_t(quarter * 32) << 16) + grp * N;
@@ -210,9 +256,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     if (lane == 0) mbar_arrive(&tempty[grp]);
                 }
 #pragma unroll
-                for (int q = 0; q < 32; ++q) {
-                    const float h = __uint_as_float(r[q]) + __ldg(b1 + c * 32 + q);
-                    s = fmaf(act_t<ACT>(h), __ldg(w2 + c * 32 + q), s);
+                for (int q = 0; q < 32; q += 4) {
+                    const float4 bb = *reinterpret_cast<const float4*>(s_b1 + c * 32 + q);
+                    const float4 ww = *reinterpret_cast<const float4*>(s_w2 + c * 32 + q);
+                    s = fmaf(EpiAct<ACT>::f(__uint_as_float(r[q + 0]) + bb.x), ww.x, s);
+                    s = fmaf(EpiAct<ACT>::f(__uint_as_float(r[q + 1]) + bb.y), ww.y, s);
+                    s = fmaf(EpiAct<ACT>::f(__uint_as_float(r[q + 2]) + bb.z), ww.z, s);
+                    s = fmaf(EpiAct<ACT>::f(__uint_as_float(r[q + 3]) + bb.w), ww.w, s);
                 }
             }
             const int row = ti.row0 + quarter * 32 + lane;

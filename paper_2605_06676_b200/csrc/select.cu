@@ -264,28 +264,26 @@ __global__ void __launch_bounds__(1024) select_resolve2_kernel(const __grid_cons
 }
 
 // ---- row gather (16-byte vectors) ----------------------------------------------------------
+// 2^log2_units 16-byte vectors per row (head_dim * elem / 16); lanes walk (row, vector)
+// pairs so a warp moves whole rows with coalesced 16-byte accesses.
 __device__ __forceinline__ void gather_rows(const uint4* __restrict__ src, uint4* __restrict__ dst,
-                                            const int32_t* rows /*smem or global*/, int n_rows, int units,
-                                            int tid, int nthreads) {
-    const int total = n_rows * units;
+                                            const int32_t* rows /*smem*/, int n_rows, int log2_units, int tid,
+                                            int nthreads) {
+    const int units = 1 << log2_units;
+    const int total = n_rows << log2_units;
     int u = tid;
-    for (; u + 3 * nthreads < total; u += 4 * nthreads) {
-        uint4 v[4];
-        int r[4], q[4];
+    for (; u + 7 * nthreads < total; u += 8 * nthreads) {
+        uint4 v[8];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < 8; ++k) {
             const int uu = u + k * nthreads;
-            r[k] = uu / units;
-            q[k] = uu - r[k] * units;
-            v[k] = __ldg(src + (size_t)rows[r[k]] * units + q[k]);
+            v[k] = __ldg(src + ((size_t)rows[uu >> log2_units] << log2_units) + (uu & (units - 1)));
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) dst[(size_t)r[k] * units + q[k]] = v[k];
+        for (int k = 0; k < 8; ++k) __stcs(dst + u + k * nthreads, v[k]);
     }
-    for (; u < total; u += nthreads) {
-        const int r = u / units, q = u - r * units;
-        dst[(size_t)r * units + q] = __ldg(src + (size_t)rows[r] * units + q);
-    }
+    for (; u < total; u += nthreads)
+        __stcs(dst + u, __ldg(src + ((size_t)rows[u >> log2_units] << log2_units) + (u & (units - 1))));
 }
 
 // ---- S5 --------------------------------------------------------------------------
@@ -343,12 +341,12 @@ __global__ void __launch_bounds__(kSelThreads) select_emit_kernel(const __grid_c
     }
     if (!p.gather) return;
     __syncthreads();
-    const int units = p.row_bytes / 16;
+    const int lu = 31 - __clz(p.row_bytes / 16);
     const size_t head_row0 = (size_t)ci.head * p.seq.T;
-    gather_rows(static_cast<const uint4*>(p.keys) + head_row0 * units, static_cast<uint4*>(p.out_keys) + obase * units,
-                s_pos, (int)tot, units, threadIdx.x, kSelThreads);
-    gather_rows(static_cast<const uint4*>(p.values) + head_row0 * units,
-                static_cast<uint4*>(p.out_values) + obase * units, s_pos, (int)tot, units, threadIdx.x, kSelThreads);
+    gather_rows(static_cast<const uint4*>(p.keys) + (head_row0 << lu), static_cast<uint4*>(p.out_keys) + (obase << lu),
+                s_pos, (int)tot, lu, threadIdx.x, kSelThreads);
+    gather_rows(static_cast<const uint4*>(p.values) + (head_row0 << lu),
+                static_cast<uint4*>(p.out_values) + (obase << lu), s_pos, (int)tot, lu, threadIdx.x, kSelThreads);
 }
 
 // ---- standalone compaction: positions given (cache_from_trace, model.cpp:289-315) -------------
@@ -377,12 +375,12 @@ __global__ void __launch_bounds__(256) compact_kernel(const __grid_constant__ Co
         s_pos[i] = pos;
     }
     __syncthreads();
-    const int units = p.row_bytes / 16;
+    const int lu = 31 - __clz(p.row_bytes / 16);
     const size_t head_row0 = (size_t)head * p.seq.T;
-    gather_rows(static_cast<const uint4*>(p.keys) + head_row0 * units, static_cast<uint4*>(p.out_keys) + obase * units,
-                s_pos, n, units, threadIdx.x, 256);
-    gather_rows(static_cast<const uint4*>(p.values) + head_row0 * units,
-                static_cast<uint4*>(p.out_values) + obase * units, s_pos, n, units, threadIdx.x, 256);
+    gather_rows(static_cast<const uint4*>(p.keys) + (head_row0 << lu), static_cast<uint4*>(p.out_keys) + (obase << lu),
+                s_pos, n, lu, threadIdx.x, 256);
+    gather_rows(static_cast<const uint4*>(p.values) + (head_row0 << lu),
+                static_cast<uint4*>(p.out_values) + (obase << lu), s_pos, n, lu, threadIdx.x, 256);
 }
 
 // ---- host launchers --------------------------------------------------------------------------

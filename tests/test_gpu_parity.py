@@ -69,7 +69,7 @@ def test_budgets_bitexact(n, sigma):
                           else O.freeze_budgets_exact(want_r, R, t))
                 assert (b[i].cpu().numpy() == want_b).all(), (rep, t, mode)
                 if mode == lkv.BUDGET_EXACT:
-                    assert int(b[i].sum()) == round(R * n * t)
+                    assert int(b[i].sum()) == math.floor(R * n * t + 0.5)  # llround: half away from zero
     print(f"ratio elements differing in the last bits: {mismatched_ratios}")
 
 
@@ -84,9 +84,17 @@ def test_budget_fixtures():
     with pytest.raises(lkv.ContractError):
         lkv.allocate_budgets(torch.zeros(7, device=DEV, dtype=torch.float64), 0.2, 4, 2)
     with pytest.raises(lkv.NumericError):
-        lkv.budgets(torch.tensor([0.0, float("nan"), 1.0], device=DEV), 0.3, [100])
+        lkv.budgets(torch.tensor([0.0, float("nan"), 1.0], dtype=torch.float64, device=DEV), 0.3, [100])
     with pytest.raises(lkv.OverflowGuardError):
-        lkv.budgets(torch.tensor([0.0, 1e301, 1.0], device=DEV), 0.3, [100])
+        lkv.budgets(torch.tensor([0.0, 1e301, 1.0], dtype=torch.float64, device=DEV), 0.3, [100])
+    # first offending element decides (soft_topk.cpp:61-64)
+    with pytest.raises(lkv.NumericError):
+        lkv.budgets(torch.tensor([0.0, float("inf"), 1e301], dtype=torch.float64, device=DEV), 0.3, [100])
+    with pytest.raises(lkv.OverflowGuardError):
+        lkv.budgets(torch.tensor([-1e302, float("nan"), 1.0], dtype=torch.float64, device=DEV), 0.3, [100])
+    # n == 1 has no magnitude guard (soft_topk.cpp:119-131): r = clamp(R, eps, 1 - eps)
+    r, b = lkv.budgets(torch.tensor([1e305], dtype=torch.float64, device=DEV), 0.3, [1000])
+    assert float(r[0]) == 0.3 and int(b[0, 0]) == 300
     with pytest.raises(lkv.ContractError):
         lkv.budgets(torch.zeros(4, device=DEV, dtype=torch.float64), 0.3, [0])
 
@@ -352,9 +360,11 @@ def test_evict_zero_and_full_budgets():
     logits = torch.tensor([-40.0, 40.0, 0.0], dtype=torch.float64, device=DEV)
     res = lkv.evict(cache, scorers, logits, 0.34, lkv.BUDGET_FLOOR)
     b = res.budgets[0].cpu().tolist()
-    assert b[0] == 0
-    k1, _, p1 = res.cache.head(1)
-    assert (p1.cpu().numpy() == np.arange(b[1])).all() or b[1] < 500
+    assert b[0] == 0 and int(res.cache.lens[0]) == 0
+    assert b[1] >= 499  # ratio ~ 1 - 1e-17 -> floor(r * 500) = 499 (no repair in floor mode)
+    _, _, p1 = res.cache.head(1)
+    p1 = p1.cpu().numpy()
+    assert len(p1) == b[1] and (np.diff(p1) > 0).all()
 
 
 # ---------------------------------------------------------------------------------------------
