@@ -34,6 +34,13 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+_T0 = time.time()
+
+
+def log(msg):
+    print(f"[bench +{time.time() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 METRIC = "KV tokens/s evicted (score+budget+top-k+compact); decode-attn HBM GB/s"
 UNIT = "KV token-rows/s"
 
@@ -110,6 +117,7 @@ def run_ours(args, rank, world, local_rank):
         cfg = synth.Config(**{**cfg.__dict__, "ratio": args.ratio})
     hbm_peak, tc_peak, peak_src = load_peaks()
 
+    log("inputs")
     # ---- inputs (per rank: its own sequence, seeded by rank) -------------------------------
     cache = synth.make_cache(cfg, device=dev, seed=1000 + cfg.cid + 17 * rank)
     scorers = synth.make_scorers(cfg, device=dev)
@@ -151,6 +159,7 @@ def run_ours(args, rank, world, local_rank):
         if evs is not None:
             evs[3].record(stream)
 
+    log("gate")
     # correctness gate before timing: device error latch + exact total
     step()
     ws.status()
@@ -166,6 +175,7 @@ def run_ours(args, rank, world, local_rank):
     for _ in range(args.warmup):
         ev.launch()
     barrier()
+    log("timed A")
     # ---- timed region A (headline): K fused steps through lkv_evict (K2 overlapped with K1)
     ev_a = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     launches0 = lib.lkv_launch_count()
@@ -180,6 +190,7 @@ def run_ours(args, rank, world, local_rank):
     ws.status()
     ms_step = ev_a[0].elapsed_time(ev_a[-1]) / args.steps
     assert int(ev.ragged.lens.sum()) == want_total
+    log("timed B")
     # ---- timed region B (breakdown + roofline): the same stages as separate C-ABI calls
     for _ in range(2):
         step()
@@ -208,6 +219,7 @@ def run_ours(args, rank, world, local_rank):
     kept_rows = want_total
     step_bytes = rows_per_step * (in_bytes + 8) + kept_rows * (4 * D * cache.keys.element_size() + 4)
 
+    log("e2e")
     # ---- end to end through the public API with HOST buffers -----------------------------------
     e2e = None
     if not args.no_e2e:
@@ -253,6 +265,7 @@ def run_ours(args, rank, world, local_rank):
                "path": "pinned host K/V -> lkv_evict (C ABI) -> pinned host ragged cache"}
         del hk, hv, ok, ov, op, oo
 
+    log("decode")
     # ---- decode over the compressed cache --------------------------------------------------------
     decode = None
     if not args.no_decode:
@@ -291,6 +304,7 @@ def run_ours(args, rank, world, local_rank):
                   "frac_of_measured_hbm": dec_gbs / hbm_peak, "frac_of_8tbs_nominal": dec_gbs / 8000.0,
                   "gpu_launches": int(dl), "note": "all 32 layers per launch; kernel = TMA + mma.sync split-K"}
 
+    log("cpu baseline")
     # ---- CPU baseline (rank 0, N=1): the oracle port on a bounded sample ------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -350,43 +350,69 @@ __global__ void __launch_bounds__(kDecThreads, 2)
                 }
             }
         }
-        // split-K: the last chunk of a head to finish merges the head's partials (no combine pass)
-        bool finalize = nch == 1;
+        // split-K: the last chunk of a head to finish merges the head's partials (no combine
+        // pass).  lens / tokens_seen stay untouched during the launch (decode_finish_kernel
+        // advances them), so every block plans from the same snapshot.
         if (nch > 1) {
             __threadfence();
             named_bar_sync(1, kDecConsumers * 32);
             if (threadIdx.x == 0) s_last = atomicAdd(&p.head_done[head], 1) == nch - 1;
             named_bar_sync(1, kDecConsumers * 32);
-            finalize = s_last;
-            if (finalize) {
+            if (s_last) {
                 __threadfence();
                 const int base = p.item_base[head];
                 for (int e = threadIdx.x; e < G * D; e += kDecConsumers * 32) {
-                    const int gg = e / D, dd = e - gg * D;
+                    const int gg = e / D;
+                    const float* pm = p.part_m + (size_t)base * G + gg;
+                    const float* pl = p.part_l + (size_t)base * G + gg;
+                    const float* po = p.part_o + (size_t)base * G * D + e;
                     float M = -INFINITY;
-                    for (int c = 0; c < nch; ++c) M = fmaxf(M, __ldcg(p.part_m + (size_t)(base + c) * G + gg));
+                    int c = 0;
+                    for (; c + 8 <= nch; c += 8) {
+                        float v[8];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) v[k] = __ldcg(pm + (size_t)(c + k) * G);
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) M = fmaxf(M, v[k]);
+                    }
+                    for (; c < nch; ++c) M = fmaxf(M, __ldcg(pm + (size_t)c * G));
                     float L = 0.f, acc = 0.f;
-                    for (int c = 0; c < nch; ++c) {
-                        const size_t i2 = (size_t)(base + c) * G + gg;
-                        const float f = exp2f(__ldcg(p.part_m + i2) - M);
-                        L += __ldcg(p.part_l + i2) * f;
-                        acc += __ldcg(p.part_o + i2 * D + dd) * f;
+                    c = 0;
+                    for (; c + 8 <= nch; c += 8) {
+                        float mv[8], lv[8], ov[8];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            mv[k] = __ldcg(pm + (size_t)(c + k) * G);
+                            lv[k] = __ldcg(pl + (size_t)(c + k) * G);
+                            ov[k] = __ldcg(po + (size_t)(c + k) * G * D);
+                        }
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const float f = exp2f(mv[k] - M);
+                            L = fmaf(lv[k], f, L);
+                            acc = fmaf(ov[k], f, acc);
+                        }
+                    }
+                    for (; c < nch; ++c) {
+                        const float f = exp2f(__ldcg(pm + (size_t)c * G) - M);
+                        L = fmaf(__ldcg(pl + (size_t)c * G), f, L);
+                        acc = fmaf(__ldcg(po + (size_t)c * G * D), f, acc);
                     }
                     outp[e] = __float2bfloat16_rn(acc / L);
                 }
                 if (threadIdx.x == 0) p.head_done[head] = 0;
             }
         }
-        if (finalize && threadIdx.x == 0) {
-            p.lens[head] = len_new;
-            const int sq = sl / (p.heads_per_seq / p.n_kv_heads);
-            if (atomicAdd(&p.seq_done[sq], 1) == p.heads_per_seq - 1) {
-                p.seq_done[sq] = 0;
-                atomicAdd(&p.tokens_seen[sq], 1);  // every head of the sequence has its new row
-            }
-        }
         named_bar_sync(1, kDecConsumers * 32);
     }
+}
+
+// ---- advance lens and tokens_seen after a step (bf16 path) ---------------------------------------
+__global__ void __launch_bounds__(256) decode_finish_kernel(int32_t* lens, int n_heads, int32_t* tokens_seen,
+                                                            int n_seq) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n_heads) lens[i] += 1;
+    if (i < n_seq) tokens_seen[i] += 1;
 }
 
 // ---- fp32 attention kernel (SIMT; correctness configs) --------------------------------------------
@@ -516,7 +542,9 @@ cudaError_t launch_decode(const DecodeParams& p, int dtype, const CUtensorMap* m
         const int per_sm = smem * 2 <= 220 * 1024 ? 2 : 1;
         const int grid = min(p.max_items, per_sm * num_sms);
         decode_attn_bf16_kernel<<<grid, kDecThreads, smem, stream>>>(p, *mk, *mv);
-        note_launches(1);
+        const int n_seq = p.n_heads / p.heads_per_seq;
+        decode_finish_kernel<<<(p.n_heads + 255) / 256, 256, 0, stream>>>(p.lens, p.n_heads, p.tokens_seen, n_seq);
+        note_launches(2);
     } else {
         const size_t smem = ((size_t)p.G * p.head_dim + (size_t)p.G * kDecCh) * sizeof(float);
         cudaError_t e = cudaFuncSetAttribute(decode_attn_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
