@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblkv_b200.so")
+# LKV_B200_LIB overrides the path (developer A/B builds of the same library only)
+LIB_PATH = os.environ.get("LKV_B200_LIB") or os.path.join(_HERE, "liblkv_b200.so")
 
 LKV_OK, CONTRACT, NUMERIC, BUDGET, OVERFLOW_GUARD, DEGENERATE_MASK, CUDA, UNSUPPORTED = range(8)
 F32, BF16 = 0, 1

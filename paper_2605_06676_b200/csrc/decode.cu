@@ -26,7 +26,14 @@ namespace lkv_dev {
 
 constexpr int kDecCh = 256;         // rows per work item
 constexpr int kDecStageRows = 64;   // rows per pipeline stage
-constexpr int kDecStages = 3;  // x 32 KB; two CTAs per SM
+#ifndef LKV_DEC_STAGES
+#define LKV_DEC_STAGES 3
+#endif
+#ifndef LKV_DEC_PER_SM
+#define LKV_DEC_PER_SM 2
+#endif
+constexpr int kDecStages = LKV_DEC_STAGES;  // x 32 KB per CTA
+constexpr int kDecPerSm = LKV_DEC_PER_SM;   // resident CTAs per SM
 constexpr int kDecConsumers = 4;    // consumer warps (16 rows of a stage each)
 constexpr int kDecThreads = (kDecConsumers + 1) * 32;
 
@@ -95,7 +102,7 @@ __device__ __forceinline__ uint32_t sw_off(int row, int q) {
 }
 
 // ---- bf16 attention kernel (tensor cores) ------------------------------------------------------
-__global__ void __launch_bounds__(kDecThreads, 2)
+__global__ void __launch_bounds__(kDecThreads, kDecPerSm)
     decode_attn_bf16_kernel(const __grid_constant__ DecodeParams p, const __grid_constant__ CUtensorMap tmap_k,
                             const __grid_constant__ CUtensorMap tmap_v) {
     constexpr int kStageBytes = 2 * kDecStageRows * 256;  // K + V, 64 rows x 256 B each
@@ -354,12 +361,16 @@ __global__ void __launch_bounds__(kDecThreads, 2)
         // pass).  lens / tokens_seen stay untouched during the launch (decode_finish_kernel
         // advances them), so every block plans from the same snapshot.
         if (nch > 1) {
-            __threadfence();
+            // all consumers' partial stores -> CTA barrier -> one gpu-scope fence + arrival
+            // (fences are cumulative); the last arriver fences again before reading
             named_bar_sync(1, kDecConsumers * 32);
-            if (threadIdx.x == 0) s_last = atomicAdd(&p.head_done[head], 1) == nch - 1;
+            if (threadIdx.x == 0) {
+                __threadfence();
+                s_last = atomicAdd(&p.head_done[head], 1) == nch - 1;
+                if (s_last) __threadfence();
+            }
             named_bar_sync(1, kDecConsumers * 32);
             if (s_last) {
-                __threadfence();
                 const int base = p.item_base[head];
                 for (int e = threadIdx.x; e < G * D; e += kDecConsumers * 32) {
                     const int gg = e / D;
@@ -539,7 +550,7 @@ cudaError_t launch_decode(const DecodeParams& p, int dtype, const CUtensorMap* m
         const size_t smem = decode_bf16_smem(p.G);
         cudaError_t e = cudaFuncSetAttribute(decode_attn_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        const int per_sm = smem * 2 <= 220 * 1024 ? 2 : 1;
+        const int per_sm = (kDecPerSm == 2 && smem * 2 <= 220 * 1024) ? 2 : 1;
         const int grid = min(p.max_items, per_sm * num_sms);
         decode_attn_bf16_kernel<<<grid, kDecThreads, smem, stream>>>(p, *mk, *mv);
         const int n_seq = p.n_heads / p.heads_per_seq;

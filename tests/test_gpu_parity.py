@@ -472,3 +472,49 @@ def test_config2_full_size_properties():
         # spot-check the oracle selection on the device scores for a few heads
         if h % 37 == 0:
             assert (p.cpu().numpy() == O.select_positions_f32(scores[h].cpu().numpy(), bh)).all()
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_decode_crosses_chunk_boundaries(dtype):
+    """Heads sitting just below a 256-row work-item boundary, with empty capacity-based
+    items behind them: every step must plan from the same lens snapshot."""
+    torch.manual_seed(23)
+    L, H, T, D, G = 2, 4, 1100, 128, 4
+    K = torch.randn(1, L, H, T, D, device=DEV).to(dtype)
+    V = torch.randn(1, L, H, T, D, device=DEV).to(dtype)
+    cache = lkv.DenseCache(K, V, [T])
+    masks = torch.zeros(L * H, T, dtype=torch.int32, device=DEV)
+    for h, keep in enumerate([254, 255, 256, 510, 511, 767, 1, 1023]):
+        masks[h, torch.randperm(T, device=DEV)[:keep]] = 1
+    rc = lkv.cache_from_trace(cache, masks, decode_slack=400)
+    scale = 1.0 / math.sqrt(D)
+    tol = 1e-5 if dtype == torch.float32 else 1e-2
+    for step in range(4):
+        q = torch.randn(1, L, H * G, D, device=DEV).to(dtype)
+        nk = torch.randn(1, L, H, D, device=DEV).to(dtype)
+        out = lkv.decode_step(rc, q, nk, nk * 0.5, scale)
+        want = _decode_oracle(rc, q, H, scale)
+        assert rel_gap(out.to(torch.float64).cpu().numpy(), want) <= tol, step
+
+
+def test_decode_many_steps_stays_consistent():
+    """200 steps over a C2-shaped (reduced) cache: lens, positions and outputs stay exact."""
+    cfg = synth.CONFIGS[2]
+    L = 2
+    cache = synth.make_cache(cfg, n_layers=L, max_tokens=2000)
+    scorers = synth.make_scorers(cfg, n_layers=L)
+    logits = synth.make_logits(cfg, n_layers=L)
+    res = lkv.evict(cache, scorers, logits, cfg.ratio, lkv.BUDGET_EXACT, decode_slack=200)
+    rc = res.cache
+    lens0 = rc.lens.clone()
+    for s in range(200):
+        q, k, v = synth.make_decode_inputs(cfg, s, n_layers=L)
+        out = lkv.decode_step(rc, q, k, v, check=(s % 50 == 49))
+    assert torch.equal(rc.lens, lens0 + 200)
+    assert int(rc.tokens_seen[0]) == 2000 + 200
+    want = _decode_oracle(rc, q, cfg.n_kv_heads, 1 / math.sqrt(cfg.head_dim))
+    assert rel_gap(out.to(torch.float64).cpu().numpy(), want) <= 1e-2
+    for h in range(L * cfg.n_kv_heads):
+        _, _, p = rc.head(h)
+        p = p.cpu().numpy()
+        assert (np.diff(p) > 0).all() and p[-1] == 2000 + 199
