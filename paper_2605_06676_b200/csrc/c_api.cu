@@ -266,7 +266,7 @@ lkv_status run_select(const lkv_cache_desc* c, const float* scores, const int32_
 
 // ---- decode workspace -------------------------------------------------------------------------------
 struct DecodeWs {
-    size_t err, n_items, item_base, head_done, seq_done, items, part_m, part_l, part_o, total;
+    size_t err, n_items, item_base, items, part_m, part_l, part_o, total;
     int64_t max_items;
 };
 DecodeWs decode_layout(const lkv_ragged_desc* r, int G) {
@@ -278,10 +278,6 @@ DecodeWs decode_layout(const lkv_ragged_desc* r, int G) {
     w.n_items = o;
     o = align_up(o + sizeof(int32_t));
     w.item_base = o;
-    o = align_up(o + sizeof(int32_t) * (size_t)r->n_heads);
-    w.head_done = o;
-    o = align_up(o + sizeof(int32_t) * (size_t)r->n_heads);
-    w.seq_done = o;  // indexed by sequence; n_heads >= n_seq entries
     o = align_up(o + sizeof(int32_t) * (size_t)r->n_heads);
     w.items = o;
     o = align_up(o + sizeof(DecodeItem) * (size_t)w.max_items);
@@ -498,9 +494,8 @@ lkv_status lkv_decode_plan(const lkv_ragged_desc* r, void* ws, size_t ws_bytes, 
     const DecodeWs w = decode_layout(r, 1);
     lkv_status st = check_ws(ws, ws_bytes, w.items + sizeof(DecodeItem) * (size_t)w.max_items);
     if (st) return st;
-    LKV_CUDA(launch_decode_plan(r->offsets, r->n_heads, r->n_heads, at<DecodeItem>(ws, w.items),
-                                at<int32_t>(ws, w.item_base), at<int32_t>(ws, w.n_items), at<int32_t>(ws, w.head_done),
-                                at<int32_t>(ws, w.seq_done), (cudaStream_t)stream),
+    LKV_CUDA(launch_decode_plan(r->offsets, r->n_heads, at<DecodeItem>(ws, w.items), at<int32_t>(ws, w.item_base),
+                                at<int32_t>(ws, w.n_items), (cudaStream_t)stream),
              "decode plan");
     return LKV_OK;
 }
@@ -549,8 +544,6 @@ lkv_status lkv_decode_step(const lkv_ragged_desc* r, int32_t n_seq, int32_t n_la
     p.part_m = at<float>(ws, w.part_m);
     p.part_l = at<float>(ws, w.part_l);
     p.part_o = at<float>(ws, w.part_o);
-    p.head_done = at<int32_t>(ws, w.head_done);
-    p.seq_done = at<int32_t>(ws, w.seq_done);
     p.err = at<ErrWord>(ws, w.err);
     CUtensorMap mk, mv;
     if (r->dtype == LKV_BF16) {

@@ -10,14 +10,14 @@
 //  * work items = (head, 256-row chunk) over each head's capacity, planned once
 //    per eviction (decode_plan_kernel); a persistent grid walks them;
 //  * per CTA: one TMA producer warp streams 64-row K+V stages (128-byte
-//    swizzle, 32 KB) through a 4-stage mbarrier ring; four consumer warps each
+//    swizzle, 32 KB) through a 3-stage mbarrier ring (2 CTAs/SM); four consumer warps each
 //    take 16 rows of a stage and run S = Q K^T and O += P V on tensor cores
 //    (mma.sync m16n8k16 bf16, ldmatrix from the swizzled tiles), every K/V
 //    byte read once for all G query heads of the group;
 //  * the chunk containing the appended row patches it into shared memory and
 //    writes it (plus its position) into the cache, so no separate append pass;
 //  * split-K partials (m, l, o) are merged by decode_combine_kernel, which also
-//    advances lens and tokens_seen.
+//    advances lens and tokens_seen (heads that fit one chunk are finalised in place).
 #include <math.h>
 
 #include "kernels.cuh"
@@ -40,14 +40,11 @@ constexpr int kDecThreads = (kDecConsumers + 1) * 32;
 
 
 // ---- plan: work items over each head's capacity (once per eviction) -------------------------
-__global__ void __launch_bounds__(1024) decode_plan_kernel(const int64_t* offsets, int n_heads, int n_seq,
-                                                           DecodeItem* items, int32_t* item_base, int32_t* n_items_out,
-                                                           int32_t* head_done, int32_t* seq_done) {
+__global__ void __launch_bounds__(1024) decode_plan_kernel(const int64_t* offsets, int n_heads, DecodeItem* items,
+                                                           int32_t* item_base, int32_t* n_items_out) {
     __shared__ uint32_t s_scan[33];
     __shared__ int32_t s_carry;
     if (threadIdx.x == 0) s_carry = 0;
-    for (int h = threadIdx.x; h < n_heads; h += 1024) head_done[h] = 0;
-    for (int q = threadIdx.x; q < n_seq; q += 1024) seq_done[q] = 0;
     __syncthreads();
     for (int base = 0; base < n_heads; base += 1024) {
         const int h = base + threadIdx.x;
@@ -111,7 +108,6 @@ __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kDecStages * kStageBytes);
     uint64_t* empty = full + kDecStages;
     float* red = reinterpret_cast<float*>(empty + kDecStages);  // [consumers][G][D + 2]
-    __shared__ int s_last;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int G = p.G;
@@ -357,73 +353,8 @@ __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
                 }
             }
         }
-        // split-K: the last chunk of a head to finish merges the head's partials (no combine
-        // pass).  lens / tokens_seen stay untouched during the launch (decode_finish_kernel
-        // advances them), so every block plans from the same snapshot.
-        if (nch > 1) {
-            // all consumers' partial stores -> CTA barrier -> one gpu-scope fence + arrival
-            // (fences are cumulative); the last arriver fences again before reading
-            named_bar_sync(1, kDecConsumers * 32);
-            if (threadIdx.x == 0) {
-                __threadfence();
-                s_last = atomicAdd(&p.head_done[head], 1) == nch - 1;
-                if (s_last) __threadfence();
-            }
-            named_bar_sync(1, kDecConsumers * 32);
-            if (s_last) {
-                const int base = p.item_base[head];
-                for (int e = threadIdx.x; e < G * D; e += kDecConsumers * 32) {
-                    const int gg = e / D;
-                    const float* pm = p.part_m + (size_t)base * G + gg;
-                    const float* pl = p.part_l + (size_t)base * G + gg;
-                    const float* po = p.part_o + (size_t)base * G * D + e;
-                    float M = -INFINITY;
-                    int c = 0;
-                    for (; c + 8 <= nch; c += 8) {
-                        float v[8];
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) v[k] = __ldcg(pm + (size_t)(c + k) * G);
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) M = fmaxf(M, v[k]);
-                    }
-                    for (; c < nch; ++c) M = fmaxf(M, __ldcg(pm + (size_t)c * G));
-                    float L = 0.f, acc = 0.f;
-                    c = 0;
-                    for (; c + 8 <= nch; c += 8) {
-                        float mv[8], lv[8], ov[8];
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) {
-                            mv[k] = __ldcg(pm + (size_t)(c + k) * G);
-                            lv[k] = __ldcg(pl + (size_t)(c + k) * G);
-                            ov[k] = __ldcg(po + (size_t)(c + k) * G * D);
-                        }
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) {
-                            const float f = exp2f(mv[k] - M);
-                            L = fmaf(lv[k], f, L);
-                            acc = fmaf(ov[k], f, acc);
-                        }
-                    }
-                    for (; c < nch; ++c) {
-                        const float f = exp2f(__ldcg(pm + (size_t)c * G) - M);
-                        L = fmaf(__ldcg(pl + (size_t)c * G), f, L);
-                        acc = fmaf(__ldcg(po + (size_t)c * G * D), f, acc);
-                    }
-                    outp[e] = __float2bfloat16_rn(acc / L);
-                }
-                if (threadIdx.x == 0) p.head_done[head] = 0;
-            }
-        }
         named_bar_sync(1, kDecConsumers * 32);
     }
-}
-
-// ---- advance lens and tokens_seen after a step (bf16 path) ---------------------------------------
-__global__ void __launch_bounds__(256) decode_finish_kernel(int32_t* lens, int n_heads, int32_t* tokens_seen,
-                                                            int n_seq) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n_heads) lens[i] += 1;
-    if (i < n_seq) tokens_seen[i] += 1;
 }
 
 // ---- fp32 attention kernel (SIMT; correctness configs) --------------------------------------------
@@ -498,43 +429,71 @@ __global__ void __launch_bounds__(kDecSimtThreads) decode_attn_f32_kernel(const 
 }
 
 // ---- combine split-K partials; advance lens and tokens_seen ------------------------------------------
+// One CTA per head.  Phase 1 turns the chunk maxima / sums into per-chunk weights in
+// shared memory; phase 2 streams the partial outputs with independent (unrolled) loads.
+// Heads that fit one chunk were finalised by the attention kernel (bf16 path).
+constexpr int kCombThreads = 128;
+constexpr int kCombMaxChunks = 8192;  // G * chunks per head (G=4: 2M rows, G=8: 1M rows)
+
 template <typename T>
-__global__ void __launch_bounds__(256) decode_combine_kernel(const __grid_constant__ DecodeParams p) {
+__global__ void __launch_bounds__(kCombThreads) decode_combine_kernel(const __grid_constant__ DecodeParams p,
+                                                                      int single_chunk_done) {
+    __shared__ float s_w[kCombMaxChunks];  // [c * G + g] weight exp2(m_c - M_g) / L_g
+    __shared__ float s_M[16], s_L[16];
     const int head = blockIdx.x;
     const int D = p.head_dim, G = p.G;
     const int len_new = p.lens[head] + 1;
     const int nch = (len_new + kDecCh - 1) / kDecCh;
-    const int base = p.item_base[head];
-    const int sl = head / p.n_kv_heads, kvh = head - sl * p.n_kv_heads;
-    T* out = static_cast<T*>(p.out) + ((size_t)sl * p.n_q_heads + kvh * G) * D;
-    for (int e = threadIdx.x; e < G * D; e += blockDim.x) {
-        const int gg = e / D, dd = e - gg * D;
-        float M = -INFINITY;
-        for (int c = 0; c < nch; ++c) M = fmaxf(M, p.part_m[(size_t)(base + c) * G + gg]);
-        float L = 0.f, acc = 0.f;
-        for (int c = 0; c < nch; ++c) {
-            const size_t i = (size_t)(base + c) * G + gg;
-            const float f = exp2f(p.part_m[i] - M);
-            L += p.part_l[i] * f;
-            acc += p.part_o[i * D + dd] * f;
+    if (!(single_chunk_done && nch == 1) && nch * G <= kCombMaxChunks) {
+        const int base = p.item_base[head];
+        const float* pm = p.part_m + (size_t)base * G;
+        const float* pl = p.part_l + (size_t)base * G;
+        const float* po = p.part_o + (size_t)base * G * D;
+        if (threadIdx.x < G) {
+            const int g = threadIdx.x;
+            float M = -INFINITY;
+            for (int c = 0; c < nch; ++c) M = fmaxf(M, pm[c * G + g]);
+            float L = 0.f;
+            for (int c = 0; c < nch; ++c) L += pl[c * G + g] * exp2f(pm[c * G + g] - M);
+            s_M[g] = M;
+            s_L[g] = L;
         }
-        const float v = acc / L;
-        if constexpr (sizeof(T) == 2) out[(size_t)gg * D + dd] = __float2bfloat16_rn(v);
-        else out[(size_t)gg * D + dd] = v;
+        __syncthreads();
+        for (int i = threadIdx.x; i < nch * G; i += kCombThreads) {
+            const int g = i % G;
+            s_w[i] = exp2f(pm[i] - s_M[g]) / s_L[g];
+        }
+        __syncthreads();
+        const int sl = head / p.n_kv_heads, kvh = head - sl * p.n_kv_heads;
+        T* out = static_cast<T*>(p.out) + ((size_t)sl * p.n_q_heads + kvh * G) * D;
+        for (int e = threadIdx.x; e < G * D; e += kCombThreads) {
+            const int g = e / D;
+            float acc = 0.f;
+            int c = 0;
+            for (; c + 8 <= nch; c += 8) {
+                float v[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) v[k] = po[(size_t)(c + k) * G * D + e];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) acc = fmaf(v[k], s_w[(c + k) * G + g], acc);
+            }
+            for (; c < nch; ++c) acc = fmaf(po[(size_t)c * G * D + e], s_w[c * G + g], acc);
+            if constexpr (sizeof(T) == 2) out[e] = __float2bfloat16_rn(acc);
+            else out[e] = acc;
+        }
+    } else if (nch * G > kCombMaxChunks && threadIdx.x == 0) {
+        latch_error(p.err, LKV_ERR_UNSUPPORTED, head);
     }
-    __syncthreads();
     if (threadIdx.x == 0) {
         p.lens[head] = len_new;
-        const int hps = p.heads_per_seq;
-        if (head % hps == 0) atomicAdd(&p.tokens_seen[head / hps], 1);
+        if (head % p.heads_per_seq == 0) p.tokens_seen[head / p.heads_per_seq] += 1;
     }
 }
 
 // ---- host launchers ---------------------------------------------------------------------------------
-cudaError_t launch_decode_plan(const int64_t* offsets, int n_heads, int n_seq, DecodeItem* items, int32_t* item_base,
-                               int32_t* n_items, int32_t* head_done, int32_t* seq_done, cudaStream_t stream) {
-    decode_plan_kernel<<<1, 1024, 0, stream>>>(offsets, n_heads, n_seq, items, item_base, n_items, head_done,
-                                               seq_done);
+cudaError_t launch_decode_plan(const int64_t* offsets, int n_heads, DecodeItem* items, int32_t* item_base,
+                               int32_t* n_items, cudaStream_t stream) {
+    decode_plan_kernel<<<1, 1024, 0, stream>>>(offsets, n_heads, items, item_base, n_items);
     note_launches(1);
     return cudaGetLastError();
 }
@@ -553,8 +512,7 @@ cudaError_t launch_decode(const DecodeParams& p, int dtype, const CUtensorMap* m
         const int per_sm = (kDecPerSm == 2 && smem * 2 <= 220 * 1024) ? 2 : 1;
         const int grid = min(p.max_items, per_sm * num_sms);
         decode_attn_bf16_kernel<<<grid, kDecThreads, smem, stream>>>(p, *mk, *mv);
-        const int n_seq = p.n_heads / p.heads_per_seq;
-        decode_finish_kernel<<<(p.n_heads + 255) / 256, 256, 0, stream>>>(p.lens, p.n_heads, p.tokens_seen, n_seq);
+        decode_combine_kernel<__nv_bfloat16><<<p.n_heads, kCombThreads, 0, stream>>>(p, 1);
         note_launches(2);
     } else {
         const size_t smem = ((size_t)p.G * p.head_dim + (size_t)p.G * kDecCh) * sizeof(float);
@@ -563,7 +521,7 @@ cudaError_t launch_decode(const DecodeParams& p, int dtype, const CUtensorMap* m
         decode_attn_f32_kernel<<<p.max_items, kDecSimtThreads, smem, stream>>>(p);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
-        decode_combine_kernel<float><<<p.n_heads, 256, 0, stream>>>(p);
+        decode_combine_kernel<float><<<p.n_heads, kCombThreads, 0, stream>>>(p, 0);
         note_launches(2);
     }
     return cudaGetLastError();

@@ -106,12 +106,10 @@ struct DecodeParams {
     float* part_m;
     float* part_l;
     float* part_o;
-    int32_t* head_done;  // [n_heads] split-K arrival counters (zeroed by the plan)
-    int32_t* seq_done;   // [n_seq] finished heads per sequence this step
     ErrWord* err;
 };
-cudaError_t launch_decode_plan(const int64_t* offsets, int n_heads, int n_seq, DecodeItem* items, int32_t* item_base,
-                               int32_t* n_items, int32_t* head_done, int32_t* seq_done, cudaStream_t stream);
+cudaError_t launch_decode_plan(const int64_t* offsets, int n_heads, DecodeItem* items, int32_t* item_base,
+                               int32_t* n_items, cudaStream_t stream);
 cudaError_t launch_decode(const DecodeParams& p, int dtype, const CUtensorMap* mk, const CUtensorMap* mv, int num_sms,
                           cudaStream_t stream);
 }  // namespace lkv_dev
