@@ -144,6 +144,13 @@ lkv_status lkv_budgets(const double* logits, int32_t n, double target_ratio, int
                        double* ratios, int32_t* budgets, int64_t* offsets,
                        void* workspace, size_t workspace_bytes, lkv_stream_t stream);
 
+/* freeze_budgets on an existing ratio table (policy.cpp:122-129): ratios device fp64 [n]
+ * -> budgets [n_seq * n] per mode (EXACT needs target_ratio in (0,1)); offsets nullable. */
+lkv_status lkv_freeze_budgets(const double* ratios, int32_t n, double target_ratio, int32_t mode,
+                              const int32_t* seq_lens, int32_t n_seq, int32_t decode_slack,
+                              int32_t* budgets, int64_t* offsets, void* workspace,
+                              size_t workspace_bytes, lkv_stream_t stream);
+
 /* Exclusive scan of (budgets[i] + decode_slack) -> offsets[n_heads+1] (device). */
 lkv_status lkv_ragged_offsets(const int32_t* budgets, int32_t n_heads, int32_t decode_slack,
                               int64_t* offsets, lkv_stream_t stream);

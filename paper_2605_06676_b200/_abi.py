@@ -23,7 +23,7 @@ MAX_SEQ = 256
 
 EXPORTED = [
     "lkv_abi_version", "lkv_launch_count", "lkv_last_error", "lkv_status_name", "lkv_device_check", "lkv_workspace_bytes",
-    "lkv_workspace_init", "lkv_workspace_status", "lkv_ragged_capacity", "lkv_budgets", "lkv_ragged_offsets",
+    "lkv_workspace_init", "lkv_workspace_status", "lkv_ragged_capacity", "lkv_budgets", "lkv_freeze_budgets", "lkv_ragged_offsets",
     "lkv_score", "lkv_select", "lkv_compact", "lkv_evict", "lkv_decode_workspace_bytes", "lkv_decode_plan",
     "lkv_decode_step",
 ]
@@ -74,6 +74,7 @@ def load():
     L.lkv_ragged_capacity.restype = i64
     L.lkv_ragged_capacity.argtypes = [P(CacheDesc), dbl, i32]
     L.lkv_budgets.argtypes = [vp, i32, dbl, i32, P(i32), i32, i32, vp, vp, vp, vp, sz, vp]
+    L.lkv_freeze_budgets.argtypes = [vp, i32, dbl, i32, P(i32), i32, i32, vp, vp, vp, sz, vp]
     L.lkv_ragged_offsets.argtypes = [vp, i32, i32, vp, vp]
     L.lkv_score.argtypes = [P(CacheDesc), P(ScorerDesc), vp, vp, sz, vp]
     L.lkv_select.argtypes = [P(CacheDesc), vp, vp, P(RaggedDesc), i32, vp, sz, vp]
@@ -83,7 +84,7 @@ def load():
     L.lkv_decode_workspace_bytes.argtypes = [P(RaggedDesc), i32]
     L.lkv_decode_plan.argtypes = [P(RaggedDesc), vp, sz, vp]
     L.lkv_decode_step.argtypes = [P(RaggedDesc), i32, i32, i32, i32, vp, vp, vp, vp, vp, dbl, vp, sz, vp]
-    for name in ["lkv_workspace_init", "lkv_workspace_status", "lkv_budgets", "lkv_ragged_offsets", "lkv_score",
+    for name in ["lkv_workspace_init", "lkv_workspace_status", "lkv_budgets", "lkv_freeze_budgets", "lkv_ragged_offsets", "lkv_score",
                  "lkv_select", "lkv_compact", "lkv_evict", "lkv_decode_plan", "lkv_decode_step"]:
         getattr(L, name).restype = C.c_int
     _lib = L

@@ -54,6 +54,90 @@ __device__ __forceinline__ double candidate_lambda(int m, int n, double k, doubl
     return d - log(root + a) - l1;
 }
 
+// Freeze ratios into integer budgets per sequence and scan the ragged offsets
+// (policy.cpp:122-129 + SURVEY A.2); shared by the solve path and the given-ratios path.
+__device__ void freeze_and_offsets(const BudgetParams& p, const double* r, double* rem, int32_t* fl, int32_t* delta,
+                                   long long* s_sum_p, int64_t* s_carry_p, uint32_t* s_scan) {
+    const int n = p.n;
+    const int tid = threadIdx.x;
+    long long& s_sum = *s_sum_p;
+    int64_t& s_carry = *s_carry_p;
+    if (p.ratios_out)
+        for (int i = tid; i < n; i += kBudgetThreads) p.ratios_out[i] = r[i];
+
+    // -- freeze per sequence
+    for (int s = 0; s < p.n_seq; ++s) {
+        const int t = p.seq_len[s];
+        if (tid == 0) s_sum = 0;
+        __syncthreads();
+        long long local = 0;
+        for (int i = tid; i < n; i += kBudgetThreads) {
+            const double prod = r[i] * t;
+            const double f = floor(prod);
+            fl[i] = (int32_t)f;
+            rem[i] = prod - f;
+            delta[i] = 0;
+            local += (int32_t)f;
+        }
+        atomicAdd(reinterpret_cast<unsigned long long*>(&s_sum), (unsigned long long)local);
+        __syncthreads();
+        if (p.mode == LKV_BUDGET_EXACT) {
+            const long long total = llround(p.R * n * t);
+            const long long D = total - s_sum;
+            if (D > n || D < -n) {
+                if (tid == 0) latch_error(p.err, LKV_ERR_NUMERIC, 3);
+                return;
+            }
+            if (D != 0) {
+                const long long need = D > 0 ? D : -D;
+                for (int i = tid; i < n; i += kBudgetThreads) {
+                    const bool elig_i = D > 0 ? (fl[i] < t) : (fl[i] > 0);
+                    if (!elig_i) continue;
+                    const double ri = rem[i];
+                    long long rank = 0;
+                    for (int j = 0; j < n; ++j) {
+                        const bool elig_j = D > 0 ? (fl[j] < t) : (fl[j] > 0);
+                        if (!elig_j || j == i) continue;
+                        const double rj = rem[j];
+                        if (D > 0) rank += (rj > ri) || (rj == ri && j < i);
+                        else rank += (rj < ri) || (rj == ri && j > i);
+                    }
+                    if (rank < need) delta[i] = D > 0 ? 1 : -1;
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    long long given = 0;
+                    for (int i = 0; i < n; ++i) given += delta[i] != 0;
+                    if (given != need) latch_error(p.err, LKV_ERR_NUMERIC, 4);
+                }
+            }
+        }
+        __syncthreads();
+        for (int i = tid; i < n; i += kBudgetThreads) p.budgets_out[(size_t)s * n + i] = fl[i] + delta[i];
+        __syncthreads();
+    }
+
+    // -- offsets = exclusive scan of (budget + slack)
+    if (p.offsets_out) {
+        __threadfence_block();
+        __syncthreads();
+        const int64_t total_heads = (int64_t)p.n_seq * n;
+        if (tid == 0) s_carry = 0;
+        __syncthreads();
+        for (int64_t base = 0; base < total_heads; base += kBudgetThreads) {
+            const int64_t i = base + tid;
+            const uint32_t v = i < total_heads ? uint32_t(p.budgets_out[i] + p.slack) : 0u;
+            uint32_t tot;
+            const uint32_t ex = block_exclusive_scan<kBudgetThreads>(v, s_scan, &tot);
+            if (i < total_heads) p.offsets_out[i] = s_carry + ex;
+            __syncthreads();
+            if (tid == 0) s_carry += tot;
+            __syncthreads();
+        }
+        if (tid == 0) p.offsets_out[total_heads] = s_carry;
+    }
+}
+
 __global__ void __launch_bounds__(kBudgetThreads, 1) budgets_kernel(const BudgetParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int n = p.n;
@@ -78,6 +162,12 @@ __global__ void __launch_bounds__(kBudgetThreads, 1) budgets_kernel(const Budget
     __shared__ uint32_t s_scan[kBudgetThreads / 32 + 1];
 
     const int tid = threadIdx.x;
+    if (p.ratios_in) {  // freeze caller-given ratios (freeze_budgets on an existing BudgetTable)
+        for (int i = tid; i < n; i += kBudgetThreads) r[i] = p.ratios_in[i];
+        __syncthreads();
+        freeze_and_offsets(p, r, rem, fl, delta, &s_sum, &s_carry, s_scan);
+        return;
+    }
     if (tid == 0) {
         s_first_bad = INT_MAX;
         s_first_ok = INT_MAX;
@@ -216,80 +306,7 @@ __global__ void __launch_bounds__(kBudgetThreads, 1) budgets_kernel(const Budget
         __syncthreads();
         if (s_fail) return;
     }
-    if (p.ratios_out)
-        for (int i = tid; i < n; i += kBudgetThreads) p.ratios_out[i] = r[i];
-
-    // -- freeze per sequence
-    for (int s = 0; s < p.n_seq; ++s) {
-        const int t = p.seq_len[s];
-        if (tid == 0) s_sum = 0;
-        __syncthreads();
-        long long local = 0;
-        for (int i = tid; i < n; i += kBudgetThreads) {
-            const double prod = r[i] * t;
-            const double f = floor(prod);
-            fl[i] = (int32_t)f;
-            rem[i] = prod - f;
-            delta[i] = 0;
-            local += (int32_t)f;
-        }
-        atomicAdd(reinterpret_cast<unsigned long long*>(&s_sum), (unsigned long long)local);
-        __syncthreads();
-        if (p.mode == LKV_BUDGET_EXACT) {
-            const long long total = llround(p.R * n * t);
-            const long long D = total - s_sum;
-            if (D > n || D < -n) {
-                if (tid == 0) latch_error(p.err, LKV_ERR_NUMERIC, 3);
-                return;
-            }
-            if (D != 0) {
-                const long long need = D > 0 ? D : -D;
-                for (int i = tid; i < n; i += kBudgetThreads) {
-                    const bool elig_i = D > 0 ? (fl[i] < t) : (fl[i] > 0);
-                    if (!elig_i) continue;
-                    const double ri = rem[i];
-                    long long rank = 0;
-                    for (int j = 0; j < n; ++j) {
-                        const bool elig_j = D > 0 ? (fl[j] < t) : (fl[j] > 0);
-                        if (!elig_j || j == i) continue;
-                        const double rj = rem[j];
-                        if (D > 0) rank += (rj > ri) || (rj == ri && j < i);
-                        else rank += (rj < ri) || (rj == ri && j > i);
-                    }
-                    if (rank < need) delta[i] = D > 0 ? 1 : -1;
-                }
-                __syncthreads();
-                if (tid == 0) {
-                    long long given = 0;
-                    for (int i = 0; i < n; ++i) given += delta[i] != 0;
-                    if (given != need) latch_error(p.err, LKV_ERR_NUMERIC, 4);
-                }
-            }
-        }
-        __syncthreads();
-        for (int i = tid; i < n; i += kBudgetThreads) p.budgets_out[(size_t)s * n + i] = fl[i] + delta[i];
-        __syncthreads();
-    }
-
-    // -- offsets = exclusive scan of (budget + slack)
-    if (p.offsets_out) {
-        __threadfence_block();
-        __syncthreads();
-        const int64_t total_heads = (int64_t)p.n_seq * n;
-        if (tid == 0) s_carry = 0;
-        __syncthreads();
-        for (int64_t base = 0; base < total_heads; base += kBudgetThreads) {
-            const int64_t i = base + tid;
-            const uint32_t v = i < total_heads ? uint32_t(p.budgets_out[i] + p.slack) : 0u;
-            uint32_t tot;
-            const uint32_t ex = block_exclusive_scan<kBudgetThreads>(v, s_scan, &tot);
-            if (i < total_heads) p.offsets_out[i] = s_carry + ex;
-            __syncthreads();
-            if (tid == 0) s_carry += tot;
-            __syncthreads();
-        }
-        if (tid == 0) p.offsets_out[total_heads] = s_carry;
-    }
+    freeze_and_offsets(p, r, rem, fl, delta, &s_sum, &s_carry, s_scan);
 }
 
 // Exclusive scan of (budgets + slack) for caller-supplied budgets.

@@ -392,6 +392,35 @@ lkv_status lkv_budgets(const double* logits, int32_t n, double R, int32_t mode, 
     return LKV_OK;
 }
 
+lkv_status lkv_freeze_budgets(const double* ratios, int32_t n, double R, int32_t mode, const int32_t* seq_lens,
+                              int32_t n_seq, int32_t slack, int32_t* budgets, int64_t* offsets, void* ws,
+                              size_t ws_bytes, lkv_stream_t stream) {
+    if (mode != LKV_BUDGET_FLOOR && mode != LKV_BUDGET_EXACT) return fail(LKV_ERR_CONTRACT, "unknown budget mode");
+    if (mode == LKV_BUDGET_EXACT && !(R > 0.0 && R < 1.0)) return fail(LKV_ERR_BUDGET, "target ratio must lie in (0,1)");
+    if (n < 1 || n > 3072) return fail(LKV_ERR_CONTRACT, "freeze_budgets: need 1 <= n <= 3072 ratios");
+    if (n_seq < 1 || n_seq > LKV_MAX_SEQ || !seq_lens) return fail(LKV_ERR_CONTRACT, "bad sequence table");
+    for (int s = 0; s < n_seq; ++s)
+        if (seq_lens[s] < 1) return fail(LKV_ERR_CONTRACT, "freeze_budgets: t must be >= 1");  // policy.cpp:123
+    if (!ratios || !budgets) return fail(LKV_ERR_CONTRACT, "ratios/budgets are null");
+    if (slack < 0) return fail(LKV_ERR_CONTRACT, "decode_slack must be >= 0");
+    lkv_status st = check_ws(ws, ws_bytes, sizeof(ErrWord));
+    if (st) return st;
+    BudgetParams p;
+    memset(&p, 0, sizeof p);
+    p.ratios_in = ratios;
+    p.n = n;
+    p.mode = mode;
+    p.R = R;
+    p.n_seq = n_seq;
+    p.slack = slack;
+    p.budgets_out = budgets;
+    p.offsets_out = offsets;
+    p.err = at<ErrWord>(ws, 0);
+    for (int s = 0; s < n_seq; ++s) p.seq_len[s] = seq_lens[s];
+    LKV_CUDA(launch_budgets(p, (cudaStream_t)stream), "freeze budgets");
+    return LKV_OK;
+}
+
 lkv_status lkv_ragged_offsets(const int32_t* budgets, int32_t n_heads, int32_t slack, int64_t* offsets,
                               lkv_stream_t stream) {
     if (!budgets || !offsets || n_heads < 1 || slack < 0) return fail(LKV_ERR_CONTRACT, "bad ragged_offsets arguments");

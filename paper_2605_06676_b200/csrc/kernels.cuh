@@ -17,6 +17,7 @@ struct BudgetParams {
     int32_t n_seq;
     int32_t slack;
     double* ratios_out;
+    const double* ratios_in;  // non-null: skip the solve, freeze these ratios
     int32_t* budgets_out;
     int64_t* offsets_out;
     ErrWord* err;

@@ -1,0 +1,477 @@
+// lkv_dropin.cpp -- C++ host layer: the reference's hot-path API (lkv::) re-expressed over
+// the C ABI of the sm_100a kernels (include/lkv_b200.h).  See include/lkv_b200_dropin.hpp.
+//
+// Every call: validate like the reference (same exception types and conditions), upload
+// host buffers, run the device kernels on a per-thread stream, synchronise, read back,
+// and rethrow device-latched errors.  No computation happens on the host except the
+// bookkeeping the reference itself does on the host (mask -> index lists, accounting).
+#include "../../include/lkv_b200_dropin.hpp"
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <limits>
+
+#include "../../include/lkv_b200.h"
+
+namespace lkv::b200 {
+namespace {
+
+[[noreturn]] void rethrow(int status, const std::string& where) {
+    const std::string msg = where + ": " + lkv_last_error();
+    switch (status) {
+        case LKV_ERR_CONTRACT: throw contract_error(msg);
+        case LKV_ERR_NUMERIC: throw numeric_error(msg);
+        case LKV_ERR_BUDGET: throw budget_error(msg);
+        case LKV_ERR_OVERFLOW_GUARD: throw overflow_guard_error(msg);
+        case LKV_ERR_DEGENERATE_MASK: throw degenerate_mask_error(msg);
+        default: throw device_error(msg);
+    }
+}
+
+void check(lkv_status s, const char* where) {
+    if (s != LKV_OK) rethrow(s, where);
+}
+
+void cuda(cudaError_t e, const char* where) {
+    if (e != cudaSuccess) throw device_error(std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+cudaStream_t stream() {
+    thread_local cudaStream_t s = nullptr;
+    if (!s) cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream create");
+    return s;
+}
+
+// RAII device buffer
+struct Dev {
+    void* p = nullptr;
+    size_t n = 0;
+    Dev() = default;
+    explicit Dev(size_t bytes) : n(bytes) {
+        if (bytes) cuda(cudaMalloc(&p, bytes + 256), "cudaMalloc");
+    }
+    ~Dev() {
+        if (p) cudaFree(p);
+    }
+    Dev(const Dev&) = delete;
+    Dev& operator=(const Dev&) = delete;
+    Dev(Dev&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+    void* aligned() const { return reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(p) + 255) & ~uintptr_t(255)); }
+};
+
+template <class T>
+Dev upload(const T* src, size_t count) {
+    Dev d(sizeof(T) * count);
+    if (count) cuda(cudaMemcpyAsync(d.p, src, sizeof(T) * count, cudaMemcpyHostToDevice, stream()), "H2D");
+    return d;
+}
+
+template <class T>
+std::vector<T> download(const Dev& d, size_t count, size_t offset_elems = 0) {
+    std::vector<T> out(count);
+    if (count)
+        cuda(cudaMemcpyAsync(out.data(), d.as<T>() + offset_elems, sizeof(T) * count, cudaMemcpyDeviceToHost, stream()),
+             "D2H");
+    cuda(cudaStreamSynchronize(stream()), "sync");
+    return out;
+}
+
+// host fp64 -> device element (fp32 or bf16 bits, round to nearest even)
+std::vector<uint16_t> to_bf16(std::span<const double> x) {
+    std::vector<uint16_t> o(x.size());
+    for (size_t i = 0; i < x.size(); ++i) o[i] = __bfloat16_as_ushort(__float2bfloat16_rn(static_cast<float>(x[i])));
+    return o;
+}
+std::vector<float> to_f32(std::span<const double> x) { return std::vector<float>(x.begin(), x.end()); }
+
+Dev upload_elems(std::span<const double> x, Precision prec) {
+    if (prec == Precision::bf16) {
+        auto v = to_bf16(x);
+        return upload(v.data(), v.size());
+    }
+    auto v = to_f32(x);
+    return upload(v.data(), v.size());
+}
+
+std::vector<double> download_elems(const Dev& d, size_t count, size_t offset_elems, Precision prec) {
+    std::vector<double> out(count);
+    if (prec == Precision::bf16) {
+        auto v = download<uint16_t>(d, count, offset_elems);
+        for (size_t i = 0; i < count; ++i) out[i] = __bfloat162float(__ushort_as_bfloat16(v[i]));
+    } else {
+        auto v = download<float>(d, count, offset_elems);
+        for (size_t i = 0; i < count; ++i) out[i] = v[i];
+    }
+    return out;
+}
+
+int dtype_of(Precision p) { return p == Precision::bf16 ? LKV_BF16 : LKV_F32; }
+
+struct Workspace {
+    Dev buf;
+    size_t bytes;
+    explicit Workspace(size_t b) : buf(b + 256), bytes(b) {
+        check(lkv_workspace_init(ptr(), bytes, (lkv_stream_t)stream()), "workspace");
+    }
+    void* ptr() const { return buf.aligned(); }
+    void status(const char* where) { check(lkv_workspace_status(ptr(), (lkv_stream_t)stream()), where); }
+};
+
+// W1 [in x hidden] (reference layout) -> device W1^T [hidden x in] in the compute dtype
+std::vector<double> transpose_w1(const Mlp2& m) {
+    std::vector<double> t((size_t)m.in * m.hidden);
+    for (int i = 0; i < m.in; ++i)
+        for (int j = 0; j < m.hidden; ++j) t[(size_t)j * m.in + i] = m.w1[(size_t)i * m.hidden + j];
+    return t;
+}
+
+void check_mlp(const Mlp2& m, int in) {
+    if (m.in != in || m.hidden < 1 || m.w1.size() != (size_t)m.in * m.hidden || m.b1.size() != (size_t)m.hidden ||
+        m.w2.size() != (size_t)m.hidden)
+        throw contract_error("scorer shape does not match the key/value width");
+}
+
+}  // namespace
+
+void require_b200() { check(lkv_device_check(), "device"); }
+
+// ---- policy.cpp:110-129 -----------------------------------------------------------------------------
+BudgetTable allocate_budgets(std::span<const double> scores, double target_ratio, int n_layers, int n_kv_heads) {
+    if (!(target_ratio > 0.0 && target_ratio < 1.0)) throw budget_error("target ratio must lie in (0,1)");
+    const int n = n_layers * n_kv_heads;
+    if ((int)scores.size() != n || n < 1) throw contract_error("allocate_budgets: score length mismatch");
+    Dev logits = upload(scores.data(), scores.size());
+    Dev ratios(sizeof(double) * n), budgets(sizeof(int32_t) * n);
+    Workspace ws(256);
+    const int32_t one = 1;
+    check(lkv_budgets(logits.as<double>(), n, target_ratio, LKV_BUDGET_FLOOR, &one, 1, 0, ratios.as<double>(),
+                      budgets.as<int32_t>(), nullptr, ws.ptr(), ws.bytes, (lkv_stream_t)stream()),
+          "allocate_budgets");
+    ws.status("allocate_budgets");
+    BudgetTable t;
+    t.n_layers = n_layers;
+    t.n_kv_heads = n_kv_heads;
+    t.target_ratio = target_ratio;
+    t.ratios = download<double>(ratios, n);
+    t.logits.assign(scores.begin(), scores.end());
+    return t;
+}
+
+static std::vector<int> freeze(const BudgetTable& table, int t, int mode) {
+    if (t < 1) throw contract_error("freeze_budgets: t must be >= 1");
+    const int n = table.n_layers * table.n_kv_heads;
+    if ((int)table.ratios.size() != n || n < 1) throw contract_error("freeze_budgets: ratio table size mismatch");
+    Dev ratios = upload(table.ratios.data(), table.ratios.size());
+    Dev budgets(sizeof(int32_t) * n);
+    Workspace ws(256);
+    const int32_t tt = t;
+    check(lkv_freeze_budgets(ratios.as<double>(), n, table.target_ratio, mode, &tt, 1, 0, budgets.as<int32_t>(), nullptr,
+                             ws.ptr(), ws.bytes, (lkv_stream_t)stream()),
+          "freeze_budgets");
+    ws.status("freeze_budgets");
+    auto b = download<int32_t>(budgets, n);
+    return std::vector<int>(b.begin(), b.end());
+}
+
+std::vector<int> freeze_budgets(const BudgetTable& table, int t) { return freeze(table, t, LKV_BUDGET_FLOOR); }
+std::vector<int> freeze_budgets_exact(const BudgetTable& table, int t) { return freeze(table, t, LKV_BUDGET_EXACT); }
+
+// ---- policy.cpp:131-136 ------------------------------------------------------------------------------
+std::vector<double> token_scores(std::span<const double> keys, std::span<const double> values, int t, int d,
+                                 const Mlp2& scorer, Activation act, Precision prec) {
+    if (t < 1 || d < 1 || keys.size() != (size_t)t * d) throw contract_error("token_scores: keys must be [t x d]");
+    const bool kv = scorer.in == 2 * d;
+    if (kv && values.size() != keys.size())
+        throw contract_error("token_scores: keys/values must be rank-2 with equal first extents");
+    check_mlp(scorer, kv ? 2 * d : d);
+    for (double x : keys)
+        if (!std::isfinite(x)) throw numeric_error("matmul: non-finite input");
+    for (double x : values)
+        if (!std::isfinite(x)) throw numeric_error("matmul: non-finite input");
+    Dev K = upload_elems(keys, prec);
+    Dev V = kv ? upload_elems(values, prec) : upload_elems(keys, prec);
+    auto w1t = transpose_w1(scorer);
+    Dev W1 = upload_elems(w1t, prec);
+    auto b1 = to_f32(scorer.b1), w2 = to_f32(scorer.w2);
+    Dev B1 = upload(b1.data(), b1.size()), W2 = upload(w2.data(), w2.size());
+    Dev S(sizeof(float) * (size_t)t);
+    const int32_t len = t;
+    lkv_cache_desc c{1, 1, 1, d, t, dtype_of(prec), 0, K.p, V.p, &len};
+    lkv_scorer_desc s{kv ? LKV_SCORER_KV : LKV_SCORER_K,
+                      act == Activation::silu ? LKV_ACT_SILU : LKV_ACT_GELU_ERF,
+                      scorer.hidden,
+                      1,
+                      0,
+                      0,
+                      W1.p,
+                      B1.as<float>(),
+                      W2.as<float>()};
+    check(lkv_score(&c, &s, S.as<float>(), nullptr, 0, (lkv_stream_t)stream()), "token_scores");
+    auto f = download<float>(S, t);
+    return std::vector<double>(f.begin(), f.end());
+}
+
+// ---- soft_topk.cpp:191-201 / policy.cpp:152-154 ------------------------------------------------------
+std::vector<int> hard_topk(std::span<const float> u, int b) {
+    const int n = (int)u.size();
+    if (b < 0 || b > n) throw budget_error("hard_topk: b outside [0, n]");
+    std::vector<int> mask((size_t)n, 0);
+    if (n == 0) return mask;
+    Dev S = upload(u.data(), u.size());
+    const int32_t len = n, bb = b;
+    Dev Bd = upload(&bb, 1);
+    lkv_cache_desc c{1, 1, 1, 8, n, LKV_F32, 0, nullptr, nullptr, &len};
+    Dev offs(sizeof(int64_t) * 2), lens(sizeof(int32_t)), pos(sizeof(int32_t) * (size_t)(b > 0 ? b : 1));
+    check(lkv_ragged_offsets(Bd.as<int32_t>(), 1, 0, offs.as<int64_t>(), (lkv_stream_t)stream()), "hard_topk");
+    lkv_ragged_desc r{1, 8, LKV_F32, 0, b, offs.as<int64_t>(), lens.as<int32_t>(), nullptr, nullptr, pos.as<int32_t>()};
+    Workspace ws(lkv_workspace_bytes(&c, 1));
+    check(lkv_select(&c, S.as<float>(), Bd.as<int32_t>(), &r, 0, ws.ptr(), ws.bytes, (lkv_stream_t)stream()),
+          "hard_topk");
+    ws.status("hard_topk");
+    for (int32_t p : download<int32_t>(pos, (size_t)b)) mask[(size_t)p] = 1;
+    return mask;
+}
+
+std::vector<int> inference_select(std::span<const float> u, int b) { return hard_topk(u, b); }
+
+// ---- shared upload of a dense trace ----------------------------------------------------------------------
+namespace {
+struct DenseUpload {
+    Dev K, V;
+    int32_t len;
+    lkv_cache_desc desc;
+};
+
+DenseUpload upload_trace(const KvTrace& tr, Precision prec) {
+    const int heads = tr.n_layers * tr.n_kv_heads;
+    if (tr.t < 1 || tr.head_dim < 1 || (int)tr.keys.size() != heads || (int)tr.values.size() != heads)
+        throw contract_error("trace head count mismatch");
+    std::vector<double> k((size_t)heads * tr.t * tr.head_dim), v(k.size());
+    for (int h = 0; h < heads; ++h) {
+        if (tr.keys[(size_t)h].size() != (size_t)tr.t * tr.head_dim || tr.values[(size_t)h].size() != (size_t)tr.t * tr.head_dim)
+            throw contract_error("trace head must be [t x head_dim]");
+        std::memcpy(k.data() + (size_t)h * tr.t * tr.head_dim, tr.keys[(size_t)h].data(), sizeof(double) * tr.t * tr.head_dim);
+        std::memcpy(v.data() + (size_t)h * tr.t * tr.head_dim, tr.values[(size_t)h].data(), sizeof(double) * tr.t * tr.head_dim);
+    }
+    DenseUpload u{upload_elems(k, prec), upload_elems(v, prec), tr.t, {}};
+    u.desc = lkv_cache_desc{1, tr.n_layers, tr.n_kv_heads, tr.head_dim, tr.t, dtype_of(prec), 0, u.K.p, u.V.p, &u.len};
+    return u;
+}
+
+KvCache download_ragged(const KvTrace& tr, const Dev& offs, const Dev& lens, const Dev& rk, const Dev& rv,
+                        const Dev& rp, Precision prec) {
+    const int heads = tr.n_layers * tr.n_kv_heads;
+    auto o = download<int64_t>(offs, (size_t)heads + 1);
+    auto l = download<int32_t>(lens, (size_t)heads);
+    KvCache cache;
+    cache.n_layers = tr.n_layers;
+    cache.n_kv_heads = tr.n_kv_heads;
+    cache.head_dim = tr.head_dim;
+    cache.tokens_seen = tr.t;
+    cache.heads.resize((size_t)heads);
+    for (int h = 0; h < heads; ++h) {
+        HeadCache& hc = cache.heads[(size_t)h];
+        const size_t rows = (size_t)l[(size_t)h];
+        hc.keys = download_elems(rk, rows * tr.head_dim, (size_t)o[(size_t)h] * tr.head_dim, prec);
+        hc.values = download_elems(rv, rows * tr.head_dim, (size_t)o[(size_t)h] * tr.head_dim, prec);
+        auto p = download<int32_t>(rp, rows, (size_t)o[(size_t)h]);
+        hc.retained_positions.assign(p.begin(), p.end());
+    }
+    return cache;
+}
+
+size_t esize(Precision p) { return p == Precision::bf16 ? 2 : 4; }
+}  // namespace
+
+// ---- model.cpp:289-315 ----------------------------------------------------------------------------------
+KvCache cache_from_trace(const KvTrace& tr, const std::vector<std::vector<int>>& hard_masks, Precision prec) {
+    const int heads = tr.n_layers * tr.n_kv_heads;
+    if ((int)hard_masks.size() != heads) throw contract_error("cache_from_trace: one mask per head required");
+    DenseUpload du = upload_trace(tr, prec);
+    std::vector<int32_t> counts((size_t)heads), positions;
+    for (int h = 0; h < heads; ++h) {
+        const auto& m = hard_masks[(size_t)h];
+        if ((int)m.size() != tr.t) throw contract_error("cache_from_trace: mask length mismatch");
+        for (int j = 0; j < tr.t; ++j)
+            if (m[(size_t)j]) {
+                positions.push_back(j);
+                ++counts[(size_t)h];
+            }
+    }
+    const int64_t rows = (int64_t)positions.size();
+    Dev B = upload(counts.data(), counts.size());
+    Dev offs(sizeof(int64_t) * ((size_t)heads + 1));
+    check(lkv_ragged_offsets(B.as<int32_t>(), heads, 0, offs.as<int64_t>(), (lkv_stream_t)stream()), "cache_from_trace");
+    Dev lens = upload(counts.data(), counts.size());
+    Dev rp = upload(positions.data(), positions.size() ? positions.size() : 1);
+    Dev rk(esize(prec) * (size_t)(rows ? rows : 1) * tr.head_dim), rv(esize(prec) * (size_t)(rows ? rows : 1) * tr.head_dim);
+    lkv_ragged_desc r{heads, tr.head_dim, dtype_of(prec), 0, rows, offs.as<int64_t>(), lens.as<int32_t>(), rk.p, rv.p,
+                      rp.as<int32_t>()};
+    check(lkv_compact(&du.desc, &r, (lkv_stream_t)stream()), "cache_from_trace");
+    return download_ragged(tr, offs, lens, rk, rv, rp, prec);
+}
+
+// ---- evictsim.cpp:95-238 (K/V-given form) ----------------------------------------------------------------
+std::pair<KvCache, SimReport> prefill_with_eviction(const KvTrace& tr, const std::vector<int>& budgets,
+                                                    const std::vector<Mlp2>& scorers, Activation act,
+                                                    Precision prec) {
+    const int heads = tr.n_layers * tr.n_kv_heads;
+    if ((int)budgets.size() != heads) throw contract_error("prefill_with_eviction: one budget per head required");
+    for (int b : budgets)
+        if (b < 0 || b > tr.t) throw budget_error("prefill_with_eviction: budget outside [0, t]");
+    const bool per_head = (int)scorers.size() == heads;
+    if (!per_head && (int)scorers.size() != tr.n_layers)
+        throw contract_error("prefill_with_eviction: one scorer per (layer, head) or per layer required");
+    const int hidden = scorers.front().hidden;
+    const int in = scorers.front().in;
+    if (in != tr.head_dim && in != 2 * tr.head_dim) throw contract_error("scorer input must be d or 2d");
+    std::vector<double> w1t, b1, w2;
+    for (const Mlp2& m : scorers) {
+        check_mlp(m, in);
+        if (m.hidden != hidden) throw contract_error("all scorers must share one hidden width");
+        auto t = transpose_w1(m);
+        w1t.insert(w1t.end(), t.begin(), t.end());
+        b1.insert(b1.end(), m.b1.begin(), m.b1.end());
+        w2.insert(w2.end(), m.w2.begin(), m.w2.end());
+    }
+    DenseUpload du = upload_trace(tr, prec);
+    Dev W1 = upload_elems(w1t, prec);
+    auto b1f = to_f32(b1), w2f = to_f32(w2);
+    Dev B1 = upload(b1f.data(), b1f.size()), W2 = upload(w2f.data(), w2f.size());
+    lkv_scorer_desc sd{in == tr.head_dim ? LKV_SCORER_K : LKV_SCORER_KV,
+                       act == Activation::silu ? LKV_ACT_SILU : LKV_ACT_GELU_ERF,
+                       hidden,
+                       (int)scorers.size(),
+                       per_head ? tr.n_kv_heads : 1,
+                       per_head ? 1 : 0,
+                       W1.p,
+                       B1.as<float>(),
+                       W2.as<float>()};
+    std::vector<int32_t> b32(budgets.begin(), budgets.end());
+    int64_t rows = 0;
+    for (int b : budgets) rows += b;
+    Dev Bd = upload(b32.data(), b32.size());
+    Dev offs(sizeof(int64_t) * ((size_t)heads + 1)), lens(sizeof(int32_t) * heads);
+    Dev rk(esize(prec) * (size_t)(rows ? rows : 1) * tr.head_dim), rv(esize(prec) * (size_t)(rows ? rows : 1) * tr.head_dim);
+    Dev rp(sizeof(int32_t) * (size_t)(rows ? rows : 1));
+    Dev S(sizeof(float) * (size_t)heads * tr.t);
+    lkv_ragged_desc r{heads, tr.head_dim, dtype_of(prec), 0, rows, offs.as<int64_t>(), lens.as<int32_t>(), rk.p, rv.p,
+                      rp.as<int32_t>()};
+    Workspace ws(lkv_workspace_bytes(&du.desc, heads));
+    cudaEvent_t e0, e1;
+    cuda(cudaEventCreate(&e0), "event");
+    cuda(cudaEventCreate(&e1), "event");
+    cuda(cudaEventRecord(e0, stream()), "event");
+    check(lkv_ragged_offsets(Bd.as<int32_t>(), heads, 0, offs.as<int64_t>(), (lkv_stream_t)stream()), "prefill");
+    check(lkv_score(&du.desc, &sd, S.as<float>(), nullptr, 0, (lkv_stream_t)stream()), "prefill score");
+    check(lkv_select(&du.desc, S.as<float>(), Bd.as<int32_t>(), &r, 1, ws.ptr(), ws.bytes, (lkv_stream_t)stream()),
+          "prefill select");
+    cuda(cudaEventRecord(e1, stream()), "event");
+    ws.status("prefill_with_eviction");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    std::pair<KvCache, SimReport> out{download_ragged(tr, offs, lens, rk, rv, rp, prec), SimReport{}};
+    SimReport& rep = out.second;
+    rep.retained_per_head.resize((size_t)heads);
+    for (int h = 0; h < heads; ++h) rep.retained_per_head[(size_t)h] = out.first.heads[(size_t)h].retained();
+    rep.evict_device_seconds = ms * 1e-3;
+    rep.scoring_ops = (int64_t)heads * tr.t * ((int64_t)in * hidden + 3 * hidden);  // evictsim.cpp:172
+    MemoryModel mm;
+    mm.n_layers = tr.n_layers;
+    mm.n_kv_heads = tr.n_kv_heads;
+    mm.head_dim = tr.head_dim;
+    mm.bytes_per_element = 8.0;  // fp64 host storage, as evictsim.cpp:231
+    mm.tokens = tr.t;
+    const MemoryReport mr = kv_memory_bytes(mm, budgets);
+    rep.kv_bytes_full = mr.full_bytes;
+    rep.kv_bytes_compressed = mr.compressed_bytes;
+    rep.reduction = mr.reduction_factor;
+    return out;
+}
+
+// ---- model.cpp:240-265 ------------------------------------------------------------------------------------
+std::vector<double> decode_attention(KvCache& cache, std::span<const double> q, int n_q_heads,
+                                     std::span<const double> k_new, std::span<const double> v_new, Precision prec) {
+    const int L = cache.n_layers, H = cache.n_kv_heads, d = cache.head_dim;
+    if (L < 1 || H < 1 || d < 1 || (int)cache.heads.size() != L * H) throw contract_error("decode_step: cache head count mismatch");
+    if (n_q_heads < H || n_q_heads % H) throw contract_error("decode_step: n_q_heads must be a multiple of n_kv_heads");
+    if (q.size() != (size_t)L * n_q_heads * d || k_new.size() != (size_t)L * H * d || v_new.size() != k_new.size())
+        throw contract_error("decode_step: q [L][Hq][d], k/v [L][H][d] required");
+    const int heads = L * H;
+    std::vector<int32_t> lens((size_t)heads), pos;
+    std::vector<double> k, v;
+    std::vector<int64_t> offs((size_t)heads + 1, 0);
+    for (int h = 0; h < heads; ++h) {
+        const HeadCache& hc = cache.heads[(size_t)h];
+        lens[(size_t)h] = hc.retained();
+        offs[(size_t)h + 1] = offs[(size_t)h] + hc.retained() + 1;  // one row of decode slack
+        k.insert(k.end(), hc.keys.begin(), hc.keys.end());
+        v.insert(v.end(), hc.values.begin(), hc.values.end());
+        k.insert(k.end(), (size_t)d, 0.0);
+        v.insert(v.end(), (size_t)d, 0.0);
+        pos.insert(pos.end(), hc.retained_positions.begin(), hc.retained_positions.end());
+        pos.push_back(-1);
+    }
+    const int64_t rows = offs.back();
+    Dev K = upload_elems(k, prec), V = upload_elems(v, prec);
+    Dev P = upload(pos.data(), pos.size()), Ld = upload(lens.data(), lens.size()), O = upload(offs.data(), offs.size());
+    Dev Q = upload_elems(q, prec), NK = upload_elems(k_new, prec), NV = upload_elems(v_new, prec);
+    const int32_t seen = cache.tokens_seen;
+    Dev TS = upload(&seen, 1);
+    Dev OUT(esize(prec) * q.size());
+    lkv_ragged_desc r{heads, d, dtype_of(prec), 1, rows, O.as<int64_t>(), Ld.as<int32_t>(), K.p, V.p, P.as<int32_t>()};
+    Workspace ws(lkv_decode_workspace_bytes(&r, n_q_heads / H));
+    check(lkv_decode_plan(&r, ws.ptr(), ws.bytes, (lkv_stream_t)stream()), "decode plan");
+    check(lkv_decode_step(&r, 1, L, H, n_q_heads, Q.p, NK.p, NV.p, TS.as<int32_t>(), OUT.p, 1.0 / std::sqrt((double)d),
+                          ws.ptr(), ws.bytes, (lkv_stream_t)stream()),
+          "decode_step");
+    ws.status("decode_step");
+    auto out = download_elems(OUT, q.size(), 0, prec);
+    // the reference appends the new k, v and position to every head (model.cpp:240-248)
+    for (int h = 0; h < heads; ++h) {
+        HeadCache& hc = cache.heads[(size_t)h];
+        hc.keys.insert(hc.keys.end(), k_new.begin() + (size_t)h * d, k_new.begin() + (size_t)(h + 1) * d);
+        hc.values.insert(hc.values.end(), v_new.begin() + (size_t)h * d, v_new.begin() + (size_t)(h + 1) * d);
+        hc.retained_positions.push_back(cache.tokens_seen);
+    }
+    cache.tokens_seen += 1;
+    return out;
+}
+
+// ---- evictsim.cpp:56-81 (accounting) ------------------------------------------------------------------------
+MemoryReport kv_memory_bytes(const MemoryModel& m, double retention) {
+    if (m.n_layers < 1 || m.n_kv_heads < 1 || m.head_dim < 1 || m.tokens < 1 || !(m.bytes_per_element > 0.0))
+        throw contract_error("memory model: all extents must be positive");
+    if (!(retention > 0.0) || retention > 1.0) throw budget_error("kv_memory_bytes: retention must lie in (0, 1]");
+    MemoryReport r;
+    r.full_bytes = (double)m.n_layers * m.n_kv_heads * m.head_dim * 2.0 * m.bytes_per_element * (double)m.tokens;
+    r.compressed_bytes = retention * r.full_bytes;
+    r.reduction_factor = r.full_bytes / r.compressed_bytes;
+    return r;
+}
+
+MemoryReport kv_memory_bytes(const MemoryModel& m, const std::vector<int>& per_head_budgets) {
+    if (m.n_layers < 1 || m.n_kv_heads < 1 || m.head_dim < 1 || m.tokens < 1 || !(m.bytes_per_element > 0.0))
+        throw contract_error("memory model: all extents must be positive");
+    if ((int)per_head_budgets.size() != m.n_layers * m.n_kv_heads)
+        throw contract_error("kv_memory_bytes: one budget per head required");
+    MemoryReport r;
+    r.full_bytes = (double)m.n_layers * m.n_kv_heads * m.head_dim * 2.0 * m.bytes_per_element * (double)m.tokens;
+    double kept = 0.0;
+    for (int b : per_head_budgets) kept += (double)b;
+    r.compressed_bytes = kept * m.head_dim * 2.0 * m.bytes_per_element;
+    r.reduction_factor = r.compressed_bytes > 0.0 ? r.full_bytes / r.compressed_bytes
+                                                  : std::numeric_limits<double>::infinity();
+    return r;
+}
+
+}  // namespace lkv::b200
