@@ -449,19 +449,37 @@ __global__ void __launch_bounds__(kCombThreads) decode_combine_kernel(const __gr
         const float* pm = p.part_m + (size_t)base * G;
         const float* pl = p.part_l + (size_t)base * G;
         const float* po = p.part_o + (size_t)base * G * D;
-        if (threadIdx.x < G) {
-            const int g = threadIdx.x;
-            float M = -INFINITY;
-            for (int c = 0; c < nch; ++c) M = fmaxf(M, pm[c * G + g]);
-            float L = 0.f;
-            for (int c = 0; c < nch; ++c) L += pl[c * G + g] * exp2f(pm[c * G + g] - M);
-            s_M[g] = M;
-            s_L[g] = L;
+        // phase 1: all (chunk, g) maxima and sums in parallel -> shared memory
+        float* s_m = s_w;                       // [nch * G] (reused for the weights below)
+        __shared__ float s_l[kCombMaxChunks / 4];
+        const bool l_in_smem = nch * G <= kCombMaxChunks / 4;
+        for (int i = threadIdx.x; i < nch * G; i += kCombThreads) {
+            s_m[i] = pm[i];
+            if (l_in_smem) s_l[i] = pl[i];
+        }
+        __syncthreads();
+        {
+            const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+            for (int g = warp; g < G; g += kCombThreads / 32) {  // one warp per query head
+                float M = -INFINITY;
+                for (int c = lane; c < nch; c += 32) M = fmaxf(M, s_m[c * G + g]);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+                float L = 0.f;
+                for (int c = lane; c < nch; c += 32)
+                    L += (l_in_smem ? s_l[c * G + g] : pl[c * G + g]) * exp2f(s_m[c * G + g] - M);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+                if (lane == 0) {
+                    s_M[g] = M;
+                    s_L[g] = L;
+                }
+            }
         }
         __syncthreads();
         for (int i = threadIdx.x; i < nch * G; i += kCombThreads) {
             const int g = i % G;
-            s_w[i] = exp2f(pm[i] - s_M[g]) / s_L[g];
+            s_w[i] = exp2f(s_m[i] - s_M[g]) / s_L[g];
         }
         __syncthreads();
         const int sl = head / p.n_kv_heads, kvh = head - sl * p.n_kv_heads;

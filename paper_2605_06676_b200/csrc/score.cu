@@ -64,6 +64,22 @@ struct EpiAct<LKV_ACT_SILU> {
 };
 __device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
+template <int C>
+__device__ __forceinline__ void tmem_ld_x(uint32_t taddr, uint32_t (&r)[C]);
+template <>
+__device__ __forceinline__ void tmem_ld_x<32>(uint32_t taddr, uint32_t (&r)[32]) {
+    tmem_ld_32x32b_x32(taddr, r);
+}
+template <>
+__device__ __forceinline__ void tmem_ld_x<16>(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+
 struct TileInfo {
     int head;      // flat head
     int row0;      // first row inside the head
@@ -92,8 +108,15 @@ __device__ __forceinline__ TileInfo decode_tile(const ScoreParams& p, int tile, 
 // ============================================================================
 // tcgen05 kernel
 // ============================================================================
-constexpr int kTcRows = 128;     // UMMA M
-constexpr int kTcThreads = 384;  // 12 warps: TMA, MMA, TMEM alloc, spare, 2 x 4 epilogue
+constexpr int kTcRows = 128;  // UMMA M
+#ifndef LKV_SCORE_EPI
+#define LKV_SCORE_EPI 4
+#endif
+// Epilogue groups of 4 warps (one TMEM lane quarter each); group g drains accumulator
+// stage g, i.e. every E-th tile.  Warps 0..3: TMA producer, MMA issuer, TMEM allocator, spare.
+constexpr int kEpi = LKV_SCORE_EPI;
+constexpr int kTcThreads = 128 + 128 * kEpi;
+constexpr int kEpiChunk = kEpi > 2 ? 16 : 32;  // TMEM columns per tcgen05.ld (register budget)
 
 template <int N, int NBOX>
 struct TcCfg {
@@ -102,8 +125,10 @@ struct TcCfg {
     static constexpr int kWBox = N * 128;
     static constexpr int kW = NBOX * kWBox;
     static constexpr int kStages = (NBOX == 2) ? 5 : 2;
-    static constexpr int kTmemCols = (2 * N <= 32) ? 32 : (2 * N <= 64) ? 64 : (2 * N <= 128) ? 128 : (2 * N <= 256) ? 256 : 512;
-    static constexpr int kSmem = kStages * kAStage + kW + 256 + 4 * N * 4 + 1024;  // + barriers, b1/w2, align
+    static constexpr int kAcc = kEpi * N;  // accumulator columns: one N-wide stage per epilogue group
+    static constexpr int kTmemCols = (kAcc <= 32) ? 32 : (kAcc <= 64) ? 64 : (kAcc <= 128) ? 128 : (kAcc <= 256) ? 256 : 512;
+    static_assert(kAcc <= 512, "TMEM holds 512 fp32 columns");
+    static constexpr int kSmem = kStages * kAStage + kW + 256 + 2 * kEpi * N * 4 + 1024;  // + barriers, b1/w2, align
 };
 
 template <int N, int NBOX, int ACT>
@@ -120,12 +145,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     uint64_t* bars = reinterpret_cast<uint64_t*>(sW + Cfg::kW);
     uint64_t* full = bars;              // [S]
     uint64_t* empty = bars + S;         // [S]
-    uint64_t* tfull = bars + 2 * S;     // [2]
-    uint64_t* tempty = bars + 2 * S + 2;  // [2]
-    uint64_t* wfull = bars + 2 * S + 4;
-    uint64_t* wempty = bars + 2 * S + 5;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 6);
-    float* sEpi = reinterpret_cast<float*>(sW + Cfg::kW + 256);  // [2 groups][b1 | w2][N]
+    uint64_t* tfull = bars + 2 * S;           // [kEpi]
+    uint64_t* tempty = bars + 2 * S + kEpi;   // [kEpi]
+    uint64_t* wfull = bars + 2 * S + 2 * kEpi;
+    uint64_t* wempty = wfull + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wempty + 1);
+    float* sEpi = reinterpret_cast<float*>(sW + Cfg::kW + 256);  // [kEpi groups][b1 | w2][N]
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -139,7 +164,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], 1);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kEpi; ++i) {
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 4);
         }
@@ -204,8 +229,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     cur = ti.scorer;
                     ++wuses;
                 }
-                const int acc = i & 1;
-                mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
+                const int acc = i % kEpi;
+                mbar_wait(&tempty[acc], ((i / kEpi) & 1) ^ 1);
                 const int st = i % S;
                 mbar_wait(&full[st], (i / S) & 1);
                 tc_fence_after();
@@ -229,7 +254,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         float* s_b1 = sEpi + grp * 2 * N;  // this group's copy of b1 and the pre-scaled w2
         float* s_w2 = s_b1 + N;
         int cur = -1;
-        for (int tile = t_begin + grp, i = grp; tile < t_end; tile += 2, i += 2) {
+        for (int tile = t_begin + grp, i = grp; tile < t_end; tile += kEpi, i += kEpi) {
             const TileInfo ti = decode_tile(p, tile, kTcRows);
             if (ti.scorer != cur) {  // stage this scorer's b1 / w2 once (group-local barrier)
                 named_bar_sync(1 + grp, 128);
@@ -241,24 +266,24 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 named_bar_sync(1 + grp, 128);
                 cur = ti.scorer;
             }
-            mbar_wait(&tfull[grp], (i >> 1) & 1);
+            mbar_wait(&tfull[grp], (i / kEpi) & 1);
             tc_fence_after();
             const uint32_t taddr = tmem_base + (uint32_t(quarter * 32) << 16) + grp * N;
             float s = 0.f;
 #pragma unroll
-            for (int c = 0; c < N / 32; ++c) {
-                uint32_t r[32];
-                tmem_ld_32x32b_x32(taddr + c * 32, r);
+            for (int c = 0; c < N / kEpiChunk; ++c) {
+                uint32_t r[kEpiChunk];
+                tmem_ld_x<kEpiChunk>(taddr + c * kEpiChunk, r);
                 tmem_ld_wait();
-                if (c == N / 32 - 1) {
+                if (c == N / kEpiChunk - 1) {
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tempty[grp]);
                 }
 #pragma unroll
-                for (int q = 0; q < 32; q += 4) {
-                    const float4 bb = *reinterpret_cast<const float4*>(s_b1 + c * 32 + q);
-                    const float4 ww = *reinterpret_cast<const float4*>(s_w2 + c * 32 + q);
+                for (int q = 0; q < kEpiChunk; q += 4) {
+                    const float4 bb = *reinterpret_cast<const float4*>(s_b1 + c * kEpiChunk + q);
+                    const float4 ww = *reinterpret_cast<const float4*>(s_w2 + c * kEpiChunk + q);
                     s = fmaf(EpiAct<ACT>::f(__uint_as_float(r[q + 0]) + bb.x), ww.x, s);
                     s = fmaf(EpiAct<ACT>::f(__uint_as_float(r[q + 1]) + bb.y), ww.y, s);
                     s = fmaf(EpiAct<ACT>::f(__uint_as_float(r[q + 2]) + bb.z), ww.z, s);
