@@ -23,9 +23,9 @@ __device__ __forceinline__ float act_f32(int act, float h) {
 }
 
 // Epilogue activations on the MUFU path (approximations far inside the 1e-2 bf16 bar):
-//  GELU-erf: gelu(h) = h * Phi(h) = 0.5 (h + |h| erf(|h|/sqrt2)), erf by Abramowitz-Stegun 7.1.26
-//            (|error| <= 1.5e-7): erf(u) = 1 - t (a1 + t (a2 + t (a3 + t (a4 + t a5)))) e^{-u^2},
-//            t = 1 / (1 + p u); one rcp + one ex2.  f() returns 2*gelu; w2 is pre-scaled by 0.5.
+//  GELU-erf: gelu(h) = h * Phi(h) = 0.5 (h + |h| erf(|h|/sqrt2)); erf by Abramowitz-Stegun
+//            7.1.28 (one rcp, default) or 7.1.26 (rcp + ex2).  f() returns 2*gelu; w2 is
+//            pre-scaled by 0.5.
 //  SiLU:     h / (1 + e^{-h}) (tensor.cpp:371-378) with ex2 + rcp.
 __device__ __forceinline__ float rcp_approx(float x) {
     float y;
@@ -39,9 +39,13 @@ __device__ __forceinline__ float ex2_approx(float x) {
 }
 template <int ACT>
 struct EpiAct;
+#ifndef LKV_GELU_AS
+#define LKV_GELU_AS 28
+#endif
 template <>
 struct EpiAct<LKV_ACT_GELU_ERF> {
     static constexpr float kW2Scale = 0.5f;
+#if LKV_GELU_AS == 26
     __device__ __forceinline__ static float f(float h) {
         const float ah = fabsf(h);
         const float t = rcp_approx(fmaf(0.3275911f * 0.70710678118654752f, ah, 1.0f));
@@ -54,6 +58,25 @@ struct EpiAct<LKV_ACT_GELU_ERF> {
         const float erf_abs = fmaf(-p, e, 1.0f);
         return fmaf(ah, erf_abs, h);
     }
+#else
+    // Abramowitz-Stegun 7.1.28: erf(u) = 1 - (1 + a1 u + ... + a6 u^6)^-16, |error| <= 3e-7
+    // (1.7e-6 in fp32); u = |h|/sqrt2 folded into the coefficients.  One MUFU (rcp).
+    __device__ __forceinline__ static float f(float h) {
+        const float ah = fabsf(h);
+        float y = fmaf(5.382975000e-06f, ah, 4.889063564e-05f);
+        y = fmaf(y, ah, 3.800357500e-05f);
+        y = fmaf(y, ah, 3.277626324e-03f);
+        y = fmaf(y, ah, 2.114100615e-02f);
+        y = fmaf(y, ah, 4.986734697e-02f);
+        y = fmaf(y, ah, 1.0f);
+        y *= y;
+        y *= y;
+        y *= y;
+        y *= y;  // y^16 (inf for large |h| -> r = 0 -> erf = 1)
+        const float r = rcp_approx(y);
+        return fmaf(-ah, r, h + ah);  // 2 gelu(h) = h + |h| erf(|h|/sqrt2)
+    }
+#endif
 };
 template <>
 struct EpiAct<LKV_ACT_SILU> {
