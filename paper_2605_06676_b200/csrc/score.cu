@@ -85,6 +85,41 @@ struct EpiAct<LKV_ACT_SILU> {
         return h * rcp_approx(1.0f + ex2_approx(h * -1.4426950408889634f));
     }
 };
+// Packed-pair forms (sm_100 FFMA2/FMUL2/FADD2): the epilogue is issue-bound, so two
+// accumulator columns go through every FP32 instruction at once; MUFU stays scalar.
+__device__ __forceinline__ float2 f2(float x, float y) { return make_float2(x, y); }
+__device__ __forceinline__ float2 abs2(float2 v) { return make_float2(fabsf(v.x), fabsf(v.y)); }
+template <int ACT>
+struct EpiAct2;
+template <>
+struct EpiAct2<LKV_ACT_GELU_ERF> {  // 2 gelu(h), A&S 7.1.28 (see EpiAct)
+    static constexpr float kW2Scale = 0.5f;
+    __device__ __forceinline__ static float2 f(float2 h) {
+        const float2 ah = abs2(h);
+        float2 y = __ffma2_rn(f2(5.382975000e-06f, 5.382975000e-06f), ah, f2(4.889063564e-05f, 4.889063564e-05f));
+        y = __ffma2_rn(y, ah, f2(3.800357500e-05f, 3.800357500e-05f));
+        y = __ffma2_rn(y, ah, f2(3.277626324e-03f, 3.277626324e-03f));
+        y = __ffma2_rn(y, ah, f2(2.114100615e-02f, 2.114100615e-02f));
+        y = __ffma2_rn(y, ah, f2(4.986734697e-02f, 4.986734697e-02f));
+        y = __ffma2_rn(y, ah, f2(1.0f, 1.0f));
+        y = __fmul2_rn(y, y);
+        y = __fmul2_rn(y, y);
+        y = __fmul2_rn(y, y);
+        y = __fmul2_rn(y, y);
+        const float2 r = f2(rcp_approx(y.x), rcp_approx(y.y));
+        return __ffma2_rn(f2(-ah.x, -ah.y), r, __fadd2_rn(h, ah));
+    }
+};
+template <>
+struct EpiAct2<LKV_ACT_SILU> {  // h / (1 + e^-h)
+    static constexpr float kW2Scale = 1.0f;
+    __device__ __forceinline__ static float2 f(float2 h) {
+        const float2 z = __fmul2_rn(h, f2(-1.4426950408889634f, -1.4426950408889634f));
+        const float2 d = __fadd2_rn(f2(ex2_approx(z.x), ex2_approx(z.y)), f2(1.0f, 1.0f));
+        return __fmul2_rn(h, f2(rcp_approx(d.x), rcp_approx(d.y)));
+    }
+};
+
 __device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
 template <int C>
@@ -284,7 +319,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 const int j = threadIdx.x & 127;
                 if (j < N) {
                     s_b1[j] = p.b1[(size_t)ti.scorer * N + j];
-                    s_w2[j] = p.w2[(size_t)ti.scorer * N + j] * EpiAct<ACT>::kW2Scale;
+                    s_w2[j] = p.w2[(size_t)ti.scorer * N + j] * EpiAct2<ACT>::kW2Scale;
                 }
                 named_bar_sync(1 + grp, 128);
                 cur = ti.scorer;
@@ -292,7 +327,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             mbar_wait(&tfull[grp], (i / kEpi) & 1);
             tc_fence_after();
             const uint32_t taddr = tmem_base + (uint32_t(quarter * 32) << 16) + grp * N;
-            float s = 0.f;
+            float2 s2 = f2(0.f, 0.f);
 #pragma unroll
             for (int c = 0; c < N / kEpiChunk; ++c) {
                 uint32_t r[kEpiChunk];
@@ -307,12 +342,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 for (int q = 0; q < kEpiChunk; q += 4) {
                     const float4 bb = *reinterpret_cast<const float4*>(s_b1 + c * kEpiChunk + q);
                     const float4 ww = *reinterpret_cast<const float4*>(s_w2 + c * kEpiChunk + q);
-                    s = fmaf(EpiAct<ACT>::f(__uint_as_float(r[q + 0]) + bb.x), ww.x, s);
-                    s = fmaf(EpiAct<ACT>::f(__uint_as_float(r[q + 1]) + bb.y), ww.y, s);
-                    s = fmaf(EpiAct<ACT>::f(__uint_as_float(r[q + 2]) + bb.z), ww.z, s);
-                    s = fmaf(EpiAct<ACT>::f(__uint_as_float(r[q + 3]) + bb.w), ww.w, s);
+                    const float2 h0 = __fadd2_rn(f2(__uint_as_float(r[q + 0]), __uint_as_float(r[q + 1])), f2(bb.x, bb.y));
+                    const float2 h1 = __fadd2_rn(f2(__uint_as_float(r[q + 2]), __uint_as_float(r[q + 3])), f2(bb.z, bb.w));
+                    s2 = __ffma2_rn(EpiAct2<ACT>::f(h0), f2(ww.x, ww.y), s2);
+                    s2 = __ffma2_rn(EpiAct2<ACT>::f(h1), f2(ww.z, ww.w), s2);
                 }
             }
+            const float s = s2.x + s2.y;
             const int row = ti.row0 + quarter * 32 + lane;
             if (row < ti.t) p.scores[(size_t)ti.head * p.seq.T + row] = s;
         }
