@@ -200,7 +200,9 @@ lkv_status check_ragged(const lkv_ragged_desc* r, int64_t n_heads, int head_dim,
 
 // ---- internal launchers shared by lkv_score / lkv_evict ---------------------------------------------
 lkv_status run_score(const lkv_cache_desc* c, const lkv_scorer_desc* s, float* scores, cudaStream_t stream,
-                     int sms_reserved = 0) {
+                     int sms_reserved = 0, uint32_t* hist = nullptr, ErrWord* err = nullptr,
+                     bool* hist_made = nullptr) {
+    if (hist_made) *hist_made = false;
     ScoreParams p;
     memset(&p, 0, sizeof p);
     p.seq = make_seq(c);
@@ -225,6 +227,12 @@ lkv_status run_score(const lkv_cache_desc* c, const lkv_scorer_desc* s, float* s
         st = make_map_bf16(&mw, s->w1t, (uint64_t)s->input * c->head_dim, (uint64_t)s->n_scorers * s->hidden,
                            (uint32_t)s->hidden);
         if (st) return st;
+        if (hist) {
+            LKV_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 2048 * (size_t)n_heads_of(c), stream), "hist clear");
+            p.hist = hist;
+            p.err = err;
+            if (hist_made) *hist_made = true;
+        }
         LKV_CUDA(launch_score_tc(p, mk, mv, mw, num_sms() - sms_reserved, stream), "score (tcgen05)");
     } else {
         const int in = s->input * c->head_dim;
@@ -236,7 +244,8 @@ lkv_status run_score(const lkv_cache_desc* c, const lkv_scorer_desc* s, float* s
 }
 
 lkv_status run_select(const lkv_cache_desc* c, const float* scores, const int32_t* budgets,
-                      const lkv_ragged_desc* out, void* ws, const EvictWs& w, bool gather, cudaStream_t stream) {
+                      const lkv_ragged_desc* out, void* ws, const EvictWs& w, bool gather, cudaStream_t stream,
+                      bool hist_ready = false) {
     for (int s = 0; s < c->n_seq; ++s)
         if (c->seq_lens[s] > 4096 * 1024) return fail(LKV_ERR_UNSUPPORTED, "top-k supports t <= 4M rows per head");
     SelectParams p;
@@ -259,6 +268,7 @@ lkv_status run_select(const lkv_cache_desc* c, const float* scores, const int32_
     p.out_values = out->values;
     p.row_bytes = c->head_dim * (c->dtype == LKV_F32 ? 4 : 2);
     p.gather = gather ? 1 : 0;
+    p.hist_ready = hist_ready ? 1 : 0;
     p.err = at<ErrWord>(ws, w.err);
     LKV_CUDA(launch_select(p, (int)n_heads_of(c), stream), "select");
     return LKV_OK;
@@ -508,9 +518,12 @@ lkv_status lkv_evict(const lkv_cache_desc* c, const lkv_scorer_desc* s, const do
                      ws_bytes, (lkv_stream_t)side);
     if (st) return st;
     LKV_CUDA(cudaEventRecord(join, side), "event record");
-    if ((st = run_score(c, s, scores, strm, /*sms_reserved=*/1))) return st;
+    bool hist_made = false;  // the tcgen05 scorer fuses top-k pass 1 (the histogram) into its epilogue
+    if ((st = run_score(c, s, scores, strm, /*sms_reserved=*/1, at<uint32_t>(ws, w.hist), at<ErrWord>(ws, w.err),
+                        &hist_made)))
+        return st;
     LKV_CUDA(cudaStreamWaitEvent(strm, join, 0), "stream wait");
-    return run_select(c, scores, budgets, out, ws, w, true, strm);
+    return run_select(c, scores, budgets, out, ws, w, true, strm, hist_made);
 }
 
 size_t lkv_decode_workspace_bytes(const lkv_ragged_desc* r, int32_t G) {

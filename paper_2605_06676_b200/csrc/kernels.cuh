@@ -35,6 +35,8 @@ struct ScoreParams {
     const float* b1;
     const float* w2;
     float* scores;
+    uint32_t* hist;  // nullable: fused top-11-bit histogram per head (tcgen05 path; zeroed by the caller)
+    ErrWord* err;
     int32_t tile_base[LKV_MAX_SEQ + 1];
 };
 cudaError_t launch_score_simt(ScoreParams p, int dtype, int num_sms, cudaStream_t stream);
@@ -65,6 +67,7 @@ struct SelectParams {
     void* out_values;
     int32_t row_bytes;
     int32_t gather;
+    int32_t hist_ready;  // the scorer already produced `hist` (fused pass 1)
     ErrWord* err;
     int32_t chunk_base[LKV_MAX_SEQ + 1];
 };

@@ -172,9 +172,7 @@ constexpr int kTcRows = 128;  // UMMA M
 #endif
 // Epilogue groups of 4 warps (one TMEM lane quarter each); group g drains accumulator
 // stage g, i.e. every E-th tile.  Warps 0..3: TMA producer, MMA issuer, TMEM allocator, spare.
-constexpr int kEpi = LKV_SCORE_EPI;
-constexpr int kTcThreads = 128 + 128 * kEpi;
-constexpr int kEpiChunk = kEpi > 2 ? 16 : 32;  // TMEM columns per tcgen05.ld (register budget)
+constexpr int kHistBins = 2048;  // top 11 key bits: the first radix digit of the top-k (select.cu)
 
 template <int N, int NBOX>
 struct TcCfg {
@@ -182,20 +180,27 @@ struct TcCfg {
     static constexpr int kAStage = NBOX * kABox;           // one tile (k or [k;v])
     static constexpr int kWBox = N * 128;
     static constexpr int kW = NBOX * kWBox;
-    static constexpr int kStages = (NBOX == 2) ? 5 : 2;
+    static constexpr int kStages = (NBOX == 2) ? (N <= 64 ? 5 : 4) : 2;
+    // [k;v] tiles (NBOX = 4) leave room for two epilogue groups only
+    static constexpr int kEpi = (NBOX == 2) ? LKV_SCORE_EPI : 2;
+    static constexpr int kThreads = 128 + 128 * kEpi;
+    static constexpr int kEpiChunk = kEpi > 2 ? 16 : 32;  // TMEM columns per tcgen05.ld (register budget)
     static constexpr int kAcc = kEpi * N;  // accumulator columns: one N-wide stage per epilogue group
     static constexpr int kTmemCols = (kAcc <= 32) ? 32 : (kAcc <= 64) ? 64 : (kAcc <= 128) ? 128 : (kAcc <= 256) ? 256 : 512;
     static_assert(kAcc <= 512, "TMEM holds 512 fp32 columns");
-    static constexpr int kSmem = kStages * kAStage + kW + 256 + 2 * kEpi * N * 4 + 1024;  // + barriers, b1/w2, align
+    static constexpr int kSmem = kStages * kAStage + kW + 256 + 2 * kEpi * N * 4 + kEpi * kHistBins * 4 + 1024;
+    static_assert(kSmem <= 227 * 1024, "shared memory budget");
 };
 
 template <int N, int NBOX, int ACT>
-__global__ void __launch_bounds__(kTcThreads, 1)
+__global__ void __launch_bounds__(TcCfg<N, NBOX>::kThreads, 1)
     score_tc_kernel(const __grid_constant__ ScoreParams p, const __grid_constant__ CUtensorMap tmap_k,
                     const __grid_constant__ CUtensorMap tmap_v, const __grid_constant__ CUtensorMap tmap_w,
                     int total_tiles) {
     using Cfg = TcCfg<N, NBOX>;
     constexpr int S = Cfg::kStages;
+    constexpr int kEpi = Cfg::kEpi;
+    constexpr int kEpiChunk = Cfg::kEpiChunk;
     extern __shared__ unsigned char smem_dyn[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
     unsigned char* sA = smem;
@@ -209,6 +214,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     uint64_t* wempty = wfull + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wempty + 1);
     float* sEpi = reinterpret_cast<float*>(sW + Cfg::kW + 256);  // [kEpi groups][b1 | w2][N]
+    uint32_t* sHist = reinterpret_cast<uint32_t*>(sEpi + 2 * kEpi * N);  // [kEpi groups][kHistBins]
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -311,9 +317,30 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const int quarter = warp & 3;  // TMEM lane quarter this warp may access
         float* s_b1 = sEpi + grp * 2 * N;  // this group's copy of b1 and the pre-scaled w2
         float* s_w2 = s_b1 + N;
-        int cur = -1;
+        uint32_t* hist_g = sHist + grp * kHistBins;  // this group's top-digit histogram (fused K3 pass 1)
+        const int j128 = threadIdx.x & 127;
+        if (p.hist) {
+            for (int b = j128; b < kHistBins; b += 128) hist_g[b] = 0;
+        }
+        auto flush_hist = [&](int head) {
+            named_bar_sync(1 + grp, 128);
+            for (int b = j128; b < kHistBins; b += 128) {
+                const uint32_t v = hist_g[b];
+                if (v) {
+                    atomicAdd(p.hist + (size_t)head * kHistBins + b, v);
+                    hist_g[b] = 0;
+                }
+            }
+            named_bar_sync(1 + grp, 128);
+        };
+        int cur = -1, cur_head = -1;
         for (int tile = t_begin + grp, i = grp; tile < t_end; tile += kEpi, i += kEpi) {
             const TileInfo ti = decode_tile(p, tile, kTcRows);
+            if (p.hist && ti.head != cur_head) {
+                if (cur_head >= 0) flush_hist(cur_head);
+                else named_bar_sync(1 + grp, 128);  // zeroing complete
+                cur_head = ti.head;
+            }
             if (ti.scorer != cur) {  // stage this scorer's b1 / w2 once (group-local barrier)
                 named_bar_sync(1 + grp, 128);
                 const int j = threadIdx.x & 127;
@@ -350,8 +377,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             }
             const float s = s2.x + s2.y;
             const int row = ti.row0 + quarter * 32 + lane;
-            if (row < ti.t) p.scores[(size_t)ti.head * p.seq.T + row] = s;
+            if (row < ti.t) {
+                p.scores[(size_t)ti.head * p.seq.T + row] = s;
+                if (p.hist) {
+                    if (f32_is_nan(s)) latch_error(p.err, LKV_ERR_NUMERIC, ti.head);
+                    atomicAdd(hist_g + (f32_key(s) >> 21), 1u);
+                }
+            }
         }
+        if (p.hist && cur_head >= 0) flush_hist(cur_head);
     }
 
     tc_fence_before();
@@ -482,7 +516,7 @@ static cudaError_t launch_tc_inst(const ScoreParams& p, const CUtensorMap& mk, c
     auto kern = score_tc_kernel<N, NBOX, ACT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
     if (e != cudaSuccess) return e;
-    kern<<<grid, kTcThreads, Cfg::kSmem, stream>>>(p, mk, mv, mw, tiles);
+    kern<<<grid, Cfg::kThreads, Cfg::kSmem, stream>>>(p, mk, mv, mw, tiles);
     note_launches(1);
     return cudaGetLastError();
 }

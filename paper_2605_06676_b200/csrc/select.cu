@@ -117,7 +117,10 @@ __global__ void __launch_bounds__(1024) select_resolve1_kernel(const __grid_cons
     const int t = head_len(p, head);
     const int b = p.budgets[head];
     HeadSel* st = p.state + head;
-    if (b < 0 || b > t) return;  // latched by S1
+    if (b < 0 || b > t) {  // budget outside [0, t] (hard_topk, soft_topk.cpp:193)
+        if (threadIdx.x == 0) latch_error(p.err, LKV_ERR_BUDGET, head);
+        return;
+    }
     if (b == 0 || b == t) {
         if (threadIdx.x == 0) {
             st->mode = b == 0 ? kModeNone : kModeAll;
@@ -138,8 +141,12 @@ __global__ void __launch_bounds__(1024) select_resolve1_kernel(const __grid_cons
 }
 
 // ---- S3 --------------------------------------------------------------------------
+// One pass over the chunk's scores (16 contiguous rows per thread, loads batched for
+// memory-level parallelism): rows above bin1 are counted, rows inside bin1 are appended
+// to the head's candidate list with one atomic per block.
 __global__ void __launch_bounds__(kSelThreads) select_collect_kernel(const __grid_constant__ SelectParams p) {
-    __shared__ uint32_t s_red[kSelThreads / 32];
+    __shared__ uint32_t s_scan[kSelThreads / 32 + 1];
+    __shared__ uint32_t s_base;
     const ChunkInfo ci = decode_chunk(p, blockIdx.x);
     HeadSel* st = p.state + ci.head;
     const int b = p.budgets[ci.head];
@@ -151,32 +158,30 @@ __global__ void __launch_bounds__(kSelThreads) select_collect_kernel(const __gri
     }
     const uint32_t bin1 = st->bin1;
     const float* sc = p.scores + (size_t)ci.head * p.seq.T + ci.c0;
-    uint32_t* cand = p.cands + (size_t)ci.head * p.seq.T;
-    uint32_t gt = 0;
-    const int lane = threadIdx.x & 31;
-    for (int i0 = 0; i0 < ci.n; i0 += kSelThreads) {
-        const int i = i0 + threadIdx.x;
-        uint32_t dig = 0;
-        const bool valid = i < ci.n;
-        if (valid) dig = f32_key(sc[i]) >> 21;
-        gt += (valid && dig > bin1);
-        const bool is_c = valid && dig == bin1;
-        const uint32_t m = __ballot_sync(0xffffffffu, is_c);
-        if (m) {
-            uint32_t base = 0;
-            if (lane == 0) base = atomicAdd(&st->n_cand, (uint32_t)__popc(m));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (is_c) cand[base + __popc(m & ((1u << lane) - 1))] = (uint32_t)(ci.c0 + i);
-        }
-    }
+    const int j0 = threadIdx.x * kPerThread;
+    uint32_t dig[kPerThread];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) gt += __shfl_xor_sync(0xffffffffu, gt, o);
-    if (lane == 0) s_red[threadIdx.x >> 5] = gt;
-    __syncthreads();
+    for (int q = 0; q < kPerThread; ++q) dig[q] = (j0 + q < ci.n) ? (f32_key(sc[j0 + q]) >> 21) : 0u;
+    uint32_t gt = 0, nc = 0;
+#pragma unroll
+    for (int q = 0; q < kPerThread; ++q) {
+        const bool valid = j0 + q < ci.n;
+        gt += valid && dig[q] > bin1;
+        nc += valid && dig[q] == bin1;
+    }
+    uint32_t tot_c, tot_gt;
+    uint32_t slot = block_exclusive_scan<kSelThreads>(nc, s_scan, &tot_c);
+    block_exclusive_scan<kSelThreads>(gt, s_scan, &tot_gt);
     if (threadIdx.x == 0) {
-        uint32_t s = 0;
-        for (int w = 0; w < kSelThreads / 32; ++w) s += s_red[w];
-        p.chunk_gt[blockIdx.x] = s;
+        p.chunk_gt[blockIdx.x] = tot_gt;
+        s_base = tot_c ? atomicAdd(&st->n_cand, tot_c) : 0u;
+    }
+    __syncthreads();
+    if (nc) {
+        uint32_t* cand = p.cands + (size_t)ci.head * p.seq.T + s_base;
+#pragma unroll
+        for (int q = 0; q < kPerThread; ++q)
+            if (j0 + q < ci.n && dig[q] == bin1) cand[slot++] = (uint32_t)(ci.c0 + j0 + q);
     }
 }
 
@@ -396,15 +401,18 @@ int select_total_chunks(SelectParams& p) {
 
 cudaError_t launch_select(SelectParams p, int n_heads, cudaStream_t stream) {
     const int chunks = select_total_chunks(p);
-    cudaError_t e = cudaMemsetAsync(p.hist, 0, sizeof(uint32_t) * 2048 * (size_t)n_heads, stream);
-    if (e != cudaSuccess) return e;
     if (chunks == 0) return cudaSuccess;
-    select_hist_kernel<<<chunks, kSelThreads, 0, stream>>>(p);
+    if (!p.hist_ready) {
+        cudaError_t e = cudaMemsetAsync(p.hist, 0, sizeof(uint32_t) * 2048 * (size_t)n_heads, stream);
+        if (e != cudaSuccess) return e;
+        select_hist_kernel<<<chunks, kSelThreads, 0, stream>>>(p);
+        note_launches(1);
+    }
     select_resolve1_kernel<<<n_heads, 1024, 0, stream>>>(p);
     select_collect_kernel<<<chunks, kSelThreads, 0, stream>>>(p);
     select_resolve2_kernel<<<n_heads, 1024, 0, stream>>>(p);
     select_emit_kernel<<<chunks, kSelThreads, 0, stream>>>(p);
-    note_launches(5);
+    note_launches(4);
     return cudaGetLastError();
 }
 
