@@ -484,25 +484,33 @@ __global__ void __launch_bounds__(kCombThreads) decode_combine_kernel(const __gr
         __syncthreads();
         const int sl = head / p.n_kv_heads, kvh = head - sl * p.n_kv_heads;
         T* out = static_cast<T*>(p.out) + ((size_t)sl * p.n_q_heads + kvh * G) * D;
-        for (int e = threadIdx.x; e < G * D; e += kCombThreads) {
+        // grid.y tiles the G*D outputs: one element per thread, all chunk loads in flight
+        const int e = blockIdx.y * kCombThreads + threadIdx.x;
+        if (e < G * D) {
             const int g = e / D;
             float acc = 0.f;
             int c = 0;
-            for (; c + 8 <= nch; c += 8) {
-                float v[8];
+            for (; c + 16 <= nch; c += 16) {
+                float v[16];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) v[k] = po[(size_t)(c + k) * G * D + e];
+                for (int k = 0; k < 16; ++k) v[k] = po[(size_t)(c + k) * G * D + e];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) acc = fmaf(v[k], s_w[(c + k) * G + g], acc);
+                for (int k = 0; k < 16; ++k) acc = fmaf(v[k], s_w[(c + k) * G + g], acc);
             }
-            for (; c < nch; ++c) acc = fmaf(po[(size_t)c * G * D + e], s_w[c * G + g], acc);
+            float v[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+                if (c + k < nch) v[k] = po[(size_t)(c + k) * G * D + e];
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+                if (c + k < nch) acc = fmaf(v[k], s_w[(c + k) * G + g], acc);
             if constexpr (sizeof(T) == 2) out[e] = __float2bfloat16_rn(acc);
             else out[e] = acc;
         }
-    } else if (nch * G > kCombMaxChunks && threadIdx.x == 0) {
+    } else if (nch * G > kCombMaxChunks && threadIdx.x == 0 && blockIdx.y == 0) {
         latch_error(p.err, LKV_ERR_UNSUPPORTED, head);
     }
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && blockIdx.y == 0) {
         p.lens[head] = len_new;
         if (head % p.heads_per_seq == 0) p.tokens_seen[head / p.heads_per_seq] += 1;
     }
@@ -530,7 +538,7 @@ cudaError_t launch_decode(const DecodeParams& p, int dtype, const CUtensorMap* m
         const int per_sm = (kDecPerSm == 2 && smem * 2 <= 220 * 1024) ? 2 : 1;
         const int grid = min(p.max_items, per_sm * num_sms);
         decode_attn_bf16_kernel<<<grid, kDecThreads, smem, stream>>>(p, *mk, *mv);
-        decode_combine_kernel<__nv_bfloat16><<<p.n_heads, kCombThreads, 0, stream>>>(p, 1);
+        decode_combine_kernel<__nv_bfloat16><<<dim3(p.n_heads, (p.G * p.head_dim + kCombThreads - 1) / kCombThreads), kCombThreads, 0, stream>>>(p, 1);
         note_launches(2);
     } else {
         const size_t smem = ((size_t)p.G * p.head_dim + (size_t)p.G * kDecCh) * sizeof(float);
@@ -539,7 +547,7 @@ cudaError_t launch_decode(const DecodeParams& p, int dtype, const CUtensorMap* m
         decode_attn_f32_kernel<<<p.max_items, kDecSimtThreads, smem, stream>>>(p);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
-        decode_combine_kernel<float><<<p.n_heads, kCombThreads, 0, stream>>>(p, 0);
+        decode_combine_kernel<float><<<dim3(p.n_heads, (p.G * p.head_dim + kCombThreads - 1) / kCombThreads), kCombThreads, 0, stream>>>(p, 0);
         note_launches(2);
     }
     return cudaGetLastError();
