@@ -124,7 +124,7 @@ def run_ours(args, rank, world, local_rank):
     logits = synth.make_logits(cfg, device=dev)
     n_seq, L, H, T, D = cache.shape
     rows_per_step = sum(cache.seq_lens) * L * H
-    ev = lkv.Evictor(cache, scorers, logits, cfg.ratio, lkv.BUDGET_EXACT, decode_slack=cfg.decode_steps + 1,
+    ev = lkv.Evictor(cache, scorers, logits, cfg.ratio, lkv.BUDGET_EXACT, decode_slack=cfg.decode_steps + 4,
                      keep_scores=False)
     lib = lkv.lib()
     stream = torch.cuda.current_stream()
