@@ -27,7 +27,7 @@ namespace lkv_dev {
 constexpr int kDecCh = 256;         // rows per work item
 constexpr int kDecStageRows = 64;   // rows per pipeline stage
 #ifndef LKV_DEC_STAGES
-#define LKV_DEC_STAGES 3
+#define LKV_DEC_STAGES 2
 #endif
 #ifndef LKV_DEC_PER_SM
 #define LKV_DEC_PER_SM 2
