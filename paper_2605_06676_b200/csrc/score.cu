@@ -219,9 +219,29 @@ __global__ void __launch_bounds__(TcCfg<N, NBOX>::kThreads, 1)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
 
-    // contiguous tile range of this CTA (tiles of a head, heads of a layer, stay together)
-    const int t_begin = (int)((int64_t)total_tiles * blockIdx.x / gridDim.x);
-    const int t_end = (int)((int64_t)total_tiles * (blockIdx.x + 1) / gridDim.x);
+    // Tile schedule.  LKV_SCORE_RR == 0: one contiguous range per CTA (tiles of a head and
+    // heads of a layer stay together).  LKV_SCORE_RR == g > 0: groups of g tiles dealt
+    // round-robin, so all CTAs stream through the same region of the cache at once.
+#ifndef LKV_SCORE_RR
+#define LKV_SCORE_RR 0
+#endif
+    constexpr int RR = LKV_SCORE_RR;
+    constexpr int RRd = RR > 0 ? RR : 1;
+    int n_local;
+    int t_begin = 0;
+    if (RR == 0) {
+        t_begin = (int)((int64_t)total_tiles * blockIdx.x / gridDim.x);
+        n_local = (int)((int64_t)total_tiles * (blockIdx.x + 1) / gridDim.x) - t_begin;
+    } else {
+        const int n_chunks = (total_tiles + RRd - 1) / RRd;
+        const int mine = (int)blockIdx.x < n_chunks ? (n_chunks - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+        n_local = mine * RRd;
+        if (mine && (n_chunks - 1) % (int)gridDim.x == (int)blockIdx.x) n_local -= n_chunks * RRd - total_tiles;
+    }
+    auto tile_of = [&](int i) -> int {
+        if (RR == 0) return t_begin + i;
+        return ((i / RRd) * (int)gridDim.x + (int)blockIdx.x) * RRd + (i % RRd);
+    };
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
@@ -253,8 +273,8 @@ __global__ void __launch_bounds__(TcCfg<N, NBOX>::kThreads, 1)
             const uint64_t pol_stream = l2_policy_evict_first();
             const uint64_t pol_keep = l2_policy_evict_last();
             int cur = -1, wloads = 0;
-            for (int tile = t_begin, i = 0; tile < t_end; ++tile, ++i) {
-                const TileInfo ti = decode_tile(p, tile, kTcRows);
+            for (int i = 0; i < n_local; ++i) {
+                const TileInfo ti = decode_tile(p, tile_of(i), kTcRows);
                 if (ti.scorer != cur) {
                     if (wloads > 0) mbar_wait(wempty, (wloads - 1) & 1);
                     mbar_arrive_expect_tx(wfull, Cfg::kW);
@@ -285,8 +305,8 @@ __global__ void __launch_bounds__(TcCfg<N, NBOX>::kThreads, 1)
             const uint32_t a_base = smem_u32(sA);
             const uint32_t w_base = smem_u32(sW);
             int cur = -1, wuses = 0;
-            for (int tile = t_begin, i = 0; tile < t_end; ++tile, ++i) {
-                const TileInfo ti = decode_tile(p, tile, kTcRows);
+            for (int i = 0; i < n_local; ++i) {
+                const TileInfo ti = decode_tile(p, tile_of(i), kTcRows);
                 if (ti.scorer != cur) {
                     if (wuses > 0) umma_commit(wempty);  // old weights free once prior MMAs retire
                     mbar_wait(wfull, wuses & 1);
@@ -334,8 +354,8 @@ __global__ void __launch_bounds__(TcCfg<N, NBOX>::kThreads, 1)
             named_bar_sync(1 + grp, 128);
         };
         int cur = -1, cur_head = -1;
-        for (int tile = t_begin + grp, i = grp; tile < t_end; tile += kEpi, i += kEpi) {
-            const TileInfo ti = decode_tile(p, tile, kTcRows);
+        for (int i = grp; i < n_local; i += kEpi) {
+            const TileInfo ti = decode_tile(p, tile_of(i), kTcRows);
             if (p.hist && ti.head != cur_head) {
                 if (cur_head >= 0) flush_hist(cur_head);
                 else named_bar_sync(1 + grp, 128);  // zeroing complete
