@@ -8,5 +8,6 @@ for flags in "$@"; do
   tag=$(echo "$flags" | tr -c 'A-Za-z0-9' '_')
   d=/tmp/lkvab_$tag; mkdir -p $d/build
   (cd paper_2605_06676_b200 && make -s OBJDIR=$d/build LIB=$d/liblkv_b200.so NVCC="nvcc $flags" $d/liblkv_b200.so >/dev/null 2>&1)
-  echo "[$flags] $(LKV_B200_LIB=$d/liblkv_b200.so python $script 2>&1 | tail -1)"
+  if [[ $script == *.sh ]]; then run="bash $script"; else run="python $script"; fi
+  echo "[$flags]"; LKV_B200_LIB=$d/liblkv_b200.so $run 2>&1 | tail -4
 done
