@@ -24,7 +24,10 @@
 
 namespace lkv_dev {
 
-constexpr int kDecCh = 256;         // rows per work item
+#ifndef LKV_DEC_CH
+#define LKV_DEC_CH 256
+#endif
+constexpr int kDecCh = LKV_DEC_CH;  // rows per work item
 constexpr int kDecStageRows = 64;   // rows per pipeline stage
 #ifndef LKV_DEC_STAGES
 #define LKV_DEC_STAGES 2
@@ -86,6 +89,24 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a
         : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
+// D = A B + C over an m16n8k16 tile; with HI == false the A rows 8..15 are zero and the
+// rows-8..15 half of C/D is dead, so it is fed zeros and discarded (no live registers).
+template <bool HI>
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    if constexpr (HI) {
+        mma_bf16_16816(d, a, b0, b1);
+    } else {
+        float x2, x3;
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+            "{%10,%11,%12,%13};"
+            : "=f"(d[0]), "=f"(d[1]), "=f"(x2), "=f"(x3)
+            : "r"(a[0]), "r"(0u), "r"(a[2]), "r"(0u), "r"(b0), "r"(b1), "f"(d[0]), "f"(d[1]), "f"(0.f), "f"(0.f));
+        d[2] = 0.f;
+        d[3] = 0.f;
+    }
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<uint32_t*>(&v);
@@ -99,6 +120,9 @@ __device__ __forceinline__ uint32_t sw_off(int row, int q) {
 }
 
 // ---- bf16 attention kernel (tensor cores) ------------------------------------------------------
+// HI: the group has more than 8 query heads, so rows 8..15 of the m16 fragments are live.
+// For G <= 8 those rows are zero padding: their accumulators are never kept in registers.
+template <bool HI>
 __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
     decode_attn_bf16_kernel(const __grid_constant__ DecodeParams p, const __grid_constant__ CUtensorMap tmap_k,
                             const __grid_constant__ CUtensorMap tmap_v) {
@@ -185,9 +209,9 @@ __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
             const uint32_t* r_lo = reinterpret_cast<const uint32_t*>(qp + (size_t)g * D);
             const uint32_t* r_hi = reinterpret_cast<const uint32_t*>(qp + (size_t)(g + 8) * D);
             qa[kk][0] = g < G ? __ldg(r_lo + (c0 >> 1)) : 0u;
-            qa[kk][1] = g + 8 < G ? __ldg(r_hi + (c0 >> 1)) : 0u;
+            qa[kk][1] = (HI && g + 8 < G) ? __ldg(r_hi + (c0 >> 1)) : 0u;
             qa[kk][2] = g < G ? __ldg(r_lo + ((c0 + 8) >> 1)) : 0u;
-            qa[kk][3] = g + 8 < G ? __ldg(r_hi + ((c0 + 8) >> 1)) : 0u;
+            qa[kk][3] = (HI && g + 8 < G) ? __ldg(r_hi + ((c0 + 8) >> 1)) : 0u;
         }
         float o[16][4];
 #pragma unroll
@@ -238,11 +262,12 @@ __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
                     const int q = kk * 2 + (j & 1);
                     uint32_t b0, b1, b2, b3;
                     ldmatrix_x4(kbase + sw_off(row, q), b0, b1, b2, b3);
-                    mma_bf16_16816(s0, qa[kk], b0, b1);
-                    mma_bf16_16816(s1, qa[kk], b2, b3);
+                    mma16816<HI>(s0, qa[kk], b0, b1);
+                    mma16816<HI>(s1, qa[kk], b2, b3);
                 }
                 // ---- mask, online softmax (log2 domain)
                 float sv[8] = {s0[0], s0[1], s1[0], s1[1], s0[2], s0[3], s1[2], s1[3]};
+                if constexpr (!HI) sv[4] = sv[5] = sv[6] = sv[7] = -INFINITY;
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
                     const int col = ((e & 2) ? 8 : 0) + cq + (e & 1);
@@ -270,8 +295,10 @@ __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
                 for (int n = 0; n < 16; ++n) {
                     o[n][0] *= a_lo;
                     o[n][1] *= a_lo;
-                    o[n][2] *= a_hi;
-                    o[n][3] *= a_hi;
+                    if constexpr (HI) {
+                        o[n][2] *= a_hi;
+                        o[n][3] *= a_hi;
+                    }
                 }
                 // P as the A operand (k = the 16 rows)
                 uint32_t pa[4];
@@ -287,8 +314,8 @@ __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
                     const int q = n2 * 2 + (j >> 1);
                     uint32_t b0, b1, b2, b3;
                     ldmatrix_x4_trans(vbase + sw_off(row, q), b0, b1, b2, b3);
-                    mma_bf16_16816(o[2 * n2], pa, b0, b1);
-                    mma_bf16_16816(o[2 * n2 + 1], pa, b2, b3);
+                    mma16816<HI>(o[2 * n2], pa, b0, b1);
+                    mma16816<HI>(o[2 * n2 + 1], pa, b2, b3);
                 }
             }
             __syncwarp();
@@ -316,7 +343,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
                 rw[g * stride + D + 1] = l_lo;
             }
         }
-        if (g + 8 < G) {
+        if (HI && g + 8 < G) {
 #pragma unroll
             for (int n = 0; n < 16; ++n) {
                 rw[(g + 8) * stride + n * 8 + cq] = o[n][2];
@@ -533,11 +560,15 @@ cudaError_t launch_decode(const DecodeParams& p, int dtype, const CUtensorMap* m
     if (p.max_items == 0) return cudaSuccess;
     if (dtype == LKV_BF16) {
         const size_t smem = decode_bf16_smem(p.G);
-        cudaError_t e = cudaFuncSetAttribute(decode_attn_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        auto kern = p.G > 8 ? decode_attn_bf16_kernel<true> : decode_attn_bf16_kernel<false>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        const int per_sm = (kDecPerSm == 2 && smem * 2 <= 220 * 1024) ? 2 : 1;
+        int per_sm = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDecThreads, smem);
+        if (e != cudaSuccess) return e;
+        per_sm = max(1, min(per_sm, kDecPerSm));
         const int grid = min(p.max_items, per_sm * num_sms);
-        decode_attn_bf16_kernel<<<grid, kDecThreads, smem, stream>>>(p, *mk, *mv);
+        kern<<<grid, kDecThreads, smem, stream>>>(p, *mk, *mv);
         decode_combine_kernel<__nv_bfloat16><<<dim3(p.n_heads, (p.G * p.head_dim + kCombThreads - 1) / kCombThreads), kCombThreads, 0, stream>>>(p, 1);
         note_launches(2);
     } else {
