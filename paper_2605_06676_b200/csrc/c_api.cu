@@ -556,7 +556,7 @@ lkv_status lkv_decode_step(const lkv_ragged_desc* r, int32_t n_seq, int32_t n_la
     const int G = n_q_heads / n_kv_heads;
     if (r->dtype == LKV_BF16 && (r->head_dim != 128 || G > 16))
         return fail(LKV_ERR_UNSUPPORTED, "bf16 decode needs head_dim 128 and group size <= 16");
-    if (r->dtype == LKV_F32 && (size_t)G * (r->head_dim + 512) * 4 > 200 * 1024)
+    if (r->dtype == LKV_F32 && (size_t)G * (r->head_dim + 1024) * 4 > 200 * 1024)
         return fail(LKV_ERR_UNSUPPORTED, "fp32 decode: group too large");
     const DecodeWs w = decode_layout(r, G);
     if ((st = check_ws(ws, ws_bytes, w.total))) return st;

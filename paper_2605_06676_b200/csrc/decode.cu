@@ -25,7 +25,7 @@
 namespace lkv_dev {
 
 #ifndef LKV_DEC_CH
-#define LKV_DEC_CH 512
+#define LKV_DEC_CH 1024
 #endif
 constexpr int kDecCh = LKV_DEC_CH;  // rows per work item
 constexpr int kDecStageRows = 64;   // rows per pipeline stage
