@@ -12,6 +12,8 @@ from paper_2605_06676_b200 import synth  # noqa: E402
 
 cfg = synth.CONFIGS[int(os.environ.get("CFG", "5"))]
 cache = synth.make_cache(cfg)
+if os.environ.get("UNIFORM"):
+    cache = lkv.DenseCache(cache.keys, cache.values, [int(os.environ["UNIFORM"])] * cache.shape[0])
 sc = synth.make_scorers(cfg)
 S, L, H, T, D = cache.shape
 out = torch.empty(S, L, H, T, dtype=torch.float32, device="cuda")
