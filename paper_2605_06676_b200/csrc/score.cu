@@ -138,12 +138,52 @@ __device__ __forceinline__ void tmem_ld_x<16>(uint32_t taddr, uint32_t (&r)[16])
         : "r"(taddr));
 }
 
+// Incremental walk over the (seq, head, 128-row tile) order: a CTA's tiles are consecutive, so
+// each step is a few integer ops instead of a search over the sequence table.
+struct TileCursor {
+    int s, hs, j, tph, t;
+};
+
 struct TileInfo {
     int head;      // flat head
     int row0;      // first row inside the head
     int t;         // tokens of this head
     int scorer;
 };
+
+__device__ __forceinline__ TileCursor cursor_at(const ScoreParams& p, int tile, int tile_rows) {
+    TileCursor c;
+    c.s = 0;
+    while (c.s + 1 < p.seq.n_seq && p.tile_base[c.s + 1] <= tile) ++c.s;
+    c.t = p.seq.len[c.s];
+    c.tph = (c.t + tile_rows - 1) / tile_rows;
+    const int local = tile - p.tile_base[c.s];
+    c.hs = local / c.tph;
+    c.j = local - c.hs * c.tph;
+    return c;
+}
+__device__ __forceinline__ void cursor_next(const ScoreParams& p, TileCursor& c, int tile_rows) {
+    if (++c.j == c.tph) {
+        c.j = 0;
+        if (++c.hs == p.seq.n_layers * p.seq.n_kv_heads) {
+            c.hs = 0;
+            if (++c.s < p.seq.n_seq) {
+                c.t = p.seq.len[c.s];
+                c.tph = (c.t + tile_rows - 1) / tile_rows;
+            }
+        }
+    }
+}
+__device__ __forceinline__ TileInfo cursor_info(const ScoreParams& p, const TileCursor& c, int tile_rows) {
+    const int H = p.seq.n_kv_heads;
+    const int l = c.hs / H, h = c.hs - l * H;
+    TileInfo ti;
+    ti.head = c.s * p.seq.n_layers * H + c.hs;
+    ti.row0 = c.j * tile_rows;
+    ti.t = c.t;
+    ti.scorer = l * p.stride_layer + h * p.stride_head;
+    return ti;
+}
 
 __device__ __forceinline__ TileInfo decode_tile(const ScoreParams& p, int tile, int tile_rows) {
     int s = 0;
@@ -273,8 +313,10 @@ __global__ void __launch_bounds__(TcCfg<N, NBOX>::kThreads, 1)
             const uint64_t pol_stream = l2_policy_evict_first();
             const uint64_t pol_keep = l2_policy_evict_last();
             int cur = -1, wloads = 0;
+            TileCursor cur_t = cursor_at(p, tile_of(0), kTcRows);
             for (int i = 0; i < n_local; ++i) {
-                const TileInfo ti = decode_tile(p, tile_of(i), kTcRows);
+                if (RR == 0 && i > 0) cursor_next(p, cur_t, kTcRows);
+                const TileInfo ti = RR == 0 ? cursor_info(p, cur_t, kTcRows) : decode_tile(p, tile_of(i), kTcRows);
                 if (ti.scorer != cur) {
                     if (wloads > 0) mbar_wait(wempty, (wloads - 1) & 1);
                     mbar_arrive_expect_tx(wfull, Cfg::kW);
@@ -305,8 +347,10 @@ __global__ void __launch_bounds__(TcCfg<N, NBOX>::kThreads, 1)
             const uint32_t a_base = smem_u32(sA);
             const uint32_t w_base = smem_u32(sW);
             int cur = -1, wuses = 0;
+            TileCursor cur_t = cursor_at(p, tile_of(0), kTcRows);
             for (int i = 0; i < n_local; ++i) {
-                const TileInfo ti = decode_tile(p, tile_of(i), kTcRows);
+                if (RR == 0 && i > 0) cursor_next(p, cur_t, kTcRows);
+                const TileInfo ti = RR == 0 ? cursor_info(p, cur_t, kTcRows) : decode_tile(p, tile_of(i), kTcRows);
                 if (ti.scorer != cur) {
                     if (wuses > 0) umma_commit(wempty);  // old weights free once prior MMAs retire
                     mbar_wait(wfull, wuses & 1);
@@ -354,8 +398,11 @@ __global__ void __launch_bounds__(TcCfg<N, NBOX>::kThreads, 1)
             named_bar_sync(1 + grp, 128);
         };
         int cur = -1, cur_head = -1;
+        TileCursor cur_t = cursor_at(p, tile_of(grp), kTcRows);
         for (int i = grp; i < n_local; i += kEpi) {
-            const TileInfo ti = decode_tile(p, tile_of(i), kTcRows);
+            if (RR == 0 && i > grp)
+                for (int k = 0; k < kEpi; ++k) cursor_next(p, cur_t, kTcRows);
+            const TileInfo ti = RR == 0 ? cursor_info(p, cur_t, kTcRows) : decode_tile(p, tile_of(i), kTcRows);
             if (p.hist && ti.head != cur_head) {
                 if (cur_head >= 0) flush_hist(cur_head);
                 else named_bar_sync(1 + grp, 128);  // zeroing complete
