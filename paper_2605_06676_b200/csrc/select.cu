@@ -277,22 +277,29 @@ __device__ __forceinline__ void gather_rows(const uint4* __restrict__ src, uint4
     const int units = 1 << log2_units;
     const int total = n_rows << log2_units;
     int u = tid;
-    for (; u + 7 * nthreads < total; u += 8 * nthreads) {
-        uint4 v[8];
+#ifndef LKV_GATHER_UNROLL
+#define LKV_GATHER_UNROLL 8
+#endif
+    constexpr int U = LKV_GATHER_UNROLL;
+    for (; u + (U - 1) * nthreads < total; u += U * nthreads) {
+        uint4 v[U];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < U; ++k) {
             const int uu = u + k * nthreads;
             v[k] = __ldg(src + ((size_t)rows[uu >> log2_units] << log2_units) + (uu & (units - 1)));
         }
 #pragma unroll
-        for (int k = 0; k < 8; ++k) __stcs(dst + u + k * nthreads, v[k]);
+        for (int k = 0; k < U; ++k) __stcs(dst + u + k * nthreads, v[k]);
     }
     for (; u < total; u += nthreads)
         __stcs(dst + u, __ldg(src + ((size_t)rows[u >> log2_units] << log2_units) + (u & (units - 1))));
 }
 
 // ---- S5 --------------------------------------------------------------------------
-__global__ void __launch_bounds__(kSelThreads) select_emit_kernel(const __grid_constant__ SelectParams p) {
+#ifndef LKV_EMIT_MINB
+#define LKV_EMIT_MINB 1
+#endif
+__global__ void __launch_bounds__(kSelThreads, LKV_EMIT_MINB) select_emit_kernel(const __grid_constant__ SelectParams p) {
     __shared__ int32_t s_pos[kChunk];
     __shared__ uint32_t s_scan[kSelThreads / 32 + 1];
     const ChunkInfo ci = decode_chunk(p, blockIdx.x);
