@@ -223,29 +223,22 @@ def run_ours(args, rank, world, local_rank):
     # ---- end to end through the public API with HOST buffers -----------------------------------
     e2e = None
     if not args.no_e2e:
-        hk = torch.empty(cache.keys.shape, dtype=cache.keys.dtype, pin_memory=True)
-        hv = torch.empty_like(hk, pin_memory=True)
-        hk.copy_(cache.keys)
-        hv.copy_(cache.values)
-        out_rows = int(ev.ragged.capacity_rows)
-        ok = torch.empty(out_rows, D, dtype=cache.keys.dtype, pin_memory=True)
-        ov = torch.empty_like(ok, pin_memory=True)
-        op = torch.empty(out_rows, dtype=torch.int32, pin_memory=True)
-        oo = torch.empty(ev.ragged.offsets.numel(), dtype=torch.int64, pin_memory=True)
+        # the host-resident form of the public API: lkv_evict_host streams K from pinned host
+        # memory (pipelined with scoring), gathers the kept V rows over PCIe and copies the
+        # compacted cache back to pinned host buffers -- every step, inside the timed region
+        hk = cache.keys.cpu().pin_memory()
+        hv = cache.values.cpu().pin_memory()
+        host_out = ev.host_result_buffer()
 
         def e2e_step():
-            cache.keys.copy_(hk, non_blocking=True)
-            cache.values.copy_(hv, non_blocking=True)
-            ev.launch()
-            ok.copy_(ev.ragged.keys, non_blocking=True)
-            ov.copy_(ev.ragged.values, non_blocking=True)
-            op.copy_(ev.ragged.positions, non_blocking=True)
-            oo.copy_(ev.ragged.offsets, non_blocking=True)
+            ev.launch_host(hk, hv, host_out, layers_per_chunk=args.e2e_chunk)
 
         e2e_steps = max(2, min(args.steps, 5))
         for _ in range(2):
             e2e_step()
         barrier()
+        ws.status()
+        assert torch.equal(host_out.lens, ev.ragged.lens.cpu())
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(e2e_steps):
@@ -258,12 +251,16 @@ def run_ours(args, rank, world, local_rank):
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             ms_e2e = float(t.item())
         ws.status()
-        h2d = 2 * hk.numel() * hk.element_size()
-        d2h = 2 * ok.numel() * ok.element_size() + op.numel() * 4 + oo.numel() * 8
+        row_b = D * cache.keys.element_size()
+        h2d = hk.numel() * hk.element_size() + (hv.numel() * hv.element_size() if scorers.input == lkv.SCORER_KV
+                                                 else kept_rows * row_b)
+        d2h = (2 * host_out.keys.numel() * host_out.keys.element_size() + host_out.positions.numel() * 4
+               + host_out.offsets.numel() * 8 + host_out.lens.numel() * 4)
         e2e = {"value": rows_per_step * world / (ms_e2e / 1e3), "unit": UNIT, "ms_per_step": ms_e2e,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "path": "pinned host K/V -> lkv_evict (C ABI) -> pinned host ragged cache"}
-        del hk, hv, ok, ov, op, oo
+               "path": "pinned host K/V -> lkv_evict_host (C ABI): K streamed per layer chunk, kept V gathered "
+                       "over PCIe, compacted cache copied back to pinned host"}
+        del hk, hv, host_out
 
     log("decode")
     # ---- decode over the compressed cache --------------------------------------------------------
@@ -437,6 +434,7 @@ def main():
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-heads", type=int, default=8)
+    ap.add_argument("--e2e-chunk", type=int, default=4, help="layers per host->device chunk in the e2e path")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 

@@ -16,6 +16,7 @@
  *                      compaction loop of prefill_with_eviction (evictsim.cpp:202-215)
  *   lkv_evict       <- prefill_with_eviction's score->select->compact loop
  *                      (evictsim.hpp:74, evictsim.cpp:161-215), K/V-given form
+ *   lkv_evict_host  <- the same, for a cache resident in (pinned) host memory
  *   lkv_decode_step <- decode_step's append + attention block (model.hpp:95,
  *                      model.cpp:240-265) -> masked_attention_dense (attention.hpp:57)
  *
@@ -186,6 +187,20 @@ lkv_status lkv_evict(const lkv_cache_desc* cache, const lkv_scorer_desc* scorer,
                      double target_ratio, int32_t mode, const lkv_ragged_desc* out, float* scores_out,
                      double* ratios_out, int32_t* budgets_out, void* workspace, size_t workspace_bytes,
                      lkv_stream_t stream);
+
+/* ---- fused, from a host-resident cache ------------------------------------------ */
+/* The same eviction for a dense cache held in pinned, device-mapped host memory
+ * (cudaHostAlloc / cudaHostRegister mapped): host_cache->keys/values are host pointers.
+ * K is uploaded into dev_keys (device, dense shape) in (sequence, layers_per_chunk-layer)
+ * chunks on a library copy stream, pipelined with scoring; the kept V rows are gathered
+ * straight from host memory (only the retained fraction of V crosses PCIe); with [k;v]
+ * scorers V is uploaded into dev_values too.  host_out (nullable) receives a copy of the
+ * compacted cache in pinned host buffers.  Everything is ordered on `stream`. */
+lkv_status lkv_evict_host(const lkv_cache_desc* host_cache, void* dev_keys, void* dev_values,
+                          const lkv_scorer_desc* scorer, const double* logits, double target_ratio,
+                          int32_t mode, const lkv_ragged_desc* out, const lkv_ragged_desc* host_out,
+                          int32_t layers_per_chunk, void* workspace, size_t workspace_bytes,
+                          lkv_stream_t stream);
 
 /* ---- K5: decode over the ragged cache ------------------------------------------- */
 /* lkv_decode_plan splits every head's capacity into 256-row work items (once

@@ -194,6 +194,7 @@ class RaggedCache:
     capacity_rows: int
     decode_slack: int
     device: str = "cuda"
+    pinned: bool = False
     offsets: torch.Tensor = field(init=False)
     lens: torch.Tensor = field(init=False)
     keys: torch.Tensor = field(init=False)
@@ -203,13 +204,14 @@ class RaggedCache:
 
     def __post_init__(self):
         n = self.n_seq * self.n_layers * self.n_kv_heads
-        self.offsets = torch.zeros(n + 1, dtype=torch.int64, device=self.device)
-        self.lens = torch.zeros(n, dtype=torch.int32, device=self.device)
+        kw = {"pin_memory": True} if self.pinned else {}
+        self.offsets = torch.zeros(n + 1, dtype=torch.int64, device=self.device, **kw)
+        self.lens = torch.zeros(n, dtype=torch.int32, device=self.device, **kw)
         rows = max(int(self.capacity_rows), 1)
-        self.keys = torch.empty(rows, self.head_dim, dtype=self.dtype, device=self.device)
-        self.values = torch.empty(rows, self.head_dim, dtype=self.dtype, device=self.device)
-        self.positions = torch.full((rows,), -1, dtype=torch.int32, device=self.device)
-        self.tokens_seen = torch.zeros(self.n_seq, dtype=torch.int32, device=self.device)
+        self.keys = torch.empty(rows, self.head_dim, dtype=self.dtype, device=self.device, **kw)
+        self.values = torch.empty(rows, self.head_dim, dtype=self.dtype, device=self.device, **kw)
+        self.positions = torch.full((rows,), -1, dtype=torch.int32, device=self.device, **kw)
+        self.tokens_seen = torch.zeros(self.n_seq, dtype=torch.int32, device=self.device, **kw)
         self._decode_ws = None
 
     @property
@@ -401,6 +403,31 @@ class Evictor:
         _check(lib().lkv_evict(C.byref(self._cd), C.byref(self._sd), _ptr(self.logits), self.R, self.mode,
                                C.byref(self._rd), _ptr(self.scores), _ptr(self.ratios), _ptr(self.budgets),
                                C.c_void_p(self.ws.ptr), self.ws.nbytes, _stream(stream)))
+
+    def launch_host(self, host_keys: torch.Tensor, host_values: torch.Tensor, host_out: "RaggedCache | None" = None,
+                    layers_per_chunk: int = 4, stream=None) -> None:
+        """Enqueue one eviction of a cache held in pinned host memory (lkv_evict_host): K is
+        streamed into this evictor's device K buffer chunk by chunk while earlier chunks are
+        scored, kept V rows are gathered straight from host memory, and the compacted cache is
+        copied into `host_out` (pinned, same capacity) when given."""
+        if not (host_keys.is_pinned() and host_values.is_pinned()):
+            raise ContractError("host K/V must be pinned (torch pin_memory)")
+        if tuple(host_keys.shape) != self.cache.shape or host_keys.dtype != self.cache.keys.dtype:
+            raise ContractError("host K/V must match the evictor's cache shape and dtype")
+        hd = CacheDesc(*[getattr(self._cd, f) for f, _ in CacheDesc._fields_])
+        hd.keys, hd.values = host_keys.data_ptr(), host_values.data_ptr()
+        dev_v = self.cache.values.data_ptr() if self.scorers.input == SCORER_KV else None
+        ho = host_out.desc() if host_out is not None else None
+        _check(lib().lkv_evict_host(C.byref(hd), C.c_void_p(self.cache.keys.data_ptr()), C.c_void_p(dev_v) if dev_v else None,
+                                    C.byref(self._sd), _ptr(self.logits), self.R, self.mode, C.byref(self._rd),
+                                    C.byref(ho) if ho is not None else None, layers_per_chunk,
+                                    C.c_void_p(self.ws.ptr), self.ws.nbytes, _stream(stream)))
+
+    def host_result_buffer(self) -> "RaggedCache":
+        """A pinned host RaggedCache with this evictor's capacity (target of launch_host)."""
+        r = self.ragged
+        return RaggedCache(r.n_seq, r.n_layers, r.n_kv_heads, r.head_dim, r.dtype, r.capacity_rows, r.decode_slack,
+                           device="cpu", pinned=True)
 
     def run(self) -> EvictResult:
         self.launch()

@@ -12,6 +12,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/lkv_b200.h"
 #include "kernels.cuh"
@@ -45,15 +46,19 @@ int num_sms() {
     return n > 0 ? n : 148;
 }
 
-// One non-blocking helper stream per (host thread, device) for fork/join inside a call.
-cudaStream_t side_stream() {
-    thread_local cudaStream_t streams[64] = {};
+// Non-blocking helper streams per (host thread, device) for fork/join inside a call:
+// `side` runs the latency-bound LKV-H solve, `copy` the host<->device transfers.
+cudaStream_t helper_stream(int which) {
+    thread_local cudaStream_t streams[2][64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= 64) return nullptr;
-    if (!streams[dev] && cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess) return nullptr;
-    return streams[dev];
+    cudaStream_t& s = streams[which][dev];
+    if (!s && cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    return s;
 }
+cudaStream_t side_stream() { return helper_stream(0); }
+cudaStream_t copy_stream() { return helper_stream(1); }
 
 constexpr size_t kAlign = 256;
 size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
@@ -201,7 +206,7 @@ lkv_status check_ragged(const lkv_ragged_desc* r, int64_t n_heads, int head_dim,
 // ---- internal launchers shared by lkv_score / lkv_evict ---------------------------------------------
 lkv_status run_score(const lkv_cache_desc* c, const lkv_scorer_desc* s, float* scores, cudaStream_t stream,
                      int sms_reserved = 0, uint32_t* hist = nullptr, ErrWord* err = nullptr,
-                     bool* hist_made = nullptr) {
+                     bool* hist_made = nullptr, bool clear_hist = true) {
     if (hist_made) *hist_made = false;
     ScoreParams p;
     memset(&p, 0, sizeof p);
@@ -228,7 +233,8 @@ lkv_status run_score(const lkv_cache_desc* c, const lkv_scorer_desc* s, float* s
                            (uint32_t)s->hidden);
         if (st) return st;
         if (hist) {
-            LKV_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 2048 * (size_t)n_heads_of(c), stream), "hist clear");
+            if (clear_hist)
+                LKV_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 2048 * (size_t)n_heads_of(c), stream), "hist clear");
             p.hist = hist;
             p.err = err;
             if (hist_made) *hist_made = true;
@@ -524,6 +530,133 @@ lkv_status lkv_evict(const lkv_cache_desc* c, const lkv_scorer_desc* s, const do
         return st;
     LKV_CUDA(cudaStreamWaitEvent(strm, join, 0), "stream wait");
     return run_select(c, scores, budgets, out, ws, w, true, strm, hist_made);
+}
+
+// Eviction of a host-resident (pinned, device-mapped) dense cache.  K is streamed to the
+// device in (sequence, layer-group) chunks on a copy stream while earlier chunks are scored;
+// the kept V rows are gathered straight from host memory (only rho of V crosses PCIe); the
+// compacted cache is optionally copied back to pinned host buffers on the copy stream.
+lkv_status lkv_evict_host(const lkv_cache_desc* hc, void* dev_keys, void* dev_values, const lkv_scorer_desc* s,
+                          const double* logits, double R, int32_t mode, const lkv_ragged_desc* out,
+                          const lkv_ragged_desc* host_out, int32_t layers_per_chunk, void* ws, size_t ws_bytes,
+                          lkv_stream_t stream) {
+    lkv_status st = check_cache(hc, true);
+    if (st) return st;
+    if ((st = check_scorer(s, hc))) return st;
+    if ((st = check_ragged(out, n_heads_of(hc), hc->head_dim, hc->dtype, true))) return st;
+    if (!dev_keys) return fail(LKV_ERR_CONTRACT, "dev_keys (device staging for K) is null");
+    const bool kv = s->input == LKV_SCORER_KV;
+    if (kv && !dev_values) return fail(LKV_ERR_CONTRACT, "[k;v] scorers need dev_values staging");
+    if (layers_per_chunk < 1) layers_per_chunk = 1;
+    // host V must be device-accessible (pinned + mapped): use its device alias for the gather
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, hc->values) != cudaSuccess || pa.type != cudaMemoryTypeHost || !pa.devicePointer)
+        return fail(LKV_ERR_CONTRACT, "host values must be pinned, device-mapped memory (cudaHostAlloc)");
+    const void* v_dev_alias = pa.devicePointer;
+    const int n = hc->n_layers * hc->n_kv_heads;
+    const EvictWs w = evict_layout(hc, n);
+    if ((st = check_ws(ws, ws_bytes, w.total))) return st;
+    cudaStream_t strm = (cudaStream_t)stream;
+    cudaStream_t side = side_stream(), cs = copy_stream();
+    if (!side || !cs) return fail(LKV_ERR_CUDA, "helper stream creation failed");
+    const size_t esz = hc->dtype == LKV_F32 ? 4 : 2;
+    const size_t head_bytes = (size_t)hc->max_tokens * hc->head_dim * esz;
+    const int H = hc->n_kv_heads, L = hc->n_layers;
+    int32_t* budgets = at<int32_t>(ws, w.budgets);
+    float* scores = at<float>(ws, w.scores);
+    uint32_t* hist = at<uint32_t>(ws, w.hist);
+
+    std::vector<cudaEvent_t> evs;
+    struct Evs {
+        std::vector<cudaEvent_t>& v;
+        ~Evs() {
+            for (auto e : v) cudaEventDestroy(e);
+        }
+    } guard{evs};
+    auto mk = [&]() -> cudaEvent_t {
+        cudaEvent_t e = nullptr;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess) evs.push_back(e);
+        return e;
+    };
+    cudaEvent_t start = mk(), join = mk();
+    if (!start || !join) return fail(LKV_ERR_CUDA, "event creation failed");
+    LKV_CUDA(cudaEventRecord(start, strm), "event record");
+    LKV_CUDA(cudaStreamWaitEvent(side, start, 0), "stream wait");
+    LKV_CUDA(cudaStreamWaitEvent(cs, start, 0), "stream wait");
+    // K2 on the side stream
+    st = lkv_budgets(logits, n, R, mode, hc->seq_lens, hc->n_seq, out->decode_slack, at<double>(ws, w.ratios), budgets,
+                     out->offsets, ws, ws_bytes, (lkv_stream_t)side);
+    if (st) return st;
+    LKV_CUDA(cudaEventRecord(join, side), "event record");
+    // K upload (copy stream) pipelined with K1 (main stream), chunk = (sequence, layer group)
+    bool hist_made = false;
+    LKV_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 2048 * (size_t)n_heads_of(hc), strm), "hist clear");
+    for (int sq = 0; sq < hc->n_seq; ++sq) {
+        for (int l0 = 0; l0 < L; l0 += layers_per_chunk) {
+            const int nl = std::min(layers_per_chunk, L - l0);
+            const size_t first_head = (size_t)(sq * L + l0) * H;
+            const size_t bytes = (size_t)nl * H * head_bytes;
+            char* dk = static_cast<char*>(dev_keys) + first_head * head_bytes;
+            LKV_CUDA(cudaMemcpyAsync(dk, static_cast<const char*>(hc->keys) + first_head * head_bytes, bytes,
+                                     cudaMemcpyHostToDevice, cs),
+                     "K upload");
+            char* dv = nullptr;
+            if (kv) {
+                dv = static_cast<char*>(dev_values) + first_head * head_bytes;
+                LKV_CUDA(cudaMemcpyAsync(dv, static_cast<const char*>(hc->values) + first_head * head_bytes, bytes,
+                                         cudaMemcpyHostToDevice, cs),
+                         "V upload");
+            }
+            cudaEvent_t ready = mk();
+            if (!ready) return fail(LKV_ERR_CUDA, "event creation failed");
+            LKV_CUDA(cudaEventRecord(ready, cs), "event record");
+            LKV_CUDA(cudaStreamWaitEvent(strm, ready, 0), "stream wait");
+            lkv_cache_desc sub = *hc;
+            sub.n_seq = 1;
+            sub.n_layers = nl;
+            sub.keys = dk;
+            sub.values = kv ? dv : dk;
+            sub.seq_lens = hc->seq_lens + sq;
+            lkv_scorer_desc ss = *s;
+            const int64_t sc0 = (int64_t)l0 * s->stride_layer;
+            const size_t in = (size_t)s->input * hc->head_dim;
+            ss.w1t = static_cast<const char*>(s->w1t) + (size_t)sc0 * s->hidden * in * esz;
+            ss.b1 = s->b1 + sc0 * s->hidden;
+            ss.w2 = s->w2 + sc0 * s->hidden;
+            ss.n_scorers = (int32_t)(s->n_scorers - sc0);
+            bool made = false;
+            if ((st = run_score(&sub, &ss, scores + first_head * hc->max_tokens, strm, 1, hist + first_head * 2048,
+                                at<ErrWord>(ws, w.err), &made, /*clear_hist=*/false)))
+                return st;
+            hist_made = made;
+        }
+    }
+    LKV_CUDA(cudaStreamWaitEvent(strm, join, 0), "stream wait");
+    lkv_cache_desc gsrc = *hc;
+    gsrc.keys = dev_keys;
+    gsrc.values = kv ? dev_values : v_dev_alias;
+    if ((st = run_select(&gsrc, scores, budgets, out, ws, w, true, strm, hist_made))) return st;
+    if (host_out) {
+        if (!host_out->keys || !host_out->values || !host_out->positions || !host_out->offsets || !host_out->lens ||
+            host_out->capacity_rows < out->capacity_rows)
+            return fail(LKV_ERR_CONTRACT, "host_out buffers missing or too small");
+        cudaEvent_t done = mk(), back = mk();
+        if (!done || !back) return fail(LKV_ERR_CUDA, "event creation failed");
+        LKV_CUDA(cudaEventRecord(done, strm), "event record");
+        LKV_CUDA(cudaStreamWaitEvent(cs, done, 0), "stream wait");
+        const size_t rowb = (size_t)hc->head_dim * esz, rows = (size_t)out->capacity_rows;
+        LKV_CUDA(cudaMemcpyAsync(host_out->keys, out->keys, rows * rowb, cudaMemcpyDeviceToHost, cs), "D2H");
+        LKV_CUDA(cudaMemcpyAsync(host_out->values, out->values, rows * rowb, cudaMemcpyDeviceToHost, cs), "D2H");
+        LKV_CUDA(cudaMemcpyAsync(host_out->positions, out->positions, rows * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+        LKV_CUDA(cudaMemcpyAsync(host_out->offsets, out->offsets, sizeof(int64_t) * (out->n_heads + 1),
+                                 cudaMemcpyDeviceToHost, cs),
+                 "D2H");
+        LKV_CUDA(cudaMemcpyAsync(host_out->lens, out->lens, sizeof(int32_t) * out->n_heads, cudaMemcpyDeviceToHost, cs),
+                 "D2H");
+        LKV_CUDA(cudaEventRecord(back, cs), "event record");
+        LKV_CUDA(cudaStreamWaitEvent(strm, back, 0), "stream wait");
+    }
+    return LKV_OK;
 }
 
 size_t lkv_decode_workspace_bytes(const lkv_ragged_desc* r, int32_t G) {

@@ -518,3 +518,35 @@ def test_decode_many_steps_stays_consistent():
         _, _, p = rc.head(h)
         p = p.cpu().numpy()
         assert (np.diff(p) > 0).all() and p[-1] == 2000 + 199
+
+
+@pytest.mark.parametrize("cid,inp", [(2, lkv.SCORER_K), (4, lkv.SCORER_K), (2, lkv.SCORER_KV)])
+def test_evict_from_host_memory_matches_device_path(cid, inp):
+    """lkv_evict_host (K streamed in chunks, kept V gathered over PCIe from pinned host memory,
+    result copied back) produces exactly the device-resident eviction."""
+    cfg = synth.CONFIGS[cid]
+    L, T, S = 3, 5000, (3 if cfg.n_seq > 1 else 1)
+    cache = synth.make_cache(cfg, n_layers=L, max_tokens=T, n_seq=S)
+    if inp == lkv.SCORER_KV:
+        w1 = (torch.randn(L * 8, 256, 128, device=DEV) / 16).to(torch.bfloat16)
+        scorers = lkv.Scorers(w1, torch.zeros(L * 8, 128, device=DEV), torch.randn(L * 8, 128, device=DEV) / 11,
+                              input=lkv.SCORER_KV, activation=lkv.SILU, stride_layer=8, stride_head=1)
+    else:
+        scorers = synth.make_scorers(cfg, n_layers=L)
+    logits = synth.make_logits(cfg, n_layers=L)
+    ref = lkv.evict(cache, scorers, logits, cfg.ratio, lkv.BUDGET_EXACT, decode_slack=2, keep_scores=False)
+    hk = cache.keys.cpu().pin_memory()
+    hv = cache.values.cpu().pin_memory()
+    dense = lkv.DenseCache(torch.zeros_like(cache.keys), torch.zeros_like(cache.values), cache.seq_lens)
+    ev = lkv.Evictor(dense, scorers, logits, cfg.ratio, lkv.BUDGET_EXACT, decode_slack=2)
+    out = ev.host_result_buffer()
+    ev.launch_host(hk, hv, out, layers_per_chunk=2)
+    ev.ws.status()
+    assert torch.equal(ev.ragged.lens, ref.cache.lens)
+    assert torch.equal(out.lens, ref.cache.lens.cpu())
+    assert torch.equal(out.offsets, ref.cache.offsets.cpu())
+    for h in range(cache.n_heads):
+        o, n = int(out.offsets[h]), int(out.lens[h])
+        ko, vo, po = ref.cache.head(h)
+        assert torch.equal(out.positions[o:o + n], po.cpu())
+        assert torch.equal(out.keys[o:o + n], ko.cpu()) and torch.equal(out.values[o:o + n], vo.cpu())
