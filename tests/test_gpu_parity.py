@@ -550,3 +550,56 @@ def test_evict_from_host_memory_matches_device_path(cid, inp):
         ko, vo, po = ref.cache.head(h)
         assert torch.equal(out.positions[o:o + n], po.cpu())
         assert torch.equal(out.keys[o:o + n], ko.cpu()) and torch.equal(out.values[o:o + n], vo.cpu())
+
+
+def test_evict_is_deterministic():
+    """Two evictions of the same inputs are byte-identical (the reference's rerun determinism,
+    test_distill.cpp:251-259): scores, budgets, positions and rows."""
+    cfg = synth.CONFIGS[4]
+    cache = synth.make_cache(cfg, n_layers=2, max_tokens=6000, n_seq=3)
+    scorers = synth.make_scorers(cfg, n_layers=2)
+    logits = synth.make_logits(cfg, n_layers=2)
+    a = lkv.evict(cache, scorers, logits, cfg.ratio, lkv.BUDGET_EXACT, decode_slack=1)
+    b = lkv.evict(cache, scorers, logits, cfg.ratio, lkv.BUDGET_EXACT, decode_slack=1)
+    assert torch.equal(a.scores, b.scores) and torch.equal(a.budgets, b.budgets)
+    assert torch.equal(a.cache.offsets, b.cache.offsets) and torch.equal(a.cache.lens, b.cache.lens)
+    cap = int(a.cache.offsets[-1])
+    for x, y in ((a.cache.positions, b.cache.positions), (a.cache.keys, b.cache.keys), (a.cache.values, b.cache.values)):
+        for h in range(cache.n_heads):
+            o, n = int(a.cache.offsets[h]), int(a.cache.lens[h])
+            assert torch.equal(x[o:o + n], y[o:o + n])
+    assert cap == int(b.cache.offsets[-1])
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("ratio", [0.05, 0.25])
+def test_config3_full_size_properties(ratio):
+    """C3 at full size (t = 131072, 256 heads): exact totals, top-b property with the
+    lowest-index tie rule, rows equal the dense rows at the kept positions."""
+    cfg = synth.CONFIGS[3]
+    cache = synth.make_cache(cfg)
+    scorers = synth.make_scorers(cfg)
+    logits = synth.make_logits(cfg)
+    res = lkv.evict(cache, scorers, logits, ratio, lkv.BUDGET_EXACT, keep_scores=True)
+    n, T = cfg.n_layers * cfg.n_kv_heads, cfg.max_tokens
+    b = res.budgets.reshape(-1)
+    assert int(b.sum()) == {0.05: 1677722, 0.25: 8388608}[ratio]
+    want_b = O.freeze_budgets_exact(O.allocate_budgets(logits.cpu().numpy(), ratio), ratio, T)
+    assert (b.cpu().numpy() == want_b).all()
+    scores = res.scores.reshape(n, T)
+    offs = res.cache.offsets.cpu().tolist()
+    Kd = cache.keys.reshape(n, T, -1)
+    Vd = cache.values.reshape(n, T, -1)
+    for h in range(n):
+        bh = int(b[h])
+        p = res.cache.positions[offs[h]:offs[h] + bh].long()
+        assert bool((p[1:] > p[:-1]).all())
+        mask = torch.zeros(T, dtype=torch.bool, device=DEV)
+        mask[p] = True
+        sel, rest = scores[h][mask], scores[h][~mask]
+        if bh and rest.numel():
+            assert sel.min() >= rest.max()
+        assert torch.equal(res.cache.keys[offs[h]:offs[h] + bh], Kd[h][p])
+        assert torch.equal(res.cache.values[offs[h]:offs[h] + bh], Vd[h][p])
+        if h % 61 == 0:
+            assert (p.cpu().numpy() == O.select_positions_f32(scores[h].cpu().numpy(), bh)).all()
