@@ -147,6 +147,18 @@ struct MemoryReport {
 MemoryReport kv_memory_bytes(const MemoryModel& model, double retention);
 MemoryReport kv_memory_bytes(const MemoryModel& model, const std::vector<int>& per_head_budgets);
 
+// ---- trained-policy ingestion (checkpoint.cpp:56-86, container.cpp:92-137) -------------------------
+// LKV policy checkpoint written by the reference (`lkv train` -> lkv_params.bin).
+struct LkvParams {
+    int n_layers = 0, n_kv_heads = 0, d_e = 0, d_head = 0;
+    std::vector<double> head_embeddings;  // [L*H x d_e]
+    Mlp2 head_predictor;                  // d_e -> d_e/2 -> 1
+    std::vector<Mlp2> token_scorers;      // one per (l, h): 2 d_head -> d_head -> 1
+};
+LkvParams load_lkv_params(const std::string& path);
+// policy.cpp:106-108 -- the LKV-H logits (fp64 host setup, once per checkpoint)
+std::vector<double> head_scores(const LkvParams& params);
+
 // Throws device_error unless an sm_100 (B200) device is current.
 void require_b200();
 

@@ -8,6 +8,7 @@
 #include <span>
 #include <vector>
 
+#include "lkv/checkpoint.hpp"
 #include "lkv/errors.hpp"
 #include "lkv/policy.hpp"
 #include "lkv/soft_topk.hpp"
@@ -96,6 +97,30 @@ int ref_token_scores(const double* k, const double* v, int t, int d, const doubl
         lkv::Tensor V = lkv::Tensor::from({t, d}, std::vector<double>(v, v + static_cast<size_t>(t) * d));
         lkv::Tensor u = lkv::token_scores(K, V, m);
         std::memcpy(out, u.data(), sizeof(double) * static_cast<size_t>(t));
+    });
+}
+
+// Writes a real LKV policy checkpoint with the reference's own init + save path
+// (policy.cpp:88-104, checkpoint.cpp:56-66) -- the trained-policy artifact of `lkv train`.
+int ref_write_lkv_params(const char* path, int n_layers, int n_kv_heads, int head_dim, int d_e, unsigned long long seed) {
+    return guarded([&] {
+        lkv::ModelConfig cfg;
+        cfg.n_layers = n_layers;
+        cfg.n_kv_heads = n_kv_heads;
+        cfg.n_query_heads = n_kv_heads;
+        cfg.head_dim = head_dim;
+        lkv::LkvParams p = lkv::init_lkv_params(cfg, seed, d_e);
+        lkv::save_lkv_params(path, p);
+    });
+}
+
+// load_lkv_params + head_scores (policy.cpp:106-108): the LKV-H logits of a checkpoint.
+int ref_head_scores(const char* path, double* out, int n) {
+    return guarded([&] {
+        lkv::LkvParams p = lkv::load_lkv_params(path);
+        lkv::Tensor s = lkv::head_scores(p);
+        if ((int)s.numel() != n) throw lkv::contract_error("ref_head_scores: size");
+        std::memcpy(out, s.data(), sizeof(double) * (size_t)n);
     });
 }
 

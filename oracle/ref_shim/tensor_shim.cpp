@@ -67,6 +67,8 @@ double Tensor::value() const {
     return (*data_)[0];
 }
 
+Tensor Tensor::detached_clone() const { return Tensor::from(shape_, *data_); }
+
 Tensor add(const Tensor& a, const Tensor& b) {
     if (a.shape() != b.shape()) throw contract_error("add: shape mismatch");
     check_finite(a, "add");
@@ -149,6 +151,12 @@ Tensor reshape(const Tensor& x, std::vector<int> shape) {
 Tensor make_op_output(std::vector<int> shape, std::vector<double> values, std::vector<Tensor>,
                       std::function<std::vector<Tensor>(const Tensor&)>) {
     return Tensor::from(std::move(shape), std::move(values));
+}
+
+// checkpoint.cpp's model save/load is not on this path; link-time stubs only.
+ModelWeights init_model(const ModelConfig&) { throw contract_error("init_model: not part of the oracle/_ref build"); }
+std::vector<std::pair<std::string, Tensor*>> ModelWeights::named_params() {
+    throw contract_error("ModelWeights::named_params: not part of the oracle/_ref build");
 }
 
 void ModelConfig::validate() const {

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <limits>
 
@@ -444,6 +445,192 @@ std::vector<double> decode_attention(KvCache& cache, std::span<const double> q, 
         hc.retained_positions.push_back(cache.tokens_seen);
     }
     cache.tokens_seen += 1;
+    return out;
+}
+
+// ---- checkpoint.cpp:68-86 / container.cpp:92-137 --------------------------------------------------------
+namespace {
+// Just enough JSON for the container metadata: an ordered object of objects holding
+// strings, non-negative integers and arrays of integers.
+struct MetaRec {
+    std::string name, dtype;
+    std::vector<int> shape;
+    uint64_t off = 0, len = 0;
+};
+struct JsonCursor {
+    const std::string& s;
+    size_t i = 0;
+    void ws() {
+        while (i < s.size() && (s[i] == ' ' || s[i] == '\n' || s[i] == '\t' || s[i] == '\r')) ++i;
+    }
+    void expect(char c) {
+        ws();
+        if (i >= s.size() || s[i] != c) throw contract_error("container: bad metadata JSON");
+        ++i;
+    }
+    bool peek(char c) {
+        ws();
+        return i < s.size() && s[i] == c;
+    }
+    std::string str() {
+        expect('"');
+        std::string o;
+        while (i < s.size() && s[i] != '"') {
+            if (s[i] == '\\') ++i;
+            if (i < s.size()) o += s[i++];
+        }
+        expect('"');
+        return o;
+    }
+    uint64_t num() {
+        ws();
+        uint64_t v = 0;
+        size_t j = i;
+        while (i < s.size() && s[i] >= '0' && s[i] <= '9') v = v * 10 + (uint64_t)(s[i++] - '0');
+        if (i == j) throw contract_error("container: bad metadata JSON");
+        return v;
+    }
+};
+
+std::vector<MetaRec> parse_meta(const std::string& js) {
+    JsonCursor c{js};
+    std::vector<MetaRec> out;
+    c.expect('{');
+    while (!c.peek('}')) {
+        MetaRec r;
+        r.name = c.str();
+        c.expect(':');
+        c.expect('{');
+        int seen = 0;
+        while (!c.peek('}')) {
+            const std::string key = c.str();
+            c.expect(':');
+            if (key == "dtype") {
+                r.dtype = c.str();
+                seen |= 1;
+            } else if (key == "shape") {
+                c.expect('[');
+                while (!c.peek(']')) {
+                    r.shape.push_back((int)c.num());
+                    if (c.peek(',')) c.expect(',');
+                }
+                c.expect(']');
+                seen |= 2;
+            } else if (key == "byte_offset") {
+                r.off = c.num();
+                seen |= 4;
+            } else if (key == "byte_length") {
+                r.len = c.num();
+                seen |= 8;
+            } else {
+                throw contract_error("container: unexpected field " + key);
+            }
+            if (c.peek(',')) c.expect(',');
+        }
+        c.expect('}');
+        if (seen != 15) throw contract_error("container: incomplete record for " + r.name);
+        out.push_back(r);
+        if (c.peek(',')) c.expect(',');
+    }
+    c.expect('}');
+    return out;
+}
+
+struct Loaded {
+    std::vector<int> shape;
+    std::vector<double> v;
+};
+
+std::vector<std::pair<std::string, Loaded>> load_container(const std::string& path) {
+    FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) throw contract_error("container: cannot open: " + path);
+    std::string raw;
+    char buf[1 << 16];
+    size_t got;
+    while ((got = std::fread(buf, 1, sizeof buf, f)) > 0) raw.append(buf, got);
+    std::fclose(f);
+    if (raw.size() < 8) throw contract_error("container: truncated header");
+    uint64_t meta_len = 0;
+    for (int i = 0; i < 8; ++i) meta_len |= (uint64_t)(unsigned char)raw[(size_t)i] << (8 * i);
+    if (8 + meta_len > raw.size()) throw contract_error("container: truncated metadata");
+    const auto recs = parse_meta(raw.substr(8, meta_len));
+    const char* payload = raw.data() + 8 + meta_len;
+    const uint64_t payload_size = raw.size() - 8 - meta_len;
+    std::vector<std::pair<std::string, Loaded>> out;
+    uint64_t expected = 0;
+    for (const MetaRec& r : recs) {
+        const size_t es = r.dtype == "f64" ? 8 : r.dtype == "f32" ? 4 : 0;
+        if (!es) throw contract_error("container: unknown dtype " + r.dtype);
+        if (r.off != expected) throw contract_error("container: offsets must be contiguous and in order");
+        if (r.off + r.len > payload_size) throw contract_error("container: payload shorter than metadata claims");
+        size_t numel = 1;
+        for (int d : r.shape) numel *= (size_t)d;
+        if (r.len != numel * es) throw contract_error("container: byte length mismatch for " + r.name);
+        Loaded L{r.shape, std::vector<double>(numel)};
+        if (es == 8) {
+            std::memcpy(L.v.data(), payload + r.off, r.len);
+        } else {
+            std::vector<float> tmp(numel);
+            std::memcpy(tmp.data(), payload + r.off, r.len);
+            for (size_t i = 0; i < numel; ++i) L.v[i] = tmp[i];
+        }
+        out.emplace_back(r.name, std::move(L));
+        expected = r.off + r.len;
+    }
+    if (expected != payload_size) throw contract_error("container: trailing bytes after last tensor");
+    return out;
+}
+
+const Loaded& entry(const std::vector<std::pair<std::string, Loaded>>& c, const std::string& name) {
+    for (const auto& e : c)
+        if (e.first == name) return e.second;
+    throw contract_error("container: missing tensor " + name);
+}
+
+Mlp2 mlp_of(const std::vector<std::pair<std::string, Loaded>>& c, const std::string& p, int in, int hidden) {
+    const Loaded &w1 = entry(c, p + "w1"), &b1 = entry(c, p + "b1"), &w2 = entry(c, p + "w2");
+    if (w1.shape != std::vector<int>{in, hidden} || b1.shape != std::vector<int>{hidden} ||
+        w2.shape != std::vector<int>{hidden, 1})
+        throw contract_error("policy checkpoint: shape mismatch for " + p);
+    return Mlp2{in, hidden, w1.v, b1.v, w2.v};
+}
+}  // namespace
+
+LkvParams load_lkv_params(const std::string& path) {
+    const auto c = load_container(path);
+    const Loaded& meta = entry(c, "__meta");
+    if (meta.v.size() != 5 || meta.v[0] != 1.0) throw contract_error("policy checkpoint: unsupported metadata");
+    LkvParams p;
+    p.n_layers = (int)meta.v[1];
+    p.n_kv_heads = (int)meta.v[2];
+    p.d_e = (int)meta.v[3];
+    p.d_head = (int)meta.v[4];
+    const int n = p.n_layers * p.n_kv_heads;
+    const Loaded& emb = entry(c, "head_embeddings");
+    if (emb.shape != std::vector<int>{n, p.d_e}) throw contract_error("policy checkpoint: shape mismatch for head_embeddings");
+    p.head_embeddings = emb.v;
+    p.head_predictor = mlp_of(c, "head_predictor.", p.d_e, p.d_e / 2);
+    for (int i = 0; i < n; ++i)
+        p.token_scorers.push_back(mlp_of(c, "token_scorers." + std::to_string(i) + ".", 2 * p.d_head, p.d_head));
+    return p;
+}
+
+std::vector<double> head_scores(const LkvParams& p) {
+    const int n = p.n_layers * p.n_kv_heads, de = p.d_e, hid = p.head_predictor.hidden;
+    std::vector<double> out((size_t)n, 0.0), h((size_t)hid);
+    for (int r = 0; r < n; ++r) {
+        std::fill(h.begin(), h.end(), 0.0);
+        for (int i = 0; i < de; ++i) {
+            const double x = p.head_embeddings[(size_t)r * de + i];
+            for (int j = 0; j < hid; ++j) h[(size_t)j] += x * p.head_predictor.w1[(size_t)i * hid + j];
+        }
+        double s = 0.0;
+        for (int j = 0; j < hid; ++j) {
+            const double v = h[(size_t)j] + p.head_predictor.b1[(size_t)j];
+            s += v / (1.0 + std::exp(-v)) * p.head_predictor.w2[(size_t)j];
+        }
+        out[(size_t)r] = s;
+    }
     return out;
 }
 

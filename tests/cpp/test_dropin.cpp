@@ -266,9 +266,37 @@ static void test_memory() {  // test_evictsim.cpp:45-80
     CHECK(r.compressed_bytes == (15 + 14) * 4 * 2.0 * 2);
 }
 
-int main() {
+static void test_checkpoint(const char* dir) {  // the reference's own lkv_params.bin (tests/golden)
+    if (!dir) return;
+    const std::string base(dir);
+    LkvParams p = load_lkv_params(base + "/lkv_params_l2h4d128.bin");
+    CHECK(p.n_layers == 2 && p.n_kv_heads == 4 && p.d_head == 128 && p.d_e == 32);
+    CHECK(p.token_scorers.size() == 8);
+    auto logits = head_scores(p);
+    // head_scores_l2h4d128.npy: 128-byte npy header then 8 little-endian doubles
+    FILE* f = std::fopen((base + "/head_scores_l2h4d128.npy").c_str(), "rb");
+    CHECK(f != nullptr);
+    if (f) {
+        std::vector<double> want(8);
+        std::fseek(f, 128, SEEK_SET);
+        CHECK(std::fread(want.data(), 8, 8, f) == 8);
+        std::fclose(f);
+        for (int i = 0; i < 8; ++i) CHECK(std::fabs(logits[(size_t)i] - want[(size_t)i]) <= 1e-12 * (1.0 + std::fabs(want[(size_t)i])));
+    }
+    // the checkpoint drives the device path end to end (reference mode, floor budgets)
+    BudgetTable t = allocate_budgets(logits, 0.15, 2, 4);
+    const int T = 600;
+    auto budgets = freeze_budgets(t, T);
+    KvTrace tr = make_trace(2, 4, 128, T, 700);
+    auto [cache, rep] = prefill_with_eviction(tr, budgets, p.token_scorers, Activation::silu, Precision::bf16);
+    for (int h = 0; h < 8; ++h) CHECK(cache.heads[(size_t)h].retained() == budgets[(size_t)h]);
+    CHECK_THROWS_AS(load_lkv_params(base + "/does_not_exist.bin"), contract_error);
+}
+
+int main(int argc, char** argv) {
     try {
         require_b200();
+        test_checkpoint(argc > 1 ? argv[1] : nullptr);
         test_budgets();
         test_hard_topk();
         test_token_scores();

@@ -25,7 +25,7 @@ def test_dropin_symbols_exported():
     names = set(re.findall(r"^[A-Za-z].*?\b([a-z_0-9]+)\(", hdr, flags=re.M)) - {"explicit", "at", "head", "retained",
                                                                                 "param_count"}
     assert {"allocate_budgets", "freeze_budgets", "token_scores", "inference_select", "hard_topk", "cache_from_trace",
-            "prefill_with_eviction", "decode_attention", "kv_memory_bytes"} <= names
+            "prefill_with_eviction", "decode_attention", "kv_memory_bytes", "load_lkv_params", "head_scores"} <= names
     for n in sorted(names):
         assert re.search(r"lkv::b200::" + n + r"\(", out), n
 
@@ -39,7 +39,7 @@ def test_dropin_binary_links():
 @pytest.mark.gpu
 def test_dropin_reference_tests_on_b200():
     _ensure_built()
-    r = subprocess.run([BIN], capture_output=True, text=True, timeout=300)
+    r = subprocess.run([BIN, os.path.join(ROOT, "tests", "golden")], capture_output=True, text=True, timeout=300)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert re.search(r"(\d+) passed, 0 failed", r.stdout)

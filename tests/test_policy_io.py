@@ -1,0 +1,86 @@
+"""Trained-policy ingestion: the reference's own checkpoint files (tests/golden, written by
+the unmodified reference save path via tests/golden/make_golden.py) -> LKV-H logits and
+LKV-T scorer tables for the device path."""
+import os
+import struct
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import paper_2605_06676_b200 as lkv
+from paper_2605_06676_b200 import policy_io
+
+G = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.mark.parametrize("name,L,H,d,de", [("desk", 4, 2, 16, 16), ("l2h4d128", 2, 4, 128, 32)])
+def test_load_reference_checkpoint(name, L, H, d, de):
+    p = policy_io.load_lkv_params(os.path.join(G, f"lkv_params_{name}.bin"))
+    assert (p.n_layers, p.n_kv_heads, p.d_head, p.d_e) == (L, H, d, de)
+    assert len(p.token_scorers) == L * H
+    assert p.head_embeddings.shape == (L * H, de)
+    assert p.head_predictor.w1.shape == (de, de // 2)
+    # init_mlp2 (policy.cpp:18-28): b1 = 0, w1 ~ N(0, 1/in)
+    assert all((m.b1 == 0).all() for m in p.token_scorers)
+    assert abs(np.std(np.concatenate([m.w1.ravel() for m in p.token_scorers])) - 1 / np.sqrt(2 * d)) < 0.1 / np.sqrt(d)
+    # the LKV-H logits equal the reference's own load_lkv_params + head_scores
+    want = np.load(os.path.join(G, f"head_scores_{name}.npy"))
+    got = policy_io.head_scores(p)
+    assert np.max(np.abs(got - want)) <= 1e-12 * max(1.0, np.max(np.abs(want)))
+    # parameter count fixture (policy.cpp:289-299): 2d*d + d + d per scorer
+    assert sum(m.w1.size + m.b1.size + m.w2.size for m in p.token_scorers) == L * H * (2 * d * d + 2 * d)
+
+
+def test_budgets_from_checkpoint_are_the_references():
+    p = policy_io.load_lkv_params(os.path.join(G, "lkv_params_desk.bin"))
+    logits = np.load(os.path.join(G, "head_scores_desk.npy"))
+    r = O.allocate_budgets(policy_io.head_scores(p), 0.15)
+    assert np.allclose(r, O.allocate_budgets(logits, 0.15), rtol=1e-12, atol=0)
+
+
+def test_container_validation(tmp_path):
+    src = open(os.path.join(G, "lkv_params_desk.bin"), "rb").read()
+    bad = tmp_path / "trunc.bin"
+    bad.write_bytes(src[:4])
+    with pytest.raises(lkv.ContractError):
+        policy_io.load_container(str(bad))
+    bad.write_bytes(src[:-3])
+    with pytest.raises(lkv.ContractError):
+        policy_io.load_container(str(bad))
+    bad.write_bytes(src + b"xx")
+    with pytest.raises(lkv.ContractError):
+        policy_io.load_container(str(bad))
+    (meta_len,) = struct.unpack("<Q", src[:8])
+    bad.write_bytes(struct.pack("<Q", meta_len) + b"{" * meta_len + src[8 + meta_len:])
+    with pytest.raises(lkv.ContractError):
+        policy_io.load_container(str(bad))
+
+
+@pytest.mark.gpu
+def test_evict_with_reference_checkpoint():
+    """Real LKV-H logits and LKV-T scorers from the reference checkpoint drive the device
+    path (reference mode: [k;v] 256 -> 128 -> 1 SiLU per (l,h), floor budgets)."""
+    p = policy_io.load_lkv_params(os.path.join(G, "lkv_params_l2h4d128.bin"))
+    logits = torch.tensor(np.load(os.path.join(G, "head_scores_l2h4d128.npy")), device="cuda")
+    torch.manual_seed(31)
+    L, H, T, D = p.n_layers, p.n_kv_heads, 3000, p.d_head
+    K = torch.randn(1, L, H, T, D, device="cuda").to(torch.bfloat16)
+    V = torch.randn(1, L, H, T, D, device="cuda").to(torch.bfloat16)
+    cache = lkv.DenseCache(K, V, [T])
+    scorers = policy_io.scorers_from_params(p)
+    res = lkv.evict(cache, scorers, logits, 0.15, lkv.BUDGET_FLOOR, keep_scores=True)
+    want_b = O.freeze_budgets(O.allocate_budgets(logits.cpu().numpy(), 0.15), T)
+    assert (res.budgets[0].cpu().numpy() == want_b).all()
+    Kn = K.view(torch.int16).cpu().numpy().view(np.uint16)
+    Vn = V.view(torch.int16).cpu().numpy().view(np.uint16)
+    sc = res.scores.reshape(L * H, T).cpu().numpy()
+    for h in range(L * H):
+        l, kh = divmod(h, H)
+        m = p.token_scorers[h]
+        w1 = scorers.w1[h].double().cpu().numpy()  # bf16-rounded, as on the device
+        ref = O.token_scores(Kn[0, l, kh], Vn[0, l, kh], w1, m.b1, m.w2, act=O.SILU)
+        assert np.max(np.abs(sc[h] - ref)) / np.max(np.abs(ref)) <= 1e-2
+        _, _, pos = res.cache.head(h)
+        assert (pos.cpu().numpy() == O.select_positions_f32(sc[h], int(want_b[h]))).all()
