@@ -8,6 +8,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/lkv_b200.h"
 
 namespace lkv_dev {
@@ -193,6 +195,28 @@ __device__ __forceinline__ bool elect_one() {
         "selp.b32 %0, 1, 0, P;\n\t}"
         : "=r"(pred));
     return pred != 0;
+}
+
+// ---- programmatic dependent launch (PDL) -----------------------------------------------
+// A kernel launched with launch_pdl may be scheduled while its predecessor in the stream is
+// still finishing; pdl_wait() blocks until the predecessor's memory is visible (a no-op for
+// kernels launched normally).  Hides the launch gap between the short select kernels.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 // ---- block-wide helpers -------------------------------------------------------------

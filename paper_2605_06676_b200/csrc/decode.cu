@@ -465,6 +465,7 @@ constexpr int kCombMaxChunks = 8192;  // G * chunks per head (G=4: 2M rows, G=8:
 template <typename T>
 __global__ void __launch_bounds__(kCombThreads) decode_combine_kernel(const __grid_constant__ DecodeParams p,
                                                                       int single_chunk_done) {
+    pdl_wait();
     __shared__ float s_w[kCombMaxChunks];  // [c * G + g] weight exp2(m_c - M_g) / L_g
     __shared__ float s_M[16], s_L[16];
     const int head = blockIdx.x;
@@ -569,7 +570,10 @@ cudaError_t launch_decode(const DecodeParams& p, int dtype, const CUtensorMap* m
         per_sm = max(1, min(per_sm, kDecPerSm));
         const int grid = min(p.max_items, per_sm * num_sms);
         kern<<<grid, kDecThreads, smem, stream>>>(p, *mk, *mv);
-        decode_combine_kernel<__nv_bfloat16><<<dim3(p.n_heads, (p.G * p.head_dim + kCombThreads - 1) / kCombThreads), kCombThreads, 0, stream>>>(p, 1);
+        e = launch_pdl(decode_combine_kernel<__nv_bfloat16>,
+                       dim3(p.n_heads, (p.G * p.head_dim + kCombThreads - 1) / kCombThreads), dim3(kCombThreads), 0,
+                       stream, p, 1);
+        if (e != cudaSuccess) return e;
         note_launches(2);
     } else {
         const size_t smem = ((size_t)p.G * p.head_dim + (size_t)p.G * kDecCh) * sizeof(float);

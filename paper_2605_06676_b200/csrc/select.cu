@@ -110,6 +110,7 @@ __device__ void find_bin_from_top(const uint32_t* cnt /*smem*/, int nbins, uint3
 }
 
 __global__ void __launch_bounds__(1024) select_resolve1_kernel(const __grid_constant__ SelectParams p) {
+    pdl_wait();
     __shared__ uint32_t cnt[2048];
     __shared__ uint32_t s_scan[33];
     __shared__ uint32_t s_bin, s_above;
@@ -145,6 +146,7 @@ __global__ void __launch_bounds__(1024) select_resolve1_kernel(const __grid_cons
 // memory-level parallelism): rows above bin1 are counted, rows inside bin1 are appended
 // to the head's candidate list with one atomic per block.
 __global__ void __launch_bounds__(kSelThreads) select_collect_kernel(const __grid_constant__ SelectParams p) {
+    pdl_wait();
     __shared__ uint32_t s_scan[kSelThreads / 32 + 1];
     __shared__ uint32_t s_base;
     const ChunkInfo ci = decode_chunk(p, blockIdx.x);
@@ -187,6 +189,7 @@ __global__ void __launch_bounds__(kSelThreads) select_collect_kernel(const __gri
 
 // ---- S4 --------------------------------------------------------------------------
 __global__ void __launch_bounds__(1024) select_resolve2_kernel(const __grid_constant__ SelectParams p) {
+    pdl_wait();
     __shared__ uint32_t cnt[2048];
     __shared__ uint32_t c_gt[kMaxChunksPerHead];
     __shared__ uint32_t c_eq[kMaxChunksPerHead];
@@ -300,6 +303,7 @@ __device__ __forceinline__ void gather_rows(const uint4* __restrict__ src, uint4
 #define LKV_EMIT_MINB 1
 #endif
 __global__ void __launch_bounds__(kSelThreads, LKV_EMIT_MINB) select_emit_kernel(const __grid_constant__ SelectParams p) {
+    pdl_wait();
     __shared__ int32_t s_pos[kChunk];
     __shared__ uint32_t s_scan[kSelThreads / 32 + 1];
     const ChunkInfo ci = decode_chunk(p, blockIdx.x);
@@ -410,15 +414,16 @@ cudaError_t launch_select(SelectParams p, int n_heads, cudaStream_t stream) {
     const int chunks = select_total_chunks(p);
     if (chunks == 0) return cudaSuccess;
     if (!p.hist_ready) {
-        cudaError_t e = cudaMemsetAsync(p.hist, 0, sizeof(uint32_t) * 2048 * (size_t)n_heads, stream);
+        const cudaError_t e = cudaMemsetAsync(p.hist, 0, sizeof(uint32_t) * 2048 * (size_t)n_heads, stream);
         if (e != cudaSuccess) return e;
         select_hist_kernel<<<chunks, kSelThreads, 0, stream>>>(p);
         note_launches(1);
     }
-    select_resolve1_kernel<<<n_heads, 1024, 0, stream>>>(p);
-    select_collect_kernel<<<chunks, kSelThreads, 0, stream>>>(p);
-    select_resolve2_kernel<<<n_heads, 1024, 0, stream>>>(p);
-    select_emit_kernel<<<chunks, kSelThreads, 0, stream>>>(p);
+    cudaError_t e;
+    if ((e = launch_pdl(select_resolve1_kernel, dim3(n_heads), dim3(1024), 0, stream, p)) != cudaSuccess) return e;
+    if ((e = launch_pdl(select_collect_kernel, dim3(chunks), dim3(kSelThreads), 0, stream, p)) != cudaSuccess) return e;
+    if ((e = launch_pdl(select_resolve2_kernel, dim3(n_heads), dim3(1024), 0, stream, p)) != cudaSuccess) return e;
+    if ((e = launch_pdl(select_emit_kernel, dim3(chunks), dim3(kSelThreads), 0, stream, p)) != cudaSuccess) return e;
     note_launches(4);
     return cudaGetLastError();
 }
