@@ -202,6 +202,18 @@ lkv_status lkv_evict_host(const lkv_cache_desc* host_cache, void* dev_keys, void
                           int32_t layers_per_chunk, void* workspace, size_t workspace_bytes,
                           lkv_stream_t stream);
 
+/* ---- K/V production for layer-by-layer prefill (the step before the path) -------- */
+/* cos/sin table [t_max][head_dim/2] of float2 (cos, sin) for positions pos_offset + p,
+ * theta = pos * base^(-2j/head_dim) evaluated in fp64 (tensor.cpp:586-623, model.cpp:38-46). */
+lkv_status lkv_rope_table(int32_t t_max, int32_t head_dim, double base, int32_t pos_offset, void* table,
+                          lkv_stream_t stream);
+/* One layer's projections, token-major [n_seq][max_tokens][n_kv_heads * head_dim] (the K/V
+ * GEMM outputs) -> the dense head-major layer [n_seq][n_kv_heads][max_tokens][head_dim] that
+ * lkv_score / lkv_select read, K rotated pairwise with `table` (V copied).  `layer` gives the
+ * shape (n_layers must be 1); k_out / v_out receive the dense layer. */
+lkv_status lkv_rope_pack(const void* k_lin, const void* v_lin, const lkv_cache_desc* layer, const void* table,
+                         void* k_out, void* v_out, lkv_stream_t stream);
+
 /* ---- K5: decode over the ragged cache ------------------------------------------- */
 /* lkv_decode_plan splits every head's capacity into 256-row work items (once
  * per eviction, after offsets are final).  lkv_decode_step then runs one decode

@@ -24,7 +24,7 @@ MAX_SEQ = 256
 EXPORTED = [
     "lkv_abi_version", "lkv_launch_count", "lkv_last_error", "lkv_status_name", "lkv_device_check", "lkv_workspace_bytes",
     "lkv_workspace_init", "lkv_workspace_status", "lkv_ragged_capacity", "lkv_budgets", "lkv_freeze_budgets", "lkv_ragged_offsets",
-    "lkv_score", "lkv_select", "lkv_compact", "lkv_evict", "lkv_evict_host", "lkv_decode_workspace_bytes", "lkv_decode_plan",
+    "lkv_score", "lkv_select", "lkv_compact", "lkv_evict", "lkv_evict_host", "lkv_rope_table", "lkv_rope_pack", "lkv_decode_workspace_bytes", "lkv_decode_plan",
     "lkv_decode_step",
 ]
 
@@ -82,12 +82,14 @@ def load():
     L.lkv_evict.argtypes = [P(CacheDesc), P(ScorerDesc), vp, dbl, i32, P(RaggedDesc), vp, vp, vp, vp, sz, vp]
     L.lkv_evict_host.argtypes = [P(CacheDesc), vp, vp, P(ScorerDesc), vp, dbl, i32, P(RaggedDesc), P(RaggedDesc), i32,
                                  vp, sz, vp]
+    L.lkv_rope_table.argtypes = [i32, i32, dbl, i32, vp, vp]
+    L.lkv_rope_pack.argtypes = [vp, vp, P(CacheDesc), vp, vp, vp, vp]
     L.lkv_decode_workspace_bytes.restype = sz
     L.lkv_decode_workspace_bytes.argtypes = [P(RaggedDesc), i32]
     L.lkv_decode_plan.argtypes = [P(RaggedDesc), vp, sz, vp]
     L.lkv_decode_step.argtypes = [P(RaggedDesc), i32, i32, i32, i32, vp, vp, vp, vp, vp, dbl, vp, sz, vp]
     for name in ["lkv_workspace_init", "lkv_workspace_status", "lkv_budgets", "lkv_freeze_budgets", "lkv_ragged_offsets", "lkv_score",
-                 "lkv_select", "lkv_compact", "lkv_evict", "lkv_evict_host", "lkv_decode_plan", "lkv_decode_step"]:
+                 "lkv_select", "lkv_compact", "lkv_evict", "lkv_evict_host", "lkv_rope_table", "lkv_rope_pack", "lkv_decode_plan", "lkv_decode_step"]:
         getattr(L, name).restype = C.c_int
     _lib = L
     return L

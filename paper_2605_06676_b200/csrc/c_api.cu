@@ -659,6 +659,31 @@ lkv_status lkv_evict_host(const lkv_cache_desc* hc, void* dev_keys, void* dev_va
     return LKV_OK;
 }
 
+lkv_status lkv_rope_table(int32_t t_max, int32_t head_dim, double base, int32_t pos_offset, void* table,
+                          lkv_stream_t stream) {
+    if (t_max < 1 || head_dim < 2 || head_dim % 2 || !(base > 0.0) || pos_offset < 0 || !table)
+        return fail(LKV_ERR_CONTRACT, "rope: bad table arguments (head_dim must be even)");  // tensor.cpp:588
+    LKV_CUDA(launch_rope_table(t_max, head_dim, base, pos_offset, static_cast<float2*>(table), (cudaStream_t)stream),
+             "rope table");
+    return LKV_OK;
+}
+
+lkv_status lkv_rope_pack(const void* k_lin, const void* v_lin, const lkv_cache_desc* layer, const void* table,
+                         void* k_out, void* v_out, lkv_stream_t stream) {
+    lkv_status st = check_cache(layer, false);
+    if (st) return st;
+    if (layer->n_layers != 1) return fail(LKV_ERR_CONTRACT, "rope_pack: one layer per call");
+    if (!k_lin || !v_lin || !table || !k_out || !v_out) return fail(LKV_ERR_CONTRACT, "rope_pack: null buffer");
+    if ((reinterpret_cast<uintptr_t>(k_lin) | reinterpret_cast<uintptr_t>(v_lin) | reinterpret_cast<uintptr_t>(k_out) |
+         reinterpret_cast<uintptr_t>(v_out)) & 15)
+        return fail(LKV_ERR_CONTRACT, "rope_pack: buffers must be 16-byte aligned");
+    LKV_CUDA(launch_rope_pack(k_lin, v_lin, layer->n_seq, (int)layer->max_tokens, layer->seq_lens, layer->n_kv_heads,
+                              layer->head_dim, layer->dtype, static_cast<const float2*>(table), k_out, v_out,
+                              (cudaStream_t)stream),
+             "rope pack");
+    return LKV_OK;
+}
+
 size_t lkv_decode_workspace_bytes(const lkv_ragged_desc* r, int32_t G) {
     if (!r || G < 1) return 0;
     return decode_layout(r, G).total;

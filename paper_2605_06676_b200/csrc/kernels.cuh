@@ -116,4 +116,8 @@ cudaError_t launch_decode_plan(const int64_t* offsets, int n_heads, DecodeItem* 
                                int32_t* n_items, cudaStream_t stream);
 cudaError_t launch_decode(const DecodeParams& p, int dtype, const CUtensorMap* mk, const CUtensorMap* mv, int num_sms,
                           cudaStream_t stream);
+// ---- rope.cu (layer-by-layer prefill: K/V production)
+cudaError_t launch_rope_table(int t_max, int head_dim, double base, int pos_offset, float2* cs, cudaStream_t stream);
+cudaError_t launch_rope_pack(const void* k_lin, const void* v_lin, int n_seq, int t_max, const int32_t* seq_lens,
+                             int H, int D, int dtype, const float2* cs, void* k_out, void* v_out, cudaStream_t stream);
 }  // namespace lkv_dev

@@ -603,3 +603,62 @@ def test_config3_full_size_properties(ratio):
         assert torch.equal(res.cache.values[offs[h]:offs[h] + bh], Vd[h][p])
         if h % 61 == 0:
             assert (p.cpu().numpy() == O.select_positions_f32(scores[h].cpu().numpy(), bh)).all()
+
+
+# ---------------------------------------------------------------------------------------------
+# layer-by-layer prefill
+# ---------------------------------------------------------------------------------------------
+def test_rope_pack_matches_fp64_rope():  # tensor.cpp:586-623 convention, absolute positions
+    from paper_2605_06676_b200 import prefill
+
+    torch.manual_seed(41)
+    S, T, H, D = 2, 600, 3, 128
+    for dtype, tol in ((torch.float32, 1e-5), (torch.bfloat16, 1e-2)):
+        k_lin = torch.randn(S, T, H * D, device=DEV).to(dtype)
+        v_lin = torch.randn(S, T, H * D, device=DEV).to(dtype)
+        tab = prefill.rope_table(T, D)
+        k, v = prefill.rope_pack(k_lin, v_lin, tab, [T, 450], H)
+        kl = k_lin.double().cpu().numpy().reshape(S, T, H, D)
+        pos = np.arange(T)[:, None]
+        freq = 10000.0 ** (-2.0 * np.arange(D // 2) / D)
+        th = pos * freq[None, :]
+        a, b = kl[..., 0::2], kl[..., 1::2]
+        want = np.empty_like(kl)
+        want[..., 0::2] = a * np.cos(th)[None, :, None, :] - b * np.sin(th)[None, :, None, :]
+        want[..., 1::2] = a * np.sin(th)[None, :, None, :] + b * np.cos(th)[None, :, None, :]
+        got = k.double().cpu().numpy()[:, 0].transpose(0, 2, 1, 3)
+        assert rel_gap(got[0], want[0]) <= tol and rel_gap(got[1, :450], want[1, :450]) <= tol
+        assert torch.equal(v[:, 0].transpose(1, 2).reshape(S, T, H * D)[1, :450], v_lin[1, :450])
+
+
+def test_layerwise_prefill_equals_one_shot_eviction():
+    """Per-layer rope + score + select into one ragged cache == one lkv_evict over the whole
+    dense cache; peak KV = one dense layer + the compressed earlier layers (evictsim.cpp:157-159)."""
+    from paper_2605_06676_b200 import prefill
+
+    torch.manual_seed(43)
+    S, L, H, D, T, dm = 2, 3, 4, 128, 3000, 256
+    cfg = synth.CONFIGS[2]
+    lens = [T, 2100]
+    x = torch.randn(S, T, dm, device=DEV).to(torch.bfloat16)
+    wk = [(torch.randn(dm, H * D, device=DEV) / dm ** 0.5).to(torch.bfloat16) for _ in range(L)]
+    wv = [(torch.randn(dm, H * D, device=DEV) / dm ** 0.5).to(torch.bfloat16) for _ in range(L)]
+    w1 = (torch.randn(L, D, 64, device=DEV) * 0.05).to(torch.bfloat16)
+    scorers = lkv.Scorers(w1, torch.zeros(L, 64, device=DEV), torch.randn(L, 64, device=DEV) * 0.05)
+    logits = torch.randn(L * H, dtype=torch.float64, device=DEV)
+    pf = prefill.LayerwisePrefill(S, L, H, D, T, lens, scorers, logits, 0.2, lkv.BUDGET_EXACT, decode_slack=3)
+    K = torch.empty(S, L, H, T, D, dtype=torch.bfloat16, device=DEV)
+    V = torch.empty_like(K)
+    for l in range(L):
+        k_lin, v_lin = x @ wk[l], x @ wv[l]          # cuBLAS projections
+        pf.ingest_layer(l, k_lin, v_lin)
+        K[:, l], V[:, l] = (t[:, 0] for t in prefill.rope_pack(k_lin, v_lin, pf.table, lens, H))
+    rc = pf.finish()
+    ref = lkv.evict(lkv.DenseCache(K, V, lens), scorers, logits, 0.2, lkv.BUDGET_EXACT, decode_slack=3)
+    assert torch.equal(rc.offsets, ref.cache.offsets) and torch.equal(rc.lens, ref.cache.lens)
+    for h in range(S * L * H):
+        a, b = rc.head(h), ref.cache.head(h)
+        assert all(torch.equal(u, w) for u, w in zip(a, b)), h
+    dense_layer = 2 * S * H * T * D * 2
+    compressed_before_last = int(ref.budgets.reshape(S, L, H)[:, :L - 1].sum()) * 2 * D * 2
+    assert pf.peak_kv_bytes == dense_layer + compressed_before_last
