@@ -10,9 +10,11 @@ Two libraries back it:
 * ``oracle/liblkv_oracle.so`` -- the fp64 plain-C restatement (``lkv_oracle.c``),
   each function citing the reference file:line it follows;
 * ``oracle/_ref/liblkv_ref.so`` (optional) -- the reference's own
-  ``proj/src/soft_topk.cpp`` and ``proj/src/policy.cpp`` compiled unmodified from
-  ``/root/reference`` over a tensor shim (``oracle/ref_shim``), used to pin the
-  restatement bit-for-bit.  Built only where ``/root/reference`` exists.
+  ``proj/src/{tensor,attention,model,soft_topk,policy,evictsim,...}.cpp`` compiled
+  unmodified from ``/root/reference`` (Eigen, absent here, replaced by our own minimal
+  compat header ``oracle/ref_shim/eigen``), used to pin the restatement.  Built only
+  where ``/root/reference`` exists.
+* ``oracle/model.py`` -- fp64 numpy restatement of the toy model's decode step.
 """
 from __future__ import annotations
 

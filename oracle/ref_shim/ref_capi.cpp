@@ -8,8 +8,11 @@
 #include <span>
 #include <vector>
 
+#include <string>
+
 #include "lkv/checkpoint.hpp"
 #include "lkv/errors.hpp"
+#include "lkv/model.hpp"
 #include "lkv/policy.hpp"
 #include "lkv/soft_topk.hpp"
 
@@ -121,6 +124,106 @@ int ref_head_scores(const char* path, double* out, int n) {
         lkv::Tensor s = lkv::head_scores(p);
         if ((int)s.numel() != n) throw lkv::contract_error("ref_head_scores: size");
         std::memcpy(out, s.data(), sizeof(double) * (size_t)n);
+    });
+}
+
+// ---- toy GQA model (model.cpp): init_model, named_params, forward_full, decode_step -------------
+// A handle owns one lkv::ModelWeights built by the reference's init_model (model.cpp:173-198).
+void* ref_model_create(int n_layers, int n_query_heads, int n_kv_heads, int head_dim, int vocab_size,
+                       int max_seq_len, int mlp_hidden, unsigned long long seed) {
+    lkv::ModelWeights* w = nullptr;
+    guarded([&] {
+        lkv::ModelConfig c;
+        c.n_layers = n_layers;
+        c.n_query_heads = n_query_heads;
+        c.n_kv_heads = n_kv_heads;
+        c.head_dim = head_dim;
+        c.vocab_size = vocab_size;
+        c.max_seq_len = max_seq_len;
+        c.mlp_hidden = mlp_hidden;
+        c.rng_seed = seed;
+        w = new lkv::ModelWeights(lkv::init_model(c));
+    });
+    return w;
+}
+
+void ref_model_free(void* h) { delete static_cast<lkv::ModelWeights*>(h); }
+
+static lkv::Tensor* find_param(void* h, const char* name) {
+    for (auto& [n, t] : static_cast<lkv::ModelWeights*>(h)->named_params())
+        if (n == name) return t;
+    throw lkv::contract_error(std::string("no parameter ") + name);
+}
+
+// numel of a named parameter (model.cpp:142-163 names), or -1
+long ref_model_param_numel(void* h, const char* name) {
+    long n = -1;
+    guarded([&] { n = (long)find_param(h, name)->numel(); });
+    return n;
+}
+
+int ref_model_get(void* h, const char* name, double* out, long n) {
+    return guarded([&] {
+        lkv::Tensor* t = find_param(h, name);
+        if ((long)t->numel() != n) throw lkv::contract_error("ref_model_get: size");
+        std::memcpy(out, t->data(), sizeof(double) * (size_t)n);
+    });
+}
+
+int ref_model_set(void* h, const char* name, const double* in, long n) {
+    return guarded([&] {
+        lkv::Tensor* t = find_param(h, name);
+        if ((long)t->numel() != n) throw lkv::contract_error("ref_model_set: size");
+        *t = lkv::Tensor::from(t->shape(), std::vector<double>(in, in + n));
+    });
+}
+
+// forward_full (model.cpp:199-201): logits [t x vocab]; keys/values [L*H][t][d] (rotary applied)
+int ref_forward_full(void* h, const int32_t* tokens, int t, double* logits, double* keys, double* values) {
+    return guarded([&] {
+        const lkv::ModelWeights& w = *static_cast<lkv::ModelWeights*>(h);
+        lkv::ForwardTrace tr = lkv::forward_full(w, std::vector<int>(tokens, tokens + t));
+        std::memcpy(logits, tr.logits.data(), sizeof(double) * tr.logits.numel());
+        size_t o = 0;
+        for (size_t i = 0; i < tr.keys.size(); ++i) {
+            std::memcpy(keys + o, tr.keys[i].data(), sizeof(double) * tr.keys[i].numel());
+            std::memcpy(values + o, tr.values[i].data(), sizeof(double) * tr.values[i].numel());
+            o += tr.keys[i].numel();
+        }
+    });
+}
+
+// decode_step (model.cpp:209-287) run n_steps times on a cache built from arrays:
+// head i (layer-major l*H+h) holds lens[i] rows at row offset row_off[i] of keys/values
+// [rows][d] and positions[rows].  Outputs: logits [n_steps][vocab]; the rows each step
+// appended, new_k/new_v [n_steps][L*H][d]; final tokens_seen.
+int ref_decode_steps(void* h, const int32_t* lens, const int64_t* row_off, const double* keys,
+                     const double* values, const int32_t* positions, int tokens_seen, const int32_t* tokens,
+                     int n_steps, double* logits, double* new_k, double* new_v, int32_t* tokens_seen_out) {
+    return guarded([&] {
+        const lkv::ModelWeights& w = *static_cast<lkv::ModelWeights*>(h);
+        const lkv::ModelConfig& c = w.config;
+        const int d = c.head_dim, n = c.total_kv_heads();
+        lkv::KvCache cache = lkv::make_cache(c);
+        cache.tokens_seen = tokens_seen;
+        for (int i = 0; i < n; ++i) {
+            lkv::HeadCache& hc = cache.heads[(size_t)i];
+            const size_t r0 = (size_t)row_off[i], r = (size_t)lens[i];
+            hc.keys.assign(keys + r0 * d, keys + (r0 + r) * d);
+            hc.values.assign(values + r0 * d, values + (r0 + r) * d);
+            hc.retained_positions.assign(positions + r0, positions + r0 + r);
+        }
+        for (int s = 0; s < n_steps; ++s) {
+            std::vector<double> lg = lkv::decode_step(w, cache, tokens[s]);
+            std::memcpy(logits + (size_t)s * c.vocab_size, lg.data(), sizeof(double) * lg.size());
+            for (int i = 0; i < n; ++i) {
+                const lkv::HeadCache& hc = cache.heads[(size_t)i];
+                const size_t last = (size_t)hc.retained() - 1;
+                std::memcpy(new_k + ((size_t)s * n + i) * d, hc.keys.data() + last * d, sizeof(double) * d);
+                std::memcpy(new_v + ((size_t)s * n + i) * d, hc.values.data() + last * d, sizeof(double) * d);
+            }
+        }
+        *tokens_seen_out = cache.tokens_seen;
     });
 }
 

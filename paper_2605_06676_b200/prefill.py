@@ -55,6 +55,7 @@ class LayerwisePrefill:
         self.dense_layer_bytes = 2 * self.k_layer.numel() * self.k_layer.element_size()
         self.peak_kv_bytes = 0
         self._ingested = 0
+        self._budget_prefix = None
         s = _stream()
         lens_c = (C.c_int32 * n_seq)(*self.seq_lens)
         _check(lib().lkv_rope_table(max_tokens, head_dim, float(rope_base), 0, _ptr(self.table), s))
@@ -93,7 +94,10 @@ class LayerwisePrefill:
             _check(lib().lkv_select(C.byref(cd), _ptr(self.scores), _ptr(b), C.byref(rd), 1, C.c_void_p(self._ws.ptr),
                                     self._ws.nbytes, s))
         self._ingested += 1
-        compressed = int(self.budgets[:, :l * H].sum().item()) * 2 * D * self.k_layer.element_size()
+        if self._budget_prefix is None:  # one host read of the budgets, for the peak accounting only
+            per_layer = self.budgets.reshape(S, self.L, H).sum(dim=(0, 2)).cpu().tolist()
+            self._budget_prefix = [sum(per_layer[:i]) for i in range(self.L + 1)]
+        compressed = self._budget_prefix[l] * 2 * D * self.k_layer.element_size()
         self.peak_kv_bytes = max(self.peak_kv_bytes, compressed + self.dense_layer_bytes)
 
     def finish(self) -> RaggedCache:

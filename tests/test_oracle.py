@@ -374,3 +374,58 @@ def test_reference_mode_scorer_vs_reference():
                          b1.ctypes.data_as(O._dp), w2.ctypes.data_as(O._dp), hid, out_ref2.ctypes.data_as(O._dp))
     mine = O.token_scores(k32, v32, w1, b1, w2, act=O.SILU)
     assert np.max(np.abs(mine - out_ref2)) <= 1e-13 * max(1.0, np.max(np.abs(out_ref2)))
+
+
+# ---------------------------------------------------------------------------------------------
+# toy GQA model decode step: numpy restatement vs the reference's model.cpp
+# ---------------------------------------------------------------------------------------------
+from oracle import model as OM  # noqa: E402
+
+
+def _trace_cache(cfg, K, V, rng, keep=0.6):
+    heads = []
+    t = K.shape[1]
+    for i in range(cfg.total_kv_heads):
+        m = rng.random(t) < keep
+        idx = np.nonzero(m)[0]
+        heads.append(OM.HeadCache(K[i][idx].copy(), V[i][idx].copy(), idx.astype(np.int32)))
+    return heads
+
+
+@needs_ref
+def test_model_oracle_matches_reference_model_cpp():
+    cfg = OM.ModelConfig(n_layers=3, n_query_heads=8, n_kv_heads=2, head_dim=16, vocab_size=97, max_seq_len=64)
+    R = OM.RefModel(cfg)
+    P = R.params()                                   # the reference's own init_model weights
+    P["layers.1.attn_norm"] = 1.0 + 0.1 * np.random.default_rng(3).standard_normal(cfg.d_model)
+    R.set_params(P)
+    toks = np.random.default_rng(4).integers(0, cfg.vocab_size, 20)
+    lr, kr, vr = R.forward_full(toks)
+    lo, ko, vo = OM.forward_full(cfg, P, toks)
+    assert np.abs(lo - lr).max() <= 1e-12 * np.abs(lr).max()
+    assert np.abs(ko - kr).max() <= 1e-12 and np.abs(vo - vr).max() <= 1e-12
+    heads = _trace_cache(cfg, kr, vr, np.random.default_rng(5))
+    steps = [7, 0, 96]
+    lref, nk, nv, ts = R.decode_steps(heads, 20, steps)
+    mine = [OM.HeadCache(h.keys.copy(), h.values.copy(), h.positions.copy()) for h in heads]
+    seen = 20
+    for s, tok in enumerate(steps):
+        lg, seen = OM.decode_step(cfg, P, mine, seen, tok)
+        assert np.abs(lg - lref[s]).max() <= 1e-12 * np.abs(lref[s]).max(), s
+        for i, hc in enumerate(mine):
+            assert np.abs(hc.keys[-1] - nk[s, i]).max() <= 1e-12 and np.abs(hc.values[-1] - nv[s, i]).max() <= 1e-12
+            assert hc.positions[-1] == 20 + s
+    assert seen == ts == 23
+
+
+def test_model_oracle_prefill_then_decode_equals_one_shot():
+    """test_model.cpp:101-115: decoding token t over the full prefix cache reproduces the full
+    forward's last row (<= 1e-10)."""
+    cfg = OM.ModelConfig(n_layers=2, n_query_heads=4, n_kv_heads=2, head_dim=8, vocab_size=50, max_seq_len=32)
+    P = OM.random_params(cfg, 11, gain=0.2)
+    toks = np.random.default_rng(12).integers(0, cfg.vocab_size, 12)
+    full, _, _ = OM.forward_full(cfg, P, toks)
+    _, K, V = OM.forward_full(cfg, P, toks[:-1])
+    heads = [OM.HeadCache(K[i].copy(), V[i].copy(), np.arange(11, dtype=np.int32)) for i in range(cfg.total_kv_heads)]
+    lg, seen = OM.decode_step(cfg, P, heads, 11, int(toks[-1]))
+    assert seen == 12 and np.abs(lg - full[-1]).max() <= 1e-10
