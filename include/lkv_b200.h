@@ -19,6 +19,8 @@
  *   lkv_evict_host  <- the same, for a cache resident in (pinned) host memory
  *   lkv_decode_step <- decode_step's append + attention block (model.hpp:95,
  *                      model.cpp:240-265) -> masked_attention_dense (attention.hpp:57)
+ *   lkv_model_*     <- the whole decode_step (model.hpp:95, model.cpp:209-287):
+ *                      projections, RoPE at tokens_seen, attention, SwiGLU MLP, logits
  *
  * Status codes map 1:1 onto the reference's exception types
  * (proj/include/lkv/errors.hpp:10-32); lkv_last_error() returns a thread-local
@@ -232,6 +234,52 @@ lkv_status lkv_decode_step(const lkv_ragged_desc* cache, int32_t n_seq, int32_t 
                            int32_t n_kv_heads, int32_t n_q_heads, const void* q, const void* new_k,
                            const void* new_v, int32_t* tokens_seen, void* out, double scale,
                            void* workspace, size_t workspace_bytes, lkv_stream_t stream);
+
+/* ---- full decode step of the reference's toy GQA model --------------------
+ * Replaces decode_step (model.hpp:95, model.cpp:209-287) for a batch of n_seq <= 16 sequences
+ * whose compacted caches live in one ragged cache (flat head (s * L + l) * H + h).  Weights are
+ * the reference's ModelWeights (model.hpp:35-47) in the reference layout (x W, row-major
+ * [rows][cols]), repacked once into a library-owned blob by lkv_model_load_param:
+ *   LKV_P_TOK_EMBED [vocab][dm], WQ [dm][dm], WK/WV [dm][H*d], WO [dm][dm], ATTN_NORM/MLP_NORM [dm],
+ *   W_GATE/W_UP [dm][mlp_width], W_DOWN [mlp_width][dm], FINAL_NORM [dm], LM_HEAD [dm][vocab]
+ * (dm = n_q_heads * head_dim), each in the model dtype.  The blob must be zero-filled before the
+ * first load.  lkv_model_plan (after every eviction / change of the cache's offsets) plans the
+ * per-layer decode attention and builds the RoPE table; lkv_model_decode_step then runs one
+ * step: tokens [n_seq] and tokens_seen [n_seq] are device int32, logits [n_seq][vocab] fp32.
+ * Token / position range errors are latched (lkv_workspace_status -> LKV_ERR_CONTRACT). */
+typedef struct lkv_model_desc {
+    int32_t n_layers, n_q_heads, n_kv_heads, head_dim, vocab_size, max_seq_len, mlp_width, dtype;
+    double rope_base; /* 10000 (model.cpp:38) */
+    double norm_eps;  /* 1e-6 (model.cpp:48) */
+} lkv_model_desc;
+
+enum {
+    LKV_P_TOK_EMBED = 0,
+    LKV_P_WQ = 1,
+    LKV_P_WK = 2,
+    LKV_P_WV = 3,
+    LKV_P_WO = 4,
+    LKV_P_ATTN_NORM = 5,
+    LKV_P_MLP_NORM = 6,
+    LKV_P_W_GATE = 7,
+    LKV_P_W_UP = 8,
+    LKV_P_W_DOWN = 9,
+    LKV_P_FINAL_NORM = 10,
+    LKV_P_LM_HEAD = 11
+};
+
+#define LKV_MODEL_MAX_SEQ 16
+
+lkv_status lkv_model_validate(const lkv_model_desc* model); /* ModelConfig::validate, model.cpp:124-133 */
+size_t lkv_model_weights_bytes(const lkv_model_desc* model);
+lkv_status lkv_model_load_param(const lkv_model_desc* model, void* weights, int32_t param, int32_t layer,
+                                const void* src, lkv_stream_t stream);
+size_t lkv_model_workspace_bytes(const lkv_model_desc* model, int32_t n_seq, const lkv_ragged_desc* cache);
+lkv_status lkv_model_plan(const lkv_model_desc* model, const lkv_ragged_desc* cache, int32_t n_seq, void* workspace,
+                          size_t workspace_bytes, lkv_stream_t stream);
+lkv_status lkv_model_decode_step(const lkv_model_desc* model, const void* weights, const lkv_ragged_desc* cache,
+                                 int32_t n_seq, const int32_t* tokens, int32_t* tokens_seen, float* logits,
+                                 void* workspace, size_t workspace_bytes, lkv_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -25,7 +25,8 @@ EXPORTED = [
     "lkv_abi_version", "lkv_launch_count", "lkv_last_error", "lkv_status_name", "lkv_device_check", "lkv_workspace_bytes",
     "lkv_workspace_init", "lkv_workspace_status", "lkv_ragged_capacity", "lkv_budgets", "lkv_freeze_budgets", "lkv_ragged_offsets",
     "lkv_score", "lkv_select", "lkv_compact", "lkv_evict", "lkv_evict_host", "lkv_rope_table", "lkv_rope_pack", "lkv_decode_workspace_bytes", "lkv_decode_plan",
-    "lkv_decode_step",
+    "lkv_decode_step", "lkv_model_validate", "lkv_model_weights_bytes", "lkv_model_load_param", "lkv_model_workspace_bytes", "lkv_model_plan",
+    "lkv_model_decode_step",
 ]
 
 
@@ -46,6 +47,16 @@ class RaggedDesc(C.Structure):
                 ("capacity_rows", C.c_int64), ("offsets", C.c_void_p), ("lens", C.c_void_p), ("keys", C.c_void_p),
                 ("values", C.c_void_p), ("positions", C.c_void_p)]
 
+
+class ModelDesc(C.Structure):
+    _fields_ = [("n_layers", C.c_int32), ("n_q_heads", C.c_int32), ("n_kv_heads", C.c_int32), ("head_dim", C.c_int32),
+                ("vocab_size", C.c_int32), ("max_seq_len", C.c_int32), ("mlp_width", C.c_int32), ("dtype", C.c_int32),
+                ("rope_base", C.c_double), ("norm_eps", C.c_double)]
+
+
+(P_TOK_EMBED, P_WQ, P_WK, P_WV, P_WO, P_ATTN_NORM, P_MLP_NORM, P_W_GATE, P_W_UP, P_W_DOWN, P_FINAL_NORM,
+ P_LM_HEAD) = range(12)
+MODEL_MAX_SEQ = 16
 
 _lib = None
 
@@ -88,8 +99,17 @@ def load():
     L.lkv_decode_workspace_bytes.argtypes = [P(RaggedDesc), i32]
     L.lkv_decode_plan.argtypes = [P(RaggedDesc), vp, sz, vp]
     L.lkv_decode_step.argtypes = [P(RaggedDesc), i32, i32, i32, i32, vp, vp, vp, vp, vp, dbl, vp, sz, vp]
+    L.lkv_model_validate.argtypes = [P(ModelDesc)]
+    L.lkv_model_weights_bytes.restype = sz
+    L.lkv_model_weights_bytes.argtypes = [P(ModelDesc)]
+    L.lkv_model_load_param.argtypes = [P(ModelDesc), vp, i32, i32, vp, vp]
+    L.lkv_model_workspace_bytes.restype = sz
+    L.lkv_model_workspace_bytes.argtypes = [P(ModelDesc), i32, P(RaggedDesc)]
+    L.lkv_model_plan.argtypes = [P(ModelDesc), P(RaggedDesc), i32, vp, sz, vp]
+    L.lkv_model_decode_step.argtypes = [P(ModelDesc), vp, P(RaggedDesc), i32, vp, vp, vp, vp, sz, vp]
     for name in ["lkv_workspace_init", "lkv_workspace_status", "lkv_budgets", "lkv_freeze_budgets", "lkv_ragged_offsets", "lkv_score",
-                 "lkv_select", "lkv_compact", "lkv_evict", "lkv_evict_host", "lkv_rope_table", "lkv_rope_pack", "lkv_decode_plan", "lkv_decode_step"]:
+                 "lkv_select", "lkv_compact", "lkv_evict", "lkv_evict_host", "lkv_rope_table", "lkv_rope_pack", "lkv_decode_plan", "lkv_decode_step",
+                 "lkv_model_validate", "lkv_model_load_param", "lkv_model_plan", "lkv_model_decode_step"]:
         getattr(L, name).restype = C.c_int
     _lib = L
     return L

@@ -7,6 +7,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -282,7 +283,7 @@ lkv_status run_select(const lkv_cache_desc* c, const float* scores, const int32_
 
 // ---- decode workspace -------------------------------------------------------------------------------
 struct DecodeWs {
-    size_t err, n_items, item_base, items, part_m, part_l, part_o, total;
+    size_t err, n_items, layer_begin, item_base, items, part_m, part_l, part_o, total;
     int64_t max_items;
 };
 DecodeWs decode_layout(const lkv_ragged_desc* r, int G) {
@@ -293,6 +294,8 @@ DecodeWs decode_layout(const lkv_ragged_desc* r, int G) {
     o = align_up(o + sizeof(ErrWord));
     w.n_items = o;
     o = align_up(o + sizeof(int32_t));
+    w.layer_begin = o;  // [n_layers + 1] of the plan (n_layers <= n_heads)
+    o = align_up(o + sizeof(int32_t) * ((size_t)r->n_heads + 1));
     w.item_base = o;
     o = align_up(o + sizeof(int32_t) * (size_t)r->n_heads);
     w.items = o;
@@ -694,8 +697,8 @@ lkv_status lkv_decode_plan(const lkv_ragged_desc* r, void* ws, size_t ws_bytes, 
     const DecodeWs w = decode_layout(r, 1);
     lkv_status st = check_ws(ws, ws_bytes, w.items + sizeof(DecodeItem) * (size_t)w.max_items);
     if (st) return st;
-    LKV_CUDA(launch_decode_plan(r->offsets, r->n_heads, at<DecodeItem>(ws, w.items), at<int32_t>(ws, w.item_base),
-                                at<int32_t>(ws, w.n_items), (cudaStream_t)stream),
+    LKV_CUDA(launch_decode_plan(r->offsets, r->n_heads, 1, 1, at<DecodeItem>(ws, w.items), at<int32_t>(ws, w.item_base),
+                                at<int32_t>(ws, w.layer_begin), at<int32_t>(ws, w.n_items), (cudaStream_t)stream),
              "decode plan");
     return LKV_OK;
 }
@@ -725,7 +728,13 @@ lkv_status lkv_decode_step(const lkv_ragged_desc* r, int32_t n_seq, int32_t n_la
     p.n_q_heads = n_q_heads;
     p.G = G;
     p.head_dim = r->head_dim;
-    p.n_items = at<int32_t>(ws, w.n_items);
+    p.n_seq = n_seq;
+    p.n_layers = n_layers;
+    p.layer0 = 0;
+    p.q_layers = n_layers;
+    p.item_lo = at<int32_t>(ws, w.layer_begin);  // layer_begin[0] == 0 for every plan
+    p.item_hi = at<int32_t>(ws, w.n_items);
+    p.out_nbt = 0;
     p.max_items = (int32_t)w.max_items;
     p.scale_log2 = (float)(scale * 1.4426950408889634);
     p.offsets = r->offsets;
@@ -737,7 +746,6 @@ lkv_status lkv_decode_step(const lkv_ragged_desc* r, int32_t n_seq, int32_t n_la
     p.new_k = new_k;
     p.new_v = new_v;
     p.tokens_seen = tokens_seen;
-    p.heads_per_seq = n_layers * n_kv_heads;
     p.out = out;
     p.items = at<DecodeItem>(ws, w.items);
     p.item_base = at<int32_t>(ws, w.item_base);
@@ -751,6 +759,330 @@ lkv_status lkv_decode_step(const lkv_ragged_desc* r, int32_t n_seq, int32_t n_la
         if ((st = make_map_bf16(&mv, r->values, 128, (uint64_t)r->capacity_rows, 64))) return st;
     }
     LKV_CUDA(launch_decode(p, r->dtype, &mk, &mv, num_sms(), (cudaStream_t)stream), "decode");
+    return LKV_OK;
+}
+
+}  // extern "C"
+
+// ============================ full model decode step ============================
+namespace {
+
+struct MatGeom {
+    int N, K, NG, KU;
+    size_t bytes;
+};
+MatGeom mat_geom(int n_virt, int K, int dtype) {
+    MatGeom m;
+    m.N = n_virt;
+    m.K = K;
+    m.NG = (n_virt + 63) / 64;
+    m.KU = (K + 127) / 128;
+    m.bytes = dtype == LKV_BF16 ? (size_t)m.NG * m.KU * 16384 : (size_t)K * m.NG * 64 * 4;
+    return m;
+}
+
+struct ModelGeom {
+    int dm, dkv, ff, D, L, Hq, H, vocab, dtype;
+    size_t esz;
+    MatGeom qkv, wo, gu, down, lm;
+    size_t tok_embed, final_norm, lm_head, layer0, layer_stride;
+    size_t o_qkv, o_wo, o_gu, o_down, o_attn_norm, o_mlp_norm, total;
+};
+
+lkv_status check_model(const lkv_model_desc* m) {
+    if (!m) return fail(LKV_ERR_CONTRACT, "model descriptor is null");
+    if (m->n_layers < 1 || m->n_q_heads < 1 || m->n_kv_heads < 1 || m->head_dim < 1 || m->vocab_size < 1 ||
+        m->max_seq_len < 1 || m->mlp_width < 1)
+        return fail(LKV_ERR_CONTRACT, "model config: extents must be >= 1");  // model.cpp:126-129
+    if (m->n_q_heads % m->n_kv_heads) return fail(LKV_ERR_CONTRACT, "model config: n_query_heads must divide by n_kv_heads");
+    if (m->head_dim % 2) return fail(LKV_ERR_CONTRACT, "model config: head_dim must be even for rotary pairs");
+    if (m->dtype != LKV_BF16 && m->dtype != LKV_F32) return fail(LKV_ERR_CONTRACT, "model dtype must be F32 or BF16");
+    if (!(m->rope_base > 0.0) || !(m->norm_eps > 0.0)) return fail(LKV_ERR_CONTRACT, "model: rope_base and norm_eps must be > 0");
+    if (m->dtype == LKV_BF16 && (m->head_dim != 128 || m->n_q_heads / m->n_kv_heads > 16))
+        return fail(LKV_ERR_UNSUPPORTED, "bf16 model decode needs head_dim 128 and group size <= 16");
+    return LKV_OK;
+}
+
+ModelGeom model_geom(const lkv_model_desc* m) {
+    ModelGeom g;
+    g.D = m->head_dim;
+    g.L = m->n_layers;
+    g.Hq = m->n_q_heads;
+    g.H = m->n_kv_heads;
+    g.dm = g.Hq * g.D;
+    g.dkv = g.H * g.D;
+    g.ff = m->mlp_width;
+    g.vocab = m->vocab_size;
+    g.dtype = m->dtype;
+    g.esz = m->dtype == LKV_BF16 ? 2 : 4;
+    g.qkv = mat_geom(g.dm + 2 * g.dkv, g.dm, g.dtype);
+    g.wo = mat_geom(g.dm, g.dm, g.dtype);
+    g.gu = mat_geom(64 * ((g.ff + 31) / 32), g.dm, g.dtype);
+    g.down = mat_geom(g.dm, g.ff, g.dtype);
+    g.lm = mat_geom(g.vocab, g.dm, g.dtype);
+    size_t o = 0;
+    g.tok_embed = o;
+    o = align_up(o + (size_t)g.vocab * g.dm * g.esz);
+    g.final_norm = o;
+    o = align_up(o + (size_t)g.dm * 4);
+    g.lm_head = o;
+    o = align_up(o + g.lm.bytes);
+    g.layer0 = o;
+    size_t q = 0;
+    g.o_qkv = q;
+    q = align_up(q + g.qkv.bytes);
+    g.o_wo = q;
+    q = align_up(q + g.wo.bytes);
+    g.o_gu = q;
+    q = align_up(q + g.gu.bytes);
+    g.o_down = q;
+    q = align_up(q + g.down.bytes);
+    g.o_attn_norm = q;
+    q = align_up(q + (size_t)g.dm * 4);
+    g.o_mlp_norm = q;
+    q = align_up(q + (size_t)g.dm * 4);
+    g.layer_stride = q;
+    g.total = o + q * g.L;
+    return g;
+}
+
+struct ModelWs {
+    DecodeWs dec;
+    size_t x, ss, act_h, act_attn, act_ff, q, nk, nv, part, cnt, rope, total;
+    int nbt;
+};
+size_t act_bytes(const ModelGeom& g, int K, int B, int nbt) {
+    return g.dtype == LKV_BF16 ? (size_t)((K + 127) / 128) * 8 * nbt * 256 : (size_t)B * K * 4;
+}
+ModelWs model_ws(const ModelGeom& g, int B, const lkv_ragged_desc* r, const lkv_model_desc* m) {
+    ModelWs w;
+    w.dec = decode_layout(r, g.Hq / g.H);
+    w.nbt = (B + 7) / 8;
+    size_t o = align_up(w.dec.total);
+    w.x = o;
+    o = align_up(o + (size_t)B * g.dm * 4);
+    w.ss = o;
+    o = align_up(o + (size_t)((g.dm + 63) / 64) * B * 4);
+    w.act_h = o;
+    o = align_up(o + act_bytes(g, g.dm, B, w.nbt));
+    w.act_attn = o;
+    o = align_up(o + act_bytes(g, g.dm, B, w.nbt));
+    w.act_ff = o;
+    o = align_up(o + act_bytes(g, g.ff, B, w.nbt));
+    w.q = o;
+    o = align_up(o + (size_t)B * g.dm * g.esz);
+    w.nk = o;
+    o = align_up(o + (size_t)B * g.dkv * g.esz);
+    w.nv = o;
+    o = align_up(o + (size_t)B * g.dkv * g.esz);
+    w.part = o;
+    o = align_up(o + gemv_max_grid(num_sms()) * 2 * 64 * 16 * 4);
+    w.cnt = o;
+    const int ng_max = std::max(std::max(g.qkv.NG, g.wo.NG), std::max(std::max(g.gu.NG, g.down.NG), g.lm.NG));
+    o = align_up(o + (size_t)ng_max * 4);
+    w.rope = o;
+    o = align_up(o + (size_t)m->max_seq_len * (g.D / 2) * 8);
+    w.total = o;
+    return w;
+}
+
+lkv_status check_model_cache(const lkv_model_desc* m, const lkv_ragged_desc* r, int n_seq) {
+    if (n_seq < 1 || n_seq > LKV_MODEL_MAX_SEQ) return fail(LKV_ERR_UNSUPPORTED, "model decode: 1 <= n_seq <= 16");
+    return check_ragged(r, (int64_t)n_seq * m->n_layers * m->n_kv_heads, m->head_dim, m->dtype, true);
+}
+
+}  // namespace
+
+extern "C" {
+
+lkv_status lkv_model_validate(const lkv_model_desc* m) { return check_model(m); }
+
+size_t lkv_model_weights_bytes(const lkv_model_desc* m) {
+    if (check_model(m)) return 0;
+    return model_geom(m).total;
+}
+
+lkv_status lkv_model_load_param(const lkv_model_desc* m, void* weights, int32_t param, int32_t layer, const void* src,
+                                lkv_stream_t stream) {
+    lkv_status st = check_model(m);
+    if (st) return st;
+    if (!weights || !src) return fail(LKV_ERR_CONTRACT, "load_param: null buffer");
+    const ModelGeom g = model_geom(m);
+    const bool per_layer = param != LKV_P_TOK_EMBED && param != LKV_P_FINAL_NORM && param != LKV_P_LM_HEAD;
+    if (param < LKV_P_TOK_EMBED || param > LKV_P_LM_HEAD) return fail(LKV_ERR_CONTRACT, "load_param: unknown parameter");
+    if (per_layer && (layer < 0 || layer >= g.L)) return fail(LKV_ERR_CONTRACT, "load_param: layer out of range");
+    unsigned char* base = static_cast<unsigned char*>(weights);
+    unsigned char* lb = base + g.layer0 + (size_t)(per_layer ? layer : 0) * g.layer_stride;
+    cudaStream_t s = (cudaStream_t)stream;
+    auto pack = [&](const MatGeom& mg, unsigned char* dst, int K, int cols, int mode, int off) -> lkv_status {
+        LKV_CUDA(launch_pack_weight(src, g.dtype, K, cols, mode, off, mg.NG, mg.KU, dst, s), "pack weight");
+        return LKV_OK;
+    };
+    switch (param) {
+        case LKV_P_TOK_EMBED:
+            LKV_CUDA(cudaMemcpyAsync(base + g.tok_embed, src, (size_t)g.vocab * g.dm * g.esz, cudaMemcpyDeviceToDevice, s),
+                     "tok_embed copy");
+            return LKV_OK;
+        case LKV_P_FINAL_NORM:
+            LKV_CUDA(launch_to_f32(src, g.dtype, g.dm, reinterpret_cast<float*>(base + g.final_norm), s), "norm");
+            return LKV_OK;
+        case LKV_P_ATTN_NORM:
+        case LKV_P_MLP_NORM:
+            LKV_CUDA(launch_to_f32(src, g.dtype, g.dm,
+                                   reinterpret_cast<float*>(lb + (param == LKV_P_ATTN_NORM ? g.o_attn_norm : g.o_mlp_norm)), s),
+                     "norm");
+            return LKV_OK;
+        case LKV_P_WQ: return pack(g.qkv, lb + g.o_qkv, g.dm, g.dm, 0, 0);
+        case LKV_P_WK: return pack(g.qkv, lb + g.o_qkv, g.dm, g.dkv, 0, g.dm);
+        case LKV_P_WV: return pack(g.qkv, lb + g.o_qkv, g.dm, g.dkv, 0, g.dm + g.dkv);
+        case LKV_P_WO: return pack(g.wo, lb + g.o_wo, g.dm, g.dm, 0, 0);
+        case LKV_P_W_GATE: return pack(g.gu, lb + g.o_gu, g.dm, g.ff, 1, 0);
+        case LKV_P_W_UP: return pack(g.gu, lb + g.o_gu, g.dm, g.ff, 2, 0);
+        case LKV_P_W_DOWN: return pack(g.down, lb + g.o_down, g.ff, g.dm, 0, 0);
+        default: return pack(g.lm, base + g.lm_head, g.dm, g.vocab, 0, 0);
+    }
+}
+
+size_t lkv_model_workspace_bytes(const lkv_model_desc* m, int32_t n_seq, const lkv_ragged_desc* r) {
+    if (check_model(m) || check_model_cache(m, r, n_seq)) return 0;
+    return model_ws(model_geom(m), n_seq, r, m).total;
+}
+
+lkv_status lkv_model_plan(const lkv_model_desc* m, const lkv_ragged_desc* r, int32_t n_seq, void* ws, size_t ws_bytes,
+                          lkv_stream_t stream) {
+    lkv_status st = check_model(m);
+    if (st || (st = check_model_cache(m, r, n_seq))) return st;
+    const ModelGeom g = model_geom(m);
+    const ModelWs w = model_ws(g, n_seq, r, m);
+    if ((st = check_ws(ws, ws_bytes, w.total))) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    LKV_CUDA(cudaMemsetAsync(ws, 0, w.total, s), "workspace clear");
+    LKV_CUDA(launch_decode_plan(r->offsets, n_seq, g.L, g.H, at<DecodeItem>(ws, w.dec.items),
+                                at<int32_t>(ws, w.dec.item_base), at<int32_t>(ws, w.dec.layer_begin),
+                                at<int32_t>(ws, w.dec.n_items), s),
+             "decode plan");
+    LKV_CUDA(launch_rope_table(m->max_seq_len, g.D, m->rope_base, 0, at<float2>(ws, w.rope), s), "rope table");
+    return LKV_OK;
+}
+
+lkv_status lkv_model_decode_step(const lkv_model_desc* m, const void* weights, const lkv_ragged_desc* r, int32_t n_seq,
+                                 const int32_t* tokens, int32_t* tokens_seen, float* logits, void* ws, size_t ws_bytes,
+                                 lkv_stream_t stream) {
+    lkv_status st = check_model(m);
+    if (st || (st = check_model_cache(m, r, n_seq))) return st;
+    if (!weights || !tokens || !tokens_seen || !logits) return fail(LKV_ERR_CONTRACT, "model decode: null buffer");
+    const ModelGeom g = model_geom(m);
+    const ModelWs w = model_ws(g, n_seq, r, m);
+    if ((st = check_ws(ws, ws_bytes, w.total))) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int B = n_seq, G = g.Hq / g.H, sms = num_sms();
+    const unsigned char* wb = static_cast<const unsigned char*>(weights);
+    ErrWord* err = at<ErrWord>(ws, w.dec.err);
+    float* x = at<float>(ws, w.x);
+    float* ss = at<float>(ws, w.ss);
+
+    GemvParams gp;
+    memset(&gp, 0, sizeof gp);
+    gp.B = B;
+    gp.nbt = g.dtype == LKV_BF16 ? w.nbt : 0;
+    gp.part = at<float>(ws, w.part);
+    gp.cnt = at<uint32_t>(ws, w.cnt);
+    gp.err = err;
+    gp.dm = g.dm;
+    gp.dkv = g.dkv;
+    gp.head_dim = g.D;
+    gp.max_seq = m->max_seq_len;
+    gp.q_out = at<void>(ws, w.q);
+    gp.k_out = at<void>(ws, w.nk);
+    gp.v_out = at<void>(ws, w.nv);
+    gp.rope = at<float2>(ws, w.rope);
+    gp.tokens_seen = tokens_seen;
+    gp.x = x;
+    gp.ss_part = ss;
+    gp.nbt_out = gp.nbt;
+    gp.act_out = at<void>(ws, w.act_ff);
+    gp.ff = g.ff;
+    auto gemv = [&](const MatGeom& mg, const unsigned char* wp, int epi, const void* act, int n_real) -> cudaError_t {
+        GemvParams q = gp;
+        q.w = wp;
+        q.NG = mg.NG;
+        q.KU = mg.KU;
+        q.N = n_real;
+        q.K = mg.K;
+        q.act = act;
+        q.epi = epi;
+        return launch_gemv(q, g.dtype, sms, s);
+    };
+
+    DecodeParams dp;
+    memset(&dp, 0, sizeof dp);
+    dp.n_heads = B * g.L * g.H;
+    dp.n_kv_heads = g.H;
+    dp.n_q_heads = g.Hq;
+    dp.G = G;
+    dp.head_dim = g.D;
+    dp.n_seq = B;
+    dp.n_layers = g.L;
+    dp.q_layers = 1;
+    dp.max_items = (int32_t)w.dec.max_items;
+    dp.out_nbt = g.dtype == LKV_BF16 ? w.nbt : 0;
+    dp.scale_log2 = (float)(1.0 / std::sqrt((double)g.D) * 1.4426950408889634);  // model.cpp:223
+    dp.offsets = r->offsets;
+    dp.lens = r->lens;
+    dp.positions = r->positions;
+    dp.keys = r->keys;
+    dp.values = r->values;
+    dp.q = at<void>(ws, w.q);
+    dp.new_k = at<void>(ws, w.nk);
+    dp.new_v = at<void>(ws, w.nv);
+    dp.tokens_seen = tokens_seen;
+    dp.out = at<void>(ws, w.act_attn);
+    dp.items = at<DecodeItem>(ws, w.dec.items);
+    dp.item_base = at<int32_t>(ws, w.dec.item_base);
+    dp.part_m = at<float>(ws, w.dec.part_m);
+    dp.part_l = at<float>(ws, w.dec.part_l);
+    dp.part_o = at<float>(ws, w.dec.part_o);
+    dp.err = err;
+    CUtensorMap mk, mv;
+    if (g.dtype == LKV_BF16) {
+        if ((st = make_map_bf16(&mk, r->keys, 128, (uint64_t)r->capacity_rows, 64))) return st;
+        if ((st = make_map_bf16(&mv, r->values, 128, (uint64_t)r->capacity_rows, 64))) return st;
+    }
+    int32_t* lbeg = at<int32_t>(ws, w.dec.layer_begin);
+
+    LKV_CUDA(launch_embed(wb + g.tok_embed, g.dtype, tokens, B, g.dm, g.vocab, tokens_seen, m->max_seq_len, x, ss, err, s),
+             "embed");
+    const float eps = (float)m->norm_eps;
+    for (int l = 0; l < g.L; ++l) {
+        const unsigned char* lw = wb + g.layer0 + (size_t)l * g.layer_stride;
+        const float* attn_norm = reinterpret_cast<const float*>(lw + g.o_attn_norm);
+        const float* mlp_norm = reinterpret_cast<const float*>(lw + g.o_mlp_norm);
+        LKV_CUDA(launch_norm_pack(x, ss, attn_norm, B, g.dm, eps, at<void>(ws, w.act_h), w.nbt, g.dtype, s), "attn norm");
+        LKV_CUDA(gemv(g.qkv, lw + g.o_qkv, EPI_QKV, at<void>(ws, w.act_h), g.dm + 2 * g.dkv), "qkv");
+        dp.layer0 = l;
+        dp.item_lo = lbeg + l;
+        dp.item_hi = lbeg + l + 1;
+        LKV_CUDA(launch_decode(dp, g.dtype, &mk, &mv, sms, s), "attention");
+        LKV_CUDA(gemv(g.wo, lw + g.o_wo, EPI_RESID, at<void>(ws, w.act_attn), g.dm), "wo");
+        LKV_CUDA(launch_norm_pack(x, ss, mlp_norm, B, g.dm, eps, at<void>(ws, w.act_h), w.nbt, g.dtype, s), "mlp norm");
+        LKV_CUDA(gemv(g.gu, lw + g.o_gu, EPI_SWIGLU, at<void>(ws, w.act_h), g.ff), "gate/up");
+        LKV_CUDA(gemv(g.down, lw + g.o_down, EPI_RESID, at<void>(ws, w.act_ff), g.dm), "down");
+    }
+    LKV_CUDA(launch_norm_pack(x, ss, reinterpret_cast<const float*>(wb + g.final_norm), B, g.dm, eps,
+                              at<void>(ws, w.act_h), w.nbt, g.dtype, s),
+             "final norm");
+    GemvParams q = gp;
+    q.f_out = logits;
+    {
+        q.w = wb + g.lm_head;
+        q.NG = g.lm.NG;
+        q.KU = g.lm.KU;
+        q.N = g.vocab;
+        q.K = g.dm;
+        q.act = at<void>(ws, w.act_h);
+        q.epi = EPI_F32;
+        LKV_CUDA(launch_gemv(q, g.dtype, sms, s), "lm_head");
+    }
     return LKV_OK;
 }
 

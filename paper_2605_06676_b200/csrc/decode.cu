@@ -43,31 +43,69 @@ constexpr int kDecThreads = (kDecConsumers + 1) * 32;
 
 
 // ---- plan: work items over each head's capacity (once per eviction) -------------------------
-__global__ void __launch_bounds__(1024) decode_plan_kernel(const int64_t* offsets, int n_heads, DecodeItem* items,
-                                                           int32_t* item_base, int32_t* n_items_out) {
+// Heads are enumerated LAYER-major, j -> (l, s, h), head = (s * n_layers + l) * n_kv + h, so the
+// items of one layer are contiguous: layer_begin[l] .. layer_begin[l + 1] (a per-layer decode
+// launch, as in a full model decode step, walks just that range; an all-layer launch walks
+// layer_begin[0] .. layer_begin[n_layers]).
+__global__ void __launch_bounds__(1024) decode_plan_kernel(const int64_t* offsets, int n_seq, int n_layers, int n_kv,
+                                                           DecodeItem* items, int32_t* item_base,
+                                                           int32_t* layer_begin, int32_t* n_items) {
     __shared__ uint32_t s_scan[33];
     __shared__ int32_t s_carry;
+    const int n_heads = n_seq * n_layers * n_kv;
+    const int per_layer = n_seq * n_kv;
     if (threadIdx.x == 0) s_carry = 0;
     __syncthreads();
     for (int base = 0; base < n_heads; base += 1024) {
-        const int h = base + threadIdx.x;
+        const int j = base + threadIdx.x;
         uint32_t nch = 0;
-        if (h < n_heads) {
+        int h = 0;
+        if (j < n_heads) {
+            const int l = j / per_layer, r = j - l * per_layer;
+            const int s = r / n_kv, kh = r - s * n_kv;
+            h = (s * n_layers + l) * n_kv + kh;
             const int64_t cap = offsets[h + 1] - offsets[h];
             nch = (uint32_t)((cap + kDecCh - 1) / kDecCh);
         }
         uint32_t tot;
         const uint32_t ex = block_exclusive_scan<1024>(nch, s_scan, &tot);
-        if (h < n_heads) {
+        if (j < n_heads) {
             const int b0 = s_carry + (int)ex;
             item_base[h] = b0;
+            if (j % per_layer == 0) layer_begin[j / per_layer] = b0;
             for (uint32_t c = 0; c < nch; ++c) items[b0 + c] = DecodeItem{h, (int32_t)c};
         }
         __syncthreads();
         if (threadIdx.x == 0) s_carry += (int32_t)tot;
         __syncthreads();
     }
-    if (threadIdx.x == 0) *n_items_out = s_carry;
+    if (threadIdx.x == 0) {
+        layer_begin[n_layers] = s_carry;
+        *n_items = s_carry;
+    }
+}
+
+// (s, l, kv head) of a flat head, and the row of the q / out / new_k tensors of this launch,
+// which hold the q_layers layers starting at layer0: qsl = s * q_layers + (l - layer0).
+struct HeadCoord {
+    int s, l, kvh, qsl;
+};
+__device__ __forceinline__ HeadCoord head_coord(const DecodeParams& p, int head) {
+    HeadCoord c;
+    const int sl = head / p.n_kv_heads;
+    c.kvh = head - sl * p.n_kv_heads;
+    c.s = sl / p.n_layers;
+    c.l = sl - c.s * p.n_layers;
+    c.qsl = c.s * p.q_layers + (c.l - p.layer0);
+    return c;
+}
+// element (g, dd) of a head's G x D output block -> index into out.  Plain: [qsl][Hq][D].
+// Packed (out_nbt > 0, q_layers == 1): the mma B-fragment layout the weight-streaming GEMV
+// reads (model.cu act_index), with batch = s and feature = (kvh * G + g) * D + dd.
+__device__ __forceinline__ size_t out_index(const DecodeParams& p, const HeadCoord& c, int g, int dd) {
+    const int D = p.head_dim;
+    if (p.out_nbt == 0) return ((size_t)c.qsl * p.n_q_heads + c.kvh * p.G + g) * D + dd;
+    return act_index(c.s, (c.kvh * p.G + g) * D + dd, p.out_nbt);
 }
 
 // ---- helpers ---------------------------------------------------------------------------------
@@ -136,7 +174,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int G = p.G;
     const int D = 128;
-    const int n_items = *p.n_items;
+    const int it_lo = *p.item_lo, it_hi = *p.item_hi;
     if (threadIdx.x == 0) {
         for (int i = 0; i < kDecStages; ++i) {
             mbar_init(&full[i], 1);
@@ -154,7 +192,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
             const uint64_t pol = l2_policy_evict_first();
             int st = 0;
             uint32_t ph = 0;
-            for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+            for (int it = it_lo + blockIdx.x; it < it_hi; it += gridDim.x) {
                 const DecodeItem wi = p.items[it];
                 const int len_new = p.lens[wi.head] + 1;
                 const int r0 = wi.chunk * kDecCh;
@@ -185,7 +223,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
     const int cq = (lane & 3) * 2;  // fragment column pair
     int st = 0;
     uint32_t ph = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    for (int it = it_lo + blockIdx.x; it < it_hi; it += gridDim.x) {
         const DecodeItem wi = p.items[it];
         const int head = wi.head;
         const int len_old = p.lens[head];
@@ -198,8 +236,11 @@ __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
         if (has_new && off + len_new > p.offsets[head + 1]) {
             if (threadIdx.x == 0) latch_error(p.err, LKV_ERR_CONTRACT, head);
         }
-        const int sl = head / p.n_kv_heads, kvh = head - sl * p.n_kv_heads;
-        const __nv_bfloat16* qp = static_cast<const __nv_bfloat16*>(p.q) + ((size_t)sl * p.n_q_heads + kvh * G) * D;
+        const __nv_bfloat16* qp;
+        {
+            const HeadCoord hc = head_coord(p, head);
+            qp = static_cast<const __nv_bfloat16*>(p.q) + ((size_t)hc.qsl * p.n_q_heads + hc.kvh * G) * D;
+        }
 
         // Q fragments (rows g and g+8 of the padded 16-row tile)
         uint32_t qa[8][4];
@@ -230,12 +271,14 @@ __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
                 if (nr >= wr0 && nr < wr0 + 16) {
                     const int hq = lane & 15;
                     const bool isv = lane >= 16;
-                    const uint4* src = static_cast<const uint4*>(isv ? p.new_v : p.new_k) + (size_t)head * 16;
+                    const HeadCoord hc = head_coord(p, head);
+                    const uint4* src =
+                        static_cast<const uint4*>(isv ? p.new_v : p.new_k) + ((size_t)hc.qsl * p.n_kv_heads + hc.kvh) * 16;
                     const uint4 v = __ldg(src + hq);
                     *reinterpret_cast<uint4*>(sbase + (isv ? 2 * kDecStageRows * 128 : 0) + sw_off(nr, hq)) = v;
                     uint4* dstg = static_cast<uint4*>(isv ? p.values : p.keys) + (size_t)(off + len_old) * 16;
                     dstg[hq] = v;
-                    if (lane == 0) p.positions[off + len_old] = p.tokens_seen[sl / (p.heads_per_seq / p.n_kv_heads)];
+                    if (lane == 0) p.positions[off + len_old] = p.tokens_seen[hc.s];
                     fence_proxy_async_smem();
                     __syncwarp();
                 }
@@ -356,7 +399,8 @@ __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
         }
         named_bar_sync(1, kDecConsumers * 32);
         const int nch = (len_new + kDecCh - 1) / kDecCh;
-        __nv_bfloat16* outp = static_cast<__nv_bfloat16*>(p.out) + ((size_t)sl * p.n_q_heads + kvh * G) * D;
+        __nv_bfloat16* outp = static_cast<__nv_bfloat16*>(p.out);
+        const HeadCoord hc = head_coord(p, head);
         for (int e = threadIdx.x; e < G * D; e += kDecConsumers * 32) {
             const int gg = e / D, dd = e - gg * D;
             float M = -INFINITY;
@@ -371,7 +415,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
                 acc += r[dd] * f;
             }
             if (nch == 1) {
-                outp[e] = __float2bfloat16_rn(acc / L);
+                outp[out_index(p, hc, gg, dd)] = __float2bfloat16_rn(acc / L);
             } else {
                 p.part_o[((size_t)it * G + gg) * D + dd] = acc;
                 if (dd == 0) {
@@ -392,8 +436,8 @@ __global__ void __launch_bounds__(kDecSimtThreads) decode_attn_f32_kernel(const 
     const int D = p.head_dim, G = p.G;
     float* qs = sm;                 // [G][D]
     float* sc = qs + G * D;         // [G][kDecCh]
-    const int it = blockIdx.x;
-    if (it >= *p.n_items) return;
+    const int it = *p.item_lo + blockIdx.x;
+    if (it >= *p.item_hi) return;
     const DecodeItem wi = p.items[it];
     const int head = wi.head;
     const int len_old = p.lens[head];
@@ -407,19 +451,19 @@ __global__ void __launch_bounds__(kDecSimtThreads) decode_attn_f32_kernel(const 
         if (threadIdx.x == 0) latch_error(p.err, LKV_ERR_CONTRACT, head);
         return;
     }
-    const int sl = head / p.n_kv_heads, kvh = head - sl * p.n_kv_heads;
-    const float* qp = static_cast<const float*>(p.q) + ((size_t)sl * p.n_q_heads + kvh * G) * D;
+    const HeadCoord hc = head_coord(p, head);
+    const float* qp = static_cast<const float*>(p.q) + ((size_t)hc.qsl * p.n_q_heads + hc.kvh * G) * D;
     for (int e = threadIdx.x; e < G * D; e += kDecSimtThreads) qs[e] = qp[e];
     float* K = static_cast<float*>(p.keys) + (size_t)off * D;
     float* V = static_cast<float*>(p.values) + (size_t)off * D;
-    const float* nk = static_cast<const float*>(p.new_k) + (size_t)head * D;
-    const float* nv = static_cast<const float*>(p.new_v) + (size_t)head * D;
+    const float* nk = static_cast<const float*>(p.new_k) + ((size_t)hc.qsl * p.n_kv_heads + hc.kvh) * D;
+    const float* nv = static_cast<const float*>(p.new_v) + ((size_t)hc.qsl * p.n_kv_heads + hc.kvh) * D;
     if (has_new) {
         for (int e = threadIdx.x; e < D; e += kDecSimtThreads) {
             K[(size_t)len_old * D + e] = nk[e];
             V[(size_t)len_old * D + e] = nv[e];
         }
-        if (threadIdx.x == 0) p.positions[off + len_old] = p.tokens_seen[sl / (p.heads_per_seq / p.n_kv_heads)];
+        if (threadIdx.x == 0) p.positions[off + len_old] = p.tokens_seen[hc.s];
     }
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -468,7 +512,11 @@ __global__ void __launch_bounds__(kCombThreads) decode_combine_kernel(const __gr
     pdl_wait();
     __shared__ float s_w[kCombMaxChunks];  // [c * G + g] weight exp2(m_c - M_g) / L_g
     __shared__ float s_M[16], s_L[16];
-    const int head = blockIdx.x;
+    // blockIdx.x enumerates this launch's heads layer-major (as the plan does)
+    const int per_layer = p.n_seq * p.n_kv_heads;
+    const int jl = blockIdx.x / per_layer, jr = blockIdx.x - jl * per_layer;
+    const int js = jr / p.n_kv_heads;
+    const int head = (js * p.n_layers + p.layer0 + jl) * p.n_kv_heads + (jr - js * p.n_kv_heads);
     const int D = p.head_dim, G = p.G;
     const int len_new = p.lens[head] + 1;
     const int nch = (len_new + kDecCh - 1) / kDecCh;
@@ -510,8 +558,8 @@ __global__ void __launch_bounds__(kCombThreads) decode_combine_kernel(const __gr
             s_w[i] = exp2f(s_m[i] - s_M[g]) / s_L[g];
         }
         __syncthreads();
-        const int sl = head / p.n_kv_heads, kvh = head - sl * p.n_kv_heads;
-        T* out = static_cast<T*>(p.out) + ((size_t)sl * p.n_q_heads + kvh * G) * D;
+        const HeadCoord hc = head_coord(p, head);
+        T* out = static_cast<T*>(p.out);
         // grid.y tiles the G*D outputs: one element per thread, all chunk loads in flight
         const int e = blockIdx.y * kCombThreads + threadIdx.x;
         if (e < G * D) {
@@ -532,22 +580,27 @@ __global__ void __launch_bounds__(kCombThreads) decode_combine_kernel(const __gr
 #pragma unroll
             for (int k = 0; k < 16; ++k)
                 if (c + k < nch) acc = fmaf(v[k], s_w[(c + k) * G + g], acc);
-            if constexpr (sizeof(T) == 2) out[e] = __float2bfloat16_rn(acc);
-            else out[e] = acc;
+            const size_t oi = out_index(p, hc, g, e - g * D);
+            if constexpr (sizeof(T) == 2) out[oi] = __float2bfloat16_rn(acc);
+            else out[oi] = acc;
         }
     } else if (nch * G > kCombMaxChunks && threadIdx.x == 0 && blockIdx.y == 0) {
         latch_error(p.err, LKV_ERR_UNSUPPORTED, head);
     }
     if (threadIdx.x == 0 && blockIdx.y == 0) {
         p.lens[head] = len_new;
-        if (head % p.heads_per_seq == 0) p.tokens_seen[head / p.heads_per_seq] += 1;
+        // tokens_seen advances once per step, after the last layer's append (the position of
+        // every layer's new row is the step's starting tokens_seen, model.cpp:218,246)
+        const HeadCoord hc = head_coord(p, head);
+        if (hc.l == p.n_layers - 1 && hc.kvh == 0) p.tokens_seen[hc.s] += 1;
     }
 }
 
 // ---- host launchers ---------------------------------------------------------------------------------
-cudaError_t launch_decode_plan(const int64_t* offsets, int n_heads, DecodeItem* items, int32_t* item_base,
-                               int32_t* n_items, cudaStream_t stream) {
-    decode_plan_kernel<<<1, 1024, 0, stream>>>(offsets, n_heads, items, item_base, n_items);
+cudaError_t launch_decode_plan(const int64_t* offsets, int n_seq, int n_layers, int n_kv, DecodeItem* items,
+                               int32_t* item_base, int32_t* layer_begin, int32_t* n_items, cudaStream_t stream) {
+    decode_plan_kernel<<<1, 1024, 0, stream>>>(offsets, n_seq, n_layers, n_kv, items, item_base, layer_begin,
+                                               n_items);
     note_launches(1);
     return cudaGetLastError();
 }
@@ -571,7 +624,7 @@ cudaError_t launch_decode(const DecodeParams& p, int dtype, const CUtensorMap* m
         const int grid = min(p.max_items, per_sm * num_sms);
         kern<<<grid, kDecThreads, smem, stream>>>(p, *mk, *mv);
         e = launch_pdl(decode_combine_kernel<__nv_bfloat16>,
-                       dim3(p.n_heads, (p.G * p.head_dim + kCombThreads - 1) / kCombThreads), dim3(kCombThreads), 0,
+                       dim3(p.n_seq * p.q_layers * p.n_kv_heads, (p.G * p.head_dim + kCombThreads - 1) / kCombThreads), dim3(kCombThreads), 0,
                        stream, p, 1);
         if (e != cudaSuccess) return e;
         note_launches(2);
@@ -582,7 +635,7 @@ cudaError_t launch_decode(const DecodeParams& p, int dtype, const CUtensorMap* m
         decode_attn_f32_kernel<<<p.max_items, kDecSimtThreads, smem, stream>>>(p);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
-        decode_combine_kernel<float><<<dim3(p.n_heads, (p.G * p.head_dim + kCombThreads - 1) / kCombThreads), kCombThreads, 0, stream>>>(p, 0);
+        decode_combine_kernel<float><<<dim3(p.n_seq * p.q_layers * p.n_kv_heads, (p.G * p.head_dim + kCombThreads - 1) / kCombThreads), kCombThreads, 0, stream>>>(p, 0);
         note_launches(2);
     }
     return cudaGetLastError();

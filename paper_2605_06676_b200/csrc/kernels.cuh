@@ -86,13 +86,26 @@ struct CompactParams {
 cudaError_t launch_select(SelectParams p, int n_heads, cudaStream_t stream);
 cudaError_t launch_compact(const CompactParams& p, int n_heads, cudaStream_t stream);
 // ---- decode.cu (K5)
+// Packed activation layout read by the weight-streaming GEMV (model.cu): the bf16 B operand of
+// mma.m16n8k16 (k = feature, n = batch), one 8-byte fragment per lane per (16-feature step,
+// 8-row batch tile).  Element (b, k) -> index in bf16 elements.
+__host__ __device__ __forceinline__ size_t act_index(int b, int k, int nbt) {
+    const int s = k >> 4, kk = k & 15, bt = b >> 3, g = b & 7;
+    const int lane = g * 4 + ((kk & 7) >> 1);
+    return (((size_t)s * nbt + bt) * 32 + lane) * 4 + (size_t)(kk >> 3) * 2 + (kk & 1);
+}
+
 struct DecodeItem {
     int32_t head, chunk;
 };
 struct DecodeParams {
     int32_t n_heads, n_kv_heads, n_q_heads, G, head_dim;
-    const int32_t* n_items;
-    int32_t max_items;
+    int32_t n_seq, n_layers;    // cache geometry (flat head = (s * n_layers + l) * n_kv_heads + h)
+    int32_t layer0, q_layers;   // this launch: layers [layer0, layer0 + q_layers) (q/out/new_k hold those)
+    const int32_t* item_lo;     // device: first / one-past-last work item of this launch
+    const int32_t* item_hi;
+    int32_t max_items;          // upper bound on item_hi - item_lo (grid sizing)
+    int32_t out_nbt;            // 0: out is [qsl][Hq][D]; > 0: packed GEMV activations (q_layers == 1)
     float scale_log2;
     const int64_t* offsets;
     int32_t* lens;
@@ -103,7 +116,6 @@ struct DecodeParams {
     const void* new_k;
     const void* new_v;
     int32_t* tokens_seen;
-    int32_t heads_per_seq;
     void* out;
     const DecodeItem* items;
     const int32_t* item_base;
@@ -112,10 +124,49 @@ struct DecodeParams {
     float* part_o;
     ErrWord* err;
 };
-cudaError_t launch_decode_plan(const int64_t* offsets, int n_heads, DecodeItem* items, int32_t* item_base,
-                               int32_t* n_items, cudaStream_t stream);
+cudaError_t launch_decode_plan(const int64_t* offsets, int n_seq, int n_layers, int n_kv, DecodeItem* items,
+                               int32_t* item_base, int32_t* layer_begin, int32_t* n_items, cudaStream_t stream);
 cudaError_t launch_decode(const DecodeParams& p, int dtype, const CUtensorMap* mk, const CUtensorMap* mv, int num_sms,
                           cudaStream_t stream);
+
+// ---- model.cu (full decode step of the toy GQA model)
+enum GemvEpi { EPI_QKV = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_F32 = 3 };
+struct GemvParams {
+    const void* w;       // bf16: packed 64-col x 128-k units [NG][KU]; f32: row-major [K][NG * 64]
+    int32_t NG, KU;      // column groups of 64, k-units of 128
+    int32_t N, K;        // real output columns (virtual order) / reduction length
+    int32_t B, nbt;      // batch rows, 8-row batch tiles of the packed activations
+    const void* act;     // bf16: packed (act_index), K padded to KU * 128; f32: row-major [B][K]
+    float* part;         // stream-K partials [2 * grid][64][16]
+    uint32_t* cnt;       // per-group arrival counters (zero, self-resetting)
+    ErrWord* err;
+    int32_t epi;
+    // EPI_QKV: columns [0, dm) -> q (RoPE), [dm, dm + dkv) -> new k (RoPE), then -> new v
+    int32_t dm, dkv, head_dim, max_seq;
+    void* q_out;
+    void* k_out;
+    void* v_out;
+    const float2* rope;          // [max_seq][head_dim / 2] (cos, sin)
+    const int32_t* tokens_seen;  // [B]: the step's absolute position
+    // EPI_RESID: x[b][n] += y; ss_part[group][b] = sum over the group's columns of x^2
+    float* x;
+    float* ss_part;
+    // EPI_SWIGLU: virtual column group g = gate cols [32g, 32g+32) then up cols [32g, 32g+32)
+    void* act_out;
+    int32_t nbt_out, ff;
+    // EPI_F32
+    float* f_out;
+};
+cudaError_t launch_gemv(const GemvParams& p, int dtype, int num_sms, cudaStream_t stream);
+size_t gemv_max_grid(int num_sms);
+cudaError_t launch_embed(const void* tok_embed, int dtype, const int32_t* tokens, int B, int dm, int vocab,
+                         const int32_t* tokens_seen, int max_seq, float* x, float* ss_part, ErrWord* err,
+                         cudaStream_t stream);
+cudaError_t launch_norm_pack(const float* x, const float* ss_part, const float* gain, int B, int dm, float eps,
+                             void* act, int nbt, int dtype, cudaStream_t stream);
+cudaError_t launch_pack_weight(const void* src, int dtype, int K, int cols, int col_mode, int col_off, int NG, int KU,
+                               void* dst, cudaStream_t stream);
+cudaError_t launch_to_f32(const void* src, int dtype, int n, float* dst, cudaStream_t stream);
 // ---- rope.cu (layer-by-layer prefill: K/V production)
 cudaError_t launch_rope_table(int t_max, int head_dim, double base, int pos_offset, float2* cs, cudaStream_t stream);
 cudaError_t launch_rope_pack(const void* k_lin, const void* v_lin, int n_seq, int t_max, const int32_t* seq_lens,

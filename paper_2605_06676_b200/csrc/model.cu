@@ -1,0 +1,473 @@
+// model.cu -- the full decode step of the reference's toy GQA model: the
+// step AFTER the eviction path.  Reference: decode_step (model.cpp:209-287): per layer
+//   h = rmsnorm(x, attn_norm); q, k, v = h Wq, h Wk, h Wv; RoPE(q, k) at tokens_seen;
+//   append (k, v) and attend (K5, decode.cu); x += attn Wo;
+//   h2 = rmsnorm(x, mlp_norm); x += (silu(h2 Wgate) * (h2 Wup)) Wdown;
+// then logits = rmsnorm(x, final_norm) lm_head.
+//
+// At decode batch sizes (B <= 16 sequences) every projection is a skinny GEMM whose cost is
+// streaming the weights once from HBM (B flop per weight element, far below the ridge), so the
+// kernel is a WEIGHT STREAM:
+//  * weights are repacked once (lkv_model_load_param) into 16 KB units of 64 output columns x
+//    128 k, stored in the register-fragment order of mma.m16n8k16 (A = W^T): one lds.128 per
+//    lane per 16x16 tile, no ldmatrix, no bank conflicts; units of a matrix form one contiguous
+//    stream [column group][k-unit];
+//  * a persistent grid (2 CTAs / SM) splits the unit stream EVENLY (stream-K): CTA c owns units
+//    [c U / P, (c+1) U / P), so every SM streams the same number of bytes whatever the shape;
+//  * one producer thread moves each unit (plus the matching 2-4 KB slice of the packed
+//    activations) with a 1-D bulk TMA copy into a 4-stage mbarrier ring; the first stages'
+//    WEIGHT copies are issued before griddepcontrol.wait, i.e. while the previous kernel of
+//    the step is still finishing (PDL);
+//  * 4 consumer warps split each unit's 8 k-steps, accumulate on tensor cores (fp32), and
+//    reduce across warps in fixed order; a column group cut by a CTA boundary is finished by
+//    the last-arriving CTA, which sums the partials in CTA order (deterministic);
+//  * the epilogue is fused: RoPE + scatter into q / new k / new v (QKV), residual add + the
+//    group's sum of squares for the next rmsnorm (Wo, Wdown), SiLU(gate) * up written straight
+//    into the next GEMV's packed activations (Wgate|Wup interleaved by 32 columns), fp32 logits.
+// fp32 models (correctness configs) run a SIMT kernel over plain row-major weights with the
+// same virtual column order and the same epilogues.
+#include <math.h>
+
+#include "kernels.cuh"
+
+namespace lkv_dev {
+
+constexpr int kWsCols = 64;                    // output columns per unit (4 m16 tiles)
+constexpr int kWsK = 128;                      // k per unit (8 k16 steps)
+constexpr int kWsUnitBytes = kWsCols * kWsK * 2;  // 16 KB of bf16
+constexpr int kWsStages = 4;
+constexpr int kWsConsumers = 4;
+constexpr int kWsThreads = (kWsConsumers + 1) * 32;
+constexpr int kWsPerSm = 2;
+constexpr int kYPad = 17;                      // y[64][17]: columns x batch (B <= 16)
+
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+
+__device__ __forceinline__ void mma_16816(float (&d)[4], const uint4& a, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
+}
+
+// ---- fused epilogues: y[n][b] = the finished fp32 product of column group ng ----------------------
+template <typename T>
+__device__ __forceinline__ void store2(void* base, size_t i, float a, float b) {
+    if constexpr (sizeof(T) == 2) {
+        *reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(base) + i) = __floats2bfloat162_rn(a, b);
+    } else {
+        *reinterpret_cast<float2*>(static_cast<float*>(base) + i) = make_float2(a, b);
+    }
+}
+
+template <typename T>
+__device__ void gemv_epilogue(const GemvParams& p, int ng, float (*y)[kYPad], int tid, int nthr) {
+    const int B = p.B;
+    if (p.epi == EPI_QKV) {
+        const int D = p.head_dim;
+        for (int e = tid; e < 32 * B; e += nthr) {
+            const int pr = e & 31, b = e >> 5;
+            const int n = ng * kWsCols + 2 * pr;
+            if (n >= p.N) continue;
+            float a = y[2 * pr][b], c = y[2 * pr + 1][b];
+            void* dst;
+            int col, ld;
+            bool rot = true;
+            if (n < p.dm) {
+                dst = p.q_out, col = n, ld = p.dm;
+            } else if (n < p.dm + p.dkv) {
+                dst = p.k_out, col = n - p.dm, ld = p.dkv;
+            } else {
+                dst = p.v_out, col = n - p.dm - p.dkv, ld = p.dkv, rot = false;
+            }
+            if (rot) {  // rope_row (model.cpp:38-46): pair j of the head, theta = pos * base^(-2j/d)
+                const int pos = min(max(p.tokens_seen[b], 0), p.max_seq - 1);
+                const float2 cs = p.rope[(size_t)pos * (D / 2) + (col % D) / 2];
+                const float r0 = a * cs.x - c * cs.y, r1 = a * cs.y + c * cs.x;
+                a = r0;
+                c = r1;
+            }
+            store2<T>(dst, (size_t)b * ld + col, a, c);
+        }
+    } else if (p.epi == EPI_RESID) {
+        for (int e = tid; e < kWsCols * B; e += nthr) {
+            const int nl = e & 63, b = e >> 6;
+            const int n = ng * kWsCols + nl;
+            float v = 0.f;
+            if (n < p.N) {
+                v = p.x[(size_t)b * p.N + n] + y[nl][b];
+                p.x[(size_t)b * p.N + n] = v;
+            }
+            y[nl][b] = v * v;
+        }
+        named_sync(1, nthr);
+        if (tid < B) {
+            float s = 0.f;
+            for (int nl = 0; nl < kWsCols; ++nl) s += y[nl][tid];
+            p.ss_part[(size_t)ng * B + tid] = s;
+        }
+    } else if (p.epi == EPI_SWIGLU) {
+        for (int e = tid; e < 32 * B; e += nthr) {
+            const int i = e & 31, b = e >> 5;
+            const int c = ng * 32 + i;
+            if (c >= p.ff) continue;
+            const float g = y[i][b], u = y[32 + i][b];
+            const float a = g / (1.f + expf(-g)) * u;  // model.cpp:274-277
+            if constexpr (sizeof(T) == 2)
+                static_cast<__nv_bfloat16*>(p.act_out)[act_index(b, c, p.nbt_out)] = __float2bfloat16_rn(a);
+            else
+                static_cast<float*>(p.act_out)[(size_t)b * p.ff + c] = a;
+        }
+    } else {
+        for (int e = tid; e < kWsCols * B; e += nthr) {
+            const int nl = e & 63, b = e >> 6;
+            const int n = ng * kWsCols + nl;
+            if (n < p.N) p.f_out[(size_t)b * p.N + n] = y[nl][b];
+        }
+    }
+}
+
+// ---- bf16 weight-stream GEMV (tensor cores, stream-K) -------------------------------------------
+__host__ __device__ __forceinline__ int64_t unit_begin(int c, int64_t U, int P) { return (int64_t)c * U / P; }
+__device__ __forceinline__ int unit_owner(int64_t u, int64_t U, int P) { return (int)(((u + 1) * P - 1) / U); }
+
+template <int NBT>
+__global__ void __launch_bounds__(kWsThreads, kWsPerSm) wstream_gemv_kernel(const __grid_constant__ GemvParams p) {
+    constexpr int kActBytes = 8 * NBT * 256;  // 8 k16 steps x NBT tiles x 32 lanes x 8 B
+    constexpr int kStage = kWsUnitBytes + kActBytes;
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kWsStages * kStage);
+    uint64_t* empty = full + kWsStages;
+    float* red = reinterpret_cast<float*>(empty + kWsStages);  // [4][64][NBT * 8]
+    float(*y)[kYPad] = reinterpret_cast<float(*)[kYPad]>(red + kWsConsumers * kWsCols * NBT * 8);
+    int* s_last = reinterpret_cast<int*>(y + kWsCols);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t U = (int64_t)p.NG * p.KU;
+    const int P = gridDim.x, c = blockIdx.x;
+    const int64_t u0 = unit_begin(c, U, P), u1 = unit_begin(c + 1, U, P);
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kWsStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], kWsConsumers);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    pdl_trigger();
+
+    if (warp == kWsConsumers) {
+        // ===================== producer =====================
+        if (lane == 0 && u1 > u0) {
+            const uint64_t pol_w = l2_policy_evict_first(), pol_a = l2_policy_evict_last();
+            const unsigned char* wsrc = static_cast<const unsigned char*>(p.w);
+            const unsigned char* asrc = static_cast<const unsigned char*>(p.act);
+            const int npre = (int)(u1 - u0 < kWsStages ? u1 - u0 : kWsStages);
+            // weights do not depend on the previous kernel: start streaming them before the wait
+            for (int i = 0; i < npre; ++i) {
+                mbar_arrive_expect_tx(&full[i], kStage);
+                bulk_g2s(smem + i * kStage, wsrc + (size_t)(u0 + i) * kWsUnitBytes, kWsUnitBytes, &full[i], pol_w);
+            }
+            pdl_wait();
+            for (int i = 0; i < npre; ++i) {
+                const int ku = (int)((u0 + i) % p.KU);
+                bulk_g2s(smem + i * kStage + kWsUnitBytes, asrc + (size_t)ku * kActBytes, kActBytes, &full[i], pol_a);
+            }
+            int st = npre % kWsStages;
+            uint32_t ph = (npre == kWsStages) ? 1u : 0u;
+            for (int64_t u = u0 + npre; u < u1; ++u) {
+                mbar_wait(&empty[st], ph ^ 1);
+                mbar_arrive_expect_tx(&full[st], kStage);
+                const int ku = (int)(u % p.KU);
+                bulk_g2s(smem + st * kStage, wsrc + (size_t)u * kWsUnitBytes, kWsUnitBytes, &full[st], pol_w);
+                bulk_g2s(smem + st * kStage + kWsUnitBytes, asrc + (size_t)ku * kActBytes, kActBytes, &full[st],
+                         pol_a);
+                if (++st == kWsStages) {
+                    st = 0;
+                    ph ^= 1;
+                }
+            }
+        }
+        return;
+    }
+
+    // ===================== consumers =====================
+    pdl_wait();
+    const int tid = threadIdx.x;  // 0..127
+    const int g = lane >> 2, cq = (lane & 3) * 2;
+    int st = 0;
+    uint32_t ph = 0;
+    int64_t u = u0;
+    const int ng_first = (int)(u0 / p.KU);
+    while (u < u1) {
+        const int ng = (int)(u / p.KU);
+        const int64_t gbeg = (int64_t)ng * p.KU, gend = gbeg + p.KU;
+        const int64_t se = min(u1, gend);
+        const bool whole = (u == gbeg) && (se == gend);
+        float acc[4][NBT][4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+            for (int bt = 0; bt < NBT; ++bt) acc[t][bt][0] = acc[t][bt][1] = acc[t][bt][2] = acc[t][bt][3] = 0.f;
+        for (; u < se; ++u) {
+            mbar_wait(&full[st], ph);
+            const unsigned char* stg = smem + st * kStage;
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk) {
+                const int ks = warp * 2 + kk;
+                uint2 bf[NBT];
+#pragma unroll
+                for (int bt = 0; bt < NBT; ++bt)
+                    bf[bt] = *reinterpret_cast<const uint2*>(stg + kWsUnitBytes + ((ks * NBT + bt) * 32 + lane) * 8);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const uint4 a = *reinterpret_cast<const uint4*>(stg + ((ks * 4 + t) * 32 + lane) * 16);
+#pragma unroll
+                    for (int bt = 0; bt < NBT; ++bt) mma_16816(acc[t][bt], a, bf[bt].x, bf[bt].y);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+            if (++st == kWsStages) {
+                st = 0;
+                ph ^= 1;
+            }
+        }
+        // ---- cross-warp reduction (fixed order) -> y[64][b]
+        constexpr int BW = NBT * 8;
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+            for (int bt = 0; bt < NBT; ++bt) {
+                float* r = red + (size_t)warp * kWsCols * BW;
+                const int n = t * 16 + g, b = bt * 8 + cq;
+                r[n * BW + b] = acc[t][bt][0];
+                r[n * BW + b + 1] = acc[t][bt][1];
+                r[(n + 8) * BW + b] = acc[t][bt][2];
+                r[(n + 8) * BW + b + 1] = acc[t][bt][3];
+            }
+        named_sync(1, kWsConsumers * 32);
+        for (int e = tid; e < kWsCols * BW; e += kWsConsumers * 32) {
+            const int n = e / BW, b = e - n * BW;
+            float v = red[e];
+#pragma unroll
+            for (int w = 1; w < kWsConsumers; ++w) v += red[(size_t)w * kWsCols * BW + e];
+            y[n][b] = v;
+        }
+        named_sync(1, kWsConsumers * 32);
+        if (!whole) {
+            // stream-K fix-up: partial -> global slot; the last CTA of the group sums in CTA order
+            const int slot = 2 * c + (ng == ng_first ? 0 : 1);
+            float* mine = p.part + (size_t)slot * kWsCols * 16;
+            for (int e = tid; e < kWsCols * 16; e += kWsConsumers * 32) mine[e] = y[e >> 4][e & 15];
+            __threadfence();
+            named_sync(1, kWsConsumers * 32);
+            const int cf = unit_owner(gbeg, U, P), cl = unit_owner(gend - 1, U, P);
+            if (tid == 0) {
+                const uint32_t old = atomicAdd(&p.cnt[ng], 1u);
+                const int last = (int)old == cl - cf;
+                if (last) p.cnt[ng] = 0u;  // self-reset for the next launch
+                *s_last = last;
+            }
+            named_sync(1, kWsConsumers * 32);
+            if (!*s_last) continue;
+            __threadfence();
+            for (int e = tid; e < kWsCols * 16; e += kWsConsumers * 32) {
+                float v = 0.f;
+                for (int cc = cf; cc <= cl; ++cc) {
+                    const int sl = 2 * cc + (ng == (int)(unit_begin(cc, U, P) / p.KU) ? 0 : 1);
+                    v += __ldcg(p.part + (size_t)sl * kWsCols * 16 + e);
+                }
+                y[e >> 4][e & 15] = v;
+            }
+            named_sync(1, kWsConsumers * 32);
+        }
+        gemv_epilogue<__nv_bfloat16>(p, ng, y, tid, kWsConsumers * 32);
+        named_sync(1, kWsConsumers * 32);
+    }
+}
+
+// ---- fp32 SIMT GEMV (correctness configs): one 64-thread block per column group ------------------
+__global__ void __launch_bounds__(64) gemv_f32_kernel(const __grid_constant__ GemvParams p) {
+    pdl_wait();
+    __shared__ float y[kWsCols][kYPad];
+    const int ng = blockIdx.x, nl = threadIdx.x;
+    const int ldw = p.NG * kWsCols;
+    const float* w = static_cast<const float*>(p.w) + ng * kWsCols + nl;
+    const float* act = static_cast<const float*>(p.act);
+    float acc[16];
+#pragma unroll
+    for (int b = 0; b < 16; ++b) acc[b] = 0.f;
+    for (int k = 0; k < p.K; ++k) {
+        const float wv = w[(size_t)k * ldw];
+#pragma unroll
+        for (int b = 0; b < 16; ++b)
+            if (b < p.B) acc[b] = fmaf(act[(size_t)b * p.K + k], wv, acc[b]);
+    }
+#pragma unroll
+    for (int b = 0; b < 16; ++b) y[nl][b] = acc[b];
+    __syncthreads();
+    gemv_epilogue<float>(p, ng, y, nl, 64);
+}
+
+// ---- embedding (model.cpp:218-219): x = tok_embed[token]; per-group sums of squares --------------
+template <typename T>
+__global__ void __launch_bounds__(64) embed_kernel(const T* __restrict__ tab, const int32_t* tokens, int B, int dm,
+                                                  int vocab, const int32_t* tokens_seen, int max_seq, float* x,
+                                                  float* ss_part, ErrWord* err) {
+    pdl_wait();
+    __shared__ float s_w[2];
+    const int ng = blockIdx.x, b = blockIdx.y, n = ng * 64 + threadIdx.x;
+    int tok = tokens[b];
+    if (tok < 0 || tok >= vocab) {
+        if (threadIdx.x == 0 && ng == 0) latch_error(err, LKV_ERR_CONTRACT, b);  // "token id out of vocab"
+        tok = 0;
+    }
+    if (threadIdx.x == 0 && ng == 0 && (tokens_seen[b] < 0 || tokens_seen[b] >= max_seq))
+        latch_error(err, LKV_ERR_CONTRACT, b);  // "sequence exceeds max_seq_len" (model.cpp:215)
+    float v = 0.f;
+    if (n < dm) {
+        if constexpr (sizeof(T) == 2) v = __bfloat162float(tab[(size_t)tok * dm + n]);
+        else v = tab[(size_t)tok * dm + n];
+        x[(size_t)b * dm + n] = v;
+    }
+    float s = v * v;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) ss_part[(size_t)ng * B + b] = s_w[0] + s_w[1];
+}
+
+// ---- rmsnorm (model.cpp:48-53) -> next GEMV's activations ---------------------------------------------
+__global__ void __launch_bounds__(128) norm_pack_kernel(const float* x, const float* ss_part, const float* gain, int B,
+                                                        int dm, float eps, void* act, int nbt, int is_bf16) {
+    pdl_wait();
+    __shared__ float s_inv;
+    const int b = blockIdx.y;
+    if (threadIdx.x == 0) {
+        const int ngx = (dm + 63) / 64;
+        float s = 0.f;
+        for (int gi = 0; gi < ngx; ++gi) s += ss_part[(size_t)gi * B + b];
+        s_inv = 1.f / sqrtf(s / (float)dm + eps);
+    }
+    __syncthreads();
+    const int k = blockIdx.x * 128 + threadIdx.x;
+    if (k >= dm) return;
+    const float h = x[(size_t)b * dm + k] * gain[k] * s_inv;
+    if (is_bf16) static_cast<__nv_bfloat16*>(act)[act_index(b, k, nbt)] = __float2bfloat16_rn(h);
+    else static_cast<float*>(act)[(size_t)b * dm + k] = h;
+}
+
+// ---- weight repacking (once per model load) -----------------------------------------------------------
+// src [K][cols] row-major (reference layout, x W); column c lands on virtual column
+//   col_mode 0: col_off + c;   col_mode 1/2 (gate/up): (c / 32) * 64 + (mode == 2 ? 32 : 0) + c % 32.
+__device__ __forceinline__ int virt_col(int c, int mode, int off) {
+    return mode == 0 ? off + c : (c >> 5) * 64 + (mode == 2 ? 32 : 0) + (c & 31);
+}
+template <typename T>
+__global__ void pack_weight_kernel(const T* __restrict__ src, int K, int cols, int mode, int off, int NG, int KU,
+                                   T* __restrict__ dst) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)K * cols) return;
+    const int k = (int)(i / cols), c = (int)(i - (int64_t)k * cols);
+    const int vn = virt_col(c, mode, off);
+    if constexpr (sizeof(T) == 4) {
+        dst[(size_t)k * NG * 64 + vn] = src[i];
+    } else {
+        const int ng = vn >> 6, r = vn & 63, t = r >> 4, m = r & 15;
+        const int ku = k >> 7, kk = k & 127, s = kk >> 4, kc = kk & 15;
+        const int lane = (m & 7) * 4 + ((kc & 7) >> 1);
+        const int reg = (m >> 3) + 2 * (kc >> 3);
+        const size_t unit = (size_t)ng * KU + ku;
+        dst[unit * (kWsUnitBytes / 2) + (((size_t)(s * 4 + t) * 32 + lane) * 8) + reg * 2 + (kc & 1)] = src[i];
+    }
+}
+
+template <typename T>
+__global__ void to_f32_kernel(const T* src, int n, float* dst) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        if constexpr (sizeof(T) == 2) dst[i] = __bfloat162float(src[i]);
+        else dst[i] = src[i];
+    }
+}
+
+// ---- host launchers ----------------------------------------------------------------------------------
+size_t gemv_max_grid(int num_sms) { return (size_t)kWsPerSm * num_sms; }
+
+static size_t wstream_smem(int nbt) {
+    const size_t stage = kWsUnitBytes + 8 * nbt * 256;
+    return 128 + kWsStages * stage + 2 * kWsStages * 8 + (size_t)kWsConsumers * kWsCols * nbt * 8 * 4 +
+           (size_t)kWsCols * kYPad * 4 + 16;
+}
+
+cudaError_t launch_gemv(const GemvParams& p, int dtype, int num_sms, cudaStream_t stream) {
+    if (dtype == LKV_BF16) {
+        const int64_t U = (int64_t)p.NG * p.KU;
+        const int64_t cap = (int64_t)kWsPerSm * num_sms;
+        const int grid = (int)(U < cap ? U : cap);
+        const size_t smem = wstream_smem(p.nbt);
+        auto kern = p.nbt == 1 ? wstream_gemv_kernel<1> : wstream_gemv_kernel<2>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        e = launch_pdl(kern, dim3(grid), dim3(kWsThreads), smem, stream, p);
+        note_launches(1);
+        return e;
+    }
+    cudaError_t e = launch_pdl(gemv_f32_kernel, dim3(p.NG), dim3(64), 0, stream, p);
+    note_launches(1);
+    return e;
+}
+
+cudaError_t launch_embed(const void* tok_embed, int dtype, const int32_t* tokens, int B, int dm, int vocab,
+                         const int32_t* tokens_seen, int max_seq, float* x, float* ss_part, ErrWord* err,
+                         cudaStream_t stream) {
+    const dim3 grid((dm + 63) / 64, B);
+    cudaError_t e;
+    if (dtype == LKV_BF16)
+        e = launch_pdl(embed_kernel<__nv_bfloat16>, grid, dim3(64), 0, stream,
+                       static_cast<const __nv_bfloat16*>(tok_embed), tokens, B, dm, vocab, tokens_seen, max_seq, x,
+                       ss_part, err);
+    else
+        e = launch_pdl(embed_kernel<float>, grid, dim3(64), 0, stream, static_cast<const float*>(tok_embed), tokens,
+                       B, dm, vocab, tokens_seen, max_seq, x, ss_part, err);
+    note_launches(1);
+    return e;
+}
+
+cudaError_t launch_norm_pack(const float* x, const float* ss_part, const float* gain, int B, int dm, float eps,
+                             void* act, int nbt, int dtype, cudaStream_t stream) {
+    cudaError_t e = launch_pdl(norm_pack_kernel, dim3((dm + 127) / 128, B), dim3(128), 0, stream, x, ss_part, gain, B,
+                               dm, eps, act, nbt, (int)(dtype == LKV_BF16));
+    note_launches(1);
+    return e;
+}
+
+cudaError_t launch_pack_weight(const void* src, int dtype, int K, int cols, int col_mode, int col_off, int NG, int KU,
+                               void* dst, cudaStream_t stream) {
+    const int64_t n = (int64_t)K * cols;
+    const unsigned blocks = (unsigned)((n + 255) / 256);
+    if (dtype == LKV_BF16)
+        pack_weight_kernel<__nv_bfloat16><<<blocks, 256, 0, stream>>>(static_cast<const __nv_bfloat16*>(src), K, cols,
+                                                                      col_mode, col_off, NG, KU,
+                                                                      static_cast<__nv_bfloat16*>(dst));
+    else
+        pack_weight_kernel<float><<<blocks, 256, 0, stream>>>(static_cast<const float*>(src), K, cols, col_mode,
+                                                              col_off, NG, KU, static_cast<float*>(dst));
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_to_f32(const void* src, int dtype, int n, float* dst, cudaStream_t stream) {
+    if (dtype == LKV_BF16)
+        to_f32_kernel<__nv_bfloat16><<<(n + 255) / 256, 256, 0, stream>>>(static_cast<const __nv_bfloat16*>(src), n, dst);
+    else
+        to_f32_kernel<float><<<(n + 255) / 256, 256, 0, stream>>>(static_cast<const float*>(src), n, dst);
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+}  // namespace lkv_dev
