@@ -254,12 +254,25 @@ def run_ours(args, rank, world, local_rank):
         row_b = D * cache.keys.element_size()
         h2d = hk.numel() * hk.element_size() + (hv.numel() * hv.element_size() if scorers.input == lkv.SCORER_KV
                                                  else kept_rows * row_b)
-        d2h = (2 * host_out.keys.numel() * host_out.keys.element_size() + host_out.positions.numel() * 4
-               + host_out.offsets.numel() * 8 + host_out.lens.numel() * 4)
+        # the transfer floor of this step: the same H2D bytes as one plain pinned copy
+        probe = torch.empty(hk.numel() * hk.element_size(), dtype=torch.uint8, device=dev)
+        src = hk.view(-1).view(torch.uint8)
+        probe.copy_(src, non_blocking=True)
+        e0.record(stream)
+        probe.copy_(src, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        h2d_gbs = probe.numel() / (e0.elapsed_time(e1) / 1e3) / 1e9
+        del probe, src
+        used = int(host_out.offsets[-1])  # rows copied back: every head's budget + decode slack
+        d2h = (2 * used * row_b + used * 4 + host_out.offsets.numel() * 8 + host_out.lens.numel() * 4)
         e2e = {"value": rows_per_step * world / (ms_e2e / 1e3), "unit": UNIT, "ms_per_step": ms_e2e,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "path": "pinned host K/V -> lkv_evict_host (C ABI): K streamed per layer chunk, kept V gathered "
-                       "over PCIe, compacted cache copied back to pinned host"}
+               "path": "pinned host K/V -> lkv_evict_host (C ABI): per layer chunk, K streamed H2D, scored, "
+                       "selected, kept V gathered over PCIe, compacted rows copied D2H while later chunks upload",
+               "layers_per_chunk": args.e2e_chunk, "pcie_h2d_gbs_measured": h2d_gbs,
+               "h2d_floor_ms": h2d / 1e9 / h2d_gbs * 1e3,
+               "frac_of_h2d_floor": (h2d / 1e9 / h2d_gbs * 1e3) / ms_e2e}
         del hk, hv, host_out
 
     log("decode")
@@ -312,7 +325,7 @@ def run_ours(args, rank, world, local_rank):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded; BASELINE.json configs[1] shapes)",
-            "config": {"workload": f"C2: L{L} x H{H} x d{D}, t={T}, batch 1/GPU, R={cfg.ratio}, exact budgets",
+            "config": {"workload": f"C{args.config}: L{L} x H{H} x d{D}, t={T}, batch {n_seq}/GPU, R={cfg.ratio}, exact budgets",
                        "rows_per_gpu_step": rows_per_step, "kept_rows_per_gpu_step": kept_rows,
                        "scorer": "K-only 128->64->1 GELU-erf per layer", "parallelism": f"batch-sharded x{world}",
                        "l2": "inputs (4.3 GB K/V per GPU) larger than L2; no flush"},
@@ -321,7 +334,10 @@ def run_ours(args, rank, world, local_rank):
                           "note": "stage times from a second timed region (separate C-ABI calls); the headline "
                                   "step is lkv_evict with K2 overlapped on a side stream"},
             "roofline": {"bound": "hbm", "kernel": "score_tc_kernel (K1)", "achieved": score_gbs, "peak": hbm_peak,
-                         "unit": "GB/s", "frac": score_gbs / hbm_peak, "traffic": None,
+                         "unit": "GB/s", "frac": score_gbs / hbm_peak,
+                         "traffic": ncu_traffic("ncu_score_tc_c2.txt") if args.config == 2 else None,
+                         "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum of one `ncu --set full` "
+                                           "capture of this kernel on this workload (profiles/r01/ncu_score_tc_c2.txt)",
                          "algorithmic_bytes_per_launch": int(score_bytes), "peak_source": peak_src,
                          "tensor_tflops": score_tflops, "tensor_frac": score_tflops / tc_peak},
             "step_roofline": {"algorithmic_bytes": int(step_bytes), "achieved_gbs": step_bytes / (ms_step / 1e3) / 1e9,
@@ -333,6 +349,22 @@ def run_ours(args, rank, world, local_rank):
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
+
+
+def ncu_traffic(name, round_dir="r01"):
+    """DRAM bytes (read + write) of one launch from a committed `ncu --set full` summary."""
+    units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    try:
+        tot = 0.0
+        with open(os.path.join(ROOT, "profiles", round_dir, name)) as f:
+            for ln in f:
+                ln = ln.strip()
+                if ln.startswith("dram__bytes_read.sum") or ln.startswith("dram__bytes_write.sum"):
+                    val, unit = ln.split("=")[1].split()
+                    tot += float(val) * units[unit]
+        return int(tot) if tot > 0 else None
+    except Exception:
+        return None
 
 
 def cpu_baseline(cache, scorers, ev, n_threads=1, n_heads=8):
@@ -434,7 +466,7 @@ def main():
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-heads", type=int, default=8)
-    ap.add_argument("--e2e-chunk", type=int, default=4, help="layers per host->device chunk in the e2e path")
+    ap.add_argument("--e2e-chunk", type=int, default=1, help="layers per host->device chunk in the e2e path")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 

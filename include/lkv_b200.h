@@ -196,8 +196,12 @@ lkv_status lkv_evict(const lkv_cache_desc* cache, const lkv_scorer_desc* scorer,
  * K is uploaded into dev_keys (device, dense shape) in (sequence, layers_per_chunk-layer)
  * chunks on a library copy stream, pipelined with scoring; the kept V rows are gathered
  * straight from host memory (only the retained fraction of V crosses PCIe); with [k;v]
- * scorers V is uploaded into dev_values too.  host_out (nullable) receives a copy of the
- * compacted cache in pinned host buffers.  Everything is ordered on `stream`. */
+ * scorers V is uploaded into dev_values too.  Each chunk is scored, selected and gathered
+ * as soon as its K has landed.  host_out (nullable, pinned) receives the compacted cache
+ * chunk by chunk on a third (device->host) stream while later chunks still upload; to size
+ * those copies the call waits once on the host for the budget solve's ragged offsets (all
+ * uploads are queued first, so the wait overlaps the transfer).  Everything else is ordered
+ * on `stream`. */
 lkv_status lkv_evict_host(const lkv_cache_desc* host_cache, void* dev_keys, void* dev_values,
                           const lkv_scorer_desc* scorer, const double* logits, double target_ratio,
                           int32_t mode, const lkv_ragged_desc* out, const lkv_ragged_desc* host_out,

@@ -50,7 +50,7 @@ int num_sms() {
 // Non-blocking helper streams per (host thread, device) for fork/join inside a call:
 // `side` runs the latency-bound LKV-H solve, `copy` the host<->device transfers.
 cudaStream_t helper_stream(int which) {
-    thread_local cudaStream_t streams[2][64] = {};
+    thread_local cudaStream_t streams[3][64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= 64) return nullptr;
@@ -60,6 +60,7 @@ cudaStream_t helper_stream(int which) {
 }
 cudaStream_t side_stream() { return helper_stream(0); }
 cudaStream_t copy_stream() { return helper_stream(1); }
+cudaStream_t d2h_stream() { return helper_stream(2); }  // device->host, so it overlaps H2D (full duplex)
 
 constexpr size_t kAlign = 256;
 size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
@@ -250,25 +251,28 @@ lkv_status run_score(const lkv_cache_desc* c, const lkv_scorer_desc* s, float* s
     return LKV_OK;
 }
 
+// `c` may describe a contiguous sub-range of the flat heads of the cache the workspace was laid
+// out for: h0 = its first flat head, chunk0 = its first 4096-row select chunk.  Every per-head
+// buffer is offset by h0; the ragged rows are addressed through the (absolute) offsets.
 lkv_status run_select(const lkv_cache_desc* c, const float* scores, const int32_t* budgets,
                       const lkv_ragged_desc* out, void* ws, const EvictWs& w, bool gather, cudaStream_t stream,
-                      bool hist_ready = false) {
+                      bool hist_ready = false, int64_t h0 = 0, int64_t chunk0 = 0) {
     for (int s = 0; s < c->n_seq; ++s)
         if (c->seq_lens[s] > 4096 * 1024) return fail(LKV_ERR_UNSUPPORTED, "top-k supports t <= 4M rows per head");
     SelectParams p;
     memset(&p, 0, sizeof p);
     p.seq = make_seq(c);
     p.scores = scores;
-    p.budgets = budgets;
-    p.hist = at<uint32_t>(ws, w.hist);
-    p.state = at<HeadSel>(ws, w.state);
-    p.chunk_gt = at<uint32_t>(ws, w.chunk_gt);
-    p.chunk_out = at<uint32_t>(ws, w.chunk_out);
-    p.chunk_eqb = at<uint32_t>(ws, w.chunk_eqb);
-    p.cands = at<uint32_t>(ws, w.cands);
-    p.offsets = out->offsets;
+    p.budgets = budgets + h0;
+    p.hist = at<uint32_t>(ws, w.hist) + h0 * 2048;
+    p.state = at<HeadSel>(ws, w.state) + h0;
+    p.chunk_gt = at<uint32_t>(ws, w.chunk_gt) + chunk0;
+    p.chunk_out = at<uint32_t>(ws, w.chunk_out) + chunk0;
+    p.chunk_eqb = at<uint32_t>(ws, w.chunk_eqb) + chunk0;
+    p.cands = at<uint32_t>(ws, w.cands) + h0 * c->max_tokens;
+    p.offsets = out->offsets + h0;
     p.out_pos = out->positions;
-    p.out_lens = out->lens;
+    p.out_lens = out->lens + h0;
     p.keys = c->keys;
     p.values = c->values;
     p.out_keys = out->keys;
@@ -535,10 +539,16 @@ lkv_status lkv_evict(const lkv_cache_desc* c, const lkv_scorer_desc* s, const do
     return run_select(c, scores, budgets, out, ws, w, true, strm, hist_made);
 }
 
-// Eviction of a host-resident (pinned, device-mapped) dense cache.  K is streamed to the
-// device in (sequence, layer-group) chunks on a copy stream while earlier chunks are scored;
-// the kept V rows are gathered straight from host memory (only rho of V crosses PCIe); the
-// compacted cache is optionally copied back to pinned host buffers on the copy stream.
+// Eviction of a host-resident (pinned, device-mapped) dense cache, pipelined per chunk =
+// (sequence, layer group) over three streams:
+//   copy stream : K (and V for [k;v] scorers) of chunk i uploaded H2D;
+//   main stream : chunk i scored (K1 + fused histogram) and selected/gathered (K3+K4) as soon as
+//                 its K landed; its kept V rows are read straight from the mapped host V (only
+//                 rho of V crosses PCIe);
+//   d2h stream  : chunk i's compacted rows copied back to the pinned host cache while later
+//                 chunks are still uploading (PCIe is full duplex).
+// The D2H ranges need the ragged offsets on the host: K2 runs first on the side stream and
+// its offsets are read back once (all K uploads are already queued, so the wait is hidden).
 lkv_status lkv_evict_host(const lkv_cache_desc* hc, void* dev_keys, void* dev_values, const lkv_scorer_desc* s,
                           const double* logits, double R, int32_t mode, const lkv_ragged_desc* out,
                           const lkv_ragged_desc* host_out, int32_t layers_per_chunk, void* ws, size_t ws_bytes,
@@ -551,19 +561,28 @@ lkv_status lkv_evict_host(const lkv_cache_desc* hc, void* dev_keys, void* dev_va
     const bool kv = s->input == LKV_SCORER_KV;
     if (kv && !dev_values) return fail(LKV_ERR_CONTRACT, "[k;v] scorers need dev_values staging");
     if (layers_per_chunk < 1) layers_per_chunk = 1;
+    if (host_out && (!host_out->keys || !host_out->values || !host_out->positions || !host_out->offsets ||
+                     !host_out->lens || host_out->capacity_rows < out->capacity_rows))
+        return fail(LKV_ERR_CONTRACT, "host_out buffers missing or too small");
     // host V must be device-accessible (pinned + mapped): use its device alias for the gather
     cudaPointerAttributes pa{};
     if (cudaPointerGetAttributes(&pa, hc->values) != cudaSuccess || pa.type != cudaMemoryTypeHost || !pa.devicePointer)
         return fail(LKV_ERR_CONTRACT, "host values must be pinned, device-mapped memory (cudaHostAlloc)");
-    const void* v_dev_alias = pa.devicePointer;
+    if (host_out) {
+        cudaPointerAttributes po{};
+        if (cudaPointerGetAttributes(&po, host_out->offsets) != cudaSuccess || po.type != cudaMemoryTypeHost)
+            return fail(LKV_ERR_CONTRACT, "host_out buffers must be pinned host memory");
+    }
+    const char* v_dev_alias = static_cast<const char*>(pa.devicePointer);
     const int n = hc->n_layers * hc->n_kv_heads;
     const EvictWs w = evict_layout(hc, n);
     if ((st = check_ws(ws, ws_bytes, w.total))) return st;
     cudaStream_t strm = (cudaStream_t)stream;
-    cudaStream_t side = side_stream(), cs = copy_stream();
-    if (!side || !cs) return fail(LKV_ERR_CUDA, "helper stream creation failed");
+    cudaStream_t side = side_stream(), cs = copy_stream(), ds = d2h_stream();
+    if (!side || !cs || !ds) return fail(LKV_ERR_CUDA, "helper stream creation failed");
     const size_t esz = hc->dtype == LKV_F32 ? 4 : 2;
-    const size_t head_bytes = (size_t)hc->max_tokens * hc->head_dim * esz;
+    const size_t rowb = (size_t)hc->head_dim * esz;
+    const size_t head_bytes = (size_t)hc->max_tokens * rowb;
     const int H = hc->n_kv_heads, L = hc->n_layers;
     int32_t* budgets = at<int32_t>(ws, w.budgets);
     float* scores = at<float>(ws, w.scores);
@@ -586,77 +605,108 @@ lkv_status lkv_evict_host(const lkv_cache_desc* hc, void* dev_keys, void* dev_va
     LKV_CUDA(cudaEventRecord(start, strm), "event record");
     LKV_CUDA(cudaStreamWaitEvent(side, start, 0), "stream wait");
     LKV_CUDA(cudaStreamWaitEvent(cs, start, 0), "stream wait");
-    // K2 on the side stream
+    LKV_CUDA(cudaStreamWaitEvent(ds, start, 0), "stream wait");
+    // K2 on the side stream; its offsets go to the host when the compacted cache is copied back
     st = lkv_budgets(logits, n, R, mode, hc->seq_lens, hc->n_seq, out->decode_slack, at<double>(ws, w.ratios), budgets,
                      out->offsets, ws, ws_bytes, (lkv_stream_t)side);
     if (st) return st;
+    const int64_t n_heads = n_heads_of(hc);
+    if (host_out)
+        LKV_CUDA(cudaMemcpyAsync(host_out->offsets, out->offsets, sizeof(int64_t) * (n_heads + 1), cudaMemcpyDeviceToHost,
+                                 side),
+                 "offsets D2H");
     LKV_CUDA(cudaEventRecord(join, side), "event record");
-    // K upload (copy stream) pipelined with K1 (main stream), chunk = (sequence, layer group)
-    bool hist_made = false;
-    LKV_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 2048 * (size_t)n_heads_of(hc), strm), "hist clear");
+    // 1. queue every chunk's upload on the copy stream
+    struct Chunk {
+        int sq, l0, nl;
+        int64_t h0, c0;
+        cudaEvent_t ready;
+    };
+    std::vector<Chunk> chunks;
+    int64_t cbase = 0;
     for (int sq = 0; sq < hc->n_seq; ++sq) {
+        const int64_t cph = (hc->seq_lens[sq] + 4095) / 4096;  // select chunks per head
         for (int l0 = 0; l0 < L; l0 += layers_per_chunk) {
-            const int nl = std::min(layers_per_chunk, L - l0);
-            const size_t first_head = (size_t)(sq * L + l0) * H;
-            const size_t bytes = (size_t)nl * H * head_bytes;
-            char* dk = static_cast<char*>(dev_keys) + first_head * head_bytes;
-            LKV_CUDA(cudaMemcpyAsync(dk, static_cast<const char*>(hc->keys) + first_head * head_bytes, bytes,
+            Chunk ch;
+            ch.sq = sq;
+            ch.l0 = l0;
+            ch.nl = std::min(layers_per_chunk, L - l0);
+            ch.h0 = (int64_t)(sq * L + l0) * H;
+            ch.c0 = cbase + (int64_t)l0 * H * cph;
+            const size_t bytes = (size_t)ch.nl * H * head_bytes;
+            LKV_CUDA(cudaMemcpyAsync(static_cast<char*>(dev_keys) + ch.h0 * head_bytes,
+                                     static_cast<const char*>(hc->keys) + ch.h0 * head_bytes, bytes,
                                      cudaMemcpyHostToDevice, cs),
                      "K upload");
-            char* dv = nullptr;
-            if (kv) {
-                dv = static_cast<char*>(dev_values) + first_head * head_bytes;
-                LKV_CUDA(cudaMemcpyAsync(dv, static_cast<const char*>(hc->values) + first_head * head_bytes, bytes,
+            if (kv)
+                LKV_CUDA(cudaMemcpyAsync(static_cast<char*>(dev_values) + ch.h0 * head_bytes,
+                                         static_cast<const char*>(hc->values) + ch.h0 * head_bytes, bytes,
                                          cudaMemcpyHostToDevice, cs),
                          "V upload");
-            }
-            cudaEvent_t ready = mk();
-            if (!ready) return fail(LKV_ERR_CUDA, "event creation failed");
-            LKV_CUDA(cudaEventRecord(ready, cs), "event record");
-            LKV_CUDA(cudaStreamWaitEvent(strm, ready, 0), "stream wait");
-            lkv_cache_desc sub = *hc;
-            sub.n_seq = 1;
-            sub.n_layers = nl;
-            sub.keys = dk;
-            sub.values = kv ? dv : dk;
-            sub.seq_lens = hc->seq_lens + sq;
-            lkv_scorer_desc ss = *s;
-            const int64_t sc0 = (int64_t)l0 * s->stride_layer;
-            const size_t in = (size_t)s->input * hc->head_dim;
-            ss.w1t = static_cast<const char*>(s->w1t) + (size_t)sc0 * s->hidden * in * esz;
-            ss.b1 = s->b1 + sc0 * s->hidden;
-            ss.w2 = s->w2 + sc0 * s->hidden;
-            ss.n_scorers = (int32_t)(s->n_scorers - sc0);
-            bool made = false;
-            if ((st = run_score(&sub, &ss, scores + first_head * hc->max_tokens, strm, 1, hist + first_head * 2048,
-                                at<ErrWord>(ws, w.err), &made, /*clear_hist=*/false)))
-                return st;
-            hist_made = made;
+            if (!(ch.ready = mk())) return fail(LKV_ERR_CUDA, "event creation failed");
+            LKV_CUDA(cudaEventRecord(ch.ready, cs), "event record");
+            chunks.push_back(ch);
         }
+        cbase += (int64_t)L * H * cph;
     }
+    // 2. the host needs the ragged offsets to size the per-chunk copy-back
+    if (host_out) LKV_CUDA(cudaEventSynchronize(join), "offsets wait");
+    LKV_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 2048 * (size_t)n_heads, strm), "hist clear");
     LKV_CUDA(cudaStreamWaitEvent(strm, join, 0), "stream wait");
-    lkv_cache_desc gsrc = *hc;
-    gsrc.keys = dev_keys;
-    gsrc.values = kv ? dev_values : v_dev_alias;
-    if ((st = run_select(&gsrc, scores, budgets, out, ws, w, true, strm, hist_made))) return st;
-    if (host_out) {
-        if (!host_out->keys || !host_out->values || !host_out->positions || !host_out->offsets || !host_out->lens ||
-            host_out->capacity_rows < out->capacity_rows)
-            return fail(LKV_ERR_CONTRACT, "host_out buffers missing or too small");
-        cudaEvent_t done = mk(), back = mk();
-        if (!done || !back) return fail(LKV_ERR_CUDA, "event creation failed");
+    // 3. per chunk: score -> select + gather -> copy back
+    for (const Chunk& ch : chunks) {
+        LKV_CUDA(cudaStreamWaitEvent(strm, ch.ready, 0), "stream wait");
+        lkv_cache_desc sub = *hc;
+        sub.n_seq = 1;
+        sub.n_layers = ch.nl;
+        sub.keys = static_cast<char*>(dev_keys) + ch.h0 * head_bytes;
+        sub.values = kv ? static_cast<char*>(dev_values) + ch.h0 * head_bytes : sub.keys;
+        sub.seq_lens = hc->seq_lens + ch.sq;
+        lkv_scorer_desc ss = *s;
+        const int64_t sc0 = (int64_t)ch.l0 * s->stride_layer;
+        const size_t in = (size_t)s->input * hc->head_dim;
+        ss.w1t = static_cast<const char*>(s->w1t) + (size_t)sc0 * s->hidden * in * esz;
+        ss.b1 = s->b1 + sc0 * s->hidden;
+        ss.w2 = s->w2 + sc0 * s->hidden;
+        ss.n_scorers = (int32_t)(s->n_scorers - sc0);
+        float* sc = scores + ch.h0 * hc->max_tokens;
+        bool made = false;
+        if ((st = run_score(&sub, &ss, sc, strm, 0, hist + ch.h0 * 2048, at<ErrWord>(ws, w.err), &made,
+                            /*clear_hist=*/false)))
+            return st;
+        lkv_cache_desc gsrc = sub;
+        gsrc.values = kv ? sub.values : v_dev_alias + ch.h0 * head_bytes;
+        if ((st = run_select(&gsrc, sc, budgets, out, ws, w, true, strm, made, ch.h0, ch.c0))) return st;
+        if (!host_out) continue;
+        cudaEvent_t done = mk();
+        if (!done) return fail(LKV_ERR_CUDA, "event creation failed");
         LKV_CUDA(cudaEventRecord(done, strm), "event record");
-        LKV_CUDA(cudaStreamWaitEvent(cs, done, 0), "stream wait");
-        const size_t rowb = (size_t)hc->head_dim * esz, rows = (size_t)out->capacity_rows;
-        LKV_CUDA(cudaMemcpyAsync(host_out->keys, out->keys, rows * rowb, cudaMemcpyDeviceToHost, cs), "D2H");
-        LKV_CUDA(cudaMemcpyAsync(host_out->values, out->values, rows * rowb, cudaMemcpyDeviceToHost, cs), "D2H");
-        LKV_CUDA(cudaMemcpyAsync(host_out->positions, out->positions, rows * 4, cudaMemcpyDeviceToHost, cs), "D2H");
-        LKV_CUDA(cudaMemcpyAsync(host_out->offsets, out->offsets, sizeof(int64_t) * (out->n_heads + 1),
-                                 cudaMemcpyDeviceToHost, cs),
+        LKV_CUDA(cudaStreamWaitEvent(ds, done, 0), "stream wait");
+        const int64_t nh = (int64_t)ch.nl * H;
+        const int64_t r0 = host_out->offsets[ch.h0], r1 = host_out->offsets[ch.h0 + nh];
+        if (r0 < 0 || r1 < r0 || r1 > out->capacity_rows)  // K2 failed (latched in the workspace) or capacity short
+            return fail(LKV_ERR_CONTRACT, "ragged offsets exceed the output capacity (see lkv_workspace_status)");
+        if (r1 > r0) {
+            LKV_CUDA(cudaMemcpyAsync(static_cast<char*>(host_out->keys) + r0 * rowb,
+                                     static_cast<const char*>(out->keys) + r0 * rowb, (r1 - r0) * rowb,
+                                     cudaMemcpyDeviceToHost, ds),
+                     "D2H");
+            LKV_CUDA(cudaMemcpyAsync(static_cast<char*>(host_out->values) + r0 * rowb,
+                                     static_cast<const char*>(out->values) + r0 * rowb, (r1 - r0) * rowb,
+                                     cudaMemcpyDeviceToHost, ds),
+                     "D2H");
+            LKV_CUDA(cudaMemcpyAsync(host_out->positions + r0, out->positions + r0, (r1 - r0) * sizeof(int32_t),
+                                     cudaMemcpyDeviceToHost, ds),
+                     "D2H");
+        }
+        LKV_CUDA(cudaMemcpyAsync(host_out->lens + ch.h0, out->lens + ch.h0, nh * sizeof(int32_t),
+                                 cudaMemcpyDeviceToHost, ds),
                  "D2H");
-        LKV_CUDA(cudaMemcpyAsync(host_out->lens, out->lens, sizeof(int32_t) * out->n_heads, cudaMemcpyDeviceToHost, cs),
-                 "D2H");
-        LKV_CUDA(cudaEventRecord(back, cs), "event record");
+    }
+    if (host_out) {
+        cudaEvent_t back = mk();
+        if (!back) return fail(LKV_ERR_CUDA, "event creation failed");
+        LKV_CUDA(cudaEventRecord(back, ds), "event record");
         LKV_CUDA(cudaStreamWaitEvent(strm, back, 0), "stream wait");
     }
     return LKV_OK;

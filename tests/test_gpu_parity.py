@@ -520,10 +520,12 @@ def test_decode_many_steps_stays_consistent():
         assert (np.diff(p) > 0).all() and p[-1] == 2000 + 199
 
 
-@pytest.mark.parametrize("cid,inp", [(2, lkv.SCORER_K), (4, lkv.SCORER_K), (2, lkv.SCORER_KV)])
-def test_evict_from_host_memory_matches_device_path(cid, inp):
-    """lkv_evict_host (K streamed in chunks, kept V gathered over PCIe from pinned host memory,
-    result copied back) produces exactly the device-resident eviction."""
+@pytest.mark.parametrize("cid,inp,chunk", [(2, lkv.SCORER_K, 2), (4, lkv.SCORER_K, 2), (2, lkv.SCORER_KV, 2),
+                                            (1, lkv.SCORER_K, 1), (4, lkv.SCORER_K, 3), (4, lkv.SCORER_K, 5)])
+def test_evict_from_host_memory_matches_device_path(cid, inp, chunk):
+    """lkv_evict_host (per-chunk pipeline: K streamed in, scored, selected, kept V gathered over
+    PCIe from pinned host memory, chunk copied back while later chunks upload) produces exactly
+    the device-resident eviction, for chunkings that split, cover and exceed the layer count."""
     cfg = synth.CONFIGS[cid]
     L, T, S = 3, 5000, (3 if cfg.n_seq > 1 else 1)
     cache = synth.make_cache(cfg, n_layers=L, max_tokens=T, n_seq=S)
@@ -540,8 +542,9 @@ def test_evict_from_host_memory_matches_device_path(cid, inp):
     dense = lkv.DenseCache(torch.zeros_like(cache.keys), torch.zeros_like(cache.values), cache.seq_lens)
     ev = lkv.Evictor(dense, scorers, logits, cfg.ratio, lkv.BUDGET_EXACT, decode_slack=2)
     out = ev.host_result_buffer()
-    ev.launch_host(hk, hv, out, layers_per_chunk=2)
+    ev.launch_host(hk, hv, out, layers_per_chunk=chunk)
     ev.ws.status()
+    torch.cuda.synchronize()
     assert torch.equal(ev.ragged.lens, ref.cache.lens)
     assert torch.equal(out.lens, ref.cache.lens.cpu())
     assert torch.equal(out.offsets, ref.cache.offsets.cpu())
@@ -550,6 +553,25 @@ def test_evict_from_host_memory_matches_device_path(cid, inp):
         ko, vo, po = ref.cache.head(h)
         assert torch.equal(out.positions[o:o + n], po.cpu())
         assert torch.equal(out.keys[o:o + n], ko.cpu()) and torch.equal(out.values[o:o + n], vo.cpu())
+
+
+def test_evict_from_host_memory_without_copy_back():
+    """host_out = NULL: the compacted cache stays on the device, identical to lkv_evict's."""
+    cfg = synth.CONFIGS[2]
+    cache = synth.make_cache(cfg, n_layers=5, max_tokens=3000)
+    scorers = synth.make_scorers(cfg, n_layers=5)
+    logits = synth.make_logits(cfg, n_layers=5)
+    ref = lkv.evict(cache, scorers, logits, cfg.ratio, lkv.BUDGET_EXACT, decode_slack=1)
+    dense = lkv.DenseCache(torch.zeros_like(cache.keys), torch.zeros_like(cache.values), cache.seq_lens)
+    ev = lkv.Evictor(dense, scorers, logits, cfg.ratio, lkv.BUDGET_EXACT, decode_slack=1)
+    ev.launch_host(cache.keys.cpu().pin_memory(), cache.values.cpu().pin_memory(), None, layers_per_chunk=2)
+    ev.ws.status()
+    torch.cuda.synchronize()
+    assert torch.equal(ev.ragged.offsets, ref.cache.offsets) and torch.equal(ev.ragged.lens, ref.cache.lens)
+    for h in range(cache.n_heads):
+        k, v, p = ev.ragged.head(h)
+        ko, vo, po = ref.cache.head(h)
+        assert torch.equal(p, po) and torch.equal(k, ko) and torch.equal(v, vo)
 
 
 def test_evict_is_deterministic():
