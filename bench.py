@@ -454,6 +454,136 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def run_sharded(args, rank, world, local_rank):
+    """--shard heads: ONE long sequence (default C3, t = 131072) split by layer range over the
+    ranks (strong scaling).  Per step: the LKV-H logits allgatherv through the library's NCCL
+    communicator, then lkv_evict_shard on this rank's layers (K2 solves the global threshold
+    redundantly).  Decode: every rank decodes its layers, outputs gathered to rank 0 (NCCL
+    gatherv) every step."""
+    import torch
+
+    import paper_2605_06676_b200 as lkv
+    from paper_2605_06676_b200 import sharded, synth
+
+    torch.cuda.set_device(local_rank)
+    dev = f"cuda:{local_rank}"
+    assert lkv.lib().lkv_device_check() == 0, lkv.lib().lkv_last_error()
+    cid = args.config if args.config != 2 else 3
+    cfg = synth.CONFIGS[cid]
+    if args.ratio:
+        cfg = synth.Config(**{**cfg.__dict__, "ratio": args.ratio})
+    hbm_peak, _, peak_src = load_peaks()
+    comm = sharded.Comm.from_process_group()
+    L, H, D = cfg.n_layers, cfg.n_kv_heads, cfg.head_dim
+    plan = sharded.ShardPlan(L, H, world)
+    l0, l1 = plan.layers[rank]
+    h0, n_local = plan.head_range(rank)
+    log(f"inputs: layers [{l0}, {l1})")
+    # this rank's layers only (the same seeded data an unsharded run would hold for them)
+    full_scorers = synth.make_scorers(cfg, device=dev)
+    gen = torch.Generator(device=dev).manual_seed(1000 + cid + 31 * rank)
+    T = cfg.max_tokens
+    K = torch.empty(cfg.n_seq, l1 - l0, H, T, D, dtype=cfg.dtype, device=dev)
+    V = torch.empty_like(K)
+    for X in (K, V):
+        for i in range(l1 - l0):
+            X[:, i].copy_(torch.randn(cfg.n_seq, H, T, D, generator=gen, device=dev).to(cfg.dtype))
+    cache = lkv.DenseCache(K, V, [T] * cfg.n_seq)
+    scorers = lkv.Scorers(full_scorers.w1[l0:l1], full_scorers.b1[l0:l1], full_scorers.w2[l0:l1])
+    local_logits = synth.make_logits(cfg, device=dev)[h0:h0 + n_local].contiguous()
+    ev = sharded.ShardEvictor(cache, scorers, plan, rank, cfg.ratio, lkv.BUDGET_EXACT,
+                              decode_slack=cfg.decode_steps + 4)
+    rows_total = L * H * T * cfg.n_seq
+    lib = lkv.lib()
+    stream = torch.cuda.current_stream()
+
+    def step():
+        logits = sharded.gather_logits(comm, plan, local_logits)
+        ev.launch(logits)
+
+    step()
+    ev.ws.status()
+    kept_local = torch.tensor([int(ev.ragged.lens.sum())], dtype=torch.int64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(kept_local)
+    assert int(kept_local.item()) == round(cfg.ratio * L * H * T) * cfg.n_seq
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l_before = lib.lkv_launch_count()
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        barrier()
+    launches = lib.lkv_launch_count() - l_before
+    ev.ws.status()
+    ms = e0.elapsed_time(e1) / args.steps
+    ms = sharded_max(ms, world, dev)
+    decode = None
+    if not args.no_decode:
+        rc = ev.ragged
+        rc.tokens_seen.copy_(torch.tensor(cache.seq_lens, dtype=torch.int32))
+        G = cfg.n_q_heads // H
+        lkv.decode_plan(rc, G)
+        qs = [synth.make_decode_inputs(cfg, st, device=dev, n_layers=l1 - l0, seed=rank) for st in range(2)]
+        out_local = torch.empty_like(qs[0][0])
+        nsteps = cfg.decode_steps
+        lens0 = rc.lens.clone()
+        for st in range(2):
+            sharded.decode_and_gather(comm, plan, rc, *qs[st], out_local=out_local)
+        barrier()
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        rc.lens.copy_(lens0)
+        barrier()
+        d0.record(stream)
+        for st in range(nsteps - 2):
+            gathered = sharded.decode_and_gather(comm, plan, rc, *qs[st & 1], out_local=out_local)
+        d1.record(stream)
+        barrier()
+        rc._decode_ws.status()
+        ms_dec = sharded_max(d0.elapsed_time(d1) / (nsteps - 2), world, dev)
+        mean_len = float(lens0.double().sum()) + (nsteps - 2) / 2 * rc.n_heads
+        dec_bytes = torch.tensor([mean_len * 2 * D * cache.keys.element_size()], dtype=torch.float64, device=dev)
+        if world > 1:
+            torch.distributed.all_reduce(dec_bytes)
+        dec_gbs = float(dec_bytes.item()) / (ms_dec / 1e3) / 1e9
+        decode = {"steps": nsteps - 2, "ms_per_step": ms_dec, "hbm_gbs_all_ranks": dec_gbs,
+                  "frac_of_measured_hbm_per_gpu": dec_gbs / world / hbm_peak,
+                  "note": "each rank decodes its layers; outputs NCCL-gathered to rank 0 every step"}
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": rows_total / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": f"synthetic (seeded; BASELINE.json configs[{cid - 1}] shapes)",
+            "config": {"workload": f"C{cid}: L{L} x H{H} x d{D}, t={T}, batch {cfg.n_seq}, R={cfg.ratio}, exact budgets",
+                       "parallelism": f"head-sharded (layer ranges) x{world}", "rows_per_step": rows_total,
+                       "l2": "inputs larger than L2; no flush"},
+            "north_star_target_ms": 5.0, "clocks": clk.summary(), "gpu_launches": int(launches),
+            "exchange": "LKV-H logits allgatherv + decode-output gatherv via lkv_comm_* (NCCL)",
+            "peak_source": peak_src, "decode": decode, "e2e": None}), flush=True)
+    comm.close()
+
+
+def sharded_max(v, world, dev):
+    if world == 1:
+        return v
+    import torch
+
+    t = torch.tensor([v], device=dev)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -467,6 +597,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-heads", type=int, default=8)
     ap.add_argument("--e2e-chunk", type=int, default=1, help="layers per host->device chunk in the e2e path")
+    ap.add_argument("--shard", default="batch", choices=["batch", "heads"],
+                    help="batch: one sequence per GPU (weak scaling, default); heads: one long sequence split by "
+                         "layer range over the GPUs (strong scaling, NCCL logits/outputs exchange)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -482,7 +615,7 @@ def main():
         torch.cuda.set_device(local_rank)
         torch.distributed.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
     try:
-        run_ours(args, rank, world, local_rank)
+        (run_sharded if args.shard == "heads" else run_ours)(args, rank, world, local_rank)
     finally:
         if world > 1:
             import torch

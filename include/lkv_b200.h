@@ -17,6 +17,7 @@
  *   lkv_evict       <- prefill_with_eviction's score->select->compact loop
  *                      (evictsim.hpp:74, evictsim.cpp:161-215), K/V-given form
  *   lkv_evict_host  <- the same, for a cache resident in (pinned) host memory
+ *   lkv_evict_shard <- the same on one rank's head shard (multi-GPU; lkv_comm_* = NCCL)
  *   lkv_decode_step <- decode_step's append + attention block (model.hpp:95,
  *                      model.cpp:240-265) -> masked_attention_dense (attention.hpp:57)
  *   lkv_model_*     <- the whole decode_step (model.hpp:95, model.cpp:209-287):
@@ -61,7 +62,8 @@ typedef enum lkv_status {
     LKV_ERR_OVERFLOW_GUARD = 4,  /* lkv::overflow_guard_error  errors.hpp:35-37 */
     LKV_ERR_DEGENERATE_MASK = 5, /* lkv::degenerate_mask_error errors.hpp:40-42 */
     LKV_ERR_CUDA = 6,            /* CUDA runtime / launch failure (no reference analogue) */
-    LKV_ERR_UNSUPPORTED = 7      /* device is not sm_100 or shape outside the kernel envelope */
+    LKV_ERR_UNSUPPORTED = 7,     /* device is not sm_100 or shape outside the kernel envelope */
+    LKV_ERR_NCCL = 8             /* NCCL missing or a collective failed (multi-GPU plumbing only) */
 } lkv_status;
 
 typedef enum lkv_dtype { LKV_F32 = 0, LKV_BF16 = 1 } lkv_dtype;
@@ -207,6 +209,41 @@ lkv_status lkv_evict_host(const lkv_cache_desc* host_cache, void* dev_keys, void
                           int32_t mode, const lkv_ragged_desc* out, const lkv_ragged_desc* host_out,
                           int32_t layers_per_chunk, void* workspace, size_t workspace_bytes,
                           lkv_stream_t stream);
+
+/* ---- head shards (multi-GPU: one process per GPU) -------------------- */
+/* A rank owns a contiguous range of flat per-sequence heads [head_begin, head_begin +
+ * n_layers*n_kv_heads) -- i.e. a layer range -- of every sequence; its local cache/scorers
+ * describe only those layers.  LKV-H is one Soft-TopK over ALL n_logits heads
+ * (policy.cpp:110-120), so every rank solves it redundantly from the full logit vector (see
+ * lkv_comm_allgatherv) and freezes every head's budget bit-identically; only its own heads'
+ * budgets ([n_seq][n_local]) and ragged offsets are kept. */
+lkv_status lkv_budgets_shard(const double* logits, int32_t n_logits, double target_ratio, int32_t mode,
+                             const int32_t* seq_lens, int32_t n_seq, int32_t decode_slack, int32_t head_begin,
+                             int32_t n_local, double* ratios, int32_t* budgets_all, int32_t* budgets_local,
+                             int64_t* offsets_local, void* workspace, size_t workspace_bytes, lkv_stream_t stream);
+/* lkv_evict on a head shard; the workspace is lkv_workspace_bytes(local_cache, n_logits). */
+lkv_status lkv_evict_shard(const lkv_cache_desc* local_cache, const lkv_scorer_desc* scorer, const double* logits,
+                           int32_t n_logits, int32_t head_begin, double target_ratio, int32_t mode,
+                           const lkv_ragged_desc* out, float* scores_out, double* ratios_out, int32_t* budgets_out,
+                           void* workspace, size_t workspace_bytes, lkv_stream_t stream);
+/* Upper bound on a shard's compacted rows (caller allocates; -1 on bad input). */
+int64_t lkv_ragged_capacity_shard(const lkv_cache_desc* local_cache, int32_t n_logits, double target_ratio,
+                                  int32_t decode_slack);
+
+/* NCCL over NVLink/NVSwitch (resolved at run time from libnccl.so.2).  The path's only
+ * exchanges: the LKV-H logits (allgatherv, a few KB) and the decode outputs (gatherv to a
+ * root, or allgatherv), both latency-bound.  Byte counts/displacements are per rank. */
+#define LKV_COMM_ID_BYTES 128
+typedef struct lkv_comm_s* lkv_comm_t;
+lkv_status lkv_comm_get_unique_id(void* id /* LKV_COMM_ID_BYTES */);
+lkv_status lkv_comm_init(lkv_comm_t* comm, const void* id, int32_t n_ranks, int32_t rank);
+lkv_status lkv_comm_destroy(lkv_comm_t comm);
+int32_t lkv_comm_size(lkv_comm_t comm);
+int32_t lkv_comm_rank(lkv_comm_t comm);
+lkv_status lkv_comm_allgatherv(lkv_comm_t comm, const void* send, void* recv, const int64_t* bytes,
+                               const int64_t* displs, lkv_stream_t stream);
+lkv_status lkv_comm_gatherv(lkv_comm_t comm, const void* send, void* recv, const int64_t* bytes,
+                            const int64_t* displs, int32_t root, lkv_stream_t stream);
 
 /* ---- K/V production for layer-by-layer prefill (the step before the path) -------- */
 /* cos/sin table [t_max][head_dim/2] of float2 (cos, sin) for positions pos_offset + p,

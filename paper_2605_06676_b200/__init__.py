@@ -74,8 +74,12 @@ class UnsupportedError(LkvError):
     code = _abi.UNSUPPORTED
 
 
+class NcclError(LkvError):
+    code = _abi.NCCL
+
+
 _ERR = {c.code: c for c in (ContractError, NumericError, BudgetError, OverflowGuardError, DegenerateMaskError,
-                            CudaError, UnsupportedError)}
+                            CudaError, UnsupportedError, NcclError)}
 
 
 def lib():

@@ -14,7 +14,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # LKV_B200_LIB overrides the path (developer A/B builds of the same library only)
 LIB_PATH = os.environ.get("LKV_B200_LIB") or os.path.join(_HERE, "liblkv_b200.so")
 
-LKV_OK, CONTRACT, NUMERIC, BUDGET, OVERFLOW_GUARD, DEGENERATE_MASK, CUDA, UNSUPPORTED = range(8)
+LKV_OK, CONTRACT, NUMERIC, BUDGET, OVERFLOW_GUARD, DEGENERATE_MASK, CUDA, UNSUPPORTED, NCCL = range(9)
+COMM_ID_BYTES = 128
 F32, BF16 = 0, 1
 SILU, GELU_ERF = 0, 1
 SCORER_K, SCORER_KV = 1, 2
@@ -26,7 +27,8 @@ EXPORTED = [
     "lkv_workspace_init", "lkv_workspace_status", "lkv_ragged_capacity", "lkv_budgets", "lkv_freeze_budgets", "lkv_ragged_offsets",
     "lkv_score", "lkv_select", "lkv_compact", "lkv_evict", "lkv_evict_host", "lkv_rope_table", "lkv_rope_pack", "lkv_decode_workspace_bytes", "lkv_decode_plan",
     "lkv_decode_step", "lkv_model_validate", "lkv_model_weights_bytes", "lkv_model_load_param", "lkv_model_workspace_bytes", "lkv_model_plan",
-    "lkv_model_decode_step",
+    "lkv_model_decode_step", "lkv_budgets_shard", "lkv_evict_shard", "lkv_ragged_capacity_shard", "lkv_comm_get_unique_id",
+    "lkv_comm_init", "lkv_comm_destroy", "lkv_comm_size", "lkv_comm_rank", "lkv_comm_allgatherv", "lkv_comm_gatherv",
 ]
 
 
@@ -107,6 +109,23 @@ def load():
     L.lkv_model_workspace_bytes.argtypes = [P(ModelDesc), i32, P(RaggedDesc)]
     L.lkv_model_plan.argtypes = [P(ModelDesc), P(RaggedDesc), i32, vp, sz, vp]
     L.lkv_model_decode_step.argtypes = [P(ModelDesc), vp, P(RaggedDesc), i32, vp, vp, vp, vp, sz, vp]
+    L.lkv_budgets_shard.argtypes = [vp, i32, dbl, i32, P(i32), i32, i32, i32, i32, vp, vp, vp, vp, vp, sz, vp]
+    L.lkv_evict_shard.argtypes = [P(CacheDesc), P(ScorerDesc), vp, i32, i32, dbl, i32, P(RaggedDesc), vp, vp, vp, vp,
+                                  sz, vp]
+    L.lkv_ragged_capacity_shard.restype = i64
+    L.lkv_ragged_capacity_shard.argtypes = [P(CacheDesc), i32, dbl, i32]
+    L.lkv_comm_get_unique_id.argtypes = [vp]
+    L.lkv_comm_init.argtypes = [P(vp), vp, i32, i32]
+    L.lkv_comm_destroy.argtypes = [vp]
+    L.lkv_comm_size.restype = i32
+    L.lkv_comm_size.argtypes = [vp]
+    L.lkv_comm_rank.restype = i32
+    L.lkv_comm_rank.argtypes = [vp]
+    L.lkv_comm_allgatherv.argtypes = [vp, vp, vp, P(i64), P(i64), vp]
+    L.lkv_comm_gatherv.argtypes = [vp, vp, vp, P(i64), P(i64), i32, vp]
+    for name in ["lkv_budgets_shard", "lkv_evict_shard", "lkv_comm_get_unique_id", "lkv_comm_init", "lkv_comm_destroy",
+                 "lkv_comm_allgatherv", "lkv_comm_gatherv"]:
+        getattr(L, name).restype = C.c_int
     for name in ["lkv_workspace_init", "lkv_workspace_status", "lkv_budgets", "lkv_freeze_budgets", "lkv_ragged_offsets", "lkv_score",
                  "lkv_select", "lkv_compact", "lkv_evict", "lkv_evict_host", "lkv_rope_table", "lkv_rope_pack", "lkv_decode_plan", "lkv_decode_step",
                  "lkv_model_validate", "lkv_model_load_param", "lkv_model_plan", "lkv_model_decode_step"]:

@@ -114,6 +114,9 @@ __device__ void freeze_and_offsets(const BudgetParams& p, const double* r, doubl
         }
         __syncthreads();
         for (int i = tid; i < n; i += kBudgetThreads) p.budgets_out[(size_t)s * n + i] = fl[i] + delta[i];
+        if (p.local_count > 0)
+            for (int i = tid; i < p.local_count; i += kBudgetThreads)
+                p.budgets_local_out[(size_t)s * p.local_count + i] = fl[p.local_begin + i] + delta[p.local_begin + i];
         __syncthreads();
     }
 
@@ -121,12 +124,14 @@ __device__ void freeze_and_offsets(const BudgetParams& p, const double* r, doubl
     if (p.offsets_out) {
         __threadfence_block();
         __syncthreads();
-        const int64_t total_heads = (int64_t)p.n_seq * n;
+        const bool shard = p.local_count > 0;
+        const int64_t total_heads = (int64_t)p.n_seq * (shard ? p.local_count : n);
+        const int32_t* bsrc = shard ? p.budgets_local_out : p.budgets_out;
         if (tid == 0) s_carry = 0;
         __syncthreads();
         for (int64_t base = 0; base < total_heads; base += kBudgetThreads) {
             const int64_t i = base + tid;
-            const uint32_t v = i < total_heads ? uint32_t(p.budgets_out[i] + p.slack) : 0u;
+            const uint32_t v = i < total_heads ? uint32_t(bsrc[i] + p.slack) : 0u;
             uint32_t tot;
             const uint32_t ex = block_exclusive_scan<kBudgetThreads>(v, s_scan, &tot);
             if (i < total_heads) p.offsets_out[i] = s_carry + ex;

@@ -22,13 +22,18 @@
 using namespace lkv_dev;
 
 namespace {
-
 thread_local std::string g_err;
+}  // namespace
 
-lkv_status fail(lkv_status code, const std::string& msg) {
+// shared with comm.cu
+lkv_status lkv_internal_fail(lkv_status code, const std::string& msg) {
     g_err = msg;
     return code;
 }
+
+namespace {
+
+lkv_status fail(lkv_status code, const std::string& msg) { return lkv_internal_fail(code, msg); }
 
 lkv_status cuda_fail(cudaError_t e, const char* where) {
     return fail(LKV_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
@@ -136,7 +141,7 @@ int64_t n_heads_of(const lkv_cache_desc* c) { return (int64_t)c->n_seq * c->n_la
 
 // ---- workspace layout -----------------------------------------------------------------------------
 struct EvictWs {
-    size_t err, ratios, budgets, scores, hist, state, chunk_gt, chunk_out, chunk_eqb, cands, total;
+    size_t err, ratios, budgets, budgets_all, scores, hist, state, chunk_gt, chunk_out, chunk_eqb, cands, total;
 };
 
 EvictWs evict_layout(const lkv_cache_desc* c, int n_logits) {
@@ -151,6 +156,8 @@ EvictWs evict_layout(const lkv_cache_desc* c, int n_logits) {
     o = align_up(o + sizeof(double) * (size_t)(n_logits > 0 ? n_logits : 1));
     w.budgets = o;
     o = align_up(o + sizeof(int32_t) * (size_t)H);
+    w.budgets_all = o;  // [n_seq][n_logits]: every head's budget when this cache is a head shard
+    o = align_up(o + sizeof(int32_t) * (size_t)c->n_seq * (size_t)(n_logits > 0 ? n_logits : 1));
     w.scores = o;
     o = align_up(o + sizeof(float) * (size_t)H * c->max_tokens);
     w.hist = o;
@@ -335,6 +342,7 @@ const char* lkv_status_name(int s) {
         case LKV_ERR_DEGENERATE_MASK: return "degenerate_mask_error";
         case LKV_ERR_CUDA: return "cuda_error";
         case LKV_ERR_UNSUPPORTED: return "unsupported";
+        case LKV_ERR_NCCL: return "nccl_error";
     }
     return "unknown";
 }
@@ -385,6 +393,15 @@ int64_t lkv_ragged_capacity(const lkv_cache_desc* c, double R, int32_t slack) {
     return rows + n_heads_of(c) * (int64_t)slack;
 }
 
+int64_t lkv_ragged_capacity_shard(const lkv_cache_desc* c, int32_t n_logits, double R, int32_t slack) {
+    if (check_cache(c, false) || n_logits < 1) return -1;
+    const int64_t nl = (int64_t)c->n_layers * c->n_kv_heads;
+    int64_t rows = 0;
+    for (int s = 0; s < c->n_seq; ++s)  // the shard holds at most the whole budget, at most every row
+        rows += std::min<int64_t>(llround(R * n_logits * c->seq_lens[s]) + n_logits, nl * c->seq_lens[s]);
+    return rows + n_heads_of(c) * (int64_t)slack;
+}
+
 lkv_status lkv_budgets(const double* logits, int32_t n, double R, int32_t mode, const int32_t* seq_lens, int32_t n_seq,
                        int32_t slack, double* ratios, int32_t* budgets, int64_t* offsets, void* ws, size_t ws_bytes,
                        lkv_stream_t stream) {
@@ -412,6 +429,43 @@ lkv_status lkv_budgets(const double* logits, int32_t n, double R, int32_t mode, 
     p.err = at<ErrWord>(ws, 0);
     for (int s = 0; s < n_seq; ++s) p.seq_len[s] = seq_lens[s];
     LKV_CUDA(launch_budgets(p, (cudaStream_t)stream), "budgets");
+    return LKV_OK;
+}
+
+lkv_status lkv_budgets_shard(const double* logits, int32_t n, double R, int32_t mode, const int32_t* seq_lens,
+                             int32_t n_seq, int32_t slack, int32_t head_begin, int32_t n_local, double* ratios,
+                             int32_t* budgets_all, int32_t* budgets_local, int64_t* offsets_local, void* ws,
+                             size_t ws_bytes, lkv_stream_t stream) {
+    if (n_local < 1 || head_begin < 0 || (int64_t)head_begin + n_local > n)
+        return fail(LKV_ERR_CONTRACT, "budgets_shard: need 0 <= head_begin and head_begin + n_local <= n");
+    if (!budgets_all || !budgets_local) return fail(LKV_ERR_CONTRACT, "budgets_shard: null budget buffers");
+    if (!(R > 0.0 && R < 1.0)) return fail(LKV_ERR_BUDGET, "target ratio must lie in (0,1)");  // policy.cpp:111
+    if (n > 3072) return fail(LKV_ERR_CONTRACT, "allocate_budgets: need 1 <= n <= 3072 head logits");
+    if (mode != LKV_BUDGET_FLOOR && mode != LKV_BUDGET_EXACT) return fail(LKV_ERR_CONTRACT, "unknown budget mode");
+    if (n_seq < 1 || n_seq > LKV_MAX_SEQ || !seq_lens) return fail(LKV_ERR_CONTRACT, "bad sequence table");
+    for (int s = 0; s < n_seq; ++s)
+        if (seq_lens[s] < 1) return fail(LKV_ERR_CONTRACT, "freeze_budgets: t must be >= 1");  // policy.cpp:123
+    if (!logits) return fail(LKV_ERR_CONTRACT, "logits are null");
+    if (slack < 0) return fail(LKV_ERR_CONTRACT, "decode_slack must be >= 0");
+    lkv_status st = check_ws(ws, ws_bytes, sizeof(ErrWord));
+    if (st) return st;
+    BudgetParams p;
+    memset(&p, 0, sizeof p);
+    p.logits = logits;
+    p.n = n;
+    p.mode = mode;
+    p.R = R;
+    p.n_seq = n_seq;
+    p.slack = slack;
+    p.ratios_out = ratios;
+    p.budgets_out = budgets_all;
+    p.offsets_out = offsets_local;
+    p.local_begin = head_begin;
+    p.local_count = n_local;
+    p.budgets_local_out = budgets_local;
+    p.err = at<ErrWord>(ws, 0);
+    for (int s = 0; s < n_seq; ++s) p.seq_len[s] = seq_lens[s];
+    LKV_CUDA(launch_budgets(p, (cudaStream_t)stream), "budgets (shard)");
     return LKV_OK;
 }
 
@@ -497,17 +551,16 @@ lkv_status lkv_compact(const lkv_cache_desc* c, const lkv_ragged_desc* out, lkv_
     return LKV_OK;
 }
 
-lkv_status lkv_evict(const lkv_cache_desc* c, const lkv_scorer_desc* s, const double* logits, double R, int32_t mode,
-                     const lkv_ragged_desc* out, float* scores_out, double* ratios_out, int32_t* budgets_out, void* ws,
-                     size_t ws_bytes, lkv_stream_t stream) {
+static lkv_status evict_impl(const lkv_cache_desc* c, const lkv_scorer_desc* s, const double* logits, int n,
+                             int head_begin, bool shard, double R, int32_t mode, const lkv_ragged_desc* out,
+                             float* scores_out, double* ratios_out, int32_t* budgets_out, void* ws, size_t ws_bytes,
+                             cudaStream_t strm) {
     lkv_status st = check_cache(c, true);
     if (st) return st;
     if ((st = check_scorer(s, c))) return st;
     if ((st = check_ragged(out, n_heads_of(c), c->head_dim, c->dtype, true))) return st;
-    const int n = c->n_layers * c->n_kv_heads;
     const EvictWs w = evict_layout(c, n);
     if ((st = check_ws(ws, ws_bytes, w.total))) return st;
-    cudaStream_t strm = (cudaStream_t)stream;
     int32_t* budgets = budgets_out ? budgets_out : at<int32_t>(ws, w.budgets);
     double* ratios = ratios_out ? ratios_out : at<double>(ws, w.ratios);
     float* scores = scores_out ? scores_out : at<float>(ws, w.scores);
@@ -527,8 +580,13 @@ lkv_status lkv_evict(const lkv_cache_desc* c, const lkv_scorer_desc* s, const do
     } guard{fork, join};
     LKV_CUDA(cudaEventRecord(fork, strm), "event record");
     LKV_CUDA(cudaStreamWaitEvent(side, fork, 0), "stream wait");
-    st = lkv_budgets(logits, n, R, mode, c->seq_lens, c->n_seq, out->decode_slack, ratios, budgets, out->offsets, ws,
-                     ws_bytes, (lkv_stream_t)side);
+    if (shard)
+        st = lkv_budgets_shard(logits, n, R, mode, c->seq_lens, c->n_seq, out->decode_slack, head_begin,
+                               c->n_layers * c->n_kv_heads, ratios, at<int32_t>(ws, w.budgets_all), budgets,
+                               out->offsets, ws, ws_bytes, (lkv_stream_t)side);
+    else
+        st = lkv_budgets(logits, n, R, mode, c->seq_lens, c->n_seq, out->decode_slack, ratios, budgets, out->offsets,
+                         ws, ws_bytes, (lkv_stream_t)side);
     if (st) return st;
     LKV_CUDA(cudaEventRecord(join, side), "event record");
     bool hist_made = false;  // the tcgen05 scorer fuses top-k pass 1 (the histogram) into its epilogue
@@ -537,6 +595,24 @@ lkv_status lkv_evict(const lkv_cache_desc* c, const lkv_scorer_desc* s, const do
         return st;
     LKV_CUDA(cudaStreamWaitEvent(strm, join, 0), "stream wait");
     return run_select(c, scores, budgets, out, ws, w, true, strm, hist_made);
+}
+
+lkv_status lkv_evict(const lkv_cache_desc* c, const lkv_scorer_desc* s, const double* logits, double R, int32_t mode,
+                     const lkv_ragged_desc* out, float* scores_out, double* ratios_out, int32_t* budgets_out, void* ws,
+                     size_t ws_bytes, lkv_stream_t stream) {
+    if (!c) return fail(LKV_ERR_CONTRACT, "cache descriptor is null");
+    return evict_impl(c, s, logits, c->n_layers * c->n_kv_heads, 0, false, R, mode, out, scores_out, ratios_out,
+                      budgets_out, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+lkv_status lkv_evict_shard(const lkv_cache_desc* c, const lkv_scorer_desc* s, const double* logits, int32_t n_logits,
+                           int32_t head_begin, double R, int32_t mode, const lkv_ragged_desc* out, float* scores_out,
+                           double* ratios_out, int32_t* budgets_out, void* ws, size_t ws_bytes, lkv_stream_t stream) {
+    if (!c) return fail(LKV_ERR_CONTRACT, "cache descriptor is null");
+    if (n_logits < 1 || head_begin < 0 || (int64_t)head_begin + (int64_t)c->n_layers * c->n_kv_heads > n_logits)
+        return fail(LKV_ERR_CONTRACT, "evict_shard: the shard's heads must lie inside the n_logits global heads");
+    return evict_impl(c, s, logits, n_logits, head_begin, true, R, mode, out, scores_out, ratios_out, budgets_out, ws,
+                      ws_bytes, (cudaStream_t)stream);
 }
 
 // Eviction of a host-resident (pinned, device-mapped) dense cache, pipelined per chunk =

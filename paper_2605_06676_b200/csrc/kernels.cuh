@@ -21,6 +21,12 @@ struct BudgetParams {
     int32_t* budgets_out;
     int64_t* offsets_out;
     ErrWord* err;
+    // head shard (local_count > 0): this rank owns flat heads [local_begin, local_begin +
+    // local_count) of every sequence; budgets_local_out gets them contiguously
+    // ([n_seq][local_count]) and the offsets are scanned over the local heads only.
+    int32_t local_begin;
+    int32_t local_count;
+    int32_t* budgets_local_out;
     int32_t seq_len[LKV_MAX_SEQ];
 };
 cudaError_t launch_budgets(const BudgetParams& p, cudaStream_t stream);

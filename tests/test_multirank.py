@@ -88,3 +88,68 @@ def test_lpt_balances_skewed_budgets():
     assert shard.imbalance([int(x) for x in b], contiguous, 8) > shard.imbalance([int(x) for x in b], owner, 8)
     # deterministic
     assert owner == shard.lpt_assign([int(x) for x in b], 8)
+
+
+def _sharded_worker(rank, world, port, out_dir):
+    """The head-sharded path's host logic through the same interface the NCCL communicator
+    implements (sharded.TorchComm over gloo): logits allgatherv, decode-output gatherv and
+    reassembly, budgets agreeing on every rank."""
+    from paper_2605_06676_b200 import sharded
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        comm = sharded.TorchComm()
+        L, H, Hq, D, n_seq = 5, 8, 32, 16, 3  # 5 layers over 2 ranks: uneven ranges (3 + 2)
+        plan = sharded.ShardPlan(L, H, world)
+        rng = np.random.default_rng(77)
+        full = torch.tensor(rng.normal(0, 1, L * H))
+        h0, n = plan.head_range(rank)
+        got = sharded.gather_logits(comm, plan, full[h0:h0 + n].clone())
+        assert torch.equal(got, full)  # every rank holds the full logit vector
+        # every rank's redundant solve agrees; its slice is its heads' budgets
+        b = O.freeze_budgets_exact(O.allocate_budgets(got.numpy(), 0.15), 0.15, 4096)
+        mine = torch.tensor(b[h0:h0 + n], dtype=torch.int64)
+        parts = [torch.zeros(plan.head_range(r)[1], dtype=torch.int64) for r in range(world)]
+        padded = [torch.zeros(L * H, dtype=torch.int64) for _ in range(world)]
+        pad = torch.zeros(L * H, dtype=torch.int64)
+        pad[:n] = mine
+        dist.all_gather(padded, pad)
+        for r in range(world):
+            parts[r] = padded[r][: plan.head_range(r)[1]]
+        assert torch.equal(torch.cat(parts), torch.tensor(b, dtype=torch.int64))
+        assert int(torch.cat(parts).sum()) == round(0.15 * L * H * 4096)
+        # decode outputs: element (s, l, qh, d) encodes its global coordinates
+        l0, l1 = plan.layers[rank]
+        s_i, l_i, q_i, d_i = torch.meshgrid(torch.arange(n_seq), torch.arange(l0, l1), torch.arange(Hq),
+                                            torch.arange(D), indexing="ij")
+        local = (((s_i * 100 + l_i) * 100 + q_i) * 100 + d_i).to(torch.float64)
+        counts, displs = plan.output_counts(n_seq, Hq * D)
+        gathered = torch.empty(sum(counts), dtype=torch.float64) if rank == 0 else None
+        comm.gatherv(local.reshape(-1), gathered, counts, displs, root=0)
+        if rank == 0:
+            out = plan.assemble(gathered, n_seq, Hq, D)
+            s_i, l_i, q_i, d_i = torch.meshgrid(torch.arange(n_seq), torch.arange(L), torch.arange(Hq),
+                                                torch.arange(D), indexing="ij")
+            assert torch.equal(out, (((s_i * 100 + l_i) * 100 + q_i) * 100 + d_i).to(torch.float64))
+        with open(os.path.join(out_dir, f"ok{rank}"), "w") as f:
+            f.write("ok")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_head_sharded_host_logic(tmp_path):
+    world = 2
+    mp.spawn(_sharded_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    assert all((tmp_path / f"ok{r}").exists() for r in range(world))
+
+
+def test_shard_plan_ranges():
+    from paper_2605_06676_b200 import sharded
+
+    for L, W in ((32, 8), (80, 8), (5, 2), (3, 4)):
+        plan = sharded.ShardPlan(L, 8, W)
+        counts, displs = plan.logit_counts()
+        assert sum(counts) == L * 8 and displs[0] == 0
+        assert all(displs[r] + counts[r] == displs[r + 1] for r in range(W - 1))

@@ -1,0 +1,102 @@
+"""Head-sharded eviction + decode on one B200.
+
+Every shard is independent on the data path, so the N-rank result can be checked on one GPU by
+running each rank's shard in turn (no kernel waits on another rank) and comparing the union with
+the unsharded path: budgets, offsets, kept positions and rows bit-exact, decode outputs equal.
+The NCCL communicator (lkv_comm_*) is exercised with a 1-rank communicator: allgatherv and
+gatherv through NCCL on this GPU.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import paper_2605_06676_b200 as lkv
+from paper_2605_06676_b200 import sharded, synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _local(cache, scorers, l0, l1):
+    c = lkv.DenseCache(cache.keys[:, l0:l1].contiguous(), cache.values[:, l0:l1].contiguous(), cache.seq_lens)
+    s = lkv.Scorers(scorers.w1[l0:l1], scorers.b1[l0:l1], scorers.w2[l0:l1], input=scorers.input,
+                    activation=scorers.activation, stride_layer=1, stride_head=0)
+    return c, s
+
+
+@pytest.mark.parametrize("cid,world,L,T", [(2, 4, 8, 5000), (2, 3, 8, 4096), (4, 2, 5, 6000), (5, 8, 8, 3000)])
+def test_head_shards_equal_unsharded(cid, world, L, T):
+    cfg = synth.CONFIGS[cid]
+    S = min(cfg.n_seq, 3)
+    cache = synth.make_cache(cfg, n_layers=L, max_tokens=T, n_seq=S)
+    scorers = synth.make_scorers(cfg, n_layers=L)
+    logits = synth.make_logits(cfg, n_layers=L)
+    full = lkv.evict(cache, scorers, logits, cfg.ratio, lkv.BUDGET_EXACT, decode_slack=4, keep_scores=False)
+    H = cfg.n_kv_heads
+    plan = sharded.ShardPlan(L, H, world)
+    # the oracle's budgets from the same logits (K2 bit-exact on every rank)
+    want_b = [O.freeze_budgets_exact(O.allocate_budgets(logits.cpu().numpy(), cfg.ratio), cfg.ratio, t)
+              for t in cache.seq_lens]
+    G = cfg.n_q_heads // H
+    steps = [synth.make_decode_inputs(cfg, s, n_layers=L, n_seq=S) for s in range(3)]
+    shard_out = [[] for _ in range(3)]
+    for r in range(world):
+        l0, l1 = plan.layers[r]
+        if l1 == l0:
+            continue
+        lc, ls = _local(cache, scorers, l0, l1)
+        ev = sharded.ShardEvictor(lc, ls, plan, r, cfg.ratio, lkv.BUDGET_EXACT, decode_slack=4)
+        rc = ev.run(logits)
+        h0, n = plan.head_range(r)
+        for s in range(S):
+            assert (ev.budgets[s].cpu().numpy() == want_b[s][h0:h0 + n]).all()
+        assert torch.equal(rc.lens.view(S, -1), full.cache.lens.view(S, -1)[:, h0:h0 + n])
+        for s in range(S):
+            for j in range(n):
+                k, v, p = rc.head(s * n + j)
+                kf, vf, pf = full.cache.head(s * L * H + h0 + j)
+                assert torch.equal(p, pf) and torch.equal(k, kf) and torch.equal(v, vf)
+        for st in range(3):
+            q, k, v = (x[:, l0:l1].contiguous() for x in steps[st])
+            shard_out[st].append(lkv.decode_step(rc, q, k, v).clone())
+    full_out = [lkv.decode_step(full.cache, *steps[s]).clone() for s in range(3)]  # after the layout checks
+    for st in range(3):
+        got = torch.cat(shard_out[st], dim=1)
+        assert got.shape == full_out[st].shape
+        assert torch.allclose(got.float(), full_out[st].float(), rtol=0, atol=1e-6 * float(full_out[st].float().abs().max()))
+
+
+def test_evict_shard_contract_errors():
+    cfg = synth.CONFIGS[2]
+    cache = synth.make_cache(cfg, n_layers=4, max_tokens=1000)
+    scorers = synth.make_scorers(cfg, n_layers=4)
+    plan = sharded.ShardPlan(8, 8, 2)  # the 4 local layers are rank 1's layers 4..7
+    ev = sharded.ShardEvictor(cache, scorers, plan, 1, 0.15)
+    with pytest.raises(lkv.ContractError):
+        ev.launch(synth.make_logits(cfg, n_layers=4))  # not the full logit vector
+    with pytest.raises(lkv.ContractError):
+        sharded.ShardEvictor(cache, scorers, sharded.ShardPlan(8, 8, 4), 1, 0.15)  # wrong layer count
+    ev.run(synth.make_logits(cfg, n_layers=8))
+    with pytest.raises(lkv.BudgetError):
+        sharded.ShardEvictor(cache, scorers, plan, 1, 1.5).run(synth.make_logits(cfg, n_layers=8))
+
+
+def test_nccl_comm_single_rank():
+    comm = sharded.Comm(1, 0, sharded.Comm.unique_id())
+    try:
+        x = torch.arange(40, dtype=torch.float64, device="cuda")
+        out = torch.full((50,), -1.0, dtype=torch.float64, device="cuda")
+        comm.allgatherv(x, out, [40], [7])
+        torch.cuda.synchronize()
+        assert torch.equal(out[7:47], x) and (out[:7] == -1).all() and (out[47:] == -1).all()
+        y = torch.randn(3, 5, 32, 16, device="cuda").to(torch.bfloat16)
+        g = torch.zeros(y.numel() + 10, dtype=torch.bfloat16, device="cuda")
+        comm.gatherv(y.reshape(-1), g, [y.numel()], [10], root=0)
+        torch.cuda.synchronize()
+        assert torch.equal(g[10:], y.reshape(-1))
+        # the sharded helpers on a 1-rank communicator
+        plan = sharded.ShardPlan(4, 8, 1)
+        lg = torch.randn(32, dtype=torch.float64, device="cuda")
+        assert torch.equal(sharded.gather_logits(comm, plan, lg), lg)
+    finally:
+        comm.close()
