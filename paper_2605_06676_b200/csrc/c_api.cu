@@ -294,16 +294,18 @@ lkv_status run_select(const lkv_cache_desc* c, const float* scores, const int32_
 
 // ---- decode workspace -------------------------------------------------------------------------------
 struct DecodeWs {
-    size_t err, n_items, layer_begin, item_base, items, part_m, part_l, part_o, total;
+    size_t err, n_items, ch, layer_begin, item_base, items, part_m, part_l, part_o, total;
     int64_t max_items;
 };
 DecodeWs decode_layout(const lkv_ragged_desc* r, int G) {
     DecodeWs w;
-    w.max_items = r->capacity_rows / 256 + r->n_heads;
+    w.max_items = r->capacity_rows / kDecMinCh + r->n_heads;
     size_t o = 0;
     w.err = o;
     o = align_up(o + sizeof(ErrWord));
     w.n_items = o;
+    o = align_up(o + sizeof(int32_t));
+    w.ch = o;  // rows per work item, chosen by the plan
     o = align_up(o + sizeof(int32_t));
     w.layer_begin = o;  // [n_layers + 1] of the plan (n_layers <= n_heads)
     o = align_up(o + sizeof(int32_t) * ((size_t)r->n_heads + 1));
@@ -823,8 +825,11 @@ lkv_status lkv_decode_plan(const lkv_ragged_desc* r, void* ws, size_t ws_bytes, 
     const DecodeWs w = decode_layout(r, 1);
     lkv_status st = check_ws(ws, ws_bytes, w.items + sizeof(DecodeItem) * (size_t)w.max_items);
     if (st) return st;
+    // one all-layer launch walks every item: aim for ~4 items per resident CTA; G unknown here, so
+    // the combine bound assumes the largest group (16)
     LKV_CUDA(launch_decode_plan(r->offsets, r->n_heads, 1, 1, at<DecodeItem>(ws, w.items), at<int32_t>(ws, w.item_base),
-                                at<int32_t>(ws, w.layer_begin), at<int32_t>(ws, w.n_items), (cudaStream_t)stream),
+                                at<int32_t>(ws, w.layer_begin), at<int32_t>(ws, w.n_items), at<int32_t>(ws, w.ch),
+                                8 * num_sms(), 16, (cudaStream_t)stream),
              "decode plan");
     return LKV_OK;
 }
@@ -860,6 +865,7 @@ lkv_status lkv_decode_step(const lkv_ragged_desc* r, int32_t n_seq, int32_t n_la
     p.q_layers = n_layers;
     p.item_lo = at<int32_t>(ws, w.layer_begin);  // layer_begin[0] == 0 for every plan
     p.item_hi = at<int32_t>(ws, w.n_items);
+    p.ch = at<int32_t>(ws, w.ch);
     p.out_nbt = 0;
     p.max_items = (int32_t)w.max_items;
     p.scale_log2 = (float)(scale * 1.4426950408889634);
@@ -926,6 +932,8 @@ lkv_status check_model(const lkv_model_desc* m) {
     if (!(m->rope_base > 0.0) || !(m->norm_eps > 0.0)) return fail(LKV_ERR_CONTRACT, "model: rope_base and norm_eps must be > 0");
     if (m->dtype == LKV_BF16 && (m->head_dim != 128 || m->n_q_heads / m->n_kv_heads > 16))
         return fail(LKV_ERR_UNSUPPORTED, "bf16 model decode needs head_dim 128 and group size <= 16");
+    if ((int64_t)m->n_q_heads * m->head_dim > 128 * 1000 || m->mlp_width > 128 * 1000)
+        return fail(LKV_ERR_UNSUPPORTED, "model decode: reduction lengths above 128000 exceed the stream-K split table");
     return LKV_OK;
 }
 
@@ -1083,9 +1091,11 @@ lkv_status lkv_model_plan(const lkv_model_desc* m, const lkv_ragged_desc* r, int
     if ((st = check_ws(ws, ws_bytes, w.total))) return st;
     cudaStream_t s = (cudaStream_t)stream;
     LKV_CUDA(cudaMemsetAsync(ws, 0, w.total, s), "workspace clear");
+    // per-layer launches: aim for ~2 items per resident CTA in each layer
     LKV_CUDA(launch_decode_plan(r->offsets, n_seq, g.L, g.H, at<DecodeItem>(ws, w.dec.items),
                                 at<int32_t>(ws, w.dec.item_base), at<int32_t>(ws, w.dec.layer_begin),
-                                at<int32_t>(ws, w.dec.n_items), s),
+                                at<int32_t>(ws, w.dec.n_items), at<int32_t>(ws, w.dec.ch), 4 * num_sms(),
+                                g.Hq / g.H, s),
              "decode plan");
     LKV_CUDA(launch_rope_table(m->max_seq_len, g.D, m->rope_base, 0, at<float2>(ws, w.rope), s), "rope table");
     return LKV_OK;
@@ -1165,6 +1175,7 @@ lkv_status lkv_model_decode_step(const lkv_model_desc* m, const void* weights, c
     dp.out = at<void>(ws, w.act_attn);
     dp.items = at<DecodeItem>(ws, w.dec.items);
     dp.item_base = at<int32_t>(ws, w.dec.item_base);
+    dp.ch = at<int32_t>(ws, w.dec.ch);
     dp.part_m = at<float>(ws, w.dec.part_m);
     dp.part_l = at<float>(ws, w.dec.part_l);
     dp.part_o = at<float>(ws, w.dec.part_o);

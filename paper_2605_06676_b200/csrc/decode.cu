@@ -7,8 +7,9 @@
 // online-softmax form of masked_attention_blocked (attention.cpp:96-143).
 //
 // B200 design (HBM-bound, 4-8 flop/byte):
-//  * work items = (head, 256-row chunk) over each head's capacity, planned once
-//    per eviction (decode_plan_kernel); a persistent grid walks them;
+//  * work items = (head, ch-row chunk) over each head's capacity, planned once per eviction
+//    (decode_plan_kernel, ch in 128..1024 chosen so one launch has enough items for every SM);
+//    a persistent grid walks them;
 //  * per CTA: one TMA producer warp streams 64-row K+V stages (128-byte
 //    swizzle, 32 KB) through a 3-stage mbarrier ring (2 CTAs/SM); four consumer warps each
 //    take 16 rows of a stage and run S = Q K^T and O += P V on tensor cores
@@ -24,10 +25,7 @@
 
 namespace lkv_dev {
 
-#ifndef LKV_DEC_CH
-#define LKV_DEC_CH 1024
-#endif
-constexpr int kDecCh = LKV_DEC_CH;  // rows per work item
+constexpr int kDecMaxCh = 1024;  // largest work item (rows); the plan picks 128..1024 per cache
 constexpr int kDecStageRows = 64;   // rows per pipeline stage
 #ifndef LKV_DEC_STAGES
 #define LKV_DEC_STAGES 2
@@ -47,15 +45,39 @@ constexpr int kDecThreads = (kDecConsumers + 1) * 32;
 // items of one layer are contiguous: layer_begin[l] .. layer_begin[l + 1] (a per-layer decode
 // launch, as in a full model decode step, walks just that range; an all-layer launch walks
 // layer_begin[0] .. layer_begin[n_layers]).
+// Work-item size: the largest ch in {1024, 512, 256, 128} that still gives a launch (one plan
+// layer) >= target_items items, so a per-layer launch of a small cache still spreads over every
+// SM while an all-layer launch keeps long items; ch never leaves G * chunks of a head above
+// the combine's table (kCombMaxChunks).
+constexpr int kCombMaxChunks = 8192;  // G * chunks per head (G=4: 2M rows, G=8: 1M rows at ch=1024)
 __global__ void __launch_bounds__(1024) decode_plan_kernel(const int64_t* offsets, int n_seq, int n_layers, int n_kv,
                                                            DecodeItem* items, int32_t* item_base,
-                                                           int32_t* layer_begin, int32_t* n_items) {
+                                                           int32_t* layer_begin, int32_t* n_items, int32_t* ch_out,
+                                                           int target_items, int G) {
     __shared__ uint32_t s_scan[33];
     __shared__ int32_t s_carry;
+    __shared__ unsigned long long s_cnt[4];
+    __shared__ unsigned long long s_maxcap;
     const int n_heads = n_seq * n_layers * n_kv;
     const int per_layer = n_seq * n_kv;
-    if (threadIdx.x == 0) s_carry = 0;
+    if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
+    if (threadIdx.x == 0) {
+        s_carry = 0;
+        s_maxcap = 0;
+    }
     __syncthreads();
+    for (int h = threadIdx.x; h < n_heads; h += 1024) {
+        const int64_t cap = offsets[h + 1] - offsets[h];
+        for (int i = 0; i < 4; ++i) atomicAdd(&s_cnt[i], (unsigned long long)((cap + (128 << i) - 1) >> (7 + i)));
+        atomicMax(&s_maxcap, (unsigned long long)cap);
+    }
+    __syncthreads();
+    // the largest ch meeting the target, else the smallest; then grown until the combine fits
+    int ch = 128;
+    for (int i = 0; i < 4; ++i)
+        if ((long long)s_cnt[i] >= (long long)target_items * n_layers) ch = 128 << i;
+    while (ch < kDecMaxCh && (long long)((s_maxcap + ch - 1) / ch) * G > kCombMaxChunks) ch <<= 1;
+    if (threadIdx.x == 0) *ch_out = ch;
     for (int base = 0; base < n_heads; base += 1024) {
         const int j = base + threadIdx.x;
         uint32_t nch = 0;
@@ -65,7 +87,7 @@ __global__ void __launch_bounds__(1024) decode_plan_kernel(const int64_t* offset
             const int s = r / n_kv, kh = r - s * n_kv;
             h = (s * n_layers + l) * n_kv + kh;
             const int64_t cap = offsets[h + 1] - offsets[h];
-            nch = (uint32_t)((cap + kDecCh - 1) / kDecCh);
+            nch = (uint32_t)((cap + ch - 1) / ch);
         }
         uint32_t tot;
         const uint32_t ex = block_exclusive_scan<1024>(nch, s_scan, &tot);
@@ -175,6 +197,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
     const int G = p.G;
     const int D = 128;
     const int it_lo = *p.item_lo, it_hi = *p.item_hi;
+    const int ch = *p.ch;
     if (threadIdx.x == 0) {
         for (int i = 0; i < kDecStages; ++i) {
             mbar_init(&full[i], 1);
@@ -195,9 +218,9 @@ __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
             for (int it = it_lo + blockIdx.x; it < it_hi; it += gridDim.x) {
                 const DecodeItem wi = p.items[it];
                 const int len_new = p.lens[wi.head] + 1;
-                const int r0 = wi.chunk * kDecCh;
+                const int r0 = wi.chunk * ch;
                 if (r0 >= len_new) continue;
-                const int rows = min(kDecCh, len_new - r0);
+                const int rows = min(ch, len_new - r0);
                 const int64_t grow0 = p.offsets[wi.head] + r0;
                 for (int sr = 0; sr < rows; sr += kDecStageRows) {
                     mbar_wait(&empty[st], ph ^ 1);
@@ -228,11 +251,11 @@ __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
         const int head = wi.head;
         const int len_old = p.lens[head];
         const int len_new = len_old + 1;
-        const int r0 = wi.chunk * kDecCh;
+        const int r0 = wi.chunk * ch;
         if (r0 >= len_new) continue;
-        const int rows = min(kDecCh, len_new - r0);
+        const int rows = min(ch, len_new - r0);
         const int64_t off = p.offsets[head];
-        const bool has_new = (len_old >= r0) && (len_old < r0 + kDecCh);
+        const bool has_new = (len_old >= r0) && (len_old < r0 + ch);
         if (has_new && off + len_new > p.offsets[head + 1]) {
             if (threadIdx.x == 0) latch_error(p.err, LKV_ERR_CONTRACT, head);
         }
@@ -398,7 +421,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
             }
         }
         named_bar_sync(1, kDecConsumers * 32);
-        const int nch = (len_new + kDecCh - 1) / kDecCh;
+        const int nch = (len_new + ch - 1) / ch;
         __nv_bfloat16* outp = static_cast<__nv_bfloat16*>(p.out);
         const HeadCoord hc = head_coord(p, head);
         for (int e = threadIdx.x; e < G * D; e += kDecConsumers * 32) {
@@ -435,18 +458,19 @@ __global__ void __launch_bounds__(kDecSimtThreads) decode_attn_f32_kernel(const 
     extern __shared__ float sm[];
     const int D = p.head_dim, G = p.G;
     float* qs = sm;                 // [G][D]
-    float* sc = qs + G * D;         // [G][kDecCh]
+    const int ch = *p.ch;
+    float* sc = qs + G * D;         // [G][ch]
     const int it = *p.item_lo + blockIdx.x;
     if (it >= *p.item_hi) return;
     const DecodeItem wi = p.items[it];
     const int head = wi.head;
     const int len_old = p.lens[head];
     const int len_new = len_old + 1;
-    const int r0 = wi.chunk * kDecCh;
+    const int r0 = wi.chunk * ch;
     if (r0 >= len_new) return;
-    const int rows = min(kDecCh, len_new - r0);
+    const int rows = min(ch, len_new - r0);
     const int64_t off = p.offsets[head];
-    const bool has_new = len_old >= r0 && len_old < r0 + kDecCh;
+    const bool has_new = len_old >= r0 && len_old < r0 + ch;
     if (has_new && off + len_new > p.offsets[head + 1]) {
         if (threadIdx.x == 0) latch_error(p.err, LKV_ERR_CONTRACT, head);
         return;
@@ -475,17 +499,17 @@ __global__ void __launch_bounds__(kDecSimtThreads) decode_attn_f32_kernel(const 
             for (int c = lane; c < D; c += 32) acc = fmaf(qs[gg * D + c], kr[c], acc);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (lane == 0) sc[gg * kDecCh + r] = acc * p.scale_log2;
+            if (lane == 0) sc[gg * ch + r] = acc * p.scale_log2;
         }
     }
     __syncthreads();
     for (int e = threadIdx.x; e < G * D; e += kDecSimtThreads) {
         const int gg = e / D, dd = e - gg * D;
         float M = -INFINITY;
-        for (int r = 0; r < rows; ++r) M = fmaxf(M, sc[gg * kDecCh + r]);
+        for (int r = 0; r < rows; ++r) M = fmaxf(M, sc[gg * ch + r]);
         float L = 0.f, acc = 0.f;
         for (int r = 0; r < rows; ++r) {
-            const float w = exp2f(sc[gg * kDecCh + r] - M);
+            const float w = exp2f(sc[gg * ch + r] - M);
             const int row = r0 + r;
             const float v = (row == len_old) ? nv[dd] : V[(size_t)row * D + dd];
             L += w;
@@ -504,7 +528,6 @@ __global__ void __launch_bounds__(kDecSimtThreads) decode_attn_f32_kernel(const 
 // shared memory; phase 2 streams the partial outputs with independent (unrolled) loads.
 // Heads that fit one chunk were finalised by the attention kernel (bf16 path).
 constexpr int kCombThreads = 128;
-constexpr int kCombMaxChunks = 8192;  // G * chunks per head (G=4: 2M rows, G=8: 1M rows)
 
 template <typename T>
 __global__ void __launch_bounds__(kCombThreads) decode_combine_kernel(const __grid_constant__ DecodeParams p,
@@ -519,7 +542,8 @@ __global__ void __launch_bounds__(kCombThreads) decode_combine_kernel(const __gr
     const int head = (js * p.n_layers + p.layer0 + jl) * p.n_kv_heads + (jr - js * p.n_kv_heads);
     const int D = p.head_dim, G = p.G;
     const int len_new = p.lens[head] + 1;
-    const int nch = (len_new + kDecCh - 1) / kDecCh;
+    const int ch = *p.ch;
+    const int nch = (len_new + ch - 1) / ch;
     if (!(single_chunk_done && nch == 1) && nch * G <= kCombMaxChunks) {
         const int base = p.item_base[head];
         const float* pm = p.part_m + (size_t)base * G;
@@ -598,9 +622,10 @@ __global__ void __launch_bounds__(kCombThreads) decode_combine_kernel(const __gr
 
 // ---- host launchers ---------------------------------------------------------------------------------
 cudaError_t launch_decode_plan(const int64_t* offsets, int n_seq, int n_layers, int n_kv, DecodeItem* items,
-                               int32_t* item_base, int32_t* layer_begin, int32_t* n_items, cudaStream_t stream) {
+                               int32_t* item_base, int32_t* layer_begin, int32_t* n_items, int32_t* ch,
+                               int target_items, int G, cudaStream_t stream) {
     decode_plan_kernel<<<1, 1024, 0, stream>>>(offsets, n_seq, n_layers, n_kv, items, item_base, layer_begin,
-                                               n_items);
+                                               n_items, ch, target_items, G);
     note_launches(1);
     return cudaGetLastError();
 }
@@ -629,7 +654,7 @@ cudaError_t launch_decode(const DecodeParams& p, int dtype, const CUtensorMap* m
         if (e != cudaSuccess) return e;
         note_launches(2);
     } else {
-        const size_t smem = ((size_t)p.G * p.head_dim + (size_t)p.G * kDecCh) * sizeof(float);
+        const size_t smem = ((size_t)p.G * p.head_dim + (size_t)p.G * kDecMaxCh) * sizeof(float);
         cudaError_t e = cudaFuncSetAttribute(decode_attn_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         decode_attn_f32_kernel<<<p.max_items, kDecSimtThreads, smem, stream>>>(p);

@@ -111,6 +111,7 @@ struct DecodeParams {
     const int32_t* item_lo;     // device: first / one-past-last work item of this launch
     const int32_t* item_hi;
     int32_t max_items;          // upper bound on item_hi - item_lo (grid sizing)
+    const int32_t* ch;          // device: rows per work item, chosen by the plan (64 | ch, <= 1024)
     int32_t out_nbt;            // 0: out is [qsl][Hq][D]; > 0: packed GEMV activations (q_layers == 1)
     float scale_log2;
     const int64_t* offsets;
@@ -131,7 +132,9 @@ struct DecodeParams {
     ErrWord* err;
 };
 cudaError_t launch_decode_plan(const int64_t* offsets, int n_seq, int n_layers, int n_kv, DecodeItem* items,
-                               int32_t* item_base, int32_t* layer_begin, int32_t* n_items, cudaStream_t stream);
+                               int32_t* item_base, int32_t* layer_begin, int32_t* n_items, int32_t* ch,
+                               int target_items, int G, cudaStream_t stream);
+constexpr int kDecMinCh = 128;  // smallest work item the plan may choose (workspace sizing)
 cudaError_t launch_decode(const DecodeParams& p, int dtype, const CUtensorMap* mk, const CUtensorMap* mv, int num_sms,
                           cudaStream_t stream);
 

@@ -40,6 +40,22 @@ constexpr int kWsConsumers = 4;
 constexpr int kWsThreads = (kWsConsumers + 1) * 32;
 constexpr int kWsPerSm = 2;
 constexpr int kYPad = 17;                      // y[64][17]: columns x batch (B <= 16)
+constexpr int kWsMaxSplit = 1024;              // CTAs sharing one column group (<= KU + 1; K <= 130k)
+#ifndef LKV_GEMV_EXPT
+#define LKV_GEMV_EXPT 0  // profiles/gemv_bench.cu bisection knobs: 1 no mma, 2 no fix-up, 4 no epilogue, 8 trace
+#endif
+#if LKV_GEMV_EXPT & 8
+__device__ unsigned long long g_gemv_trace[512][8];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define GTRACE(i) \
+    if ((LKV_GEMV_EXPT & 8) && threadIdx.x == 0) g_gemv_trace[blockIdx.x][i] = gtime()
+#else
+#define GTRACE(i)
+#endif
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
@@ -143,8 +159,10 @@ __global__ void __launch_bounds__(kWsThreads, kWsPerSm) wstream_gemv_kernel(cons
     float* red = reinterpret_cast<float*>(empty + kWsStages);  // [4][64][NBT * 8]
     float(*y)[kYPad] = reinterpret_cast<float(*)[kYPad]>(red + kWsConsumers * kWsCols * NBT * 8);
     int* s_last = reinterpret_cast<int*>(y + kWsCols);
+    int* s_slot = s_last + 4;  // [kWsMaxSplit]: partial slots of the CTAs sharing a column group
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    GTRACE(5);
     const int64_t U = (int64_t)p.NG * p.KU;
     const int P = gridDim.x, c = blockIdx.x;
     const int64_t u0 = unit_begin(c, U, P), u1 = unit_begin(c + 1, U, P);
@@ -196,6 +214,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsPerSm) wstream_gemv_kernel(cons
     // ===================== consumers =====================
     pdl_wait();
     const int tid = threadIdx.x;  // 0..127
+    GTRACE(0);
     const int g = lane >> 2, cq = (lane & 3) * 2;
     int st = 0;
     uint32_t ph = 0;
@@ -224,6 +243,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsPerSm) wstream_gemv_kernel(cons
 #pragma unroll
                 for (int t = 0; t < 4; ++t) {
                     const uint4 a = *reinterpret_cast<const uint4*>(stg + ((ks * 4 + t) * 32 + lane) * 16);
+                    if (LKV_GEMV_EXPT & 1) { acc[t][0][0] += __uint_as_float(a.x); continue; }
 #pragma unroll
                     for (int bt = 0; bt < NBT; ++bt) mma_16816(acc[t][bt], a, bf[bt].x, bf[bt].y);
                 }
@@ -235,6 +255,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsPerSm) wstream_gemv_kernel(cons
                 ph ^= 1;
             }
         }
+        GTRACE(1);
         // ---- cross-warp reduction (fixed order) -> y[64][b]
         constexpr int BW = NBT * 8;
 #pragma unroll
@@ -257,35 +278,59 @@ __global__ void __launch_bounds__(kWsThreads, kWsPerSm) wstream_gemv_kernel(cons
             y[n][b] = v;
         }
         named_sync(1, kWsConsumers * 32);
-        if (!whole) {
+        if (!whole && !(LKV_GEMV_EXPT & 2)) {
             // stream-K fix-up: partial -> global slot; the last CTA of the group sums in CTA order
             const int slot = 2 * c + (ng == ng_first ? 0 : 1);
             float* mine = p.part + (size_t)slot * kWsCols * 16;
-            for (int e = tid; e < kWsCols * 16; e += kWsConsumers * 32) mine[e] = y[e >> 4][e & 15];
-            __threadfence();
+            for (int e = tid; e < kWsCols * 16; e += kWsConsumers * 32) __stcg(mine + e, y[e >> 4][e & 15]);
+            // one release/acquire pair per CTA (bar.sync orders the other consumers' stores
+            // before thread 0's fence, which is cumulative): a fence in every thread costs ~25 us
             named_sync(1, kWsConsumers * 32);
             const int cf = unit_owner(gbeg, U, P), cl = unit_owner(gend - 1, U, P);
             if (tid == 0) {
+                __threadfence();
                 const uint32_t old = atomicAdd(&p.cnt[ng], 1u);
                 const int last = (int)old == cl - cf;
-                if (last) p.cnt[ng] = 0u;  // self-reset for the next launch
+                if (last) {
+                    p.cnt[ng] = 0u;  // self-reset for the next launch
+                    __threadfence();
+                }
                 *s_last = last;
             }
             named_sync(1, kWsConsumers * 32);
+            GTRACE(2);
             if (!*s_last) continue;
-            __threadfence();
-            for (int e = tid; e < kWsCols * 16; e += kWsConsumers * 32) {
-                float v = 0.f;
-                for (int cc = cf; cc <= cl; ++cc) {
-                    const int sl = 2 * cc + (ng == (int)(unit_begin(cc, U, P) / p.KU) ? 0 : 1);
-                    v += __ldcg(p.part + (size_t)sl * kWsCols * 16 + e);
-                }
-                y[e >> 4][e & 15] = v;
+            // slot of every contributing CTA computed once (one 64-bit division each), then each
+            // thread streams its two float4 of every partial with the loads of 4 CTAs in flight --
+            // a division + dependent L2 round trip per element cost ~20 us per launch.  The sum
+            // runs in CTA order, as before (deterministic).
+            const int ncta = cl - cf + 1;
+            for (int i = tid; i < ncta; i += kWsConsumers * 32) {
+                const int cc = cf + i;
+                s_slot[i] = 2 * cc + (ng == (int)(unit_begin(cc, U, P) / p.KU) ? 0 : 1);
+            }
+            named_sync(1, kWsConsumers * 32);
+            float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
+#pragma unroll 4
+            for (int i = 0; i < ncta; ++i) {
+                const float4* src = reinterpret_cast<const float4*>(p.part + (size_t)s_slot[i] * kWsCols * 16);
+                const float4 a = __ldcg(src + tid), b = __ldcg(src + tid + kWsConsumers * 32);
+                v0.x += a.x, v0.y += a.y, v0.z += a.z, v0.w += a.w;
+                v1.x += b.x, v1.y += b.y, v1.z += b.z, v1.w += b.w;
+            }
+            {
+                const int e0 = 4 * tid, e1 = 4 * (tid + kWsConsumers * 32);  // 16 | e: one y row each
+                y[e0 >> 4][(e0 & 15) + 0] = v0.x, y[e0 >> 4][(e0 & 15) + 1] = v0.y;
+                y[e0 >> 4][(e0 & 15) + 2] = v0.z, y[e0 >> 4][(e0 & 15) + 3] = v0.w;
+                y[e1 >> 4][(e1 & 15) + 0] = v1.x, y[e1 >> 4][(e1 & 15) + 1] = v1.y;
+                y[e1 >> 4][(e1 & 15) + 2] = v1.z, y[e1 >> 4][(e1 & 15) + 3] = v1.w;
             }
             named_sync(1, kWsConsumers * 32);
         }
-        gemv_epilogue<__nv_bfloat16>(p, ng, y, tid, kWsConsumers * 32);
+        GTRACE(3);
+        if (!(LKV_GEMV_EXPT & 4)) gemv_epilogue<__nv_bfloat16>(p, ng, y, tid, kWsConsumers * 32);
         named_sync(1, kWsConsumers * 32);
+        GTRACE(4);
     }
 }
 
@@ -401,7 +446,7 @@ size_t gemv_max_grid(int num_sms) { return (size_t)kWsPerSm * num_sms; }
 static size_t wstream_smem(int nbt) {
     const size_t stage = kWsUnitBytes + 8 * nbt * 256;
     return 128 + kWsStages * stage + 2 * kWsStages * 8 + (size_t)kWsConsumers * kWsCols * nbt * 8 * 4 +
-           (size_t)kWsCols * kYPad * 4 + 16;
+           (size_t)kWsCols * kYPad * 4 + 16 + 4 * kWsMaxSplit;
 }
 
 cudaError_t launch_gemv(const GemvParams& p, int dtype, int num_sms, cudaStream_t stream) {
