@@ -35,10 +35,16 @@ namespace lkv_dev {
 constexpr int kWsCols = 64;                    // output columns per unit (4 m16 tiles)
 constexpr int kWsK = 128;                      // k per unit (8 k16 steps)
 constexpr int kWsUnitBytes = kWsCols * kWsK * 2;  // 16 KB of bf16
-constexpr int kWsStages = 4;
+#ifndef LKV_WS_STAGES
+#define LKV_WS_STAGES 4
+#endif
+#ifndef LKV_WS_PER_SM
+#define LKV_WS_PER_SM 2
+#endif
+constexpr int kWsStages = LKV_WS_STAGES;
 constexpr int kWsConsumers = 4;
 constexpr int kWsThreads = (kWsConsumers + 1) * 32;
-constexpr int kWsPerSm = 2;
+constexpr int kWsPerSm = LKV_WS_PER_SM;
 constexpr int kYPad = 17;                      // y[64][17]: columns x batch (B <= 16)
 constexpr int kWsMaxSplit = 1024;              // CTAs sharing one column group (<= KU + 1; K <= 130k)
 #ifndef LKV_GEMV_EXPT
