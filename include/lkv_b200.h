@@ -20,6 +20,8 @@
  *   lkv_evict_shard <- the same on one rank's head shard (multi-GPU; lkv_comm_* = NCCL)
  *   lkv_decode_step <- decode_step's append + attention block (model.hpp:95,
  *                      model.cpp:240-265) -> masked_attention_dense (attention.hpp:57)
+ *   lkv_masked_attention_fwd/_bwd <- masked_attention_dense / masked_attention_vjp
+ *                      (attention.hpp:57-69; training)
  *   lkv_model_*     <- the whole decode_step (model.hpp:95, model.cpp:209-287):
  *                      projections, RoPE at tokens_seen, attention, SwiGLU MLP, logits
  *
@@ -244,6 +246,34 @@ lkv_status lkv_comm_allgatherv(lkv_comm_t comm, const void* send, void* recv, co
                                const int64_t* displs, lkv_stream_t stream);
 lkv_status lkv_comm_gatherv(lkv_comm_t comm, const void* send, void* recv, const int64_t* bytes,
                             const int64_t* displs, int32_t root, lkv_stream_t stream);
+
+/* ---- training-time operators ---------------------------------- */
+/* Multiplicative soft-mask attention, forward and backward: masked_attention_dense /
+ * masked_attention_vjp (attention.hpp:52-69, attention.cpp:46-201) for a batch of heads with
+ * GQA (query head h reads kv head h / (n_q_heads / n_kv_heads)); the per-query-head calls of
+ * forward_masked (model.cpp:100-112) in one launch.  Layouts: q, out, d_out
+ * [batch][n_q_heads][t_q][head_dim]; k, v [batch][n_kv_heads][t_k][head_dim] (dtype);
+ * mask [batch][n_kv_heads][t_k] fp32 or NULL (all ones); lse [batch][n_q_heads][t_q] fp32
+ * (log2-domain masked log-sum-exp of scale * q.k, saved by the forward for the backward);
+ * gradients fp32, dk/dv/dmask summed over the query heads of a group.  bf16 needs
+ * head_dim 128 (tensor cores); fp32 runs the exact SIMT path (head_dim <= 256).  Errors:
+ * mask value < 0 or non-finite -> CONTRACT, a row whose masked mass vanishes ->
+ * DEGENERATE_MASK (both latched in the workspace). */
+typedef struct lkv_attn_desc {
+    int32_t batch, n_q_heads, n_kv_heads, t_q, t_k, head_dim, dtype;
+    int32_t causal;               /* row r admits keys j <= query_pos_offset + r */
+    int32_t query_pos_offset;
+    int32_t self_always_retained; /* key j == query_pos_offset + r keeps multiplier 1 */
+    double scale;
+} lkv_attn_desc;
+size_t lkv_attn_workspace_bytes(const lkv_attn_desc* attn);
+lkv_status lkv_masked_attention_fwd(const lkv_attn_desc* attn, const void* q, const void* k, const void* v,
+                                    const float* mask, void* out, float* lse, void* workspace,
+                                    size_t workspace_bytes, lkv_stream_t stream);
+lkv_status lkv_masked_attention_bwd(const lkv_attn_desc* attn, const void* q, const void* k, const void* v,
+                                    const float* mask, const void* out, const float* lse, const void* d_out,
+                                    float* dq, float* dk, float* dv, float* dmask, void* workspace,
+                                    size_t workspace_bytes, lkv_stream_t stream);
 
 /* ---- K/V production for layer-by-layer prefill (the step before the path) -------- */
 /* cos/sin table [t_max][head_dim/2] of float2 (cos, sin) for positions pos_offset + p,

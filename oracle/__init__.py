@@ -82,6 +82,12 @@ def lib():
         L.lkvo_compact_rows.restype = None
         L.lkvo_decode_attention.argtypes = [C.c_int, _dp, C.c_int, C.c_void_p, C.c_void_p, C.c_int64,
                                             C.c_int, C.c_double, _dp]
+        L.lkvo_soft_topk_density.argtypes = [_dp, C.c_int, C.c_double, C.c_double, C.c_double, _dp]
+        L.lkvo_soft_topk_vjp.argtypes = [_dp, _dp, C.c_int, C.c_double, _dp, _dp]
+        L.lkvo_masked_attention.argtypes = [_dp, _dp, _dp, _dp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
+                                            C.c_int, C.c_int, _dp, _dp, _dp, _dp]
+        L.lkvo_masked_attention_vjp.argtypes = [_dp, _dp, _dp, _dp, C.c_int, C.c_int, C.c_int, C.c_int,
+                                                C.c_double, C.c_int, C.c_int, _dp, _dp, _dp, _dp, _dp]
         L.lkvo_kv_memory_bytes.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_int64, C.c_double,
                                            _dp, _dp, _dp]
         L.lkvo_kv_memory_bytes_budgets.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_int64,
@@ -119,6 +125,9 @@ def ref_lib():
         R.ref_freeze_budgets.argtypes = [_dp, C.c_int, C.c_int, C.c_int, _ip]
         R.ref_hard_topk.argtypes = [_dp, C.c_int, C.c_int, _ip]
         R.ref_token_scores.argtypes = [_dp, _dp, C.c_int, C.c_int, _dp, _dp, _dp, C.c_int, _dp]
+        R.ref_soft_topk_vjp.argtypes = [_dp, C.c_int, C.c_double, C.c_double, _dp, _dp, _dp, _dp, _dp]
+        R.ref_masked_attention.argtypes = [_dp, _dp, _dp, _dp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
+                                           C.c_int, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp]
         _ref = R
     return _ref
 
@@ -278,6 +287,53 @@ def decode_attention(q, keys, values, scale: float) -> np.ndarray:
     _check(lib().lkvo_decode_attention(dtype, _ptr(q, _dp), G, keys.ctypes.data, values.ctypes.data,
                                        keys.shape[0], d, scale, _ptr(out, _dp)))
     return out
+
+
+# ---- training-time operators ---------------------------------
+def soft_topk_full(x, k: float, tau: float = 1.0):
+    """soft_topk_forward (soft_topk.cpp:111-164) -> (values, lambda, clamped_k, density_terms)."""
+    x = _d(x)
+    n = x.size
+    vals = np.empty(n, np.float64)
+    lam, m, kc = C.c_double(), C.c_int(), C.c_double()
+    _check(lib().lkvo_soft_topk_forward(_ptr(x, _dp), n, k, tau, _ptr(vals, _dp), C.byref(lam), C.byref(m),
+                                        C.byref(kc)))
+    dens = np.empty(n, np.float64)
+    _check(lib().lkvo_soft_topk_density(_ptr(x, _dp), n, tau, lam.value, kc.value, _ptr(dens, _dp)))
+    return vals, lam.value, kc.value, dens
+
+
+def soft_topk_vjp(density, upstream, tau: float = 1.0):
+    """soft_topk_vjp (soft_topk.cpp:166-189) -> (grad_x, grad_k)."""
+    density, upstream = _d(density), _d(upstream)
+    gx = np.empty(density.size, np.float64)
+    gk = C.c_double()
+    _check(lib().lkvo_soft_topk_vjp(_ptr(density, _dp), _ptr(upstream, _dp), density.size, tau, _ptr(gx, _dp),
+                                    C.byref(gk)))
+    return gx, gk.value
+
+
+def masked_attention(q, k, v, mask=None, causal=True, scale=None, pos_offset=0, self_keep=False, upstream=None):
+    """masked_attention_dense (+ masked_attention_vjp when `upstream` is given), one head, fp64:
+    q [n_q][d], k/v [t][d], mask [t] or None.  Returns out, or (out, dq, dk, dv, dmask)."""
+    q, k, v = _d(q), _d(k), _d(v)
+    n_q, d = q.shape
+    t = k.shape[0]
+    scale = 1.0 / np.sqrt(d) if scale is None else scale
+    m = _d(mask) if mask is not None else None
+    mp = _ptr(m, _dp) if m is not None else None
+    out = np.empty((n_q, d), np.float64)
+    _check(lib().lkvo_masked_attention(_ptr(q, _dp), _ptr(k, _dp), _ptr(v, _dp), mp, n_q, t, d, int(causal), scale,
+                                       pos_offset, int(self_keep), _ptr(out, _dp), None, None, None))
+    if upstream is None:
+        return out
+    u = _d(upstream)
+    dq, dk, dv = np.zeros_like(q), np.zeros_like(k), np.zeros_like(v)
+    dm = np.zeros(t, np.float64) if m is not None else None
+    _check(lib().lkvo_masked_attention_vjp(_ptr(q, _dp), _ptr(k, _dp), _ptr(v, _dp), mp, n_q, t, d, int(causal),
+                                           scale, pos_offset, int(self_keep), _ptr(u, _dp), _ptr(dq, _dp),
+                                           _ptr(dk, _dp), _ptr(dv, _dp), _ptr(dm, _dp) if dm is not None else None))
+    return out, dq, dk, dv, dm
 
 
 def kv_memory_bytes(n_layers=32, n_kv_heads=8, head_dim=128, bytes_per_element=2.0, tokens=200000,

@@ -289,6 +289,164 @@ int lkvo_soft_topk_forward(const double* x, int n, double k, double tau, double*
     return LKVO_OK;
 }
 
+int lkvo_soft_topk_density(const double* x, int n, double tau, double lambda, double clamped_k, double* density) {
+    /* soft_topk.cpp:123,153: density_terms = max(0.5 exp(-|z|), DBL_MIN), z = x/tau - lambda
+     * (n == 1: z is the pinned-budget log ratio) */
+    if (n == 1) {
+        const double z = clamped_k >= 0.5 ? -log(2.0 * (1.0 - clamped_k)) : log(2.0 * clamped_k);
+        density[0] = std_max(0.5 * exp(-fabs(z)), DBL_MIN);
+        return LKVO_OK;
+    }
+    for (int i = 0; i < n; ++i) density[i] = std_max(0.5 * exp(-fabs(x[i] / tau - lambda)), DBL_MIN);
+    return LKVO_OK;
+}
+
+int lkvo_soft_topk_vjp(const double* density, const double* upstream, int n, double tau, double* grad_x,
+                       double* grad_k) {
+    /* soft_topk.cpp:166-189: one summation order for both reductions, so a constant upstream
+     * gives an exactly zero score gradient and an exactly unit budget gradient */
+    if (!(tau > 0.0)) return fail(LKVO_CONTRACT, "soft_topk_vjp: tau must be positive");
+    if (n == 1) {
+        grad_x[0] = 0.0;
+        *grad_k = 1.0;
+        return LKVO_OK;
+    }
+    double sum_fp = 0.0, dot = 0.0;
+    for (int i = 0; i < n; ++i) {
+        sum_fp += density[i];
+        dot += upstream[i] * density[i];
+    }
+    const double mean_up = dot / sum_fp;
+    for (int i = 0; i < n; ++i) grad_x[i] = density[i] * (upstream[i] - mean_up) / tau;
+    *grad_k = mean_up;
+    return LKVO_OK;
+}
+
+/* ---- attention.cpp:20-201: multiplicative soft-mask attention, one head ---------------- */
+static inline int adm_end(int causal, int t, int pos_offset, int r) { /* attention.cpp:27-30 */
+    if (!causal) return t;
+    const int e = pos_offset + r + 1;
+    return e < t ? e : t;
+}
+static inline double mask_at(const double* mask, int self_keep, int j, int pos) { /* :21-24 */
+    if (self_keep && j == pos) return 1.0;
+    return mask ? mask[j] : 1.0;
+}
+static int attn_validate(const double* mask, int n_q, int t, int d, int causal, int pos_offset) { /* :33-44 */
+    if (n_q < 1 || t < 1 || d < 1) return fail(LKVO_CONTRACT, "attention: empty extents");
+    if (mask)
+        for (int j = 0; j < t; ++j)
+            if (!(mask[j] >= 0.0) || !isfinite(mask[j]))
+                return fail(LKVO_CONTRACT, "attention: mask values must be finite and >= 0");
+    if (causal && adm_end(causal, t, pos_offset, 0) < 1) return fail(LKVO_CONTRACT, "attention: first query row admits no key");
+    return LKVO_OK;
+}
+
+int lkvo_masked_attention(const double* q, const double* k, const double* v, const double* mask, int n_q, int t,
+                          int d, int causal, double scale, int pos_offset, int self_keep, double* out,
+                          double* p_raw, double* p, double* renorm) {
+    /* masked_attention_dense (attention.cpp:46-94): p_raw = softmax(s) over admissible keys,
+     * p~ = p_raw m, p = p~ / sum p~ (degenerate if sum <= 1e-300), out = p V.  p_raw, p
+     * [n_q][t] and renorm [n_q] are the AttentionSaved fields (nullable). */
+    int st = attn_validate(mask, n_q, t, d, causal, pos_offset);
+    if (st) return st;
+    double* pr = (double*)calloc((size_t)t, sizeof(double));
+    double* w = (double*)calloc((size_t)t, sizeof(double));
+    for (int r = 0; r < n_q && st == LKVO_OK; ++r) {
+        const int end = adm_end(causal, t, pos_offset, r), pos = pos_offset + r;
+        const double* qr = q + (size_t)r * d;
+        double mx = -INFINITY;
+        for (int j = 0; j < end; ++j) {
+            double dot = 0.0;
+            for (int c = 0; c < d; ++c) dot += qr[c] * k[(size_t)j * d + c];
+            pr[j] = scale * dot;
+            mx = std_max(mx, pr[j]);
+        }
+        double z_raw = 0.0;
+        for (int j = 0; j < end; ++j) {
+            pr[j] = exp(pr[j] - mx);
+            z_raw += pr[j];
+        }
+        double z_masked = 0.0;
+        for (int j = 0; j < end; ++j) {
+            pr[j] /= z_raw;
+            w[j] = pr[j] * mask_at(mask, self_keep, j, pos);
+            z_masked += w[j];
+        }
+        if (!(z_masked > 1e-300)) {
+            st = fail(LKVO_DEGENERATE_MASK, "attention row lost all admissible mass");
+            break;
+        }
+        for (int j = 0; j < end; ++j) w[j] /= z_masked;
+        for (int c = 0; c < d; ++c) {
+            double acc = 0.0;
+            for (int j = 0; j < end; ++j) acc += w[j] * v[(size_t)j * d + c];
+            out[(size_t)r * d + c] = acc;
+        }
+        if (p_raw)
+            for (int j = 0; j < t; ++j) p_raw[(size_t)r * t + j] = j < end ? pr[j] : 0.0;
+        if (p)
+            for (int j = 0; j < t; ++j) p[(size_t)r * t + j] = j < end ? w[j] : 0.0;
+        if (renorm) renorm[r] = z_masked;
+    }
+    free(pr);
+    free(w);
+    return st;
+}
+
+int lkvo_masked_attention_vjp(const double* q, const double* k, const double* v, const double* mask, int n_q,
+                              int t, int d, int causal, double scale, int pos_offset, int self_keep,
+                              const double* upstream, double* dq, double* dk, double* dv, double* dmask) {
+    /* masked_attention_vjp (attention.cpp:145-201), forward state recomputed in place:
+     * W = U V^T; per row wp = sum_j w p; d p~ = (w - wp) / z; dmask += d p~ p_raw (self keys
+     * excluded); d p_raw = d p~ m; dp_dot = sum d p_raw p_raw; ds = p_raw (d p_raw - dp_dot) scale;
+     * dV = P^T U, dQ = dS K, dK = dS^T Q.  Gradients are ACCUMULATED into dq/dk/dv/dmask. */
+    double* P = (double*)malloc(sizeof(double) * (size_t)n_q * t);
+    double* PR = (double*)malloc(sizeof(double) * (size_t)n_q * t);
+    double* Z = (double*)malloc(sizeof(double) * (size_t)n_q);
+    double* out = (double*)malloc(sizeof(double) * (size_t)n_q * d);
+    int st = lkvo_masked_attention(q, k, v, mask, n_q, t, d, causal, scale, pos_offset, self_keep, out, PR, P, Z);
+    double* ds = (double*)malloc(sizeof(double) * (size_t)t);
+    double* w = (double*)malloc(sizeof(double) * (size_t)t);
+    for (int r = 0; r < n_q && st == LKVO_OK; ++r) {
+        const int end = adm_end(causal, t, pos_offset, r), pos = pos_offset + r;
+        const double* u = upstream + (size_t)r * d;
+        const double* p_raw = PR + (size_t)r * t;
+        const double* p = P + (size_t)r * t;
+        for (int j = 0; j < t; ++j) {
+            double acc = 0.0;
+            for (int c = 0; c < d; ++c) acc += u[c] * v[(size_t)j * d + c];
+            w[j] = acc;
+            ds[j] = 0.0;
+        }
+        double wp = 0.0;
+        for (int j = 0; j < end; ++j) wp += w[j] * p[j];
+        double dp_dot = 0.0;
+        for (int j = 0; j < end; ++j) {
+            const double d_ptilde = (w[j] - wp) / Z[r];
+            if (mask && dmask && !(self_keep && j == pos)) dmask[j] += d_ptilde * p_raw[j];
+            const double d_praw = d_ptilde * mask_at(mask, self_keep, j, pos);
+            ds[j] = d_praw;
+            dp_dot += d_praw * p_raw[j];
+        }
+        for (int j = 0; j < end; ++j) ds[j] = p_raw[j] * (ds[j] - dp_dot) * scale;
+        for (int j = 0; j < t; ++j) {
+            for (int c = 0; c < d; ++c) {
+                dv[(size_t)j * d + c] += p[j] * u[c];
+                dq[(size_t)r * d + c] += ds[j] * k[(size_t)j * d + c];
+                dk[(size_t)j * d + c] += ds[j] * q[(size_t)r * d + c];
+            }
+        }
+    }
+    free(P);
+    free(PR);
+    free(Z);
+    free(out);
+    free(ds);
+    free(w);
+    return st;
+}
+
 double lkvo_bisect_lambda(const double* x, int n, double k, double tol) {
     /* proj/tests/oracles.hpp:25-40 */
     double lo = x[0], hi = x[0];

@@ -119,6 +119,19 @@ int lkvo_evict_heads(int dtype, const void* keys, const void* values, int n_head
                      void* dst_k, void* dst_v, int32_t* dst_pos, double* scores_out,
                      int n_threads);
 
+/* ---- soft_topk.cpp:123,153,166-189 ----------------------------------------- */
+int lkvo_soft_topk_density(const double* x, int n, double tau, double lambda, double clamped_k, double* density);
+int lkvo_soft_topk_vjp(const double* density, const double* upstream, int n, double tau, double* grad_x,
+                       double* grad_k);
+
+/* ---- attention.cpp:46-94,145-201 (one head; mask nullable = all ones) ---------- */
+int lkvo_masked_attention(const double* q, const double* k, const double* v, const double* mask, int n_q, int t,
+                          int d, int causal, double scale, int pos_offset, int self_keep, double* out,
+                          double* p_raw, double* p, double* renorm);
+int lkvo_masked_attention_vjp(const double* q, const double* k, const double* v, const double* mask, int n_q,
+                              int t, int d, int causal, double scale, int pos_offset, int self_keep,
+                              const double* upstream, double* dq, double* dk, double* dv, double* dmask);
+
 const char* lkvo_last_error(void);
 
 #ifdef __cplusplus

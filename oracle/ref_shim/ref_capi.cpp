@@ -10,6 +10,7 @@
 
 #include <string>
 
+#include "lkv/attention.hpp"
 #include "lkv/checkpoint.hpp"
 #include "lkv/errors.hpp"
 #include "lkv/model.hpp"
@@ -47,6 +48,50 @@ int ref_solve_threshold(const double* x, int n, double k, double* lambda, int* m
         auto [l, mm] = lkv::solve_threshold(std::span<const double>(x, static_cast<size_t>(n)), k);
         *lambda = l;
         *m = mm;
+    });
+}
+
+// soft_topk_forward + soft_topk_vjp (soft_topk.cpp:111-189): values, density terms, then the
+// vjp of `upstream` -> grad_x [n], grad_k
+int ref_soft_topk_vjp(const double* x, int n, double k, double tau, const double* upstream, double* values,
+                      double* density, double* grad_x, double* grad_k) {
+    return guarded([&] {
+        auto out = lkv::soft_topk_forward(std::span<const double>(x, static_cast<size_t>(n)), k, tau);
+        std::memcpy(values, out.values.data(), sizeof(double) * out.values.size());
+        std::memcpy(density, out.density_terms.data(), sizeof(double) * out.density_terms.size());
+        auto [gx, gk] = lkv::soft_topk_vjp(out, std::span<const double>(upstream, static_cast<size_t>(n)), tau);
+        std::memcpy(grad_x, gx.data(), sizeof(double) * gx.size());
+        *grad_k = gk;
+    });
+}
+
+// masked_attention_dense + masked_attention_vjp (attention.cpp:46-94,145-201), one head
+int ref_masked_attention(const double* q, const double* k, const double* v, const double* mask, int n_q, int t,
+                         int d, int causal, double scale, int pos_offset, int self_keep, const double* upstream,
+                         double* out, double* dq, double* dk, double* dv, double* dmask) {
+    return guarded([&] {
+        lkv::AttentionCall c;
+        c.n_q = n_q;
+        c.t = t;
+        c.d = d;
+        c.queries.assign(q, q + (size_t)n_q * d);
+        c.keys.assign(k, k + (size_t)t * d);
+        c.values.assign(v, v + (size_t)t * d);
+        if (mask) c.soft_mask.assign(mask, mask + t);
+        c.causal = causal != 0;
+        c.scale = scale;
+        c.query_pos_offset = pos_offset;
+        c.self_always_retained = self_keep != 0;
+        lkv::AttentionSaved sv;
+        std::vector<double> o = lkv::masked_attention_dense(c, &sv);
+        std::memcpy(out, o.data(), sizeof(double) * o.size());
+        if (upstream) {
+            lkv::AttentionGrads g = lkv::masked_attention_vjp(c, sv, std::vector<double>(upstream, upstream + (size_t)n_q * d));
+            std::memcpy(dq, g.queries.data(), sizeof(double) * g.queries.size());
+            std::memcpy(dk, g.keys.data(), sizeof(double) * g.keys.size());
+            std::memcpy(dv, g.values.data(), sizeof(double) * g.values.size());
+            if (mask && dmask) std::memcpy(dmask, g.soft_mask.data(), sizeof(double) * g.soft_mask.size());
+        }
     });
 }
 

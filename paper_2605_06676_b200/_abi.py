@@ -29,6 +29,7 @@ EXPORTED = [
     "lkv_decode_step", "lkv_model_validate", "lkv_model_weights_bytes", "lkv_model_load_param", "lkv_model_workspace_bytes", "lkv_model_plan",
     "lkv_model_decode_step", "lkv_budgets_shard", "lkv_evict_shard", "lkv_ragged_capacity_shard", "lkv_comm_get_unique_id",
     "lkv_comm_init", "lkv_comm_destroy", "lkv_comm_size", "lkv_comm_rank", "lkv_comm_allgatherv", "lkv_comm_gatherv",
+    "lkv_attn_workspace_bytes", "lkv_masked_attention_fwd", "lkv_masked_attention_bwd",
 ]
 
 
@@ -48,6 +49,12 @@ class RaggedDesc(C.Structure):
     _fields_ = [("n_heads", C.c_int32), ("head_dim", C.c_int32), ("dtype", C.c_int32), ("decode_slack", C.c_int32),
                 ("capacity_rows", C.c_int64), ("offsets", C.c_void_p), ("lens", C.c_void_p), ("keys", C.c_void_p),
                 ("values", C.c_void_p), ("positions", C.c_void_p)]
+
+
+class AttnDesc(C.Structure):
+    _fields_ = [("batch", C.c_int32), ("n_q_heads", C.c_int32), ("n_kv_heads", C.c_int32), ("t_q", C.c_int32),
+                ("t_k", C.c_int32), ("head_dim", C.c_int32), ("dtype", C.c_int32), ("causal", C.c_int32),
+                ("query_pos_offset", C.c_int32), ("self_always_retained", C.c_int32), ("scale", C.c_double)]
 
 
 class ModelDesc(C.Structure):
@@ -123,6 +130,12 @@ def load():
     L.lkv_comm_rank.argtypes = [vp]
     L.lkv_comm_allgatherv.argtypes = [vp, vp, vp, P(i64), P(i64), vp]
     L.lkv_comm_gatherv.argtypes = [vp, vp, vp, P(i64), P(i64), i32, vp]
+    L.lkv_attn_workspace_bytes.restype = sz
+    L.lkv_attn_workspace_bytes.argtypes = [P(AttnDesc)]
+    L.lkv_masked_attention_fwd.argtypes = [P(AttnDesc), vp, vp, vp, vp, vp, vp, vp, sz, vp]
+    L.lkv_masked_attention_bwd.argtypes = [P(AttnDesc), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+    L.lkv_masked_attention_fwd.restype = C.c_int
+    L.lkv_masked_attention_bwd.restype = C.c_int
     for name in ["lkv_budgets_shard", "lkv_evict_shard", "lkv_comm_get_unique_id", "lkv_comm_init", "lkv_comm_destroy",
                  "lkv_comm_allgatherv", "lkv_comm_gatherv"]:
         getattr(L, name).restype = C.c_int

@@ -790,6 +790,103 @@ lkv_status lkv_evict_host(const lkv_cache_desc* hc, void* dev_keys, void* dev_va
     return LKV_OK;
 }
 
+// ---- masked attention (training) -------------------------------------------
+static lkv_status check_attn(const lkv_attn_desc* a) {
+    if (!a) return fail(LKV_ERR_CONTRACT, "attention descriptor is null");
+    if (a->batch < 1 || a->n_q_heads < 1 || a->n_kv_heads < 1 || a->t_q < 1 || a->t_k < 1 || a->head_dim < 1)
+        return fail(LKV_ERR_CONTRACT, "attention: empty extents");  // attention.cpp:34
+    if (a->n_q_heads % a->n_kv_heads) return fail(LKV_ERR_CONTRACT, "attention: n_q_heads must be a multiple of n_kv_heads");
+    if (a->causal && a->query_pos_offset + 1 < 1)
+        return fail(LKV_ERR_CONTRACT, "attention: first query row admits no key");  // attention.cpp:43
+    if (!std::isfinite(a->scale)) return fail(LKV_ERR_CONTRACT, "attention: scale must be finite");
+    if (a->dtype == LKV_BF16) {
+        if (a->head_dim != 128) return fail(LKV_ERR_UNSUPPORTED, "bf16 masked attention needs head_dim 128");
+    } else if (a->dtype == LKV_F32) {
+        if (a->head_dim > 256 || (size_t)(a->head_dim + a->t_k) * 4 > 200 * 1024)
+            return fail(LKV_ERR_UNSUPPORTED, "fp32 masked attention: head_dim <= 256 and t_k <= ~51000");
+    } else {
+        return fail(LKV_ERR_CONTRACT, "unknown dtype");
+    }
+    const int64_t rows_q = (int64_t)a->batch * a->n_q_heads * a->t_q, rows_k = (int64_t)a->batch * a->n_kv_heads * a->t_k;
+    if (rows_q >= (int64_t(1) << 31) || rows_k >= (int64_t(1) << 31)) return fail(LKV_ERR_CONTRACT, "attention: too many rows");
+    return LKV_OK;
+}
+
+static AttnParams attn_params(const lkv_attn_desc* a, const void* q, const void* k, const void* v, const float* mask,
+                              void* ws) {
+    AttnParams p;
+    memset(&p, 0, sizeof p);
+    p.batch = a->batch;
+    p.n_q_heads = a->n_q_heads;
+    p.n_kv_heads = a->n_kv_heads;
+    p.t_q = a->t_q;
+    p.t_k = a->t_k;
+    p.causal = a->causal != 0;
+    p.pos_offset = a->query_pos_offset;
+    p.self_keep = a->self_always_retained != 0;
+    p.scale = (float)a->scale;
+    p.q = q;
+    p.k = k;
+    p.v = v;
+    p.mask = mask;
+    p.err = at<ErrWord>(ws, 0);
+    return p;
+}
+
+size_t lkv_attn_workspace_bytes(const lkv_attn_desc* a) {
+    if (check_attn(a)) return 0;
+    return 256 + align_up(sizeof(float) * (size_t)a->batch * a->n_q_heads * a->t_q);
+}
+
+lkv_status lkv_masked_attention_fwd(const lkv_attn_desc* a, const void* q, const void* k, const void* v,
+                                    const float* mask, void* out, float* lse, void* ws, size_t ws_bytes,
+                                    lkv_stream_t stream) {
+    lkv_status st = check_attn(a);
+    if (st) return st;
+    if (!q || !k || !v || !out || !lse) return fail(LKV_ERR_CONTRACT, "attention: null buffer");
+    if ((st = check_ws(ws, ws_bytes, lkv_attn_workspace_bytes(a)))) return st;
+    AttnParams p = attn_params(a, q, k, v, mask, ws);
+    p.out = out;
+    p.lse = lse;
+    CUtensorMap mk, mv;
+    if (a->dtype == LKV_BF16) {
+        const uint64_t rk = (uint64_t)a->batch * a->n_kv_heads * a->t_k;
+        if ((st = make_map_bf16(&mk, k, 128, rk, 64)) || (st = make_map_bf16(&mv, v, 128, rk, 64))) return st;
+    }
+    LKV_CUDA(launch_attn_fwd(p, a->dtype, a->head_dim, &mk, &mv, (cudaStream_t)stream), "masked attention fwd");
+    return LKV_OK;
+}
+
+lkv_status lkv_masked_attention_bwd(const lkv_attn_desc* a, const void* q, const void* k, const void* v,
+                                    const float* mask, const void* out, const float* lse, const void* d_out, float* dq,
+                                    float* dk, float* dv, float* dmask, void* ws, size_t ws_bytes, lkv_stream_t stream) {
+    lkv_status st = check_attn(a);
+    if (st) return st;
+    if (!q || !k || !v || !out || !lse || !d_out || !dq || !dk || !dv) return fail(LKV_ERR_CONTRACT, "attention vjp: null buffer");
+    if (mask && !dmask) return fail(LKV_ERR_CONTRACT, "attention vjp: a masked call needs dmask");
+    if ((st = check_ws(ws, ws_bytes, lkv_attn_workspace_bytes(a)))) return st;
+    AttnParams p = attn_params(a, q, k, v, mask, ws);
+    p.out = const_cast<void*>(out);
+    p.lse = const_cast<float*>(lse);
+    p.dout = d_out;
+    p.dsum = at<float>(ws, 256);
+    p.dq = dq;
+    p.dk = dk;
+    p.dv = dv;
+    p.dmask = mask ? dmask : nullptr;
+    CUtensorMap mk, mv, mq, mdo, mq32, mdo32;
+    if (a->dtype == LKV_BF16) {
+        const uint64_t rk = (uint64_t)a->batch * a->n_kv_heads * a->t_k, rq = (uint64_t)a->batch * a->n_q_heads * a->t_q;
+        if ((st = make_map_bf16(&mk, k, 128, rk, 64)) || (st = make_map_bf16(&mv, v, 128, rk, 64)) ||
+            (st = make_map_bf16(&mq, q, 128, rq, 64)) || (st = make_map_bf16(&mdo, d_out, 128, rq, 64)) ||
+            (st = make_map_bf16(&mq32, q, 128, rq, 32)) || (st = make_map_bf16(&mdo32, d_out, 128, rq, 32)))
+            return st;
+    }
+    LKV_CUDA(launch_attn_bwd(p, a->dtype, a->head_dim, &mk, &mv, &mq, &mdo, &mq32, &mdo32, (cudaStream_t)stream),
+             "masked attention bwd");
+    return LKV_OK;
+}
+
 lkv_status lkv_rope_table(int32_t t_max, int32_t head_dim, double base, int32_t pos_offset, void* table,
                           lkv_stream_t stream) {
     if (t_max < 1 || head_dim < 2 || head_dim % 2 || !(base > 0.0) || pos_offset < 0 || !table)

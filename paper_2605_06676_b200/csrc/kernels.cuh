@@ -138,6 +138,34 @@ constexpr int kDecMinCh = 128;  // smallest work item the plan may choose (works
 cudaError_t launch_decode(const DecodeParams& p, int dtype, const CUtensorMap* mk, const CUtensorMap* mv, int num_sms,
                           cudaStream_t stream);
 
+// ---- attn.cu (training-time multiplicative-mask attention)
+struct AttnParams {
+    int32_t batch, n_q_heads, n_kv_heads, t_q, t_k;
+    int32_t causal, pos_offset, self_keep;
+    float scale;
+    const void* q;      // [batch][n_q_heads][t_q][d]
+    const void* k;      // [batch][n_kv_heads][t_k][d]
+    const void* v;
+    const float* mask;  // [batch][n_kv_heads][t_k] or null (all ones)
+    void* out;          // [batch][n_q_heads][t_q][d], input dtype
+    float* lse;         // [batch][n_q_heads][t_q]: log2-domain masked log-sum-exp of scale * q.k
+    const void* dout;
+    float* dsum;        // [batch][n_q_heads][t_q] = rowsum(dO * O) (workspace)
+    float* dq;          // fp32 gradients
+    float* dk;
+    float* dv;
+    float* dmask;       // null when mask is null
+    ErrWord* err;
+};
+cudaError_t launch_attn_fwd(const AttnParams& p, int dtype, int d, const CUtensorMap* mk, const CUtensorMap* mv,
+                            cudaStream_t stream);
+cudaError_t launch_attn_bwd(const AttnParams& p, int dtype, int d, const CUtensorMap* mk, const CUtensorMap* mv,
+                            const CUtensorMap* mq, const CUtensorMap* mdo, const CUtensorMap* mq32,
+                            const CUtensorMap* mdo32, cudaStream_t stream);
+size_t attn_fwd_smem();
+size_t attn_dq_smem();
+size_t attn_dkv_smem();
+
 // ---- model.cu (full decode step of the toy GQA model)
 enum GemvEpi { EPI_QKV = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_F32 = 3 };
 struct GemvParams {

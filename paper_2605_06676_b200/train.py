@@ -1,0 +1,78 @@
+"""Training-time operators of LKV on the B200.
+
+* ``masked_attention_fwd`` / ``masked_attention_bwd`` -- the multiplicative soft-mask attention
+  of ``attention.hpp:52-69`` (``masked_attention_dense`` + ``masked_attention_vjp``,
+  ``attention.cpp:46-201``) for a batch of heads with GQA, i.e. every per-query-head call of
+  ``forward_masked`` (``model.cpp:100-112``) in one launch; dK, dV and the mask gradient are
+  summed over the query heads of a group, as the reference's autodiff accumulates them.
+  Over the C ABI ``lkv_masked_attention_fwd`` / ``_bwd``.
+
+Layouts: q / out / d_out ``[B, Hq, Tq, D]``; k / v ``[B, Hkv, Tk, D]`` (bf16 with D = 128 on
+tensor cores, or fp32); mask ``[B, Hkv, Tk]`` fp32 or None; gradients fp32.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import torch
+
+from . import ContractError, Workspace, _check, _dtype_code, _ptr, _stream, lib
+from ._abi import AttnDesc
+
+
+def _desc(q, k, causal, scale, pos_offset, self_keep) -> AttnDesc:
+    if q.dim() != 4 or k.dim() != 4:
+        raise ContractError("masked attention: q [B,Hq,Tq,D] and k/v [B,Hkv,Tk,D] required")
+    B, Hq, Tq, D = q.shape
+    Bk, Hkv, Tk, Dk = k.shape
+    if Bk != B or Dk != D:
+        raise ContractError("masked attention: q/k/v shape mismatch")
+    scale = 1.0 / math.sqrt(D) if scale is None else float(scale)
+    return AttnDesc(B, Hq, Hkv, Tq, Tk, D, _dtype_code(q.dtype), int(causal), int(pos_offset), int(self_keep), scale)
+
+
+def _ws(desc: AttnDesc, device) -> Workspace:
+    n = lib().lkv_attn_workspace_bytes(C.byref(desc))
+    if n == 0:
+        _check(lib().lkv_masked_attention_fwd(C.byref(desc), None, None, None, None, None, None, None, 0, None))
+    return Workspace(n, device=device)
+
+
+def masked_attention_fwd(q, k, v, mask=None, causal=True, scale=None, pos_offset=0, self_keep=False,
+                         ws: Workspace | None = None, check=True):
+    """-> (out [B,Hq,Tq,D] in q's dtype, lse [B,Hq,Tq] fp32, log2 domain)."""
+    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    if k.shape != v.shape or k.dtype != q.dtype or v.dtype != q.dtype:
+        raise ContractError("masked attention: k/v must match and share q's dtype")
+    desc = _desc(q, k, causal, scale, pos_offset, self_keep)
+    m = mask.to(torch.float32).contiguous() if mask is not None else None
+    if m is not None and tuple(m.shape) != tuple(k.shape[:3]):
+        raise ContractError("masked attention: mask must be [B, Hkv, Tk]")
+    ws = ws or _ws(desc, q.device)
+    out = torch.empty_like(q)
+    lse = torch.empty(q.shape[:3], dtype=torch.float32, device=q.device)
+    _check(lib().lkv_masked_attention_fwd(C.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(m), _ptr(out), _ptr(lse),
+                                          C.c_void_p(ws.ptr), ws.nbytes, _stream()))
+    if check:
+        ws.status()
+    return out, lse
+
+
+def masked_attention_bwd(q, k, v, mask, out, lse, d_out, causal=True, scale=None, pos_offset=0, self_keep=False,
+                         ws: Workspace | None = None, check=True):
+    """-> (dq [B,Hq,Tq,D], dk, dv [B,Hkv,Tk,D], dmask [B,Hkv,Tk] or None), all fp32."""
+    q, k, v, d_out = q.contiguous(), k.contiguous(), v.contiguous(), d_out.contiguous().to(q.dtype)
+    desc = _desc(q, k, causal, scale, pos_offset, self_keep)
+    m = mask.to(torch.float32).contiguous() if mask is not None else None
+    ws = ws or _ws(desc, q.device)
+    dq = torch.empty(q.shape, dtype=torch.float32, device=q.device)
+    dk = torch.empty(k.shape, dtype=torch.float32, device=q.device)
+    dv = torch.empty(k.shape, dtype=torch.float32, device=q.device)
+    dm = torch.empty(k.shape[:3], dtype=torch.float32, device=q.device) if m is not None else None
+    _check(lib().lkv_masked_attention_bwd(C.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(m), _ptr(out.contiguous()),
+                                          _ptr(lse), _ptr(d_out), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(dm),
+                                          C.c_void_p(ws.ptr), ws.nbytes, _stream()))
+    if check:
+        ws.status()
+    return dq, dk, dv, dm

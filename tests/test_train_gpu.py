@@ -1,0 +1,140 @@
+"""GPU parity of the training-time operators against the fp64 oracle.
+
+masked attention forward + backward (attention.cpp:46-201): the GPU output, dQ, dK, dV and the
+mask gradient vs the oracle's restatement of masked_attention_dense / masked_attention_vjp on the
+same (rounded) inputs, per query head, with dK/dV/dmask summed over each GQA group.  Tolerance
+max|d| / max|ref| <= 1e-5 for fp32 inputs and <= 1e-2 for bf16 (north_star), written per case.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import paper_2605_06676_b200 as lkv
+from paper_2605_06676_b200 import train
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def rel_gap(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b)) / (np.max(np.abs(b)) + 1e-12)) if a.size else 0.0
+
+
+def _inputs(B, Hq, Hkv, Tq, Tk, D, dtype, masked, seed, zero_frac=0.2):
+    g = torch.Generator(device=DEV).manual_seed(seed)
+    q = torch.randn(B, Hq, Tq, D, generator=g, device=DEV).to(dtype)
+    k = torch.randn(B, Hkv, Tk, D, generator=g, device=DEV).to(dtype)
+    v = torch.randn(B, Hkv, Tk, D, generator=g, device=DEV).to(dtype)
+    du = torch.randn(B, Hq, Tq, D, generator=g, device=DEV).to(dtype)
+    mask = None
+    if masked:
+        mask = torch.rand(B, Hkv, Tk, generator=g, device=DEV)
+        mask[torch.rand(B, Hkv, Tk, generator=g, device=DEV) < zero_frac] = 0.0
+        mask[:, :, 0] = 1.0  # every causal row keeps some mass
+    return q, k, v, du, mask
+
+
+def _oracle(q, k, v, mask, du, causal, scale, pos_offset, self_keep):
+    B, Hq, Tq, D = q.shape
+    Hkv, Tk = k.shape[1], k.shape[2]
+    G = Hq // Hkv
+    f = lambda t: t.detach().to(torch.float64).cpu().numpy()
+    qn, kn, vn, un = f(q), f(k), f(v), f(du)
+    mn = mask.detach().double().cpu().numpy() if mask is not None else None
+    out = np.zeros((B, Hq, Tq, D))
+    dq = np.zeros_like(out)
+    dk = np.zeros((B, Hkv, Tk, D))
+    dv = np.zeros_like(dk)
+    dm = np.zeros((B, Hkv, Tk)) if mask is not None else None
+    for b in range(B):
+        for h in range(Hq):
+            kv = h // G
+            o, gq, gk, gv, gm = O.masked_attention(qn[b, h], kn[b, kv], vn[b, kv], None if mn is None else mn[b, kv],
+                                                   causal, scale, pos_offset, self_keep, upstream=un[b, h])
+            out[b, h] = o
+            dq[b, h] = gq
+            dk[b, kv] += gk
+            dv[b, kv] += gv
+            if dm is not None:
+                dm[b, kv] += gm
+    return out, dq, dk, dv, dm
+
+
+CASES = [
+    # B, Hq, Hkv, Tq, Tk, D, dtype, masked, causal, pos_offset, self_keep, tol
+    (1, 4, 1, 130, 130, 128, torch.bfloat16, True, True, 0, False, 1e-2),
+    (2, 8, 2, 64, 64, 128, torch.bfloat16, True, True, 0, True, 1e-2),
+    (1, 4, 4, 100, 257, 128, torch.bfloat16, True, True, 157, False, 1e-2),  # query chunk at the end of the keys
+    (1, 2, 1, 70, 200, 128, torch.bfloat16, True, False, 0, False, 1e-2),     # not causal
+    (1, 4, 2, 96, 96, 128, torch.bfloat16, False, True, 0, False, 1e-2),      # no mask
+    (1, 8, 2, 45, 45, 16, torch.float32, True, True, 0, False, 1e-5),         # the reference's toy head width
+    (2, 4, 1, 33, 80, 128, torch.float32, True, True, 47, True, 1e-5),
+    (1, 2, 2, 20, 50, 64, torch.float32, False, False, 0, False, 1e-5),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[f"c{i}" for i in range(len(CASES))])
+def test_masked_attention_fwd_bwd_vs_oracle(case):
+    B, Hq, Hkv, Tq, Tk, D, dtype, masked, causal, off, self_keep, tol = case
+    q, k, v, du, mask = _inputs(B, Hq, Hkv, Tq, Tk, D, dtype, masked, seed=hash(case) % 10000)
+    scale = 1.0 / np.sqrt(D)
+    out, lse = train.masked_attention_fwd(q, k, v, mask, causal, scale, off, self_keep)
+    dq, dk, dv, dm = train.masked_attention_bwd(q, k, v, mask, out, lse, du, causal, scale, off, self_keep)
+    ref = _oracle(q, k, v, mask, du, causal, scale, off, self_keep)
+    got = [out, dq, dk, dv, dm]
+    for name, g, r in zip(["out", "dq", "dk", "dv", "dmask"], got, ref):
+        if r is None:
+            assert g is None
+            continue
+        gap = rel_gap(g.double().cpu().numpy(), r)
+        assert gap <= tol, (name, gap)
+
+
+def test_masked_attention_matches_reference_known_answers():
+    """test_attention.cpp:105-114 (rows stochastic): with V = I-like one-hot rows the output rows
+    are the attention weights, which sum to 1 and vanish on zero-mask keys."""
+    T, D = 64, 128
+    q = torch.randn(1, 1, T, D, device=DEV).to(torch.bfloat16)
+    k = torch.randn(1, 1, T, D, device=DEV).to(torch.bfloat16)
+    v = torch.zeros(1, 1, T, D, device=DEV)
+    v[0, 0, torch.arange(T), torch.arange(T)] = 1.0
+    v = v.to(torch.bfloat16)
+    mask = torch.ones(1, 1, T, device=DEV)
+    mask[0, 0, 5] = 0.0
+    out, _ = train.masked_attention_fwd(q, k, v, mask, True, 1.0 / np.sqrt(D))
+    w = out[0, 0, :, :T].float()
+    assert torch.allclose(w.sum(dim=1), torch.ones(T, device=DEV), atol=2e-2)
+    assert float(w[:, 5].abs().max()) == 0.0
+    assert float(torch.triu(w, diagonal=1).abs().max()) == 0.0  # causal
+
+
+def test_masked_attention_errors():
+    q, k, v, du, mask = _inputs(1, 2, 1, 16, 16, 128, torch.bfloat16, True, seed=3)
+    bad = mask.clone()
+    bad[0, 0, 3] = -1.0
+    with pytest.raises(lkv.ContractError):  # attention.cpp:40-42
+        train.masked_attention_fwd(q, k, v, bad)
+    zero = torch.zeros_like(mask)
+    with pytest.raises(lkv.DegenerateMaskError):  # attention.cpp:82-84
+        train.masked_attention_fwd(q, k, v, zero)
+    # self_always_retained keeps the row alive even with an all-zero mask (decode-style call)
+    out, _ = train.masked_attention_fwd(q, k, v, zero, True, None, 0, True)
+    assert torch.isfinite(out.float()).all()
+    with pytest.raises(lkv.ContractError):  # first row admits no key
+        train.masked_attention_fwd(q, k, v, mask, True, None, -1)
+    with pytest.raises(lkv.UnsupportedError):
+        train.masked_attention_fwd(q[..., :64].contiguous(), k[..., :64].contiguous(), v[..., :64].contiguous())
+
+
+def test_masked_attention_deterministic():
+    q, k, v, du, mask = _inputs(1, 4, 2, 200, 200, 128, torch.bfloat16, True, seed=9)
+    a = train.masked_attention_fwd(q, k, v, mask)
+    b = train.masked_attention_fwd(q, k, v, mask)
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+    ga = train.masked_attention_bwd(q, k, v, mask, a[0], a[1], du)
+    gb = train.masked_attention_bwd(q, k, v, mask, a[0], a[1], du)
+    for x, y in zip(ga, gb):
+        assert torch.equal(x, y)
