@@ -20,6 +20,8 @@
  *   lkv_evict_shard <- the same on one rank's head shard (multi-GPU; lkv_comm_* = NCCL)
  *   lkv_decode_step <- decode_step's append + attention block (model.hpp:95,
  *                      model.cpp:240-265) -> masked_attention_dense (attention.hpp:57)
+ *   lkv_soft_topk_fwd/_vjp <- soft_topk_forward / soft_topk_vjp (soft_topk.hpp:60-67;
+ *                      training)
  *   lkv_masked_attention_fwd/_bwd <- masked_attention_dense / masked_attention_vjp
  *                      (attention.hpp:57-69; training)
  *   lkv_model_*     <- the whole decode_step (model.hpp:95, model.cpp:209-287):
@@ -259,6 +261,22 @@ lkv_status lkv_comm_gatherv(lkv_comm_t comm, const void* send, void* recv, const
  * head_dim 128 (tensor cores); fp32 runs the exact SIMT path (head_dim <= 256).  Errors:
  * mask value < 0 or non-finite -> CONTRACT, a row whose masked mass vanishes ->
  * DEGENERATE_MASK (both latched in the workspace). */
+/* Soft-TopK over n_seg independent segments of n scores (row stride ld):
+ * soft_topk_forward (soft_topk.hpp:60, soft_topk.cpp:111-164) with k[seg] in (0, n), tau > 0;
+ * optional noise: scores are x + noise_scale * noise (training_mask, policy.cpp:138-150).
+ * Outputs values [n_seg][ld] (fp64), density (the VJP's saved state, nullable), values_f32
+ * (nullable: an fp32 copy usable directly as the masked-attention mask) and lambda [n_seg]
+ * (nullable).  Device-side errors: k outside (0, n) -> BUDGET, non-finite score -> NUMERIC,
+ * |score| > 1e300 -> OVERFLOW_GUARD, constraint |sum - k| > 1e-9 n -> NUMERIC.
+ * lkv_soft_topk_vjp: soft_topk_vjp (soft_topk.cpp:166-189) -> grad_x [n_seg][ld], grad_k [n_seg].
+ * Workspace: >= 256 bytes (the error latch). */
+lkv_status lkv_soft_topk_fwd(const double* x, const double* noise, double noise_scale, int32_t n_seg, int32_t n,
+                             int64_t ld, const double* k, double tau, double* values, double* density,
+                             float* values_f32, double* lambda, void* workspace, size_t workspace_bytes,
+                             lkv_stream_t stream);
+lkv_status lkv_soft_topk_vjp(const double* density, const double* upstream, int32_t n_seg, int32_t n, int64_t ld,
+                             double tau, double* grad_x, double* grad_k, lkv_stream_t stream);
+
 typedef struct lkv_attn_desc {
     int32_t batch, n_q_heads, n_kv_heads, t_q, t_k, head_dim, dtype;
     int32_t causal;               /* row r admits keys j <= query_pos_offset + r */

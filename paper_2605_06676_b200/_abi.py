@@ -29,7 +29,8 @@ EXPORTED = [
     "lkv_decode_step", "lkv_model_validate", "lkv_model_weights_bytes", "lkv_model_load_param", "lkv_model_workspace_bytes", "lkv_model_plan",
     "lkv_model_decode_step", "lkv_budgets_shard", "lkv_evict_shard", "lkv_ragged_capacity_shard", "lkv_comm_get_unique_id",
     "lkv_comm_init", "lkv_comm_destroy", "lkv_comm_size", "lkv_comm_rank", "lkv_comm_allgatherv", "lkv_comm_gatherv",
-    "lkv_attn_workspace_bytes", "lkv_masked_attention_fwd", "lkv_masked_attention_bwd",
+    "lkv_attn_workspace_bytes", "lkv_masked_attention_fwd", "lkv_masked_attention_bwd", "lkv_soft_topk_fwd",
+    "lkv_soft_topk_vjp",
 ]
 
 
@@ -134,6 +135,10 @@ def load():
     L.lkv_attn_workspace_bytes.argtypes = [P(AttnDesc)]
     L.lkv_masked_attention_fwd.argtypes = [P(AttnDesc), vp, vp, vp, vp, vp, vp, vp, sz, vp]
     L.lkv_masked_attention_bwd.argtypes = [P(AttnDesc), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+    L.lkv_soft_topk_fwd.argtypes = [vp, vp, dbl, i32, i32, i64, vp, dbl, vp, vp, vp, vp, vp, sz, vp]
+    L.lkv_soft_topk_vjp.argtypes = [vp, vp, i32, i32, i64, dbl, vp, vp, vp]
+    L.lkv_soft_topk_fwd.restype = C.c_int
+    L.lkv_soft_topk_vjp.restype = C.c_int
     L.lkv_masked_attention_fwd.restype = C.c_int
     L.lkv_masked_attention_bwd.restype = C.c_int
     for name in ["lkv_budgets_shard", "lkv_evict_shard", "lkv_comm_get_unique_id", "lkv_comm_init", "lkv_comm_destroy",

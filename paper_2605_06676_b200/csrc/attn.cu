@@ -72,6 +72,11 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
     return *reinterpret_cast<uint32_t*>(&v);
 }
 __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+__device__ __forceinline__ float fast_exp2(float x) {  // MUFU.EX2 (2 ulp); ex2(-inf) = +0
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 
 // byte offset of (row, 16-byte chunk q in 0..15) of a ROWS x 256 B tile stored as two
 // ROWS x 128 B TMA boxes with the 128-byte swizzle
@@ -107,6 +112,13 @@ __device__ __forceinline__ void frag_bk(uint32_t base, int r0, int n2, int lane,
     ldsm_x4_t(base + sw<ROWS>(r0 + ((j & 1) << 3) + (lane & 7), n2 * 2 + (j >> 1)), b);
 }
 
+// mask values of key columns j, j+1 (j even): 0 past t_k, 1 without a mask
+__device__ __forceinline__ float2 load_mask2(const float* mask, bool vec, int j, int t_k) {
+    if (!mask) return make_float2(1.f, 1.f);
+    if (vec && j + 1 < t_k) return __ldg(reinterpret_cast<const float2*>(mask + j));
+    return make_float2(j < t_k ? __ldg(mask + j) : 0.f, j + 1 < t_k ? __ldg(mask + j + 1) : 0.f);
+}
+
 struct Geo {
     int n_q_heads, n_kv_heads, G, t_q, t_k, causal, pos_offset, self_keep;
     float c;      // scale * log2(e)
@@ -129,12 +141,14 @@ __device__ __forceinline__ float mask_eff(const Geo& g, const float* mask, int j
 // =====================================================================================================
 __global__ void __launch_bounds__(kThreads, 2)
     fwd_bf16_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ CUtensorMap tk,
-                    const __grid_constant__ CUtensorMap tv) {
+                    const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tq) {
     constexpr int kStageBytes = 2 * kKB * 256;
     extern __shared__ unsigned char smem_dyn[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+    unsigned char* qs = smem + kStages * kStageBytes;  // Q tile [64][256 B]
+    uint64_t* full = reinterpret_cast<uint64_t*>(qs + kQB * 256);
     uint64_t* empty = full + kStages;
+    uint64_t* qbar = empty + kStages;
     const Geo g{p.n_q_heads, p.n_kv_heads, p.n_q_heads / p.n_kv_heads, p.t_q, p.t_k, p.causal, p.pos_offset,
                 p.self_keep, p.scale * kLog2e, p.scale};
     const int b = blockIdx.z, qh = blockIdx.y, kvh = qh / g.G;
@@ -147,6 +161,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], kConsumers);
         }
+        mbar_init(qbar, 1);
         fence_barrier_init();
     }
     __syncthreads();
@@ -156,6 +171,8 @@ __global__ void __launch_bounds__(kThreads, 2)
             tma_prefetch_desc(&tk);
             tma_prefetch_desc(&tv);
             const uint64_t pol = l2_policy_evict_last();  // K/V tiles are re-read by every query block
+            mbar_arrive_expect_tx(qbar, kQB * 256);
+            tma_tile<kQB>(qs, &tq, qbar, (int)(((size_t)b * g.n_q_heads + qh) * g.t_q + q0), pol);
             for (int t = 0; t < ntiles; ++t) {
                 const int st = t % kStages;
                 if (t >= kStages) mbar_wait(&empty[st], ((t / kStages) - 1) & 1);
@@ -170,25 +187,13 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int gq = lane >> 2, cq = (lane & 3) * 2;
     const int r_lo = q0 + warp * 16 + gq, r_hi = r_lo + 8;  // this thread's two query rows
     const float* mask = p.mask ? p.mask + ((size_t)b * g.n_kv_heads + kvh) * g.t_k : nullptr;
-    // Q fragments straight from global (rows past t_q read as 0)
-    uint32_t qa[8][4];
-    {
-        const __nv_bfloat16* qb = static_cast<const __nv_bfloat16*>(p.q) + (((size_t)b * g.n_q_heads + qh) * g.t_q) * kD;
-        const uint32_t* lo = reinterpret_cast<const uint32_t*>(qb + (size_t)r_lo * kD);
-        const uint32_t* hi = reinterpret_cast<const uint32_t*>(qb + (size_t)r_hi * kD);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-            const int c0 = (kk * 16 + cq) >> 1;
-            qa[kk][0] = r_lo < g.t_q ? __ldg(lo + c0) : 0u;
-            qa[kk][1] = r_hi < g.t_q ? __ldg(hi + c0) : 0u;
-            qa[kk][2] = r_lo < g.t_q ? __ldg(lo + c0 + 4) : 0u;
-            qa[kk][3] = r_hi < g.t_q ? __ldg(hi + c0 + 4) : 0u;
-        }
-    }
+    const bool mask_vec = (reinterpret_cast<uintptr_t>(mask) & 7) == 0;
+    const uint32_t qsb = smem_u32(qs);
+    mbar_wait(qbar, 0);
     float o[16][4];
 #pragma unroll
     for (int n = 0; n < 16; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-    float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f, raw_lo = 0.f, raw_hi = 0.f;
+    float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;
     for (int t = 0; t < ntiles; ++t) {
         const int st = t % kStages;
         mbar_wait(&full[st], (t / kStages) & 1);
@@ -199,57 +204,76 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int n = 0; n < 8; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
+            uint32_t qa[4];
+            frag_a<kQB>(qsb, warp * 16, kk, lane, qa);
 #pragma unroll
             for (int np = 0; np < 4; ++np) {
                 uint32_t bf[4];
                 frag_bn<kKB>(kb, np * 16, kk, lane, bf);
-                mma(s[2 * np], qa[kk], bf[0], bf[1]);
-                mma(s[2 * np + 1], qa[kk], bf[2], bf[3]);
+                mma(s[2 * np], qa, bf[0], bf[1]);
+                mma(s[2 * np + 1], qa, bf[2], bf[3]);
             }
         }
-        // admissibility, scale, running max over the RAW admissible scores
+        // interior tiles (every key admissible for all 16 rows of this warp) skip the per-element
+        // admissibility tests; only the causal diagonal and the ragged ends take the slow path
+        const int wr0 = q0 + warp * 16;
+        const bool interior = j0 + kKB <= g.t_k && wr0 + 16 <= g.t_q && (!g.causal || j0 + kKB - 1 <= g.pos_offset + wr0) &&
+                              !(g.self_keep && j0 + kKB - 1 >= g.pos_offset + wr0);
+        // this thread's 16 mask values (the same key columns for both rows)
         float mx_lo = -INFINITY, mx_hi = -INFINITY;
+        if (interior) {
 #pragma unroll
-        for (int n = 0; n < 8; ++n)
+            for (int n = 0; n < 8; ++n)
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int j = j0 + n * 8 + cq + e;
-                s[n][e] = admissible(g, j, r_lo) ? s[n][e] * g.c : -INFINITY;
-                s[n][2 + e] = admissible(g, j, r_hi) ? s[n][2 + e] * g.c : -INFINITY;
-                mx_lo = fmaxf(mx_lo, s[n][e]);
-                mx_hi = fmaxf(mx_hi, s[n][2 + e]);
-            }
+                for (int e = 0; e < 2; ++e) {
+                    s[n][e] *= g.c;
+                    s[n][2 + e] *= g.c;
+                    mx_lo = fmaxf(mx_lo, s[n][e]);
+                    mx_hi = fmaxf(mx_hi, s[n][2 + e]);
+                }
+        } else {
+#pragma unroll
+            for (int n = 0; n < 8; ++n)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int j = j0 + n * 8 + cq + e;
+                    s[n][e] = admissible(g, j, r_lo) ? s[n][e] * g.c : -INFINITY;
+                    s[n][2 + e] = admissible(g, j, r_hi) ? s[n][2 + e] * g.c : -INFINITY;
+                    mx_lo = fmaxf(mx_lo, s[n][e]);
+                    mx_hi = fmaxf(mx_hi, s[n][2 + e]);
+                }
+        }
         mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 1));
         mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 2));
         mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 1));
         mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 2));
         const float mn_lo = fmaxf(m_lo, mx_lo), mn_hi = fmaxf(m_hi, mx_hi);
-        const float a_lo = mn_lo == -INFINITY ? 1.f : exp2f(m_lo - mn_lo);
-        const float a_hi = mn_hi == -INFINITY ? 1.f : exp2f(m_hi - mn_hi);
+        const float a_lo = mn_lo == -INFINITY ? 1.f : fast_exp2(m_lo - mn_lo);
+        const float a_hi = mn_hi == -INFINITY ? 1.f : fast_exp2(m_hi - mn_hi);
         m_lo = mn_lo;
         m_hi = mn_hi;
-        float sl = 0.f, sh = 0.f, rl = 0.f, rh = 0.f;
+        // a row with no admissible key yet has mn = -inf: exp2(-inf - -inf) would be NaN
+        const float sub_lo = mn_lo == -INFINITY ? 0.f : mn_lo, sub_hi = mn_hi == -INFINITY ? 0.f : mn_hi;
+        float sl = 0.f, sh = 0.f;
 #pragma unroll
-        for (int n = 0; n < 8; ++n)
+        for (int n = 0; n < 8; ++n) {
+            const float2 m2 = load_mask2(mask, mask_vec, j0 + n * 8 + cq, g.t_k);
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                const int j = j0 + n * 8 + cq + e;
-                const bool al = s[n][e] != -INFINITY, ah = s[n][2 + e] != -INFINITY;
-                const float pl = al ? exp2f(s[n][e] - mn_lo) : 0.f;
-                const float ph = ah ? exp2f(s[n][2 + e] - mn_hi) : 0.f;
-                const float ml = al ? mask_eff(g, mask, j, r_lo) : 0.f;
-                const float mh = ah ? mask_eff(g, mask, j, r_hi) : 0.f;
-                rl += pl;
-                rh += ph;
-                s[n][e] = pl * ml;
-                s[n][2 + e] = ph * mh;
+                float ml = e ? m2.y : m2.x, mh = ml;
+                if (!interior && g.self_keep) {
+                    const int j = j0 + n * 8 + cq + e;
+                    if (j == g.pos_offset + r_lo) ml = 1.f;
+                    if (j == g.pos_offset + r_hi) mh = 1.f;
+                }
+                s[n][e] = fast_exp2(s[n][e] - sub_lo) * ml;  // exp2(-inf) = 0 for inadmissible keys
+                s[n][2 + e] = fast_exp2(s[n][2 + e] - sub_hi) * mh;
                 sl += s[n][e];
                 sh += s[n][2 + e];
             }
+        }
         l_lo = l_lo * a_lo + sl;
         l_hi = l_hi * a_hi + sh;
-        raw_lo = raw_lo * a_lo + rl;
-        raw_hi = raw_hi * a_hi + rh;
 #pragma unroll
         for (int n = 0; n < 16; ++n) {
             o[n][0] *= a_lo;
@@ -277,8 +301,6 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int x = 1; x <= 2; x <<= 1) {
         l_lo += __shfl_xor_sync(0xffffffffu, l_lo, x);
         l_hi += __shfl_xor_sync(0xffffffffu, l_hi, x);
-        raw_lo += __shfl_xor_sync(0xffffffffu, raw_lo, x);
-        raw_hi += __shfl_xor_sync(0xffffffffu, raw_hi, x);
     }
     const size_t row_base = ((size_t)b * g.n_q_heads + qh) * g.t_q;
     __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
@@ -286,9 +308,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int h = 0; h < 2; ++h) {
         const int r = h ? r_hi : r_lo;
         if (r >= g.t_q) continue;
-        const float l = h ? l_hi : l_lo, raw = h ? raw_hi : raw_lo, m = h ? m_hi : m_lo;
-        // attention.cpp:82-84: the masked mass z = l / raw must stay above 1e-300 (fp32: > 0)
-        if (!(l > 0.f) || !(raw > 0.f)) {
+        const float l = h ? l_hi : l_lo, m = h ? m_hi : m_lo;
+        // attention.cpp:82-84: the masked mass z = l / raw must stay above 1e-300; every row
+        // admits key 0, so raw >= 1 after the max shift and the test is l > 0 in fp32
+        if (!(l > 0.f)) {
             if ((lane & 3) == 0) latch_error(p.err, LKV_ERR_DEGENERATE_MASK, r);
             continue;
         }
@@ -391,6 +414,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int gq = lane >> 2, cq = (lane & 3) * 2;
     const int r_lo = q0 + warp * 16 + gq, r_hi = r_lo + 8;
     const float* mask = p.mask ? p.mask + ((size_t)b * g.n_kv_heads + kvh) * g.t_k : nullptr;
+    const bool mask_vec = (reinterpret_cast<uintptr_t>(mask) & 7) == 0;
     const float lse_lo = r_lo < g.t_q ? p.lse[q_row0 + r_lo] : 0.f, lse_hi = r_hi < g.t_q ? p.lse[q_row0 + r_hi] : 0.f;
     const float d_lo = r_lo < g.t_q ? p.dsum[q_row0 + r_lo] : 0.f, d_hi = r_hi < g.t_q ? p.dsum[q_row0 + r_hi] : 0.f;
     const uint32_t qsb = smem_u32(qs), dob = qsb + kQB * 256;
@@ -424,18 +448,27 @@ __global__ void __launch_bounds__(kThreads, 2)
                 mma(dp[2 * np + 1], ua, bv[2], bv[3]);
             }
         }
-        // dS = P (dP - D), P = exp2(s c - lse) m
+        // dS = P (dP - D), P = exp2(s c - lse) m; interior tiles skip the admissibility tests
+        const int wr0 = q0 + warp * 16;
+        const bool interior = j0 + kKB <= g.t_k && wr0 + 16 <= g.t_q && (!g.causal || j0 + kKB - 1 <= g.pos_offset + wr0) &&
+                              !(g.self_keep && j0 + kKB - 1 >= g.pos_offset + wr0);
 #pragma unroll
-        for (int n = 0; n < 8; ++n)
+        for (int n = 0; n < 8; ++n) {
+            const float2 m2 = load_mask2(mask, mask_vec, j0 + n * 8 + cq, g.t_k);
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                const int j = j0 + n * 8 + cq + e;
-                const float pl = admissible(g, j, r_lo) ? exp2f(s[n][e] * g.c - lse_lo) * mask_eff(g, mask, j, r_lo) : 0.f;
-                const float ph =
-                    admissible(g, j, r_hi) ? exp2f(s[n][2 + e] * g.c - lse_hi) * mask_eff(g, mask, j, r_hi) : 0.f;
+                const float el = fast_exp2(s[n][e] * g.c - lse_lo), eh = fast_exp2(s[n][2 + e] * g.c - lse_hi);
+                const float mj = e ? m2.y : m2.x;
+                float pl = el * mj, ph = eh * mj;
+                if (!interior) {
+                    const int j = j0 + n * 8 + cq + e;
+                    pl = !admissible(g, j, r_lo) ? 0.f : (g.self_keep && j == g.pos_offset + r_lo) ? el : pl;
+                    ph = !admissible(g, j, r_hi) ? 0.f : (g.self_keep && j == g.pos_offset + r_hi) ? eh : ph;
+                }
                 s[n][e] = pl * (dp[n][e] - d_lo);
                 s[n][2 + e] = ph * (dp[n][2 + e] - d_hi);
             }
+        }
         // dQ += dS K
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
@@ -530,6 +563,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int e = 0; e < 4; ++e) dk[n][e] = dv[n][e] = 0.f;
     float dm_lo = 0.f, dm_hi = 0.f;
+    const float mk_lo = !mask ? 1.f : j_lo < g.t_k ? __ldg(mask + j_lo) : 0.f;
+    const float mk_hi = !mask ? 1.f : j_hi < g.t_k ? __ldg(mask + j_hi) : 0.f;
     for (int t = 0; t < ntiles; ++t) {
         const int st = t % kStages;
         mbar_wait(&full[st], (t / kStages) & 1);
@@ -557,7 +592,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mma(dp[2 * np + 1], va, bu[2], bu[3]);
             }
         }
-        // element (key jx, query r): P = exp2(s c - lse_r) m, Pm = exp2(s c - lse_r)
+        // element (key j, query r): P = exp2(s c - lse_r) m_j, Pm = exp2(s c - lse_r); interior tiles
+        // (all 16 keys of the warp admissible for all 32 queries, no self key) skip the tests
+        const int wk0 = k0 + warp * 16;
+        const bool interior = wk0 + 16 <= g.t_k && r0 + kQT <= g.t_q && (!g.causal || wk0 + 15 <= g.pos_offset + r0) &&
+                              !(g.self_keep && wk0 + 15 >= g.pos_offset + r0);
         float pt[4][4];
 #pragma unroll
         for (int n = 0; n < 4; ++n)
@@ -571,16 +610,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int h = 0; h < 2; ++h) {
                     const int j = h ? j_hi : j_lo;
                     float& sv = s[n][2 * h + e];
-                    const float dpv = dp[n][2 * h + e];
-                    float pm = 0.f, pv = 0.f;
-                    if (admissible(g, j, r)) {
-                        pm = exp2f(sv * g.c - lse);
-                        const bool self = g.self_keep && j == g.pos_offset + r;
-                        pv = pm * (self ? 1.f : (mask ? __ldg(mask + j) : 1.f));
-                        if (!self) (h ? dm_hi : dm_lo) += pm * (dpv - dd);
+                    const float dpv = dp[n][2 * h + e] - dd;
+                    float pm = fast_exp2(sv * g.c - lse), mj = h ? mk_hi : mk_lo;
+                    if (!interior) {
+                        if (!admissible(g, j, r)) pm = 0.f;
+                        if (g.self_keep && j == g.pos_offset + r) mj = -1.f;  // self: multiplier 1, no dmask
                     }
+                    const float pv = mj < 0.f ? pm : pm * mj;
+                    if (mj >= 0.f) (h ? dm_hi : dm_lo) += pm * dpv;
                     pt[n][2 * h + e] = pv;
-                    sv = pv * (dpv - dd);  // dS^T
+                    sv = pv * dpv;  // dS^T
                 }
             }
         // dV += P^T dO, dK += dS^T Q  (k = the 32 queries: 2 k16 steps)
@@ -796,14 +835,14 @@ __global__ void __launch_bounds__(kSimt) dkv_f32_kernel(const __grid_constant__ 
 }  // namespace attn
 
 // ---- host launchers ----------------------------------------------------------------------------------
-size_t attn_fwd_smem() { return 1024 + attn::kStages * (2 * attn::kKB * 256) + 2 * attn::kStages * 8; }
-size_t attn_dq_smem() { return attn_fwd_smem() + 2 * attn::kQB * 256 + 8; }
+size_t attn_fwd_smem() { return 1024 + attn::kStages * (2 * attn::kKB * 256) + attn::kQB * 256 + 2 * attn::kStages * 8 + 8; }
+size_t attn_dq_smem() { return 1024 + attn::kStages * (2 * attn::kKB * 256) + 2 * attn::kQB * 256 + 2 * attn::kStages * 8 + 8; }
 size_t attn_dkv_smem() {
     return 1024 + attn::kStages * (2 * attn::kQT * 256) + 2 * attn::kKB * 256 + 2 * attn::kStages * 8 + 8;
 }
 
 cudaError_t launch_attn_fwd(const AttnParams& p, int dtype, int d, const CUtensorMap* mk, const CUtensorMap* mv,
-                            cudaStream_t stream) {
+                            const CUtensorMap* mq, cudaStream_t stream) {
     if (p.mask) {
         const int64_t n = (int64_t)p.batch * p.n_kv_heads * p.t_k;
         attn::mask_check_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 1184), 256, 0, stream>>>(p.mask, n, p.err);
@@ -814,7 +853,7 @@ cudaError_t launch_attn_fwd(const AttnParams& p, int dtype, int d, const CUtenso
         cudaError_t e = cudaFuncSetAttribute(attn::fwd_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         attn::fwd_bf16_kernel<<<dim3((p.t_q + attn::kQB - 1) / attn::kQB, p.n_q_heads, p.batch), attn::kThreads, smem,
-                                stream>>>(p, *mk, *mv);
+                                stream>>>(p, *mk, *mv, *mq);
     } else {
         const size_t smem = (size_t)(d + p.t_k) * 4;
         cudaError_t e = cudaFuncSetAttribute(attn::fwd_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

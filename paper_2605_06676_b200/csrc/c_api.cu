@@ -790,6 +790,55 @@ lkv_status lkv_evict_host(const lkv_cache_desc* hc, void* dev_keys, void* dev_va
     return LKV_OK;
 }
 
+// ---- Soft-TopK (training) -------------------------------------------------
+lkv_status lkv_soft_topk_fwd(const double* x, const double* noise, double noise_scale, int32_t n_seg, int32_t n,
+                             int64_t ld, const double* k, double tau, double* values, double* density,
+                             float* values_f32, double* lambda, void* ws, size_t ws_bytes, lkv_stream_t stream) {
+    if (!(tau > 0.0)) return fail(LKV_ERR_CONTRACT, "soft_topk_forward: tau must be positive");  // soft_topk.cpp:112
+    if (n < 1) return fail(LKV_ERR_CONTRACT, "soft_topk_forward: empty scores");              // :114
+    if (n_seg < 1 || ld < n) return fail(LKV_ERR_CONTRACT, "soft_topk: need n_seg >= 1 and ld >= n");
+    if (!x || !k || !values) return fail(LKV_ERR_CONTRACT, "soft_topk: null buffer");
+    if (noise && !std::isfinite(noise_scale)) return fail(LKV_ERR_CONTRACT, "soft_topk: noise_scale must be finite");
+    lkv_status st = check_ws(ws, ws_bytes, sizeof(ErrWord));
+    if (st) return st;
+    SoftTopKParams p;
+    memset(&p, 0, sizeof p);
+    p.n_seg = n_seg;
+    p.n = n;
+    p.ld = ld;
+    p.tau = tau;
+    p.noise_scale = noise_scale;
+    p.x = x;
+    p.noise = noise;
+    p.k = k;
+    p.values = values;
+    p.density = density;
+    p.values_f32 = values_f32;
+    p.lambda = lambda;
+    p.err = at<ErrWord>(ws, 0);
+    LKV_CUDA(launch_soft_topk_fwd(p, (cudaStream_t)stream), "soft topk forward");
+    return LKV_OK;
+}
+
+lkv_status lkv_soft_topk_vjp(const double* density, const double* upstream, int32_t n_seg, int32_t n, int64_t ld,
+                             double tau, double* grad_x, double* grad_k, lkv_stream_t stream) {
+    if (!(tau > 0.0)) return fail(LKV_ERR_CONTRACT, "soft_topk_vjp: tau must be positive");  // soft_topk.cpp:171
+    if (n < 1 || n_seg < 1 || ld < n) return fail(LKV_ERR_CONTRACT, "soft_topk_vjp: bad extents");
+    if (!density || !upstream || !grad_x || !grad_k) return fail(LKV_ERR_CONTRACT, "soft_topk_vjp: null buffer");
+    SoftTopKParams p;
+    memset(&p, 0, sizeof p);
+    p.n_seg = n_seg;
+    p.n = n;
+    p.ld = ld;
+    p.tau = tau;
+    p.density = const_cast<double*>(density);
+    p.upstream = upstream;
+    p.grad_x = grad_x;
+    p.grad_k = grad_k;
+    LKV_CUDA(launch_soft_topk_vjp(p, (cudaStream_t)stream), "soft topk vjp");
+    return LKV_OK;
+}
+
 // ---- masked attention (training) -------------------------------------------
 static lkv_status check_attn(const lkv_attn_desc* a) {
     if (!a) return fail(LKV_ERR_CONTRACT, "attention descriptor is null");
@@ -848,12 +897,14 @@ lkv_status lkv_masked_attention_fwd(const lkv_attn_desc* a, const void* q, const
     AttnParams p = attn_params(a, q, k, v, mask, ws);
     p.out = out;
     p.lse = lse;
-    CUtensorMap mk, mv;
+    CUtensorMap mk, mv, mq;
     if (a->dtype == LKV_BF16) {
-        const uint64_t rk = (uint64_t)a->batch * a->n_kv_heads * a->t_k;
-        if ((st = make_map_bf16(&mk, k, 128, rk, 64)) || (st = make_map_bf16(&mv, v, 128, rk, 64))) return st;
+        const uint64_t rk = (uint64_t)a->batch * a->n_kv_heads * a->t_k, rq = (uint64_t)a->batch * a->n_q_heads * a->t_q;
+        if ((st = make_map_bf16(&mk, k, 128, rk, 64)) || (st = make_map_bf16(&mv, v, 128, rk, 64)) ||
+            (st = make_map_bf16(&mq, q, 128, rq, 64)))
+            return st;
     }
-    LKV_CUDA(launch_attn_fwd(p, a->dtype, a->head_dim, &mk, &mv, (cudaStream_t)stream), "masked attention fwd");
+    LKV_CUDA(launch_attn_fwd(p, a->dtype, a->head_dim, &mk, &mv, &mq, (cudaStream_t)stream), "masked attention fwd");
     return LKV_OK;
 }
 

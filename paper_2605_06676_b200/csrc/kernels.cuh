@@ -158,13 +158,33 @@ struct AttnParams {
     ErrWord* err;
 };
 cudaError_t launch_attn_fwd(const AttnParams& p, int dtype, int d, const CUtensorMap* mk, const CUtensorMap* mv,
-                            cudaStream_t stream);
+                            const CUtensorMap* mq, cudaStream_t stream);
 cudaError_t launch_attn_bwd(const AttnParams& p, int dtype, int d, const CUtensorMap* mk, const CUtensorMap* mv,
                             const CUtensorMap* mq, const CUtensorMap* mdo, const CUtensorMap* mq32,
                             const CUtensorMap* mdo32, cudaStream_t stream);
 size_t attn_fwd_smem();
 size_t attn_dq_smem();
 size_t attn_dkv_smem();
+
+// ---- softtopk.cu (Soft-TopK forward / VJP over many segments)
+struct SoftTopKParams {
+    int32_t n_seg, n;
+    int64_t ld;            // row stride (elements) of every [n_seg][ld] array
+    double tau, noise_scale;
+    const double* x;       // scores
+    const double* noise;   // nullable: x + noise_scale * noise (training_mask's Gumbel noise)
+    const double* k;       // [n_seg] budgets
+    double* values;
+    double* density;       // nullable in the forward (the VJP's saved state)
+    float* values_f32;     // nullable: the values as an fp32 attention mask
+    double* lambda;        // nullable [n_seg]
+    const double* upstream;  // VJP
+    double* grad_x;
+    double* grad_k;        // [n_seg]
+    ErrWord* err;
+};
+cudaError_t launch_soft_topk_fwd(const SoftTopKParams& p, cudaStream_t stream);
+cudaError_t launch_soft_topk_vjp(const SoftTopKParams& p, cudaStream_t stream);
 
 // ---- model.cu (full decode step of the toy GQA model)
 enum GemvEpi { EPI_QKV = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_F32 = 3 };

@@ -76,3 +76,45 @@ def masked_attention_bwd(q, k, v, mask, out, lse, d_out, causal=True, scale=None
     if check:
         ws.status()
     return dq, dk, dv, dm
+
+
+# ---- Soft-TopK (soft_topk.hpp:60-67) -------------------------------------------------------------
+def soft_topk(x, k, tau: float = 1.0, noise=None, noise_scale: float = 1.0, f32_mask: bool = False,
+              ws: Workspace | None = None, check=True):
+    """soft_topk_forward for every row of x [n_seg, n] (fp64) with budgets k [n_seg];
+    scores are x + noise_scale * noise when noise is given (training_mask, policy.cpp:138-150).
+    -> (values fp64, density fp64, lambda [n_seg], values_f32 or None)."""
+    x = x.to(torch.float64).contiguous()
+    if x.dim() == 1:
+        x = x.view(1, -1)
+    n_seg, n = x.shape
+    kk = torch.as_tensor(k, dtype=torch.float64, device=x.device).reshape(-1).contiguous()
+    if kk.numel() == 1 and n_seg > 1:
+        kk = kk.expand(n_seg).contiguous()
+    if kk.numel() != n_seg:
+        raise ContractError("soft_topk: one budget per segment")
+    nz = noise.to(torch.float64).contiguous().view(n_seg, n) if noise is not None else None
+    vals = torch.empty_like(x)
+    dens = torch.empty_like(x)
+    lam = torch.empty(n_seg, dtype=torch.float64, device=x.device)
+    v32 = torch.empty(n_seg, n, dtype=torch.float32, device=x.device) if f32_mask else None
+    ws = ws or Workspace(256, device=x.device)
+    _check(lib().lkv_soft_topk_fwd(_ptr(x), _ptr(nz), float(noise_scale), n_seg, n, n, _ptr(kk), float(tau),
+                                   _ptr(vals), _ptr(dens), _ptr(v32), _ptr(lam), C.c_void_p(ws.ptr), ws.nbytes,
+                                   _stream()))
+    if check:
+        ws.status()
+    return vals, dens, lam, v32
+
+
+def soft_topk_vjp(density, upstream, tau: float = 1.0):
+    """soft_topk_vjp per segment -> (grad_x [n_seg, n], grad_k [n_seg])."""
+    d = density.to(torch.float64).contiguous()
+    if d.dim() == 1:
+        d = d.view(1, -1)
+    u = upstream.to(torch.float64).contiguous().view(d.shape)
+    n_seg, n = d.shape
+    gx = torch.empty_like(d)
+    gk = torch.empty(n_seg, dtype=torch.float64, device=d.device)
+    _check(lib().lkv_soft_topk_vjp(_ptr(d), _ptr(u), n_seg, n, n, float(tau), _ptr(gx), _ptr(gk), _stream()))
+    return gx, gk
