@@ -51,6 +51,26 @@ def main():
                                            "MEASURED_PEAKS.json")))["bf16_tflops"]
     except Exception:
         pass
+    # Soft-TopK over every (layer, kv head) token row of a C2-sized cache (training_mask)
+    ns, nt = 256, a.t
+    x = torch.randn(ns, nt, dtype=torch.float64, device="cuda", generator=g)
+    kb = torch.full((ns,), 0.15 * nt, dtype=torch.float64, device="cuda")
+    vals, dens, _, _ = train.soft_topk(x, kb)
+    up = torch.randn_like(x)
+    train.soft_topk_vjp(dens, up)
+    torch.cuda.synchronize()
+    e[0].record()
+    for _ in range(a.reps):
+        vals, dens, _, _ = train.soft_topk(x, kb, check=False)
+    e[1].record()
+    for _ in range(a.reps):
+        train.soft_topk_vjp(dens, up)
+    e[2].record()
+    torch.cuda.synchronize()
+    stk_f = e[0].elapsed_time(e[1]) / a.reps
+    stk_b = e[1].elapsed_time(e[2]) / a.reps
+    print(json.dumps({"what": "soft-topk fwd/vjp, 256 segments (L32 x H8) x t tokens, fp64", "t": nt,
+                      "fwd_ms": stk_f, "vjp_ms": stk_b, "rows_per_s": ns * nt / (stk_f / 1e3)}))
     print(json.dumps({"what": "masked attention train, Llama-3-8B heads (32q/8kv, d128), causal, bf16", "B": B, "T": T,
                       "fwd_ms": fwd, "bwd_ms": bwd, "fwd_tflops": 2 * 2 * tri / fwd / 1e9,
                       "bwd_tflops": 5 * 2 * tri / bwd / 1e9, "bf16_peak_tflops": peak,
