@@ -21,11 +21,10 @@
 // model.cpp:100-112).
 //
 // B200 design (bf16 inputs, fp32 accumulate, head_dim 128):
-//   * forward: CTA = 64 queries of one (batch, q head), 4 consumer warps x 16 rows + 1 TMA
-//     producer warp streaming 64-key K/V tiles (128 B swizzle) through a 3-stage mbarrier ring;
-//     S = Q K^T and O += P V on tensor cores (mma.sync m16n8k16 + ldmatrix); causal tiles past
-//     the block's last admissible key are never loaded;
-//   * backward, two kernels with no atomics (deterministic):
+//   * forward on tcgen05 (fwd_tc_kernel below): S and O accumulate in TMEM, P goes through
+//     swizzled shared memory, V is read from a transposed copy so both UMMA B operands are
+//     K-major; causal tiles past the block's last admissible key are never loaded;
+//   * backward (mma.sync m16n8k16 + ldmatrix, TMA-fed), two kernels with no atomics (deterministic):
 //     dQ:  CTA = 64 queries (Q, dO in smem), K/V tiles streamed as in the forward; recomputes S, P,
 //          dP = dO V^T, dS and accumulates dS K;
 //     dKV: CTA = 64 keys (K, V in smem for the CTA's life), 4 warps x 16 keys, streams 32-query
@@ -137,191 +136,292 @@ __device__ __forceinline__ float mask_eff(const Geo& g, const float* mask, int j
 }
 
 // =====================================================================================================
-// forward
+// forward on tcgen05 (5th-gen tensor cores, accumulators in TMEM)
+//   CTA = 128 queries (UMMA M) of one (batch, q head); 64-key tiles.
+//   warp 4: TMA (Q once; K tiles [64 keys][128 d]; V^T tiles [128 d][64 keys] from a transposed
+//           copy, so both UMMA B operands are K-major), 3-stage rings;
+//   warp 5: one thread issues S_t = Q K_t^T (M128 N64 K128) into a double-buffered TMEM S and
+//           O += P_t V_t (M128 N128 K64) into TMEM O, running S one tile ahead of P V;
+//   warps 0-3: thread = query row = TMEM lane: tcgen05.ld of the S row, admissibility, online
+//           max with lazy rescaling (O in TMEM is rescaled only when the row max grows by more
+//           than 2^8, FA4-style), exp2 x mask, P row -> shared memory in the 128-byte-swizzled
+//           K-major layout the UMMA descriptor reads; epilogue O / l from TMEM.
 // =====================================================================================================
-__global__ void __launch_bounds__(kThreads, 2)
-    fwd_bf16_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ CUtensorMap tk,
-                    const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tq) {
-    constexpr int kStageBytes = 2 * kKB * 256;
+constexpr int kTcQ = 128, kTcK = 64, kTcStages = 3, kTcThreads = 192;
+constexpr float kTcRescale = 8.f;  // log2 units
+constexpr uint32_t kTcCols = 256;  // TMEM: S0 [0,64), S1 [64,128), O [128,256)
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+        "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+        "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+    fwd_tc_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ CUtensorMap tq,
+                  const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tvt, int tk_pad) {
+    constexpr uint32_t kQBytes = kTcQ * 256, kKBytes = kTcK * 256, kVBytes = kD * kTcK * 2, kPBytes = kTcQ * kTcK * 2;
     extern __shared__ unsigned char smem_dyn[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
-    unsigned char* qs = smem + kStages * kStageBytes;  // Q tile [64][256 B]
-    uint64_t* full = reinterpret_cast<uint64_t*>(qs + kQB * 256);
-    uint64_t* empty = full + kStages;
-    uint64_t* qbar = empty + kStages;
+    unsigned char* qs = smem;
+    unsigned char* ks = qs + kQBytes;
+    unsigned char* vs = ks + kTcStages * kKBytes;
+    unsigned char* ps = vs + kTcStages * kVBytes;
+    float* mw = reinterpret_cast<float*>(ps + 2 * kPBytes);  // [4 warps][64] mask tile
+    uint64_t* bars = reinterpret_cast<uint64_t*>(mw + 4 * kTcK);
+    uint64_t* q_full = bars;
+    uint64_t* k_full = bars + 1;
+    uint64_t* k_empty = k_full + kTcStages;
+    uint64_t* v_full = k_empty + kTcStages;
+    uint64_t* v_empty = v_full + kTcStages;
+    uint64_t* s_full = v_empty + kTcStages;
+    uint64_t* s_empty = s_full + 2;
+    uint64_t* p_full = s_empty + 2;
+    uint64_t* p_empty = p_full + 2;
+    uint64_t* o_bar = p_empty + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_bar + 1);
+
     const Geo g{p.n_q_heads, p.n_kv_heads, p.n_q_heads / p.n_kv_heads, p.t_q, p.t_k, p.causal, p.pos_offset,
                 p.self_keep, p.scale * kLog2e, p.scale};
     const int b = blockIdx.z, qh = blockIdx.y, kvh = qh / g.G;
-    const int q0 = blockIdx.x * kQB;
-    const int kend = key_end(g, min(g.t_q, q0 + kQB) - 1);
-    const int ntiles = kend > 0 ? (kend + kKB - 1) / kKB : 0;
+    const int q0 = blockIdx.x * kTcQ;
+    const int kend = key_end(g, min(g.t_q, q0 + kTcQ) - 1);
+    const int ntiles = kend > 0 ? (kend + kTcK - 1) / kTcK : 0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int i = 0; i < kStages; ++i) {
-            mbar_init(&full[i], 1);
-            mbar_init(&empty[i], kConsumers);
+        mbar_init(q_full, 1);
+        for (int i = 0; i < kTcStages; ++i) {
+            mbar_init(&k_full[i], 1);
+            mbar_init(&k_empty[i], 1);
+            mbar_init(&v_full[i], 1);
+            mbar_init(&v_empty[i], 1);
         }
-        mbar_init(qbar, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&s_full[i], 1);
+            mbar_init(&s_empty[i], 4);
+            mbar_init(&p_full[i], 4);
+            mbar_init(&p_empty[i], 1);
+        }
+        mbar_init(o_bar, 1);
         fence_barrier_init();
     }
+    if (warp == 5) tmem_alloc(tmem_slot, kTcCols);
+    tc_fence_before();
     __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
     const size_t kv_row0 = ((size_t)b * g.n_kv_heads + kvh) * g.t_k;
-    if (warp == kConsumers) {
+    const size_t q_row0 = ((size_t)b * g.n_q_heads + qh) * g.t_q;
+
+    if (warp == 4) {
+        // ===================== TMA producer =====================
         if (lane == 0) {
-            tma_prefetch_desc(&tk);
-            tma_prefetch_desc(&tv);
-            const uint64_t pol = l2_policy_evict_last();  // K/V tiles are re-read by every query block
-            mbar_arrive_expect_tx(qbar, kQB * 256);
-            tma_tile<kQB>(qs, &tq, qbar, (int)(((size_t)b * g.n_q_heads + qh) * g.t_q + q0), pol);
+            const uint64_t pol = l2_policy_evict_last();
+            mbar_arrive_expect_tx(q_full, kQBytes);
+            tma_tile<kTcQ>(qs, &tq, q_full, (int)(q_row0 + q0), pol);
+            const int vt_row0 = (b * g.n_kv_heads + kvh) * kD;
             for (int t = 0; t < ntiles; ++t) {
-                const int st = t % kStages;
-                if (t >= kStages) mbar_wait(&empty[st], ((t / kStages) - 1) & 1);
-                mbar_arrive_expect_tx(&full[st], kStageBytes);
-                unsigned char* dst = smem + st * kStageBytes;
-                tma_tile<kKB>(dst, &tk, &full[st], (int)(kv_row0 + t * kKB), pol);
-                tma_tile<kKB>(dst + kKB * 256, &tv, &full[st], (int)(kv_row0 + t * kKB), pol);
+                const int st = t % kTcStages;
+                if (t >= kTcStages) mbar_wait(&k_empty[st], ((t / kTcStages) - 1) & 1);
+                mbar_arrive_expect_tx(&k_full[st], kKBytes);
+                tma_tile<kTcK>(ks + st * kKBytes, &tk, &k_full[st], (int)(kv_row0 + t * kTcK), pol);
+                if (t >= kTcStages) mbar_wait(&v_empty[st], ((t / kTcStages) - 1) & 1);
+                mbar_arrive_expect_tx(&v_full[st], kVBytes);
+                tma_load_2d(vs + st * kVBytes, &tvt, &v_full[st], t * kTcK, vt_row0, pol);
             }
         }
-        return;
-    }
-    const int gq = lane >> 2, cq = (lane & 3) * 2;
-    const int r_lo = q0 + warp * 16 + gq, r_hi = r_lo + 8;  // this thread's two query rows
-    const float* mask = p.mask ? p.mask + ((size_t)b * g.n_kv_heads + kvh) * g.t_k : nullptr;
-    const bool mask_vec = (reinterpret_cast<uintptr_t>(mask) & 7) == 0;
-    const uint32_t qsb = smem_u32(qs);
-    mbar_wait(qbar, 0);
-    float o[16][4];
+    } else if (warp == 5) {
+        // ===================== MMA issuer =====================
+        if (lane == 0) {
+            constexpr uint32_t idesc_s = umma_idesc_bf16(kTcQ, kTcK), idesc_o = umma_idesc_bf16(kTcQ, kD);
+            const uint32_t qa = smem_u32(qs), ka = smem_u32(ks), va = smem_u32(vs), pa = smem_u32(ps);
+            mbar_wait(q_full, 0);
+            auto issue_s = [&](int t) {
+                const int st = t % kTcStages, bb = t & 1;
+                mbar_wait(&k_full[st], (t / kTcStages) & 1);
+                if (t >= 2) mbar_wait(&s_empty[bb], ((t >> 1) - 1) & 1);
+                tc_fence_after();
 #pragma unroll
-    for (int n = 0; n < 16; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-    float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;
-    for (int t = 0; t < ntiles; ++t) {
-        const int st = t % kStages;
-        mbar_wait(&full[st], (t / kStages) & 1);
-        const uint32_t kb = smem_u32(smem + st * kStageBytes), vb = kb + kKB * 256;
-        const int j0 = t * kKB;
-        float s[8][4];
-#pragma unroll
-        for (int n = 0; n < 8; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-            uint32_t qa[4];
-            frag_a<kQB>(qsb, warp * 16, kk, lane, qa);
-#pragma unroll
-            for (int np = 0; np < 4; ++np) {
-                uint32_t bf[4];
-                frag_bn<kKB>(kb, np * 16, kk, lane, bf);
-                mma(s[2 * np], qa, bf[0], bf[1]);
-                mma(s[2 * np + 1], qa, bf[2], bf[3]);
-            }
-        }
-        // interior tiles (every key admissible for all 16 rows of this warp) skip the per-element
-        // admissibility tests; only the causal diagonal and the ragged ends take the slow path
-        const int wr0 = q0 + warp * 16;
-        const bool interior = j0 + kKB <= g.t_k && wr0 + 16 <= g.t_q && (!g.causal || j0 + kKB - 1 <= g.pos_offset + wr0) &&
-                              !(g.self_keep && j0 + kKB - 1 >= g.pos_offset + wr0);
-        // this thread's 16 mask values (the same key columns for both rows)
-        float mx_lo = -INFINITY, mx_hi = -INFINITY;
-        if (interior) {
-#pragma unroll
-            for (int n = 0; n < 8; ++n)
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    s[n][e] *= g.c;
-                    s[n][2 + e] *= g.c;
-                    mx_lo = fmaxf(mx_lo, s[n][e]);
-                    mx_hi = fmaxf(mx_hi, s[n][2 + e]);
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint64_t ad = umma_desc_sw128(qa + (kk >> 2) * (kTcQ * 128) + (kk & 3) * 32);
+                    const uint64_t bd = umma_desc_sw128(ka + st * kKBytes + (kk >> 2) * (kTcK * 128) + (kk & 3) * 32);
+                    umma_bf16(tmem + bb * kTcK, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
                 }
-        } else {
+                umma_commit(&s_full[bb]);
+                umma_commit(&k_empty[st]);
+            };
+            if (ntiles > 0) issue_s(0);
+            for (int t = 0; t < ntiles; ++t) {
+                if (t + 1 < ntiles) issue_s(t + 1);
+                const int st = t % kTcStages, bb = t & 1;
+                mbar_wait(&p_full[bb], (t >> 1) & 1);
+                mbar_wait(&v_full[st], (t / kTcStages) & 1);
+                tc_fence_after();
 #pragma unroll
-            for (int n = 0; n < 8; ++n)
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int j = j0 + n * 8 + cq + e;
-                    s[n][e] = admissible(g, j, r_lo) ? s[n][e] * g.c : -INFINITY;
-                    s[n][2 + e] = admissible(g, j, r_hi) ? s[n][2 + e] * g.c : -INFINITY;
-                    mx_lo = fmaxf(mx_lo, s[n][e]);
-                    mx_hi = fmaxf(mx_hi, s[n][2 + e]);
+                for (int kk = 0; kk < 4; ++kk) {
+                    const uint64_t ad = umma_desc_sw128(pa + bb * kPBytes + kk * 32);
+                    const uint64_t bd = umma_desc_sw128(va + st * kVBytes + kk * 32);
+                    umma_bf16(tmem + 2 * kTcK, ad, bd, idesc_o, (t > 0 || kk > 0) ? 1u : 0u);
                 }
-        }
-        mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 1));
-        mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 2));
-        mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 1));
-        mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 2));
-        const float mn_lo = fmaxf(m_lo, mx_lo), mn_hi = fmaxf(m_hi, mx_hi);
-        const float a_lo = mn_lo == -INFINITY ? 1.f : fast_exp2(m_lo - mn_lo);
-        const float a_hi = mn_hi == -INFINITY ? 1.f : fast_exp2(m_hi - mn_hi);
-        m_lo = mn_lo;
-        m_hi = mn_hi;
-        // a row with no admissible key yet has mn = -inf: exp2(-inf - -inf) would be NaN
-        const float sub_lo = mn_lo == -INFINITY ? 0.f : mn_lo, sub_hi = mn_hi == -INFINITY ? 0.f : mn_hi;
-        float sl = 0.f, sh = 0.f;
-#pragma unroll
-        for (int n = 0; n < 8; ++n) {
-            const float2 m2 = load_mask2(mask, mask_vec, j0 + n * 8 + cq, g.t_k);
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                float ml = e ? m2.y : m2.x, mh = ml;
-                if (!interior && g.self_keep) {
-                    const int j = j0 + n * 8 + cq + e;
-                    if (j == g.pos_offset + r_lo) ml = 1.f;
-                    if (j == g.pos_offset + r_hi) mh = 1.f;
-                }
-                s[n][e] = fast_exp2(s[n][e] - sub_lo) * ml;  // exp2(-inf) = 0 for inadmissible keys
-                s[n][2 + e] = fast_exp2(s[n][2 + e] - sub_hi) * mh;
-                sl += s[n][e];
-                sh += s[n][2 + e];
+                umma_commit(o_bar);
+                umma_commit(&p_empty[bb]);
+                umma_commit(&v_empty[st]);
             }
         }
-        l_lo = l_lo * a_lo + sl;
-        l_hi = l_hi * a_hi + sh;
-#pragma unroll
-        for (int n = 0; n < 16; ++n) {
-            o[n][0] *= a_lo;
-            o[n][1] *= a_lo;
-            o[n][2] *= a_hi;
-            o[n][3] *= a_hi;
+    } else {
+        // ===================== softmax / epilogue (thread = query row = TMEM lane) =====================
+        const int rl = warp * 32 + lane, r = q0 + rl;
+        const uint32_t lane_addr = tmem + (uint32_t(warp * 32) << 16);
+        const float* mask = p.mask ? p.mask + kv_row0 : nullptr;
+        float* mwarp = mw + warp * kTcK;
+        float m_run = -INFINITY, l_run = 0.f;
+        // the mask values of tile t + 1 are fetched while tile t is processed (the global load
+        // latency was on the softmax critical path)
+        float mnext0 = 0.f, mnext1 = 0.f;
+        if (mask) {
+            mnext0 = lane < g.t_k ? __ldg(mask + lane) : 0.f;
+            mnext1 = lane + 32 < g.t_k ? __ldg(mask + lane + 32) : 0.f;
         }
-        // O += P V  (P: 16 rows x 64 keys = 4 k16 steps)
+        for (int t = 0; t < ntiles; ++t) {
+            const int bb = t & 1, j0 = t * kTcK;
+            if (mask) {
+                mwarp[lane] = mnext0;
+                mwarp[lane + 32] = mnext1;
+                __syncwarp();
+                const int jn = j0 + kTcK;
+                mnext0 = jn + lane < g.t_k ? __ldg(mask + jn + lane) : 0.f;
+                mnext1 = jn + lane + 32 < g.t_k ? __ldg(mask + jn + lane + 32) : 0.f;
+            }
+            mbar_wait(&s_full[bb], (t >> 1) & 1);
+            tc_fence_after();
+            uint32_t sr[64];
+            tmem_ld_32x32b_x32(lane_addr + bb * kTcK, *reinterpret_cast<uint32_t(*)[32]>(sr));
+            tmem_ld_32x32b_x32(lane_addr + bb * kTcK + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[bb]);
+            const int wr0 = q0 + warp * 32;
+            const bool interior = j0 + kTcK <= g.t_k && wr0 + 32 <= g.t_q &&
+                                  (!g.causal || j0 + kTcK - 1 <= g.pos_offset + wr0) &&
+                                  !(g.self_keep && j0 + kTcK - 1 >= g.pos_offset + wr0);
+            float x[64];
+            float mt = -INFINITY;
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-            uint32_t pa[4] = {pack2(s[2 * kk][0], s[2 * kk][1]), pack2(s[2 * kk][2], s[2 * kk][3]),
-                              pack2(s[2 * kk + 1][0], s[2 * kk + 1][1]), pack2(s[2 * kk + 1][2], s[2 * kk + 1][3])};
+            for (int i = 0; i < 64; ++i) {
+                x[i] = __uint_as_float(sr[i]) * g.c;
+                if (!interior && !admissible(g, j0 + i, r)) x[i] = -INFINITY;
+                mt = fmaxf(mt, x[i]);
+            }
+            const float m_new = fmaxf(m_run, mt);
+            const bool need = m_new != -INFINITY && (m_run == -INFINITY || m_new > m_run + kTcRescale);
+            float alpha = 1.f;
+            if (need) {
+                alpha = m_run == -INFINITY ? 0.f : fast_exp2(m_run - m_new);
+                m_run = m_new;
+            }
+            // P buffer bb is free once P V of tile t-2 has retired (also orders the o_bar parity
+            // waits below: at most P V of tile t-1 can still be in flight)
+            if (t >= 2) mbar_wait(&p_empty[bb], ((t >> 1) - 1) & 1);
+            if (__any_sync(0xffffffffu, need) && t > 0) {
+                // rescale this warp's O rows once P V of the previous tile has landed
+                mbar_wait(o_bar, (t - 1) & 1);
+                tc_fence_after();
 #pragma unroll
-            for (int n2 = 0; n2 < 8; ++n2) {
-                uint32_t bf[4];
-                frag_bk<kKB>(vb, kk * 16, n2, lane, bf);
-                mma(o[2 * n2], pa, bf[0], bf[1]);
-                mma(o[2 * n2 + 1], pa, bf[2], bf[3]);
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t orr[32];
+                    tmem_ld_32x32b_x32(lane_addr + 2 * kTcK + c * 32, orr);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) orr[i] = __float_as_uint(__uint_as_float(orr[i]) * alpha);
+                    tmem_st32(lane_addr + 2 * kTcK + c * 32, orr);
+                }
+                tmem_st_wait();
+            }
+            l_run *= alpha;
+            // P row -> shared memory (bf16, 128-byte swizzle, K-major: 8 chunks of 8 keys)
+            unsigned char* prow = ps + bb * kPBytes + rl * 128;
+            const float sub = m_run == -INFINITY ? 0.f : m_run;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                uint32_t w4[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    float pv[2];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int i = c * 8 + e * 2 + h, j = j0 + i;
+                        float mj = mask ? mwarp[i] : 1.f;
+                        if (!interior && g.self_keep && j == g.pos_offset + r) mj = 1.f;
+                        pv[h] = fast_exp2(x[i] - sub) * mj;  // x = -inf -> 0
+                        l_run += pv[h];
+                    }
+                    w4[e] = pack2(pv[0], pv[1]);
+                }
+                *reinterpret_cast<uint4*>(prow + ((c ^ (rl & 7)) << 4)) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+            }
+            fence_proxy_async_smem();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_full[bb]);
+        }
+        // ---- epilogue: O / l from TMEM
+        if (ntiles > 1) mbar_wait(o_bar, (ntiles - 2) & 1);  // phases in order: never two behind
+        if (ntiles > 0) {
+            mbar_wait(o_bar, (ntiles - 1) & 1);
+            tc_fence_after();
+        }
+        const bool ok = l_run > 0.f;
+        if (r < g.t_q && !ok) latch_error(p.err, LKV_ERR_DEGENERATE_MASK, r);  // attention.cpp:82-84
+        const float inv = ok ? 1.f / l_run : 0.f;
+        __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(p.out) + (q_row0 + r) * kD;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            uint32_t orr[32];
+            tmem_ld_32x32b_x32(lane_addr + 2 * kTcK + c * 32, orr);
+            tmem_ld_wait();
+            if (r < g.t_q && ok) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    uint32_t w4[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        w4[e] = pack2(__uint_as_float(orr[q * 8 + 2 * e]) * inv, __uint_as_float(orr[q * 8 + 2 * e + 1]) * inv);
+                    *reinterpret_cast<uint4*>(orow + c * 32 + q * 8) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                }
             }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[st]);
+        if (r < g.t_q && ok) p.lse[q_row0 + r] = m_run + log2f(l_run);
     }
-#pragma unroll
-    for (int x = 1; x <= 2; x <<= 1) {
-        l_lo += __shfl_xor_sync(0xffffffffu, l_lo, x);
-        l_hi += __shfl_xor_sync(0xffffffffu, l_hi, x);
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 5) {
+        tc_fence_after();
+        tmem_dealloc(tmem, kTcCols);
     }
-    const size_t row_base = ((size_t)b * g.n_q_heads + qh) * g.t_q;
-    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int r = h ? r_hi : r_lo;
-        if (r >= g.t_q) continue;
-        const float l = h ? l_hi : l_lo, m = h ? m_hi : m_lo;
-        // attention.cpp:82-84: the masked mass z = l / raw must stay above 1e-300; every row
-        // admits key 0, so raw >= 1 after the max shift and the test is l > 0 in fp32
-        if (!(l > 0.f)) {
-            if ((lane & 3) == 0) latch_error(p.err, LKV_ERR_DEGENERATE_MASK, r);
-            continue;
-        }
-        const float inv = 1.f / l;
-        __nv_bfloat16* orow = out + (row_base + r) * kD;
-#pragma unroll
-        for (int n = 0; n < 16; ++n)
-            *reinterpret_cast<__nv_bfloat162*>(orow + n * 8 + cq) =
-                __floats2bfloat162_rn(o[n][2 * h] * inv, o[n][2 * h + 1] * inv);
-        if ((lane & 3) == 0) p.lse[row_base + r] = m + log2f(l);
+}
+
+// V [rows = (b, kvh, key)][128] -> V^T [(b, kvh, d)][tk_pad] (keys past t_k zero), 32x32 tiles
+__global__ void transpose_v_kernel(const __nv_bfloat16* __restrict__ v, __nv_bfloat16* __restrict__ vt, int t_k,
+                                   int tk_pad) {
+    __shared__ __nv_bfloat16 tile[32][33];
+    const int bh = blockIdx.z, k0 = blockIdx.x * 32, d0 = blockIdx.y * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+    for (int i = ty; i < 32; i += 8) {
+        const int key = k0 + i;
+        tile[i][tx] = key < t_k ? v[((size_t)bh * t_k + key) * kD + d0 + tx] : __float2bfloat16(0.f);
+    }
+    __syncthreads();
+    for (int i = ty; i < 32; i += 8) {
+        const int d = d0 + i, key = k0 + tx;
+        if (key < tk_pad) vt[((size_t)bh * kD + d) * tk_pad + key] = tile[tx][i];
     }
 }
 
@@ -835,13 +935,18 @@ __global__ void __launch_bounds__(kSimt) dkv_f32_kernel(const __grid_constant__ 
 }  // namespace attn
 
 // ---- host launchers ----------------------------------------------------------------------------------
-size_t attn_fwd_smem() { return 1024 + attn::kStages * (2 * attn::kKB * 256) + attn::kQB * 256 + 2 * attn::kStages * 8 + 8; }
 size_t attn_dq_smem() { return 1024 + attn::kStages * (2 * attn::kKB * 256) + 2 * attn::kQB * 256 + 2 * attn::kStages * 8 + 8; }
 size_t attn_dkv_smem() {
     return 1024 + attn::kStages * (2 * attn::kQT * 256) + 2 * attn::kKB * 256 + 2 * attn::kStages * 8 + 8;
 }
 
-cudaError_t launch_attn_fwd(const AttnParams& p, int dtype, int d, const CUtensorMap* mk, const CUtensorMap* mv,
+int attn_tk_pad(int t_k) { return (t_k + attn::kTcK - 1) / attn::kTcK * attn::kTcK; }
+size_t attn_fwd_tc_smem() {
+    return 1024 + attn::kTcQ * 256 + attn::kTcStages * (attn::kTcK * 256 + attn::kD * attn::kTcK * 2) +
+           2 * attn::kTcQ * attn::kTcK * 2 + 4 * attn::kTcK * 4 + 32 * 8 + 16;
+}
+
+cudaError_t launch_attn_fwd(const AttnParams& p, int dtype, int d, const CUtensorMap* mk, const CUtensorMap* mvt,
                             const CUtensorMap* mq, cudaStream_t stream) {
     if (p.mask) {
         const int64_t n = (int64_t)p.batch * p.n_kv_heads * p.t_k;
@@ -849,11 +954,15 @@ cudaError_t launch_attn_fwd(const AttnParams& p, int dtype, int d, const CUtenso
         note_launches(1);
     }
     if (dtype == LKV_BF16) {
-        const size_t smem = attn_fwd_smem();
-        cudaError_t e = cudaFuncSetAttribute(attn::fwd_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const int tk_pad = attn_tk_pad(p.t_k);
+        attn::transpose_v_kernel<<<dim3(tk_pad / 32, attn::kD / 32, p.batch * p.n_kv_heads), dim3(32, 8), 0, stream>>>(
+            static_cast<const __nv_bfloat16*>(p.v), static_cast<__nv_bfloat16*>(p.vt), p.t_k, tk_pad);
+        const size_t smem = attn_fwd_tc_smem();
+        cudaError_t e = cudaFuncSetAttribute(attn::fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        attn::fwd_bf16_kernel<<<dim3((p.t_q + attn::kQB - 1) / attn::kQB, p.n_q_heads, p.batch), attn::kThreads, smem,
-                                stream>>>(p, *mk, *mv, *mq);
+        attn::fwd_tc_kernel<<<dim3((p.t_q + attn::kTcQ - 1) / attn::kTcQ, p.n_q_heads, p.batch), attn::kTcThreads, smem,
+                              stream>>>(p, *mq, *mk, *mvt, tk_pad);
+        note_launches(1);
     } else {
         const size_t smem = (size_t)(d + p.t_k) * 4;
         cudaError_t e = cudaFuncSetAttribute(attn::fwd_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -882,9 +882,15 @@ static AttnParams attn_params(const lkv_attn_desc* a, const void* q, const void*
     return p;
 }
 
+// workspace: [error latch | D = rowsum(dO * O) (backward) | V^T (bf16 forward)]
+static size_t attn_vt_offset(const lkv_attn_desc* a) {
+    return 256 + align_up(sizeof(float) * (size_t)a->batch * a->n_q_heads * a->t_q);
+}
 size_t lkv_attn_workspace_bytes(const lkv_attn_desc* a) {
     if (check_attn(a)) return 0;
-    return 256 + align_up(sizeof(float) * (size_t)a->batch * a->n_q_heads * a->t_q);
+    size_t n = attn_vt_offset(a);
+    if (a->dtype == LKV_BF16) n += align_up((size_t)a->batch * a->n_kv_heads * 128 * attn_tk_pad(a->t_k) * 2);
+    return n;
 }
 
 lkv_status lkv_masked_attention_fwd(const lkv_attn_desc* a, const void* q, const void* k, const void* v,
@@ -897,14 +903,15 @@ lkv_status lkv_masked_attention_fwd(const lkv_attn_desc* a, const void* q, const
     AttnParams p = attn_params(a, q, k, v, mask, ws);
     p.out = out;
     p.lse = lse;
-    CUtensorMap mk, mv, mq;
+    CUtensorMap mk, mvt, mq;
     if (a->dtype == LKV_BF16) {
         const uint64_t rk = (uint64_t)a->batch * a->n_kv_heads * a->t_k, rq = (uint64_t)a->batch * a->n_q_heads * a->t_q;
-        if ((st = make_map_bf16(&mk, k, 128, rk, 64)) || (st = make_map_bf16(&mv, v, 128, rk, 64)) ||
-            (st = make_map_bf16(&mq, q, 128, rq, 64)))
+        p.vt = at<void>(ws, attn_vt_offset(a));
+        if ((st = make_map_bf16(&mk, k, 128, rk, 64)) || (st = make_map_bf16(&mq, q, 128, rq, 128)) ||
+            (st = make_map_bf16(&mvt, p.vt, (uint64_t)attn_tk_pad(a->t_k), (uint64_t)a->batch * a->n_kv_heads * 128, 128)))
             return st;
     }
-    LKV_CUDA(launch_attn_fwd(p, a->dtype, a->head_dim, &mk, &mv, &mq, (cudaStream_t)stream), "masked attention fwd");
+    LKV_CUDA(launch_attn_fwd(p, a->dtype, a->head_dim, &mk, &mvt, &mq, (cudaStream_t)stream), "masked attention fwd");
     return LKV_OK;
 }
 
