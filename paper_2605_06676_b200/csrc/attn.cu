@@ -147,9 +147,10 @@ __device__ __forceinline__ float mask_eff(const Geo& g, const float* mask, int j
 //           than 2^8, FA4-style), exp2 x mask, P row -> shared memory in the 128-byte-swizzled
 //           K-major layout the UMMA descriptor reads; epilogue O / l from TMEM.
 // =====================================================================================================
-constexpr int kTcQ = 128, kTcK = 64, kTcStages = 3, kTcThreads = 192;
+constexpr int kTcQ = 128, kTcK = 64, kTcStages = 2, kTcWG = 2;
+constexpr int kTcThreads = (kTcWG * 4 + 2) * 32;  // 2 softmax warpgroups + TMA warp + MMA warp
 constexpr float kTcRescale = 8.f;  // log2 units
-constexpr uint32_t kTcCols = 256;  // TMEM: S0 [0,64), S1 [64,128), O [128,256)
+constexpr uint32_t kTcCols = 512;  // TMEM: S[wg][2] at wg*128 + b*64, O[wg] at 256 + wg*128
 
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
     asm volatile(
@@ -164,36 +165,47 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// tiles of 64 keys that query rows [r0, r0 + 128) need (0 when no row is valid)
+__device__ __forceinline__ int tc_tiles(const Geo& g, int r0) {
+    if (r0 >= g.t_q) return 0;
+    const int kend = key_end(g, min(g.t_q, r0 + kTcQ) - 1);
+    return kend > 0 ? (kend + kTcK - 1) / kTcK : 0;
+}
+
+// CTA = two 128-query tiles (one softmax warpgroup each) sharing every K/V tile: while one
+// warpgroup runs its softmax the tensor core works on the other's S / P V (FA4-style ping-pong).
 __global__ void __launch_bounds__(kTcThreads, 1)
     fwd_tc_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ CUtensorMap tq,
                   const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tvt, int tk_pad) {
     constexpr uint32_t kQBytes = kTcQ * 256, kKBytes = kTcK * 256, kVBytes = kD * kTcK * 2, kPBytes = kTcQ * kTcK * 2;
     extern __shared__ unsigned char smem_dyn[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
-    unsigned char* qs = smem;
-    unsigned char* ks = qs + kQBytes;
-    unsigned char* vs = ks + kTcStages * kKBytes;
-    unsigned char* ps = vs + kTcStages * kVBytes;
-    float* mw = reinterpret_cast<float*>(ps + 2 * kPBytes);  // [4 warps][64] mask tile
-    uint64_t* bars = reinterpret_cast<uint64_t*>(mw + 4 * kTcK);
+    unsigned char* qs = smem;                                 // [wg] Q tiles
+    unsigned char* ks = qs + kTcWG * kQBytes;                 // [stage] K tiles
+    unsigned char* vs = ks + kTcStages * kKBytes;             // [stage] V^T tiles
+    unsigned char* ps = vs + kTcStages * kVBytes;             // [wg][2] P tiles
+    float* mw = reinterpret_cast<float*>(ps + kTcWG * 2 * kPBytes);  // [8 warps][64] mask tile
+    uint64_t* bars = reinterpret_cast<uint64_t*>(mw + kTcWG * 4 * kTcK);
     uint64_t* q_full = bars;
     uint64_t* k_full = bars + 1;
     uint64_t* k_empty = k_full + kTcStages;
     uint64_t* v_full = k_empty + kTcStages;
     uint64_t* v_empty = v_full + kTcStages;
-    uint64_t* s_full = v_empty + kTcStages;
-    uint64_t* s_empty = s_full + 2;
-    uint64_t* p_full = s_empty + 2;
-    uint64_t* p_empty = p_full + 2;
-    uint64_t* o_bar = p_empty + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_bar + 1);
+    uint64_t* s_full = v_empty + kTcStages;  // [wg][2]
+    uint64_t* s_empty = s_full + 2 * kTcWG;
+    uint64_t* p_full = s_empty + 2 * kTcWG;
+    uint64_t* p_empty = p_full + 2 * kTcWG;
+    uint64_t* o_bar = p_empty + 2 * kTcWG;   // [wg]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_bar + kTcWG);
 
     const Geo g{p.n_q_heads, p.n_kv_heads, p.n_q_heads / p.n_kv_heads, p.t_q, p.t_k, p.causal, p.pos_offset,
                 p.self_keep, p.scale * kLog2e, p.scale};
     const int b = blockIdx.z, qh = blockIdx.y, kvh = qh / g.G;
-    const int q0 = blockIdx.x * kTcQ;
-    const int kend = key_end(g, min(g.t_q, q0 + kTcQ) - 1);
-    const int ntiles = kend > 0 ? (kend + kTcK - 1) / kTcK : 0;
+    const int q0 = blockIdx.x * (kTcWG * kTcQ);
+    int nt[kTcWG];
+#pragma unroll
+    for (int w = 0; w < kTcWG; ++w) nt[w] = tc_tiles(g, q0 + w * kTcQ);
+    const int n_all = max(nt[0], nt[1]);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         mbar_init(q_full, 1);
@@ -203,16 +215,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             mbar_init(&v_full[i], 1);
             mbar_init(&v_empty[i], 1);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < 2 * kTcWG; ++i) {
             mbar_init(&s_full[i], 1);
             mbar_init(&s_empty[i], 4);
             mbar_init(&p_full[i], 4);
             mbar_init(&p_empty[i], 1);
         }
-        mbar_init(o_bar, 1);
+        for (int w = 0; w < kTcWG; ++w) mbar_init(&o_bar[w], 1);
         fence_barrier_init();
     }
-    if (warp == 5) tmem_alloc(tmem_slot, kTcCols);
+    if (warp == kTcWG * 4 + 1) tmem_alloc(tmem_slot, kTcCols);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -220,14 +232,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const size_t kv_row0 = ((size_t)b * g.n_kv_heads + kvh) * g.t_k;
     const size_t q_row0 = ((size_t)b * g.n_q_heads + qh) * g.t_q;
 
-    if (warp == 4) {
+    if (warp == kTcWG * 4) {
         // ===================== TMA producer =====================
         if (lane == 0) {
             const uint64_t pol = l2_policy_evict_last();
-            mbar_arrive_expect_tx(q_full, kQBytes);
-            tma_tile<kTcQ>(qs, &tq, q_full, (int)(q_row0 + q0), pol);
+            mbar_arrive_expect_tx(q_full, kTcWG * kQBytes);
+#pragma unroll
+            for (int w = 0; w < kTcWG; ++w) tma_tile<kTcQ>(qs + w * kQBytes, &tq, q_full, (int)(q_row0 + q0 + w * kTcQ), pol);
             const int vt_row0 = (b * g.n_kv_heads + kvh) * kD;
-            for (int t = 0; t < ntiles; ++t) {
+            for (int t = 0; t < n_all; ++t) {
                 const int st = t % kTcStages;
                 if (t >= kTcStages) mbar_wait(&k_empty[st], ((t / kTcStages) - 1) & 1);
                 mbar_arrive_expect_tx(&k_full[st], kKBytes);
@@ -237,8 +250,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 tma_load_2d(vs + st * kVBytes, &tvt, &v_full[st], t * kTcK, vt_row0, pol);
             }
         }
-    } else if (warp == 5) {
-        // ===================== MMA issuer =====================
+    } else if (warp == kTcWG * 4 + 1) {
+        // ===================== MMA issuer: S of tile t+1 (both warpgroups), then P V of tile t
         if (lane == 0) {
             constexpr uint32_t idesc_s = umma_idesc_bf16(kTcQ, kTcK), idesc_o = umma_idesc_bf16(kTcQ, kD);
             const uint32_t qa = smem_u32(qs), ka = smem_u32(ks), va = smem_u32(vs), pa = smem_u32(ps);
@@ -246,50 +259,66 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             auto issue_s = [&](int t) {
                 const int st = t % kTcStages, bb = t & 1;
                 mbar_wait(&k_full[st], (t / kTcStages) & 1);
-                if (t >= 2) mbar_wait(&s_empty[bb], ((t >> 1) - 1) & 1);
-                tc_fence_after();
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint64_t ad = umma_desc_sw128(qa + (kk >> 2) * (kTcQ * 128) + (kk & 3) * 32);
-                    const uint64_t bd = umma_desc_sw128(ka + st * kKBytes + (kk >> 2) * (kTcK * 128) + (kk & 3) * 32);
-                    umma_bf16(tmem + bb * kTcK, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
+                for (int w = 0; w < kTcWG; ++w) {
+                    if (t >= nt[w]) continue;
+                    if (t >= 2) mbar_wait(&s_empty[w * 2 + bb], ((t >> 1) - 1) & 1);
+                    tc_fence_after();
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) {
+                        const uint64_t ad = umma_desc_sw128(qa + w * kQBytes + (kk >> 2) * (kTcQ * 128) + (kk & 3) * 32);
+                        const uint64_t bd = umma_desc_sw128(ka + st * kKBytes + (kk >> 2) * (kTcK * 128) + (kk & 3) * 32);
+                        umma_bf16(tmem + w * 128 + bb * kTcK, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
+                    }
+                    umma_commit(&s_full[w * 2 + bb]);
                 }
-                umma_commit(&s_full[bb]);
                 umma_commit(&k_empty[st]);
             };
-            if (ntiles > 0) issue_s(0);
-            for (int t = 0; t < ntiles; ++t) {
-                if (t + 1 < ntiles) issue_s(t + 1);
+            if (n_all > 0) issue_s(0);
+            for (int t = 0; t < n_all; ++t) {
+                if (t + 1 < n_all) issue_s(t + 1);
                 const int st = t % kTcStages, bb = t & 1;
-                mbar_wait(&p_full[bb], (t >> 1) & 1);
                 mbar_wait(&v_full[st], (t / kTcStages) & 1);
-                tc_fence_after();
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {
-                    const uint64_t ad = umma_desc_sw128(pa + bb * kPBytes + kk * 32);
-                    const uint64_t bd = umma_desc_sw128(va + st * kVBytes + kk * 32);
-                    umma_bf16(tmem + 2 * kTcK, ad, bd, idesc_o, (t > 0 || kk > 0) ? 1u : 0u);
+                for (int w = 0; w < kTcWG; ++w) {
+                    if (t >= nt[w]) continue;
+                    mbar_wait(&p_full[w * 2 + bb], (t >> 1) & 1);
+                    tc_fence_after();
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const uint64_t ad = umma_desc_sw128(pa + (w * 2 + bb) * kPBytes + kk * 32);
+                        const uint64_t bd = umma_desc_sw128(va + st * kVBytes + kk * 32);
+                        umma_bf16(tmem + 256 + w * 128, ad, bd, idesc_o, (t > 0 || kk > 0) ? 1u : 0u);
+                    }
+                    umma_commit(&o_bar[w]);
+                    umma_commit(&p_empty[w * 2 + bb]);
                 }
-                umma_commit(o_bar);
-                umma_commit(&p_empty[bb]);
                 umma_commit(&v_empty[st]);
             }
         }
     } else {
-        // ===================== softmax / epilogue (thread = query row = TMEM lane) =====================
-        const int rl = warp * 32 + lane, r = q0 + rl;
-        const uint32_t lane_addr = tmem + (uint32_t(warp * 32) << 16);
+        // ===================== softmax / epilogue: warpgroup wg, thread = query row = TMEM lane
+        const int wg = warp >> 2, w4 = warp & 3;
+        const int ntw = nt[wg];
+        const int rl = w4 * 32 + lane, r = q0 + wg * kTcQ + rl;
+        const uint32_t lane_addr = tmem + (uint32_t(w4 * 32) << 16);
+        const uint32_t s_col = wg * 128, o_col = 256 + wg * 128;
         const float* mask = p.mask ? p.mask + kv_row0 : nullptr;
         float* mwarp = mw + warp * kTcK;
+        uint64_t* my_s_full = s_full + wg * 2;
+        uint64_t* my_s_empty = s_empty + wg * 2;
+        uint64_t* my_p_full = p_full + wg * 2;
+        uint64_t* my_p_empty = p_empty + wg * 2;
+        unsigned char* my_ps = ps + wg * 2 * kPBytes;
         float m_run = -INFINITY, l_run = 0.f;
-        // the mask values of tile t + 1 are fetched while tile t is processed (the global load
-        // latency was on the softmax critical path)
+        // the mask values of tile t + 1 are fetched while tile t is processed
         float mnext0 = 0.f, mnext1 = 0.f;
         if (mask) {
             mnext0 = lane < g.t_k ? __ldg(mask + lane) : 0.f;
             mnext1 = lane + 32 < g.t_k ? __ldg(mask + lane + 32) : 0.f;
         }
-        for (int t = 0; t < ntiles; ++t) {
+        const int wr0 = q0 + wg * kTcQ + w4 * 32;
+        for (int t = 0; t < ntw; ++t) {
             const int bb = t & 1, j0 = t * kTcK;
             if (mask) {
                 mwarp[lane] = mnext0;
@@ -299,16 +328,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 mnext0 = jn + lane < g.t_k ? __ldg(mask + jn + lane) : 0.f;
                 mnext1 = jn + lane + 32 < g.t_k ? __ldg(mask + jn + lane + 32) : 0.f;
             }
-            mbar_wait(&s_full[bb], (t >> 1) & 1);
+            mbar_wait(&my_s_full[bb], (t >> 1) & 1);
             tc_fence_after();
             uint32_t sr[64];
-            tmem_ld_32x32b_x32(lane_addr + bb * kTcK, *reinterpret_cast<uint32_t(*)[32]>(sr));
-            tmem_ld_32x32b_x32(lane_addr + bb * kTcK + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
+            tmem_ld_32x32b_x32(lane_addr + s_col + bb * kTcK, *reinterpret_cast<uint32_t(*)[32]>(sr));
+            tmem_ld_32x32b_x32(lane_addr + s_col + bb * kTcK + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
             tmem_ld_wait();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&s_empty[bb]);
-            const int wr0 = q0 + warp * 32;
+            if (lane == 0) mbar_arrive(&my_s_empty[bb]);
             const bool interior = j0 + kTcK <= g.t_k && wr0 + 32 <= g.t_q &&
                                   (!g.causal || j0 + kTcK - 1 <= g.pos_offset + wr0) &&
                                   !(g.self_keep && j0 + kTcK - 1 >= g.pos_offset + wr0);
@@ -327,31 +355,30 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 alpha = m_run == -INFINITY ? 0.f : fast_exp2(m_run - m_new);
                 m_run = m_new;
             }
-            // P buffer bb is free once P V of tile t-2 has retired (also orders the o_bar parity
-            // waits below: at most P V of tile t-1 can still be in flight)
-            if (t >= 2) mbar_wait(&p_empty[bb], ((t >> 1) - 1) & 1);
+            // P buffer bb is free once P V of tile t-2 has retired (this also bounds the o_bar
+            // phases in flight to one, so the parity waits below are exact)
+            if (t >= 2) mbar_wait(&my_p_empty[bb], ((t >> 1) - 1) & 1);
             if (__any_sync(0xffffffffu, need) && t > 0) {
-                // rescale this warp's O rows once P V of the previous tile has landed
-                mbar_wait(o_bar, (t - 1) & 1);
+                mbar_wait(&o_bar[wg], (t - 1) & 1);  // rescale O once P V of tile t-1 has landed
                 tc_fence_after();
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     uint32_t orr[32];
-                    tmem_ld_32x32b_x32(lane_addr + 2 * kTcK + c * 32, orr);
+                    tmem_ld_32x32b_x32(lane_addr + o_col + c * 32, orr);
                     tmem_ld_wait();
 #pragma unroll
                     for (int i = 0; i < 32; ++i) orr[i] = __float_as_uint(__uint_as_float(orr[i]) * alpha);
-                    tmem_st32(lane_addr + 2 * kTcK + c * 32, orr);
+                    tmem_st32(lane_addr + o_col + c * 32, orr);
                 }
                 tmem_st_wait();
             }
             l_run *= alpha;
             // P row -> shared memory (bf16, 128-byte swizzle, K-major: 8 chunks of 8 keys)
-            unsigned char* prow = ps + bb * kPBytes + rl * 128;
+            unsigned char* prow = my_ps + bb * kPBytes + rl * 128;
             const float sub = m_run == -INFINITY ? 0.f : m_run;
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
-                uint32_t w4[4];
+                uint32_t w4v[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     float pv[2];
@@ -363,38 +390,40 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                         pv[h] = fast_exp2(x[i] - sub) * mj;  // x = -inf -> 0
                         l_run += pv[h];
                     }
-                    w4[e] = pack2(pv[0], pv[1]);
+                    w4v[e] = pack2(pv[0], pv[1]);
                 }
-                *reinterpret_cast<uint4*>(prow + ((c ^ (rl & 7)) << 4)) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                *reinterpret_cast<uint4*>(prow + ((c ^ (rl & 7)) << 4)) = make_uint4(w4v[0], w4v[1], w4v[2], w4v[3]);
             }
             fence_proxy_async_smem();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&p_full[bb]);
+            if (lane == 0) mbar_arrive(&my_p_full[bb]);
         }
         // ---- epilogue: O / l from TMEM
-        if (ntiles > 1) mbar_wait(o_bar, (ntiles - 2) & 1);  // phases in order: never two behind
-        if (ntiles > 0) {
-            mbar_wait(o_bar, (ntiles - 1) & 1);
+        if (ntw > 1) mbar_wait(&o_bar[wg], (ntw - 2) & 1);  // phases in order: never two behind
+        if (ntw > 0) {
+            mbar_wait(&o_bar[wg], (ntw - 1) & 1);
             tc_fence_after();
         }
         const bool ok = l_run > 0.f;
         if (r < g.t_q && !ok) latch_error(p.err, LKV_ERR_DEGENERATE_MASK, r);  // attention.cpp:82-84
         const float inv = ok ? 1.f / l_run : 0.f;
         __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(p.out) + (q_row0 + r) * kD;
+        if (ntw > 0) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            uint32_t orr[32];
-            tmem_ld_32x32b_x32(lane_addr + 2 * kTcK + c * 32, orr);
-            tmem_ld_wait();
-            if (r < g.t_q && ok) {
+            for (int c = 0; c < 4; ++c) {
+                uint32_t orr[32];
+                tmem_ld_32x32b_x32(lane_addr + o_col + c * 32, orr);
+                tmem_ld_wait();
+                if (r < g.t_q && ok) {
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    uint32_t w4[4];
+                    for (int q = 0; q < 4; ++q) {
+                        uint32_t w4v[4];
 #pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        w4[e] = pack2(__uint_as_float(orr[q * 8 + 2 * e]) * inv, __uint_as_float(orr[q * 8 + 2 * e + 1]) * inv);
-                    *reinterpret_cast<uint4*>(orow + c * 32 + q * 8) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                        for (int e = 0; e < 4; ++e)
+                            w4v[e] = pack2(__uint_as_float(orr[q * 8 + 2 * e]) * inv, __uint_as_float(orr[q * 8 + 2 * e + 1]) * inv);
+                        *reinterpret_cast<uint4*>(orow + c * 32 + q * 8) = make_uint4(w4v[0], w4v[1], w4v[2], w4v[3]);
+                    }
                 }
             }
         }
@@ -402,7 +431,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 5) {
+    if (warp == kTcWG * 4 + 1) {
         tc_fence_after();
         tmem_dealloc(tmem, kTcCols);
     }
@@ -942,8 +971,8 @@ size_t attn_dkv_smem() {
 
 int attn_tk_pad(int t_k) { return (t_k + attn::kTcK - 1) / attn::kTcK * attn::kTcK; }
 size_t attn_fwd_tc_smem() {
-    return 1024 + attn::kTcQ * 256 + attn::kTcStages * (attn::kTcK * 256 + attn::kD * attn::kTcK * 2) +
-           2 * attn::kTcQ * attn::kTcK * 2 + 4 * attn::kTcK * 4 + 32 * 8 + 16;
+    return 1024 + attn::kTcWG * attn::kTcQ * 256 + attn::kTcStages * (attn::kTcK * 256 + attn::kD * attn::kTcK * 2) +
+           attn::kTcWG * 2 * attn::kTcQ * attn::kTcK * 2 + attn::kTcWG * 4 * attn::kTcK * 4 + 64 * 8 + 16;
 }
 
 cudaError_t launch_attn_fwd(const AttnParams& p, int dtype, int d, const CUtensorMap* mk, const CUtensorMap* mvt,
@@ -960,8 +989,9 @@ cudaError_t launch_attn_fwd(const AttnParams& p, int dtype, int d, const CUtenso
         const size_t smem = attn_fwd_tc_smem();
         cudaError_t e = cudaFuncSetAttribute(attn::fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        attn::fwd_tc_kernel<<<dim3((p.t_q + attn::kTcQ - 1) / attn::kTcQ, p.n_q_heads, p.batch), attn::kTcThreads, smem,
-                              stream>>>(p, *mq, *mk, *mvt, tk_pad);
+        constexpr int rows_per_cta = attn::kTcWG * attn::kTcQ;
+        attn::fwd_tc_kernel<<<dim3((p.t_q + rows_per_cta - 1) / rows_per_cta, p.n_q_heads, p.batch), attn::kTcThreads,
+                              smem, stream>>>(p, *mq, *mk, *mvt, tk_pad);
         note_launches(1);
     } else {
         const size_t smem = (size_t)(d + p.t_k) * 4;
