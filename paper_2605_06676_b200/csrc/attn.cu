@@ -437,6 +437,446 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
 }
 
+// =====================================================================================================
+// backward on tcgen05: dKV (key-major) and dQ (query-major); every UMMA operand K-major, the
+// transposed operands (Q^T, dO^T, K^T) read from transposed copies made by transpose_kernel.
+// =====================================================================================================
+constexpr int kBwK = 128;   // dKV: keys per CTA (UMMA M)
+constexpr int kBwQ = 64;    // dKV: queries per streamed tile (UMMA N of S^T, K of dV / dK)
+constexpr int kBwThreads = 192;  // warps 0-3 compute (thread = row = TMEM lane), 4 TMA, 5 MMA
+
+__global__ void __launch_bounds__(kBwThreads, 1)
+    dkv_tc_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ CUtensorMap tk128,
+                  const __grid_constant__ CUtensorMap tv128, const __grid_constant__ CUtensorMap tq64,
+                  const __grid_constant__ CUtensorMap tdo64, const __grid_constant__ CUtensorMap tqt,
+                  const __grid_constant__ CUtensorMap tdot) {
+    constexpr uint32_t kKB128 = kBwK * 256, kT64 = kBwQ * 256, kStage = 4 * kT64, kPT = kBwK * kBwQ * 2;
+    // this kernel uses all but ~1 KB of the 227 KB per-block shared memory, so there is no room for
+    // a manual 1024-byte round-up: the dynamic window starts after the 1 KB reserved block (aligned)
+    extern __shared__ __align__(1024) unsigned char smem_dyn[];
+    unsigned char* smem = smem_dyn;
+    if ((smem_u32(smem) & 1023) != 0) {
+        if (threadIdx.x == 0) latch_error(p.err, LKV_ERR_UNSUPPORTED, 1024);
+        return;
+    }
+    unsigned char* ks = smem;
+    unsigned char* vs = ks + kKB128;
+    unsigned char* stg = vs + kKB128;          // [2] x {Q, dO, Q^T, dO^T}
+    unsigned char* pts = stg + 2 * kStage;     // P^T [128 keys][64 q]
+    unsigned char* dss = pts + kPT;            // dS^T
+    float* cw = reinterpret_cast<float*>(dss + kPT);  // [4 warps][lse 64 | D 64]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(cw + 4 * 2 * kBwQ);
+    uint64_t* kv_full = bars;
+    uint64_t* st_full = bars + 1;    // [2]
+    uint64_t* st_empty = bars + 3;   // [2]
+    uint64_t* s_full = bars + 5;     // [2]
+    uint64_t* s_empty = bars + 7;    // [2]
+    uint64_t* pt_full = bars + 9;
+    uint64_t* pt_empty = bars + 10;
+    uint64_t* acc_done = bars + 11;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+
+    const Geo g{p.n_q_heads, p.n_kv_heads, p.n_q_heads / p.n_kv_heads, p.t_q, p.t_k, p.causal, p.pos_offset,
+                p.self_keep, p.scale * kLog2e, p.scale};
+    const int b = blockIdx.z, kvh = blockIdx.y;
+    const int k0 = blockIdx.x * kBwK;
+    const int rstart = g.causal ? max(0, k0 - g.pos_offset) : 0;
+    const int qt0 = rstart / kBwQ;
+    const int nq = rstart < g.t_q ? (g.t_q + kBwQ - 1) / kBwQ - qt0 : 0;
+    const int ntiles = nq * g.G;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        mbar_init(kv_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&st_full[i], 1);
+            mbar_init(&st_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+            mbar_init(&s_empty[i], 4);
+        }
+        mbar_init(pt_full, 4);
+        mbar_init(pt_empty, 1);
+        mbar_init(acc_done, 1);
+        fence_barrier_init();
+    }
+    if (warp == 5) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;  // S^T[2] 0/64, dP^T[2] 128/192, dV 256, dK 384
+    const size_t kv_row0 = ((size_t)b * g.n_kv_heads + kvh) * g.t_k;
+    auto head_of = [&](int t) { return (b * g.n_q_heads + kvh * g.G + t / nq); };  // flat q head
+    auto qtile_of = [&](int t) { return qt0 + t % nq; };
+
+    if (warp == 4) {
+        if (lane == 0 && ntiles > 0) {
+            const uint64_t pol = l2_policy_evict_last();
+            mbar_arrive_expect_tx(kv_full, 2 * kKB128);
+            tma_tile<kBwK>(ks, &tk128, kv_full, (int)(kv_row0 + k0), pol);
+            tma_tile<kBwK>(vs, &tv128, kv_full, (int)(kv_row0 + k0), pol);
+            for (int t = 0; t < ntiles; ++t) {
+                const int st = t & 1;
+                if (t >= 2) mbar_wait(&st_empty[st], ((t >> 1) - 1) & 1);
+                mbar_arrive_expect_tx(&st_full[st], kStage);
+                unsigned char* d = stg + st * kStage;
+                const int hq = head_of(t), r0 = qtile_of(t) * kBwQ;
+                const int qrow = (int)((size_t)hq * g.t_q + r0);
+                tma_tile<kBwQ>(d, &tq64, &st_full[st], qrow, pol);
+                tma_tile<kBwQ>(d + kT64, &tdo64, &st_full[st], qrow, pol);
+                tma_load_2d(d + 2 * kT64, &tqt, &st_full[st], r0, hq * kD, pol);
+                tma_load_2d(d + 3 * kT64, &tdot, &st_full[st], r0, hq * kD, pol);
+            }
+        }
+    } else if (warp == 5) {
+        if (lane == 0 && ntiles > 0) {
+            constexpr uint32_t id_s = umma_idesc_bf16(kBwK, kBwQ), id_o = umma_idesc_bf16(kBwK, kD);
+            const uint32_t ka = smem_u32(ks), va = smem_u32(vs), sa = smem_u32(stg), pa = smem_u32(pts),
+                           da = smem_u32(dss);
+            mbar_wait(kv_full, 0);
+            auto issue_s = [&](int t) {
+                const int st = t & 1, bb = t & 1;
+                mbar_wait(&st_full[st], (t >> 1) & 1);
+                if (t >= 2) mbar_wait(&s_empty[bb], ((t >> 1) - 1) & 1);
+                tc_fence_after();
+                const uint32_t qb = sa + st * kStage, ub = qb + kT64;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t ao = (kk >> 2) * (kBwK * 128) + (kk & 3) * 32, bo = (kk >> 2) * (kBwQ * 128) + (kk & 3) * 32;
+                    umma_bf16(tmem + bb * 64, umma_desc_sw128(ka + ao), umma_desc_sw128(qb + bo), id_s, kk > 0);
+                    umma_bf16(tmem + 128 + bb * 64, umma_desc_sw128(va + ao), umma_desc_sw128(ub + bo), id_s, kk > 0);
+                }
+                umma_commit(&s_full[bb]);
+            };
+            issue_s(0);
+            for (int t = 0; t < ntiles; ++t) {
+                if (t + 1 < ntiles) issue_s(t + 1);
+                const int st = t & 1;
+                mbar_wait(pt_full, t & 1);
+                tc_fence_after();
+                const uint32_t qtb = sa + st * kStage + 2 * kT64, utb = qtb + kT64;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    umma_bf16(tmem + 256, umma_desc_sw128(pa + kk * 32), umma_desc_sw128(utb + kk * 32), id_o,
+                              (t > 0 || kk > 0) ? 1u : 0u);
+                    umma_bf16(tmem + 384, umma_desc_sw128(da + kk * 32), umma_desc_sw128(qtb + kk * 32), id_o,
+                              (t > 0 || kk > 0) ? 1u : 0u);
+                }
+                umma_commit(pt_empty);
+                umma_commit(&st_empty[st]);
+            }
+            umma_commit(acc_done);
+        }
+    } else {
+        // ===================== compute: thread = key row
+        const int kr = warp * 32 + lane, j = k0 + kr;
+        const uint32_t la = tmem + (uint32_t(warp * 32) << 16);
+        const float mkey = !p.mask ? 1.f : j < g.t_k ? __ldg(p.mask + kv_row0 + j) : 0.f;
+        float* wl = cw + warp * 2 * kBwQ;  // lse[64], D[64]
+        float dm = 0.f;
+        float nl0 = 0.f, nl1 = 0.f, nd0 = 0.f, nd1 = 0.f;
+        auto fetch = [&](int t) {
+            if (t >= ntiles) return;
+            const size_t rb = (size_t)head_of(t) * g.t_q;
+            const int r0 = qtile_of(t) * kBwQ;
+            nl0 = r0 + lane < g.t_q ? __ldg(p.lse + rb + r0 + lane) : 0.f;
+            nl1 = r0 + lane + 32 < g.t_q ? __ldg(p.lse + rb + r0 + lane + 32) : 0.f;
+            nd0 = r0 + lane < g.t_q ? __ldg(p.dsum + rb + r0 + lane) : 0.f;
+            nd1 = r0 + lane + 32 < g.t_q ? __ldg(p.dsum + rb + r0 + lane + 32) : 0.f;
+        };
+        fetch(0);
+        const int jw0 = k0 + warp * 32;
+        for (int t = 0; t < ntiles; ++t) {
+            const int bb = t & 1, r0 = qtile_of(t) * kBwQ;
+            wl[lane] = nl0;
+            wl[lane + 32] = nl1;
+            wl[kBwQ + lane] = nd0;
+            wl[kBwQ + lane + 32] = nd1;
+            __syncwarp();
+            fetch(t + 1);
+            mbar_wait(&s_full[bb], (t >> 1) & 1);
+            tc_fence_after();
+            uint32_t sv[64], dv[64];
+            tmem_ld_32x32b_x32(la + bb * 64, *reinterpret_cast<uint32_t(*)[32]>(sv));
+            tmem_ld_32x32b_x32(la + bb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
+            tmem_ld_32x32b_x32(la + 128 + bb * 64, *reinterpret_cast<uint32_t(*)[32]>(dv));
+            tmem_ld_32x32b_x32(la + 128 + bb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(dv + 32));
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[bb]);
+            const bool interior = jw0 + 32 <= g.t_k && r0 + kBwQ <= g.t_q && (!g.causal || jw0 + 31 <= g.pos_offset + r0) &&
+                                  !(g.self_keep && jw0 + 31 >= g.pos_offset + r0);
+            if (t >= 1) mbar_wait(pt_empty, (t - 1) & 1);  // dV / dK of tile t-1 done with P^T, dS^T
+            unsigned char* prow = pts + kr * 128;
+            unsigned char* drow = dss + kr * 128;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                uint32_t pw[4], dw[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    float pv[2], dsv[2];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int i = c * 8 + e * 2 + h, r = r0 + i;
+                        float pm = fast_exp2(__uint_as_float(sv[i]) * g.c - wl[i]);
+                        bool self = false;
+                        if (!interior) {
+                            if (!admissible(g, j, r)) pm = 0.f;
+                            self = g.self_keep && j == g.pos_offset + r;
+                        }
+                        const float dpv = __uint_as_float(dv[i]) - wl[kBwQ + i];
+                        const float pj = self ? pm : pm * mkey;
+                        if (!self) dm = fmaf(pm, dpv, dm);
+                        pv[h] = pj;
+                        dsv[h] = pj * dpv;
+                    }
+                    pw[e] = pack2(pv[0], pv[1]);
+                    dw[e] = pack2(dsv[0], dsv[1]);
+                }
+                const int off = (c ^ (kr & 7)) << 4;
+                *reinterpret_cast<uint4*>(prow + off) = make_uint4(pw[0], pw[1], pw[2], pw[3]);
+                *reinterpret_cast<uint4*>(drow + off) = make_uint4(dw[0], dw[1], dw[2], dw[3]);
+            }
+            fence_proxy_async_smem();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(pt_full);
+        }
+        // ---- epilogue: dV, dK (x scale) rows from TMEM, dmask
+        if (ntiles > 0) {
+            mbar_wait(acc_done, 0);
+            tc_fence_after();
+        }
+#pragma unroll
+        for (int which = 0; which < 2; ++which) {
+            float* dst = (which ? p.dk : p.dv) + (kv_row0 + j) * kD;
+            const float f = which ? g.scale : 1.f;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint32_t rr[32];
+                if (ntiles > 0) {
+                    tmem_ld_32x32b_x32(la + 256 + which * 128 + c * 32, rr);
+                    tmem_ld_wait();
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) rr[i] = 0u;
+                }
+                if (j < g.t_k) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        *reinterpret_cast<float4*>(dst + c * 32 + q * 4) =
+                            make_float4(__uint_as_float(rr[q * 4]) * f, __uint_as_float(rr[q * 4 + 1]) * f,
+                                        __uint_as_float(rr[q * 4 + 2]) * f, __uint_as_float(rr[q * 4 + 3]) * f);
+                }
+            }
+        }
+        if (p.dmask && j < g.t_k) p.dmask[kv_row0 + j] = dm;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 5) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+__global__ void __launch_bounds__(kBwThreads, 1)
+    dq_tc_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ CUtensorMap tq128,
+                 const __grid_constant__ CUtensorMap tdo128, const __grid_constant__ CUtensorMap tk64,
+                 const __grid_constant__ CUtensorMap tv64, const __grid_constant__ CUtensorMap tkt) {
+    constexpr uint32_t kQ128 = kTcQ * 256, kT64 = kTcK * 256, kStage = 3 * kT64, kDS = kTcQ * kTcK * 2;
+    extern __shared__ unsigned char smem_dyn[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+    unsigned char* qs = smem;
+    unsigned char* us = qs + kQ128;
+    unsigned char* stg = us + kQ128;            // [2] x {K, V, K^T}
+    unsigned char* dss = stg + 2 * kStage;      // dS [2][128 q][64 keys]
+    float* mw = reinterpret_cast<float*>(dss + 2 * kDS);  // [4 warps][64]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(mw + 4 * kTcK);
+    uint64_t* q_full = bars;
+    uint64_t* st_full = bars + 1;
+    uint64_t* st_empty = bars + 3;
+    uint64_t* s_full = bars + 5;
+    uint64_t* s_empty = bars + 7;
+    uint64_t* ds_full = bars + 9;
+    uint64_t* ds_empty = bars + 11;
+    uint64_t* acc_done = bars + 13;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+
+    const Geo g{p.n_q_heads, p.n_kv_heads, p.n_q_heads / p.n_kv_heads, p.t_q, p.t_k, p.causal, p.pos_offset,
+                p.self_keep, p.scale * kLog2e, p.scale};
+    const int b = blockIdx.z, qh = blockIdx.y, kvh = qh / g.G;
+    const int q0 = blockIdx.x * kTcQ;
+    const int ntiles = tc_tiles(g, q0);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        mbar_init(q_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&st_full[i], 1);
+            mbar_init(&st_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+            mbar_init(&s_empty[i], 4);
+            mbar_init(&ds_full[i], 4);
+            mbar_init(&ds_empty[i], 1);
+        }
+        mbar_init(acc_done, 1);
+        fence_barrier_init();
+    }
+    if (warp == 5) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;  // S[2] 0/64, dP[2] 128/192, dQ 256
+    const size_t kv_row0 = ((size_t)b * g.n_kv_heads + kvh) * g.t_k;
+    const size_t q_row0 = ((size_t)b * g.n_q_heads + qh) * g.t_q;
+
+    if (warp == 4) {
+        if (lane == 0 && ntiles > 0) {
+            const uint64_t pol = l2_policy_evict_last();
+            mbar_arrive_expect_tx(q_full, 2 * kQ128);
+            tma_tile<kTcQ>(qs, &tq128, q_full, (int)(q_row0 + q0), pol);
+            tma_tile<kTcQ>(us, &tdo128, q_full, (int)(q_row0 + q0), pol);
+            const int kt_row0 = (b * g.n_kv_heads + kvh) * kD;
+            for (int t = 0; t < ntiles; ++t) {
+                const int st = t & 1;
+                if (t >= 2) mbar_wait(&st_empty[st], ((t >> 1) - 1) & 1);
+                mbar_arrive_expect_tx(&st_full[st], kStage);
+                unsigned char* d = stg + st * kStage;
+                tma_tile<kTcK>(d, &tk64, &st_full[st], (int)(kv_row0 + t * kTcK), pol);
+                tma_tile<kTcK>(d + kT64, &tv64, &st_full[st], (int)(kv_row0 + t * kTcK), pol);
+                tma_load_2d(d + 2 * kT64, &tkt, &st_full[st], t * kTcK, kt_row0, pol);
+            }
+        }
+    } else if (warp == 5) {
+        if (lane == 0 && ntiles > 0) {
+            constexpr uint32_t id_s = umma_idesc_bf16(kTcQ, kTcK), id_o = umma_idesc_bf16(kTcQ, kD);
+            const uint32_t qa = smem_u32(qs), ua = smem_u32(us), sa = smem_u32(stg), da = smem_u32(dss);
+            mbar_wait(q_full, 0);
+            auto issue_s = [&](int t) {
+                const int st = t & 1, bb = t & 1;
+                mbar_wait(&st_full[st], (t >> 1) & 1);
+                if (t >= 2) mbar_wait(&s_empty[bb], ((t >> 1) - 1) & 1);
+                tc_fence_after();
+                const uint32_t kb = sa + st * kStage, vb = kb + kT64;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t ao = (kk >> 2) * (kTcQ * 128) + (kk & 3) * 32, bo = (kk >> 2) * (kTcK * 128) + (kk & 3) * 32;
+                    umma_bf16(tmem + bb * 64, umma_desc_sw128(qa + ao), umma_desc_sw128(kb + bo), id_s, kk > 0);
+                    umma_bf16(tmem + 128 + bb * 64, umma_desc_sw128(ua + ao), umma_desc_sw128(vb + bo), id_s, kk > 0);
+                }
+                umma_commit(&s_full[bb]);
+            };
+            issue_s(0);
+            for (int t = 0; t < ntiles; ++t) {
+                if (t + 1 < ntiles) issue_s(t + 1);
+                const int st = t & 1, bb = t & 1;
+                mbar_wait(&ds_full[bb], (t >> 1) & 1);
+                tc_fence_after();
+                const uint32_t ktb = sa + st * kStage + 2 * kT64;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                    umma_bf16(tmem + 256, umma_desc_sw128(da + bb * kDS + kk * 32), umma_desc_sw128(ktb + kk * 32), id_o,
+                              (t > 0 || kk > 0) ? 1u : 0u);
+                umma_commit(&ds_empty[bb]);
+                umma_commit(&st_empty[st]);
+            }
+            umma_commit(acc_done);
+        }
+    } else {
+        // ===================== compute: thread = query row
+        const int rl = warp * 32 + lane, r = q0 + rl;
+        const uint32_t la = tmem + (uint32_t(warp * 32) << 16);
+        const float lse = r < g.t_q ? p.lse[q_row0 + r] : 0.f, dd = r < g.t_q ? p.dsum[q_row0 + r] : 0.f;
+        const float* mask = p.mask ? p.mask + kv_row0 : nullptr;
+        float* mwarp = mw + warp * kTcK;
+        float mn0 = 0.f, mn1 = 0.f;
+        if (mask) {
+            mn0 = lane < g.t_k ? __ldg(mask + lane) : 0.f;
+            mn1 = lane + 32 < g.t_k ? __ldg(mask + lane + 32) : 0.f;
+        }
+        const int wr0 = q0 + warp * 32;
+        for (int t = 0; t < ntiles; ++t) {
+            const int bb = t & 1, j0 = t * kTcK;
+            if (mask) {
+                mwarp[lane] = mn0;
+                mwarp[lane + 32] = mn1;
+                __syncwarp();
+                const int jn = j0 + kTcK;
+                mn0 = jn + lane < g.t_k ? __ldg(mask + jn + lane) : 0.f;
+                mn1 = jn + lane + 32 < g.t_k ? __ldg(mask + jn + lane + 32) : 0.f;
+            }
+            mbar_wait(&s_full[bb], (t >> 1) & 1);
+            tc_fence_after();
+            uint32_t sv[64], dv[64];
+            tmem_ld_32x32b_x32(la + bb * 64, *reinterpret_cast<uint32_t(*)[32]>(sv));
+            tmem_ld_32x32b_x32(la + bb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
+            tmem_ld_32x32b_x32(la + 128 + bb * 64, *reinterpret_cast<uint32_t(*)[32]>(dv));
+            tmem_ld_32x32b_x32(la + 128 + bb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(dv + 32));
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[bb]);
+            const bool interior = j0 + kTcK <= g.t_k && wr0 + 32 <= g.t_q && (!g.causal || j0 + kTcK - 1 <= g.pos_offset + wr0) &&
+                                  !(g.self_keep && j0 + kTcK - 1 >= g.pos_offset + wr0);
+            if (t >= 2) mbar_wait(&ds_empty[bb], ((t >> 1) - 1) & 1);
+            unsigned char* drow = dss + bb * kDS + rl * 128;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                uint32_t dw[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    float dsv[2];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int i = c * 8 + e * 2 + h, jj = j0 + i;
+                        float mj = mask ? mwarp[i] : 1.f;
+                        float pm = fast_exp2(__uint_as_float(sv[i]) * g.c - lse);
+                        if (!interior) {
+                            if (!admissible(g, jj, r)) pm = 0.f;
+                            if (g.self_keep && jj == g.pos_offset + r) mj = 1.f;
+                        }
+                        dsv[h] = pm * mj * (__uint_as_float(dv[i]) - dd);
+                    }
+                    dw[e] = pack2(dsv[0], dsv[1]);
+                }
+                *reinterpret_cast<uint4*>(drow + ((c ^ (rl & 7)) << 4)) = make_uint4(dw[0], dw[1], dw[2], dw[3]);
+            }
+            fence_proxy_async_smem();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ds_full[bb]);
+        }
+        if (ntiles > 0) {
+            mbar_wait(acc_done, 0);
+            tc_fence_after();
+        }
+        float* drow = p.dq + (q_row0 + r) * kD;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            uint32_t rr[32];
+            if (ntiles > 0) {
+                tmem_ld_32x32b_x32(la + 256 + c * 32, rr);
+                tmem_ld_wait();
+            } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) rr[i] = 0u;
+            }
+            if (r < g.t_q) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    *reinterpret_cast<float4*>(drow + c * 32 + q * 4) =
+                        make_float4(__uint_as_float(rr[q * 4]) * g.scale, __uint_as_float(rr[q * 4 + 1]) * g.scale,
+                                    __uint_as_float(rr[q * 4 + 2]) * g.scale, __uint_as_float(rr[q * 4 + 3]) * g.scale);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 5) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
 // V [rows = (b, kvh, key)][128] -> V^T [(b, kvh, d)][tk_pad] (keys past t_k zero), 32x32 tiles
 __global__ void transpose_v_kernel(const __nv_bfloat16* __restrict__ v, __nv_bfloat16* __restrict__ vt, int t_k,
                                    int tk_pad) {
@@ -1003,23 +1443,41 @@ cudaError_t launch_attn_fwd(const AttnParams& p, int dtype, int d, const CUtenso
     return cudaGetLastError();
 }
 
-cudaError_t launch_attn_bwd(const AttnParams& p, int dtype, int d, const CUtensorMap* mk, const CUtensorMap* mv,
-                            const CUtensorMap* mq, const CUtensorMap* mdo, const CUtensorMap* mq32,
-                            const CUtensorMap* mdo32, cudaStream_t stream) {
+size_t attn_dq_tc_smem() {
+    return 1024 + 2 * attn::kTcQ * 256 + 2 * 3 * attn::kTcK * 256 + 2 * attn::kTcQ * attn::kTcK * 2 + 4 * attn::kTcK * 4 +
+           16 * 8;
+}
+size_t attn_dkv_tc_smem() {  // no alignment slack (see dkv_tc_kernel)
+    return 2 * attn::kBwK * 256 + 2 * 4 * attn::kBwQ * 256 + 2 * attn::kBwK * attn::kBwQ * 2 + 4 * 2 * attn::kBwQ * 4 +
+           16 * 8;
+}
+
+// m: dQ maps {Q(128 rows), dO(128), K(64), V(64), K^T(128 x 64)}, dKV maps {K(128), V(128), Q(64), dO(64),
+//    Q^T(128 x 64), dO^T(128 x 64)}
+cudaError_t launch_attn_bwd(const AttnParams& p, int dtype, int d, const CUtensorMap* m, cudaStream_t stream) {
     const int64_t rows = (int64_t)p.batch * p.n_q_heads * p.t_q;
     cudaError_t e;
     if (dtype == LKV_BF16) {
         attn::bwd_prep_kernel<__nv_bfloat16><<<(unsigned)((rows + 3) / 4), 128, 0, stream>>>(
             static_cast<const __nv_bfloat16*>(p.out), static_cast<const __nv_bfloat16*>(p.dout), p.dsum, rows, d);
-        const size_t s1 = attn_dq_smem(), s2 = attn_dkv_smem();
-        if ((e = cudaFuncSetAttribute(attn::dq_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1)))
+        // transposed operand copies: K^T, Q^T, dO^T ([(b, head, d)][pad])
+        const int tk_pad = attn_tk_pad(p.t_k), tq_pad = attn_tk_pad(p.t_q);
+        attn::transpose_v_kernel<<<dim3(tk_pad / 32, attn::kD / 32, p.batch * p.n_kv_heads), dim3(32, 8), 0, stream>>>(
+            static_cast<const __nv_bfloat16*>(p.k), static_cast<__nv_bfloat16*>(p.kt), p.t_k, tk_pad);
+        attn::transpose_v_kernel<<<dim3(tq_pad / 32, attn::kD / 32, p.batch * p.n_q_heads), dim3(32, 8), 0, stream>>>(
+            static_cast<const __nv_bfloat16*>(p.q), static_cast<__nv_bfloat16*>(p.qt), p.t_q, tq_pad);
+        attn::transpose_v_kernel<<<dim3(tq_pad / 32, attn::kD / 32, p.batch * p.n_q_heads), dim3(32, 8), 0, stream>>>(
+            static_cast<const __nv_bfloat16*>(p.dout), static_cast<__nv_bfloat16*>(p.dot), p.t_q, tq_pad);
+        const size_t s1 = attn_dq_tc_smem(), s2 = attn_dkv_tc_smem();
+        if ((e = cudaFuncSetAttribute(attn::dq_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1)))
             return e;
-        if ((e = cudaFuncSetAttribute(attn::dkv_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2)))
+        if ((e = cudaFuncSetAttribute(attn::dkv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2)))
             return e;
-        attn::dq_bf16_kernel<<<dim3((p.t_q + attn::kQB - 1) / attn::kQB, p.n_q_heads, p.batch), attn::kThreads, s1,
-                               stream>>>(p, *mk, *mv, *mq, *mdo);
-        attn::dkv_bf16_kernel<<<dim3((p.t_k + attn::kKB - 1) / attn::kKB, p.n_kv_heads, p.batch), attn::kThreads, s2,
-                                stream>>>(p, *mk, *mv, *mq32, *mdo32);
+        attn::dq_tc_kernel<<<dim3((p.t_q + attn::kTcQ - 1) / attn::kTcQ, p.n_q_heads, p.batch), attn::kBwThreads, s1,
+                             stream>>>(p, m[0], m[1], m[2], m[3], m[4]);
+        attn::dkv_tc_kernel<<<dim3((p.t_k + attn::kBwK - 1) / attn::kBwK, p.n_kv_heads, p.batch), attn::kBwThreads, s2,
+                              stream>>>(p, m[5], m[6], m[7], m[8], m[9], m[10]);
+        note_launches(3);
     } else {
         attn::bwd_prep_kernel<float><<<(unsigned)((rows + 3) / 4), 128, 0, stream>>>(
             static_cast<const float*>(p.out), static_cast<const float*>(p.dout), p.dsum, rows, d);
