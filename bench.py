@@ -390,12 +390,13 @@ def cpu_baseline(cache, scorers, ev, n_threads=1, n_heads=8):
     t_per_head = np.full(nh, cache.seq_lens[0], np.int32)
     t0 = time.perf_counter()
     O.evict_heads(K, V, t_per_head, scorers.input, w1, b1, w2, scorers.activation, head_scorer, b, offs,
-                  n_threads=n_threads)
+                  n_threads=n_threads, fast=True)
     dt = time.perf_counter() - t0
     rows = int(t_per_head.sum())
     return {"value": rows / dt, "unit": UNIT, "cores": n_threads, "kind": "port",
             "sample": f"{nh} heads x {cache.seq_lens[0]} rows of the same C2 workload (layer 0..), fp64 score + "
-                      f"stable-sort top-k + gather, {dt:.2f} s",
+                      f"stable-sort top-k + gather, {dt:.2f} s; port built -O3 -march=x86-64-v3 (the reference's "
+                      f"Release + -march=native recipe)",
             "seconds": dt}
 
 
@@ -429,7 +430,7 @@ def run_reference(args, rank, world):
 
     def one():
         O.allocate_budgets(logits, cfg.ratio)
-        O.evict_heads(K, V, tph, 1, w1, b1, w2, O.GELU_ERF, hs, b, offs, n_threads=ncores)
+        O.evict_heads(K, V, tph, 1, w1, b1, w2, O.GELU_ERF, hs, b, offs, n_threads=ncores, fast=True)
 
     for _ in range(max(args.warmup, 0)):
         one()
@@ -448,7 +449,9 @@ def run_reference(args, rank, world):
         "config": {"workload": f"C2 sample: {nh} heads x {T} rows (one head per host thread)",
                    "parallelism": f"{ncores} host threads"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": ncores, "kind": "port",
-                         "sample": f"{nh} heads x {T} rows per step: fp64 LKV-H solve + scorer + stable-sort top-k + gather"},
+                         "sample": f"{nh} heads x {T} rows per step: fp64 LKV-H solve + scorer + stable-sort top-k + "
+                                   f"gather; port of proj/src built -O3 -march=x86-64-v3 (the reference's Release + "
+                                   f"-march=native recipe; its Eigen GEMM is replaced by a row-blocked loop)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

@@ -27,6 +27,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liblkv_oracle.so")
 _REF_PATH = os.path.join(_HERE, "_ref", "liblkv_ref.so")
+# the same source built like the reference builds itself (-O3, AVX2/FMA): the CPU-baseline timer only
+_FAST_PATH = os.path.join(_HERE, "liblkv_oracle_fast.so")
 
 OK, CONTRACT, NUMERIC, BUDGET, OVERFLOW_GUARD, DEGENERATE_MASK = range(6)
 F32, BF16 = 0, 1
@@ -350,8 +352,26 @@ def kv_memory_bytes(n_layers=32, n_kv_heads=8, head_dim=128, bytes_per_element=2
     return {"full_bytes": full.value, "compressed_bytes": comp.value, "reduction_factor": red.value}
 
 
+_fast = None
+
+
+def fast_lib():
+    """liblkv_oracle_fast.so (timing of the CPU baseline only; never a parity reference)."""
+    global _fast
+    if _fast is None:
+        if not os.path.exists(_FAST_PATH):
+            subprocess.check_call(["make", "-s", "liblkv_oracle_fast.so"], cwd=_HERE)
+        L = C.CDLL(_FAST_PATH)
+        L.lkvo_last_error.restype = C.c_char_p
+        L.lkvo_evict_heads.argtypes = lib().lkvo_evict_heads.argtypes
+        for name in ("lkvo_allocate_budgets", "lkvo_freeze_budgets_exact"):
+            getattr(L, name).argtypes = getattr(lib(), name).argtypes
+        _fast = L
+    return _fast
+
+
 def evict_heads(keys, values, t_per_head, in_mode, w1_all, b1_all, w2_all, act, head_scorer, budgets,
-                offsets, n_threads=1, want_scores=False):
+                offsets, n_threads=1, want_scores=False, fast=False):
     """Whole CPU eviction over heads.  keys/values: numpy [n_heads][T][d] (float32 or
     uint16 bf16 bits).  Returns (dst_k, dst_v, dst_pos[, scores])."""
     keys = np.ascontiguousarray(keys)
@@ -369,7 +389,8 @@ def evict_heads(keys, values, t_per_head, in_mode, w1_all, b1_all, w2_all, act, 
     dst_v = np.zeros((max(total, 1), d), keys.dtype)
     dst_pos = np.full(max(total, 1), -1, np.int32)
     scores = np.zeros((n_heads, T), np.float64) if want_scores else None
-    _check(lib().lkvo_evict_heads(dtype, keys.ctypes.data, values.ctypes.data, n_heads, T,
+    L = fast_lib() if fast else lib()
+    _check(L.lkvo_evict_heads(dtype, keys.ctypes.data, values.ctypes.data, n_heads, T,
                                   _ptr(t_per_head, _ip), d, in_mode, _ptr(w1_all, _dp), _ptr(b1_all, _dp),
                                   _ptr(w2_all, _dp), hidden, act, _ptr(head_scorer, _ip), _ptr(budgets, _ip),
                                   _ptr(offsets, _lp), dst_k.ctypes.data, dst_v.ctypes.data, _ptr(dst_pos, _ip),

@@ -588,24 +588,38 @@ int lkvo_token_scores(int dtype, const void* keys, const void* values, int64_t t
         return fail(LKVO_CONTRACT, "token_scores: bad geometry");
     if (in_mode == 2 && !values) return fail(LKVO_CONTRACT, "token_scores: values required");
     const int in = in_mode * d;
-    double* x = (double*)malloc(sizeof(double) * (size_t)in);
-    double* acc = (double*)malloc(sizeof(double) * (size_t)hidden);
+    /* rows in blocks of 4 so each W1 row is reused from cache four times; every row keeps the
+     * reference's summation order (i ascending), so results are identical to a row-at-a-time loop */
+    enum { RB = 4 };
+    double* x = (double*)malloc(sizeof(double) * (size_t)in * RB);
+    double* acc = (double*)malloc(sizeof(double) * (size_t)hidden * RB);
     int rc = LKVO_OK;
-    for (int64_t r = 0; r < t && rc == LKVO_OK; ++r) {
-        for (int c = 0; c < d; ++c) x[c] = widen(dtype, keys, r * d + c);
-        if (in_mode == 2)
-            for (int c = 0; c < d; ++c) x[d + c] = widen(dtype, values, r * d + c);
-        for (int c = 0; c < in; ++c)
-            if (!isfinite(x[c])) rc = fail(LKVO_NUMERIC, "matmul: non-finite input");
-        for (int j = 0; j < hidden; ++j) acc[j] = 0.0;
-        for (int i = 0; i < in; ++i) {
-            const double xi = x[i];
-            const double* wr = w1 + (size_t)i * hidden;
-            for (int j = 0; j < hidden; ++j) acc[j] += xi * wr[j];
+    for (int64_t r0 = 0; r0 < t && rc == LKVO_OK; r0 += RB) {
+        const int nb = (int)(t - r0 < RB ? t - r0 : RB);
+        for (int b = 0; b < nb; ++b) {
+            double* xb = x + (size_t)b * in;
+            const int64_t r = r0 + b;
+            for (int c = 0; c < d; ++c) xb[c] = widen(dtype, keys, r * d + c);
+            if (in_mode == 2)
+                for (int c = 0; c < d; ++c) xb[d + c] = widen(dtype, values, r * d + c);
+            for (int c = 0; c < in; ++c)
+                if (!isfinite(xb[c])) rc = fail(LKVO_NUMERIC, "matmul: non-finite input");
+            for (int j = 0; j < hidden; ++j) acc[(size_t)b * hidden + j] = 0.0;
         }
-        double s = 0.0;
-        for (int j = 0; j < hidden; ++j) s += act_apply(act, acc[j] + b1[j]) * w2[j];
-        out[r] = s;
+        for (int i = 0; i < in; ++i) {
+            const double* wr = w1 + (size_t)i * hidden;
+            for (int b = 0; b < nb; ++b) {
+                const double xi = x[(size_t)b * in + i];
+                double* ab = acc + (size_t)b * hidden;
+                for (int j = 0; j < hidden; ++j) ab[j] += xi * wr[j];
+            }
+        }
+        for (int b = 0; b < nb; ++b) {
+            const double* ab = acc + (size_t)b * hidden;
+            double s = 0.0;
+            for (int j = 0; j < hidden; ++j) s += act_apply(act, ab[j] + b1[j]) * w2[j];
+            out[r0 + b] = s;
+        }
     }
     free(x);
     free(acc);
