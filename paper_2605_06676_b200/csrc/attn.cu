@@ -22,12 +22,12 @@
 //
 // B200 design (bf16 inputs, fp32 accumulate, head_dim 128):
 //   * forward on tcgen05 (fwd_tc_kernel below): S and O accumulate in TMEM, P goes through
-//     swizzled shared memory, V is read from a transposed copy so both UMMA B operands are
-//     K-major; causal tiles past the block's last admissible key are never loaded;
+//     swizzled shared memory, the V tile is the B operand of P V read MN-major straight from the
+//     TMA layout; causal tiles past the block's last admissible key are never loaded;
 //   * backward on tcgen05, two kernels with no atomics (deterministic):
-//     dQ:  CTA = 128 queries (Q, dO in smem), K/V/K^T tiles streamed; S = Q K^T and dP = dO V^T in
+//     dQ:  CTA = 128 queries (Q, dO in smem), K/V tiles streamed; S = Q K^T and dP = dO V^T in
 //          TMEM, dS = P (dP - D) written by the row threads to smem, dQ += dS K accumulated in TMEM;
-//     dKV: CTA = 128 keys (K, V in smem for the CTA's life), streams 64-query Q/dO/Q^T/dO^T tiles of
+//     dKV: CTA = 128 keys (K, V in smem for the CTA's life), streams 64-query Q/dO tiles of
 //          all G query heads; S^T, dP^T in TMEM; P^T, dS^T through smem; dV += P^T dO and
 //          dK += dS^T Q in TMEM; the mask gradient per key accumulates in the key-row thread.
 // fp32 inputs run SIMT kernels (exact two-pass softmax, the 1e-5 correctness path).
@@ -118,8 +118,8 @@ __device__ __forceinline__ int tc_tiles(const Geo& g, int r0) {
 // warpgroup runs its softmax the tensor core works on the other's S / P V (FA4-style ping-pong).
 __global__ void __launch_bounds__(kTcThreads, 1)
     fwd_tc_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ CUtensorMap tq,
-                  const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tvt, int tk_pad) {
-    constexpr uint32_t kQBytes = kTcQ * 256, kKBytes = kTcK * 256, kVBytes = kD * kTcK * 2, kPBytes = kTcQ * kTcK * 2;
+                  const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tv) {
+    constexpr uint32_t kQBytes = kTcQ * 256, kKBytes = kTcK * 256, kVBytes = kTcK * 256, kPBytes = kTcQ * kTcK * 2;
     extern __shared__ unsigned char smem_dyn[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
     unsigned char* qs = smem;                                 // [wg] Q tiles
@@ -181,7 +181,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             mbar_arrive_expect_tx(q_full, kTcWG * kQBytes);
 #pragma unroll
             for (int w = 0; w < kTcWG; ++w) tma_tile<kTcQ>(qs + w * kQBytes, &tq, q_full, (int)(q_row0 + q0 + w * kTcQ), pol);
-            const int vt_row0 = (b * g.n_kv_heads + kvh) * kD;
             for (int t = 0; t < n_all; ++t) {
                 const int st = t % kTcStages;
                 if (t >= kTcStages) mbar_wait(&k_empty[st], ((t / kTcStages) - 1) & 1);
@@ -189,13 +188,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 tma_tile<kTcK>(ks + st * kKBytes, &tk, &k_full[st], (int)(kv_row0 + t * kTcK), pol);
                 if (t >= kTcStages) mbar_wait(&v_empty[st], ((t / kTcStages) - 1) & 1);
                 mbar_arrive_expect_tx(&v_full[st], kVBytes);
-                tma_load_2d(vs + st * kVBytes, &tvt, &v_full[st], t * kTcK, vt_row0, pol);
+                tma_tile<kTcK>(vs + st * kVBytes, &tv, &v_full[st], (int)(kv_row0 + t * kTcK), pol);
             }
         }
     } else if (warp == kTcWG * 4 + 1) {
         // ===================== MMA issuer: S of tile t+1 (both warpgroups), then P V of tile t
         if (lane == 0) {
-            constexpr uint32_t idesc_s = umma_idesc_bf16(kTcQ, kTcK), idesc_o = umma_idesc_bf16(kTcQ, kD);
+            constexpr uint32_t idesc_s = umma_idesc_bf16(kTcQ, kTcK), idesc_o = umma_idesc_bf16_bmn(kTcQ, kD);
             const uint32_t qa = smem_u32(qs), ka = smem_u32(ks), va = smem_u32(vs), pa = smem_u32(ps);
             mbar_wait(q_full, 0);
             auto issue_s = [&](int t) {
@@ -229,7 +228,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
                         const uint64_t ad = umma_desc_sw128(pa + (w * 2 + bb) * kPBytes + kk * 32);
-                        const uint64_t bd = umma_desc_sw128(va + st * kVBytes + kk * 32);
+                        // B = the V tile read MN-major: keys 16kk.. at +2048 B, d 64..127 one box on
+                        const uint64_t bd = umma_desc_sw128_mn(va + st * kVBytes + kk * 2048, kTcK * 128);
                         umma_bf16(tmem + 256 + w * 128, ad, bd, idesc_o, (t > 0 || kk > 0) ? 1u : 0u);
                     }
                     umma_commit(&o_bar[w]);
@@ -380,8 +380,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 }
 
 // =====================================================================================================
-// backward on tcgen05: dKV (key-major) and dQ (query-major); every UMMA operand K-major, the
-// transposed operands (Q^T, dO^T, K^T) read from transposed copies made by transpose_kernel.
+// backward on tcgen05: dKV (key-major) and dQ (query-major); the transposed B operands (Q and dO
+// for dK / dV, K for dQ) are the TMA tiles themselves read through MN-major UMMA descriptors.
 // =====================================================================================================
 constexpr int kBwK = 128;   // dKV: keys per CTA (UMMA M)
 constexpr int kBwQ = 64;    // dKV: queries per streamed tile (UMMA N of S^T, K of dV / dK)
@@ -390,20 +390,13 @@ constexpr int kBwThreads = 192;  // warps 0-3 compute (thread = row = TMEM lane)
 __global__ void __launch_bounds__(kBwThreads, 1)
     dkv_tc_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ CUtensorMap tk128,
                   const __grid_constant__ CUtensorMap tv128, const __grid_constant__ CUtensorMap tq64,
-                  const __grid_constant__ CUtensorMap tdo64, const __grid_constant__ CUtensorMap tqt,
-                  const __grid_constant__ CUtensorMap tdot) {
-    constexpr uint32_t kKB128 = kBwK * 256, kT64 = kBwQ * 256, kStage = 4 * kT64, kPT = kBwK * kBwQ * 2;
-    // this kernel uses all but ~1 KB of the 227 KB per-block shared memory, so there is no room for
-    // a manual 1024-byte round-up: the dynamic window starts after the 1 KB reserved block (aligned)
-    extern __shared__ __align__(1024) unsigned char smem_dyn[];
-    unsigned char* smem = smem_dyn;
-    if ((smem_u32(smem) & 1023) != 0) {
-        if (threadIdx.x == 0) latch_error(p.err, LKV_ERR_UNSUPPORTED, 1024);
-        return;
-    }
+                  const __grid_constant__ CUtensorMap tdo64) {
+    constexpr uint32_t kKB128 = kBwK * 256, kT64 = kBwQ * 256, kStage = 2 * kT64, kPT = kBwK * kBwQ * 2;
+    extern __shared__ unsigned char smem_dyn[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
     unsigned char* ks = smem;
     unsigned char* vs = ks + kKB128;
-    unsigned char* stg = vs + kKB128;          // [2] x {Q, dO, Q^T, dO^T}
+    unsigned char* stg = vs + kKB128;          // [2] x {Q, dO}
     unsigned char* pts = stg + 2 * kStage;     // P^T [128 keys][64 q]
     unsigned char* dss = pts + kPT;            // dS^T
     float* cw = reinterpret_cast<float*>(dss + kPT);  // [4 warps][lse 64 | D 64]
@@ -464,13 +457,12 @@ __global__ void __launch_bounds__(kBwThreads, 1)
                 const int qrow = (int)((size_t)hq * g.t_q + r0);
                 tma_tile<kBwQ>(d, &tq64, &st_full[st], qrow, pol);
                 tma_tile<kBwQ>(d + kT64, &tdo64, &st_full[st], qrow, pol);
-                tma_load_2d(d + 2 * kT64, &tqt, &st_full[st], r0, hq * kD, pol);
-                tma_load_2d(d + 3 * kT64, &tdot, &st_full[st], r0, hq * kD, pol);
+
             }
         }
     } else if (warp == 5) {
         if (lane == 0 && ntiles > 0) {
-            constexpr uint32_t id_s = umma_idesc_bf16(kBwK, kBwQ), id_o = umma_idesc_bf16(kBwK, kD);
+            constexpr uint32_t id_s = umma_idesc_bf16(kBwK, kBwQ), id_o = umma_idesc_bf16_bmn(kBwK, kD);
             const uint32_t ka = smem_u32(ks), va = smem_u32(vs), sa = smem_u32(stg), pa = smem_u32(pts),
                            da = smem_u32(dss);
             mbar_wait(kv_full, 0);
@@ -494,13 +486,14 @@ __global__ void __launch_bounds__(kBwThreads, 1)
                 const int st = t & 1;
                 mbar_wait(pt_full, t & 1);
                 tc_fence_after();
-                const uint32_t qtb = sa + st * kStage + 2 * kT64, utb = qtb + kT64;
+                // B = the Q / dO tiles themselves, read MN-major ([queries][d] rows, d contiguous)
+                const uint32_t qb = sa + st * kStage, ub = qb + kT64;
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
-                    umma_bf16(tmem + 256, umma_desc_sw128(pa + kk * 32), umma_desc_sw128(utb + kk * 32), id_o,
-                              (t > 0 || kk > 0) ? 1u : 0u);
-                    umma_bf16(tmem + 384, umma_desc_sw128(da + kk * 32), umma_desc_sw128(qtb + kk * 32), id_o,
-                              (t > 0 || kk > 0) ? 1u : 0u);
+                    umma_bf16(tmem + 256, umma_desc_sw128(pa + kk * 32), umma_desc_sw128_mn(ub + kk * 2048, kBwQ * 128),
+                              id_o, (t > 0 || kk > 0) ? 1u : 0u);
+                    umma_bf16(tmem + 384, umma_desc_sw128(da + kk * 32), umma_desc_sw128_mn(qb + kk * 2048, kBwQ * 128),
+                              id_o, (t > 0 || kk > 0) ? 1u : 0u);
                 }
                 umma_commit(pt_empty);
                 umma_commit(&st_empty[st]);
@@ -624,13 +617,13 @@ __global__ void __launch_bounds__(kBwThreads, 1)
 __global__ void __launch_bounds__(kBwThreads, 1)
     dq_tc_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ CUtensorMap tq128,
                  const __grid_constant__ CUtensorMap tdo128, const __grid_constant__ CUtensorMap tk64,
-                 const __grid_constant__ CUtensorMap tv64, const __grid_constant__ CUtensorMap tkt) {
-    constexpr uint32_t kQ128 = kTcQ * 256, kT64 = kTcK * 256, kStage = 3 * kT64, kDS = kTcQ * kTcK * 2;
+                 const __grid_constant__ CUtensorMap tv64) {
+    constexpr uint32_t kQ128 = kTcQ * 256, kT64 = kTcK * 256, kStage = 2 * kT64, kDS = kTcQ * kTcK * 2;
     extern __shared__ unsigned char smem_dyn[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
     unsigned char* qs = smem;
     unsigned char* us = qs + kQ128;
-    unsigned char* stg = us + kQ128;            // [2] x {K, V, K^T}
+    unsigned char* stg = us + kQ128;            // [2] x {K, V}
     unsigned char* dss = stg + 2 * kStage;      // dS [2][128 q][64 keys]
     float* mw = reinterpret_cast<float*>(dss + 2 * kDS);  // [4 warps][64]
     uint64_t* bars = reinterpret_cast<uint64_t*>(mw + 4 * kTcK);
@@ -677,7 +670,6 @@ __global__ void __launch_bounds__(kBwThreads, 1)
             mbar_arrive_expect_tx(q_full, 2 * kQ128);
             tma_tile<kTcQ>(qs, &tq128, q_full, (int)(q_row0 + q0), pol);
             tma_tile<kTcQ>(us, &tdo128, q_full, (int)(q_row0 + q0), pol);
-            const int kt_row0 = (b * g.n_kv_heads + kvh) * kD;
             for (int t = 0; t < ntiles; ++t) {
                 const int st = t & 1;
                 if (t >= 2) mbar_wait(&st_empty[st], ((t >> 1) - 1) & 1);
@@ -685,12 +677,12 @@ __global__ void __launch_bounds__(kBwThreads, 1)
                 unsigned char* d = stg + st * kStage;
                 tma_tile<kTcK>(d, &tk64, &st_full[st], (int)(kv_row0 + t * kTcK), pol);
                 tma_tile<kTcK>(d + kT64, &tv64, &st_full[st], (int)(kv_row0 + t * kTcK), pol);
-                tma_load_2d(d + 2 * kT64, &tkt, &st_full[st], t * kTcK, kt_row0, pol);
+
             }
         }
     } else if (warp == 5) {
         if (lane == 0 && ntiles > 0) {
-            constexpr uint32_t id_s = umma_idesc_bf16(kTcQ, kTcK), id_o = umma_idesc_bf16(kTcQ, kD);
+            constexpr uint32_t id_s = umma_idesc_bf16(kTcQ, kTcK), id_o_mn = umma_idesc_bf16_bmn(kTcQ, kD);
             const uint32_t qa = smem_u32(qs), ua = smem_u32(us), sa = smem_u32(stg), da = smem_u32(dss);
             mbar_wait(q_full, 0);
             auto issue_s = [&](int t) {
@@ -713,11 +705,13 @@ __global__ void __launch_bounds__(kBwThreads, 1)
                 const int st = t & 1, bb = t & 1;
                 mbar_wait(&ds_full[bb], (t >> 1) & 1);
                 tc_fence_after();
-                const uint32_t ktb = sa + st * kStage + 2 * kT64;
+                // dQ += dS K: B = the K tile itself read MN-major ([keys][d] rows, d contiguous):
+                // k-step kk = keys 16kk.. -> +2048 B; the second 64-column box is the next MN atom
+                const uint32_t kb = sa + st * kStage;
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk)
-                    umma_bf16(tmem + 256, umma_desc_sw128(da + bb * kDS + kk * 32), umma_desc_sw128(ktb + kk * 32), id_o,
-                              (t > 0 || kk > 0) ? 1u : 0u);
+                    umma_bf16(tmem + 256, umma_desc_sw128(da + bb * kDS + kk * 32),
+                              umma_desc_sw128_mn(kb + kk * 2048, kTcK * 128), id_o_mn, (t > 0 || kk > 0) ? 1u : 0u);
                 umma_commit(&ds_empty[bb]);
                 umma_commit(&st_empty[st]);
             }
@@ -819,22 +813,6 @@ __global__ void __launch_bounds__(kBwThreads, 1)
     }
 }
 
-// V [rows = (b, kvh, key)][128] -> V^T [(b, kvh, d)][tk_pad] (keys past t_k zero), 32x32 tiles
-__global__ void transpose_v_kernel(const __nv_bfloat16* __restrict__ v, __nv_bfloat16* __restrict__ vt, int t_k,
-                                   int tk_pad) {
-    __shared__ __nv_bfloat16 tile[32][33];
-    const int bh = blockIdx.z, k0 = blockIdx.x * 32, d0 = blockIdx.y * 32;
-    const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
-    for (int i = ty; i < 32; i += 8) {
-        const int key = k0 + i;
-        tile[i][tx] = key < t_k ? v[((size_t)bh * t_k + key) * kD + d0 + tx] : __float2bfloat16(0.f);
-    }
-    __syncthreads();
-    for (int i = ty; i < 32; i += 8) {
-        const int d = d0 + i, key = k0 + tx;
-        if (key < tk_pad) vt[((size_t)bh * kD + d) * tk_pad + key] = tile[tx][i];
-    }
-}
 
 // validate_call (attention.cpp:40-42): every mask value finite and >= 0
 __global__ void mask_check_kernel(const float* __restrict__ mask, int64_t n, ErrWord* err) {
@@ -1046,13 +1024,12 @@ __global__ void __launch_bounds__(kSimt) dkv_f32_kernel(const __grid_constant__ 
 // ---- host launchers ----------------------------------------------------------------------------------
 
 
-int attn_tk_pad(int t_k) { return (t_k + attn::kTcK - 1) / attn::kTcK * attn::kTcK; }
 size_t attn_fwd_tc_smem() {
-    return 1024 + attn::kTcWG * attn::kTcQ * 256 + attn::kTcStages * (attn::kTcK * 256 + attn::kD * attn::kTcK * 2) +
+    return 1024 + attn::kTcWG * attn::kTcQ * 256 + attn::kTcStages * (attn::kTcK * 256 + attn::kTcK * 256) +
            attn::kTcWG * 2 * attn::kTcQ * attn::kTcK * 2 + attn::kTcWG * 4 * attn::kTcK * 4 + 64 * 8 + 16;
 }
 
-cudaError_t launch_attn_fwd(const AttnParams& p, int dtype, int d, const CUtensorMap* mk, const CUtensorMap* mvt,
+cudaError_t launch_attn_fwd(const AttnParams& p, int dtype, int d, const CUtensorMap* mk, const CUtensorMap* mv,
                             const CUtensorMap* mq, cudaStream_t stream) {
     if (p.mask) {
         const int64_t n = (int64_t)p.batch * p.n_kv_heads * p.t_k;
@@ -1060,15 +1037,12 @@ cudaError_t launch_attn_fwd(const AttnParams& p, int dtype, int d, const CUtenso
         note_launches(1);
     }
     if (dtype == LKV_BF16) {
-        const int tk_pad = attn_tk_pad(p.t_k);
-        attn::transpose_v_kernel<<<dim3(tk_pad / 32, attn::kD / 32, p.batch * p.n_kv_heads), dim3(32, 8), 0, stream>>>(
-            static_cast<const __nv_bfloat16*>(p.v), static_cast<__nv_bfloat16*>(p.vt), p.t_k, tk_pad);
         const size_t smem = attn_fwd_tc_smem();
         cudaError_t e = cudaFuncSetAttribute(attn::fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         constexpr int rows_per_cta = attn::kTcWG * attn::kTcQ;
         attn::fwd_tc_kernel<<<dim3((p.t_q + rows_per_cta - 1) / rows_per_cta, p.n_q_heads, p.batch), attn::kTcThreads,
-                              smem, stream>>>(p, *mq, *mk, *mvt, tk_pad);
+                              smem, stream>>>(p, *mq, *mk, *mv);
         note_launches(1);
     } else {
         const size_t smem = (size_t)(d + p.t_k) * 4;
@@ -1081,39 +1055,30 @@ cudaError_t launch_attn_fwd(const AttnParams& p, int dtype, int d, const CUtenso
 }
 
 size_t attn_dq_tc_smem() {
-    return 1024 + 2 * attn::kTcQ * 256 + 2 * 3 * attn::kTcK * 256 + 2 * attn::kTcQ * attn::kTcK * 2 + 4 * attn::kTcK * 4 +
+    return 1024 + 2 * attn::kTcQ * 256 + 2 * 2 * attn::kTcK * 256 + 2 * attn::kTcQ * attn::kTcK * 2 + 4 * attn::kTcK * 4 +
            16 * 8;
 }
-size_t attn_dkv_tc_smem() {  // no alignment slack (see dkv_tc_kernel)
-    return 2 * attn::kBwK * 256 + 2 * 4 * attn::kBwQ * 256 + 2 * attn::kBwK * attn::kBwQ * 2 + 4 * 2 * attn::kBwQ * 4 +
-           16 * 8;
+size_t attn_dkv_tc_smem() {
+    return 1024 + 2 * attn::kBwK * 256 + 2 * 2 * attn::kBwQ * 256 + 2 * attn::kBwK * attn::kBwQ * 2 +
+           4 * 2 * attn::kBwQ * 4 + 16 * 8;
 }
 
-// m: dQ maps {Q(128 rows), dO(128), K(64), V(64), K^T(128 x 64)}, dKV maps {K(128), V(128), Q(64), dO(64),
-//    Q^T(128 x 64), dO^T(128 x 64)}
+// m: dQ maps {Q(128-row boxes), dO(128), K(64), V(64)}, dKV maps {K(128), V(128), Q(64), dO(64)}
 cudaError_t launch_attn_bwd(const AttnParams& p, int dtype, int d, const CUtensorMap* m, cudaStream_t stream) {
     const int64_t rows = (int64_t)p.batch * p.n_q_heads * p.t_q;
     cudaError_t e;
     if (dtype == LKV_BF16) {
         attn::bwd_prep_kernel<__nv_bfloat16><<<(unsigned)((rows + 3) / 4), 128, 0, stream>>>(
             static_cast<const __nv_bfloat16*>(p.out), static_cast<const __nv_bfloat16*>(p.dout), p.dsum, rows, d);
-        // transposed operand copies: K^T, Q^T, dO^T ([(b, head, d)][pad])
-        const int tk_pad = attn_tk_pad(p.t_k), tq_pad = attn_tk_pad(p.t_q);
-        attn::transpose_v_kernel<<<dim3(tk_pad / 32, attn::kD / 32, p.batch * p.n_kv_heads), dim3(32, 8), 0, stream>>>(
-            static_cast<const __nv_bfloat16*>(p.k), static_cast<__nv_bfloat16*>(p.kt), p.t_k, tk_pad);
-        attn::transpose_v_kernel<<<dim3(tq_pad / 32, attn::kD / 32, p.batch * p.n_q_heads), dim3(32, 8), 0, stream>>>(
-            static_cast<const __nv_bfloat16*>(p.q), static_cast<__nv_bfloat16*>(p.qt), p.t_q, tq_pad);
-        attn::transpose_v_kernel<<<dim3(tq_pad / 32, attn::kD / 32, p.batch * p.n_q_heads), dim3(32, 8), 0, stream>>>(
-            static_cast<const __nv_bfloat16*>(p.dout), static_cast<__nv_bfloat16*>(p.dot), p.t_q, tq_pad);
         const size_t s1 = attn_dq_tc_smem(), s2 = attn_dkv_tc_smem();
         if ((e = cudaFuncSetAttribute(attn::dq_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1)))
             return e;
         if ((e = cudaFuncSetAttribute(attn::dkv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2)))
             return e;
         attn::dq_tc_kernel<<<dim3((p.t_q + attn::kTcQ - 1) / attn::kTcQ, p.n_q_heads, p.batch), attn::kBwThreads, s1,
-                             stream>>>(p, m[0], m[1], m[2], m[3], m[4]);
+                             stream>>>(p, m[0], m[1], m[2], m[3]);
         attn::dkv_tc_kernel<<<dim3((p.t_k + attn::kBwK - 1) / attn::kBwK, p.n_kv_heads, p.batch), attn::kBwThreads, s2,
-                              stream>>>(p, m[5], m[6], m[7], m[8], m[9], m[10]);
+                              stream>>>(p, m[4], m[5], m[6], m[7]);
         note_launches(3);
     } else {
         attn::bwd_prep_kernel<float><<<(unsigned)((rows + 3) / 4), 128, 0, stream>>>(

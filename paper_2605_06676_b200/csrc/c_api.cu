@@ -882,22 +882,10 @@ static AttnParams attn_params(const lkv_attn_desc* a, const void* q, const void*
     return p;
 }
 
-// workspace: [error latch | D = rowsum(dO * O) (backward) | V^T (bf16 forward)]
-static size_t attn_vt_offset(const lkv_attn_desc* a) {
-    return 256 + align_up(sizeof(float) * (size_t)a->batch * a->n_q_heads * a->t_q);
-}
-static size_t attn_kvt_bytes(const lkv_attn_desc* a) {
-    return align_up((size_t)a->batch * a->n_kv_heads * 128 * attn_tk_pad(a->t_k) * 2);
-}
-static size_t attn_qt_bytes(const lkv_attn_desc* a) {
-    return align_up((size_t)a->batch * a->n_q_heads * 128 * attn_tk_pad(a->t_q) * 2);
-}
+// workspace: [error latch | D = rowsum(dO * O) (backward)]
 size_t lkv_attn_workspace_bytes(const lkv_attn_desc* a) {
     if (check_attn(a)) return 0;
-    size_t n = attn_vt_offset(a);
-    // bf16: V^T (forward) or K^T + Q^T + dO^T (backward), sized for the larger
-    if (a->dtype == LKV_BF16) n += std::max(attn_kvt_bytes(a), attn_kvt_bytes(a) + 2 * attn_qt_bytes(a));
-    return n;
+    return 256 + align_up(sizeof(float) * (size_t)a->batch * a->n_q_heads * a->t_q);
 }
 
 lkv_status lkv_masked_attention_fwd(const lkv_attn_desc* a, const void* q, const void* k, const void* v,
@@ -910,15 +898,14 @@ lkv_status lkv_masked_attention_fwd(const lkv_attn_desc* a, const void* q, const
     AttnParams p = attn_params(a, q, k, v, mask, ws);
     p.out = out;
     p.lse = lse;
-    CUtensorMap mk, mvt, mq;
+    CUtensorMap mk, mv, mq;
     if (a->dtype == LKV_BF16) {
         const uint64_t rk = (uint64_t)a->batch * a->n_kv_heads * a->t_k, rq = (uint64_t)a->batch * a->n_q_heads * a->t_q;
-        p.vt = at<void>(ws, attn_vt_offset(a));
-        if ((st = make_map_bf16(&mk, k, 128, rk, 64)) || (st = make_map_bf16(&mq, q, 128, rq, 128)) ||
-            (st = make_map_bf16(&mvt, p.vt, (uint64_t)attn_tk_pad(a->t_k), (uint64_t)a->batch * a->n_kv_heads * 128, 128)))
+        if ((st = make_map_bf16(&mk, k, 128, rk, 64)) || (st = make_map_bf16(&mv, v, 128, rk, 64)) ||
+            (st = make_map_bf16(&mq, q, 128, rq, 128)))
             return st;
     }
-    LKV_CUDA(launch_attn_fwd(p, a->dtype, a->head_dim, &mk, &mvt, &mq, (cudaStream_t)stream), "masked attention fwd");
+    LKV_CUDA(launch_attn_fwd(p, a->dtype, a->head_dim, &mk, &mv, &mq, (cudaStream_t)stream), "masked attention fwd");
     return LKV_OK;
 }
 
@@ -939,20 +926,13 @@ lkv_status lkv_masked_attention_bwd(const lkv_attn_desc* a, const void* q, const
     p.dk = dk;
     p.dv = dv;
     p.dmask = mask ? dmask : nullptr;
-    CUtensorMap m[11];
+    CUtensorMap m[8];
     if (a->dtype == LKV_BF16) {
         const uint64_t rk = (uint64_t)a->batch * a->n_kv_heads * a->t_k, rq = (uint64_t)a->batch * a->n_q_heads * a->t_q;
-        p.kt = at<void>(ws, attn_vt_offset(a));
-        p.qt = static_cast<char*>(p.kt) + attn_kvt_bytes(a);
-        p.dot = static_cast<char*>(p.qt) + attn_qt_bytes(a);
-        const uint64_t tkp = attn_tk_pad(a->t_k), tqp = attn_tk_pad(a->t_q);
-        const uint64_t rkt = (uint64_t)a->batch * a->n_kv_heads * 128, rqt = (uint64_t)a->batch * a->n_q_heads * 128;
         if ((st = make_map_bf16(&m[0], q, 128, rq, 128)) || (st = make_map_bf16(&m[1], d_out, 128, rq, 128)) ||
             (st = make_map_bf16(&m[2], k, 128, rk, 64)) || (st = make_map_bf16(&m[3], v, 128, rk, 64)) ||
-            (st = make_map_bf16(&m[4], p.kt, tkp, rkt, 128)) || (st = make_map_bf16(&m[5], k, 128, rk, 128)) ||
-            (st = make_map_bf16(&m[6], v, 128, rk, 128)) || (st = make_map_bf16(&m[7], q, 128, rq, 64)) ||
-            (st = make_map_bf16(&m[8], d_out, 128, rq, 64)) || (st = make_map_bf16(&m[9], p.qt, tqp, rqt, 128)) ||
-            (st = make_map_bf16(&m[10], p.dot, tqp, rqt, 128)))
+            (st = make_map_bf16(&m[4], k, 128, rk, 128)) || (st = make_map_bf16(&m[5], v, 128, rk, 128)) ||
+            (st = make_map_bf16(&m[6], q, 128, rq, 64)) || (st = make_map_bf16(&m[7], d_out, 128, rq, 64)))
             return st;
     }
     LKV_CUDA(launch_attn_bwd(p, a->dtype, a->head_dim, m, (cudaStream_t)stream), "masked attention bwd");

@@ -178,6 +178,18 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
     d |= uint64_t(2u) << 61;            // SWIZZLE_128B
     return d;
 }
+// UMMA shared-memory descriptor for an MN-major operand with the 128-byte swizzle, as TMA writes a
+// [K rows][64 MN elements] box: 8-row x 128-byte atoms; LBO = byte stride between atoms along MN
+// (the next 64-element box), SBO = byte stride between 8-row groups along K (1024 B).
+__device__ __forceinline__ uint64_t umma_desc_sw128_mn(uint32_t smem_addr, uint32_t lbo_bytes) {
+    uint64_t d = 0;
+    d |= uint64_t((smem_addr >> 4) & 0x3FFFu);
+    d |= uint64_t((lbo_bytes >> 4) & 0x3FFFu) << 16;
+    d |= uint64_t(1024u >> 4) << 32;
+    d |= uint64_t(1u) << 46;
+    d |= uint64_t(2u) << 61;
+    return d;
+}
 // Instruction descriptor: kind::f16, A = B = bf16, D = fp32, both K-major.
 __host__ __device__ constexpr uint32_t umma_idesc_bf16(int M, int N) {
     return (1u << 4)                       // D format f32
@@ -186,6 +198,8 @@ __host__ __device__ constexpr uint32_t umma_idesc_bf16(int M, int N) {
            | (uint32_t(N >> 3) << 17)      // N / 8
            | (uint32_t(M >> 4) << 24);     // M / 16
 }
+// ... with B MN-major (transposed B, bit 16)
+__host__ __device__ constexpr uint32_t umma_idesc_bf16_bmn(int M, int N) { return umma_idesc_bf16(M, N) | (1u << 16); }
 
 __device__ __forceinline__ bool elect_one() {
     uint32_t pred = 0;

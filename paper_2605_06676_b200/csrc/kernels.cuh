@@ -155,15 +155,10 @@ struct AttnParams {
     float* dk;
     float* dv;
     float* dmask;       // null when mask is null
-    void* vt;           // bf16 forward: V^T [batch][n_kv_heads][d][attn_tk_pad(t_k)] (workspace)
-    void* kt;           // bf16 backward: K^T (as V^T), Q^T and dO^T [batch][n_q_heads][d][attn_tk_pad(t_q)]
-    void* qt;
-    void* dot;
     ErrWord* err;
 };
-cudaError_t launch_attn_fwd(const AttnParams& p, int dtype, int d, const CUtensorMap* mk, const CUtensorMap* mvt,
+cudaError_t launch_attn_fwd(const AttnParams& p, int dtype, int d, const CUtensorMap* mk, const CUtensorMap* mv,
                             const CUtensorMap* mq, cudaStream_t stream);
-int attn_tk_pad(int t_k);
 size_t attn_fwd_tc_smem();
 cudaError_t launch_attn_bwd(const AttnParams& p, int dtype, int d, const CUtensorMap* maps, cudaStream_t stream);
 size_t attn_dq_tc_smem();
