@@ -614,124 +614,142 @@ __global__ void __launch_bounds__(kBwThreads, 1)
     }
 }
 
-__global__ void __launch_bounds__(kBwThreads, 1)
+// dQ: CTA = two 128-query tiles, one compute warpgroup each (ping-pong on shared K/V tiles, as in
+// the forward).  TMEM per warpgroup: S [0,64), dP [64,128), dQ [128,256) at wg * 256.
+constexpr int kDqThreads = (kTcWG * 4 + 2) * 32;
+
+__global__ void __launch_bounds__(kDqThreads, 1)
     dq_tc_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ CUtensorMap tq128,
                  const __grid_constant__ CUtensorMap tdo128, const __grid_constant__ CUtensorMap tk64,
                  const __grid_constant__ CUtensorMap tv64) {
     constexpr uint32_t kQ128 = kTcQ * 256, kT64 = kTcK * 256, kStage = 2 * kT64, kDS = kTcQ * kTcK * 2;
-    extern __shared__ unsigned char smem_dyn[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
-    unsigned char* qs = smem;
-    unsigned char* us = qs + kQ128;
-    unsigned char* stg = us + kQ128;            // [2] x {K, V}
-    unsigned char* dss = stg + 2 * kStage;      // dS [2][128 q][64 keys]
-    float* mw = reinterpret_cast<float*>(dss + 2 * kDS);  // [4 warps][64]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(mw + 4 * kTcK);
+    // ~226 KB of shared memory: no room for a manual 1024-byte round-up; the dynamic window starts
+    // right after the 1 KB reserved block, which is 1024-aligned (checked below)
+    extern __shared__ __align__(1024) unsigned char smem_dyn[];
+    unsigned char* smem = smem_dyn;
+    unsigned char* qs = smem;                        // [wg] Q tiles
+    unsigned char* us = qs + kTcWG * kQ128;          // [wg] dO tiles
+    unsigned char* stg = us + kTcWG * kQ128;         // [2] x {K, V}
+    unsigned char* dss = stg + 2 * kStage;           // [wg] dS [128 q][64 keys]
+    float* mw = reinterpret_cast<float*>(dss + kTcWG * kDS);  // [8 warps][64]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(mw + kTcWG * 4 * kTcK);
     uint64_t* q_full = bars;
-    uint64_t* st_full = bars + 1;
-    uint64_t* st_empty = bars + 3;
-    uint64_t* s_full = bars + 5;
-    uint64_t* s_empty = bars + 7;
-    uint64_t* ds_full = bars + 9;
-    uint64_t* ds_empty = bars + 11;
-    uint64_t* acc_done = bars + 13;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+    uint64_t* st_full = bars + 1;   // [2]
+    uint64_t* st_empty = bars + 3;  // [2]
+    uint64_t* s_full = bars + 5;    // [wg]
+    uint64_t* ds_full = bars + 7;   // [wg]
+    uint64_t* ds_empty = bars + 9;  // [wg]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
+    if ((smem_u32(smem) & 1023) != 0) {
+        if (threadIdx.x == 0) latch_error(p.err, LKV_ERR_UNSUPPORTED, 1024);
+        return;
+    }
 
     const Geo g{p.n_q_heads, p.n_kv_heads, p.n_q_heads / p.n_kv_heads, p.t_q, p.t_k, p.causal, p.pos_offset,
                 p.self_keep, p.scale * kLog2e, p.scale};
     const int b = blockIdx.z, qh = blockIdx.y, kvh = qh / g.G;
-    const int q0 = blockIdx.x * kTcQ;
-    const int ntiles = tc_tiles(g, q0);
+    const int q0 = blockIdx.x * (kTcWG * kTcQ);
+    int nt[kTcWG];
+#pragma unroll
+    for (int w = 0; w < kTcWG; ++w) nt[w] = tc_tiles(g, q0 + w * kTcQ);
+    const int n_all = max(nt[0], nt[1]);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int kTmaWarp = kTcWG * 4, kMmaWarp = kTcWG * 4 + 1;
     if (threadIdx.x == 0) {
         mbar_init(q_full, 1);
         for (int i = 0; i < 2; ++i) {
             mbar_init(&st_full[i], 1);
             mbar_init(&st_empty[i], 1);
-            mbar_init(&s_full[i], 1);
-            mbar_init(&s_empty[i], 4);
-            mbar_init(&ds_full[i], 4);
-            mbar_init(&ds_empty[i], 1);
         }
-        mbar_init(acc_done, 1);
+        for (int w = 0; w < kTcWG; ++w) {
+            mbar_init(&s_full[w], 1);
+            mbar_init(&ds_full[w], 4);
+            mbar_init(&ds_empty[w], 1);
+        }
         fence_barrier_init();
     }
-    if (warp == 5) tmem_alloc(tmem_slot, 512);
+    if (warp == kMmaWarp) tmem_alloc(tmem_slot, 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;  // S[2] 0/64, dP[2] 128/192, dQ 256
+    const uint32_t tmem = *tmem_slot;
     const size_t kv_row0 = ((size_t)b * g.n_kv_heads + kvh) * g.t_k;
     const size_t q_row0 = ((size_t)b * g.n_q_heads + qh) * g.t_q;
 
-    if (warp == 4) {
-        if (lane == 0 && ntiles > 0) {
+    if (warp == kTmaWarp) {
+        if (lane == 0 && n_all > 0) {
             const uint64_t pol = l2_policy_evict_last();
-            mbar_arrive_expect_tx(q_full, 2 * kQ128);
-            tma_tile<kTcQ>(qs, &tq128, q_full, (int)(q_row0 + q0), pol);
-            tma_tile<kTcQ>(us, &tdo128, q_full, (int)(q_row0 + q0), pol);
-            for (int t = 0; t < ntiles; ++t) {
+            mbar_arrive_expect_tx(q_full, 2 * kTcWG * kQ128);
+#pragma unroll
+            for (int w = 0; w < kTcWG; ++w) {
+                tma_tile<kTcQ>(qs + w * kQ128, &tq128, q_full, (int)(q_row0 + q0 + w * kTcQ), pol);
+                tma_tile<kTcQ>(us + w * kQ128, &tdo128, q_full, (int)(q_row0 + q0 + w * kTcQ), pol);
+            }
+            for (int t = 0; t < n_all; ++t) {
                 const int st = t & 1;
                 if (t >= 2) mbar_wait(&st_empty[st], ((t >> 1) - 1) & 1);
                 mbar_arrive_expect_tx(&st_full[st], kStage);
                 unsigned char* d = stg + st * kStage;
                 tma_tile<kTcK>(d, &tk64, &st_full[st], (int)(kv_row0 + t * kTcK), pol);
                 tma_tile<kTcK>(d + kT64, &tv64, &st_full[st], (int)(kv_row0 + t * kTcK), pol);
-
             }
         }
-    } else if (warp == 5) {
-        if (lane == 0 && ntiles > 0) {
+    } else if (warp == kMmaWarp) {
+        if (lane == 0 && n_all > 0) {
             constexpr uint32_t id_s = umma_idesc_bf16(kTcQ, kTcK), id_o_mn = umma_idesc_bf16_bmn(kTcQ, kD);
-            const uint32_t qa = smem_u32(qs), ua = smem_u32(us), sa = smem_u32(stg), da = smem_u32(dss);
+            const uint32_t sa = smem_u32(stg), da = smem_u32(dss);
             mbar_wait(q_full, 0);
-            auto issue_s = [&](int t) {
-                const int st = t & 1, bb = t & 1;
+            for (int t = 0; t < n_all; ++t) {
+                const int st = t & 1;
                 mbar_wait(&st_full[st], (t >> 1) & 1);
-                if (t >= 2) mbar_wait(&s_empty[bb], ((t >> 1) - 1) & 1);
                 tc_fence_after();
                 const uint32_t kb = sa + st * kStage, vb = kb + kT64;
+                // S, dP of both warpgroups (their previous S / dP were consumed before ds_full)
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint32_t ao = (kk >> 2) * (kTcQ * 128) + (kk & 3) * 32, bo = (kk >> 2) * (kTcK * 128) + (kk & 3) * 32;
-                    umma_bf16(tmem + bb * 64, umma_desc_sw128(qa + ao), umma_desc_sw128(kb + bo), id_s, kk > 0);
-                    umma_bf16(tmem + 128 + bb * 64, umma_desc_sw128(ua + ao), umma_desc_sw128(vb + bo), id_s, kk > 0);
+                for (int w = 0; w < kTcWG; ++w) {
+                    if (t >= nt[w]) continue;
+                    const uint32_t qa = smem_u32(qs + w * kQ128), ua = smem_u32(us + w * kQ128);
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) {
+                        const uint32_t ao = (kk >> 2) * (kTcQ * 128) + (kk & 3) * 32, bo = (kk >> 2) * (kTcK * 128) + (kk & 3) * 32;
+                        umma_bf16(tmem + w * 256, umma_desc_sw128(qa + ao), umma_desc_sw128(kb + bo), id_s, kk > 0);
+                        umma_bf16(tmem + w * 256 + 64, umma_desc_sw128(ua + ao), umma_desc_sw128(vb + bo), id_s, kk > 0);
+                    }
+                    umma_commit(&s_full[w]);
                 }
-                umma_commit(&s_full[bb]);
-            };
-            issue_s(0);
-            for (int t = 0; t < ntiles; ++t) {
-                if (t + 1 < ntiles) issue_s(t + 1);
-                const int st = t & 1, bb = t & 1;
-                mbar_wait(&ds_full[bb], (t >> 1) & 1);
-                tc_fence_after();
-                // dQ += dS K: B = the K tile itself read MN-major ([keys][d] rows, d contiguous):
-                // k-step kk = keys 16kk.. -> +2048 B; the second 64-column box is the next MN atom
-                const uint32_t kb = sa + st * kStage;
+                // dQ += dS K (B = the K tile read MN-major)
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk)
-                    umma_bf16(tmem + 256, umma_desc_sw128(da + bb * kDS + kk * 32),
-                              umma_desc_sw128_mn(kb + kk * 2048, kTcK * 128), id_o_mn, (t > 0 || kk > 0) ? 1u : 0u);
-                umma_commit(&ds_empty[bb]);
+                for (int w = 0; w < kTcWG; ++w) {
+                    if (t >= nt[w]) continue;
+                    mbar_wait(&ds_full[w], t & 1);
+                    tc_fence_after();
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk)
+                        umma_bf16(tmem + w * 256 + 128, umma_desc_sw128(da + w * kDS + kk * 32),
+                                  umma_desc_sw128_mn(kb + kk * 2048, kTcK * 128), id_o_mn, (t > 0 || kk > 0) ? 1u : 0u);
+                    umma_commit(&ds_empty[w]);
+                }
                 umma_commit(&st_empty[st]);
             }
-            umma_commit(acc_done);
         }
     } else {
-        // ===================== compute: thread = query row
-        const int rl = warp * 32 + lane, r = q0 + rl;
-        const uint32_t la = tmem + (uint32_t(warp * 32) << 16);
+        // ===================== compute: warpgroup wg, thread = query row
+        const int wg = warp >> 2, w4 = warp & 3;
+        const int ntw = nt[wg];
+        const int rl = w4 * 32 + lane, r = q0 + wg * kTcQ + rl;
+        const uint32_t la = tmem + (uint32_t(w4 * 32) << 16) + wg * 256;
         const float lse = r < g.t_q ? p.lse[q_row0 + r] : 0.f, dd = r < g.t_q ? p.dsum[q_row0 + r] : 0.f;
         const float* mask = p.mask ? p.mask + kv_row0 : nullptr;
         float* mwarp = mw + warp * kTcK;
+        unsigned char* my_ds = dss + wg * kDS;
         float mn0 = 0.f, mn1 = 0.f;
         if (mask) {
             mn0 = lane < g.t_k ? __ldg(mask + lane) : 0.f;
             mn1 = lane + 32 < g.t_k ? __ldg(mask + lane + 32) : 0.f;
         }
-        const int wr0 = q0 + warp * 32;
-        for (int t = 0; t < ntiles; ++t) {
-            const int bb = t & 1, j0 = t * kTcK;
+        const int wr0 = q0 + wg * kTcQ + w4 * 32;
+        for (int t = 0; t < ntw; ++t) {
+            const int j0 = t * kTcK;
             if (mask) {
                 mwarp[lane] = mn0;
                 mwarp[lane + 32] = mn1;
@@ -740,21 +758,18 @@ __global__ void __launch_bounds__(kBwThreads, 1)
                 mn0 = jn + lane < g.t_k ? __ldg(mask + jn + lane) : 0.f;
                 mn1 = jn + lane + 32 < g.t_k ? __ldg(mask + jn + lane + 32) : 0.f;
             }
-            mbar_wait(&s_full[bb], (t >> 1) & 1);
+            mbar_wait(&s_full[wg], t & 1);
             tc_fence_after();
             uint32_t sv[64], dv[64];
-            tmem_ld_32x32b_x32(la + bb * 64, *reinterpret_cast<uint32_t(*)[32]>(sv));
-            tmem_ld_32x32b_x32(la + bb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
-            tmem_ld_32x32b_x32(la + 128 + bb * 64, *reinterpret_cast<uint32_t(*)[32]>(dv));
-            tmem_ld_32x32b_x32(la + 128 + bb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(dv + 32));
+            tmem_ld_32x32b_x32(la, *reinterpret_cast<uint32_t(*)[32]>(sv));
+            tmem_ld_32x32b_x32(la + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
+            tmem_ld_32x32b_x32(la + 64, *reinterpret_cast<uint32_t(*)[32]>(dv));
+            tmem_ld_32x32b_x32(la + 96, *reinterpret_cast<uint32_t(*)[32]>(dv + 32));
             tmem_ld_wait();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&s_empty[bb]);
             const bool interior = j0 + kTcK <= g.t_k && wr0 + 32 <= g.t_q && (!g.causal || j0 + kTcK - 1 <= g.pos_offset + wr0) &&
                                   !(g.self_keep && j0 + kTcK - 1 >= g.pos_offset + wr0);
-            if (t >= 2) mbar_wait(&ds_empty[bb], ((t >> 1) - 1) & 1);
-            unsigned char* drow = dss + bb * kDS + rl * 128;
+            if (t >= 1) mbar_wait(&ds_empty[wg], (t - 1) & 1);  // dQ of tile t-1 done reading dS
+            unsigned char* drow = my_ds + rl * 128;
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
                 uint32_t dw[4];
@@ -779,18 +794,20 @@ __global__ void __launch_bounds__(kBwThreads, 1)
             fence_proxy_async_smem();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&ds_full[bb]);
+            if (lane == 0) mbar_arrive(&ds_full[wg]);
         }
-        if (ntiles > 0) {
-            mbar_wait(acc_done, 0);
+        // the last dQ of this warpgroup has retired once its ds_empty phase completes
+        if (ntw > 1) mbar_wait(&ds_empty[wg], (ntw - 2) & 1);
+        if (ntw > 0) {
+            mbar_wait(&ds_empty[wg], (ntw - 1) & 1);
             tc_fence_after();
         }
-        float* drow = p.dq + (q_row0 + r) * kD;
+        float* drw = p.dq + (q_row0 + r) * kD;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             uint32_t rr[32];
-            if (ntiles > 0) {
-                tmem_ld_32x32b_x32(la + 256 + c * 32, rr);
+            if (ntw > 0) {
+                tmem_ld_32x32b_x32(la + 128 + c * 32, rr);
                 tmem_ld_wait();
             } else {
 #pragma unroll
@@ -799,7 +816,7 @@ __global__ void __launch_bounds__(kBwThreads, 1)
             if (r < g.t_q) {
 #pragma unroll
                 for (int q = 0; q < 8; ++q)
-                    *reinterpret_cast<float4*>(drow + c * 32 + q * 4) =
+                    *reinterpret_cast<float4*>(drw + c * 32 + q * 4) =
                         make_float4(__uint_as_float(rr[q * 4]) * g.scale, __uint_as_float(rr[q * 4 + 1]) * g.scale,
                                     __uint_as_float(rr[q * 4 + 2]) * g.scale, __uint_as_float(rr[q * 4 + 3]) * g.scale);
             }
@@ -807,12 +824,11 @@ __global__ void __launch_bounds__(kBwThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 5) {
+    if (warp == kMmaWarp) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
     }
 }
-
 
 // validate_call (attention.cpp:40-42): every mask value finite and >= 0
 __global__ void mask_check_kernel(const float* __restrict__ mask, int64_t n, ErrWord* err) {
@@ -1054,9 +1070,9 @@ cudaError_t launch_attn_fwd(const AttnParams& p, int dtype, int d, const CUtenso
     return cudaGetLastError();
 }
 
-size_t attn_dq_tc_smem() {
-    return 1024 + 2 * attn::kTcQ * 256 + 2 * 2 * attn::kTcK * 256 + 2 * attn::kTcQ * attn::kTcK * 2 + 4 * attn::kTcK * 4 +
-           16 * 8;
+size_t attn_dq_tc_smem() {  // no alignment slack (see dq_tc_kernel)
+    return 2 * attn::kTcWG * attn::kTcQ * 256 + 2 * 2 * attn::kTcK * 256 + attn::kTcWG * attn::kTcQ * attn::kTcK * 2 +
+           attn::kTcWG * 4 * attn::kTcK * 4 + 16 * 8;
 }
 size_t attn_dkv_tc_smem() {
     return 1024 + 2 * attn::kBwK * 256 + 2 * 2 * attn::kBwQ * 256 + 2 * attn::kBwK * attn::kBwQ * 2 +
@@ -1075,7 +1091,8 @@ cudaError_t launch_attn_bwd(const AttnParams& p, int dtype, int d, const CUtenso
             return e;
         if ((e = cudaFuncSetAttribute(attn::dkv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2)))
             return e;
-        attn::dq_tc_kernel<<<dim3((p.t_q + attn::kTcQ - 1) / attn::kTcQ, p.n_q_heads, p.batch), attn::kBwThreads, s1,
+        constexpr int dq_rows = attn::kTcWG * attn::kTcQ;
+        attn::dq_tc_kernel<<<dim3((p.t_q + dq_rows - 1) / dq_rows, p.n_q_heads, p.batch), attn::kDqThreads, s1,
                              stream>>>(p, m[0], m[1], m[2], m[3]);
         attn::dkv_tc_kernel<<<dim3((p.t_k + attn::kBwK - 1) / attn::kBwK, p.n_kv_heads, p.batch), attn::kBwThreads, s2,
                               stream>>>(p, m[4], m[5], m[6], m[7]);
