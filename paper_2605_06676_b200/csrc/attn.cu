@@ -397,19 +397,19 @@ __global__ void __launch_bounds__(kBwThreads, 1)
     unsigned char* ks = smem;
     unsigned char* vs = ks + kKB128;
     unsigned char* stg = vs + kKB128;          // [2] x {Q, dO}
-    unsigned char* pts = stg + 2 * kStage;     // P^T [128 keys][64 q]
-    unsigned char* dss = pts + kPT;            // dS^T
-    float* cw = reinterpret_cast<float*>(dss + kPT);  // [4 warps][lse 64 | D 64]
+    unsigned char* pts = stg + 2 * kStage;     // [2] P^T [128 keys][64 q]
+    unsigned char* dss = pts + 2 * kPT;        // [2] dS^T
+    float* cw = reinterpret_cast<float*>(dss + 2 * kPT);  // [4 warps][lse 64 | D 64]
     uint64_t* bars = reinterpret_cast<uint64_t*>(cw + 4 * 2 * kBwQ);
     uint64_t* kv_full = bars;
     uint64_t* st_full = bars + 1;    // [2]
     uint64_t* st_empty = bars + 3;   // [2]
     uint64_t* s_full = bars + 5;     // [2]
     uint64_t* s_empty = bars + 7;    // [2]
-    uint64_t* pt_full = bars + 9;
-    uint64_t* pt_empty = bars + 10;
-    uint64_t* acc_done = bars + 11;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+    uint64_t* pt_full = bars + 9;    // [2]
+    uint64_t* pt_empty = bars + 11;  // [2]
+    uint64_t* acc_done = bars + 13;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
 
     const Geo g{p.n_q_heads, p.n_kv_heads, p.n_q_heads / p.n_kv_heads, p.t_q, p.t_k, p.causal, p.pos_offset,
                 p.self_keep, p.scale * kLog2e, p.scale};
@@ -428,8 +428,10 @@ __global__ void __launch_bounds__(kBwThreads, 1)
             mbar_init(&s_full[i], 1);
             mbar_init(&s_empty[i], 4);
         }
-        mbar_init(pt_full, 4);
-        mbar_init(pt_empty, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&pt_full[i], 4);
+            mbar_init(&pt_empty[i], 1);
+        }
         mbar_init(acc_done, 1);
         fence_barrier_init();
     }
@@ -483,19 +485,19 @@ __global__ void __launch_bounds__(kBwThreads, 1)
             issue_s(0);
             for (int t = 0; t < ntiles; ++t) {
                 if (t + 1 < ntiles) issue_s(t + 1);
-                const int st = t & 1;
-                mbar_wait(pt_full, t & 1);
+                const int st = t & 1, pb = t & 1;
+                mbar_wait(&pt_full[pb], (t >> 1) & 1);
                 tc_fence_after();
                 // B = the Q / dO tiles themselves, read MN-major ([queries][d] rows, d contiguous)
                 const uint32_t qb = sa + st * kStage, ub = qb + kT64;
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
-                    umma_bf16(tmem + 256, umma_desc_sw128(pa + kk * 32), umma_desc_sw128_mn(ub + kk * 2048, kBwQ * 128),
-                              id_o, (t > 0 || kk > 0) ? 1u : 0u);
-                    umma_bf16(tmem + 384, umma_desc_sw128(da + kk * 32), umma_desc_sw128_mn(qb + kk * 2048, kBwQ * 128),
-                              id_o, (t > 0 || kk > 0) ? 1u : 0u);
+                    umma_bf16(tmem + 256, umma_desc_sw128(pa + pb * kPT + kk * 32),
+                              umma_desc_sw128_mn(ub + kk * 2048, kBwQ * 128), id_o, (t > 0 || kk > 0) ? 1u : 0u);
+                    umma_bf16(tmem + 384, umma_desc_sw128(da + pb * kPT + kk * 32),
+                              umma_desc_sw128_mn(qb + kk * 2048, kBwQ * 128), id_o, (t > 0 || kk > 0) ? 1u : 0u);
                 }
-                umma_commit(pt_empty);
+                umma_commit(&pt_empty[pb]);
                 umma_commit(&st_empty[st]);
             }
             umma_commit(acc_done);
@@ -540,9 +542,9 @@ __global__ void __launch_bounds__(kBwThreads, 1)
             if (lane == 0) mbar_arrive(&s_empty[bb]);
             const bool interior = jw0 + 32 <= g.t_k && r0 + kBwQ <= g.t_q && (!g.causal || jw0 + 31 <= g.pos_offset + r0) &&
                                   !(g.self_keep && jw0 + 31 >= g.pos_offset + r0);
-            if (t >= 1) mbar_wait(pt_empty, (t - 1) & 1);  // dV / dK of tile t-1 done with P^T, dS^T
-            unsigned char* prow = pts + kr * 128;
-            unsigned char* drow = dss + kr * 128;
+            if (t >= 2) mbar_wait(&pt_empty[bb], ((t >> 1) - 1) & 1);  // dV / dK of tile t-2 done with buffer bb
+            unsigned char* prow = pts + bb * kPT + kr * 128;
+            unsigned char* drow = dss + bb * kPT + kr * 128;
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
                 uint32_t pw[4], dw[4];
@@ -574,7 +576,7 @@ __global__ void __launch_bounds__(kBwThreads, 1)
             fence_proxy_async_smem();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(pt_full);
+            if (lane == 0) mbar_arrive(&pt_full[bb]);
         }
         // ---- epilogue: dV, dK (x scale) rows from TMEM, dmask
         if (ntiles > 0) {
@@ -1075,7 +1077,7 @@ size_t attn_dq_tc_smem() {  // no alignment slack (see dq_tc_kernel)
            attn::kTcWG * 4 * attn::kTcK * 4 + 16 * 8;
 }
 size_t attn_dkv_tc_smem() {
-    return 1024 + 2 * attn::kBwK * 256 + 2 * 2 * attn::kBwQ * 256 + 2 * attn::kBwK * attn::kBwQ * 2 +
+    return 1024 + 2 * attn::kBwK * 256 + 2 * 2 * attn::kBwQ * 256 + 2 * 2 * attn::kBwK * attn::kBwQ * 2 +
            4 * 2 * attn::kBwQ * 4 + 16 * 8;
 }
 
