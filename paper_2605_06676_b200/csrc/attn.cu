@@ -701,25 +701,28 @@ __global__ void __launch_bounds__(kDqThreads, 1)
             constexpr uint32_t id_s = umma_idesc_bf16(kTcQ, kTcK), id_o_mn = umma_idesc_bf16_bmn(kTcQ, kD);
             const uint32_t sa = smem_u32(stg), da = smem_u32(dss);
             mbar_wait(q_full, 0);
+            auto issue_s = [&](int w, int t) {  // S = Q K^T and dP = dO V^T of warpgroup w, tile t
+                const uint32_t kb = sa + (t & 1) * kStage, vb = kb + kT64;
+                const uint32_t qa = smem_u32(qs + w * kQ128), ua = smem_u32(us + w * kQ128);
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t ao = (kk >> 2) * (kTcQ * 128) + (kk & 3) * 32, bo = (kk >> 2) * (kTcK * 128) + (kk & 3) * 32;
+                    umma_bf16(tmem + w * 256, umma_desc_sw128(qa + ao), umma_desc_sw128(kb + bo), id_s, kk > 0);
+                    umma_bf16(tmem + w * 256 + 64, umma_desc_sw128(ua + ao), umma_desc_sw128(vb + bo), id_s, kk > 0);
+                }
+                umma_commit(&s_full[w]);
+            };
+            mbar_wait(&st_full[0], 0);
+            tc_fence_after();
+#pragma unroll
+            for (int w = 0; w < kTcWG; ++w)
+                if (nt[w] > 0) issue_s(w, 0);
             for (int t = 0; t < n_all; ++t) {
                 const int st = t & 1;
-                mbar_wait(&st_full[st], (t >> 1) & 1);
-                tc_fence_after();
-                const uint32_t kb = sa + st * kStage, vb = kb + kT64;
-                // S, dP of both warpgroups (their previous S / dP were consumed before ds_full)
-#pragma unroll
-                for (int w = 0; w < kTcWG; ++w) {
-                    if (t >= nt[w]) continue;
-                    const uint32_t qa = smem_u32(qs + w * kQ128), ua = smem_u32(us + w * kQ128);
-#pragma unroll
-                    for (int kk = 0; kk < 8; ++kk) {
-                        const uint32_t ao = (kk >> 2) * (kTcQ * 128) + (kk & 3) * 32, bo = (kk >> 2) * (kTcK * 128) + (kk & 3) * 32;
-                        umma_bf16(tmem + w * 256, umma_desc_sw128(qa + ao), umma_desc_sw128(kb + bo), id_s, kk > 0);
-                        umma_bf16(tmem + w * 256 + 64, umma_desc_sw128(ua + ao), umma_desc_sw128(vb + bo), id_s, kk > 0);
-                    }
-                    umma_commit(&s_full[w]);
-                }
-                // dQ += dS K (B = the K tile read MN-major)
+                const uint32_t kb = sa + st * kStage;
+                bool next_ready = false;
+                // per warpgroup: dQ of tile t as soon as its dS lands, then at once its S / dP of tile
+                // t + 1, so each warpgroup's row math overlaps the other's MMAs
 #pragma unroll
                 for (int w = 0; w < kTcWG; ++w) {
                     if (t >= nt[w]) continue;
@@ -730,6 +733,14 @@ __global__ void __launch_bounds__(kDqThreads, 1)
                         umma_bf16(tmem + w * 256 + 128, umma_desc_sw128(da + w * kDS + kk * 32),
                                   umma_desc_sw128_mn(kb + kk * 2048, kTcK * 128), id_o_mn, (t > 0 || kk > 0) ? 1u : 0u);
                     umma_commit(&ds_empty[w]);
+                    if (t + 1 < nt[w]) {
+                        if (!next_ready) {
+                            mbar_wait(&st_full[(t + 1) & 1], ((t + 1) >> 1) & 1);
+                            tc_fence_after();
+                            next_ready = true;
+                        }
+                        issue_s(w, t + 1);
+                    }
                 }
                 umma_commit(&st_empty[st]);
             }
