@@ -79,3 +79,31 @@ def test_error_classes_mirror_reference():
     r = lkv.kv_memory_bytes(retention=1.0)
     assert r["full_bytes"] == pytest.approx(26214400000.0)  # test_evictsim.cpp:45-49
     assert abs(lkv.kv_memory_bytes(retention=0.15)["reduction_factor"] - 6.67) < 0.01
+
+
+def test_host_validation_of_row4_and_comm_entry_points():
+    """Host-side contract checks of the training / multi-GPU entry points (no device work)."""
+    L = lkv.lib()
+    # soft_topk_forward: tau must be positive (soft_topk.cpp:112), scores non-empty (:114)
+    assert L.lkv_soft_topk_fwd(None, None, 0.0, 1, 8, 8, None, 0.0, None, None, None, None, None, 0, None) == _abi.CONTRACT
+    assert L.lkv_soft_topk_fwd(None, None, 0.0, 1, 0, 8, None, 1.0, None, None, None, None, None, 0, None) == _abi.CONTRACT
+    assert L.lkv_soft_topk_vjp(None, None, 1, 8, 8, -1.0, None, None, None) == _abi.CONTRACT
+    # masked attention: empty extents / first row admits no key (attention.cpp:34,43) / GQA ratio
+    a = _abi.AttnDesc(1, 4, 1, 16, 16, 128, 1, 1, -1, 0, 0.1)
+    assert L.lkv_attn_workspace_bytes(C.byref(a)) == 0
+    assert L.lkv_masked_attention_fwd(C.byref(a), None, None, None, None, None, None, None, 0, None) == _abi.CONTRACT
+    a = _abi.AttnDesc(1, 3, 2, 16, 16, 128, 1, 1, 0, 0, 0.1)
+    assert L.lkv_masked_attention_fwd(C.byref(a), None, None, None, None, None, None, None, 0, None) == _abi.CONTRACT
+    a = _abi.AttnDesc(1, 4, 1, 16, 16, 64, 1, 1, 0, 0, 0.1)  # bf16 needs head_dim 128
+    assert L.lkv_masked_attention_fwd(C.byref(a), None, None, None, None, None, None, None, 0, None) == _abi.UNSUPPORTED
+    a = _abi.AttnDesc(2, 8, 2, 100, 300, 128, 1, 1, 0, 0, 0.1)
+    assert L.lkv_attn_workspace_bytes(C.byref(a)) >= 256 + 2 * 8 * 100 * 4
+    # NCCL communicator: rank outside [0, n_ranks)
+    h = C.c_void_p()
+    assert L.lkv_comm_init(C.byref(h), C.create_string_buffer(128), 2, 2) == _abi.CONTRACT
+    assert L.lkv_comm_size(None) == 0 and L.lkv_comm_rank(None) == -1
+    # head shard: the shard's heads must lie inside the global logit vector
+    lens = (C.c_int32 * 1)(100)
+    cd = _abi.CacheDesc(1, 4, 8, 128, 100, 1, 0, C.c_void_p(256), C.c_void_p(256), C.cast(lens, C.POINTER(C.c_int32)))
+    assert L.lkv_evict_shard(C.byref(cd), None, None, 32, 8, 0.15, 1, None, None, None, None, None, 0, None) == _abi.CONTRACT
+    assert L.lkv_ragged_capacity_shard(C.byref(cd), 64, 0.15, 2) > 0
