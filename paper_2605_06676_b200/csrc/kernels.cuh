@@ -191,6 +191,7 @@ enum GemvEpi { EPI_QKV = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_F32 = 3 };
 struct GemvParams {
     const void* w;       // bf16: packed 64-col x 128-k units [NG][KU]; f32: row-major [K][NG * 64]
     int32_t NG, KU;      // column groups of 64, k-units of 128
+    int32_t split;       // > 0: cluster split-K (split CTAs per column group, DSMEM reduction)
     int32_t N, K;        // real output columns (virtual order) / reduction length
     int32_t B, nbt;      // batch rows, 8-row batch tiles of the packed activations
     const void* act;     // bf16: packed (act_index), K padded to KU * 128; f32: row-major [B][K]

@@ -28,6 +28,8 @@
 // same virtual column order and the same epilogues.
 #include <math.h>
 
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace lkv_dev {
@@ -47,6 +49,9 @@ constexpr int kWsThreads = (kWsConsumers + 1) * 32;
 constexpr int kWsPerSm = LKV_WS_PER_SM;
 constexpr int kYPad = 17;                      // y[64][17]: columns x batch (B <= 16)
 constexpr int kWsMaxSplit = 1024;              // CTAs sharing one column group (<= KU + 1; K <= 130k)
+#ifndef LKV_GEMV_SPLIT
+#define LKV_GEMV_SPLIT 1  // cluster split-K for narrow matrices (0: stream-K everywhere, for A/B)
+#endif
 #ifndef LKV_GEMV_EXPT
 #define LKV_GEMV_EXPT 0  // profiles/gemv_bench.cu bisection knobs: 1 no mma, 2 no fix-up, 4 no epilogue, 8 trace
 #endif
@@ -154,7 +159,11 @@ __device__ void gemv_epilogue(const GemvParams& p, int ng, float (*y)[kYPad], in
 __host__ __device__ __forceinline__ int64_t unit_begin(int c, int64_t U, int P) { return (int64_t)c * U / P; }
 __device__ __forceinline__ int unit_owner(int64_t u, int64_t U, int P) { return (int)(((u + 1) * P - 1) / U); }
 
-template <int NBT>
+// SPLIT: narrow matrices (few column groups) run split-K instead of stream-K: each column group is
+// cut into p.split equal k-ranges, one CTA each, forming a thread-block cluster; the partial
+// products are summed by the cluster's rank-0 CTA straight from its peers' shared memory (DSMEM),
+// in rank order (deterministic), instead of the stream-K global partials + arrival counter.
+template <int NBT, bool SPLIT>
 __global__ void __launch_bounds__(kWsThreads, kWsPerSm) wstream_gemv_kernel(const __grid_constant__ GemvParams p) {
     constexpr int kActBytes = 8 * NBT * 256;  // 8 k16 steps x NBT tiles x 32 lanes x 8 B
     constexpr int kStage = kWsUnitBytes + kActBytes;
@@ -171,7 +180,17 @@ __global__ void __launch_bounds__(kWsThreads, kWsPerSm) wstream_gemv_kernel(cons
     GTRACE(5);
     const int64_t U = (int64_t)p.NG * p.KU;
     const int P = gridDim.x, c = blockIdx.x;
-    const int64_t u0 = unit_begin(c, U, P), u1 = unit_begin(c + 1, U, P);
+    int64_t u0, u1;
+    int rank = 0;
+    if constexpr (SPLIT) {
+        const int S = p.split, ng = c / S;
+        rank = c - ng * S;  // == %cluster_ctarank (clusters of S consecutive CTAs)
+        u0 = (int64_t)ng * p.KU + (int64_t)rank * p.KU / S;
+        u1 = (int64_t)ng * p.KU + (int64_t)(rank + 1) * p.KU / S;
+    } else {
+        u0 = unit_begin(c, U, P);
+        u1 = unit_begin(c + 1, U, P);
+    }
     if (threadIdx.x == 0) {
         for (int i = 0; i < kWsStages; ++i) {
             mbar_init(&full[i], 1);
@@ -214,8 +233,8 @@ __global__ void __launch_bounds__(kWsThreads, kWsPerSm) wstream_gemv_kernel(cons
                 }
             }
         }
-        return;
-    }
+        if constexpr (!SPLIT) return;
+    } else {
 
     // ===================== consumers =====================
     pdl_wait();
@@ -284,6 +303,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsPerSm) wstream_gemv_kernel(cons
             y[n][b] = v;
         }
         named_sync(1, kWsConsumers * 32);
+        if constexpr (SPLIT) break;  // one column group per CTA: reduced across the cluster below
         if (!whole && !(LKV_GEMV_EXPT & 2)) {
             // stream-K fix-up: partial -> global slot; the last CTA of the group sums in CTA order
             const int slot = 2 * c + (ng == ng_first ? 0 : 1);
@@ -337,6 +357,25 @@ __global__ void __launch_bounds__(kWsThreads, kWsPerSm) wstream_gemv_kernel(cons
         if (!(LKV_GEMV_EXPT & 4)) gemv_epilogue<__nv_bfloat16>(p, ng, y, tid, kWsConsumers * 32);
         named_sync(1, kWsConsumers * 32);
         GTRACE(4);
+    }
+    }  // consumers
+    if constexpr (SPLIT) {
+        // every thread of every CTA in the cluster (the producer warp too) joins both barriers
+        cluster_sync_all();
+        const int S = p.split;
+        if (rank == 0 && warp < kWsConsumers) {
+            const int tid = threadIdx.x;
+            const uint32_t ybase = smem_u32(&y[0][0]);
+            for (int e = tid; e < kWsCols * 16; e += kWsConsumers * 32) {
+                const int n = e >> 4, b = e & 15;
+                float v = y[n][b];
+                for (int r = 1; r < S; ++r) v += dsmem_ld(dsmem_map(ybase + (uint32_t)(n * kYPad + b) * 4u, r));
+                y[n][b] = v;
+            }
+            named_sync(1, kWsConsumers * 32);
+            gemv_epilogue<__nv_bfloat16>(p, c / S, y, tid, kWsConsumers * 32);
+        }
+        cluster_sync_all();  // peers stay resident until rank 0 has read their partials
     }
 }
 
@@ -459,9 +498,24 @@ cudaError_t launch_gemv(const GemvParams& p, int dtype, int num_sms, cudaStream_
     if (dtype == LKV_BF16) {
         const int64_t U = (int64_t)p.NG * p.KU;
         const int64_t cap = (int64_t)kWsPerSm * num_sms;
-        const int grid = (int)(U < cap ? U : cap);
         const size_t smem = wstream_smem(p.nbt);
-        auto kern = p.nbt == 1 ? wstream_gemv_kernel<1> : wstream_gemv_kernel<2>;
+        // narrow matrices: cluster split-K with S CTAs per column group, S a power of two <= 8, used
+        // when the NG * S CTAs still fill >= 80% of the one-wave slots (measured: Wo / down at S = 4
+        // beat stream-K; QKV at S = 3 was slower, odd cluster sizes pack poorly)
+        int S = 1;
+        while (S < 8 && (int64_t)p.NG * S * 2 <= cap && S * 2 <= p.KU) S *= 2;
+        if (S >= 2 && (int64_t)p.NG * S * 5 >= cap * 4 && LKV_GEMV_SPLIT) {
+            GemvParams q = p;
+            q.split = S;
+            auto kern = q.nbt == 1 ? wstream_gemv_kernel<1, true> : wstream_gemv_kernel<2, true>;
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            e = launch_pdl_cluster(kern, dim3(q.NG * S), dim3(kWsThreads), smem, stream, S, q);
+            note_launches(1);
+            return e;
+        }
+        const int grid = (int)(U < cap ? U : cap);
+        auto kern = p.nbt == 1 ? wstream_gemv_kernel<1, false> : wstream_gemv_kernel<2, false>;
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         e = launch_pdl(kern, dim3(grid), dim3(kWsThreads), smem, stream, p);

@@ -86,10 +86,10 @@ int main(int argc, char** argv) {
         const int64_t U = (int64_t)NG * KU;
         const int grid = (int)(U < 2 * sms ? U : 2 * sms);
         const size_t smem = wstream_smem(1);
-        CK(cudaFuncSetAttribute(wstream_gemv_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute(wstream_gemv_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         auto launch = [&]() {
             if (mode == 0) CK(launch_gemv(p, LKV_BF16, sms, s));
-            else wstream_gemv_kernel<1><<<grid, kWsThreads, smem, s>>>(p);
+            else wstream_gemv_kernel<1, false><<<grid, kWsThreads, smem, s>>>(p);
         };
         cudaEvent_t e0, e1;
         CK(cudaEventCreate(&e0));
