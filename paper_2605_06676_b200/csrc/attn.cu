@@ -183,10 +183,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             for (int w = 0; w < kTcWG; ++w) tma_tile<kTcQ>(qs + w * kQBytes, &tq, q_full, (int)(q_row0 + q0 + w * kTcQ), pol);
             for (int t = 0; t < n_all; ++t) {
                 const int st = t % kTcStages;
-                if (t >= kTcStages) mbar_wait(&k_empty[st], ((t / kTcStages) - 1) & 1);
+                if (t >= kTcStages) mbar_wait_backoff(&k_empty[st], ((t / kTcStages) - 1) & 1);
                 mbar_arrive_expect_tx(&k_full[st], kKBytes);
                 tma_tile<kTcK>(ks + st * kKBytes, &tk, &k_full[st], (int)(kv_row0 + t * kTcK), pol);
-                if (t >= kTcStages) mbar_wait(&v_empty[st], ((t / kTcStages) - 1) & 1);
+                if (t >= kTcStages) mbar_wait_backoff(&v_empty[st], ((t / kTcStages) - 1) & 1);
                 mbar_arrive_expect_tx(&v_full[st], kVBytes);
                 tma_tile<kTcK>(vs + st * kVBytes, &tv, &v_full[st], (int)(kv_row0 + t * kTcK), pol);
             }
@@ -196,14 +196,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (lane == 0) {
             constexpr uint32_t idesc_s = umma_idesc_bf16(kTcQ, kTcK), idesc_o = umma_idesc_bf16_bmn(kTcQ, kD);
             const uint32_t qa = smem_u32(qs), ka = smem_u32(ks), va = smem_u32(vs), pa = smem_u32(ps);
-            mbar_wait(q_full, 0);
+            mbar_wait_backoff(q_full, 0);
             auto issue_s = [&](int t) {
                 const int st = t % kTcStages, bb = t & 1;
-                mbar_wait(&k_full[st], (t / kTcStages) & 1);
+                mbar_wait_backoff(&k_full[st], (t / kTcStages) & 1);
 #pragma unroll
                 for (int w = 0; w < kTcWG; ++w) {
                     if (t >= nt[w]) continue;
-                    if (t >= 2) mbar_wait(&s_empty[w * 2 + bb], ((t >> 1) - 1) & 1);
+                    if (t >= 2) mbar_wait_backoff(&s_empty[w * 2 + bb], ((t >> 1) - 1) & 1);
                     tc_fence_after();
 #pragma unroll
                     for (int kk = 0; kk < 8; ++kk) {
@@ -219,11 +219,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             for (int t = 0; t < n_all; ++t) {
                 if (t + 1 < n_all) issue_s(t + 1);
                 const int st = t % kTcStages, bb = t & 1;
-                mbar_wait(&v_full[st], (t / kTcStages) & 1);
+                mbar_wait_backoff(&v_full[st], (t / kTcStages) & 1);
 #pragma unroll
                 for (int w = 0; w < kTcWG; ++w) {
                     if (t >= nt[w]) continue;
-                    mbar_wait(&p_full[w * 2 + bb], (t >> 1) & 1);
+                    mbar_wait_backoff(&p_full[w * 2 + bb], (t >> 1) & 1);
                     tc_fence_after();
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(kBwThreads, 1)
             tma_tile<kBwK>(vs, &tv128, kv_full, (int)(kv_row0 + k0), pol);
             for (int t = 0; t < ntiles; ++t) {
                 const int st = t & 1;
-                if (t >= 2) mbar_wait(&st_empty[st], ((t >> 1) - 1) & 1);
+                if (t >= 2) mbar_wait_backoff(&st_empty[st], ((t >> 1) - 1) & 1);
                 mbar_arrive_expect_tx(&st_full[st], kStage);
                 unsigned char* d = stg + st * kStage;
                 const int hq = head_of(t), r0 = qtile_of(t) * kBwQ;
@@ -467,11 +467,11 @@ __global__ void __launch_bounds__(kBwThreads, 1)
             constexpr uint32_t id_s = umma_idesc_bf16(kBwK, kBwQ), id_o = umma_idesc_bf16_bmn(kBwK, kD);
             const uint32_t ka = smem_u32(ks), va = smem_u32(vs), sa = smem_u32(stg), pa = smem_u32(pts),
                            da = smem_u32(dss);
-            mbar_wait(kv_full, 0);
+            mbar_wait_backoff(kv_full, 0);
             auto issue_s = [&](int t) {
                 const int st = t & 1, bb = t & 1;
-                mbar_wait(&st_full[st], (t >> 1) & 1);
-                if (t >= 2) mbar_wait(&s_empty[bb], ((t >> 1) - 1) & 1);
+                mbar_wait_backoff(&st_full[st], (t >> 1) & 1);
+                if (t >= 2) mbar_wait_backoff(&s_empty[bb], ((t >> 1) - 1) & 1);
                 tc_fence_after();
                 const uint32_t qb = sa + st * kStage, ub = qb + kT64;
 #pragma unroll
@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(kBwThreads, 1)
             for (int t = 0; t < ntiles; ++t) {
                 if (t + 1 < ntiles) issue_s(t + 1);
                 const int st = t & 1, pb = t & 1;
-                mbar_wait(&pt_full[pb], (t >> 1) & 1);
+                mbar_wait_backoff(&pt_full[pb], (t >> 1) & 1);
                 tc_fence_after();
                 // B = the Q / dO tiles themselves, read MN-major ([queries][d] rows, d contiguous)
                 const uint32_t qb = sa + st * kStage, ub = qb + kT64;
@@ -689,7 +689,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
             }
             for (int t = 0; t < n_all; ++t) {
                 const int st = t & 1;
-                if (t >= 2) mbar_wait(&st_empty[st], ((t >> 1) - 1) & 1);
+                if (t >= 2) mbar_wait_backoff(&st_empty[st], ((t >> 1) - 1) & 1);
                 mbar_arrive_expect_tx(&st_full[st], kStage);
                 unsigned char* d = stg + st * kStage;
                 tma_tile<kTcK>(d, &tk64, &st_full[st], (int)(kv_row0 + t * kTcK), pol);
@@ -700,7 +700,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         if (lane == 0 && n_all > 0) {
             constexpr uint32_t id_s = umma_idesc_bf16(kTcQ, kTcK), id_o_mn = umma_idesc_bf16_bmn(kTcQ, kD);
             const uint32_t sa = smem_u32(stg), da = smem_u32(dss);
-            mbar_wait(q_full, 0);
+            mbar_wait_backoff(q_full, 0);
             auto issue_s = [&](int w, int t) {  // S = Q K^T and dP = dO V^T of warpgroup w, tile t
                 const uint32_t kb = sa + (t & 1) * kStage, vb = kb + kT64;
                 const uint32_t qa = smem_u32(qs + w * kQ128), ua = smem_u32(us + w * kQ128);
@@ -712,7 +712,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
                 }
                 umma_commit(&s_full[w]);
             };
-            mbar_wait(&st_full[0], 0);
+            mbar_wait_backoff(&st_full[0], 0);
             tc_fence_after();
 #pragma unroll
             for (int w = 0; w < kTcWG; ++w)
@@ -726,7 +726,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
 #pragma unroll
                 for (int w = 0; w < kTcWG; ++w) {
                     if (t >= nt[w]) continue;
-                    mbar_wait(&ds_full[w], t & 1);
+                    mbar_wait_backoff(&ds_full[w], t & 1);
                     tc_fence_after();
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk)
@@ -735,7 +735,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
                     umma_commit(&ds_empty[w]);
                     if (t + 1 < nt[w]) {
                         if (!next_ready) {
-                            mbar_wait(&st_full[(t + 1) & 1], ((t + 1) >> 1) & 1);
+                            mbar_wait_backoff(&st_full[(t + 1) & 1], ((t + 1) >> 1) & 1);
                             tc_fence_after();
                             next_ready = true;
                         }

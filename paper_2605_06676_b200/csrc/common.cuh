@@ -90,6 +90,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     while (!mbar_try_wait(a, parity)) {
     }
 }
+// For single-thread roles (TMA producer, MMA issuer) that are usually AHEAD of the warps they
+// feed: back off between polls so the spin does not take issue slots from the math warps that
+// share the SM sub-partition.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    while (!mbar_try_wait(a, parity)) __nanosleep(64);
+}
 
 // ---- TMA ------------------------------------------------------------------------
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* m) {
