@@ -159,6 +159,45 @@ LkvParams load_lkv_params(const std::string& path);
 // policy.cpp:106-108 -- the LKV-H logits (fp64 host setup, once per checkpoint)
 std::vector<double> head_scores(const LkvParams& params);
 
+// ---- training-time operators -----------------------------------------------
+// soft_topk.hpp:36-44 / :60-67 -- values sum to the clamped k; the saved density terms feed the VJP.
+struct SoftTopKOutput {
+    std::vector<double> values;
+    std::vector<double> density_terms;
+    double threshold_lambda = 0.0;
+    double clamped_k = 0.0;
+    double tau = 1.0;
+};
+SoftTopKOutput soft_topk_forward(std::span<const double> x, double k, double tau);
+std::pair<std::vector<double>, double> soft_topk_vjp(const SoftTopKOutput& saved, std::span<const double> upstream,
+                                                     double tau);
+// training_mask (policy.cpp:138-150) with the Gumbel noise supplied (scores + noise_scale * noise)
+SoftTopKOutput training_mask(std::span<const double> u, double b_continuous, double tau,
+                             std::span<const double> gumbel_noise, double noise_scale);
+
+// attention.hpp:20-74 -- one head; the saved state is the device form (log2 masked LSE and the
+// output the backward's D = rowsum(dO * O) reads) instead of the reference's p_raw / p matrices.
+struct AttentionCall {
+    int n_q = 0, t = 0, d = 0;
+    std::vector<double> queries, keys, values, soft_mask;  // soft_mask empty = all ones
+    bool causal = true;
+    double scale = 0.0;
+    int query_pos_offset = 0;
+    bool self_always_retained = false;
+};
+struct AttentionSaved {
+    std::vector<float> lse;     // [n_q], log2 domain
+    std::vector<double> out;    // [n_q x d] as computed on the device (rounded to the compute dtype)
+    Precision prec = Precision::fp32;
+};
+struct AttentionGrads {
+    std::vector<double> queries, keys, values, soft_mask;  // soft_mask empty when the call had none
+};
+std::vector<double> masked_attention_dense(const AttentionCall& call, AttentionSaved* saved = nullptr,
+                                           Precision prec = Precision::fp32);
+AttentionGrads masked_attention_vjp(const AttentionCall& call, const AttentionSaved& saved,
+                                    const std::vector<double>& upstream);
+
 // Throws device_error unless an sm_100 (B200) device is current.
 void require_b200();
 

@@ -10,6 +10,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -446,6 +447,116 @@ std::vector<double> decode_attention(KvCache& cache, std::span<const double> q, 
     }
     cache.tokens_seen += 1;
     return out;
+}
+
+// ---- soft_topk.cpp:111-189 (training) ---------------------------------------------------
+static SoftTopKOutput soft_topk_impl(std::span<const double> x, double k, double tau, std::span<const double> noise,
+                                     double noise_scale) {
+    if (!(tau > 0.0)) throw contract_error("soft_topk_forward: tau must be positive");  // soft_topk.cpp:112
+    const int n = (int)x.size();
+    if (n < 1) throw contract_error("soft_topk_forward: empty scores");  // :114
+    Dev X = upload(x.data(), x.size()), K = upload(&k, 1);
+    Dev N = noise.empty() ? Dev() : upload(noise.data(), noise.size());
+    if (!noise.empty() && (int)noise.size() != n) throw contract_error("training_mask: noise length must equal t");
+    Dev VAL(sizeof(double) * n), DEN(sizeof(double) * n), LAM(sizeof(double));
+    Workspace ws(256);
+    check(lkv_soft_topk_fwd(X.as<double>(), noise.empty() ? nullptr : N.as<double>(), noise_scale, 1, n, n,
+                            K.as<double>(), tau, VAL.as<double>(), DEN.as<double>(), nullptr, LAM.as<double>(), ws.ptr(),
+                            ws.bytes, (lkv_stream_t)stream()),
+          "soft_topk_forward");
+    ws.status("soft_topk_forward");
+    SoftTopKOutput out;
+    out.values = download<double>(VAL, n);
+    out.density_terms = download<double>(DEN, n);
+    out.threshold_lambda = download<double>(LAM, 1)[0];
+    const double eps = std::min(1e-3, 0.01 * n);  // clamp_budget (soft_topk.cpp:27-33)
+    out.clamped_k = std::min(std::max(k, eps), n - eps);
+    out.tau = tau;
+    return out;
+}
+
+SoftTopKOutput soft_topk_forward(std::span<const double> x, double k, double tau) {
+    return soft_topk_impl(x, k, tau, {}, 0.0);
+}
+
+SoftTopKOutput training_mask(std::span<const double> u, double b_continuous, double tau,
+                             std::span<const double> gumbel_noise, double noise_scale) {
+    return soft_topk_impl(u, b_continuous, tau, gumbel_noise, noise_scale);
+}
+
+std::pair<std::vector<double>, double> soft_topk_vjp(const SoftTopKOutput& saved, std::span<const double> upstream,
+                                                     double tau) {
+    const size_t n = saved.values.size();
+    if (upstream.size() != n) throw contract_error("soft_topk_vjp: upstream length mismatch");  // :170
+    if (!(tau > 0.0)) throw contract_error("soft_topk_vjp: tau must be positive");             // :171
+    Dev D = upload(saved.density_terms.data(), n), U = upload(upstream.data(), n);
+    Dev GX(sizeof(double) * n), GK(sizeof(double));
+    check(lkv_soft_topk_vjp(D.as<double>(), U.as<double>(), 1, (int)n, (int64_t)n, tau, GX.as<double>(), GK.as<double>(),
+                            (lkv_stream_t)stream()),
+          "soft_topk_vjp");
+    return {download<double>(GX, n), download<double>(GK, 1)[0]};
+}
+
+// ---- attention.cpp:46-201 (training) ---------------------------------------------------
+static lkv_attn_desc attn_desc(const AttentionCall& c, Precision prec) {
+    if (c.n_q < 1 || c.t < 1 || c.d < 1) throw contract_error("attention: empty extents");  // attention.cpp:34
+    if (c.queries.size() != (size_t)c.n_q * c.d) throw contract_error("attention: query size");
+    if (c.keys.size() != (size_t)c.t * c.d) throw contract_error("attention: key size");
+    if (c.values.size() != (size_t)c.t * c.d) throw contract_error("attention: value size");
+    if (!c.soft_mask.empty() && c.soft_mask.size() != (size_t)c.t) throw contract_error("attention: mask length must equal t");
+    return lkv_attn_desc{1, 1, 1, c.n_q, c.t, c.d, dtype_of(prec), c.causal ? 1 : 0, c.query_pos_offset,
+                         c.self_always_retained ? 1 : 0, c.scale};
+}
+
+std::vector<double> masked_attention_dense(const AttentionCall& call, AttentionSaved* saved, Precision prec) {
+    lkv_attn_desc a = attn_desc(call, prec);
+    Dev Q = upload_elems(call.queries, prec), K = upload_elems(call.keys, prec), V = upload_elems(call.values, prec);
+    std::vector<float> m(call.soft_mask.begin(), call.soft_mask.end());
+    Dev M = m.empty() ? Dev() : upload(m.data(), m.size());
+    Dev OUT(esize(prec) * call.queries.size()), LSE(sizeof(float) * call.n_q);
+    const size_t wsb = lkv_attn_workspace_bytes(&a);
+    if (wsb == 0) check(lkv_masked_attention_fwd(&a, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, nullptr),
+                        "masked_attention_dense");
+    Workspace ws(wsb);
+    check(lkv_masked_attention_fwd(&a, Q.p, K.p, V.p, m.empty() ? nullptr : M.as<float>(), OUT.p, LSE.as<float>(), ws.ptr(),
+                                   ws.bytes, (lkv_stream_t)stream()),
+          "masked_attention_dense");
+    ws.status("masked_attention_dense");
+    auto out = download_elems(OUT, call.queries.size(), 0, prec);
+    if (saved) {
+        saved->lse = download<float>(LSE, call.n_q);
+        saved->out = out;
+        saved->prec = prec;
+    }
+    return out;
+}
+
+AttentionGrads masked_attention_vjp(const AttentionCall& call, const AttentionSaved& saved,
+                                    const std::vector<double>& upstream) {
+    const Precision prec = saved.prec;
+    lkv_attn_desc a = attn_desc(call, prec);
+    if (upstream.size() != (size_t)call.n_q * call.d) throw contract_error("attention vjp: upstream size");
+    if (saved.lse.size() != (size_t)call.n_q || saved.out.size() != upstream.size())
+        throw contract_error("attention vjp: stale saved state");
+    Dev Q = upload_elems(call.queries, prec), K = upload_elems(call.keys, prec), V = upload_elems(call.values, prec);
+    std::vector<float> m(call.soft_mask.begin(), call.soft_mask.end());
+    Dev M = m.empty() ? Dev() : upload(m.data(), m.size());
+    Dev O = upload_elems(saved.out, prec), U = upload_elems(upstream, prec), LSE = upload(saved.lse.data(), saved.lse.size());
+    Dev DQ(sizeof(float) * call.queries.size()), DK(sizeof(float) * call.keys.size()), DV(sizeof(float) * call.values.size());
+    Dev DM(sizeof(float) * (m.empty() ? 1 : m.size()));
+    Workspace ws(lkv_attn_workspace_bytes(&a));
+    check(lkv_masked_attention_bwd(&a, Q.p, K.p, V.p, m.empty() ? nullptr : M.as<float>(), O.p, LSE.as<float>(), U.p,
+                                   DQ.as<float>(), DK.as<float>(), DV.as<float>(), m.empty() ? nullptr : DM.as<float>(),
+                                   ws.ptr(), ws.bytes, (lkv_stream_t)stream()),
+          "masked_attention_vjp");
+    ws.status("masked_attention_vjp");
+    auto widen = [](const std::vector<float>& f) { return std::vector<double>(f.begin(), f.end()); };
+    AttentionGrads g;
+    g.queries = widen(download<float>(DQ, call.queries.size()));
+    g.keys = widen(download<float>(DK, call.keys.size()));
+    g.values = widen(download<float>(DV, call.values.size()));
+    if (!m.empty()) g.soft_mask = widen(download<float>(DM, m.size()));
+    return g;
 }
 
 // ---- checkpoint.cpp:68-86 / container.cpp:92-137 --------------------------------------------------------

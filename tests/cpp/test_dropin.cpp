@@ -1,6 +1,9 @@
 // C++ drop-in tests: the reference's own hot-path test expectations (proj/tests/*.cpp)
 // exercised through lkv::b200:: (include/lkv_b200_dropin.hpp) on the B200.
 // Built by `make -C paper_2605_06676_b200 test_dropin`; run by tests/test_dropin_cpp.py.
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
 #include <cmath>
 #include <cstdio>
 #include <random>
@@ -42,6 +45,16 @@ static std::vector<double> uniform(size_t n, double lo, double hi, unsigned seed
 }
 
 static double f32(double x) { return (double)(float)x; }
+
+// round to bf16 (nearest even), as the device sees bf16 inputs
+static double bf16(double x) {
+    float f = (float)x;
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    u = (u + 0x7fffu + ((u >> 16) & 1u)) & 0xffff0000u;
+    std::memcpy(&f, &u, 4);
+    return (double)f;
+}
 
 static Mlp2 make_mlp(int in, int hidden, unsigned seed) {
     Mlp2 m;
@@ -293,6 +306,180 @@ static void test_checkpoint(const char* dir) {  // the reference's own lkv_param
     CHECK_THROWS_AS(load_lkv_params(base + "/does_not_exist.bin"), contract_error);
 }
 
+static void test_soft_topk_training() {
+    // test_soft_topk.cpp:36-41: four equal scores, k = 1 -> lambda = ln 2
+    std::vector<double> z(4, 0.0);
+    auto o = soft_topk_forward(z, 1.0, 1.0);
+    CHECK(std::fabs(o.threshold_lambda - std::log(2.0)) <= 1e-12);
+    for (double v : o.values) CHECK(std::fabs(v - 0.25) <= 1e-12);
+    // :43-50: (2, 1, 0) with k = 1.5 -> lambda = 1
+    std::vector<double> x{2.0, 1.0, 0.0};
+    o = soft_topk_forward(x, 1.5, 1.0);
+    CHECK(std::fabs(o.threshold_lambda - 1.0) <= 1e-12);
+    double sum = 0.0;
+    for (double v : o.values) sum += v;
+    CHECK(std::fabs(sum - 1.5) <= 1e-9 * 3);
+    // :129-136: unit upstream -> exactly zero score gradient and unit budget gradient
+    auto r = uniform(11, -3.0, 3.0, 55);
+    o = soft_topk_forward(r, 4.2, 0.7);
+    std::vector<double> ones(11, 1.0);
+    auto [gx, gk] = soft_topk_vjp(o, ones, 0.7);
+    for (double g : gx) CHECK(g == 0.0);
+    CHECK(gk == 1.0);
+    // :138-170: vjp vs central differences of <u, values>
+    auto u = uniform(11, -1.0, 1.0, 72);
+    auto [gx2, gk2] = soft_topk_vjp(o, u, 0.7);
+    for (int i : {0, 5, 10}) {
+        auto xp = r, xm = r;
+        xp[(size_t)i] += 1e-5;
+        xm[(size_t)i] -= 1e-5;
+        auto vp = soft_topk_forward(xp, 4.2, 0.7).values, vm = soft_topk_forward(xm, 4.2, 0.7).values;
+        double fd = 0.0;
+        for (size_t j = 0; j < 11; ++j) fd += u[j] * (vp[j] - vm[j]) / 2e-5;
+        CHECK(std::fabs(fd - gx2[(size_t)i]) <= 1e-6 * (1.0 + std::fabs(fd)));
+    }
+    // :180-188: n = 1 pins the value to k; vjp (0, 1)
+    std::vector<double> one{0.3};
+    o = soft_topk_forward(one, 0.4, 1.0);
+    CHECK(std::fabs(o.values[0] - 0.4) <= 1e-15);
+    std::vector<double> up{2.0};
+    auto [g1, k1] = soft_topk_vjp(o, up, 1.0);
+    CHECK(g1[0] == 0.0 && k1 == 1.0);
+    // clamp_budget: k outside (0, n) -> budget_error; tau <= 0 -> contract_error
+    CHECK_THROWS_AS(soft_topk_forward(x, 3.0, 1.0), budget_error);
+    CHECK_THROWS_AS(soft_topk_forward(x, 0.0, 1.0), budget_error);
+    CHECK_THROWS_AS(soft_topk_forward(x, 1.0, 0.0), contract_error);
+    // training_mask: noised scores
+    auto g = uniform(11, -1.0, 1.0, 9);
+    auto m = training_mask(r, 4.2, 0.7, g, 0.5);
+    std::vector<double> rn(11);
+    for (size_t i = 0; i < 11; ++i) rn[i] = r[i] + 0.5 * g[i];
+    auto ref = soft_topk_forward(rn, 4.2, 0.7);
+    for (size_t i = 0; i < 11; ++i) CHECK(std::fabs(m.values[i] - ref.values[i]) <= 1e-12);
+}
+
+// fp64 host statement of masked attention + its VJP (attention.cpp:46-201), for the checks below
+static void host_attention(const AttentionCall& c, std::vector<double>& out, const std::vector<double>* u,
+                           AttentionGrads* g) {
+    out.assign((size_t)c.n_q * c.d, 0.0);
+    if (g) {
+        g->queries.assign((size_t)c.n_q * c.d, 0.0);
+        g->keys.assign((size_t)c.t * c.d, 0.0);
+        g->values.assign((size_t)c.t * c.d, 0.0);
+        g->soft_mask.assign(c.soft_mask.size(), 0.0);
+    }
+    for (int r = 0; r < c.n_q; ++r) {
+        const int pos = c.query_pos_offset + r, end = c.causal ? std::min(c.t, pos + 1) : c.t;
+        std::vector<double> s((size_t)end), pr((size_t)end), p((size_t)end);
+        double mx = -INFINITY, zr = 0.0, zm = 0.0;
+        for (int j = 0; j < end; ++j) {
+            double dot = 0.0;
+            for (int e = 0; e < c.d; ++e) dot += c.queries[(size_t)r * c.d + e] * c.keys[(size_t)j * c.d + e];
+            s[(size_t)j] = c.scale * dot;
+            mx = std::max(mx, s[(size_t)j]);
+        }
+        for (int j = 0; j < end; ++j) zr += (pr[(size_t)j] = std::exp(s[(size_t)j] - mx));
+        auto mask_at = [&](int j) {
+            return (c.self_always_retained && j == pos) ? 1.0 : (c.soft_mask.empty() ? 1.0 : c.soft_mask[(size_t)j]);
+        };
+        for (int j = 0; j < end; ++j) {
+            pr[(size_t)j] /= zr;
+            zm += (p[(size_t)j] = pr[(size_t)j] * mask_at(j));
+        }
+        for (int j = 0; j < end; ++j) p[(size_t)j] /= zm;
+        for (int e = 0; e < c.d; ++e)
+            for (int j = 0; j < end; ++j) out[(size_t)r * c.d + e] += p[(size_t)j] * c.values[(size_t)j * c.d + e];
+        if (!g) continue;
+        const double* ur = u->data() + (size_t)r * c.d;
+        std::vector<double> w((size_t)end), ds((size_t)end);
+        double wp = 0.0, dpd = 0.0;
+        for (int j = 0; j < end; ++j) {
+            double acc = 0.0;
+            for (int e = 0; e < c.d; ++e) acc += ur[e] * c.values[(size_t)j * c.d + e];
+            w[(size_t)j] = acc;
+            wp += acc * p[(size_t)j];
+        }
+        for (int j = 0; j < end; ++j) {
+            const double dpt = (w[(size_t)j] - wp) / zm;
+            if (!c.soft_mask.empty() && !(c.self_always_retained && j == pos)) g->soft_mask[(size_t)j] += dpt * pr[(size_t)j];
+            ds[(size_t)j] = dpt * mask_at(j);
+            dpd += ds[(size_t)j] * pr[(size_t)j];
+        }
+        for (int j = 0; j < end; ++j) {
+            const double dsj = pr[(size_t)j] * (ds[(size_t)j] - dpd) * c.scale;
+            for (int e = 0; e < c.d; ++e) {
+                g->values[(size_t)j * c.d + e] += p[(size_t)j] * ur[e];
+                g->queries[(size_t)r * c.d + e] += dsj * c.keys[(size_t)j * c.d + e];
+                g->keys[(size_t)j * c.d + e] += dsj * c.queries[(size_t)r * c.d + e];
+            }
+        }
+    }
+}
+
+static double max_rel(const std::vector<double>& a, const std::vector<double>& b) {
+    double num = 0.0, den = 1e-12;
+    for (size_t i = 0; i < a.size(); ++i) {
+        num = std::max(num, std::fabs(a[i] - b[i]));
+        den = std::max(den, std::fabs(b[i]));
+    }
+    return num / den;
+}
+
+static void test_masked_attention_training() {
+    for (int rep = 0; rep < 6; ++rep) {
+        const bool bf = rep >= 3;
+        AttentionCall c;
+        c.n_q = bf ? 70 : 9;
+        c.t = bf ? 150 : 21;
+        c.d = bf ? 128 : 16;
+        c.queries = uniform((size_t)c.n_q * c.d, -1.0, 1.0, 100 + rep);
+        c.keys = uniform((size_t)c.t * c.d, -1.0, 1.0, 200 + rep);
+        c.values = uniform((size_t)c.t * c.d, -1.0, 1.0, 300 + rep);
+        if (rep % 3 != 2) {
+            c.soft_mask = uniform((size_t)c.t, 0.0, 1.0, 400 + rep);
+            c.soft_mask[0] = 1.0;
+        }
+        c.causal = rep % 3 != 1;
+        c.query_pos_offset = c.causal ? c.t - c.n_q : 0;
+        c.self_always_retained = rep % 2 == 1;
+        c.scale = 1.0 / std::sqrt((double)c.d);
+        if (bf) {  // the device sees bf16 inputs: compare on the same rounded values
+            for (auto* v : {&c.queries, &c.keys, &c.values})
+                for (double& e : *v) e = bf16(e);
+        }
+        auto u = uniform((size_t)c.n_q * c.d, -1.0, 1.0, 500 + rep);
+        if (bf)
+            for (double& e : u) e = bf16(e);
+        AttentionSaved sv;
+        auto out = masked_attention_dense(c, &sv, bf ? Precision::bf16 : Precision::fp32);
+        auto g = masked_attention_vjp(c, sv, u);
+        std::vector<double> ref;
+        AttentionGrads rg;
+        host_attention(c, ref, &u, &rg);
+        const double tol = bf ? 1e-2 : 1e-5;  // north_star: 1e-2 bf16, 1e-5 fp32
+        CHECK(max_rel(out, ref) <= tol);
+        CHECK(max_rel(g.queries, rg.queries) <= tol);
+        CHECK(max_rel(g.keys, rg.keys) <= tol);
+        CHECK(max_rel(g.values, rg.values) <= tol);
+        if (!c.soft_mask.empty()) CHECK(max_rel(g.soft_mask, rg.soft_mask) <= tol);
+    }
+    // attention.cpp:82-84: a row without masked mass -> degenerate_mask_error
+    AttentionCall c;
+    c.n_q = 2;
+    c.t = 4;
+    c.d = 8;
+    c.queries = uniform(16, -1, 1, 1);
+    c.keys = uniform(32, -1, 1, 2);
+    c.values = uniform(32, -1, 1, 3);
+    c.soft_mask.assign(4, 0.0);
+    c.scale = 0.3;
+    CHECK_THROWS_AS(masked_attention_dense(c), degenerate_mask_error);
+    c.soft_mask[1] = -0.5;  // attention.cpp:40-42
+    CHECK_THROWS_AS(masked_attention_dense(c), contract_error);
+    c.soft_mask.assign(3, 1.0);
+    CHECK_THROWS_AS(masked_attention_dense(c), contract_error);
+}
+
 int main(int argc, char** argv) {
     try {
         require_b200();
@@ -303,6 +490,8 @@ int main(int argc, char** argv) {
         test_cache_and_prefill();
         test_decode();
         test_memory();
+        test_soft_topk_training();
+        test_masked_attention_training();
     } catch (const std::exception& e) {
         std::printf("UNCAUGHT %s\n", e.what());
         return 2;
