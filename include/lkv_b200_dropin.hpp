@@ -29,6 +29,9 @@
 #include <string>
 #include <vector>
 
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)  // exported from the -fvisibility=hidden library
+#endif
 namespace lkv::b200 {
 
 // ---- errors (errors.hpp:10-32) ------------------------------------------------------------
@@ -202,3 +205,6 @@ AttentionGrads masked_attention_vjp(const AttentionCall& call, const AttentionSa
 void require_b200();
 
 }  // namespace lkv::b200
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
