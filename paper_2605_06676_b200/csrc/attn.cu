@@ -42,6 +42,9 @@ namespace attn {
 
 constexpr int kD = 128;
 constexpr float kLog2e = 1.4426950408889634f;
+#ifndef LKV_ATTN_EXPT
+#define LKV_ATTN_EXPT 0  // forward bisection knobs (profiles/attn_ab.sh): 1 no exp, 2 no P store
+#endif
 
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
@@ -329,12 +332,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                         const int i = c * 8 + e * 2 + h, j = j0 + i;
                         float mj = mask ? mwarp[i] : 1.f;
                         if (!interior && g.self_keep && j == g.pos_offset + r) mj = 1.f;
+#if LKV_ATTN_EXPT & 1
+                        pv[h] = (x[i] - sub) * mj;  // bisection knob: no exp
+#else
                         pv[h] = fast_exp2(x[i] - sub) * mj;  // x = -inf -> 0
+#endif
                         l_run += pv[h];
                     }
                     w4v[e] = pack2(pv[0], pv[1]);
                 }
-                *reinterpret_cast<uint4*>(prow + ((c ^ (rl & 7)) << 4)) = make_uint4(w4v[0], w4v[1], w4v[2], w4v[3]);
+                if (!(LKV_ATTN_EXPT & 2))
+                    *reinterpret_cast<uint4*>(prow + ((c ^ (rl & 7)) << 4)) = make_uint4(w4v[0], w4v[1], w4v[2], w4v[3]);
             }
             fence_proxy_async_smem();
             tc_fence_before();
