@@ -286,13 +286,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                                   (!g.causal || j0 + kTcK - 1 <= g.pos_offset + wr0) &&
                                   !(g.self_keep && j0 + kTcK - 1 >= g.pos_offset + wr0);
             float x[64];
-            float mt = -INFINITY;
+            float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // 4 chains, not one 64-long
 #pragma unroll
             for (int i = 0; i < 64; ++i) {
                 x[i] = __uint_as_float(sr[i]) * g.c;
                 if (!interior && !admissible(g, j0 + i, r)) x[i] = -INFINITY;
-                mt = fmaxf(mt, x[i]);
+                mq[i & 3] = fmaxf(mq[i & 3], x[i]);
             }
+            const float mt = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
             const float m_new = fmaxf(m_run, mt);
             const bool need = m_new != -INFINITY && (m_run == -INFINITY || m_new > m_run + kTcRescale);
             float alpha = 1.f;
@@ -321,6 +322,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             // P row -> shared memory (bf16, 128-byte swizzle, K-major: 8 chunks of 8 keys)
             unsigned char* prow = my_ps + bb * kPBytes + rl * 128;
             const float sub = m_run == -INFINITY ? 0.f : m_run;
+            float ls[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
                 uint32_t w4v[4];
@@ -337,13 +339,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #else
                         pv[h] = fast_exp2(x[i] - sub) * mj;  // x = -inf -> 0
 #endif
-                        l_run += pv[h];
+                        ls[i & 3] += pv[h];
                     }
                     w4v[e] = pack2(pv[0], pv[1]);
                 }
                 if (!(LKV_ATTN_EXPT & 2))
                     *reinterpret_cast<uint4*>(prow + ((c ^ (rl & 7)) << 4)) = make_uint4(w4v[0], w4v[1], w4v[2], w4v[3]);
             }
+            l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
             fence_proxy_async_smem();
             tc_fence_before();
             __syncwarp();
