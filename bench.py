@@ -351,6 +351,17 @@ def run_ours(args, rank, world, local_rank):
         print(json.dumps(line), flush=True)
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 def ncu_traffic(name, round_dir="r01"):
     """DRAM bytes (read + write) of one launch from a committed `ncu --set full` summary."""
     units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
@@ -393,7 +404,8 @@ def cpu_baseline(cache, scorers, ev, n_threads=1, n_heads=8):
                   n_threads=n_threads, fast=True)
     dt = time.perf_counter() - t0
     rows = int(t_per_head.sum())
-    return {"value": rows / dt, "unit": UNIT, "cores": n_threads, "kind": "port",
+    return {"value": rows / dt, "unit": UNIT, "cores": n_threads, "kind": "port", "cpu_model": cpu_model(),
+            "host_threads_available": os.cpu_count(),
             "sample": f"{nh} heads x {cache.seq_lens[0]} rows of the same C2 workload (layer 0..), fp64 score + "
                       f"stable-sort top-k + gather, {dt:.2f} s; port built -O3 -march=x86-64-v3 (the reference's "
                       f"Release + -march=native recipe)",
@@ -448,7 +460,7 @@ def run_reference(args, rank, world):
         "data": "synthetic (seeded; BASELINE.json configs[1] shapes)", "impl": "reference",
         "config": {"workload": f"C2 sample: {nh} heads x {T} rows (one head per host thread)",
                    "parallelism": f"{ncores} host threads"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": ncores, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": ncores, "kind": "port", "cpu_model": cpu_model(),
                          "sample": f"{nh} heads x {T} rows per step: fp64 LKV-H solve + scorer + stable-sort top-k + "
                                    f"gather; port of proj/src built -O3 -march=x86-64-v3 (the reference's Release + "
                                    f"-march=native recipe; its Eigen GEMM is replaced by a row-blocked loop)"},
