@@ -200,6 +200,15 @@ lkv_status lkv_evict(const lkv_cache_desc* cache, const lkv_scorer_desc* scorer,
                      double* ratios_out, int32_t* budgets_out, void* workspace, size_t workspace_bytes,
                      lkv_stream_t stream);
 
+/* score -> select -> compact with budgets given (no LKV-H solve): the per-layer step of the
+ * layer-wise prefill (evictsim.cpp:161-215 with the budgets of policy_budget_table) or budgets
+ * from an external source (export-budgets CSV, tools/lkv.cpp:154-177).  out->offsets must hold the
+ * exclusive scan of budget + decode_slack (lkv_ragged_offsets / lkv_budgets); workspace as
+ * lkv_workspace_bytes(cache, 1). */
+lkv_status lkv_evict_budgets(const lkv_cache_desc* cache, const lkv_scorer_desc* scorer, const int32_t* budgets,
+                             const lkv_ragged_desc* out, float* scores_out, void* workspace, size_t workspace_bytes,
+                             lkv_stream_t stream);
+
 /* ---- fused, from a host-resident cache ------------------------------------------ */
 /* The same eviction for a dense cache held in pinned, device-mapped host memory
  * (cudaHostAlloc / cudaHostRegister mapped): host_cache->keys/values are host pointers.

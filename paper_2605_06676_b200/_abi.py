@@ -30,7 +30,7 @@ EXPORTED = [
     "lkv_model_decode_step", "lkv_budgets_shard", "lkv_evict_shard", "lkv_ragged_capacity_shard", "lkv_comm_get_unique_id",
     "lkv_comm_init", "lkv_comm_destroy", "lkv_comm_size", "lkv_comm_rank", "lkv_comm_allgatherv", "lkv_comm_gatherv",
     "lkv_attn_workspace_bytes", "lkv_masked_attention_fwd", "lkv_masked_attention_bwd", "lkv_soft_topk_fwd",
-    "lkv_soft_topk_vjp",
+    "lkv_soft_topk_vjp", "lkv_evict_budgets",
 ]
 
 
@@ -137,6 +137,8 @@ def load():
     L.lkv_masked_attention_bwd.argtypes = [P(AttnDesc), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     L.lkv_soft_topk_fwd.argtypes = [vp, vp, dbl, i32, i32, i64, vp, dbl, vp, vp, vp, vp, vp, sz, vp]
     L.lkv_soft_topk_vjp.argtypes = [vp, vp, i32, i32, i64, dbl, vp, vp, vp]
+    L.lkv_evict_budgets.argtypes = [P(CacheDesc), P(ScorerDesc), vp, P(RaggedDesc), vp, vp, sz, vp]
+    L.lkv_evict_budgets.restype = C.c_int
     L.lkv_soft_topk_fwd.restype = C.c_int
     L.lkv_soft_topk_vjp.restype = C.c_int
     L.lkv_masked_attention_fwd.restype = C.c_int

@@ -607,6 +607,23 @@ lkv_status lkv_evict(const lkv_cache_desc* c, const lkv_scorer_desc* s, const do
                       budgets_out, ws, ws_bytes, (cudaStream_t)stream);
 }
 
+lkv_status lkv_evict_budgets(const lkv_cache_desc* c, const lkv_scorer_desc* s, const int32_t* budgets,
+                             const lkv_ragged_desc* out, float* scores_out, void* ws, size_t ws_bytes,
+                             lkv_stream_t stream) {
+    lkv_status st = check_cache(c, true);
+    if (st) return st;
+    if ((st = check_scorer(s, c))) return st;
+    if ((st = check_ragged(out, n_heads_of(c), c->head_dim, c->dtype, true))) return st;
+    if (!budgets) return fail(LKV_ERR_CONTRACT, "budgets are null");
+    const EvictWs w = evict_layout(c, 1);
+    if ((st = check_ws(ws, ws_bytes, w.total))) return st;
+    cudaStream_t strm = (cudaStream_t)stream;
+    float* scores = scores_out ? scores_out : at<float>(ws, w.scores);
+    bool hist_made = false;  // K1 fuses top-k pass 1 into its epilogue (tcgen05 path)
+    if ((st = run_score(c, s, scores, strm, 0, at<uint32_t>(ws, w.hist), at<ErrWord>(ws, w.err), &hist_made))) return st;
+    return run_select(c, scores, budgets, out, ws, w, true, strm, hist_made);
+}
+
 lkv_status lkv_evict_shard(const lkv_cache_desc* c, const lkv_scorer_desc* s, const double* logits, int32_t n_logits,
                            int32_t head_begin, double R, int32_t mode, const lkv_ragged_desc* out, float* scores_out,
                            double* ratios_out, int32_t* budgets_out, void* ws, size_t ws_bytes, lkv_stream_t stream) {

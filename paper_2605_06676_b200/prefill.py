@@ -86,13 +86,13 @@ class LayerwisePrefill:
         for q in range(S):
             lens_q = (C.c_int32 * 1)(self.seq_lens[q])
             cd = CacheDesc(1, 1, H, D, T, ld.dtype, 0, self.k_layer[q].data_ptr(), self.v_layer[q].data_ptr(), lens_q)
-            _check(lib().lkv_score(C.byref(cd), C.byref(sd), _ptr(self.scores), None, 0, s))
             h0 = (q * self.L + l) * H  # first flat head of (q, l) in the global ragged cache
             rd = RaggedDesc(H, D, ld.dtype, r.decode_slack, r.capacity_rows, r.offsets.data_ptr() + 8 * h0,
                             r.lens.data_ptr() + 4 * h0, r.keys.data_ptr(), r.values.data_ptr(), r.positions.data_ptr())
             b = self.budgets[q, l * H:(l + 1) * H]
-            _check(lib().lkv_select(C.byref(cd), _ptr(self.scores), _ptr(b), C.byref(rd), 1, C.c_void_p(self._ws.ptr),
-                                    self._ws.nbytes, s))
+            # score (top-k histogram fused into the scorer epilogue) -> select -> gather, one call
+            _check(lib().lkv_evict_budgets(C.byref(cd), C.byref(sd), _ptr(b), C.byref(rd), _ptr(self.scores),
+                                           C.c_void_p(self._ws.ptr), self._ws.nbytes, s))
         self._ingested += 1
         if self._budget_prefix is None:  # one host read of the budgets, for the peak accounting only
             per_layer = self.budgets.reshape(S, self.L, H).sum(dim=(0, 2)).cpu().tolist()
