@@ -54,6 +54,26 @@ __device__ __forceinline__ ChunkInfo decode_chunk(const SelectParams& p, int chu
 
 __device__ __forceinline__ int head_len(const SelectParams& p, int head) { return p.seq.len[head_seq(p.seq, head)]; }
 
+// the radix keys of a thread's 16 contiguous rows [j0, j0 + 16) of a chunk (n rows): four 16-byte
+// loads when the rows are all present and aligned, else guarded scalar loads (rows past n -> 0)
+__device__ __forceinline__ void load_keys16(const float* sc, int j0, int n, uint32_t (&k)[kPerThread]) {
+    static_assert(kPerThread == 16, "four float4 per thread");
+    if (j0 + kPerThread <= n && (reinterpret_cast<uintptr_t>(sc + j0) & 15) == 0) {
+        const float4* v = reinterpret_cast<const float4*>(sc + j0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float4 f = __ldg(v + q);
+            k[4 * q + 0] = f32_key(f.x);
+            k[4 * q + 1] = f32_key(f.y);
+            k[4 * q + 2] = f32_key(f.z);
+            k[4 * q + 3] = f32_key(f.w);
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < kPerThread; ++q) k[q] = (j0 + q < n) ? f32_key(sc[j0 + q]) : 0u;
+    }
+}
+
 // ---- S1 --------------------------------------------------------------------------
 __global__ void __launch_bounds__(kSelThreads) select_hist_kernel(const __grid_constant__ SelectParams p) {
     __shared__ uint32_t h[2048];
@@ -162,8 +182,9 @@ __global__ void __launch_bounds__(kSelThreads) select_collect_kernel(const __gri
     const float* sc = p.scores + (size_t)ci.head * p.seq.T + ci.c0;
     const int j0 = threadIdx.x * kPerThread;
     uint32_t dig[kPerThread];
+    load_keys16(sc, j0, ci.n, dig);
 #pragma unroll
-    for (int q = 0; q < kPerThread; ++q) dig[q] = (j0 + q < ci.n) ? (f32_key(sc[j0 + q]) >> 21) : 0u;
+    for (int q = 0; q < kPerThread; ++q) dig[q] >>= 21;
     uint32_t gt = 0, nc = 0;
 #pragma unroll
     for (int q = 0; q < kPerThread; ++q) {
@@ -320,12 +341,9 @@ __global__ void __launch_bounds__(kSelThreads, LKV_EMIT_MINB) select_emit_kernel
     const int j0 = threadIdx.x * kPerThread;
     uint32_t keys[kPerThread];
     uint32_t n_eq = 0;
+    load_keys16(sc, j0, ci.n, keys);
 #pragma unroll
-    for (int q = 0; q < kPerThread; ++q) {
-        const int j = j0 + q;
-        keys[q] = j < ci.n ? f32_key(sc[j]) : 0u;
-        n_eq += (j < ci.n) && keys[q] == key_t;
-    }
+    for (int q = 0; q < kPerThread; ++q) n_eq += (j0 + q < ci.n) && keys[q] == key_t;
     uint32_t tot;
     uint32_t eq_rank = eqb + block_exclusive_scan<kSelThreads>(n_eq, s_scan, &tot);
     uint32_t keepmask = 0, n_keep = 0;
