@@ -79,6 +79,8 @@ struct BudgetTable {
 BudgetTable allocate_budgets(std::span<const double> scores, double target_ratio, int n_layers, int n_kv_heads);
 std::vector<int> freeze_budgets(const BudgetTable& table, int t);
 std::vector<int> freeze_budgets_exact(const BudgetTable& table, int t);
+// policy.cpp:301-311 -- "layer,head,ratio" ("%.6f"), the `lkv export-budgets` budgets.csv
+std::string budget_table_csv(const BudgetTable& table);
 
 // ---- scorer / selection ------------------------------------------------------------------------
 // keys, values: [t x d] row-major.  in = d (values ignored, pass empty) or 2d ([k;v]).

@@ -3,6 +3,7 @@
 // so tests/ can check the oracle restatement bit-for-bit against them.
 // Exceptions map onto the same status codes as include/lkv_b200.h.
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <span>
@@ -92,6 +93,19 @@ int ref_masked_attention(const double* q, const double* k, const double* v, cons
             std::memcpy(dv, g.values.data(), sizeof(double) * g.values.size());
             if (mask && dmask) std::memcpy(dmask, g.soft_mask.data(), sizeof(double) * g.soft_mask.size());
         }
+    });
+}
+
+// budget_table_csv (policy.cpp:301-311) of allocate_budgets(scores, ratio, L, H): the CSV text is
+// copied into out (capacity cap, NUL-terminated); returns the status
+int ref_budget_table_csv(const double* scores, int n_layers, int n_kv_heads, double ratio, char* out, int cap) {
+    return guarded([&] {
+        lkv::Tensor s = lkv::Tensor::from({n_layers * n_kv_heads}, std::vector<double>(scores, scores + n_layers * n_kv_heads));
+        lkv::BudgetTable t = lkv::allocate_budgets(s, ratio, n_layers, n_kv_heads);
+        const std::string csv = lkv::budget_table_csv(t);
+        const size_t n = std::min<size_t>(csv.size(), (size_t)cap - 1);
+        std::memcpy(out, csv.data(), n);
+        out[n] = 0;
     });
 }
 

@@ -449,6 +449,17 @@ std::vector<double> decode_attention(KvCache& cache, std::span<const double> q, 
     return out;
 }
 
+std::string budget_table_csv(const BudgetTable& table) {  // policy.cpp:301-311
+    std::string out = "layer,head,ratio\n";
+    char buf[64];
+    for (int l = 0; l < table.n_layers; ++l)
+        for (int h = 0; h < table.n_kv_heads; ++h) {
+            std::snprintf(buf, sizeof buf, "%d,%d,%.6f\n", l, h, table.at(l, h));
+            out += buf;
+        }
+    return out;
+}
+
 // ---- soft_topk.cpp:111-189 (training) ---------------------------------------------------
 static SoftTopKOutput soft_topk_impl(std::span<const double> x, double k, double tau, std::span<const double> noise,
                                      double noise_scale) {

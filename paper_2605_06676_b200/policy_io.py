@@ -120,3 +120,49 @@ def scorers_from_params(p: LkvParams, dtype=None, device="cuda") -> Scorers:
     b1 = torch.tensor(np.stack([m.b1 for m in p.token_scorers]), dtype=torch.float32, device=device)
     w2 = torch.tensor(np.stack([m.w2 for m in p.token_scorers]), dtype=torch.float32, device=device)
     return Scorers(w1, b1, w2, input=SCORER_KV, activation=SILU, stride_layer=p.n_kv_heads, stride_head=1)
+
+
+# ---- export-budgets (tools/lkv.cpp:154-177, policy.cpp:301-311) ----------------------------------
+def budget_table_csv(ratios, n_layers: int, n_kv_heads: int) -> str:
+    """policy.cpp:301-311 -- "layer,head,ratio" with the ratio printed "%.6f"."""
+    r = np.asarray(ratios, np.float64).reshape(-1)
+    if r.size != n_layers * n_kv_heads:
+        raise ContractError("budget_table_csv: one ratio per (layer, kv head)")
+    lines = ["layer,head,ratio"]
+    lines += ["%d,%d,%.6f" % (l, h, r[l * n_kv_heads + h]) for l in range(n_layers) for h in range(n_kv_heads)]
+    return "\n".join(lines) + "\n"
+
+
+def budget_int_csv(budgets, n_layers: int, n_kv_heads: int) -> str:
+    """tools/lkv.cpp:164-173 -- "layer,head,budget" with the frozen integer budgets."""
+    b = np.asarray(budgets).reshape(-1)
+    if b.size != n_layers * n_kv_heads:
+        raise ContractError("budget_int_csv: one budget per (layer, kv head)")
+    lines = ["layer,head,budget"]
+    lines += ["%d,%d,%d" % (l, h, int(b[l * n_kv_heads + h])) for l in range(n_layers) for h in range(n_kv_heads)]
+    return "\n".join(lines) + "\n"
+
+
+def export_budgets(checkpoint: str, ratio: float, t: int, out_dir: str, device="cuda") -> tuple:
+    """`lkv export-budgets` (tools/lkv.cpp:154-177) with the LKV-H solve and the freeze on the
+    device (K2): writes budgets.csv (ratios) and, for t > 0, budgets_int.csv (floor budgets,
+    freeze_budgets).  Returns the two paths (the second None when t <= 0)."""
+    import os
+
+    import torch
+
+    from . import BUDGET_FLOOR, budgets as device_budgets
+
+    p = load_lkv_params(checkpoint)
+    logits = torch.tensor(head_scores(p), dtype=torch.float64, device=device)
+    ratios, b = device_budgets(logits, ratio, [max(int(t), 1)], BUDGET_FLOOR)
+    os.makedirs(out_dir, exist_ok=True)
+    p1 = os.path.join(out_dir, "budgets.csv")
+    with open(p1, "w") as f:
+        f.write(budget_table_csv(ratios.cpu().numpy(), p.n_layers, p.n_kv_heads))
+    p2 = None
+    if t > 0:
+        p2 = os.path.join(out_dir, "budgets_int.csv")
+        with open(p2, "w") as f:
+            f.write(budget_int_csv(b[0].cpu().numpy(), p.n_layers, p.n_kv_heads))
+    return p1, p2

@@ -108,6 +108,12 @@ static void test_budgets() {
     CHECK(s == 1258291);
 }
 
+static void test_budget_csv() {  // policy.cpp:301-311
+    std::vector<double> eq(4, 0.3);
+    BudgetTable t = allocate_budgets(eq, 0.15, 2, 2);
+    CHECK(budget_table_csv(t) == "layer,head,ratio\n0,0,0.150000\n0,1,0.150000\n1,0,0.150000\n1,1,0.150000\n");
+}
+
 static void test_hard_topk() {  // test_soft_topk.cpp:190-199
     std::vector<float> x{0.1f, 0.9f, 0.5f};
     CHECK((hard_topk(x, 2) == std::vector<int>{0, 1, 1}));
@@ -485,6 +491,7 @@ int main(int argc, char** argv) {
         require_b200();
         test_checkpoint(argc > 1 ? argv[1] : nullptr);
         test_budgets();
+        test_budget_csv();
         test_hard_topk();
         test_token_scores();
         test_cache_and_prefill();

@@ -27,7 +27,7 @@ def test_dropin_symbols_exported():
     assert {"allocate_budgets", "freeze_budgets", "token_scores", "inference_select", "hard_topk", "cache_from_trace",
             "prefill_with_eviction", "decode_attention", "kv_memory_bytes", "load_lkv_params", "head_scores"} <= names
     for n in sorted(names):
-        assert re.search(r"lkv::b200::" + n + r"\(", out), n
+        assert re.search(r"lkv::b200::" + n + r"(\[abi:cxx11\])?\(", out), n
 
 
 def test_dropin_binary_links():

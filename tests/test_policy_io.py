@@ -84,3 +84,45 @@ def test_evict_with_reference_checkpoint():
         assert np.max(np.abs(sc[h] - ref)) / np.max(np.abs(ref)) <= 1e-2
         _, _, pos = res.cache.head(h)
         assert (pos.cpu().numpy() == O.select_positions_f32(sc[h], int(want_b[h]))).all()
+
+
+def _ref_csv(scores, L, H, ratio):
+    import ctypes as C
+
+    R = O.ref_lib()
+    R.ref_budget_table_csv.argtypes = [C.POINTER(C.c_double), C.c_int, C.c_int, C.c_double, C.c_char_p, C.c_int]
+    x = np.ascontiguousarray(scores, np.float64)
+    buf = C.create_string_buffer(1 << 20)
+    assert R.ref_budget_table_csv(x.ctypes.data_as(C.POINTER(C.c_double)), L, H, ratio, buf, 1 << 20) == 0
+    return buf.value.decode()
+
+
+@pytest.mark.skipif(O.ref_lib() is None, reason="oracle/_ref not built (reference not mounted)")
+def test_budget_csv_equals_the_references():
+    """budget_table_csv (policy.cpp:301-311) byte-identical to the reference's own function."""
+    rng = np.random.default_rng(8)
+    for L, H, r in ((2, 4, 0.15), (32, 8, 0.1), (80, 8, 0.25)):
+        x = rng.normal(0, 1.5, L * H)
+        assert policy_io.budget_table_csv(O.allocate_budgets(x, r), L, H) == _ref_csv(x, L, H, r)
+
+
+def test_budget_int_csv_format():
+    """tools/lkv.cpp:164-173: header then one "l,h,budget" line per (layer, kv head)."""
+    assert policy_io.budget_int_csv([150, 150, 3, 0], 2, 2) == "layer,head,budget\n0,0,150\n0,1,150\n1,0,3\n1,1,0\n"
+    with pytest.raises(lkv.ContractError):
+        policy_io.budget_int_csv([1, 2, 3], 2, 2)
+
+
+@pytest.mark.gpu
+def test_export_budgets_from_reference_checkpoint(tmp_path):
+    """`lkv export-budgets` (tools/lkv.cpp:154-177) with the LKV-H solve on the device: the CSVs
+    equal the reference's (ratios through its own budget_table_csv, floor budgets bit-exact)."""
+    ck = os.path.join(G, "lkv_params_l2h4d128.bin")
+    p1, p2 = policy_io.export_budgets(ck, 0.15, 1000, str(tmp_path))
+    p = policy_io.load_lkv_params(ck)
+    scores = policy_io.head_scores(p)
+    want_ratios = O.allocate_budgets(scores, 0.15)
+    assert open(p1).read() == policy_io.budget_table_csv(want_ratios, p.n_layers, p.n_kv_heads)
+    if O.ref_lib() is not None:
+        assert open(p1).read() == _ref_csv(scores, p.n_layers, p.n_kv_heads, 0.15)
+    assert open(p2).read() == policy_io.budget_int_csv(O.freeze_budgets(want_ratios, 1000), p.n_layers, p.n_kv_heads)
