@@ -274,6 +274,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 mnext1 = jn + lane + 32 < g.t_k ? __ldg(mask + jn + lane + 32) : 0.f;
             }
             mbar_wait(&my_s_full[bb], (t >> 1) & 1);
+            __syncwarp();  // reconverge before .sync.aligned tcgen05.ld
             tc_fence_after();
             uint32_t sr[64];
             tmem_ld_32x32b_x32(lane_addr + s_col + bb * kTcK, *reinterpret_cast<uint32_t(*)[32]>(sr));
@@ -306,6 +307,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             if (t >= 2) mbar_wait(&my_p_empty[bb], ((t >> 1) - 1) & 1);
             if (__any_sync(0xffffffffu, need) && t > 0) {
                 mbar_wait(&o_bar[wg], (t - 1) & 1);  // rescale O once P V of tile t-1 has landed
+                __syncwarp();  // reconverge before .sync.aligned tcgen05.ld
                 tc_fence_after();
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
@@ -356,6 +358,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (ntw > 1) mbar_wait(&o_bar[wg], (ntw - 2) & 1);  // phases in order: never two behind
         if (ntw > 0) {
             mbar_wait(&o_bar[wg], (ntw - 1) & 1);
+            __syncwarp();  // reconverge before .sync.aligned tcgen05.ld
             tc_fence_after();
         }
         const bool ok = l_run > 0.f;
@@ -541,6 +544,7 @@ __global__ void __launch_bounds__(kBwThreads, 1)
             __syncwarp();
             fetch(t + 1);
             mbar_wait(&s_full[bb], (t >> 1) & 1);
+            __syncwarp();  // reconverge before .sync.aligned tcgen05.ld
             tc_fence_after();
             uint32_t sv[64], dv[64];
             tmem_ld_32x32b_x32(la + bb * 64, *reinterpret_cast<uint32_t(*)[32]>(sv));
@@ -592,6 +596,7 @@ __global__ void __launch_bounds__(kBwThreads, 1)
         // ---- epilogue: dV, dK (x scale) rows from TMEM, dmask
         if (ntiles > 0) {
             mbar_wait(acc_done, 0);
+            __syncwarp();  // reconverge before .sync.aligned tcgen05.ld
             tc_fence_after();
         }
 #pragma unroll
@@ -783,6 +788,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
                 mn1 = jn + lane + 32 < g.t_k ? __ldg(mask + jn + lane + 32) : 0.f;
             }
             mbar_wait(&s_full[wg], t & 1);
+            __syncwarp();  // reconverge before .sync.aligned tcgen05.ld
             tc_fence_after();
             uint32_t sv[64], dv[64];
             tmem_ld_32x32b_x32(la, *reinterpret_cast<uint32_t(*)[32]>(sv));
@@ -824,6 +830,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         if (ntw > 1) mbar_wait(&ds_empty[wg], (ntw - 2) & 1);
         if (ntw > 0) {
             mbar_wait(&ds_empty[wg], (ntw - 1) & 1);
+            __syncwarp();  // reconverge before .sync.aligned tcgen05.ld
             tc_fence_after();
         }
         float* drw = p.dq + (q_row0 + r) * kD;

@@ -196,6 +196,8 @@ __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int G = p.G;
     const int D = 128;
+    pdl_trigger();  // the combine's CTAs may become resident (they wait for this grid to finish)
+    pdl_wait();     // q / new k / new v come from the previous kernel
     const int it_lo = *p.item_lo, it_hi = *p.item_hi;
     const int ch = *p.ch;
     if (threadIdx.x == 0) {
@@ -256,7 +258,8 @@ __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
         const int rows = min(ch, len_new - r0);
         const int64_t off = p.offsets[head];
         const bool has_new = (len_old >= r0) && (len_old < r0 + ch);
-        if (has_new && off + len_new > p.offsets[head + 1]) {
+        const bool fits = off + len_new <= p.offsets[head + 1];
+        if (has_new && !fits) {
             if (threadIdx.x == 0) latch_error(p.err, LKV_ERR_CONTRACT, head);
         }
         const __nv_bfloat16* qp;
@@ -299,9 +302,11 @@ __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
                         static_cast<const uint4*>(isv ? p.new_v : p.new_k) + ((size_t)hc.qsl * p.n_kv_heads + hc.kvh) * 16;
                     const uint4 v = __ldg(src + hq);
                     *reinterpret_cast<uint4*>(sbase + (isv ? 2 * kDecStageRows * 128 : 0) + sw_off(nr, hq)) = v;
-                    uint4* dstg = static_cast<uint4*>(isv ? p.values : p.keys) + (size_t)(off + len_old) * 16;
-                    dstg[hq] = v;
-                    if (lane == 0) p.positions[off + len_old] = p.tokens_seen[hc.s];
+                    if (fits) {  // never write past the head's capacity (the error is latched above)
+                        uint4* dstg = static_cast<uint4*>(isv ? p.values : p.keys) + (size_t)(off + len_old) * 16;
+                        dstg[hq] = v;
+                        if (lane == 0) p.positions[off + len_old] = p.tokens_seen[hc.s];
+                    }
                     fence_proxy_async_smem();
                     __syncwarp();
                 }
@@ -532,6 +537,7 @@ constexpr int kCombThreads = 128;
 template <typename T>
 __global__ void __launch_bounds__(kCombThreads) decode_combine_kernel(const __grid_constant__ DecodeParams p,
                                                                       int single_chunk_done) {
+    pdl_trigger();  // the next GEMV may start streaming its weights
     pdl_wait();
     __shared__ float s_w[kCombMaxChunks];  // [c * G + g] weight exp2(m_c - M_g) / L_g
     __shared__ float s_M[16], s_L[16];
@@ -647,7 +653,8 @@ cudaError_t launch_decode(const DecodeParams& p, int dtype, const CUtensorMap* m
         if (e != cudaSuccess) return e;
         per_sm = max(1, min(per_sm, kDecPerSm));
         const int grid = min(p.max_items, per_sm * num_sms);
-        kern<<<grid, kDecThreads, smem, stream>>>(p, *mk, *mv);
+        e = launch_pdl(kern, dim3(grid), dim3(kDecThreads), smem, stream, p, *mk, *mv);
+        if (e != cudaSuccess) return e;
         e = launch_pdl(decode_combine_kernel<__nv_bfloat16>,
                        dim3(p.n_seq * p.q_layers * p.n_kv_heads, (p.G * p.head_dim + kCombThreads - 1) / kCombThreads), dim3(kCombThreads), 0,
                        stream, p, 1);

@@ -407,6 +407,7 @@ template <typename T>
 __global__ void __launch_bounds__(64) embed_kernel(const T* __restrict__ tab, const int32_t* tokens, int B, int dm,
                                                   int vocab, const int32_t* tokens_seen, int max_seq, float* x,
                                                   float* ss_part, ErrWord* err) {
+    pdl_trigger();  // let the next GEMV start streaming its weights
     pdl_wait();
     __shared__ float s_w[2];
     const int ng = blockIdx.x, b = blockIdx.y, n = ng * 64 + threadIdx.x;
@@ -434,6 +435,7 @@ __global__ void __launch_bounds__(64) embed_kernel(const T* __restrict__ tab, co
 // ---- rmsnorm (model.cpp:48-53) -> next GEMV's activations ---------------------------------------------
 __global__ void __launch_bounds__(128) norm_pack_kernel(const float* x, const float* ss_part, const float* gain, int B,
                                                         int dm, float eps, void* act, int nbt, int is_bf16) {
+    pdl_trigger();  // let the next GEMV start streaming its weights
     pdl_wait();
     __shared__ float s_inv;
     const int b = blockIdx.y;

@@ -419,6 +419,7 @@ __global__ void __launch_bounds__(TcCfg<N, NBOX>::kThreads, 1)
                 cur = ti.scorer;
             }
             mbar_wait(&tfull[grp], (i / kEpi) & 1);
+            __syncwarp();  // reconverge before .sync.aligned tcgen05.ld
             tc_fence_after();
             const uint32_t taddr = tmem_base + (uint32_t(quarter * 32) << 16) + grp * N;
             float2 s2 = f2(0.f, 0.f);
