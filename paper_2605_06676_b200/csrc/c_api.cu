@@ -1304,8 +1304,10 @@ lkv_status lkv_model_decode_step(const lkv_model_desc* m, const void* weights, c
     gp.nbt_out = gp.nbt;
     gp.act_out = at<void>(ws, w.act_ff);
     gp.ff = g.ff;
-    auto gemv = [&](const MatGeom& mg, const unsigned char* wp, int epi, const void* act, int n_real) -> cudaError_t {
+    auto gemv = [&](const MatGeom& mg, const unsigned char* wp, int epi, const void* act, int n_real,
+                    auto&& tweak) -> cudaError_t {
         GemvParams q = gp;
+        tweak(q);
         q.w = wp;
         q.NG = mg.NG;
         q.KU = mg.KU;
@@ -1353,27 +1355,40 @@ lkv_status lkv_model_decode_step(const lkv_model_desc* m, const void* weights, c
     }
     int32_t* lbeg = at<int32_t>(ws, w.dec.layer_begin);
 
-    LKV_CUDA(launch_embed(wb + g.tok_embed, g.dtype, tokens, B, g.dm, g.vocab, tokens_seen, m->max_seq_len, x, ss, err, s),
+    // rmsnorm is folded into its neighbours (model.cpp:48-53): the producer of x (embed, or the
+    // residual epilogue of wo / down) also writes x * gain of the next norm as the next GEMV's
+    // activations, and that GEMV scales its outputs by 1 / rms from the per-group sums of squares.
+    auto norm_gain = [&](int l, bool mlp) -> const float* {
+        if (l == g.L) return reinterpret_cast<const float*>(wb + g.final_norm);
+        const unsigned char* lw = wb + g.layer0 + (size_t)l * g.layer_stride;
+        return reinterpret_cast<const float*>(lw + (mlp ? g.o_mlp_norm : g.o_attn_norm));
+    };
+    void* act_h = at<void>(ws, w.act_h);
+    LKV_CUDA(launch_embed(wb + g.tok_embed, g.dtype, tokens, B, g.dm, g.vocab, tokens_seen, m->max_seq_len, x, ss,
+                          norm_gain(0, false), act_h, w.nbt, err, s),
              "embed");
-    const float eps = (float)m->norm_eps;
+    gp.ss_in = nullptr;
+    gp.norm_dm = g.dm;
+    gp.norm_eps = (float)m->norm_eps;
+    gp.act_next = act_h;
+    auto normed = [&](GemvParams& q) { q.ss_in = ss; };
     for (int l = 0; l < g.L; ++l) {
         const unsigned char* lw = wb + g.layer0 + (size_t)l * g.layer_stride;
-        const float* attn_norm = reinterpret_cast<const float*>(lw + g.o_attn_norm);
-        const float* mlp_norm = reinterpret_cast<const float*>(lw + g.o_mlp_norm);
-        LKV_CUDA(launch_norm_pack(x, ss, attn_norm, B, g.dm, eps, at<void>(ws, w.act_h), w.nbt, g.dtype, s), "attn norm");
-        LKV_CUDA(gemv(g.qkv, lw + g.o_qkv, EPI_QKV, at<void>(ws, w.act_h), g.dm + 2 * g.dkv), "qkv");
+        LKV_CUDA(gemv(g.qkv, lw + g.o_qkv, EPI_QKV, act_h, g.dm + 2 * g.dkv, normed), "qkv");
         dp.layer0 = l;
         dp.item_lo = lbeg + l;
         dp.item_hi = lbeg + l + 1;
         LKV_CUDA(launch_decode(dp, g.dtype, &mk, &mv, sms, s), "attention");
-        LKV_CUDA(gemv(g.wo, lw + g.o_wo, EPI_RESID, at<void>(ws, w.act_attn), g.dm), "wo");
-        LKV_CUDA(launch_norm_pack(x, ss, mlp_norm, B, g.dm, eps, at<void>(ws, w.act_h), w.nbt, g.dtype, s), "mlp norm");
-        LKV_CUDA(gemv(g.gu, lw + g.o_gu, EPI_SWIGLU, at<void>(ws, w.act_h), g.ff), "gate/up");
-        LKV_CUDA(gemv(g.down, lw + g.o_down, EPI_RESID, at<void>(ws, w.act_ff), g.dm), "down");
+        const float* g_mlp = norm_gain(l, true);
+        LKV_CUDA(gemv(g.wo, lw + g.o_wo, EPI_RESID, at<void>(ws, w.act_attn), g.dm,
+                      [&](GemvParams& q) { q.gain_next = g_mlp; }),
+                 "wo");
+        LKV_CUDA(gemv(g.gu, lw + g.o_gu, EPI_SWIGLU, act_h, g.ff, normed), "gate/up");
+        const float* g_next = norm_gain(l + 1, false);
+        LKV_CUDA(gemv(g.down, lw + g.o_down, EPI_RESID, at<void>(ws, w.act_ff), g.dm,
+                      [&](GemvParams& q) { q.gain_next = g_next; }),
+                 "down");
     }
-    LKV_CUDA(launch_norm_pack(x, ss, reinterpret_cast<const float*>(wb + g.final_norm), B, g.dm, eps,
-                              at<void>(ws, w.act_h), w.nbt, g.dtype, s),
-             "final norm");
     GemvParams q = gp;
     q.f_out = logits;
     {
@@ -1382,8 +1397,9 @@ lkv_status lkv_model_decode_step(const lkv_model_desc* m, const void* weights, c
         q.KU = g.lm.KU;
         q.N = g.vocab;
         q.K = g.dm;
-        q.act = at<void>(ws, w.act_h);
+        q.act = act_h;
         q.epi = EPI_F32;
+        q.ss_in = ss;  // final_norm's 1 / rms
         LKV_CUDA(launch_gemv(q, g.dtype, sms, s), "lm_head");
     }
     return LKV_OK;

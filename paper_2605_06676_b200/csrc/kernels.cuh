@@ -206,9 +206,18 @@ struct GemvParams {
     void* v_out;
     const float2* rope;          // [max_seq][head_dim / 2] (cos, sin)
     const int32_t* tokens_seen;  // [B]: the step's absolute position
-    // EPI_RESID: x[b][n] += y; ss_part[group][b] = sum over the group's columns of x^2
+    // EPI_RESID: x[b][n] += y; ss_part[group][b] = sum over the group's columns of x^2; and, when
+    // gain_next is set, the next rmsnorm's activations act_next = x * gain_next (packed bf16 /
+    // row-major f32) -- its 1 / rms factor is applied by the consuming GEMV (ss_in below)
     float* x;
     float* ss_part;
+    const float* gain_next;
+    void* act_next;
+    // any epi, when ss_in is set: y[n][b] *= 1 / sqrt(sum_g ss_in[g][b] / norm_dm + norm_eps), the
+    // rmsnorm scale (model.cpp:48-53) of the activations this GEMV consumed
+    const float* ss_in;
+    int32_t norm_dm;
+    float norm_eps;
     // EPI_SWIGLU: virtual column group g = gate cols [32g, 32g+32) then up cols [32g, 32g+32)
     void* act_out;
     int32_t nbt_out, ff;
@@ -218,10 +227,9 @@ struct GemvParams {
 cudaError_t launch_gemv(const GemvParams& p, int dtype, int num_sms, cudaStream_t stream);
 size_t gemv_max_grid(int num_sms);
 cudaError_t launch_embed(const void* tok_embed, int dtype, const int32_t* tokens, int B, int dm, int vocab,
-                         const int32_t* tokens_seen, int max_seq, float* x, float* ss_part, ErrWord* err,
+                         const int32_t* tokens_seen, int max_seq, float* x, float* ss_part, const float* gain,
+                         void* act, int nbt, ErrWord* err,
                          cudaStream_t stream);
-cudaError_t launch_norm_pack(const float* x, const float* ss_part, const float* gain, int B, int dm, float eps,
-                             void* act, int nbt, int dtype, cudaStream_t stream);
 cudaError_t launch_pack_weight(const void* src, int dtype, int K, int cols, int col_mode, int col_off, int NG, int KU,
                                void* dst, cudaStream_t stream);
 cudaError_t launch_to_f32(const void* src, int dtype, int n, float* dst, cudaStream_t stream);

@@ -22,8 +22,13 @@
 //    reduce across warps in fixed order; a column group cut by a CTA boundary is finished by
 //    the last-arriving CTA, which sums the partials in CTA order (deterministic);
 //  * the epilogue is fused: RoPE + scatter into q / new k / new v (QKV), residual add + the
-//    group's sum of squares for the next rmsnorm (Wo, Wdown), SiLU(gate) * up written straight
-//    into the next GEMV's packed activations (Wgate|Wup interleaved by 32 columns), fp32 logits.
+//    group's sum of squares + x * gain of the next rmsnorm written as the next GEMV's packed
+//    activations (Wo, Wdown), SiLU(gate) * up written straight into the next GEMV's packed
+//    activations (Wgate|Wup interleaved by 32 columns), fp32 logits;
+//  * rmsnorm has no kernel of its own: rmsnorm(x) W = ((x * gain) W) / rms(x), so the GEMV that
+//    consumes a normalised input scales its outputs by 1 / rms, computed from the producer's
+//    per-group sums of squares (the bf16 rounding then applies to x * gain instead of
+//    x * gain / rms -- the same relative error).
 // fp32 models (correctness configs) run a SIMT kernel over plain row-major weights with the
 // same virtual column order and the same epilogues.
 #include <math.h>
@@ -88,9 +93,28 @@ __device__ __forceinline__ void store2(void* base, size_t i, float a, float b) {
     }
 }
 
+// the next rmsnorm's input, x * gain (its 1 / rms is applied by the consuming GEMV's epilogue)
+template <typename T>
+__device__ __forceinline__ void store_norm_act(void* act, int b, int n, int dm, int nbt, float v) {
+    if constexpr (sizeof(T) == 2) static_cast<__nv_bfloat16*>(act)[act_index(b, n, nbt)] = __float2bfloat16_rn(v);
+    else static_cast<float*>(act)[(size_t)b * dm + n] = v;
+}
+
 template <typename T>
 __device__ void gemv_epilogue(const GemvParams& p, int ng, float (*y)[kYPad], int tid, int nthr) {
     const int B = p.B;
+    if (p.ss_in) {  // rmsnorm (model.cpp:48-53) of the consumed activations: W^T (x g / rms) = (W^T x g) / rms
+        __shared__ float s_inv[16];
+        if (tid < B) {
+            const int ngx = (p.norm_dm + 63) / 64;
+            float s = 0.f;
+            for (int gi = 0; gi < ngx; ++gi) s += p.ss_in[(size_t)gi * B + tid];
+            s_inv[tid] = 1.f / sqrtf(s / (float)p.norm_dm + p.norm_eps);
+        }
+        named_sync(1, nthr);
+        for (int e = tid; e < kWsCols * B; e += nthr) y[e & 63][e >> 6] *= s_inv[e >> 6];
+        named_sync(1, nthr);
+    }
     if (p.epi == EPI_QKV) {
         const int D = p.head_dim;
         for (int e = tid; e < 32 * B; e += nthr) {
@@ -125,6 +149,7 @@ __device__ void gemv_epilogue(const GemvParams& p, int ng, float (*y)[kYPad], in
             if (n < p.N) {
                 v = p.x[(size_t)b * p.N + n] + y[nl][b];
                 p.x[(size_t)b * p.N + n] = v;
+                if (p.gain_next) store_norm_act<T>(p.act_next, b, n, p.N, p.nbt, v * p.gain_next[n]);
             }
             y[nl][b] = v * v;
         }
@@ -406,7 +431,7 @@ __global__ void __launch_bounds__(64) gemv_f32_kernel(const __grid_constant__ Ge
 template <typename T>
 __global__ void __launch_bounds__(64) embed_kernel(const T* __restrict__ tab, const int32_t* tokens, int B, int dm,
                                                   int vocab, const int32_t* tokens_seen, int max_seq, float* x,
-                                                  float* ss_part, ErrWord* err) {
+                                                  float* ss_part, const float* gain, void* act, int nbt, ErrWord* err) {
     pdl_trigger();  // let the next GEMV start streaming its weights
     pdl_wait();
     __shared__ float s_w[2];
@@ -423,6 +448,7 @@ __global__ void __launch_bounds__(64) embed_kernel(const T* __restrict__ tab, co
         if constexpr (sizeof(T) == 2) v = __bfloat162float(tab[(size_t)tok * dm + n]);
         else v = tab[(size_t)tok * dm + n];
         x[(size_t)b * dm + n] = v;
+        if (gain) store_norm_act<T>(act, b, n, dm, nbt, v * gain[n]);  // layer 0's attn_norm input
     }
     float s = v * v;
 #pragma unroll
@@ -430,27 +456,6 @@ __global__ void __launch_bounds__(64) embed_kernel(const T* __restrict__ tab, co
     if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = s;
     __syncthreads();
     if (threadIdx.x == 0) ss_part[(size_t)ng * B + b] = s_w[0] + s_w[1];
-}
-
-// ---- rmsnorm (model.cpp:48-53) -> next GEMV's activations ---------------------------------------------
-__global__ void __launch_bounds__(128) norm_pack_kernel(const float* x, const float* ss_part, const float* gain, int B,
-                                                        int dm, float eps, void* act, int nbt, int is_bf16) {
-    pdl_trigger();  // let the next GEMV start streaming its weights
-    pdl_wait();
-    __shared__ float s_inv;
-    const int b = blockIdx.y;
-    if (threadIdx.x == 0) {
-        const int ngx = (dm + 63) / 64;
-        float s = 0.f;
-        for (int gi = 0; gi < ngx; ++gi) s += ss_part[(size_t)gi * B + b];
-        s_inv = 1.f / sqrtf(s / (float)dm + eps);
-    }
-    __syncthreads();
-    const int k = blockIdx.x * 128 + threadIdx.x;
-    if (k >= dm) return;
-    const float h = x[(size_t)b * dm + k] * gain[k] * s_inv;
-    if (is_bf16) static_cast<__nv_bfloat16*>(act)[act_index(b, k, nbt)] = __float2bfloat16_rn(h);
-    else static_cast<float*>(act)[(size_t)b * dm + k] = h;
 }
 
 // ---- weight repacking (once per model load) -----------------------------------------------------------
@@ -530,25 +535,17 @@ cudaError_t launch_gemv(const GemvParams& p, int dtype, int num_sms, cudaStream_
 }
 
 cudaError_t launch_embed(const void* tok_embed, int dtype, const int32_t* tokens, int B, int dm, int vocab,
-                         const int32_t* tokens_seen, int max_seq, float* x, float* ss_part, ErrWord* err,
-                         cudaStream_t stream) {
+                         const int32_t* tokens_seen, int max_seq, float* x, float* ss_part, const float* gain,
+                         void* act, int nbt, ErrWord* err, cudaStream_t stream) {
     const dim3 grid((dm + 63) / 64, B);
     cudaError_t e;
     if (dtype == LKV_BF16)
         e = launch_pdl(embed_kernel<__nv_bfloat16>, grid, dim3(64), 0, stream,
                        static_cast<const __nv_bfloat16*>(tok_embed), tokens, B, dm, vocab, tokens_seen, max_seq, x,
-                       ss_part, err);
+                       ss_part, gain, act, nbt, err);
     else
         e = launch_pdl(embed_kernel<float>, grid, dim3(64), 0, stream, static_cast<const float*>(tok_embed), tokens,
-                       B, dm, vocab, tokens_seen, max_seq, x, ss_part, err);
-    note_launches(1);
-    return e;
-}
-
-cudaError_t launch_norm_pack(const float* x, const float* ss_part, const float* gain, int B, int dm, float eps,
-                             void* act, int nbt, int dtype, cudaStream_t stream) {
-    cudaError_t e = launch_pdl(norm_pack_kernel, dim3((dm + 127) / 128, B), dim3(128), 0, stream, x, ss_part, gain, B,
-                               dm, eps, act, nbt, (int)(dtype == LKV_BF16));
+                       B, dm, vocab, tokens_seen, max_seq, x, ss_part, gain, act, nbt, err);
     note_launches(1);
     return e;
 }
