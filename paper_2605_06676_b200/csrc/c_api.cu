@@ -294,7 +294,7 @@ lkv_status run_select(const lkv_cache_desc* c, const float* scores, const int32_
 
 // ---- decode workspace -------------------------------------------------------------------------------
 struct DecodeWs {
-    size_t err, n_items, ch, layer_begin, item_base, items, part_m, part_l, part_o, total;
+    size_t err, n_items, ch, layer_begin, item_base, new_len, items, part_m, part_l, part_o, total;
     int64_t max_items;
 };
 DecodeWs decode_layout(const lkv_ragged_desc* r, int G) {
@@ -310,6 +310,8 @@ DecodeWs decode_layout(const lkv_ragged_desc* r, int G) {
     w.layer_begin = o;  // [n_layers + 1] of the plan (n_layers <= n_heads)
     o = align_up(o + sizeof(int32_t) * ((size_t)r->n_heads + 1));
     w.item_base = o;
+    o = align_up(o + sizeof(int32_t) * (size_t)r->n_heads);
+    w.new_len = o;
     o = align_up(o + sizeof(int32_t) * (size_t)r->n_heads);
     w.items = o;
     o = align_up(o + sizeof(DecodeItem) * (size_t)w.max_items);
@@ -1050,6 +1052,7 @@ lkv_status lkv_decode_step(const lkv_ragged_desc* r, int32_t n_seq, int32_t n_la
     p.part_m = at<float>(ws, w.part_m);
     p.part_l = at<float>(ws, w.part_l);
     p.part_o = at<float>(ws, w.part_o);
+    p.new_len = at<int32_t>(ws, w.new_len);
     p.err = at<ErrWord>(ws, w.err);
     CUtensorMap mk, mv;
     if (r->dtype == LKV_BF16) {
@@ -1347,6 +1350,7 @@ lkv_status lkv_model_decode_step(const lkv_model_desc* m, const void* weights, c
     dp.part_m = at<float>(ws, w.dec.part_m);
     dp.part_l = at<float>(ws, w.dec.part_l);
     dp.part_o = at<float>(ws, w.dec.part_o);
+    dp.new_len = at<int32_t>(ws, w.dec.new_len);
     dp.err = err;
     CUtensorMap mk, mv;
     if (g.dtype == LKV_BF16) {

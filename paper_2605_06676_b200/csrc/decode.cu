@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(1024) decode_plan_kernel(const int64_t* offset
             const int s = r / n_kv, kh = r - s * n_kv;
             h = (s * n_layers + l) * n_kv + kh;
             const int64_t cap = offsets[h + 1] - offsets[h];
-            nch = (uint32_t)((cap + ch - 1) / ch);
+            nch = (uint32_t)(cap > 0 ? (cap + ch - 1) / ch : 1);  // >= 1: chunk 0 checks every append
         }
         uint32_t tot;
         const uint32_t ex = block_exclusive_scan<1024>(nch, s_scan, &tot);
@@ -254,6 +254,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
         const int len_old = p.lens[head];
         const int len_new = len_old + 1;
         const int r0 = wi.chunk * ch;
+        if (wi.chunk == 0 && threadIdx.x == 0) p.new_len[head] = len_new;  // for the combine (never reads lens)
         if (r0 >= len_new) continue;
         const int rows = min(ch, len_new - r0);
         const int64_t off = p.offsets[head];
@@ -472,6 +473,7 @@ __global__ void __launch_bounds__(kDecSimtThreads) decode_attn_f32_kernel(const 
     const int len_old = p.lens[head];
     const int len_new = len_old + 1;
     const int r0 = wi.chunk * ch;
+    if (wi.chunk == 0 && threadIdx.x == 0) p.new_len[head] = len_new;  // for the combine
     if (r0 >= len_new) return;
     const int rows = min(ch, len_new - r0);
     const int64_t off = p.offsets[head];
@@ -529,14 +531,17 @@ __global__ void __launch_bounds__(kDecSimtThreads) decode_attn_f32_kernel(const 
 }
 
 // ---- combine split-K partials; advance lens and tokens_seen ------------------------------------------
-// One CTA per head.  Phase 1 turns the chunk maxima / sums into per-chunk weights in
-// shared memory; phase 2 streams the partial outputs with independent (unrolled) loads.
+// One CTA per (head, 128 outputs).  Phase 1 turns the chunk maxima / sums into per-chunk weights in
+// shared memory; phase 2 streams the partial outputs with independent (unrolled) loads, the
+// chunks split over kCombSlices thread slices (a head's chunk count follows its budget, so a
+// long head would otherwise set the kernel's latency) and the slices summed in fixed order.
 // Heads that fit one chunk were finalised by the attention kernel (bf16 path).
-constexpr int kCombThreads = 128;
+constexpr int kCombCols = 128;    // outputs per CTA
 
-template <typename T>
-__global__ void __launch_bounds__(kCombThreads) decode_combine_kernel(const __grid_constant__ DecodeParams p,
-                                                                      int single_chunk_done) {
+template <typename T, int kCombSlices>  // chunk slices per output: 4 for a few heads, else 1
+__global__ void __launch_bounds__(kCombCols * kCombSlices) decode_combine_kernel(const __grid_constant__ DecodeParams p,
+                                                                                int single_chunk_done) {
+    constexpr int kCombThreads = kCombCols * kCombSlices;
     pdl_trigger();  // the next GEMV may start streaming its weights
     pdl_wait();
     __shared__ float s_w[kCombMaxChunks];  // [c * G + g] weight exp2(m_c - M_g) / L_g
@@ -547,7 +552,9 @@ __global__ void __launch_bounds__(kCombThreads) decode_combine_kernel(const __gr
     const int js = jr / p.n_kv_heads;
     const int head = (js * p.n_layers + p.layer0 + jl) * p.n_kv_heads + (jr - js * p.n_kv_heads);
     const int D = p.head_dim, G = p.G;
-    const int len_new = p.lens[head] + 1;
+    // the length the attention kernel saw: lens[head] itself is advanced below by the y = 0 CTA
+    // while other CTAs of the head may not have started (so it is never read here)
+    const int len_new = p.new_len[head];
     const int ch = *p.ch;
     const int nch = (len_new + ch - 1) / ch;
     if (!(single_chunk_done && nch == 1) && nch * G <= kCombMaxChunks) {
@@ -590,29 +597,52 @@ __global__ void __launch_bounds__(kCombThreads) decode_combine_kernel(const __gr
         __syncthreads();
         const HeadCoord hc = head_coord(p, head);
         T* out = static_cast<T*>(p.out);
-        // grid.y tiles the G*D outputs: one element per thread, all chunk loads in flight
-        const int e = blockIdx.y * kCombThreads + threadIdx.x;
+        // grid.y tiles the G*D outputs.  Chunk c is summed into partial c % 4 and the four partials
+        // are added in order, whether one thread holds all four (kCombSlices = 1) or slice sl of
+        // the threads holds partial sl (kCombSlices = 4): the result does not depend on the launch
+        // shape.  A thread's 16 chunk loads of a block are in flight together.
+        static_assert(kCombSlices == 1 || kCombSlices == 4, "combine slices");
+        constexpr int S = kCombSlices;
+        __shared__ float s_part[S][kCombCols];
+        const int col = threadIdx.x % kCombCols, sl = threadIdx.x / kCombCols;
+        const int e = blockIdx.y * kCombCols + col;
+        const int g = min(e, G * D - 1) / D;
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
         if (e < G * D) {
-            const int g = e / D;
-            float acc = 0.f;
-            int c = 0;
-            for (; c + 16 <= nch; c += 16) {
+            int c = sl;
+            for (; c + 15 * S < nch; c += 16 * S) {
                 float v[16];
 #pragma unroll
-                for (int k = 0; k < 16; ++k) v[k] = po[(size_t)(c + k) * G * D + e];
+                for (int k = 0; k < 16; ++k) v[k] = po[(size_t)(c + k * S) * G * D + e];
 #pragma unroll
-                for (int k = 0; k < 16; ++k) acc = fmaf(v[k], s_w[(c + k) * G + g], acc);
+                for (int k = 0; k < 16; ++k) {
+                    float& a = acc[S == 4 ? 0 : (k & 3)];
+                    a = fmaf(v[k], s_w[(c + k * S) * G + g], a);
+                }
             }
             float v[16];
 #pragma unroll
             for (int k = 0; k < 16; ++k)
-                if (c + k < nch) v[k] = po[(size_t)(c + k) * G * D + e];
+                if (c + k * S < nch) v[k] = po[(size_t)(c + k * S) * G * D + e];
 #pragma unroll
             for (int k = 0; k < 16; ++k)
-                if (c + k < nch) acc = fmaf(v[k], s_w[(c + k) * G + g], acc);
+                if (c + k * S < nch) {
+                    float& a = acc[S == 4 ? 0 : (k & 3)];
+                    a = fmaf(v[k], s_w[(c + k * S) * G + g], a);
+                }
+        }
+        float sum;
+        if constexpr (S == 4) {
+            s_part[sl][col] = acc[0];
+            __syncthreads();
+            sum = ((s_part[0][col] + s_part[1][col]) + s_part[2][col]) + s_part[3][col];
+        } else {
+            sum = ((acc[0] + acc[1]) + acc[2]) + acc[3];
+        }
+        if (sl == 0 && e < G * D) {
             const size_t oi = out_index(p, hc, g, e - g * D);
-            if constexpr (sizeof(T) == 2) out[oi] = __float2bfloat16_rn(acc);
-            else out[oi] = acc;
+            if constexpr (sizeof(T) == 2) out[oi] = __float2bfloat16_rn(sum);
+            else out[oi] = sum;
         }
     } else if (nch * G > kCombMaxChunks && threadIdx.x == 0 && blockIdx.y == 0) {
         latch_error(p.err, LKV_ERR_UNSUPPORTED, head);
@@ -655,9 +685,12 @@ cudaError_t launch_decode(const DecodeParams& p, int dtype, const CUtensorMap* m
         const int grid = min(p.max_items, per_sm * num_sms);
         e = launch_pdl(kern, dim3(grid), dim3(kDecThreads), smem, stream, p, *mk, *mv);
         if (e != cudaSuccess) return e;
-        e = launch_pdl(decode_combine_kernel<__nv_bfloat16>,
-                       dim3(p.n_seq * p.q_layers * p.n_kv_heads, (p.G * p.head_dim + kCombThreads - 1) / kCombThreads), dim3(kCombThreads), 0,
-                       stream, p, 1);
+        const dim3 cgrid(p.n_seq * p.q_layers * p.n_kv_heads, (p.G * p.head_dim + kCombCols - 1) / kCombCols);
+        // few heads (a per-layer launch): split each head's chunks over 4 thread slices
+        if (cgrid.x * cgrid.y < (unsigned)num_sms)
+            e = launch_pdl(decode_combine_kernel<__nv_bfloat16, 4>, cgrid, dim3(kCombCols * 4), 0, stream, p, 1);
+        else
+            e = launch_pdl(decode_combine_kernel<__nv_bfloat16, 1>, cgrid, dim3(kCombCols), 0, stream, p, 1);
         if (e != cudaSuccess) return e;
         note_launches(2);
     } else {
@@ -667,7 +700,7 @@ cudaError_t launch_decode(const DecodeParams& p, int dtype, const CUtensorMap* m
         decode_attn_f32_kernel<<<p.max_items, kDecSimtThreads, smem, stream>>>(p);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
-        decode_combine_kernel<float><<<dim3(p.n_seq * p.q_layers * p.n_kv_heads, (p.G * p.head_dim + kCombThreads - 1) / kCombThreads), kCombThreads, 0, stream>>>(p, 0);
+        decode_combine_kernel<float, 1><<<dim3(p.n_seq * p.q_layers * p.n_kv_heads, (p.G * p.head_dim + kCombCols - 1) / kCombCols), kCombCols, 0, stream>>>(p, 0);
         note_launches(2);
     }
     return cudaGetLastError();

@@ -129,6 +129,7 @@ struct DecodeParams {
     float* part_m;
     float* part_l;
     float* part_o;
+    int32_t* new_len;  // [n_heads] lens + 1 as the attention kernel read it (chunk 0 writes it)
     ErrWord* err;
 };
 cudaError_t launch_decode_plan(const int64_t* offsets, int n_seq, int n_layers, int n_kv, DecodeItem* items,
