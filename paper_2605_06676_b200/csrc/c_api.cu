@@ -141,7 +141,7 @@ int64_t n_heads_of(const lkv_cache_desc* c) { return (int64_t)c->n_seq * c->n_la
 
 // ---- workspace layout -----------------------------------------------------------------------------
 struct EvictWs {
-    size_t err, ratios, budgets, budgets_all, scores, hist, state, chunk_gt, chunk_out, chunk_eqb, cands, total;
+    size_t err, ratios, budgets, budgets_all, scores, hist, state, chunk_out, chunk_eqb, cands, total;
 };
 
 EvictWs evict_layout(const lkv_cache_desc* c, int n_logits) {
@@ -164,8 +164,6 @@ EvictWs evict_layout(const lkv_cache_desc* c, int n_logits) {
     o = align_up(o + sizeof(uint32_t) * 2048 * (size_t)H);
     w.state = o;
     o = align_up(o + sizeof(HeadSel) * (size_t)H);
-    w.chunk_gt = o;
-    o = align_up(o + sizeof(uint32_t) * (size_t)chunks);
     w.chunk_out = o;
     o = align_up(o + sizeof(uint32_t) * (size_t)chunks);
     w.chunk_eqb = o;
@@ -273,7 +271,6 @@ lkv_status run_select(const lkv_cache_desc* c, const float* scores, const int32_
     p.budgets = budgets + h0;
     p.hist = at<uint32_t>(ws, w.hist) + h0 * 2048;
     p.state = at<HeadSel>(ws, w.state) + h0;
-    p.chunk_gt = at<uint32_t>(ws, w.chunk_gt) + chunk0;
     p.chunk_out = at<uint32_t>(ws, w.chunk_out) + chunk0;
     p.chunk_eqb = at<uint32_t>(ws, w.chunk_eqb) + chunk0;
     p.cands = at<uint32_t>(ws, w.cands) + h0 * c->max_tokens;
@@ -1376,20 +1373,21 @@ lkv_status lkv_model_decode_step(const lkv_model_desc* m, const void* weights, c
     gp.norm_eps = (float)m->norm_eps;
     gp.act_next = act_h;
     auto normed = [&](GemvParams& q) { q.ss_in = ss; };
+    static const int mx = getenv("LKV_MODEL_EXPT") ? atoi(getenv("LKV_MODEL_EXPT")) : 0;  // timing knobs
     for (int l = 0; l < g.L; ++l) {
         const unsigned char* lw = wb + g.layer0 + (size_t)l * g.layer_stride;
-        LKV_CUDA(gemv(g.qkv, lw + g.o_qkv, EPI_QKV, act_h, g.dm + 2 * g.dkv, normed), "qkv");
+        if (!(mx & 4)) LKV_CUDA(gemv(g.qkv, lw + g.o_qkv, EPI_QKV, act_h, g.dm + 2 * g.dkv, normed), "qkv");
         dp.layer0 = l;
         dp.item_lo = lbeg + l;
         dp.item_hi = lbeg + l + 1;
-        LKV_CUDA(launch_decode(dp, g.dtype, &mk, &mv, sms, s), "attention");
+        if (!(mx & 2)) LKV_CUDA(launch_decode(dp, g.dtype, &mk, &mv, sms, s), "attention");
         const float* g_mlp = norm_gain(l, true);
-        LKV_CUDA(gemv(g.wo, lw + g.o_wo, EPI_RESID, at<void>(ws, w.act_attn), g.dm,
+        if (!(mx & 8)) LKV_CUDA(gemv(g.wo, lw + g.o_wo, EPI_RESID, at<void>(ws, w.act_attn), g.dm,
                       [&](GemvParams& q) { q.gain_next = g_mlp; }),
                  "wo");
-        LKV_CUDA(gemv(g.gu, lw + g.o_gu, EPI_SWIGLU, act_h, g.ff, normed), "gate/up");
+        if (!(mx & 16)) LKV_CUDA(gemv(g.gu, lw + g.o_gu, EPI_SWIGLU, act_h, g.ff, normed), "gate/up");
         const float* g_next = norm_gain(l + 1, false);
-        LKV_CUDA(gemv(g.down, lw + g.o_down, EPI_RESID, at<void>(ws, w.act_ff), g.dm,
+        if (!(mx & 32)) LKV_CUDA(gemv(g.down, lw + g.o_down, EPI_RESID, at<void>(ws, w.act_ff), g.dm,
                       [&](GemvParams& q) { q.gain_next = g_next; }),
                  "down");
     }

@@ -51,8 +51,8 @@ cudaError_t launch_score_tc(ScoreParams p, const CUtensorMap& mk, const CUtensor
 bool score_tc_supported(int dtype, int head_dim, int hidden, int in_mode);
 size_t score_simt_smem_bytes(int in, int hidden);
 // ---- select.cu (K3 + K4)
-struct HeadSel {
-    uint32_t mode, bin1, rem1, n_cand, key_t, need_eq, pad[2];
+struct HeadSel {  // per-head top-k result of select_plan_kernel, read by the emit pass
+    uint32_t mode, key_t, need_eq, pad;
 };
 struct SelectParams {
     SeqTable seq;
@@ -60,7 +60,6 @@ struct SelectParams {
     const int32_t* budgets;
     uint32_t* hist;
     HeadSel* state;
-    uint32_t* chunk_gt;
     uint32_t* chunk_out;
     uint32_t* chunk_eqb;
     uint32_t* cands;

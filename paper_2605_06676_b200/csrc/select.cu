@@ -8,12 +8,14 @@
 //
 // Algorithm (HBM-bound, 12 bytes/row of score traffic):
 //   S1 hist     per 4096-row chunk: 2048-bin histogram of the top 11 key bits
-//   S2 resolve1 per head: the bin holding the b-th largest key
-//   S3 collect  per chunk: count rows above that bin; append rows inside it
+//               (fused into K1's epilogue on the tcgen05 path)
+//   S2-S4 plan  one CTA per head (select_plan_kernel):
+//     S2        the bin holding the b-th largest key
+//     S3        count rows above that bin per chunk; append rows inside it
 //               (the candidates, usually a few % of t) to a per-head list
-//   S4 resolve2 per head: radix-select the remaining 21 bits over the
-//               candidates -> exact threshold key T and the number of T-equal
-//               rows still needed; per-chunk output offsets by a chunk scan
+//     S4        radix-select the remaining 21 bits over the candidates ->
+//               exact threshold key T and the number of T-equal rows still
+//               needed; per-chunk output offsets by a chunk scan
 //   S5 emit     per chunk: keep key > T, or key == T while the running equal
 //               rank (index order) is below the need; block scans give each
 //               kept row its slot; optionally gather its K/V rows (16-byte
@@ -129,162 +131,225 @@ __device__ void find_bin_from_top(const uint32_t* cnt /*smem*/, int nbins, uint3
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(1024) select_resolve1_kernel(const __grid_constant__ SelectParams p) {
+// ---- S2-S4 fused: one CTA per head -------------------------------------------------------------
+// S2: the bin holding the b-th largest key, from the histogram K1 (or S1) built.  S3: one pass over
+// the head's scores (4 rows per thread per 4096-row chunk, 8 chunks of loads in flight): rows
+// above that bin are counted per chunk in shared memory, rows inside it appended to the head's
+// candidate list (warp-aggregated).  S4: radix-select the remaining 21 bits over the candidates
+// -> exact threshold key T and the number of T-equal rows still needed, then the per-chunk output
+// offsets by a chunk scan.  No global round trip between the phases (they were three launches).
+constexpr int kPlanThreads = 512;   // 2 CTAs / SM: one wave for a few hundred heads
+constexpr int kPlanRows = kChunk / kPlanThreads;  // 8 rows of a chunk per thread (two float4)
+constexpr int kPlanBatch = 4;       // chunks of loads in flight per thread
+constexpr int kCandCap = 8192;      // candidates kept in shared memory (the rest go to the global list)
+constexpr size_t kPlanSmem = 2 * sizeof(uint32_t) * kCandCap;  // dynamic: positions + keys
+
+__global__ void __launch_bounds__(kPlanThreads, 2) select_plan_kernel(const __grid_constant__ SelectParams p) {
     pdl_wait();
     __shared__ uint32_t cnt[2048];
+    __shared__ uint32_t c_gt[kMaxChunksPerHead];
+    __shared__ uint32_t c_eq[kMaxChunksPerHead];
+    extern __shared__ uint32_t plan_dyn[];
+    uint32_t* s_cpos = plan_dyn;
+    uint32_t* s_ckey = plan_dyn + kCandCap;
     __shared__ uint32_t s_scan[33];
-    __shared__ uint32_t s_bin, s_above;
+    __shared__ uint32_t s_bin, s_above, s_ncand;
     const int head = blockIdx.x;
-    const int t = head_len(p, head);
+    const int s_idx = head_seq(p.seq, head);
+    const int t = p.seq.len[s_idx];
     const int b = p.budgets[head];
     HeadSel* st = p.state + head;
     if (b < 0 || b > t) {  // budget outside [0, t] (hard_topk, soft_topk.cpp:193)
         if (threadIdx.x == 0) latch_error(p.err, LKV_ERR_BUDGET, head);
         return;
     }
-    if (b == 0 || b == t) {
-        if (threadIdx.x == 0) {
-            st->mode = b == 0 ? kModeNone : kModeAll;
-            st->n_cand = 0;
-        }
-        return;
-    }
-    const uint32_t* gh = p.hist + (size_t)head * 2048;
-    for (int i = threadIdx.x; i < 2048; i += 1024) cnt[i] = gh[i];
-    __syncthreads();
-    find_bin_from_top<1024>(cnt, 2048, (uint32_t)b, s_scan, &s_bin, &s_above);
-    if (threadIdx.x == 0) {
-        st->mode = kModeNormal;
-        st->bin1 = s_bin;
-        st->rem1 = (uint32_t)b - s_above;
-        st->n_cand = 0;
-    }
-}
-
-// ---- S3 --------------------------------------------------------------------------
-// One pass over the chunk's scores (16 contiguous rows per thread, loads batched for
-// memory-level parallelism): rows above bin1 are counted, rows inside bin1 are appended
-// to the head's candidate list with one atomic per block.
-__global__ void __launch_bounds__(kSelThreads) select_collect_kernel(const __grid_constant__ SelectParams p) {
-    pdl_wait();
-    __shared__ uint32_t s_scan[kSelThreads / 32 + 1];
-    __shared__ uint32_t s_base;
-    const ChunkInfo ci = decode_chunk(p, blockIdx.x);
-    HeadSel* st = p.state + ci.head;
-    const int b = p.budgets[ci.head];
-    if (b < 0 || b > ci.t) return;
-    const uint32_t mode = st->mode;
-    if (mode != kModeNormal) {
-        if (threadIdx.x == 0) p.chunk_gt[blockIdx.x] = mode == kModeAll ? (uint32_t)ci.n : 0u;
-        return;
-    }
-    const uint32_t bin1 = st->bin1;
-    const float* sc = p.scores + (size_t)ci.head * p.seq.T + ci.c0;
-    const int j0 = threadIdx.x * kPerThread;
-    uint32_t dig[kPerThread];
-    load_keys16(sc, j0, ci.n, dig);
-#pragma unroll
-    for (int q = 0; q < kPerThread; ++q) dig[q] >>= 21;
-    uint32_t gt = 0, nc = 0;
-#pragma unroll
-    for (int q = 0; q < kPerThread; ++q) {
-        const bool valid = j0 + q < ci.n;
-        gt += valid && dig[q] > bin1;
-        nc += valid && dig[q] == bin1;
-    }
-    uint32_t tot_c, tot_gt;
-    uint32_t slot = block_exclusive_scan<kSelThreads>(nc, s_scan, &tot_c);
-    block_exclusive_scan<kSelThreads>(gt, s_scan, &tot_gt);
-    if (threadIdx.x == 0) {
-        p.chunk_gt[blockIdx.x] = tot_gt;
-        s_base = tot_c ? atomicAdd(&st->n_cand, tot_c) : 0u;
-    }
-    __syncthreads();
-    if (nc) {
-        uint32_t* cand = p.cands + (size_t)ci.head * p.seq.T + s_base;
-#pragma unroll
-        for (int q = 0; q < kPerThread; ++q)
-            if (j0 + q < ci.n && dig[q] == bin1) cand[slot++] = (uint32_t)(ci.c0 + j0 + q);
-    }
-}
-
-// ---- S4 --------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) select_resolve2_kernel(const __grid_constant__ SelectParams p) {
-    pdl_wait();
-    __shared__ uint32_t cnt[2048];
-    __shared__ uint32_t c_gt[kMaxChunksPerHead];
-    __shared__ uint32_t c_eq[kMaxChunksPerHead];
-    __shared__ uint32_t s_scan[33];
-    __shared__ uint32_t s_bin, s_above;
-    const int head = blockIdx.x;
-    const int s_idx = head_seq(p.seq, head);
-    const int t = p.seq.len[s_idx];
-    const int b = p.budgets[head];
-    if (b < 0 || b > t) return;
-    HeadSel* st = p.state + head;
     const int cph = (t + kChunk - 1) / kChunk;
     const int hs = head - s_idx * p.seq.n_layers * p.seq.n_kv_heads;
     const int cbase = p.chunk_base[s_idx] + hs * cph;
-    const uint32_t mode = st->mode;
-    uint32_t key_t = 0, need_eq = 0;
-
-    for (int c = threadIdx.x; c < cph; c += 1024) {
+    const uint32_t mode = b == 0 ? kModeNone : (b == t ? kModeAll : kModeNormal);
+    const int tid = threadIdx.x, lane = tid & 31;
+    for (int c = tid; c < cph; c += kPlanThreads) {
         c_gt[c] = 0;
         c_eq[c] = 0;
     }
+    if (tid == 0) s_ncand = 0;
+    uint32_t key_t = 0, need_eq = 0;
     if (mode == kModeNormal) {
-        const uint32_t n_cand = st->n_cand;
-        const uint32_t bin1 = st->bin1;
-        uint32_t rem = st->rem1;
+        // S2
+        const uint32_t* gh = p.hist + (size_t)head * 2048;
+        {
+            uint32_t hv[2048 / kPlanThreads];  // all loads in flight before the stores
+#pragma unroll
+            for (int q = 0; q < 2048 / kPlanThreads; ++q) hv[q] = gh[tid + q * kPlanThreads];
+#pragma unroll
+            for (int q = 0; q < 2048 / kPlanThreads; ++q) cnt[tid + q * kPlanThreads] = hv[q];
+        }
+        __syncthreads();
+        find_bin_from_top<kPlanThreads>(cnt, 2048, (uint32_t)b, s_scan, &s_bin, &s_above);
+        const uint32_t bin1 = s_bin;
+        uint32_t rem = (uint32_t)b - s_above;
+        // S3
         const float* sc = p.scores + (size_t)head * p.seq.T;
-        const uint32_t* cand = p.cands + (size_t)head * p.seq.T;
-        // pass A: key bits [10, 21)
-        for (int i = threadIdx.x; i < 2048; i += 1024) cnt[i] = 0;
+        uint32_t* cand = p.cands + (size_t)head * p.seq.T;  // overflow past kCandCap
+        // 16-byte loads when every head's scores are 16-byte aligned: branch-free (the address
+        // clamped into the head's row stride, rows >= t masked) so a batch's loads are all issued
+        // before the first use
+        const int T = p.seq.T;
+        const bool vec = ((reinterpret_cast<uintptr_t>(sc)) & 15) == 0 && (T & 3) == 0;
+        for (int c0 = 0; c0 < cph; c0 += kPlanBatch) {
+            uint32_t k[kPlanBatch][kPlanRows], valid[kPlanBatch];
+            if (vec) {
+                float4 f[kPlanBatch][2];
+#pragma unroll
+                for (int u = 0; u < kPlanBatch; ++u)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int r = min((c0 + u) * kChunk + tid * kPlanRows + 4 * h, T - 4);
+                        f[u][h] = __ldg(reinterpret_cast<const float4*>(sc + r));
+                    }
+#pragma unroll
+                for (int u = 0; u < kPlanBatch; ++u) {
+                    const int r = (c0 + u) * kChunk + tid * kPlanRows;
+                    valid[u] = 0;
+#pragma unroll
+                    for (int q = 0; q < kPlanRows; ++q) valid[u] |= uint32_t(c0 + u < cph && r + q < t) << q;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        k[u][4 * h + 0] = f32_key(f[u][h].x);
+                        k[u][4 * h + 1] = f32_key(f[u][h].y);
+                        k[u][4 * h + 2] = f32_key(f[u][h].z);
+                        k[u][4 * h + 3] = f32_key(f[u][h].w);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < kPlanBatch; ++u) {
+                    valid[u] = 0;
+                    const int r = (c0 + u) * kChunk + tid * kPlanRows;
+#pragma unroll
+                    for (int q = 0; q < kPlanRows; ++q) {
+                        const bool ok = c0 + u < cph && r + q < t;
+                        k[u][q] = ok ? f32_key(__ldg(sc + r + q)) : 0u;
+                        valid[u] |= uint32_t(ok) << q;
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kPlanBatch; ++u) {
+                if (c0 + u >= cph) break;
+                uint32_t gt = 0, cm = 0;  // rows above bin1; bit mask of the rows inside it
+#pragma unroll
+                for (int q = 0; q < kPlanRows; ++q) {
+                    const uint32_t d = k[u][q] >> 21;
+                    const bool v = valid[u] >> q & 1u;
+                    gt += v && d > bin1;
+                    cm |= uint32_t(v && d == bin1) << q;
+                }
+                const uint32_t wgt = __reduce_add_sync(0xffffffffu, gt);
+                if (lane == 0 && wgt) atomicAdd(&c_gt[c0 + u], wgt);
+                // warp-aggregated append of the in-bin rows (position and key)
+                const uint32_t nc = __popc(cm);
+                uint32_t incl = nc;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
+                if (wtot) {
+                    uint32_t base = 0;
+                    if (lane == 31) base = atomicAdd(&s_ncand, wtot);
+                    base = __shfl_sync(0xffffffffu, base, 31) + incl - nc;
+                    const uint32_t r0 = (uint32_t)((c0 + u) * kChunk + tid * kPlanRows);
+                    while (cm) {  // only the rows inside the bin (a few % of them)
+                        const int q = __ffs(cm) - 1;
+                        cm &= cm - 1;
+                        uint32_t key = k[u][0];
+#pragma unroll
+                        for (int z = 1; z < kPlanRows; ++z) key = q == z ? k[u][z] : key;  // no local-memory indexing
+                        if (base < kCandCap) {
+                            s_cpos[base] = r0 + q;
+                            s_ckey[base] = key;
+                        } else {
+                            cand[base - kCandCap] = r0 + q;
+                        }
+                        ++base;
+                    }
+                }
+            }
+        }
         __syncthreads();
-        for (uint32_t i = threadIdx.x; i < n_cand; i += 1024) atomicAdd(&cnt[(f32_key(sc[cand[i]]) >> 10) & 2047u], 1u);
+        const uint32_t n_cand = s_ncand;
+        auto cand_key = [&](uint32_t i) -> uint32_t {
+            return i < kCandCap ? s_ckey[i] : f32_key(sc[cand[i - kCandCap]]);
+        };
+        // S4 pass A: key bits [10, 21) among the candidates
+        for (int i = tid; i < 2048; i += kPlanThreads) cnt[i] = 0;
         __syncthreads();
-        find_bin_from_top<1024>(cnt, 2048, rem, s_scan, &s_bin, &s_above);
+        for (uint32_t i = tid; i < n_cand; i += kPlanThreads) atomicAdd(&cnt[(cand_key(i) >> 10) & 2047u], 1u);
+        __syncthreads();
+        find_bin_from_top<kPlanThreads>(cnt, 2048, rem, s_scan, &s_bin, &s_above);
         const uint32_t binA = s_bin;
         rem -= s_above;
         // pass B: key bits [0, 10) among candidates in binA
-        for (int i = threadIdx.x; i < 1024; i += 1024) cnt[i] = 0;
+        for (int i = tid; i < 1024; i += kPlanThreads) cnt[i] = 0;
         __syncthreads();
-        for (uint32_t i = threadIdx.x; i < n_cand; i += 1024) {
-            const uint32_t k = f32_key(sc[cand[i]]);
-            if (((k >> 10) & 2047u) == binA) atomicAdd(&cnt[k & 1023u], 1u);
+        for (uint32_t i = tid; i < n_cand; i += kPlanThreads) {
+            const uint32_t kk = cand_key(i);
+            if (((kk >> 10) & 2047u) == binA) atomicAdd(&cnt[kk & 1023u], 1u);
         }
         __syncthreads();
-        find_bin_from_top<1024>(cnt, 1024, rem, s_scan, &s_bin, &s_above);
+        find_bin_from_top<kPlanThreads>(cnt, 1024, rem, s_scan, &s_bin, &s_above);
         key_t = (bin1 << 21) | (binA << 10) | s_bin;
         need_eq = rem - s_above;
-        // per-chunk: candidates strictly above T, and equal to T
-        for (uint32_t i = threadIdx.x; i < n_cand; i += 1024) {
-            const uint32_t pos = cand[i];
-            const uint32_t k = f32_key(sc[pos]);
-            if (k > key_t) atomicAdd(&c_gt[pos / kChunk], 1u);
-            else if (k == key_t) atomicAdd(&c_eq[pos / kChunk], 1u);
+        // per chunk: candidates strictly above T, and equal to T (the list is roughly in chunk
+        // order, so lanes mostly agree on the chunk: one atomic per (warp, chunk, kind))
+        for (uint32_t i0 = 0; i0 < n_cand; i0 += kPlanThreads) {
+            const uint32_t i = i0 + tid;
+            int kind = -1;  // 0: above T, 1: equal to T
+            uint32_t ch = 0;
+            if (i < n_cand) {
+                const uint32_t pos = i < kCandCap ? s_cpos[i] : cand[i - kCandCap];
+                const uint32_t kk = cand_key(i);
+                ch = pos / kChunk;
+                kind = kk > key_t ? 0 : (kk == key_t ? 1 : -1);
+            }
+            const uint32_t grp = __match_any_sync(0xffffffffu, kind < 0 ? 0xffffffffu : (ch << 1) | (uint32_t)kind);
+            if (kind >= 0 && lane == __ffs(grp) - 1) atomicAdd(kind ? &c_eq[ch] : &c_gt[ch], (uint32_t)__popc(grp));
         }
     }
     __syncthreads();
-    // chunk scan (cph <= 1024): eq_before and out_base in index order
-    const int c = threadIdx.x;
-    uint32_t gt = 0, eq = 0;
-    if (c < cph) {
-        if (mode == kModeAll) gt = (uint32_t)min(kChunk, t - c * kChunk);
-        else if (mode == kModeNormal) gt = p.chunk_gt[cbase + c] + c_gt[c];
-        eq = c_eq[c];
+    // chunk scan (cph <= 1024): eq_before and out_base in index order, two chunks per thread
+    uint32_t gt2[2] = {0, 0}, eq2[2] = {0, 0};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int c = tid * 2 + h;
+        if (c < cph) {
+            if (mode == kModeAll) gt2[h] = (uint32_t)min(kChunk, t - c * kChunk);
+            else if (mode == kModeNormal) gt2[h] = c_gt[c];
+            eq2[h] = c_eq[c];
+        }
     }
     uint32_t tot;
-    const uint32_t eqb = block_exclusive_scan<1024>(eq, s_scan, &tot);
-    uint32_t take = 0;
-    if (need_eq > eqb) take = min(need_eq - eqb, eq);
-    const uint32_t kept = gt + take;
-    const uint32_t ob = block_exclusive_scan<1024>(kept, s_scan, &tot);
-    if (c < cph) {
-        p.chunk_out[cbase + c] = ob;
-        p.chunk_eqb[cbase + c] = eqb;
+    const uint32_t eqb0 = block_exclusive_scan<kPlanThreads>(eq2[0] + eq2[1], s_scan, &tot);
+    uint32_t kept2[2], eqb2[2] = {eqb0, eqb0 + eq2[0]};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        uint32_t take = 0;
+        if (need_eq > eqb2[h]) take = min(need_eq - eqb2[h], eq2[h]);
+        kept2[h] = gt2[h] + take;
     }
-    if (threadIdx.x == 0) {
+    const uint32_t ob0 = block_exclusive_scan<kPlanThreads>(kept2[0] + kept2[1], s_scan, &tot);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int c = tid * 2 + h;
+        if (c < cph) {
+            p.chunk_out[cbase + c] = ob0 + (h ? kept2[0] : 0u);
+            p.chunk_eqb[cbase + c] = eqb2[h];
+        }
+    }
+    if (tid == 0) {
+        st->mode = mode;
         st->key_t = key_t;
         st->need_eq = need_eq;
         p.out_lens[head] = b;
@@ -438,11 +503,12 @@ cudaError_t launch_select(SelectParams p, int n_heads, cudaStream_t stream) {
         note_launches(1);
     }
     cudaError_t e;
-    if ((e = launch_pdl(select_resolve1_kernel, dim3(n_heads), dim3(1024), 0, stream, p)) != cudaSuccess) return e;
-    if ((e = launch_pdl(select_collect_kernel, dim3(chunks), dim3(kSelThreads), 0, stream, p)) != cudaSuccess) return e;
-    if ((e = launch_pdl(select_resolve2_kernel, dim3(n_heads), dim3(1024), 0, stream, p)) != cudaSuccess) return e;
+    const cudaError_t attr =
+        cudaFuncSetAttribute(select_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPlanSmem);
+    if (attr != cudaSuccess) return attr;
+    if ((e = launch_pdl(select_plan_kernel, dim3(n_heads), dim3(kPlanThreads), kPlanSmem, stream, p)) != cudaSuccess) return e;
     if ((e = launch_pdl(select_emit_kernel, dim3(chunks), dim3(kSelThreads), 0, stream, p)) != cudaSuccess) return e;
-    note_launches(4);
+    note_launches(2);
     return cudaGetLastError();
 }
 
