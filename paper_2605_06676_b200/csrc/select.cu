@@ -384,6 +384,37 @@ __device__ __forceinline__ void gather_rows(const uint4* __restrict__ src, uint4
         __stcs(dst + u, __ldg(src + ((size_t)rows[u >> log2_units] << log2_units) + (u & (units - 1))));
 }
 
+// K and V rows of the same kept positions in one loop: twice the loads in flight per thread
+__device__ __forceinline__ void gather_rows_kv(const uint4* __restrict__ ks, const uint4* __restrict__ vs,
+                                               uint4* __restrict__ kd, uint4* __restrict__ vd,
+                                               const int32_t* rows /*smem*/, int n_rows, int log2_units, int tid,
+                                               int nthreads) {
+    const int units = 1 << log2_units;
+    const int total = n_rows << log2_units;
+    int u = tid;
+    constexpr int U = LKV_GATHER_UNROLL;
+    for (; u + (U - 1) * nthreads < total; u += U * nthreads) {
+        uint4 a[U], b[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const int uu = u + k * nthreads;
+            const size_t off = ((size_t)rows[uu >> log2_units] << log2_units) + (uu & (units - 1));
+            a[k] = __ldg(ks + off);
+            b[k] = __ldg(vs + off);
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            __stcs(kd + u + k * nthreads, a[k]);
+            __stcs(vd + u + k * nthreads, b[k]);
+        }
+    }
+    for (; u < total; u += nthreads) {
+        const size_t off = ((size_t)rows[u >> log2_units] << log2_units) + (u & (units - 1));
+        __stcs(kd + u, __ldg(ks + off));
+        __stcs(vd + u, __ldg(vs + off));
+    }
+}
+
 // ---- S5 --------------------------------------------------------------------------
 #ifndef LKV_EMIT_MINB
 #define LKV_EMIT_MINB 1
@@ -442,10 +473,9 @@ __global__ void __launch_bounds__(kSelThreads, LKV_EMIT_MINB) select_emit_kernel
     __syncthreads();
     const int lu = 31 - __clz(p.row_bytes / 16);
     const size_t head_row0 = (size_t)ci.head * p.seq.T;
-    gather_rows(static_cast<const uint4*>(p.keys) + (head_row0 << lu), static_cast<uint4*>(p.out_keys) + (obase << lu),
-                s_pos, (int)tot, lu, threadIdx.x, kSelThreads);
-    gather_rows(static_cast<const uint4*>(p.values) + (head_row0 << lu),
-                static_cast<uint4*>(p.out_values) + (obase << lu), s_pos, (int)tot, lu, threadIdx.x, kSelThreads);
+    gather_rows_kv(static_cast<const uint4*>(p.keys) + (head_row0 << lu),
+                   static_cast<const uint4*>(p.values) + (head_row0 << lu), static_cast<uint4*>(p.out_keys) + (obase << lu),
+                   static_cast<uint4*>(p.out_values) + (obase << lu), s_pos, (int)tot, lu, threadIdx.x, kSelThreads);
 }
 
 // ---- standalone compaction: positions given (cache_from_trace, model.cpp:289-315) -------------
