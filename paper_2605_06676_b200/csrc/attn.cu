@@ -21,9 +21,9 @@
 // model.cpp:100-112).
 //
 // B200 design (bf16 inputs, fp32 accumulate, head_dim 128):
-//   * forward on tcgen05 (fwd_tc_kernel below): S and O accumulate in TMEM, P goes through
-//     swizzled shared memory, the V tile is the B operand of P V read MN-major straight from the
-//     TMA layout; causal tiles past the block's last admissible key are never loaded;
+//   * forward on tcgen05 (fwd_tc_kernel below): S, P and O in TMEM (P V takes its A operand from
+//     TMEM), the V tile is the B operand of P V read MN-major straight from the TMA layout;
+//     causal tiles past the block's last admissible key are never loaded;
 //   * backward on tcgen05, two kernels with no atomics (deterministic):
 //     dQ:  CTA = 128 queries (Q, dO in smem), K/V tiles streamed; S = Q K^T and dP = dO V^T in
 //          TMEM, dS = P (dP - D) written by the row threads to smem, dQ += dS K accumulated in TMEM;
@@ -32,8 +32,10 @@
 //          dK += dS^T Q in TMEM; the mask gradient per key accumulates in the key-row thread.
 // fp32 inputs run SIMT kernels (exact two-pass softmax, the 1e-5 correctness path).
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "kernels.cuh"
 
@@ -42,9 +44,6 @@ namespace attn {
 
 constexpr int kD = 128;
 constexpr float kLog2e = 1.4426950408889634f;
-#ifndef LKV_ATTN_EXPT
-#define LKV_ATTN_EXPT 0  // forward bisection knobs (profiles/attn_ab.sh): 1 no exp, 2 no P store
-#endif
 
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
@@ -92,10 +91,10 @@ __device__ __forceinline__ float mask_eff(const Geo& g, const float* mask, int j
 //           than 2^8, FA4-style), exp2 x mask, P row -> shared memory in the 128-byte-swizzled
 //           K-major layout the UMMA descriptor reads; epilogue O / l from TMEM.
 // =====================================================================================================
-constexpr int kTcQ = 128, kTcK = 64, kTcStages = 2, kTcWG = 2;
+constexpr int kTcQ = 128, kTcK = 64, kTcWG = 2;  // kTcK: key tile of the dQ kernel
 constexpr int kTcThreads = (kTcWG * 4 + 2) * 32;  // 2 softmax warpgroups + TMA warp + MMA warp
 constexpr float kTcRescale = 8.f;  // log2 units
-constexpr uint32_t kTcCols = 512;  // TMEM: S[wg][2] at wg*128 + b*64, O[wg] at 256 + wg*128
+constexpr uint32_t kTcCols = 512;  // TMEM columns of the forward / dQ kernels
 
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
     asm volatile(
@@ -117,31 +116,78 @@ __device__ __forceinline__ int tc_tiles(const Geo& g, int r0) {
     return kend > 0 ? (kend + kTcK - 1) / kTcK : 0;
 }
 
-// CTA = two 128-query tiles (one softmax warpgroup each) sharing every K/V tile: while one
-// warpgroup runs its softmax the tensor core works on the other's S / P V (FA4-style ping-pong).
+// =====================================================================================================
+// forward on tcgen05: 128-key tiles, P kept in TMEM (the A operand of P V read from TMEM)
+//   CTA = two 128-query tiles (softmax warpgroups 0 / 1) sharing every K / V tile.
+//   TMEM: S_w at column w*128 (128 fp32 columns); P_w overwrites the first 64 of them as packed
+//         bf16 pairs once the row threads have read S; O_w at 256 + w*128.
+//   MMA order per tile t and warpgroup w: P V_w(t) then S_w(t+1) -- tcgen05.mma executes in issue
+//   order, so P_w(t) is consumed before S_w(t+1) overwrites it, and when S_w(t+1) lands, P V_w(t)
+//   has landed too: the row threads may rescale O_w with no extra barrier.
+//   Row threads walk S in 32-key chunks (32 live registers): chunk max, lazy rescale against the
+//   running max (threshold 2^8; a chunk that raises it past the threshold also rescales the P
+//   chunks of this tile already in TMEM, and O), exp2 x mask, P chunk -> TMEM.
+// =====================================================================================================
+constexpr int kF2K = 128;        // keys per tile (UMMA N of S, K of P V)
+constexpr int kF2Stages = 2;     // K / V tile ring
+constexpr int kF2Chunk = 32;     // keys per row-thread chunk
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+// D (TMEM) += A (TMEM, M rows x 16 bf16 as 8 packed columns) * B (shared-memory descriptor)
+__device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                             uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ float2 unpack2(uint32_t w) {
+    return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+}
+
+__device__ __forceinline__ int f2_tiles(const Geo& g, int r0) {
+    if (r0 >= g.t_q) return 0;
+    const int kend = key_end(g, min(g.t_q, r0 + kTcQ) - 1);
+    return kend > 0 ? (kend + kF2K - 1) / kF2K : 0;
+}
+
 __global__ void __launch_bounds__(kTcThreads, 1)
     fwd_tc_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ CUtensorMap tq,
-                  const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tv) {
-    constexpr uint32_t kQBytes = kTcQ * 256, kKBytes = kTcK * 256, kVBytes = kTcK * 256, kPBytes = kTcQ * kTcK * 2;
+                   const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tv) {
+    constexpr uint32_t kQBytes = kTcQ * 256, kKBytes = kF2K * 256, kVBytes = kF2K * 256;
     extern __shared__ unsigned char smem_dyn[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
-    unsigned char* qs = smem;                                 // [wg] Q tiles
-    unsigned char* ks = qs + kTcWG * kQBytes;                 // [stage] K tiles
-    unsigned char* vs = ks + kTcStages * kKBytes;             // [stage] V^T tiles
-    unsigned char* ps = vs + kTcStages * kVBytes;             // [wg][2] P tiles
-    float* mw = reinterpret_cast<float*>(ps + kTcWG * 2 * kPBytes);  // [8 warps][64] mask tile
-    uint64_t* bars = reinterpret_cast<uint64_t*>(mw + kTcWG * 4 * kTcK);
+    unsigned char* qs = smem;                          // [wg] Q tiles
+    unsigned char* ks = qs + kTcWG * kQBytes;          // [stage] K tiles
+    unsigned char* vs = ks + kF2Stages * kKBytes;      // [stage] V tiles
+    float* mw = reinterpret_cast<float*>(vs + kF2Stages * kVBytes);  // [8 warps][128] mask tile
+    uint64_t* bars = reinterpret_cast<uint64_t*>(mw + kTcWG * 4 * kF2K);
     uint64_t* q_full = bars;
     uint64_t* k_full = bars + 1;
-    uint64_t* k_empty = k_full + kTcStages;
-    uint64_t* v_full = k_empty + kTcStages;
-    uint64_t* v_empty = v_full + kTcStages;
-    uint64_t* s_full = v_empty + kTcStages;  // [wg][2]
-    uint64_t* s_empty = s_full + 2 * kTcWG;
-    uint64_t* p_full = s_empty + 2 * kTcWG;
-    uint64_t* p_empty = p_full + 2 * kTcWG;
-    uint64_t* o_bar = p_empty + 2 * kTcWG;   // [wg]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_bar + kTcWG);
+    uint64_t* k_empty = k_full + kF2Stages;
+    uint64_t* v_full = k_empty + kF2Stages;
+    uint64_t* v_empty = v_full + kF2Stages;
+    uint64_t* s_full = v_empty + kF2Stages;  // [wg]
+    uint64_t* p_full = s_full + kTcWG;       // [wg]
+    uint64_t* o_done = p_full + kTcWG;       // [wg]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + kTcWG);
 
     const Geo g{p.n_q_heads, p.n_kv_heads, p.n_q_heads / p.n_kv_heads, p.t_q, p.t_k, p.causal, p.pos_offset,
                 p.self_keep, p.scale * kLog2e, p.scale};
@@ -149,24 +195,22 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const int q0 = blockIdx.x * (kTcWG * kTcQ);
     int nt[kTcWG];
 #pragma unroll
-    for (int w = 0; w < kTcWG; ++w) nt[w] = tc_tiles(g, q0 + w * kTcQ);
+    for (int w = 0; w < kTcWG; ++w) nt[w] = f2_tiles(g, q0 + w * kTcQ);
     const int n_all = max(nt[0], nt[1]);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         mbar_init(q_full, 1);
-        for (int i = 0; i < kTcStages; ++i) {
+        for (int i = 0; i < kF2Stages; ++i) {
             mbar_init(&k_full[i], 1);
             mbar_init(&k_empty[i], 1);
             mbar_init(&v_full[i], 1);
             mbar_init(&v_empty[i], 1);
         }
-        for (int i = 0; i < 2 * kTcWG; ++i) {
-            mbar_init(&s_full[i], 1);
-            mbar_init(&s_empty[i], 4);
-            mbar_init(&p_full[i], 4);
-            mbar_init(&p_empty[i], 1);
+        for (int w = 0; w < kTcWG; ++w) {
+            mbar_init(&s_full[w], 1);
+            mbar_init(&p_full[w], 4);
+            mbar_init(&o_done[w], 1);
         }
-        for (int w = 0; w < kTcWG; ++w) mbar_init(&o_bar[w], 1);
         fence_barrier_init();
     }
     if (warp == kTcWG * 4 + 1) tmem_alloc(tmem_slot, kTcCols);
@@ -185,60 +229,71 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
             for (int w = 0; w < kTcWG; ++w) tma_tile<kTcQ>(qs + w * kQBytes, &tq, q_full, (int)(q_row0 + q0 + w * kTcQ), pol);
             for (int t = 0; t < n_all; ++t) {
-                const int st = t % kTcStages;
-                if (t >= kTcStages) mbar_wait_backoff(&k_empty[st], ((t / kTcStages) - 1) & 1);
+                const int st = t % kF2Stages;
+                if (t >= kF2Stages) mbar_wait(&k_empty[st], ((t / kF2Stages) - 1) & 1);
                 mbar_arrive_expect_tx(&k_full[st], kKBytes);
-                tma_tile<kTcK>(ks + st * kKBytes, &tk, &k_full[st], (int)(kv_row0 + t * kTcK), pol);
-                if (t >= kTcStages) mbar_wait_backoff(&v_empty[st], ((t / kTcStages) - 1) & 1);
+                tma_tile<kF2K>(ks + st * kKBytes, &tk, &k_full[st], (int)(kv_row0 + t * kF2K), pol);
+                if (t >= kF2Stages) mbar_wait(&v_empty[st], ((t / kF2Stages) - 1) & 1);
                 mbar_arrive_expect_tx(&v_full[st], kVBytes);
-                tma_tile<kTcK>(vs + st * kVBytes, &tv, &v_full[st], (int)(kv_row0 + t * kTcK), pol);
+                tma_tile<kF2K>(vs + st * kVBytes, &tv, &v_full[st], (int)(kv_row0 + t * kF2K), pol);
             }
         }
     } else if (warp == kTcWG * 4 + 1) {
-        // ===================== MMA issuer: S of tile t+1 (both warpgroups), then P V of tile t
+        // ===================== MMA issuer =====================
         if (lane == 0) {
-            constexpr uint32_t idesc_s = umma_idesc_bf16(kTcQ, kTcK), idesc_o = umma_idesc_bf16_bmn(kTcQ, kD);
-            const uint32_t qa = smem_u32(qs), ka = smem_u32(ks), va = smem_u32(vs), pa = smem_u32(ps);
-            mbar_wait_backoff(q_full, 0);
-            auto issue_s = [&](int t) {
-                const int st = t % kTcStages, bb = t & 1;
-                mbar_wait_backoff(&k_full[st], (t / kTcStages) & 1);
+            constexpr uint32_t idesc_s = umma_idesc_bf16(kTcQ, kF2K), idesc_o = umma_idesc_bf16_bmn(kTcQ, kD);
+            const uint32_t qa = smem_u32(qs), ka = smem_u32(ks), va = smem_u32(vs);
+            auto issue_s = [&](int w, int t) {  // S_w(t) = Q_w K(t)^T into TMEM columns w*128
+                const int st = t % kF2Stages;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint64_t ad = umma_desc_sw128(qa + w * kQBytes + (kk >> 2) * (kTcQ * 128) + (kk & 3) * 32);
+                    const uint64_t bd = umma_desc_sw128(ka + st * kKBytes + (kk >> 2) * (kF2K * 128) + (kk & 3) * 32);
+                    umma_bf16(tmem + w * 128, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
+                }
+            };
+            mbar_wait(q_full, 0);
+            if (n_all > 0) {
+                mbar_wait(&k_full[0], 0);
+                tc_fence_after();
+#pragma unroll
+                for (int w = 0; w < kTcWG; ++w)
+                    if (nt[w] > 0) {
+                        issue_s(w, 0);
+                        umma_commit(&s_full[w]);
+                    }
+                umma_commit(&k_empty[0]);
+            }
+            for (int t = 0; t < n_all; ++t) {
+                const int st = t % kF2Stages, st1 = (t + 1) % kF2Stages;
+                mbar_wait(&v_full[st], (t / kF2Stages) & 1);
+                bool k_next = false;
 #pragma unroll
                 for (int w = 0; w < kTcWG; ++w) {
                     if (t >= nt[w]) continue;
-                    if (t >= 2) mbar_wait_backoff(&s_empty[w * 2 + bb], ((t >> 1) - 1) & 1);
+                    mbar_wait(&p_full[w], t & 1);
                     tc_fence_after();
 #pragma unroll
                     for (int kk = 0; kk < 8; ++kk) {
-                        const uint64_t ad = umma_desc_sw128(qa + w * kQBytes + (kk >> 2) * (kTcQ * 128) + (kk & 3) * 32);
-                        const uint64_t bd = umma_desc_sw128(ka + st * kKBytes + (kk >> 2) * (kTcK * 128) + (kk & 3) * 32);
-                        umma_bf16(tmem + w * 128 + bb * kTcK, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
-                    }
-                    umma_commit(&s_full[w * 2 + bb]);
-                }
-                umma_commit(&k_empty[st]);
-            };
-            if (n_all > 0) issue_s(0);
-            for (int t = 0; t < n_all; ++t) {
-                if (t + 1 < n_all) issue_s(t + 1);
-                const int st = t % kTcStages, bb = t & 1;
-                mbar_wait_backoff(&v_full[st], (t / kTcStages) & 1);
-#pragma unroll
-                for (int w = 0; w < kTcWG; ++w) {
-                    if (t >= nt[w]) continue;
-                    mbar_wait_backoff(&p_full[w * 2 + bb], (t >> 1) & 1);
-                    tc_fence_after();
-#pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {
-                        const uint64_t ad = umma_desc_sw128(pa + (w * 2 + bb) * kPBytes + kk * 32);
                         // B = the V tile read MN-major: keys 16kk.. at +2048 B, d 64..127 one box on
-                        const uint64_t bd = umma_desc_sw128_mn(va + st * kVBytes + kk * 2048, kTcK * 128);
-                        umma_bf16(tmem + 256 + w * 128, ad, bd, idesc_o, (t > 0 || kk > 0) ? 1u : 0u);
+                        const uint64_t bd = umma_desc_sw128_mn(va + st * kVBytes + kk * 2048, kF2K * 128);
+                        umma_bf16_ts(tmem + 256 + w * 128, tmem + w * 128 + kk * 8, bd, idesc_o,
+                                     (t > 0 || kk > 0) ? 1u : 0u);
                     }
-                    umma_commit(&o_bar[w]);
-                    umma_commit(&p_empty[w * 2 + bb]);
+                    if (t + 1 < nt[w]) {
+                        if (!k_next) {
+                            mbar_wait(&k_full[st1], ((t + 1) / kF2Stages) & 1);
+                            tc_fence_after();
+                            k_next = true;
+                        }
+                        issue_s(w, t + 1);
+                        umma_commit(&s_full[w]);
+                    } else {
+                        umma_commit(&o_done[w]);
+                    }
                 }
                 umma_commit(&v_empty[st]);
+                if (k_next) umma_commit(&k_empty[st1]);
             }
         }
     } else {
@@ -249,115 +304,125 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const uint32_t lane_addr = tmem + (uint32_t(w4 * 32) << 16);
         const uint32_t s_col = wg * 128, o_col = 256 + wg * 128;
         const float* mask = p.mask ? p.mask + kv_row0 : nullptr;
-        float* mwarp = mw + warp * kTcK;
-        uint64_t* my_s_full = s_full + wg * 2;
-        uint64_t* my_s_empty = s_empty + wg * 2;
-        uint64_t* my_p_full = p_full + wg * 2;
-        uint64_t* my_p_empty = p_empty + wg * 2;
-        unsigned char* my_ps = ps + wg * 2 * kPBytes;
+        float* mwarp = mw + warp * kF2K;
         float m_run = -INFINITY, l_run = 0.f;
-        // the mask values of tile t + 1 are fetched while tile t is processed
-        float mnext0 = 0.f, mnext1 = 0.f;
+        float mnext[4] = {0.f, 0.f, 0.f, 0.f};  // the mask of tile t + 1, fetched during tile t
         if (mask) {
-            mnext0 = lane < g.t_k ? __ldg(mask + lane) : 0.f;
-            mnext1 = lane + 32 < g.t_k ? __ldg(mask + lane + 32) : 0.f;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) mnext[i] = lane + 32 * i < g.t_k ? __ldg(mask + lane + 32 * i) : 0.f;
         }
         const int wr0 = q0 + wg * kTcQ + w4 * 32;
         for (int t = 0; t < ntw; ++t) {
-            const int bb = t & 1, j0 = t * kTcK;
+            const int j0 = t * kF2K;
             if (mask) {
-                mwarp[lane] = mnext0;
-                mwarp[lane + 32] = mnext1;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) mwarp[lane + 32 * i] = mnext[i];
                 __syncwarp();
-                const int jn = j0 + kTcK;
-                mnext0 = jn + lane < g.t_k ? __ldg(mask + jn + lane) : 0.f;
-                mnext1 = jn + lane + 32 < g.t_k ? __ldg(mask + jn + lane + 32) : 0.f;
+                const int jn = j0 + kF2K;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) mnext[i] = jn + lane + 32 * i < g.t_k ? __ldg(mask + jn + lane + 32 * i) : 0.f;
             }
-            mbar_wait(&my_s_full[bb], (t >> 1) & 1);
+            mbar_wait(&s_full[wg], t & 1);
             __syncwarp();  // reconverge before .sync.aligned tcgen05.ld
             tc_fence_after();
-            uint32_t sr[64];
-            tmem_ld_32x32b_x32(lane_addr + s_col + bb * kTcK, *reinterpret_cast<uint32_t(*)[32]>(sr));
-            tmem_ld_32x32b_x32(lane_addr + s_col + bb * kTcK + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
-            tmem_ld_wait();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&my_s_empty[bb]);
-            const bool interior = j0 + kTcK <= g.t_k && wr0 + 32 <= g.t_q &&
-                                  (!g.causal || j0 + kTcK - 1 <= g.pos_offset + wr0) &&
-                                  !(g.self_keep && j0 + kTcK - 1 >= g.pos_offset + wr0);
-            float x[64];
-            float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // 4 chains, not one 64-long
-#pragma unroll
-            for (int i = 0; i < 64; ++i) {
-                x[i] = __uint_as_float(sr[i]) * g.c;
-                if (!interior && !admissible(g, j0 + i, r)) x[i] = -INFINITY;
-                mq[i & 3] = fmaxf(mq[i & 3], x[i]);
-            }
-            const float mt = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
-            const float m_new = fmaxf(m_run, mt);
-            const bool need = m_new != -INFINITY && (m_run == -INFINITY || m_new > m_run + kTcRescale);
-            float alpha = 1.f;
-            if (need) {
-                alpha = m_run == -INFINITY ? 0.f : fast_exp2(m_run - m_new);
-                m_run = m_new;
-            }
-            // P buffer bb is free once P V of tile t-2 has retired (this also bounds the o_bar
-            // phases in flight to one, so the parity waits below are exact)
-            if (t >= 2) mbar_wait(&my_p_empty[bb], ((t >> 1) - 1) & 1);
-            if (__any_sync(0xffffffffu, need) && t > 0) {
-                mbar_wait(&o_bar[wg], (t - 1) & 1);  // rescale O once P V of tile t-1 has landed
-                __syncwarp();  // reconverge before .sync.aligned tcgen05.ld
-                tc_fence_after();
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    uint32_t orr[32];
-                    tmem_ld_32x32b_x32(lane_addr + o_col + c * 32, orr);
-                    tmem_ld_wait();
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) orr[i] = __float_as_uint(__uint_as_float(orr[i]) * alpha);
-                    tmem_st32(lane_addr + o_col + c * 32, orr);
-                }
-                tmem_st_wait();
-            }
-            l_run *= alpha;
-            // P row -> shared memory (bf16, 128-byte swizzle, K-major: 8 chunks of 8 keys)
-            unsigned char* prow = my_ps + bb * kPBytes + rl * 128;
-            const float sub = m_run == -INFINITY ? 0.f : m_run;
+            const bool interior = j0 + kF2K <= g.t_k && wr0 + 32 <= g.t_q &&
+                                  (!g.causal || j0 + kF2K - 1 <= g.pos_offset + wr0) &&
+                                  !(g.self_keep && j0 + kF2K - 1 >= g.pos_offset + wr0);
             float ls[4] = {0.f, 0.f, 0.f, 0.f};
+            // INT: every (row, key) of this warp's tile is admissible -> no per-element tests and the
+            // scale folded into the exponent's FMA (scale > 0: max(c s) = c max(s))
+            auto tile_body = [&](auto int_tag) {
+                constexpr bool INT = decltype(int_tag)::value;
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                uint32_t w4v[4];
+                for (int c = 0; c < kF2K / kF2Chunk; ++c) {
+                    uint32_t sr[32];
+                    tmem_ld_32x32b_x32(lane_addr + s_col + c * kF2Chunk, sr);
+                    tmem_ld_wait();
+                    float x[32];
+                    float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    float pv[2];
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int i = c * 8 + e * 2 + h, j = j0 + i;
-                        float mj = mask ? mwarp[i] : 1.f;
-                        if (!interior && g.self_keep && j == g.pos_offset + r) mj = 1.f;
-#if LKV_ATTN_EXPT & 1
-                        pv[h] = (x[i] - sub) * mj;  // bisection knob: no exp
-#else
-                        pv[h] = fast_exp2(x[i] - sub) * mj;  // x = -inf -> 0
-#endif
-                        ls[i & 3] += pv[h];
+                    for (int i = 0; i < 32; ++i) {
+                        if constexpr (INT) {
+                            x[i] = __uint_as_float(sr[i]);
+                        } else {
+                            x[i] = __uint_as_float(sr[i]) * g.c;
+                            if (!admissible(g, j0 + c * kF2Chunk + i, r)) x[i] = -INFINITY;
+                        }
+                        mq[i & 3] = fmaxf(mq[i & 3], x[i]);
                     }
-                    w4v[e] = pack2(pv[0], pv[1]);
+                    float mt = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
+                    if constexpr (INT) mt *= g.c;
+                    const float m_new = fmaxf(m_run, mt);
+                    const bool need = m_new != -INFINITY && (m_run == -INFINITY || m_new > m_run + kTcRescale);
+                    float alpha = 1.f;
+                    if (need) alpha = m_run == -INFINITY ? 0.f : fast_exp2(m_run - m_new);
+                    if (__any_sync(0xffffffffu, need) && (t > 0 || c > 0)) {
+                        // rare: the running max moved past the threshold -- rescale O (its last P V
+                        // has landed: S_w(t) was issued after it) and this tile's P chunks in TMEM
+                        tmem_st_wait();
+                        if (t > 0) {
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                uint32_t orr[32];
+                                tmem_ld_32x32b_x32(lane_addr + o_col + q * 32, orr);
+                                tmem_ld_wait();
+#pragma unroll
+                                for (int i = 0; i < 32; ++i) orr[i] = __float_as_uint(__uint_as_float(orr[i]) * alpha);
+                                tmem_st32(lane_addr + o_col + q * 32, orr);
+                            }
+                        }
+                        for (int pc = 0; pc < c; ++pc) {
+                            uint32_t pr[16];
+                            tmem_ld16(lane_addr + s_col + pc * 16, pr);
+                            tmem_ld_wait();
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) {
+                                const float2 f = unpack2(pr[i]);
+                                pr[i] = pack2(f.x * alpha, f.y * alpha);
+                            }
+                            tmem_st16(lane_addr + s_col + pc * 16, pr);
+                        }
+                        tmem_st_wait();
+                    }
+                    if (need) {
+                        l_run *= alpha;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) ls[q] *= alpha;
+                        m_run = m_new;
+                    }
+                    const float sub = m_run == -INFINITY ? 0.f : m_run;
+                    uint32_t pw[16];
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {
+                        float pv[2];
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int i = 2 * e + h;
+                            float mj = mask ? mwarp[c * kF2Chunk + i] : 1.f;
+                            if constexpr (INT) {
+                                pv[h] = fast_exp2(fmaf(x[i], g.c, -sub)) * mj;
+                            } else {
+                                if (g.self_keep && j0 + c * kF2Chunk + i == g.pos_offset + r) mj = 1.f;
+                                pv[h] = fast_exp2(x[i] - sub) * mj;  // x = -inf -> 0
+                            }
+                            ls[i & 3] += pv[h];
+                        }
+                        pw[e] = pack2(pv[0], pv[1]);
+                    }
+                    tmem_st16(lane_addr + s_col + c * 16, pw);  // P chunk c over S columns already read
                 }
-                if (!(LKV_ATTN_EXPT & 2))
-                    *reinterpret_cast<uint4*>(prow + ((c ^ (rl & 7)) << 4)) = make_uint4(w4v[0], w4v[1], w4v[2], w4v[3]);
-            }
+            };
+            if (interior) tile_body(std::true_type{});
+            else tile_body(std::false_type{});
             l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
-            fence_proxy_async_smem();
+            tmem_st_wait();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&my_p_full[bb]);
+            if (lane == 0) mbar_arrive(&p_full[wg]);
         }
         // ---- epilogue: O / l from TMEM
-        if (ntw > 1) mbar_wait(&o_bar[wg], (ntw - 2) & 1);  // phases in order: never two behind
         if (ntw > 0) {
-            mbar_wait(&o_bar[wg], (ntw - 1) & 1);
+            mbar_wait(&o_done[wg], 0);
             __syncwarp();  // reconverge before .sync.aligned tcgen05.ld
             tc_fence_after();
         }
@@ -1071,11 +1136,13 @@ __global__ void __launch_bounds__(kSimt) dkv_f32_kernel(const __grid_constant__ 
 // ---- host launchers ----------------------------------------------------------------------------------
 
 
+
 size_t attn_fwd_tc_smem() {
-    return 1024 + attn::kTcWG * attn::kTcQ * 256 + attn::kTcStages * (attn::kTcK * 256 + attn::kTcK * 256) +
-           attn::kTcWG * 2 * attn::kTcQ * attn::kTcK * 2 + attn::kTcWG * 4 * attn::kTcK * 4 + 64 * 8 + 16;
+    return 1024 + attn::kTcWG * attn::kTcQ * 256 + attn::kF2Stages * 2 * attn::kF2K * 256 +
+           attn::kTcWG * 4 * attn::kF2K * 4 + 16 * 8 + 16;
 }
 
+// mk / mv / mq: 128-row boxes
 cudaError_t launch_attn_fwd(const AttnParams& p, int dtype, int d, const CUtensorMap* mk, const CUtensorMap* mv,
                             const CUtensorMap* mq, cudaStream_t stream) {
     if (p.mask) {
@@ -1084,12 +1151,12 @@ cudaError_t launch_attn_fwd(const AttnParams& p, int dtype, int d, const CUtenso
         note_launches(1);
     }
     if (dtype == LKV_BF16) {
+        constexpr int rows_per_cta = attn::kTcWG * attn::kTcQ;
+        const dim3 grid((p.t_q + rows_per_cta - 1) / rows_per_cta, p.n_q_heads, p.batch);
         const size_t smem = attn_fwd_tc_smem();
         cudaError_t e = cudaFuncSetAttribute(attn::fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        constexpr int rows_per_cta = attn::kTcWG * attn::kTcQ;
-        attn::fwd_tc_kernel<<<dim3((p.t_q + rows_per_cta - 1) / rows_per_cta, p.n_q_heads, p.batch), attn::kTcThreads,
-                              smem, stream>>>(p, *mq, *mk, *mv);
+        attn::fwd_tc_kernel<<<grid, attn::kTcThreads, smem, stream>>>(p, *mq, *mk, *mv);
         note_launches(1);
     } else {
         const size_t smem = (size_t)(d + p.t_k) * 4;

@@ -917,7 +917,7 @@ lkv_status lkv_masked_attention_fwd(const lkv_attn_desc* a, const void* q, const
     CUtensorMap mk, mv, mq;
     if (a->dtype == LKV_BF16) {
         const uint64_t rk = (uint64_t)a->batch * a->n_kv_heads * a->t_k, rq = (uint64_t)a->batch * a->n_q_heads * a->t_q;
-        if ((st = make_map_bf16(&mk, k, 128, rk, 64)) || (st = make_map_bf16(&mv, v, 128, rk, 64)) ||
+        if ((st = make_map_bf16(&mk, k, 128, rk, 128)) || (st = make_map_bf16(&mv, v, 128, rk, 128)) ||
             (st = make_map_bf16(&mq, q, 128, rq, 128)))
             return st;
     }
