@@ -625,34 +625,43 @@ __global__ void __launch_bounds__(kBwThreads, 1)
             if (t >= 2) mbar_wait(&pt_empty[bb], ((t >> 1) - 1) & 1);  // dV / dK of tile t-2 done with buffer bb
             unsigned char* prow = pts + bb * kPT + kr * 128;
             unsigned char* drow = dss + bb * kPT + kr * 128;
+            // INT: every (query, key) of this warp's tile is admissible and none is a kept self
+            // key -> no per-element tests (separate code paths; the tests were most of the work)
+            auto tile_body = [&](auto int_tag) {
+                constexpr bool INT = decltype(int_tag)::value;
+                float dmq[4] = {0.f, 0.f, 0.f, 0.f};  // dmask partial sums (4 independent chains)
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                uint32_t pw[4], dw[4];
+                for (int c = 0; c < 8; ++c) {
+                    uint32_t pw[4], dw[4];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    float pv[2], dsv[2];
+                    for (int e = 0; e < 4; ++e) {
+                        float pv[2], dsv[2];
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int i = c * 8 + e * 2 + h, r = r0 + i;
-                        float pm = fast_exp2(__uint_as_float(sv[i]) * g.c - wl[i]);
-                        bool self = false;
-                        if (!interior) {
-                            if (!admissible(g, j, r)) pm = 0.f;
-                            self = g.self_keep && j == g.pos_offset + r;
+                        for (int h = 0; h < 2; ++h) {
+                            const int i = c * 8 + e * 2 + h, r = r0 + i;
+                            float pm = fast_exp2(fmaf(__uint_as_float(sv[i]), g.c, -wl[i]));
+                            bool self = false;
+                            if constexpr (!INT) {
+                                if (!admissible(g, j, r)) pm = 0.f;
+                                self = g.self_keep && j == g.pos_offset + r;
+                            }
+                            const float dpv = __uint_as_float(dv[i]) - wl[kBwQ + i];
+                            const float pj = self ? pm : pm * mkey;
+                            if (!self) dmq[i & 3] = fmaf(pm, dpv, dmq[i & 3]);
+                            pv[h] = pj;
+                            dsv[h] = pj * dpv;
                         }
-                        const float dpv = __uint_as_float(dv[i]) - wl[kBwQ + i];
-                        const float pj = self ? pm : pm * mkey;
-                        if (!self) dm = fmaf(pm, dpv, dm);
-                        pv[h] = pj;
-                        dsv[h] = pj * dpv;
+                        pw[e] = pack2(pv[0], pv[1]);
+                        dw[e] = pack2(dsv[0], dsv[1]);
                     }
-                    pw[e] = pack2(pv[0], pv[1]);
-                    dw[e] = pack2(dsv[0], dsv[1]);
+                    const int off = (c ^ (kr & 7)) << 4;
+                    *reinterpret_cast<uint4*>(prow + off) = make_uint4(pw[0], pw[1], pw[2], pw[3]);
+                    *reinterpret_cast<uint4*>(drow + off) = make_uint4(dw[0], dw[1], dw[2], dw[3]);
                 }
-                const int off = (c ^ (kr & 7)) << 4;
-                *reinterpret_cast<uint4*>(prow + off) = make_uint4(pw[0], pw[1], pw[2], pw[3]);
-                *reinterpret_cast<uint4*>(drow + off) = make_uint4(dw[0], dw[1], dw[2], dw[3]);
-            }
+                dm += (dmq[0] + dmq[1]) + (dmq[2] + dmq[3]);
+            };
+            if (interior) tile_body(std::true_type{});
+            else tile_body(std::false_type{});
             fence_proxy_async_smem();
             tc_fence_before();
             __syncwarp();
@@ -865,27 +874,32 @@ __global__ void __launch_bounds__(kDqThreads, 1)
                                   !(g.self_keep && j0 + kTcK - 1 >= g.pos_offset + wr0);
             if (t >= 1) mbar_wait(&ds_empty[wg], (t - 1) & 1);  // dQ of tile t-1 done reading dS
             unsigned char* drow = my_ds + rl * 128;
+            auto tile_body = [&](auto int_tag) {  // INT: no per-element admissibility tests
+                constexpr bool INT = decltype(int_tag)::value;
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                uint32_t dw[4];
+                for (int c = 0; c < 8; ++c) {
+                    uint32_t dw[4];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    float dsv[2];
+                    for (int e = 0; e < 4; ++e) {
+                        float dsv[2];
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int i = c * 8 + e * 2 + h, jj = j0 + i;
-                        float mj = mask ? mwarp[i] : 1.f;
-                        float pm = fast_exp2(__uint_as_float(sv[i]) * g.c - lse);
-                        if (!interior) {
-                            if (!admissible(g, jj, r)) pm = 0.f;
-                            if (g.self_keep && jj == g.pos_offset + r) mj = 1.f;
+                        for (int h = 0; h < 2; ++h) {
+                            const int i = c * 8 + e * 2 + h, jj = j0 + i;
+                            float mj = mask ? mwarp[i] : 1.f;
+                            float pm = fast_exp2(fmaf(__uint_as_float(sv[i]), g.c, -lse));
+                            if constexpr (!INT) {
+                                if (!admissible(g, jj, r)) pm = 0.f;
+                                if (g.self_keep && jj == g.pos_offset + r) mj = 1.f;
+                            }
+                            dsv[h] = pm * mj * (__uint_as_float(dv[i]) - dd);
                         }
-                        dsv[h] = pm * mj * (__uint_as_float(dv[i]) - dd);
+                        dw[e] = pack2(dsv[0], dsv[1]);
                     }
-                    dw[e] = pack2(dsv[0], dsv[1]);
+                    *reinterpret_cast<uint4*>(drow + ((c ^ (rl & 7)) << 4)) = make_uint4(dw[0], dw[1], dw[2], dw[3]);
                 }
-                *reinterpret_cast<uint4*>(drow + ((c ^ (rl & 7)) << 4)) = make_uint4(dw[0], dw[1], dw[2], dw[3]);
-            }
+            };
+            if (interior) tile_body(std::true_type{});
+            else tile_body(std::false_type{});
             fence_proxy_async_smem();
             tc_fence_before();
             __syncwarp();
