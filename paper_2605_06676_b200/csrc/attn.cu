@@ -158,6 +158,19 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, u
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// tcgen05.wait::ld that also "defines" r: the registers of an asynchronous tcgen05.ld cannot be
+// read (or the read hoisted by the compiler) before the wait
+__device__ __forceinline__ void tmem_ld_wait_dep(uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.wait::ld.sync.aligned;"
+        : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+          "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]),
+          "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]),
+          "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]),
+          "+r"(r[30]), "+r"(r[31])
+        :
+        : "memory");
+}
 __device__ __forceinline__ float2 unpack2(uint32_t w) {
     return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
 }
@@ -333,11 +346,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             // scale folded into the exponent's FMA (scale > 0: max(c s) = c max(s))
             auto tile_body = [&](auto int_tag) {
                 constexpr bool INT = decltype(int_tag)::value;
+                // S chunks double-buffered in registers: chunk c + 1 is loaded while chunk c is processed
+                uint32_t sb[2][32];
+                tmem_ld_32x32b_x32(lane_addr + s_col, sb[0]);
+                tmem_ld_wait_dep(sb[0]);
 #pragma unroll
                 for (int c = 0; c < kF2K / kF2Chunk; ++c) {
-                    uint32_t sr[32];
-                    tmem_ld_32x32b_x32(lane_addr + s_col + c * kF2Chunk, sr);
-                    tmem_ld_wait();
+                    uint32_t (&sr)[32] = sb[c & 1];
+                    if (c + 1 < kF2K / kF2Chunk) tmem_ld_32x32b_x32(lane_addr + s_col + (c + 1) * kF2Chunk, sb[(c + 1) & 1]);
                     float x[32];
                     float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
@@ -410,6 +426,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                         pw[e] = pack2(pv[0], pv[1]);
                     }
                     tmem_st16(lane_addr + s_col + c * 16, pw);  // P chunk c over S columns already read
+                    if (c + 1 < kF2K / kF2Chunk) tmem_ld_wait_dep(sb[(c + 1) & 1]);
                 }
             };
             if (interior) tile_body(std::true_type{});
