@@ -175,6 +175,36 @@ __device__ __forceinline__ float2 unpack2(uint32_t w) {
     return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
 }
 
+// The rare lazy-rescale step of the forward row threads (warp-collective): O *= alpha (when a
+// P V has landed in it) and the P chunks [0, c) of the current tile already in TMEM.  Out of line
+// to keep the hot loop small.
+__device__ __noinline__ void fwd_rescale(uint32_t lane_addr, uint32_t s_col, uint32_t o_col, int c, bool has_o,
+                                         float alpha) {
+    tmem_st_wait();
+    if (has_o) {
+        for (int q = 0; q < 4; ++q) {
+            uint32_t orr[32];
+            tmem_ld_32x32b_x32(lane_addr + o_col + q * 32, orr);
+            tmem_ld_wait_dep(orr);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) orr[i] = __float_as_uint(__uint_as_float(orr[i]) * alpha);
+            tmem_st32(lane_addr + o_col + q * 32, orr);
+        }
+    }
+    for (int pc = 0; pc < c; ++pc) {
+        uint32_t pr[16];
+        tmem_ld16(lane_addr + s_col + pc * 16, pr);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const float2 f = unpack2(pr[i]);
+            pr[i] = pack2(f.x * alpha, f.y * alpha);
+        }
+        tmem_st16(lane_addr + s_col + pc * 16, pr);
+    }
+    tmem_st_wait();
+}
+
 __device__ __forceinline__ int f2_tiles(const Geo& g, int r0) {
     if (r0 >= g.t_q) return 0;
     const int kend = key_end(g, min(g.t_q, r0 + kTcQ) - 1);
@@ -343,94 +373,92 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                                   !(g.self_keep && j0 + kF2K - 1 >= g.pos_offset + wr0);
             float ls[4] = {0.f, 0.f, 0.f, 0.f};
             // INT: every (row, key) of this warp's tile is admissible -> no per-element tests and the
-            // scale folded into the exponent's FMA (scale > 0: max(c s) = c max(s))
-            auto tile_body = [&](auto int_tag) {
+            // scale folded into the exponent's FMA (scale > 0: max(c s) = c max(s)); interior tiles
+            // run a fully unrolled loop with the next S chunk's load in flight, boundary tiles a
+            // compact one (code size: the kernel is instruction-cache sensitive)
+            auto chunk = [&](auto int_tag, int c, uint32_t (&sr)[32]) {
                 constexpr bool INT = decltype(int_tag)::value;
-                // S chunks double-buffered in registers: chunk c + 1 is loaded while chunk c is processed
-                uint32_t sb[2][32];
+                float x[32];
+                float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    if constexpr (INT) {
+                        x[i] = __uint_as_float(sr[i]);
+                    } else {
+                        x[i] = __uint_as_float(sr[i]) * g.c;
+                        if (!admissible(g, j0 + c * kF2Chunk + i, r)) x[i] = -INFINITY;
+                    }
+                    mq[i & 3] = fmaxf(mq[i & 3], x[i]);
+                }
+                float mt = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
+                if constexpr (INT) mt *= g.c;
+                const float m_new = fmaxf(m_run, mt);
+                const bool need = m_new != -INFINITY && (m_run == -INFINITY || m_new > m_run + kTcRescale);
+                float alpha = 1.f;
+                if (need) alpha = m_run == -INFINITY ? 0.f : fast_exp2(m_run - m_new);
+                if (__any_sync(0xffffffffu, need) && (t > 0 || c > 0))
+                    fwd_rescale(lane_addr, s_col, o_col, c, t > 0, alpha);  // rare
+                if (need) {
+                    l_run *= alpha;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) ls[q] *= alpha;
+                    m_run = m_new;
+                }
+                const float sub = m_run == -INFINITY ? 0.f : m_run;
+                float mk[32];
+                if (mask) {
+                    const float4* m4 = reinterpret_cast<const float4*>(mwarp + c * kF2Chunk);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const float4 v = m4[q];
+                        mk[4 * q] = v.x;
+                        mk[4 * q + 1] = v.y;
+                        mk[4 * q + 2] = v.z;
+                        mk[4 * q + 3] = v.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) mk[i] = 1.f;
+                }
+                uint32_t pw[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    float pv[2];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int i = 2 * e + h;
+                        float mj = mk[i];
+                        if constexpr (INT) {
+                            pv[h] = fast_exp2(fmaf(x[i], g.c, -sub)) * mj;
+                        } else {
+                            if (g.self_keep && j0 + c * kF2Chunk + i == g.pos_offset + r) mj = 1.f;
+                            pv[h] = fast_exp2(x[i] - sub) * mj;  // x = -inf -> 0
+                        }
+                        ls[i & 3] += pv[h];
+                    }
+                    pw[e] = pack2(pv[0], pv[1]);
+                }
+                tmem_st16(lane_addr + s_col + c * 16, pw);  // P chunk c over S columns already read
+            };
+            if (interior) {
+                uint32_t sb[2][32];  // S chunk c + 1 is loaded while chunk c is processed
                 tmem_ld_32x32b_x32(lane_addr + s_col, sb[0]);
                 tmem_ld_wait_dep(sb[0]);
 #pragma unroll
                 for (int c = 0; c < kF2K / kF2Chunk; ++c) {
-                    uint32_t (&sr)[32] = sb[c & 1];
                     if (c + 1 < kF2K / kF2Chunk) tmem_ld_32x32b_x32(lane_addr + s_col + (c + 1) * kF2Chunk, sb[(c + 1) & 1]);
-                    float x[32];
-                    float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        if constexpr (INT) {
-                            x[i] = __uint_as_float(sr[i]);
-                        } else {
-                            x[i] = __uint_as_float(sr[i]) * g.c;
-                            if (!admissible(g, j0 + c * kF2Chunk + i, r)) x[i] = -INFINITY;
-                        }
-                        mq[i & 3] = fmaxf(mq[i & 3], x[i]);
-                    }
-                    float mt = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
-                    if constexpr (INT) mt *= g.c;
-                    const float m_new = fmaxf(m_run, mt);
-                    const bool need = m_new != -INFINITY && (m_run == -INFINITY || m_new > m_run + kTcRescale);
-                    float alpha = 1.f;
-                    if (need) alpha = m_run == -INFINITY ? 0.f : fast_exp2(m_run - m_new);
-                    if (__any_sync(0xffffffffu, need) && (t > 0 || c > 0)) {
-                        // rare: the running max moved past the threshold -- rescale O (its last P V
-                        // has landed: S_w(t) was issued after it) and this tile's P chunks in TMEM
-                        tmem_st_wait();
-                        if (t > 0) {
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                uint32_t orr[32];
-                                tmem_ld_32x32b_x32(lane_addr + o_col + q * 32, orr);
-                                tmem_ld_wait();
-#pragma unroll
-                                for (int i = 0; i < 32; ++i) orr[i] = __float_as_uint(__uint_as_float(orr[i]) * alpha);
-                                tmem_st32(lane_addr + o_col + q * 32, orr);
-                            }
-                        }
-                        for (int pc = 0; pc < c; ++pc) {
-                            uint32_t pr[16];
-                            tmem_ld16(lane_addr + s_col + pc * 16, pr);
-                            tmem_ld_wait();
-#pragma unroll
-                            for (int i = 0; i < 16; ++i) {
-                                const float2 f = unpack2(pr[i]);
-                                pr[i] = pack2(f.x * alpha, f.y * alpha);
-                            }
-                            tmem_st16(lane_addr + s_col + pc * 16, pr);
-                        }
-                        tmem_st_wait();
-                    }
-                    if (need) {
-                        l_run *= alpha;
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) ls[q] *= alpha;
-                        m_run = m_new;
-                    }
-                    const float sub = m_run == -INFINITY ? 0.f : m_run;
-                    uint32_t pw[16];
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        float pv[2];
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            const int i = 2 * e + h;
-                            float mj = mask ? mwarp[c * kF2Chunk + i] : 1.f;
-                            if constexpr (INT) {
-                                pv[h] = fast_exp2(fmaf(x[i], g.c, -sub)) * mj;
-                            } else {
-                                if (g.self_keep && j0 + c * kF2Chunk + i == g.pos_offset + r) mj = 1.f;
-                                pv[h] = fast_exp2(x[i] - sub) * mj;  // x = -inf -> 0
-                            }
-                            ls[i & 3] += pv[h];
-                        }
-                        pw[e] = pack2(pv[0], pv[1]);
-                    }
-                    tmem_st16(lane_addr + s_col + c * 16, pw);  // P chunk c over S columns already read
+                    chunk(std::true_type{}, c, sb[c & 1]);
                     if (c + 1 < kF2K / kF2Chunk) tmem_ld_wait_dep(sb[(c + 1) & 1]);
                 }
-            };
-            if (interior) tile_body(std::true_type{});
-            else tile_body(std::false_type{});
+            } else {
+#pragma unroll 1
+                for (int c = 0; c < kF2K / kF2Chunk; ++c) {
+                    uint32_t sr[32];
+                    tmem_ld_32x32b_x32(lane_addr + s_col + c * kF2Chunk, sr);
+                    tmem_ld_wait_dep(sr);
+                    chunk(std::false_type{}, c, sr);
+                }
+            }
             l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
             tmem_st_wait();
             tc_fence_before();
