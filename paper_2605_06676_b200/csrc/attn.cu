@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                    const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tv) {
     constexpr uint32_t kQBytes = kTcQ * 256, kKBytes = kF2K * 256, kVBytes = kF2K * 256;
     extern __shared__ unsigned char smem_dyn[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+    unsigned char* smem = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);  // aligned, still a __shared__ pointer
     unsigned char* qs = smem;                          // [wg] Q tiles
     unsigned char* ks = qs + kTcWG * kQBytes;          // [stage] K tiles
     unsigned char* vs = ks + kF2Stages * kKBytes;      // [stage] V tiles
@@ -517,7 +517,7 @@ __global__ void __launch_bounds__(kBwThreads, 1)
                   const __grid_constant__ CUtensorMap tdo64) {
     constexpr uint32_t kKB128 = kBwK * 256, kT64 = kBwQ * 256, kStage = 2 * kT64, kPT = kBwK * kBwQ * 2;
     extern __shared__ unsigned char smem_dyn[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+    unsigned char* smem = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);  // aligned, still a __shared__ pointer
     unsigned char* ks = smem;
     unsigned char* vs = ks + kKB128;
     unsigned char* stg = vs + kKB128;          // [2] x {Q, dO}

@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
                             const __grid_constant__ CUtensorMap tmap_v) {
     constexpr int kStageBytes = 2 * kDecStageRows * 256;  // K + V, 64 rows x 256 B each
     extern __shared__ unsigned char smem_dyn[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+    unsigned char* smem = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);  // aligned, still a __shared__ pointer
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kDecStages * kStageBytes);
     uint64_t* empty = full + kDecStages;
     float* red = reinterpret_cast<float*>(empty + kDecStages);  // [consumers][G][D + 2]

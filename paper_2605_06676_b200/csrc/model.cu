@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsPerSm) wstream_gemv_kernel(cons
     constexpr int kActBytes = 8 * NBT * 256;  // 8 k16 steps x NBT tiles x 32 lanes x 8 B
     constexpr int kStage = kWsUnitBytes + kActBytes;
     extern __shared__ unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+    unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);  // aligned, still a __shared__ pointer
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kWsStages * kStage);
     uint64_t* empty = full + kWsStages;
     float* red = reinterpret_cast<float*>(empty + kWsStages);  // [4][64][NBT * 8]

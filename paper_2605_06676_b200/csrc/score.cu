@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(TcCfg<N, NBOX>::kThreads, 1)
     constexpr int kEpi = Cfg::kEpi;
     constexpr int kEpiChunk = Cfg::kEpiChunk;
     extern __shared__ unsigned char smem_dyn[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+    unsigned char* smem = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);  // aligned, still a __shared__ pointer
     unsigned char* sA = smem;
     unsigned char* sW = smem + S * Cfg::kAStage;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sW + Cfg::kW);
