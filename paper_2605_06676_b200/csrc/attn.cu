@@ -507,9 +507,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 // backward on tcgen05: dKV (key-major) and dQ (query-major); the transposed B operands (Q and dO
 // for dK / dV, K for dQ) are the TMA tiles themselves read through MN-major UMMA descriptors.
 // =====================================================================================================
+__device__ __forceinline__ void named_bar_sync_attn(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 constexpr int kBwK = 128;   // dKV: keys per CTA (UMMA M)
 constexpr int kBwQ = 64;    // dKV: queries per streamed tile (UMMA N of S^T, K of dV / dK)
-constexpr int kBwThreads = 192;  // warps 0-3 compute (thread = row = TMEM lane), 4 TMA, 5 MMA
+constexpr int kBwWG = 2;     // dKV compute warpgroups: warpgroup w takes the query tiles t = w mod 2
+constexpr int kBwThreads = (kBwWG * 4 + 2) * 32;  // warps 0-7 compute (thread = key row = TMEM lane), 8 TMA, 9 MMA
+constexpr int kBwTma = kBwWG * 4, kBwMma = kBwWG * 4 + 1;
 
 __global__ void __launch_bounds__(kBwThreads, 1)
     dkv_tc_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ CUtensorMap tk128,
@@ -523,8 +526,9 @@ __global__ void __launch_bounds__(kBwThreads, 1)
     unsigned char* stg = vs + kKB128;          // [2] x {Q, dO}
     unsigned char* pts = stg + 2 * kStage;     // [2] P^T [128 keys][64 q]
     unsigned char* dss = pts + 2 * kPT;        // [2] dS^T
-    float* cw = reinterpret_cast<float*>(dss + 2 * kPT);  // [4 warps][lse 64 | D 64]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(cw + 4 * 2 * kBwQ);
+    float* cw = reinterpret_cast<float*>(dss + 2 * kPT);  // [8 warps][lse 64 | D 64]
+    float* dmx = cw + kBwWG * 4 * 2 * kBwQ;                // [128] warpgroup 1's dmask partials
+    uint64_t* bars = reinterpret_cast<uint64_t*>(dmx + kBwK);
     uint64_t* kv_full = bars;
     uint64_t* st_full = bars + 1;    // [2]
     uint64_t* st_empty = bars + 3;   // [2]
@@ -559,16 +563,16 @@ __global__ void __launch_bounds__(kBwThreads, 1)
         mbar_init(acc_done, 1);
         fence_barrier_init();
     }
-    if (warp == 5) tmem_alloc(tmem_slot, 512);
+    if (warp == kBwMma) tmem_alloc(tmem_slot, 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;  // S^T[2] 0/64, dP^T[2] 128/192, dV 256, dK 384
+    const uint32_t tmem = *tmem_slot;  // S^T[2] 0/64, dP^T[2] 128/192 (buffer = warpgroup), dV 256, dK 384
     const size_t kv_row0 = ((size_t)b * g.n_kv_heads + kvh) * g.t_k;
     auto head_of = [&](int t) { return (b * g.n_q_heads + kvh * g.G + t / nq); };  // flat q head
     auto qtile_of = [&](int t) { return qt0 + t % nq; };
 
-    if (warp == 4) {
+    if (warp == kBwTma) {
         if (lane == 0 && ntiles > 0) {
             const uint64_t pol = l2_policy_evict_last();
             mbar_arrive_expect_tx(kv_full, 2 * kKB128);
@@ -586,7 +590,7 @@ __global__ void __launch_bounds__(kBwThreads, 1)
 
             }
         }
-    } else if (warp == 5) {
+    } else if (warp == kBwMma) {
         if (lane == 0 && ntiles > 0) {
             constexpr uint32_t id_s = umma_idesc_bf16(kBwK, kBwQ), id_o = umma_idesc_bf16_bmn(kBwK, kD);
             const uint32_t ka = smem_u32(ks), va = smem_u32(vs), sa = smem_u32(stg), pa = smem_u32(pts),
@@ -627,9 +631,10 @@ __global__ void __launch_bounds__(kBwThreads, 1)
             umma_commit(acc_done);
         }
     } else {
-        // ===================== compute: thread = key row
-        const int kr = warp * 32 + lane, j = k0 + kr;
-        const uint32_t la = tmem + (uint32_t(warp * 32) << 16);
+        // ===================== compute: warpgroup wg, thread = key row; tiles t = wg, wg + 2, ...
+        const int wg = warp >> 2, w4 = warp & 3;
+        const int kr = w4 * 32 + lane, j = k0 + kr;
+        const uint32_t la = tmem + (uint32_t(w4 * 32) << 16);
         const float mkey = !p.mask ? 1.f : j < g.t_k ? __ldg(p.mask + kv_row0 + j) : 0.f;
         float* wl = cw + warp * 2 * kBwQ;  // lse[64], D[64]
         float dm = 0.f;
@@ -643,54 +648,46 @@ __global__ void __launch_bounds__(kBwThreads, 1)
             nd0 = r0 + lane < g.t_q ? __ldg(p.dsum + rb + r0 + lane) : 0.f;
             nd1 = r0 + lane + 32 < g.t_q ? __ldg(p.dsum + rb + r0 + lane + 32) : 0.f;
         };
-        fetch(0);
-        const int jw0 = k0 + warp * 32;
-        for (int t = 0; t < ntiles; ++t) {
-            const int bb = t & 1, r0 = qtile_of(t) * kBwQ;
+        fetch(wg);
+        const int jw0 = k0 + w4 * 32;
+        const int bb = wg;  // this warpgroup's S^T / dP^T / P^T / dS^T buffers
+        unsigned char* prow = pts + bb * kPT + kr * 128;
+        unsigned char* drow = dss + bb * kPT + kr * 128;
+        for (int t = wg; t < ntiles; t += kBwWG) {
+            const int r0 = qtile_of(t) * kBwQ;
             wl[lane] = nl0;
             wl[lane + 32] = nl1;
             wl[kBwQ + lane] = nd0;
             wl[kBwQ + lane + 32] = nd1;
             __syncwarp();
-            fetch(t + 1);
+            fetch(t + kBwWG);
             mbar_wait(&s_full[bb], (t >> 1) & 1);
             __syncwarp();  // reconverge before .sync.aligned tcgen05.ld
             tc_fence_after();
-            uint32_t sv[64], dv[64];
-            tmem_ld_32x32b_x32(la + bb * 64, *reinterpret_cast<uint32_t(*)[32]>(sv));
-            tmem_ld_32x32b_x32(la + bb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
-            tmem_ld_32x32b_x32(la + 128 + bb * 64, *reinterpret_cast<uint32_t(*)[32]>(dv));
-            tmem_ld_32x32b_x32(la + 128 + bb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(dv + 32));
-            tmem_ld_wait();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&s_empty[bb]);
             const bool interior = jw0 + 32 <= g.t_k && r0 + kBwQ <= g.t_q && (!g.causal || jw0 + 31 <= g.pos_offset + r0) &&
                                   !(g.self_keep && jw0 + 31 >= g.pos_offset + r0);
             if (t >= 2) mbar_wait(&pt_empty[bb], ((t >> 1) - 1) & 1);  // dV / dK of tile t-2 done with buffer bb
-            unsigned char* prow = pts + bb * kPT + kr * 128;
-            unsigned char* drow = dss + bb * kPT + kr * 128;
-            // INT: every (query, key) of this warp's tile is admissible and none is a kept self
-            // key -> no per-element tests (separate code paths; the tests were most of the work)
-            auto tile_body = [&](auto int_tag) {
+            // two 32-query chunks: S^T and dP^T columns of a chunk (64 registers) -> P^T, dS^T rows
+            // INT: every (query, key) of this warp's tile is admissible and none is a kept self key
+            auto chunk = [&](auto int_tag, int h2, const uint32_t (&sv)[32], const uint32_t (&dv)[32]) {
                 constexpr bool INT = decltype(int_tag)::value;
                 float dmq[4] = {0.f, 0.f, 0.f, 0.f};  // dmask partial sums (4 independent chains)
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {
+                for (int c = 0; c < 4; ++c) {
                     uint32_t pw[4], dw[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         float pv[2], dsv[2];
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
-                            const int i = c * 8 + e * 2 + h, r = r0 + i;
-                            float pm = fast_exp2(fmaf(__uint_as_float(sv[i]), g.c, -wl[i]));
+                            const int i = c * 8 + e * 2 + h, q = h2 * 32 + i, r = r0 + q;
+                            float pm = fast_exp2(fmaf(__uint_as_float(sv[i]), g.c, -wl[q]));
                             bool self = false;
                             if constexpr (!INT) {
                                 if (!admissible(g, j, r)) pm = 0.f;
                                 self = g.self_keep && j == g.pos_offset + r;
                             }
-                            const float dpv = __uint_as_float(dv[i]) - wl[kBwQ + i];
+                            const float dpv = __uint_as_float(dv[i]) - wl[kBwQ + q];
                             const float pj = self ? pm : pm * mkey;
                             if (!self) dmq[i & 3] = fmaf(pm, dpv, dmq[i & 3]);
                             pv[h] = pj;
@@ -699,27 +696,40 @@ __global__ void __launch_bounds__(kBwThreads, 1)
                         pw[e] = pack2(pv[0], pv[1]);
                         dw[e] = pack2(dsv[0], dsv[1]);
                     }
-                    const int off = (c ^ (kr & 7)) << 4;
+                    const int off = ((h2 * 4 + c) ^ (kr & 7)) << 4;
                     *reinterpret_cast<uint4*>(prow + off) = make_uint4(pw[0], pw[1], pw[2], pw[3]);
                     *reinterpret_cast<uint4*>(drow + off) = make_uint4(dw[0], dw[1], dw[2], dw[3]);
                 }
                 dm += (dmq[0] + dmq[1]) + (dmq[2] + dmq[3]);
             };
-            if (interior) tile_body(std::true_type{});
-            else tile_body(std::false_type{});
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+                uint32_t sv[32], dv[32];
+                tmem_ld_32x32b_x32(la + bb * 64 + h2 * 32, sv);
+                tmem_ld_32x32b_x32(la + 128 + bb * 64 + h2 * 32, dv);
+                tmem_ld_wait_dep(sv);
+                tmem_ld_wait_dep(dv);
+                if (h2 == 1) {  // both chunks read: S^T / dP^T buffer bb may be overwritten
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&s_empty[bb]);
+                }
+                if (interior) chunk(std::true_type{}, h2, sv, dv);
+                else chunk(std::false_type{}, h2, sv, dv);
+            }
             fence_proxy_async_smem();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&pt_full[bb]);
         }
-        // ---- epilogue: dV, dK (x scale) rows from TMEM, dmask
+        // ---- epilogue: warpgroup 0 writes dV, warpgroup 1 dK (x scale); dmask from both
         if (ntiles > 0) {
             mbar_wait(acc_done, 0);
             __syncwarp();  // reconverge before .sync.aligned tcgen05.ld
             tc_fence_after();
         }
-#pragma unroll
-        for (int which = 0; which < 2; ++which) {
+        {
+            const int which = wg;
             float* dst = (which ? p.dk : p.dv) + (kv_row0 + j) * kD;
             const float f = which ? g.scale : 1.f;
 #pragma unroll
@@ -741,11 +751,13 @@ __global__ void __launch_bounds__(kBwThreads, 1)
                 }
             }
         }
-        if (p.dmask && j < g.t_k) p.dmask[kv_row0 + j] = dm;
+        if (wg == 1) dmx[kr] = dm;
+        named_bar_sync_attn(1, kBwWG * 4 * 32);
+        if (wg == 0 && p.dmask && j < g.t_k) p.dmask[kv_row0 + j] = dm + dmx[kr];
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 5) {
+    if (warp == kBwMma) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
     }
@@ -1233,7 +1245,7 @@ size_t attn_dq_tc_smem() {  // no alignment slack (see dq_tc_kernel)
 }
 size_t attn_dkv_tc_smem() {
     return 1024 + 2 * attn::kBwK * 256 + 2 * 2 * attn::kBwQ * 256 + 2 * 2 * attn::kBwK * attn::kBwQ * 2 +
-           4 * 2 * attn::kBwQ * 4 + 16 * 8;
+           attn::kBwWG * 4 * 2 * attn::kBwQ * 4 + attn::kBwK * 4 + 16 * 8;
 }
 
 // m: dQ maps {Q(128-row boxes), dO(128), K(64), V(64)}, dKV maps {K(128), V(128), Q(64), dO(64)}
