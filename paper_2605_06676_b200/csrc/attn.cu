@@ -513,31 +513,28 @@ constexpr int kBwQ = 64;    // dKV: queries per streamed tile (UMMA N of S^T, K 
 constexpr int kBwWG = 2;     // dKV compute warpgroups: warpgroup w takes the query tiles t = w mod 2
 constexpr int kBwThreads = (kBwWG * 4 + 2) * 32;  // warps 0-7 compute (thread = key row = TMEM lane), 8 TMA, 9 MMA
 constexpr int kBwTma = kBwWG * 4, kBwMma = kBwWG * 4 + 1;
+constexpr int kBwStages = 4;  // Q / dO tile ring
 
 __global__ void __launch_bounds__(kBwThreads, 1)
     dkv_tc_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ CUtensorMap tk128,
                   const __grid_constant__ CUtensorMap tv128, const __grid_constant__ CUtensorMap tq64,
                   const __grid_constant__ CUtensorMap tdo64) {
-    constexpr uint32_t kKB128 = kBwK * 256, kT64 = kBwQ * 256, kStage = 2 * kT64, kPT = kBwK * kBwQ * 2;
+    constexpr uint32_t kKB128 = kBwK * 256, kT64 = kBwQ * 256, kStage = 2 * kT64;
     extern __shared__ unsigned char smem_dyn[];
     unsigned char* smem = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);  // aligned, still a __shared__ pointer
     unsigned char* ks = smem;
     unsigned char* vs = ks + kKB128;
-    unsigned char* stg = vs + kKB128;          // [2] x {Q, dO}
-    unsigned char* pts = stg + 2 * kStage;     // [2] P^T [128 keys][64 q]
-    unsigned char* dss = pts + 2 * kPT;        // [2] dS^T
-    float* cw = reinterpret_cast<float*>(dss + 2 * kPT);  // [8 warps][lse 64 | D 64]
+    unsigned char* stg = vs + kKB128;          // [kBwStages] x {Q, dO}
+    float* cw = reinterpret_cast<float*>(stg + kBwStages * kStage);  // [8 warps][lse 64 | D 64]
     float* dmx = cw + kBwWG * 4 * 2 * kBwQ;                // [128] warpgroup 1's dmask partials
     uint64_t* bars = reinterpret_cast<uint64_t*>(dmx + kBwK);
     uint64_t* kv_full = bars;
-    uint64_t* st_full = bars + 1;    // [2]
-    uint64_t* st_empty = bars + 3;   // [2]
-    uint64_t* s_full = bars + 5;     // [2]
-    uint64_t* s_empty = bars + 7;    // [2]
-    uint64_t* pt_full = bars + 9;    // [2]
-    uint64_t* pt_empty = bars + 11;  // [2]
-    uint64_t* acc_done = bars + 13;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+    uint64_t* st_full = bars + 1;                  // [kBwStages]
+    uint64_t* st_empty = st_full + kBwStages;      // [kBwStages]
+    uint64_t* s_full = st_empty + kBwStages;       // [2] (buffer = warpgroup)
+    uint64_t* pt_full = s_full + 2;                // [2]
+    uint64_t* acc_done = pt_full + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
 
     const Geo g{p.n_q_heads, p.n_kv_heads, p.n_q_heads / p.n_kv_heads, p.t_q, p.t_k, p.causal, p.pos_offset,
                 p.self_keep, p.scale * kLog2e, p.scale};
@@ -550,15 +547,13 @@ __global__ void __launch_bounds__(kBwThreads, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         mbar_init(kv_full, 1);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kBwStages; ++i) {
             mbar_init(&st_full[i], 1);
             mbar_init(&st_empty[i], 1);
-            mbar_init(&s_full[i], 1);
-            mbar_init(&s_empty[i], 4);
         }
         for (int i = 0; i < 2; ++i) {
+            mbar_init(&s_full[i], 1);
             mbar_init(&pt_full[i], 4);
-            mbar_init(&pt_empty[i], 1);
         }
         mbar_init(acc_done, 1);
         fence_barrier_init();
@@ -567,7 +562,9 @@ __global__ void __launch_bounds__(kBwThreads, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;  // S^T[2] 0/64, dP^T[2] 128/192 (buffer = warpgroup), dV 256, dK 384
+    // TMEM: S^T[2] 0/64, dP^T[2] 128/192 (buffer = warpgroup; P^T / dS^T written over their first 32
+    // columns as packed bf16 once read: the A operands of dV / dK), dV 256, dK 384
+    const uint32_t tmem = *tmem_slot;
     const size_t kv_row0 = ((size_t)b * g.n_kv_heads + kvh) * g.t_k;
     auto head_of = [&](int t) { return (b * g.n_q_heads + kvh * g.G + t / nq); };  // flat q head
     auto qtile_of = [&](int t) { return qt0 + t % nq; };
@@ -579,8 +576,8 @@ __global__ void __launch_bounds__(kBwThreads, 1)
             tma_tile<kBwK>(ks, &tk128, kv_full, (int)(kv_row0 + k0), pol);
             tma_tile<kBwK>(vs, &tv128, kv_full, (int)(kv_row0 + k0), pol);
             for (int t = 0; t < ntiles; ++t) {
-                const int st = t & 1;
-                if (t >= 2) mbar_wait_backoff(&st_empty[st], ((t >> 1) - 1) & 1);
+                const int st = t % kBwStages;
+                if (t >= kBwStages) mbar_wait_backoff(&st_empty[st], ((t / kBwStages) - 1) & 1);
                 mbar_arrive_expect_tx(&st_full[st], kStage);
                 unsigned char* d = stg + st * kStage;
                 const int hq = head_of(t), r0 = qtile_of(t) * kBwQ;
@@ -593,13 +590,11 @@ __global__ void __launch_bounds__(kBwThreads, 1)
     } else if (warp == kBwMma) {
         if (lane == 0 && ntiles > 0) {
             constexpr uint32_t id_s = umma_idesc_bf16(kBwK, kBwQ), id_o = umma_idesc_bf16_bmn(kBwK, kD);
-            const uint32_t ka = smem_u32(ks), va = smem_u32(vs), sa = smem_u32(stg), pa = smem_u32(pts),
-                           da = smem_u32(dss);
+            const uint32_t ka = smem_u32(ks), va = smem_u32(vs), sa = smem_u32(stg);
             mbar_wait_backoff(kv_full, 0);
-            auto issue_s = [&](int t) {
-                const int st = t & 1, bb = t & 1;
-                mbar_wait_backoff(&st_full[st], (t >> 1) & 1);
-                if (t >= 2) mbar_wait_backoff(&s_empty[bb], ((t >> 1) - 1) & 1);
+            auto issue_s = [&](int t) {  // S^T, dP^T of tile t into buffer t & 1
+                const int st = t % kBwStages, bb = t & 1;
+                mbar_wait_backoff(&st_full[st], (t / kBwStages) & 1);
                 tc_fence_after();
                 const uint32_t qb = sa + st * kStage, ub = qb + kT64;
 #pragma unroll
@@ -610,22 +605,23 @@ __global__ void __launch_bounds__(kBwThreads, 1)
                 }
                 umma_commit(&s_full[bb]);
             };
+            // issue order S(t+1), dV/dK(t), S(t+2), ...: the MMAs run in issue order, so dV/dK(t) has
+            // read P^T(t) / dS^T(t) before S(t+2) overwrites buffer t & 1
             issue_s(0);
             for (int t = 0; t < ntiles; ++t) {
                 if (t + 1 < ntiles) issue_s(t + 1);
-                const int st = t & 1, pb = t & 1;
+                const int st = t % kBwStages, pb = t & 1;
                 mbar_wait_backoff(&pt_full[pb], (t >> 1) & 1);
                 tc_fence_after();
-                // B = the Q / dO tiles themselves, read MN-major ([queries][d] rows, d contiguous)
+                // A = P^T / dS^T from TMEM; B = the dO / Q tiles read MN-major ([queries][d] rows)
                 const uint32_t qb = sa + st * kStage, ub = qb + kT64;
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
-                    umma_bf16(tmem + 256, umma_desc_sw128(pa + pb * kPT + kk * 32),
-                              umma_desc_sw128_mn(ub + kk * 2048, kBwQ * 128), id_o, (t > 0 || kk > 0) ? 1u : 0u);
-                    umma_bf16(tmem + 384, umma_desc_sw128(da + pb * kPT + kk * 32),
-                              umma_desc_sw128_mn(qb + kk * 2048, kBwQ * 128), id_o, (t > 0 || kk > 0) ? 1u : 0u);
+                    umma_bf16_ts(tmem + 256, tmem + pb * 64 + kk * 8, umma_desc_sw128_mn(ub + kk * 2048, kBwQ * 128), id_o,
+                                 (t > 0 || kk > 0) ? 1u : 0u);
+                    umma_bf16_ts(tmem + 384, tmem + 128 + pb * 64 + kk * 8, umma_desc_sw128_mn(qb + kk * 2048, kBwQ * 128),
+                                 id_o, (t > 0 || kk > 0) ? 1u : 0u);
                 }
-                umma_commit(&pt_empty[pb]);
                 umma_commit(&st_empty[st]);
             }
             umma_commit(acc_done);
@@ -650,9 +646,7 @@ __global__ void __launch_bounds__(kBwThreads, 1)
         };
         fetch(wg);
         const int jw0 = k0 + w4 * 32;
-        const int bb = wg;  // this warpgroup's S^T / dP^T / P^T / dS^T buffers
-        unsigned char* prow = pts + bb * kPT + kr * 128;
-        unsigned char* drow = dss + bb * kPT + kr * 128;
+        const int bb = wg;  // this warpgroup's S^T / dP^T / P^T / dS^T TMEM buffers
         for (int t = wg; t < ntiles; t += kBwWG) {
             const int r0 = qtile_of(t) * kBwQ;
             wl[lane] = nl0;
@@ -666,12 +660,12 @@ __global__ void __launch_bounds__(kBwThreads, 1)
             tc_fence_after();
             const bool interior = jw0 + 32 <= g.t_k && r0 + kBwQ <= g.t_q && (!g.causal || jw0 + 31 <= g.pos_offset + r0) &&
                                   !(g.self_keep && jw0 + 31 >= g.pos_offset + r0);
-            if (t >= 2) mbar_wait(&pt_empty[bb], ((t >> 1) - 1) & 1);  // dV / dK of tile t-2 done with buffer bb
             // two 32-query chunks: S^T and dP^T columns of a chunk (64 registers) -> P^T, dS^T rows
             // INT: every (query, key) of this warp's tile is admissible and none is a kept self key
             auto chunk = [&](auto int_tag, int h2, const uint32_t (&sv)[32], const uint32_t (&dv)[32]) {
                 constexpr bool INT = decltype(int_tag)::value;
                 float dmq[4] = {0.f, 0.f, 0.f, 0.f};  // dmask partial sums (4 independent chains)
+                uint32_t pt[16], dt[16];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     uint32_t pw[4], dw[4];
@@ -696,10 +690,15 @@ __global__ void __launch_bounds__(kBwThreads, 1)
                         pw[e] = pack2(pv[0], pv[1]);
                         dw[e] = pack2(dsv[0], dsv[1]);
                     }
-                    const int off = ((h2 * 4 + c) ^ (kr & 7)) << 4;
-                    *reinterpret_cast<uint4*>(prow + off) = make_uint4(pw[0], pw[1], pw[2], pw[3]);
-                    *reinterpret_cast<uint4*>(drow + off) = make_uint4(dw[0], dw[1], dw[2], dw[3]);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        pt[c * 4 + e] = pw[e];
+                        dt[c * 4 + e] = dw[e];
+                    }
                 }
+                // P^T / dS^T chunk over S^T / dP^T columns this thread has already read
+                tmem_st16(la + bb * 64 + h2 * 16, pt);
+                tmem_st16(la + 128 + bb * 64 + h2 * 16, dt);
                 dm += (dmq[0] + dmq[1]) + (dmq[2] + dmq[3]);
             };
 #pragma unroll
@@ -709,15 +708,10 @@ __global__ void __launch_bounds__(kBwThreads, 1)
                 tmem_ld_32x32b_x32(la + 128 + bb * 64 + h2 * 32, dv);
                 tmem_ld_wait_dep(sv);
                 tmem_ld_wait_dep(dv);
-                if (h2 == 1) {  // both chunks read: S^T / dP^T buffer bb may be overwritten
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&s_empty[bb]);
-                }
                 if (interior) chunk(std::true_type{}, h2, sv, dv);
                 else chunk(std::false_type{}, h2, sv, dv);
             }
-            fence_proxy_async_smem();
+            tmem_st_wait();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&pt_full[bb]);
@@ -1244,8 +1238,8 @@ size_t attn_dq_tc_smem() {  // no alignment slack (see dq_tc_kernel)
            attn::kTcWG * 4 * attn::kTcK * 4 + 16 * 8;
 }
 size_t attn_dkv_tc_smem() {
-    return 1024 + 2 * attn::kBwK * 256 + 2 * 2 * attn::kBwQ * 256 + 2 * 2 * attn::kBwK * attn::kBwQ * 2 +
-           attn::kBwWG * 4 * 2 * attn::kBwQ * 4 + attn::kBwK * 4 + 16 * 8;
+    return 1024 + 2 * attn::kBwK * 256 + attn::kBwStages * 2 * attn::kBwQ * 256 + attn::kBwWG * 4 * 2 * attn::kBwQ * 4 +
+           attn::kBwK * 4 + (2 * attn::kBwStages + 6) * 8 + 16;
 }
 
 // m: dQ maps {Q(128-row boxes), dO(128), K(64), V(64)}, dKV maps {K(128), V(128), Q(64), dO(64)}
