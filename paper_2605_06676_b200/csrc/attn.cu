@@ -758,31 +758,32 @@ __global__ void __launch_bounds__(kBwThreads, 1)
 }
 
 // dQ: CTA = two 128-query tiles, one compute warpgroup each (ping-pong on shared K/V tiles, as in
-// the forward).  TMEM per warpgroup: S [0,64), dP [64,128), dQ [128,256) at wg * 256.
+// the forward).  TMEM per warpgroup: S [0,64) (dS written over its first 32 columns as packed bf16,
+// the A operand of dQ += dS K), dP [64,128), dQ [128,256) at wg * 256.
 constexpr int kDqThreads = (kTcWG * 4 + 2) * 32;
+constexpr int kDqStages = 3;  // K / V tile ring
 
 __global__ void __launch_bounds__(kDqThreads, 1)
     dq_tc_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ CUtensorMap tq128,
                  const __grid_constant__ CUtensorMap tdo128, const __grid_constant__ CUtensorMap tk64,
                  const __grid_constant__ CUtensorMap tv64) {
-    constexpr uint32_t kQ128 = kTcQ * 256, kT64 = kTcK * 256, kStage = 2 * kT64, kDS = kTcQ * kTcK * 2;
+    constexpr uint32_t kQ128 = kTcQ * 256, kT64 = kTcK * 256, kStage = 2 * kT64;
     // ~226 KB of shared memory: no room for a manual 1024-byte round-up; the dynamic window starts
     // right after the 1 KB reserved block, which is 1024-aligned (checked below)
     extern __shared__ __align__(1024) unsigned char smem_dyn[];
     unsigned char* smem = smem_dyn;
     unsigned char* qs = smem;                        // [wg] Q tiles
     unsigned char* us = qs + kTcWG * kQ128;          // [wg] dO tiles
-    unsigned char* stg = us + kTcWG * kQ128;         // [2] x {K, V}
-    unsigned char* dss = stg + 2 * kStage;           // [wg] dS [128 q][64 keys]
-    float* mw = reinterpret_cast<float*>(dss + kTcWG * kDS);  // [8 warps][64]
+    unsigned char* stg = us + kTcWG * kQ128;         // [kDqStages] x {K, V}
+    float* mw = reinterpret_cast<float*>(stg + kDqStages * kStage);  // [8 warps][64]
     uint64_t* bars = reinterpret_cast<uint64_t*>(mw + kTcWG * 4 * kTcK);
     uint64_t* q_full = bars;
-    uint64_t* st_full = bars + 1;   // [2]
-    uint64_t* st_empty = bars + 3;  // [2]
-    uint64_t* s_full = bars + 5;    // [wg]
-    uint64_t* ds_full = bars + 7;   // [wg]
-    uint64_t* ds_empty = bars + 9;  // [wg]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
+    uint64_t* st_full = bars + 1;                 // [kDqStages]
+    uint64_t* st_empty = st_full + kDqStages;     // [kDqStages]
+    uint64_t* s_full = st_empty + kDqStages;      // [wg]
+    uint64_t* ds_full = s_full + kTcWG;           // [wg]
+    uint64_t* dq_done = ds_full + kTcWG;          // [wg]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + kTcWG);
     if ((smem_u32(smem) & 1023) != 0) {
         if (threadIdx.x == 0) latch_error(p.err, LKV_ERR_UNSUPPORTED, 1024);
         return;
@@ -800,14 +801,14 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     constexpr int kTmaWarp = kTcWG * 4, kMmaWarp = kTcWG * 4 + 1;
     if (threadIdx.x == 0) {
         mbar_init(q_full, 1);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kDqStages; ++i) {
             mbar_init(&st_full[i], 1);
             mbar_init(&st_empty[i], 1);
         }
         for (int w = 0; w < kTcWG; ++w) {
             mbar_init(&s_full[w], 1);
             mbar_init(&ds_full[w], 4);
-            mbar_init(&ds_empty[w], 1);
+            mbar_init(&dq_done[w], 1);
         }
         fence_barrier_init();
     }
@@ -829,8 +830,8 @@ __global__ void __launch_bounds__(kDqThreads, 1)
                 tma_tile<kTcQ>(us + w * kQ128, &tdo128, q_full, (int)(q_row0 + q0 + w * kTcQ), pol);
             }
             for (int t = 0; t < n_all; ++t) {
-                const int st = t & 1;
-                if (t >= 2) mbar_wait_backoff(&st_empty[st], ((t >> 1) - 1) & 1);
+                const int st = t % kDqStages;
+                if (t >= kDqStages) mbar_wait_backoff(&st_empty[st], ((t / kDqStages) - 1) & 1);
                 mbar_arrive_expect_tx(&st_full[st], kStage);
                 unsigned char* d = stg + st * kStage;
                 tma_tile<kTcK>(d, &tk64, &st_full[st], (int)(kv_row0 + t * kTcK), pol);
@@ -840,10 +841,10 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     } else if (warp == kMmaWarp) {
         if (lane == 0 && n_all > 0) {
             constexpr uint32_t id_s = umma_idesc_bf16(kTcQ, kTcK), id_o_mn = umma_idesc_bf16_bmn(kTcQ, kD);
-            const uint32_t sa = smem_u32(stg), da = smem_u32(dss);
+            const uint32_t sa = smem_u32(stg);
             mbar_wait_backoff(q_full, 0);
             auto issue_s = [&](int w, int t) {  // S = Q K^T and dP = dO V^T of warpgroup w, tile t
-                const uint32_t kb = sa + (t & 1) * kStage, vb = kb + kT64;
+                const uint32_t kb = sa + (t % kDqStages) * kStage, vb = kb + kT64;
                 const uint32_t qa = smem_u32(qs + w * kQ128), ua = smem_u32(us + w * kQ128);
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
@@ -859,11 +860,12 @@ __global__ void __launch_bounds__(kDqThreads, 1)
             for (int w = 0; w < kTcWG; ++w)
                 if (nt[w] > 0) issue_s(w, 0);
             for (int t = 0; t < n_all; ++t) {
-                const int st = t & 1;
+                const int st = t % kDqStages;
                 const uint32_t kb = sa + st * kStage;
                 bool next_ready = false;
-                // per warpgroup: dQ of tile t as soon as its dS lands, then at once its S / dP of tile
-                // t + 1, so each warpgroup's row math overlaps the other's MMAs
+                // per warpgroup: dQ of tile t as soon as its dS lands (A = dS from TMEM, over S), then
+                // at once its S / dP of tile t + 1 -- in issue order, so dQ(t) has read dS(t) before
+                // S(t+1) overwrites it -- so each warpgroup's row math overlaps the other's MMAs
 #pragma unroll
                 for (int w = 0; w < kTcWG; ++w) {
                     if (t >= nt[w]) continue;
@@ -871,16 +873,17 @@ __global__ void __launch_bounds__(kDqThreads, 1)
                     tc_fence_after();
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk)
-                        umma_bf16(tmem + w * 256 + 128, umma_desc_sw128(da + w * kDS + kk * 32),
-                                  umma_desc_sw128_mn(kb + kk * 2048, kTcK * 128), id_o_mn, (t > 0 || kk > 0) ? 1u : 0u);
-                    umma_commit(&ds_empty[w]);
+                        umma_bf16_ts(tmem + w * 256 + 128, tmem + w * 256 + kk * 8,
+                                     umma_desc_sw128_mn(kb + kk * 2048, kTcK * 128), id_o_mn, (t > 0 || kk > 0) ? 1u : 0u);
                     if (t + 1 < nt[w]) {
                         if (!next_ready) {
-                            mbar_wait_backoff(&st_full[(t + 1) & 1], ((t + 1) >> 1) & 1);
+                            mbar_wait_backoff(&st_full[(t + 1) % kDqStages], ((t + 1) / kDqStages) & 1);
                             tc_fence_after();
                             next_ready = true;
                         }
                         issue_s(w, t + 1);
+                    } else {
+                        umma_commit(&dq_done[w]);
                     }
                 }
                 umma_commit(&st_empty[st]);
@@ -895,7 +898,6 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         const float lse = r < g.t_q ? p.lse[q_row0 + r] : 0.f, dd = r < g.t_q ? p.dsum[q_row0 + r] : 0.f;
         const float* mask = p.mask ? p.mask + kv_row0 : nullptr;
         float* mwarp = mw + warp * kTcK;
-        unsigned char* my_ds = dss + wg * kDS;
         float mn0 = 0.f, mn1 = 0.f;
         if (mask) {
             mn0 = lane < g.t_k ? __ldg(mask + lane) : 0.f;
@@ -920,11 +922,13 @@ __global__ void __launch_bounds__(kDqThreads, 1)
             tmem_ld_32x32b_x32(la + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
             tmem_ld_32x32b_x32(la + 64, *reinterpret_cast<uint32_t(*)[32]>(dv));
             tmem_ld_32x32b_x32(la + 96, *reinterpret_cast<uint32_t(*)[32]>(dv + 32));
-            tmem_ld_wait();
+            tmem_ld_wait_dep(*reinterpret_cast<uint32_t(*)[32]>(sv));
+            tmem_ld_wait_dep(*reinterpret_cast<uint32_t(*)[32]>(sv + 32));
+            tmem_ld_wait_dep(*reinterpret_cast<uint32_t(*)[32]>(dv));
+            tmem_ld_wait_dep(*reinterpret_cast<uint32_t(*)[32]>(dv + 32));
             const bool interior = j0 + kTcK <= g.t_k && wr0 + 32 <= g.t_q && (!g.causal || j0 + kTcK - 1 <= g.pos_offset + wr0) &&
                                   !(g.self_keep && j0 + kTcK - 1 >= g.pos_offset + wr0);
-            if (t >= 1) mbar_wait(&ds_empty[wg], (t - 1) & 1);  // dQ of tile t-1 done reading dS
-            unsigned char* drow = my_ds + rl * 128;
+            uint32_t dsw[32];  // dS row, packed bf16 -> TMEM over S (all of S and dP already read)
             auto tile_body = [&](auto int_tag) {  // INT: no per-element admissibility tests
                 constexpr bool INT = decltype(int_tag)::value;
 #pragma unroll
@@ -946,20 +950,20 @@ __global__ void __launch_bounds__(kDqThreads, 1)
                         }
                         dw[e] = pack2(dsv[0], dsv[1]);
                     }
-                    *reinterpret_cast<uint4*>(drow + ((c ^ (rl & 7)) << 4)) = make_uint4(dw[0], dw[1], dw[2], dw[3]);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) dsw[c * 4 + e] = dw[e];
                 }
             };
             if (interior) tile_body(std::true_type{});
             else tile_body(std::false_type{});
-            fence_proxy_async_smem();
+            tmem_st32(la, dsw);
+            tmem_st_wait();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&ds_full[wg]);
         }
-        // the last dQ of this warpgroup has retired once its ds_empty phase completes
-        if (ntw > 1) mbar_wait(&ds_empty[wg], (ntw - 2) & 1);
-        if (ntw > 0) {
-            mbar_wait(&ds_empty[wg], (ntw - 1) & 1);
+        if (ntw > 0) {  // the last dQ of this warpgroup has landed
+            mbar_wait(&dq_done[wg], 0);
             __syncwarp();  // reconverge before .sync.aligned tcgen05.ld
             tc_fence_after();
         }
@@ -1234,8 +1238,8 @@ cudaError_t launch_attn_fwd(const AttnParams& p, int dtype, int d, const CUtenso
 }
 
 size_t attn_dq_tc_smem() {  // no alignment slack (see dq_tc_kernel)
-    return 2 * attn::kTcWG * attn::kTcQ * 256 + 2 * 2 * attn::kTcK * 256 + attn::kTcWG * attn::kTcQ * attn::kTcK * 2 +
-           attn::kTcWG * 4 * attn::kTcK * 4 + 16 * 8;
+    return 2 * attn::kTcWG * attn::kTcQ * 256 + attn::kDqStages * 2 * attn::kTcK * 256 + attn::kTcWG * 4 * attn::kTcK * 4 +
+           (1 + 2 * attn::kDqStages + 3 * attn::kTcWG) * 8 + 16;
 }
 size_t attn_dkv_tc_smem() {
     return 1024 + 2 * attn::kBwK * 256 + attn::kBwStages * 2 * attn::kBwQ * 256 + attn::kBwWG * 4 * 2 * attn::kBwQ * 4 +
