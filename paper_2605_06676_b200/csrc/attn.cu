@@ -235,7 +235,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const Geo g{p.n_q_heads, p.n_kv_heads, p.n_q_heads / p.n_kv_heads, p.t_q, p.t_k, p.causal, p.pos_offset,
                 p.self_keep, p.scale * kLog2e, p.scale};
     const int b = blockIdx.z, qh = blockIdx.y, kvh = qh / g.G;
-    const int q0 = blockIdx.x * (kTcWG * kTcQ);
+    // causal: the last query blocks see the most keys -- dispatch them first (longest first keeps
+    // the last wave short)
+    const int qb = p.causal ? (int)(gridDim.x - 1 - blockIdx.x) : (int)blockIdx.x;
+    const int q0 = qb * (kTcWG * kTcQ);
     int nt[kTcWG];
 #pragma unroll
     for (int w = 0; w < kTcWG; ++w) nt[w] = f2_tiles(g, q0 + w * kTcQ);
@@ -792,7 +795,10 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     const Geo g{p.n_q_heads, p.n_kv_heads, p.n_q_heads / p.n_kv_heads, p.t_q, p.t_k, p.causal, p.pos_offset,
                 p.self_keep, p.scale * kLog2e, p.scale};
     const int b = blockIdx.z, qh = blockIdx.y, kvh = qh / g.G;
-    const int q0 = blockIdx.x * (kTcWG * kTcQ);
+    // causal: the last query blocks see the most keys -- dispatch them first (longest first keeps
+    // the last wave short)
+    const int qb = p.causal ? (int)(gridDim.x - 1 - blockIdx.x) : (int)blockIdx.x;
+    const int q0 = qb * (kTcWG * kTcQ);
     int nt[kTcWG];
 #pragma unroll
     for (int w = 0; w < kTcWG; ++w) nt[w] = tc_tiles(g, q0 + w * kTcQ);
