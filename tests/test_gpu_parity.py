@@ -390,7 +390,10 @@ def _decode_oracle(rc: lkv.RaggedCache, q, n_kv, scale):
 
 
 @pytest.mark.parametrize("dtype,G,steps", [(torch.float32, 4, 3), (torch.bfloat16, 4, 3), (torch.bfloat16, 8, 2),
-                                           (torch.bfloat16, 16, 1)])
+                                           (torch.bfloat16, 16, 1),
+                                           # G = 16: 16 combine CTAs per head, several steps (the combine
+                                           # must never see a length another CTA of the head advanced)
+                                           (torch.bfloat16, 16, 5)])
 def test_decode_steps(dtype, G, steps):
     torch.manual_seed(21)
     n_seq, L, H, T, D = 2, 2, 2, 1500, 128
