@@ -73,6 +73,9 @@ CASES = [
     (1, 8, 2, 45, 45, 16, torch.float32, True, True, 0, False, 1e-5),         # the reference's toy head width
     (2, 4, 1, 33, 80, 128, torch.float32, True, True, 47, True, 1e-5),
     (1, 2, 2, 20, 50, 64, torch.float32, False, False, 0, False, 1e-5),
+    # long enough for the forward / backward interior-tile fast paths and several K/V ring wraps
+    (1, 4, 1, 640, 640, 128, torch.bfloat16, True, True, 0, False, 1e-2),
+    (1, 2, 2, 384, 1024, 128, torch.bfloat16, True, True, 640, True, 1e-2),
 ]
 
 
