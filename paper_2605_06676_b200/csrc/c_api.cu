@@ -1257,10 +1257,11 @@ lkv_status lkv_model_plan(const lkv_model_desc* m, const lkv_ragged_desc* r, int
     if ((st = check_ws(ws, ws_bytes, w.total))) return st;
     cudaStream_t s = (cudaStream_t)stream;
     LKV_CUDA(cudaMemsetAsync(ws, 0, w.total, s), "workspace clear");
-    // per-layer launches: aim for ~2 items per resident CTA in each layer
+    // per-layer launches: one wave of work items per layer (bf16), ~2 items per resident CTA (fp32)
     LKV_CUDA(launch_decode_plan(r->offsets, n_seq, g.L, g.H, at<DecodeItem>(ws, w.dec.items),
                                 at<int32_t>(ws, w.dec.item_base), at<int32_t>(ws, w.dec.layer_begin),
-                                at<int32_t>(ws, w.dec.n_items), at<int32_t>(ws, w.dec.ch), 4 * num_sms(),
+                                at<int32_t>(ws, w.dec.n_items), at<int32_t>(ws, w.dec.ch),
+                                g.dtype == LKV_BF16 ? -decode_resident_ctas(g.Hq / g.H, num_sms()) : 4 * num_sms(),
                                 g.Hq / g.H, s),
              "decode plan");
     LKV_CUDA(launch_rope_table(m->max_seq_len, g.D, m->rope_base, 0, at<float2>(ws, w.rope), s), "rope table");

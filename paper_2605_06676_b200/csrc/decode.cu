@@ -50,6 +50,7 @@ constexpr int kDecThreads = (kDecConsumers + 1) * 32;
 // SM while an all-layer launch keeps long items; ch never leaves G * chunks of a head above
 // the combine's table (kCombMaxChunks).
 constexpr int kCombMaxChunks = 8192;  // G * chunks per head (G=4: 2M rows, G=8: 1M rows at ch=1024)
+constexpr int kPlanMaxLayers = 256;   // layers the one-wave policy tracks
 __global__ void __launch_bounds__(1024) decode_plan_kernel(const int64_t* offsets, int n_seq, int n_layers, int n_kv,
                                                            DecodeItem* items, int32_t* item_base,
                                                            int32_t* layer_begin, int32_t* n_items, int32_t* ch_out,
@@ -72,11 +73,41 @@ __global__ void __launch_bounds__(1024) decode_plan_kernel(const int64_t* offset
         atomicMax(&s_maxcap, (unsigned long long)cap);
     }
     __syncthreads();
-    // the largest ch meeting the target, else the smallest; then grown until the combine fits
     int ch = 128;
-    for (int i = 0; i < 4; ++i)
-        if ((long long)s_cnt[i] >= (long long)target_items * n_layers) ch = 128 << i;
-    while (ch < kDecMaxCh && (long long)((s_maxcap + ch - 1) / ch) * G > kCombMaxChunks) ch <<= 1;
+    if (target_items < 0 && n_layers <= kPlanMaxLayers) {
+        // one-wave policy (per-layer launches, target = -slots): the smallest ch (a multiple of 64)
+        // whose busiest layer has no more items than the launch has resident CTAs, so no layer's
+        // attention runs a second, mostly idle wave
+        __shared__ int32_t s_lay[kPlanMaxLayers];
+        __shared__ int32_t s_ok;
+        ch = kDecMaxCh;
+        for (int c = 128; c <= kDecMaxCh; c += 64) {
+            for (int l = threadIdx.x; l < n_layers; l += 1024) s_lay[l] = 0;
+            __syncthreads();
+            for (int h = threadIdx.x; h < n_heads; h += 1024) {
+                const int64_t cap = offsets[h + 1] - offsets[h];
+                atomicAdd(&s_lay[(h / n_kv) % n_layers], (int32_t)(cap > 0 ? (cap + c - 1) / c : 1));
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int mx = 0;
+                for (int l = 0; l < n_layers; ++l) mx = max(mx, s_lay[l]);
+                s_ok = mx <= -target_items;
+            }
+            __syncthreads();
+            if (s_ok) {
+                ch = c;
+                break;
+            }
+        }
+    } else {
+        // the largest ch meeting the target, else the smallest
+        const int tgt = target_items < 0 ? -target_items : target_items;
+        for (int i = 0; i < 4; ++i)
+            if ((long long)s_cnt[i] >= (long long)tgt * n_layers) ch = 128 << i;
+    }
+    // then grown until the combine fits
+    while (ch < kDecMaxCh && (long long)((s_maxcap + ch - 1) / ch) * G > kCombMaxChunks) ch = min(kDecMaxCh, ch * 2);
     if (threadIdx.x == 0) *ch_out = ch;
     for (int base = 0; base < n_heads; base += 1024) {
         const int j = base + threadIdx.x;
@@ -668,6 +699,17 @@ cudaError_t launch_decode_plan(const int64_t* offsets, int n_seq, int n_layers, 
 
 size_t decode_bf16_smem(int G) {
     return 1024 + kDecStages * (2 * kDecStageRows * 256) + 2 * kDecStages * 8 + (size_t)kDecConsumers * G * (128 + 2) * 4;
+}
+
+// resident CTAs of one bf16 decode launch (its persistent grid size): the one-wave plan target
+int decode_resident_ctas(int G, int num_sms) {
+    auto kern = G > 8 ? decode_attn_bf16_kernel<true> : decode_attn_bf16_kernel<false>;
+    const size_t smem = decode_bf16_smem(G);
+    int per_sm = 0;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDecThreads, smem) != cudaSuccess)
+        per_sm = 1;
+    return max(1, min(per_sm, kDecPerSm)) * num_sms;
 }
 
 cudaError_t launch_decode(const DecodeParams& p, int dtype, const CUtensorMap* mk, const CUtensorMap* mv, int num_sms,

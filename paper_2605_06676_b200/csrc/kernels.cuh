@@ -131,12 +131,15 @@ struct DecodeParams {
     int32_t* new_len;  // [n_heads] lens + 1 as the attention kernel read it (chunk 0 writes it)
     ErrWord* err;
 };
+// target_items > 0: the largest power-of-two ch giving at least that many items per layer;
+// target_items < 0: the smallest ch (multiple of 64) whose busiest layer fits -target_items items
 cudaError_t launch_decode_plan(const int64_t* offsets, int n_seq, int n_layers, int n_kv, DecodeItem* items,
                                int32_t* item_base, int32_t* layer_begin, int32_t* n_items, int32_t* ch,
                                int target_items, int G, cudaStream_t stream);
 constexpr int kDecMinCh = 128;  // smallest work item the plan may choose (workspace sizing)
 cudaError_t launch_decode(const DecodeParams& p, int dtype, const CUtensorMap* mk, const CUtensorMap* mv, int num_sms,
                           cudaStream_t stream);
+int decode_resident_ctas(int G, int num_sms);
 
 // ---- attn.cu (training-time multiplicative-mask attention)
 struct AttnParams {
