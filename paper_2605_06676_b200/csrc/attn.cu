@@ -424,22 +424,36 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     for (int i = 0; i < 32; ++i) mk[i] = 1.f;
                 }
                 uint32_t pw[16];
+                if constexpr (INT) {
+                    // packed pairs (FFMA2 / FMUL2 / FADD2): the row math is issue-bound
+                    const float2 c2 = make_float2(g.c, g.c), ns2 = make_float2(-sub, -sub);
+                    float2 acc2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                    float pv[2];
+                    for (int e = 0; e < 16; ++e) {
+                        float2 a2 = __ffma2_rn(make_float2(x[2 * e], x[2 * e + 1]), c2, ns2);
+                        a2 = make_float2(fast_exp2(a2.x), fast_exp2(a2.y));
+                        a2 = __fmul2_rn(a2, make_float2(mk[2 * e], mk[2 * e + 1]));
+                        acc2[e & 1] = __fadd2_rn(acc2[e & 1], a2);
+                        pw[e] = pack2(a2.x, a2.y);
+                    }
+                    ls[0] += acc2[0].x;
+                    ls[1] += acc2[0].y;
+                    ls[2] += acc2[1].x;
+                    ls[3] += acc2[1].y;
+                } else {
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int i = 2 * e + h;
-                        float mj = mk[i];
-                        if constexpr (INT) {
-                            pv[h] = fast_exp2(fmaf(x[i], g.c, -sub)) * mj;
-                        } else {
+                    for (int e = 0; e < 16; ++e) {
+                        float pv[2];
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int i = 2 * e + h;
+                            float mj = mk[i];
                             if (g.self_keep && j0 + c * kF2Chunk + i == g.pos_offset + r) mj = 1.f;
                             pv[h] = fast_exp2(x[i] - sub) * mj;  // x = -inf -> 0
+                            ls[i & 3] += pv[h];
                         }
-                        ls[i & 3] += pv[h];
+                        pw[e] = pack2(pv[0], pv[1]);
                     }
-                    pw[e] = pack2(pv[0], pv[1]);
                 }
                 tmem_st16(lane_addr + s_col + c * 16, pw);  // P chunk c over S columns already read
             };
