@@ -683,34 +683,57 @@ __global__ void __launch_bounds__(kBwThreads, 1)
                 constexpr bool INT = decltype(int_tag)::value;
                 float dmq[4] = {0.f, 0.f, 0.f, 0.f};  // dmask partial sums (4 independent chains)
                 uint32_t pt[16], dt[16];
+                if constexpr (INT) {
+                    // packed pairs of adjacent queries (FFMA2 / FMUL2 / FADD2; lse / D pairs as 8-byte loads)
+                    const float2 c2 = make_float2(g.c, g.c), mk2 = make_float2(mkey, mkey);
+                    const float2* wl2 = reinterpret_cast<const float2*>(wl + h2 * 32);
+                    const float2* wd2 = reinterpret_cast<const float2*>(wl + kBwQ + h2 * 32);
+                    float2 dma[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    uint32_t pw[4], dw[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        float pv[2], dsv[2];
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            const int i = c * 8 + e * 2 + h, q = h2 * 32 + i, r = r0 + q;
-                            float pm = fast_exp2(fmaf(__uint_as_float(sv[i]), g.c, -wl[q]));
-                            bool self = false;
-                            if constexpr (!INT) {
-                                if (!admissible(g, j, r)) pm = 0.f;
-                                self = g.self_keep && j == g.pos_offset + r;
-                            }
-                            const float dpv = __uint_as_float(dv[i]) - wl[kBwQ + q];
-                            const float pj = self ? pm : pm * mkey;
-                            if (!self) dmq[i & 3] = fmaf(pm, dpv, dmq[i & 3]);
-                            pv[h] = pj;
-                            dsv[h] = pj * dpv;
-                        }
-                        pw[e] = pack2(pv[0], pv[1]);
-                        dw[e] = pack2(dsv[0], dsv[1]);
+                    for (int e = 0; e < 16; ++e) {
+                        const float2 l2 = wl2[e], d2 = wd2[e];
+                        float2 a2 = __ffma2_rn(make_float2(__uint_as_float(sv[2 * e]), __uint_as_float(sv[2 * e + 1])), c2,
+                                               make_float2(-l2.x, -l2.y));
+                        const float2 pm = make_float2(fast_exp2(a2.x), fast_exp2(a2.y));
+                        const float2 dpv = __fadd2_rn(make_float2(__uint_as_float(dv[2 * e]), __uint_as_float(dv[2 * e + 1])),
+                                                      make_float2(-d2.x, -d2.y));
+                        dma[e & 1] = __ffma2_rn(pm, dpv, dma[e & 1]);
+                        const float2 pj = __fmul2_rn(pm, mk2);
+                        const float2 ds = __fmul2_rn(pj, dpv);
+                        pt[e] = pack2(pj.x, pj.y);
+                        dt[e] = pack2(ds.x, ds.y);
                     }
+                    dmq[0] = dma[0].x;
+                    dmq[1] = dma[0].y;
+                    dmq[2] = dma[1].x;
+                    dmq[3] = dma[1].y;
+                } else {
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        pt[c * 4 + e] = pw[e];
-                        dt[c * 4 + e] = dw[e];
+                    for (int c = 0; c < 4; ++c) {
+                        uint32_t pw[4], dw[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            float pv[2], dsv[2];
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                const int i = c * 8 + e * 2 + h, q = h2 * 32 + i, r = r0 + q;
+                                float pm = fast_exp2(fmaf(__uint_as_float(sv[i]), g.c, -wl[q]));
+                                if (!admissible(g, j, r)) pm = 0.f;
+                                const bool self = g.self_keep && j == g.pos_offset + r;
+                                const float dpv = __uint_as_float(dv[i]) - wl[kBwQ + q];
+                                const float pj = self ? pm : pm * mkey;
+                                if (!self) dmq[i & 3] = fmaf(pm, dpv, dmq[i & 3]);
+                                pv[h] = pj;
+                                dsv[h] = pj * dpv;
+                            }
+                            pw[e] = pack2(pv[0], pv[1]);
+                            dw[e] = pack2(dsv[0], dsv[1]);
+                        }
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            pt[c * 4 + e] = pw[e];
+                            dt[c * 4 + e] = dw[e];
+                        }
                     }
                 }
                 // P^T / dS^T chunk over S^T / dP^T columns this thread has already read
