@@ -974,27 +974,39 @@ __global__ void __launch_bounds__(kDqThreads, 1)
             uint32_t dsw[32];  // dS row, packed bf16 -> TMEM over S (all of S and dP already read)
             auto tile_body = [&](auto int_tag) {  // INT: no per-element admissibility tests
                 constexpr bool INT = decltype(int_tag)::value;
+                if constexpr (INT) {  // packed pairs of adjacent keys (FFMA2 / FMUL2 / FADD2)
+                    const float2 c2 = make_float2(g.c, g.c), nl2 = make_float2(-lse, -lse), nd2 = make_float2(-dd, -dd);
+                    const float2* m2 = reinterpret_cast<const float2*>(mwarp);
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    uint32_t dw[4];
+                    for (int e = 0; e < 32; ++e) {
+                        const float2 a2 = __ffma2_rn(make_float2(__uint_as_float(sv[2 * e]), __uint_as_float(sv[2 * e + 1])), c2, nl2);
+                        float2 pm = make_float2(fast_exp2(a2.x), fast_exp2(a2.y));
+                        if (mask) pm = __fmul2_rn(pm, m2[e]);
+                        const float2 dpv = __fadd2_rn(make_float2(__uint_as_float(dv[2 * e]), __uint_as_float(dv[2 * e + 1])), nd2);
+                        const float2 ds = __fmul2_rn(pm, dpv);
+                        dsw[e] = pack2(ds.x, ds.y);
+                    }
+                } else {
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        float dsv[2];
+                    for (int c = 0; c < 8; ++c) {
+                        uint32_t dw[4];
 #pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            const int i = c * 8 + e * 2 + h, jj = j0 + i;
-                            float mj = mask ? mwarp[i] : 1.f;
-                            float pm = fast_exp2(fmaf(__uint_as_float(sv[i]), g.c, -lse));
-                            if constexpr (!INT) {
+                        for (int e = 0; e < 4; ++e) {
+                            float dsv[2];
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                const int i = c * 8 + e * 2 + h, jj = j0 + i;
+                                float mj = mask ? mwarp[i] : 1.f;
+                                float pm = fast_exp2(fmaf(__uint_as_float(sv[i]), g.c, -lse));
                                 if (!admissible(g, jj, r)) pm = 0.f;
                                 if (g.self_keep && jj == g.pos_offset + r) mj = 1.f;
+                                dsv[h] = pm * mj * (__uint_as_float(dv[i]) - dd);
                             }
-                            dsv[h] = pm * mj * (__uint_as_float(dv[i]) - dd);
+                            dw[e] = pack2(dsv[0], dsv[1]);
                         }
-                        dw[e] = pack2(dsv[0], dsv[1]);
-                    }
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) dsw[c * 4 + e] = dw[e];
+                        for (int e = 0; e < 4; ++e) dsw[c * 4 + e] = dw[e];
+                    }
                 }
             };
             if (interior) tile_body(std::true_type{});
