@@ -79,10 +79,12 @@ CASES = [
 ]
 
 
-@pytest.mark.parametrize("case", CASES, ids=[f"c{i}" for i in range(len(CASES))])
-def test_masked_attention_fwd_bwd_vs_oracle(case):
-    B, Hq, Hkv, Tq, Tk, D, dtype, masked, causal, off, self_keep, tol = case
-    q, k, v, du, mask = _inputs(B, Hq, Hkv, Tq, Tk, D, dtype, masked, seed=hash(case) % 10000)
+@pytest.mark.parametrize("ci", range(len(CASES)), ids=[f"c{i}" for i in range(len(CASES))])
+def test_masked_attention_fwd_bwd_vs_oracle(ci):
+    # a fixed seed per case: reproducible inputs (hash() of a tuple holding a torch dtype is not
+    # stable across processes)
+    B, Hq, Hkv, Tq, Tk, D, dtype, masked, causal, off, self_keep, tol = CASES[ci]
+    q, k, v, du, mask = _inputs(B, Hq, Hkv, Tq, Tk, D, dtype, masked, seed=1000 + ci)
     scale = 1.0 / np.sqrt(D)
     out, lse = train.masked_attention_fwd(q, k, v, mask, causal, scale, off, self_keep)
     dq, dk, dv, dm = train.masked_attention_bwd(q, k, v, mask, out, lse, du, causal, scale, off, self_keep)
