@@ -188,86 +188,63 @@ __device__ __forceinline__ int unit_owner(int64_t u, int64_t U, int P) { return 
 // cut into p.split equal k-ranges, one CTA each, forming a thread-block cluster; the partial
 // products are summed by the cluster's rank-0 CTA straight from its peers' shared memory (DSMEM),
 // in rank order (deterministic), instead of the stream-K global partials + arrival counter.
-template <int NBT, bool SPLIT>
-__global__ void __launch_bounds__(kWsThreads, kWsPerSm) wstream_gemv_kernel(const __grid_constant__ GemvParams p) {
-    constexpr int kActBytes = 8 * NBT * 256;  // 8 k16 steps x NBT tiles x 32 lanes x 8 B
+// ---- one GEMV phase over the CTA's unit range [u0, u1), shared by the single-GEMV kernel and the
+// chained persistent kernel.  The ring (st, ph) carries over from phase to phase: producer and
+// consumers walk the same unit sequence.
+//
+// Producer: weight unit + activation slice per stage.  The first min(n, stages) weight copies go out
+// before `gate()` (griddepcontrol.wait for the first phase, the grid barrier of the previous phase in
+// a chain): weights never depend on earlier work, activations do.
+template <int NBT, typename Gate>
+__device__ __forceinline__ void ws_produce(const GemvParams& p, int64_t u0, int64_t u1, unsigned char* smem,
+                                           uint64_t* full, uint64_t* empty, int& st, uint32_t& ph, bool fresh,
+                                           Gate&& gate) {
+    constexpr int kActBytes = 8 * NBT * 256;
     constexpr int kStage = kWsUnitBytes + kActBytes;
-    extern __shared__ unsigned char smem_raw[];
-    unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);  // aligned, still a __shared__ pointer
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kWsStages * kStage);
-    uint64_t* empty = full + kWsStages;
-    float* red = reinterpret_cast<float*>(empty + kWsStages);  // [4][64][NBT * 8]
-    float(*y)[kYPad] = reinterpret_cast<float(*)[kYPad]>(red + kWsConsumers * kWsCols * NBT * 8);
-    int* s_last = reinterpret_cast<int*>(y + kWsCols);
-    int* s_slot = s_last + 4;  // [kWsMaxSplit]: partial slots of the CTAs sharing a column group
+    const uint64_t pol_w = l2_policy_evict_first(), pol_a = l2_policy_evict_last();
+    const unsigned char* wsrc = static_cast<const unsigned char*>(p.w);
+    const unsigned char* asrc = static_cast<const unsigned char*>(p.act);
+    const int64_t n = u1 - u0;
+    const int npre = (int)(n < kWsStages ? n : kWsStages);
+    const int st0 = st;
+    for (int64_t i = 0; i < n; ++i) {
+        if (!(fresh && i < kWsStages)) mbar_wait(&empty[st], ph ^ 1);
+        mbar_arrive_expect_tx(&full[st], kStage);
+        const int64_t u = u0 + i;
+        bulk_g2s(smem + st * kStage, wsrc + (size_t)u * kWsUnitBytes, kWsUnitBytes, &full[st], pol_w);
+        if (i >= npre)
+            bulk_g2s(smem + st * kStage + kWsUnitBytes, asrc + (size_t)(u % p.KU) * kActBytes, kActBytes, &full[st],
+                     pol_a);
+        if (i == npre - 1) {
+            gate();
+            for (int j = 0; j < npre; ++j) {
+                const int sj = (st0 + j) % kWsStages;
+                bulk_g2s(smem + sj * kStage + kWsUnitBytes, asrc + (size_t)((u0 + j) % p.KU) * kActBytes, kActBytes,
+                         &full[sj], pol_a);
+            }
+        }
+        if (++st == kWsStages) {
+            st = 0;
+            ph ^= 1;
+        }
+    }
+}
 
+// Consumers (4 warps): mma.sync over each unit, fixed-order cross-warp reduction into y, stream-K
+// fix-up of column groups cut by a CTA boundary (last-arriving CTA sums the partials in CTA order),
+// fused epilogue.  SPLIT: one column group per CTA, reduced across the cluster by the caller.
+template <int NBT, bool SPLIT>
+__device__ __forceinline__ void ws_consume(const GemvParams& p, int64_t u0, int64_t u1, unsigned char* smem,
+                                           uint64_t* full, uint64_t* empty, float* red, float (*y)[kYPad],
+                                           int* s_last, int* s_slot, int& st, uint32_t& ph) {
+    constexpr int kActBytes = 8 * NBT * 256;
+    constexpr int kStage = kWsUnitBytes + kActBytes;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    GTRACE(5);
+    const int tid = threadIdx.x;  // 0..127
     const int64_t U = (int64_t)p.NG * p.KU;
     const int P = gridDim.x, c = blockIdx.x;
-    int64_t u0, u1;
-    int rank = 0;
-    if constexpr (SPLIT) {
-        const int S = p.split, ng = c / S;
-        rank = c - ng * S;  // == %cluster_ctarank (clusters of S consecutive CTAs)
-        u0 = (int64_t)ng * p.KU + (int64_t)rank * p.KU / S;
-        u1 = (int64_t)ng * p.KU + (int64_t)(rank + 1) * p.KU / S;
-    } else {
-        u0 = unit_begin(c, U, P);
-        u1 = unit_begin(c + 1, U, P);
-    }
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < kWsStages; ++i) {
-            mbar_init(&full[i], 1);
-            mbar_init(&empty[i], kWsConsumers);
-        }
-        fence_barrier_init();
-    }
-    __syncthreads();
-    pdl_trigger();
-
-    if (warp == kWsConsumers) {
-        // ===================== producer =====================
-        if (lane == 0 && u1 > u0) {
-            const uint64_t pol_w = l2_policy_evict_first(), pol_a = l2_policy_evict_last();
-            const unsigned char* wsrc = static_cast<const unsigned char*>(p.w);
-            const unsigned char* asrc = static_cast<const unsigned char*>(p.act);
-            const int npre = (int)(u1 - u0 < kWsStages ? u1 - u0 : kWsStages);
-            // weights do not depend on the previous kernel: start streaming them before the wait
-            for (int i = 0; i < npre; ++i) {
-                mbar_arrive_expect_tx(&full[i], kStage);
-                bulk_g2s(smem + i * kStage, wsrc + (size_t)(u0 + i) * kWsUnitBytes, kWsUnitBytes, &full[i], pol_w);
-            }
-            pdl_wait();
-            for (int i = 0; i < npre; ++i) {
-                const int ku = (int)((u0 + i) % p.KU);
-                bulk_g2s(smem + i * kStage + kWsUnitBytes, asrc + (size_t)ku * kActBytes, kActBytes, &full[i], pol_a);
-            }
-            int st = npre % kWsStages;
-            uint32_t ph = (npre == kWsStages) ? 1u : 0u;
-            for (int64_t u = u0 + npre; u < u1; ++u) {
-                mbar_wait(&empty[st], ph ^ 1);
-                mbar_arrive_expect_tx(&full[st], kStage);
-                const int ku = (int)(u % p.KU);
-                bulk_g2s(smem + st * kStage, wsrc + (size_t)u * kWsUnitBytes, kWsUnitBytes, &full[st], pol_w);
-                bulk_g2s(smem + st * kStage + kWsUnitBytes, asrc + (size_t)ku * kActBytes, kActBytes, &full[st],
-                         pol_a);
-                if (++st == kWsStages) {
-                    st = 0;
-                    ph ^= 1;
-                }
-            }
-        }
-        if constexpr (!SPLIT) return;
-    } else {
-
-    // ===================== consumers =====================
-    pdl_wait();
-    const int tid = threadIdx.x;  // 0..127
     GTRACE(0);
     const int g = lane >> 2, cq = (lane & 3) * 2;
-    int st = 0;
-    uint32_t ph = 0;
     int64_t u = u0;
     const int ng_first = (int)(u0 / p.KU);
     while (u < u1) {
@@ -328,7 +305,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsPerSm) wstream_gemv_kernel(cons
             y[n][b] = v;
         }
         named_sync(1, kWsConsumers * 32);
-        if constexpr (SPLIT) break;  // one column group per CTA: reduced across the cluster below
+        if constexpr (SPLIT) break;  // one column group per CTA: reduced across the cluster by the caller
         if (!whole && !(LKV_GEMV_EXPT & 2)) {
             // stream-K fix-up: partial -> global slot; the last CTA of the group sums in CTA order
             const int slot = 2 * c + (ng == ng_first ? 0 : 1);
@@ -383,7 +360,55 @@ __global__ void __launch_bounds__(kWsThreads, kWsPerSm) wstream_gemv_kernel(cons
         named_sync(1, kWsConsumers * 32);
         GTRACE(4);
     }
-    }  // consumers
+}
+
+template <int NBT, bool SPLIT>
+__global__ void __launch_bounds__(kWsThreads, kWsPerSm) wstream_gemv_kernel(const __grid_constant__ GemvParams p) {
+    constexpr int kActBytes = 8 * NBT * 256;  // 8 k16 steps x NBT tiles x 32 lanes x 8 B
+    constexpr int kStage = kWsUnitBytes + kActBytes;
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);  // aligned, still a __shared__ pointer
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kWsStages * kStage);
+    uint64_t* empty = full + kWsStages;
+    float* red = reinterpret_cast<float*>(empty + kWsStages);  // [4][64][NBT * 8]
+    float(*y)[kYPad] = reinterpret_cast<float(*)[kYPad]>(red + kWsConsumers * kWsCols * NBT * 8);
+    int* s_last = reinterpret_cast<int*>(y + kWsCols);
+    int* s_slot = s_last + 4;  // [kWsMaxSplit]: partial slots of the CTAs sharing a column group
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    GTRACE(5);
+    const int64_t U = (int64_t)p.NG * p.KU;
+    const int P = gridDim.x, c = blockIdx.x;
+    int64_t u0, u1;
+    int rank = 0;
+    if constexpr (SPLIT) {
+        const int S = p.split, ng = c / S;
+        rank = c - ng * S;  // == %cluster_ctarank (clusters of S consecutive CTAs)
+        u0 = (int64_t)ng * p.KU + (int64_t)rank * p.KU / S;
+        u1 = (int64_t)ng * p.KU + (int64_t)(rank + 1) * p.KU / S;
+    } else {
+        u0 = unit_begin(c, U, P);
+        u1 = unit_begin(c + 1, U, P);
+    }
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kWsStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], kWsConsumers);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    pdl_trigger();
+    int st = 0;
+    uint32_t ph = 0;
+    if (warp == kWsConsumers) {
+        // weights do not depend on the previous kernel: the first stages stream before the wait
+        if (lane == 0 && u1 > u0) ws_produce<NBT>(p, u0, u1, smem, full, empty, st, ph, true, [] { pdl_wait(); });
+        if constexpr (!SPLIT) return;
+    } else {
+        pdl_wait();
+        ws_consume<NBT, SPLIT>(p, u0, u1, smem, full, empty, red, y, s_last, s_slot, st, ph);
+    }
     if constexpr (SPLIT) {
         // every thread of every CTA in the cluster (the producer warp too) joins both barriers
         cluster_sync_all();
