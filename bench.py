@@ -412,6 +412,43 @@ def cpu_baseline(cache, scorers, ev, n_threads=1, n_heads=8):
             "seconds": dt}
 
 
+def reference_code_sample(t=8192, d=128):
+    """One head through the reference's OWN compiled functions (oracle/_ref: proj/src built unmodified
+    over our minimal Eigen header): allocate_budgets (policy.cpp:110-120) + token_scores
+    (policy.cpp:131-136, its native [k;v] 256->128->1 SiLU scorer) + hard_topk (soft_topk.cpp:191-201).
+    Single-threaded, as prefill_with_eviction is (evictsim.cpp:131-222).  None when _ref is absent."""
+    import ctypes as C
+
+    import numpy as np
+
+    import oracle as O
+
+    R = O.ref_lib()
+    if R is None:
+        return None
+    rng = np.random.default_rng(7)
+    k = rng.standard_normal((t, d))
+    v = rng.standard_normal((t, d))
+    w1 = rng.standard_normal((2 * d, d)) / np.sqrt(2 * d)
+    b1 = np.zeros(d)
+    w2 = rng.standard_normal(d) / np.sqrt(d)
+    logits = rng.standard_normal(256)
+    ratios = np.empty(256)
+    u = np.empty(t)
+    mask = np.empty(t, np.int32)
+    p = lambda a: a.ctypes.data_as(O._dp)  # noqa: E731
+    t0 = time.perf_counter()
+    assert R.ref_allocate_budgets(p(logits), 32, 8, 0.15, p(ratios)) == 0
+    assert R.ref_token_scores(p(k), p(v), t, d, p(w1), p(b1), p(w2), d, p(u)) == 0
+    assert R.ref_hard_topk(p(u), t, int(0.15 * t), mask.ctypes.data_as(C.POINTER(C.c_int32))) == 0
+    dt = time.perf_counter() - t0
+    return {"value": t / dt, "unit": UNIT, "cores": 1, "kind": "reference", "seconds": dt,
+            "sample": f"1 head x {t} rows: the reference's own allocate_budgets + token_scores ([k;v] 256->128->1 "
+                      f"SiLU, its native scorer: 4x the BASELINE scorer's flops) + hard_topk, compiled from "
+                      f"/root/reference/proj/src (-O2) over oracle/ref_shim's Eigen stand-in; not the headline "
+                      f"reference arm (the BASELINE K-only GELU scorer is not expressible through the reference API)"}
+
+
 def run_reference(args, rank, world):
     """The reference's CPU algorithm (oracle port of proj/src, fp64) on all host cores."""
     import numpy as np
@@ -466,6 +503,12 @@ def run_reference(args, rank, world):
                                    f"-march=native recipe; its Eigen GEMM is replaced by a row-blocked loop)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    try:
+        rc = reference_code_sample()
+    except Exception as e:  # the side measurement never blocks the reference arm's line
+        rc = {"unavailable": str(e)[:200]}
+    if rc is not None:
+        line["reference_code"] = rc
     print(json.dumps(line), flush=True)
 
 
