@@ -1350,6 +1350,8 @@ lkv_status lkv_model_decode_step(const lkv_model_desc* m, const void* weights, c
     dp.part_o = at<float>(ws, w.dec.part_o);
     dp.new_len = at<int32_t>(ws, w.dec.new_len);
     dp.err = err;
+    static const bool no_early = getenv("LKV_NO_EARLY_KV") != nullptr;  // A/B knob (profiles/knob_combine.sh)
+    dp.early_kv = g.dtype == LKV_BF16 && !no_early ? 1 : 0;  // the step's first launch (embed) is fully serialised
     CUtensorMap mk, mv;
     if (g.dtype == LKV_BF16) {
         if ((st = make_map_bf16(&mk, r->keys, 128, (uint64_t)r->capacity_rows, 64))) return st;

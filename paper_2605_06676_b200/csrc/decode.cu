@@ -228,7 +228,10 @@ __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
     const int G = p.G;
     const int D = 128;
     pdl_trigger();  // the combine's CTAs may become resident (they wait for this grid to finish)
-    pdl_wait();     // q / new k / new v come from the previous kernel
+    // q / new k / new v come from the previous kernel.  With early_kv the producer streams the
+    // cached rows (written by earlier steps) while that kernel is still running; only the
+    // consumers wait.
+    if (!p.early_kv) pdl_wait();
     const int it_lo = *p.item_lo, it_hi = *p.item_hi;
     const int ch = *p.ch;
     if (threadIdx.x == 0) {
@@ -275,6 +278,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
     }
 
     // ===================== consumers =====================
+    if (p.early_kv) pdl_wait();
     const int g = lane >> 2;       // fragment row (query head within the group)
     const int cq = (lane & 3) * 2;  // fragment column pair
     int st = 0;
@@ -727,6 +731,8 @@ cudaError_t launch_decode(const DecodeParams& p, int dtype, const CUtensorMap* m
         const int grid = min(p.max_items, per_sm * num_sms);
         e = launch_pdl(kern, dim3(grid), dim3(kDecThreads), smem, stream, p, *mk, *mv);
         if (e != cudaSuccess) return e;
+        static const bool no_comb = getenv("LKV_NO_COMBINE") != nullptr;  // timing knob (profiles/model_knobs.sh)
+        if (no_comb) return cudaGetLastError();
         const dim3 cgrid(p.n_seq * p.q_layers * p.n_kv_heads, (p.G * p.head_dim + kCombCols - 1) / kCombCols);
         // few heads (a per-layer launch): split each head's chunks over 4 thread slices
         if (cgrid.x * cgrid.y < (unsigned)num_sms)

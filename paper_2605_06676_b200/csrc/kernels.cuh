@@ -130,6 +130,11 @@ struct DecodeParams {
     float* part_o;
     int32_t* new_len;  // [n_heads] lens + 1 as the attention kernel read it (chunk 0 writes it)
     ErrWord* err;
+    // 1: the TMA producer streams this launch's K/V rows BEFORE griddepcontrol.wait (only the
+    // consumers wait, for q / new k / new v).  Valid only when no kernel that may still be running
+    // writes these heads' rows or lens: the model step's per-layer launches, whose step starts
+    // with a fully serialised launch (lkv_model_step).
+    int32_t early_kv;
 };
 // target_items > 0: the largest power-of-two ch giving at least that many items per layer;
 // target_items < 0: the smallest ch (multiple of 64) whose busiest layer fits -target_items items

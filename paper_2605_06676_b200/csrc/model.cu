@@ -564,13 +564,16 @@ cudaError_t launch_embed(const void* tok_embed, int dtype, const int32_t* tokens
                          void* act, int nbt, ErrWord* err, cudaStream_t stream) {
     const dim3 grid((dm + 63) / 64, B);
     cudaError_t e;
+    // a plain (fully serialised) launch: every kernel of the step starts after the previous
+    // step has completed, which the per-layer attention's early K/V prefetch relies on
     if (dtype == LKV_BF16)
-        e = launch_pdl(embed_kernel<__nv_bfloat16>, grid, dim3(64), 0, stream,
-                       static_cast<const __nv_bfloat16*>(tok_embed), tokens, B, dm, vocab, tokens_seen, max_seq, x,
-                       ss_part, gain, act, nbt, err);
+        embed_kernel<__nv_bfloat16><<<grid, 64, 0, stream>>>(static_cast<const __nv_bfloat16*>(tok_embed), tokens, B,
+                                                             dm, vocab, tokens_seen, max_seq, x, ss_part, gain, act,
+                                                             nbt, err);
     else
-        e = launch_pdl(embed_kernel<float>, grid, dim3(64), 0, stream, static_cast<const float*>(tok_embed), tokens,
-                       B, dm, vocab, tokens_seen, max_seq, x, ss_part, gain, act, nbt, err);
+        embed_kernel<float><<<grid, 64, 0, stream>>>(static_cast<const float*>(tok_embed), tokens, B, dm, vocab,
+                                                     tokens_seen, max_seq, x, ss_part, gain, act, nbt, err);
+    e = cudaGetLastError();
     note_launches(1);
     return e;
 }
