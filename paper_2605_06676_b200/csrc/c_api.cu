@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -141,7 +142,7 @@ int64_t n_heads_of(const lkv_cache_desc* c) { return (int64_t)c->n_seq * c->n_la
 
 // ---- workspace layout -----------------------------------------------------------------------------
 struct EvictWs {
-    size_t err, ratios, budgets, budgets_all, scores, hist, state, chunk_out, chunk_eqb, cands, total;
+    size_t err, k2_flag, ratios, budgets, budgets_all, scores, hist, state, chunk_out, chunk_eqb, cands, total;
 };
 
 EvictWs evict_layout(const lkv_cache_desc* c, int n_logits) {
@@ -152,6 +153,8 @@ EvictWs evict_layout(const lkv_cache_desc* c, int n_logits) {
     size_t o = 0;
     w.err = o;
     o = align_up(o + sizeof(ErrWord));
+    w.k2_flag = o;  // K2 -> plan completion epoch (lkv_evict)
+    o = align_up(o + sizeof(uint32_t));
     w.ratios = o;
     o = align_up(o + sizeof(double) * (size_t)(n_logits > 0 ? n_logits : 1));
     w.budgets = o;
@@ -261,7 +264,7 @@ lkv_status run_score(const lkv_cache_desc* c, const lkv_scorer_desc* s, float* s
 // buffer is offset by h0; the ragged rows are addressed through the (absolute) offsets.
 lkv_status run_select(const lkv_cache_desc* c, const float* scores, const int32_t* budgets,
                       const lkv_ragged_desc* out, void* ws, const EvictWs& w, bool gather, cudaStream_t stream,
-                      bool hist_ready = false, int64_t h0 = 0, int64_t chunk0 = 0) {
+                      bool hist_ready = false, int64_t h0 = 0, int64_t chunk0 = 0, uint32_t k2_epoch = 0) {
     for (int s = 0; s < c->n_seq; ++s)
         if (c->seq_lens[s] > 4096 * 1024) return fail(LKV_ERR_UNSUPPORTED, "top-k supports t <= 4M rows per head");
     SelectParams p;
@@ -285,6 +288,10 @@ lkv_status run_select(const lkv_cache_desc* c, const float* scores, const int32_
     p.gather = gather ? 1 : 0;
     p.hist_ready = hist_ready ? 1 : 0;
     p.err = at<ErrWord>(ws, w.err);
+    if (k2_epoch) {
+        p.k2_flag = at<uint32_t>(ws, w.k2_flag);
+        p.k2_epoch = k2_epoch;
+    }
     LKV_CUDA(launch_select(p, (int)n_heads_of(c), stream), "select");
     return LKV_OK;
 }
@@ -579,6 +586,17 @@ static lkv_status evict_impl(const lkv_cache_desc* c, const lkv_scorer_desc* s, 
             cudaEventDestroy(b);
         }
     } guard{fork, join};
+    // timing knobs (profiles/k2_join_ab.sh): K2 before K1 on one stream / the event join instead of the flag
+    static const bool serial_k2 = getenv("LKV_SERIAL_K2") != nullptr;
+    static const bool event_join = getenv("LKV_K2_EVENT_JOIN") != nullptr;
+    if (serial_k2) side = strm;
+    const bool use_flag = !serial_k2 && !event_join;
+    static std::atomic<uint32_t> g_epoch{0};
+    uint32_t epoch = 0;
+    if (use_flag) {
+        do epoch = ++g_epoch;
+        while (epoch == 0);
+    }
     LKV_CUDA(cudaEventRecord(fork, strm), "event record");
     LKV_CUDA(cudaStreamWaitEvent(side, fork, 0), "stream wait");
     if (shard)
@@ -589,13 +607,22 @@ static lkv_status evict_impl(const lkv_cache_desc* c, const lkv_scorer_desc* s, 
         st = lkv_budgets(logits, n, R, mode, c->seq_lens, c->n_seq, out->decode_slack, ratios, budgets, out->offsets,
                          ws, ws_bytes, (lkv_stream_t)side);
     if (st) return st;
+    // the plan kernel waits for this flag (no event join: K1 -> plan -> emit stay one PDL chain)
+    if (use_flag) LKV_CUDA(launch_flag(at<uint32_t>(ws, w.k2_flag), epoch, side), "K2 flag");
     LKV_CUDA(cudaEventRecord(join, side), "event record");
     bool hist_made = false;  // the tcgen05 scorer fuses top-k pass 1 (the histogram) into its epilogue
     if ((st = run_score(c, s, scores, strm, /*sms_reserved=*/1, at<uint32_t>(ws, w.hist), at<ErrWord>(ws, w.err),
                         &hist_made)))
         return st;
-    LKV_CUDA(cudaStreamWaitEvent(strm, join, 0), "stream wait");
-    return run_select(c, scores, budgets, out, ws, w, true, strm, hist_made);
+    // without the fused histogram, select_hist_kernel reads the budgets before the plan kernel's
+    // flag wait: join the side stream first on that path
+    if (!hist_made) epoch = 0;
+    if (event_join || !epoch) LKV_CUDA(cudaStreamWaitEvent(strm, join, 0), "stream wait");
+    st = run_select(c, scores, budgets, out, ws, w, true, strm, hist_made, 0, 0, epoch);
+    // the caller's later work on `strm` must still see K2 complete (ratios / budgets / offsets
+    // outputs): join the side stream after the emit -- off the K1 -> plan -> emit path
+    if (epoch && !st) LKV_CUDA(cudaStreamWaitEvent(strm, join, 0), "stream wait");
+    return st;
 }
 
 lkv_status lkv_evict(const lkv_cache_desc* c, const lkv_scorer_desc* s, const double* logits, double R, int32_t mode,

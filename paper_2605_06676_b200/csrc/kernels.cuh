@@ -74,8 +74,14 @@ struct SelectParams {
     int32_t gather;
     int32_t hist_ready;  // the scorer already produced `hist` (fused pass 1)
     ErrWord* err;
+    // non-null: budgets / offsets come from K2 on a side stream with no event join; the plan
+    // kernel waits (bounded) until *k2_flag == k2_epoch, which launch_flag stores after K2
+    const uint32_t* k2_flag;
+    uint32_t k2_epoch;
     int32_t chunk_base[LKV_MAX_SEQ + 1];
 };
+// one-thread kernel: *flag = epoch (release, gpu scope) once every earlier op of the stream is done
+cudaError_t launch_flag(uint32_t* flag, uint32_t epoch, cudaStream_t stream);
 struct CompactParams {
     SeqTable seq;
     const int64_t* offsets;

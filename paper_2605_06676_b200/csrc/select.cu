@@ -154,6 +154,28 @@ __global__ void __launch_bounds__(kPlanThreads, 2) select_plan_kernel(const __gr
     uint32_t* s_ckey = plan_dyn + kCandCap;
     __shared__ uint32_t s_scan[33];
     __shared__ uint32_t s_bin, s_above, s_ncand;
+    if (p.k2_flag) {  // K2 ran on a side stream: wait for its flag instead of an event join
+        __shared__ int s_k2_late;
+        if (threadIdx.x == 0) {
+            uint64_t t0, t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+            uint32_t v;
+            s_k2_late = 0;
+            for (;;) {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.k2_flag) : "memory");
+                if (v == p.k2_epoch) break;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+                if (t1 - t0 > 2000000000ull) {  // 2 s: never in practice (K2 takes ~0.1 ms); no hang
+                    latch_error(p.err, LKV_ERR_CUDA, -1);
+                    s_k2_late = 1;
+                    break;
+                }
+                __nanosleep(200);
+            }
+        }
+        __syncthreads();
+        if (s_k2_late) return;
+    }
     const int head = blockIdx.x;
     const int s_idx = head_seq(p.seq, head);
     const int t = p.seq.len[s_idx];
@@ -539,6 +561,16 @@ cudaError_t launch_select(SelectParams p, int n_heads, cudaStream_t stream) {
     if ((e = launch_pdl(select_plan_kernel, dim3(n_heads), dim3(kPlanThreads), kPlanSmem, stream, p)) != cudaSuccess) return e;
     if ((e = launch_pdl(select_emit_kernel, dim3(chunks), dim3(kSelThreads), 0, stream, p)) != cudaSuccess) return e;
     note_launches(2);
+    return cudaGetLastError();
+}
+
+__global__ void flag_kernel(uint32_t* flag, uint32_t epoch) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(epoch) : "memory");
+}
+
+cudaError_t launch_flag(uint32_t* flag, uint32_t epoch, cudaStream_t stream) {
+    flag_kernel<<<1, 1, 0, stream>>>(flag, epoch);
+    note_launches(1);
     return cudaGetLastError();
 }
 
