@@ -590,7 +590,10 @@ static lkv_status evict_impl(const lkv_cache_desc* c, const lkv_scorer_desc* s, 
     static const bool serial_k2 = getenv("LKV_SERIAL_K2") != nullptr;
     static const bool event_join = getenv("LKV_K2_EVENT_JOIN") != nullptr;
     if (serial_k2) side = strm;
-    const bool use_flag = !serial_k2 && !event_join;
+    // a captured graph would bake one epoch into every replay: captures keep the event join
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    LKV_CUDA(cudaStreamIsCapturing(strm, &cap), "capture status");
+    const bool use_flag = !serial_k2 && !event_join && cap == cudaStreamCaptureStatusNone;
     static std::atomic<uint32_t> g_epoch{0};
     uint32_t epoch = 0;
     if (use_flag) {

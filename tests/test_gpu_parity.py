@@ -687,3 +687,57 @@ def test_layerwise_prefill_equals_one_shot_eviction():
     dense_layer = 2 * S * H * T * D * 2
     compressed_before_last = int(ref.budgets.reshape(S, L, H)[:, :L - 1].sum()) * 2 * D * 2
     assert pf.peak_kv_bytes == dense_layer + compressed_before_last
+
+
+@pytest.mark.gpu
+def test_evict_graph_replay_matches_eager():
+    """lkv_evict captured in a CUDA graph (the K2 -> plan hand-off then uses the event join, not the
+    per-call epoch flag) and replayed gives the eager result, also after the logits change between
+    replays (budgets re-solved inside the graph)."""
+    cfg = synth.CONFIGS[2]
+    cache = synth.make_cache(cfg, n_layers=2, max_tokens=8192)
+    scorers = synth.make_scorers(cfg, n_layers=2)
+    ev = lkv.Evictor(cache, scorers, synth.make_logits(cfg, n_layers=2), cfg.ratio, lkv.BUDGET_EXACT,
+                     decode_slack=1)
+
+    def snapshot():
+        r = ev.ragged
+        return (ev.budgets.clone(), r.offsets.clone(), r.lens.clone(), r.positions.clone(), r.keys.clone(),
+                r.values.clone())
+
+    ev.launch()
+    torch.cuda.synchronize()
+    ev.ws.status()
+    eager = snapshot()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        ev.launch(s)  # warm-up on the capture stream
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            ev.launch(s)
+    for _ in range(2):
+        ev.ragged.positions.zero_()
+        ev.ragged.keys.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        ev.ws.status()
+        for a, b in zip(eager, snapshot()):
+            assert torch.equal(a, b)
+    ev.logits.copy_(ev.logits.flip(0))  # new LKV-H logits: the replay re-solves the budgets
+    g.replay()
+    torch.cuda.synchronize()
+    ev.ws.status()
+    replayed = snapshot()
+    ev.launch()
+    torch.cuda.synchronize()
+    ev.ws.status()
+    eager2 = snapshot()
+    assert not torch.equal(eager2[0], eager[0])
+    for a, b in zip(eager2[:3], replayed[:3]):
+        assert torch.equal(a, b)
+    for h in range(cache.n_heads):
+        o, n = int(eager2[1][h]), int(eager2[2][h])
+        for a, b in zip(eager2[3:], replayed[3:]):
+            assert torch.equal(a[o:o + n], b[o:o + n])
