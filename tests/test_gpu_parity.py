@@ -717,14 +717,21 @@ def test_evict_graph_replay_matches_eager():
         torch.cuda.synchronize()
         with torch.cuda.graph(g, stream=s):
             ev.launch(s)
+    def same(x, y):  # budgets / offsets / lens in full, rows and positions over each head's kept range
+        for a, b in zip(x[:3], y[:3]):
+            assert torch.equal(a, b)
+        for h in range(cache.n_heads):
+            o, n = int(x[1][h]), int(x[2][h])
+            for a, b in zip(x[3:], y[3:]):
+                assert torch.equal(a[o:o + n], b[o:o + n])
+
     for _ in range(2):
         ev.ragged.positions.zero_()
         ev.ragged.keys.zero_()
         g.replay()
         torch.cuda.synchronize()
         ev.ws.status()
-        for a, b in zip(eager, snapshot()):
-            assert torch.equal(a, b)
+        same(eager, snapshot())
     ev.logits.copy_(ev.logits.flip(0))  # new LKV-H logits: the replay re-solves the budgets
     g.replay()
     torch.cuda.synchronize()
@@ -735,9 +742,4 @@ def test_evict_graph_replay_matches_eager():
     ev.ws.status()
     eager2 = snapshot()
     assert not torch.equal(eager2[0], eager[0])
-    for a, b in zip(eager2[:3], replayed[:3]):
-        assert torch.equal(a, b)
-    for h in range(cache.n_heads):
-        o, n = int(eager2[1][h]), int(eager2[2][h])
-        for a, b in zip(eager2[3:], replayed[3:]):
-            assert torch.equal(a[o:o + n], b[o:o + n])
+    same(eager2, replayed)
