@@ -12,8 +12,8 @@
  *   lkv_score       <- token_scores       policy.hpp:73  (policy.cpp:131-136)
  *   lkv_select      <- inference_select   policy.hpp:81  (policy.cpp:152-154)
  *                      -> hard_topk       soft_topk.hpp:71 (soft_topk.cpp:191-201)
- *   lkv_compact     <- cache_from_trace   model.hpp:99   (model.cpp:289-315) and the
- *                      compaction loop of prefill_with_eviction (evictsim.cpp:202-215)
+ *   lkv_compact     <- the compaction loop of prefill_with_eviction (evictsim.cpp:202-215)
+ *   lkv_cache_from_trace <- cache_from_trace model.hpp:99 (model.cpp:289-315): mask scan + gather
  *   lkv_evict       <- prefill_with_eviction's score->select->compact loop
  *                      (evictsim.hpp:74, evictsim.cpp:161-215), K/V-given form
  *   lkv_evict_host  <- the same, for a cache resident in (pinned) host memory
@@ -57,18 +57,18 @@
 extern "C" {
 #endif
 
-#define LKV_ABI_VERSION 1
+#define LKV_ABI_VERSION 2
 #define LKV_MAX_SEQ 256
 
 typedef struct CUstream_st* lkv_stream_t; /* identical to cudaStream_t */
 
 typedef enum lkv_status {
     LKV_OK = 0,
-    LKV_ERR_CONTRACT = 1,        /* lkv::contract_error        errors.hpp:20-22 */
-    LKV_ERR_NUMERIC = 2,         /* lkv::numeric_error         errors.hpp:25-27 */
-    LKV_ERR_BUDGET = 3,          /* lkv::budget_error          errors.hpp:30-32 */
-    LKV_ERR_OVERFLOW_GUARD = 4,  /* lkv::overflow_guard_error  errors.hpp:35-37 */
-    LKV_ERR_DEGENERATE_MASK = 5, /* lkv::degenerate_mask_error errors.hpp:40-42 */
+    LKV_ERR_CONTRACT = 1,        /* lkv::contract_error        errors.hpp:10-12 */
+    LKV_ERR_NUMERIC = 2,         /* lkv::numeric_error         errors.hpp:15-17 */
+    LKV_ERR_BUDGET = 3,          /* lkv::budget_error          errors.hpp:20-22 */
+    LKV_ERR_OVERFLOW_GUARD = 4,  /* lkv::overflow_guard_error  errors.hpp:25-27 */
+    LKV_ERR_DEGENERATE_MASK = 5, /* lkv::degenerate_mask_error errors.hpp:30-32 */
     LKV_ERR_CUDA = 6,            /* CUDA runtime / launch failure (no reference analogue) */
     LKV_ERR_UNSUPPORTED = 7,     /* device is not sm_100 or shape outside the kernel envelope */
     LKV_ERR_NCCL = 8             /* NCCL missing or a collective failed (multi-GPU plumbing only) */
@@ -190,8 +190,24 @@ lkv_status lkv_select(const lkv_cache_desc* cache, const float* scores, const in
 
 /* ---- K4: compaction ---------------------------------------------------------- */
 /* Gathers rows positions[offsets[i] + r], r < lens[i], of head i from the dense
- * cache into out->keys/values[offsets[i] + r] (16-byte vectorised). */
-lkv_status lkv_compact(const lkv_cache_desc* cache, const lkv_ragged_desc* out, lkv_stream_t stream);
+ * cache into out->keys/values[offsets[i] + r] (16-byte vectorised).  A position outside
+ * [0, t_s) or lens overrunning a head's capacity is a contract_error (model.cpp:298-312),
+ * latched in `workspace` (>= 256 bytes, lkv_workspace_status); those rows are not written. */
+lkv_status lkv_compact(const lkv_cache_desc* cache, const lkv_ragged_desc* out, void* workspace,
+                       size_t workspace_bytes, lkv_stream_t stream);
+
+/* cache_from_trace (model.hpp:99, model.cpp:289-315) on the device: keep row j < t_s of flat
+ * head i iff masks[i * mask_ld + j] != 0, ascending (the reference's `if (!m[j]) continue`).
+ * lkv_mask_counts writes the kept rows per head (to size the ragged cache);
+ * lkv_cache_from_trace writes out->lens, out->offsets (exclusive scan of count +
+ * decode_slack), the positions and the gathered K/V rows.  A ragged cache too small for the
+ * counts is a contract_error (latched; nothing is written for that head).  Workspace as
+ * lkv_workspace_bytes(cache, 1); mask_ld >= max t_s. */
+lkv_status lkv_mask_counts(const lkv_cache_desc* cache, const int32_t* masks, int64_t mask_ld, int32_t* counts,
+                           void* workspace, size_t workspace_bytes, lkv_stream_t stream);
+lkv_status lkv_cache_from_trace(const lkv_cache_desc* cache, const int32_t* masks, int64_t mask_ld,
+                                const lkv_ragged_desc* out, void* workspace, size_t workspace_bytes,
+                                lkv_stream_t stream);
 
 /* ---- fused: budgets -> score -> select -> compact ----------------------------- */
 /* scores_out, ratios_out, budgets_out may be NULL (workspace-backed). */
@@ -243,6 +259,12 @@ lkv_status lkv_evict_shard(const lkv_cache_desc* local_cache, const lkv_scorer_d
                            int32_t n_logits, int32_t head_begin, double target_ratio, int32_t mode,
                            const lkv_ragged_desc* out, float* scores_out, double* ratios_out, int32_t* budgets_out,
                            void* workspace, size_t workspace_bytes, lkv_stream_t stream);
+/* lkv_evict_host on a head shard (host_cache holds this rank's layers only; pinned + mapped). */
+lkv_status lkv_evict_host_shard(const lkv_cache_desc* host_cache, void* dev_keys, void* dev_values,
+                                const lkv_scorer_desc* scorer, const double* logits, int32_t n_logits,
+                                int32_t head_begin, double target_ratio, int32_t mode, const lkv_ragged_desc* out,
+                                const lkv_ragged_desc* host_out, int32_t layers_per_chunk, void* workspace,
+                                size_t workspace_bytes, lkv_stream_t stream);
 /* Upper bound on a shard's compacted rows (caller allocates; -1 on bad input). */
 int64_t lkv_ragged_capacity_shard(const lkv_cache_desc* local_cache, int32_t n_logits, double target_ratio,
                                   int32_t decode_slack);
@@ -319,7 +341,7 @@ lkv_status lkv_rope_pack(const void* k_lin, const void* v_lin, const lkv_cache_d
                          void* k_out, void* v_out, lkv_stream_t stream);
 
 /* ---- K5: decode over the ragged cache ------------------------------------------- */
-/* lkv_decode_plan splits every head's capacity into 256-row work items (once
+/* lkv_decode_plan splits every head's capacity into work items of 128..1024 rows (once
  * per eviction, after offsets are final).  lkv_decode_step then runs one decode
  * step for every (seq, layer): append new_k/new_v (post-RoPE) and position
  * tokens_seen[s] to each KV head (lens += 1, capacity checked), and for each
@@ -332,6 +354,14 @@ lkv_status lkv_rope_pack(const void* k_lin, const void* v_lin, const lkv_cache_d
 size_t lkv_decode_workspace_bytes(const lkv_ragged_desc* cache, int32_t group_size);
 lkv_status lkv_decode_plan(const lkv_ragged_desc* cache, void* workspace, size_t workspace_bytes,
                            lkv_stream_t stream);
+/* The same with the work-item size fixed (rows_per_item: 0 = automatic, else a multiple of 64
+ * in [128, 1024]; it may still be raised so a head's chunks fit the combine's table). */
+lkv_status lkv_decode_plan_ex(const lkv_ragged_desc* cache, int32_t rows_per_item, void* workspace,
+                              size_t workspace_bytes, lkv_stream_t stream);
+/* The plan's work-item count and size, read back from the workspace of lkv_decode_plan(_ex) or
+ * lkv_model_plan(_ex) (synchronises `stream`). */
+lkv_status lkv_decode_plan_info(const lkv_ragged_desc* cache, const void* workspace, int32_t* n_items,
+                                int32_t* rows_per_item, lkv_stream_t stream);
 lkv_status lkv_decode_step(const lkv_ragged_desc* cache, int32_t n_seq, int32_t n_layers,
                            int32_t n_kv_heads, int32_t n_q_heads, const void* q, const void* new_k,
                            const void* new_v, int32_t* tokens_seen, void* out, double scale,
@@ -379,6 +409,9 @@ lkv_status lkv_model_load_param(const lkv_model_desc* model, void* weights, int3
 size_t lkv_model_workspace_bytes(const lkv_model_desc* model, int32_t n_seq, const lkv_ragged_desc* cache);
 lkv_status lkv_model_plan(const lkv_model_desc* model, const lkv_ragged_desc* cache, int32_t n_seq, void* workspace,
                           size_t workspace_bytes, lkv_stream_t stream);
+/* lkv_model_plan with the per-layer attention work-item size fixed (as lkv_decode_plan_ex) */
+lkv_status lkv_model_plan_ex(const lkv_model_desc* model, const lkv_ragged_desc* cache, int32_t n_seq,
+                             int32_t rows_per_item, void* workspace, size_t workspace_bytes, lkv_stream_t stream);
 lkv_status lkv_model_decode_step(const lkv_model_desc* model, const void* weights, const lkv_ragged_desc* cache,
                                  int32_t n_seq, const int32_t* tokens, int32_t* tokens_seen, float* logits,
                                  void* workspace, size_t workspace_bytes, lkv_stream_t stream);

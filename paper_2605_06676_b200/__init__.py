@@ -339,32 +339,36 @@ def inference_select(scores: torch.Tensor, b: int) -> torch.Tensor:
 hard_topk = inference_select
 
 
-def compact(cache: DenseCache, ragged: RaggedCache) -> RaggedCache:
+def compact(cache: DenseCache, ragged: RaggedCache, ws: Workspace | None = None) -> RaggedCache:
+    """Gather rows positions[offsets[i] + r], r < lens[i], of every head (evictsim.cpp:202-215);
+    a position outside [0, t) raises ContractError (nothing is written for that head)."""
     cd, rd = cache.desc(), ragged.desc()
-    _check(lib().lkv_compact(C.byref(cd), C.byref(rd), _stream()))
-    torch.cuda.current_stream().synchronize()
+    ws = ws or Workspace(256, device=cache.keys.device)
+    _check(lib().lkv_compact(C.byref(cd), C.byref(rd), C.c_void_p(ws.ptr), ws.nbytes, _stream()))
+    ws.status()
     return ragged
 
 
 def cache_from_trace(cache: DenseCache, hard_masks: torch.Tensor, decode_slack: int = 0) -> RaggedCache:
-    """model.hpp:99 -- keep the rows of each head whose binary mask is set (ascending)."""
+    """model.hpp:99 -- keep the rows of each head whose binary mask is set (ascending).  The mask
+    scan, ragged offsets and row gather run on the device (lkv_mask_counts, lkv_cache_from_trace);
+    the host reads one number, the total, to allocate the ragged cache."""
     n_seq, L, H, T, D = cache.shape
     m = hard_masks.reshape(cache.n_heads, -1)
     if m.shape[1] != T and m.shape[1] != max(cache.seq_lens):
         raise ContractError("cache_from_trace: mask length mismatch")
-    counts = (m != 0).sum(dim=1).to(torch.int32)
+    m = m.to(torch.int32).contiguous()
+    ws = _workspace_for(cache, 1)
+    cd = cache.desc()
+    counts = torch.empty(cache.n_heads, dtype=torch.int32, device=cache.keys.device)
+    _check(lib().lkv_mask_counts(C.byref(cd), _ptr(m), m.shape[1], _ptr(counts), C.c_void_p(ws.ptr), ws.nbytes,
+                                 _stream()))
     cap = int(counts.sum().item()) + cache.n_heads * decode_slack
     rc = _ragged_for(cache, cap, decode_slack)
-    _check(lib().lkv_ragged_offsets(_ptr(counts), cache.n_heads, decode_slack, _ptr(rc.offsets), _stream()))
-    rc.lens.copy_(counts)
-    offs = rc.offsets[:-1].to(torch.int64)
-    idx = torch.nonzero(m != 0)  # row-major: head, position ascending
-    if idx.numel():
-        head = idx[:, 0]
-        rank = torch.arange(idx.shape[0], device=m.device) - torch.repeat_interleave(
-            torch.cumsum(counts, 0).to(torch.int64) - counts.to(torch.int64), counts.to(torch.int64))
-        rc.positions[offs[head] + rank] = idx[:, 1].to(torch.int32)
-    compact(cache, rc)
+    rd = rc.desc()
+    _check(lib().lkv_cache_from_trace(C.byref(cd), _ptr(m), m.shape[1], C.byref(rd), C.c_void_p(ws.ptr), ws.nbytes,
+                                      _stream()))
+    ws.status()
     rc.tokens_seen.copy_(torch.tensor(cache.seq_lens, dtype=torch.int32))
     return rc
 
@@ -463,12 +467,26 @@ def prefill_with_eviction(cache: DenseCache, scorers: Scorers, logits: torch.Ten
 
 
 # ---- K5: decode ------------------------------------------------------------------------------------------
-def decode_plan(ragged: RaggedCache, group_size: int) -> None:
+def decode_plan(ragged: RaggedCache, group_size: int, rows_per_item: int = 0) -> None:
+    """Split every head into attention work items (rows_per_item 0: the plan's choice for one
+    all-layer launch; else a multiple of 64 in [128, 1024])."""
     rd = ragged.desc()
     nbytes = lib().lkv_decode_workspace_bytes(C.byref(rd), group_size)
     ragged._decode_ws = Workspace(nbytes, device=ragged.device)
     ragged._decode_G = group_size
-    _check(lib().lkv_decode_plan(C.byref(rd), C.c_void_p(ragged._decode_ws.ptr), ragged._decode_ws.nbytes, _stream()))
+    _check(lib().lkv_decode_plan_ex(C.byref(rd), int(rows_per_item), C.c_void_p(ragged._decode_ws.ptr),
+                                    ragged._decode_ws.nbytes, _stream()))
+
+
+def decode_plan_info(ragged: RaggedCache, ws: Workspace | None = None) -> tuple[int, int]:
+    """(work items, rows per item) of the current decode plan (or of a model plan's workspace)."""
+    ws = ws or ragged._decode_ws
+    if ws is None:
+        raise ContractError("no decode plan")
+    n, ch = C.c_int32(0), C.c_int32(0)
+    rd = ragged.desc()
+    _check(lib().lkv_decode_plan_info(C.byref(rd), C.c_void_p(ws.ptr), C.byref(n), C.byref(ch), _stream()))
+    return int(n.value), int(ch.value)
 
 
 def decode_step(ragged: RaggedCache, q: torch.Tensor, new_k: torch.Tensor, new_v: torch.Tensor,

@@ -11,8 +11,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# LKV_B200_LIB overrides the path (developer A/B builds of the same library only)
-LIB_PATH = os.environ.get("LKV_B200_LIB") or os.path.join(_HERE, "liblkv_b200.so")
+LIB_PATH = os.path.join(_HERE, "liblkv_b200.so")
 
 LKV_OK, CONTRACT, NUMERIC, BUDGET, OVERFLOW_GUARD, DEGENERATE_MASK, CUDA, UNSUPPORTED, NCCL = range(9)
 COMM_ID_BYTES = 128
@@ -30,7 +29,8 @@ EXPORTED = [
     "lkv_model_decode_step", "lkv_budgets_shard", "lkv_evict_shard", "lkv_ragged_capacity_shard", "lkv_comm_get_unique_id",
     "lkv_comm_init", "lkv_comm_destroy", "lkv_comm_size", "lkv_comm_rank", "lkv_comm_allgatherv", "lkv_comm_gatherv",
     "lkv_attn_workspace_bytes", "lkv_masked_attention_fwd", "lkv_masked_attention_bwd", "lkv_soft_topk_fwd",
-    "lkv_soft_topk_vjp", "lkv_evict_budgets",
+    "lkv_soft_topk_vjp", "lkv_evict_budgets", "lkv_mask_counts", "lkv_cache_from_trace", "lkv_decode_plan_ex",
+    "lkv_model_plan_ex", "lkv_decode_plan_info", "lkv_evict_host_shard",
 ]
 
 
@@ -99,15 +99,22 @@ def load():
     L.lkv_ragged_offsets.argtypes = [vp, i32, i32, vp, vp]
     L.lkv_score.argtypes = [P(CacheDesc), P(ScorerDesc), vp, vp, sz, vp]
     L.lkv_select.argtypes = [P(CacheDesc), vp, vp, P(RaggedDesc), i32, vp, sz, vp]
-    L.lkv_compact.argtypes = [P(CacheDesc), P(RaggedDesc), vp]
+    L.lkv_compact.argtypes = [P(CacheDesc), P(RaggedDesc), vp, sz, vp]
+    L.lkv_mask_counts.argtypes = [P(CacheDesc), vp, i64, vp, vp, sz, vp]
+    L.lkv_cache_from_trace.argtypes = [P(CacheDesc), vp, i64, P(RaggedDesc), vp, sz, vp]
     L.lkv_evict.argtypes = [P(CacheDesc), P(ScorerDesc), vp, dbl, i32, P(RaggedDesc), vp, vp, vp, vp, sz, vp]
     L.lkv_evict_host.argtypes = [P(CacheDesc), vp, vp, P(ScorerDesc), vp, dbl, i32, P(RaggedDesc), P(RaggedDesc), i32,
                                  vp, sz, vp]
+    L.lkv_evict_host_shard.argtypes = [P(CacheDesc), vp, vp, P(ScorerDesc), vp, i32, i32, dbl, i32, P(RaggedDesc),
+                                       P(RaggedDesc), i32, vp, sz, vp]
+    L.lkv_evict_host_shard.restype = C.c_int
     L.lkv_rope_table.argtypes = [i32, i32, dbl, i32, vp, vp]
     L.lkv_rope_pack.argtypes = [vp, vp, P(CacheDesc), vp, vp, vp, vp]
     L.lkv_decode_workspace_bytes.restype = sz
     L.lkv_decode_workspace_bytes.argtypes = [P(RaggedDesc), i32]
     L.lkv_decode_plan.argtypes = [P(RaggedDesc), vp, sz, vp]
+    L.lkv_decode_plan_ex.argtypes = [P(RaggedDesc), i32, vp, sz, vp]
+    L.lkv_decode_plan_info.argtypes = [P(RaggedDesc), vp, P(i32), P(i32), vp]
     L.lkv_decode_step.argtypes = [P(RaggedDesc), i32, i32, i32, i32, vp, vp, vp, vp, vp, dbl, vp, sz, vp]
     L.lkv_model_validate.argtypes = [P(ModelDesc)]
     L.lkv_model_weights_bytes.restype = sz
@@ -116,6 +123,7 @@ def load():
     L.lkv_model_workspace_bytes.restype = sz
     L.lkv_model_workspace_bytes.argtypes = [P(ModelDesc), i32, P(RaggedDesc)]
     L.lkv_model_plan.argtypes = [P(ModelDesc), P(RaggedDesc), i32, vp, sz, vp]
+    L.lkv_model_plan_ex.argtypes = [P(ModelDesc), P(RaggedDesc), i32, i32, vp, sz, vp]
     L.lkv_model_decode_step.argtypes = [P(ModelDesc), vp, P(RaggedDesc), i32, vp, vp, vp, vp, sz, vp]
     L.lkv_budgets_shard.argtypes = [vp, i32, dbl, i32, P(i32), i32, i32, i32, i32, vp, vp, vp, vp, vp, sz, vp]
     L.lkv_evict_shard.argtypes = [P(CacheDesc), P(ScorerDesc), vp, i32, i32, dbl, i32, P(RaggedDesc), vp, vp, vp, vp,
@@ -148,7 +156,9 @@ def load():
         getattr(L, name).restype = C.c_int
     for name in ["lkv_workspace_init", "lkv_workspace_status", "lkv_budgets", "lkv_freeze_budgets", "lkv_ragged_offsets", "lkv_score",
                  "lkv_select", "lkv_compact", "lkv_evict", "lkv_evict_host", "lkv_rope_table", "lkv_rope_pack", "lkv_decode_plan", "lkv_decode_step",
-                 "lkv_model_validate", "lkv_model_load_param", "lkv_model_plan", "lkv_model_decode_step"]:
+                 "lkv_model_validate", "lkv_model_load_param", "lkv_model_plan", "lkv_model_decode_step",
+                 "lkv_mask_counts", "lkv_cache_from_trace", "lkv_decode_plan_ex", "lkv_model_plan_ex",
+                 "lkv_decode_plan_info"]:
         getattr(L, name).restype = C.c_int
     _lib = L
     return L

@@ -144,6 +144,9 @@ __device__ void freeze_and_offsets(const BudgetParams& p, const double* r, doubl
 }
 
 __global__ void __launch_bounds__(kBudgetThreads, 1) budgets_kernel(const BudgetParams p) {
+    // lkv_evict launches K1 as this kernel's programmatic dependent: let it start now, on the
+    // other SMs (K1 waits for this grid before it completes; the select kernels wait for K1)
+    pdl_trigger();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int n = p.n;
     double* x = reinterpret_cast<double*>(smem_raw);  // [n]

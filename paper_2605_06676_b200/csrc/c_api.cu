@@ -142,7 +142,7 @@ int64_t n_heads_of(const lkv_cache_desc* c) { return (int64_t)c->n_seq * c->n_la
 
 // ---- workspace layout -----------------------------------------------------------------------------
 struct EvictWs {
-    size_t err, k2_flag, ratios, budgets, budgets_all, scores, hist, state, chunk_out, chunk_eqb, cands, total;
+    size_t err, ratios, budgets, budgets_all, scores, hist, state, chunk_out, chunk_eqb, cands, total;
 };
 
 EvictWs evict_layout(const lkv_cache_desc* c, int n_logits) {
@@ -153,8 +153,6 @@ EvictWs evict_layout(const lkv_cache_desc* c, int n_logits) {
     size_t o = 0;
     w.err = o;
     o = align_up(o + sizeof(ErrWord));
-    w.k2_flag = o;  // K2 -> plan completion epoch (lkv_evict)
-    o = align_up(o + sizeof(uint32_t));
     w.ratios = o;
     o = align_up(o + sizeof(double) * (size_t)(n_logits > 0 ? n_logits : 1));
     w.budgets = o;
@@ -216,7 +214,7 @@ lkv_status check_ragged(const lkv_ragged_desc* r, int64_t n_heads, int head_dim,
 // ---- internal launchers shared by lkv_score / lkv_evict ---------------------------------------------
 lkv_status run_score(const lkv_cache_desc* c, const lkv_scorer_desc* s, float* scores, cudaStream_t stream,
                      int sms_reserved = 0, uint32_t* hist = nullptr, ErrWord* err = nullptr,
-                     bool* hist_made = nullptr, bool clear_hist = true) {
+                     bool* hist_made = nullptr, bool clear_hist = true, bool pdl = false) {
     if (hist_made) *hist_made = false;
     ScoreParams p;
     memset(&p, 0, sizeof p);
@@ -232,6 +230,7 @@ lkv_status run_score(const lkv_cache_desc* c, const lkv_scorer_desc* s, float* s
     p.b1 = s->b1;
     p.w2 = s->w2;
     p.scores = scores;
+    p.pdl = pdl ? 1 : 0;
     if (score_tc_supported(c->dtype, c->head_dim, s->hidden, s->input)) {
         CUtensorMap mk, mv, mw;
         const uint64_t rows = (uint64_t)n_heads_of(c) * c->max_tokens;
@@ -264,7 +263,7 @@ lkv_status run_score(const lkv_cache_desc* c, const lkv_scorer_desc* s, float* s
 // buffer is offset by h0; the ragged rows are addressed through the (absolute) offsets.
 lkv_status run_select(const lkv_cache_desc* c, const float* scores, const int32_t* budgets,
                       const lkv_ragged_desc* out, void* ws, const EvictWs& w, bool gather, cudaStream_t stream,
-                      bool hist_ready = false, int64_t h0 = 0, int64_t chunk0 = 0, uint32_t k2_epoch = 0) {
+                      bool hist_ready = false, int64_t h0 = 0, int64_t chunk0 = 0) {
     for (int s = 0; s < c->n_seq; ++s)
         if (c->seq_lens[s] > 4096 * 1024) return fail(LKV_ERR_UNSUPPORTED, "top-k supports t <= 4M rows per head");
     SelectParams p;
@@ -288,10 +287,6 @@ lkv_status run_select(const lkv_cache_desc* c, const float* scores, const int32_
     p.gather = gather ? 1 : 0;
     p.hist_ready = hist_ready ? 1 : 0;
     p.err = at<ErrWord>(ws, w.err);
-    if (k2_epoch) {
-        p.k2_flag = at<uint32_t>(ws, w.k2_flag);
-        p.k2_epoch = k2_epoch;
-    }
     LKV_CUDA(launch_select(p, (int)n_heads_of(c), stream), "select");
     return LKV_OK;
 }
@@ -535,10 +530,12 @@ lkv_status lkv_select(const lkv_cache_desc* c, const float* scores, const int32_
     return run_select(c, scores, budgets, out, ws, w, gather != 0, (cudaStream_t)stream);
 }
 
-lkv_status lkv_compact(const lkv_cache_desc* c, const lkv_ragged_desc* out, lkv_stream_t stream) {
+lkv_status lkv_compact(const lkv_cache_desc* c, const lkv_ragged_desc* out, void* ws, size_t ws_bytes,
+                       lkv_stream_t stream) {
     lkv_status st = check_cache(c, true);
     if (st) return st;
     if ((st = check_ragged(out, n_heads_of(c), c->head_dim, c->dtype, true))) return st;
+    if ((st = check_ws(ws, ws_bytes, sizeof(ErrWord)))) return st;
     CompactParams p;
     memset(&p, 0, sizeof p);
     p.seq = make_seq(c);
@@ -550,15 +547,72 @@ lkv_status lkv_compact(const lkv_cache_desc* c, const lkv_ragged_desc* out, lkv_
     p.out_keys = out->keys;
     p.out_values = out->values;
     p.row_bytes = c->head_dim * (c->dtype == LKV_F32 ? 4 : 2);
-    p.err = nullptr;
-    // compaction has no workspace: contract violations trap into a static latch
-    static ErrWord* s_latch = nullptr;
-    if (!s_latch) LKV_CUDA(cudaMalloc(&s_latch, sizeof(ErrWord)), "latch alloc");
-    p.err = s_latch;
+    p.err = at<ErrWord>(ws, 0);  // out-of-range positions / overrun heads -> contract_error
     LKV_CUDA(launch_compact(p, (int)n_heads_of(c), (cudaStream_t)stream), "compact");
     return LKV_OK;
 }
 
+static lkv_status trace_params(const lkv_cache_desc* c, const int32_t* masks, int64_t mask_ld, void* ws,
+                               size_t ws_bytes, TraceParams* p) {
+    lkv_status st = check_cache(c, false);
+    if (st) return st;
+    if (!masks) return fail(LKV_ERR_CONTRACT, "cache_from_trace: masks are null");
+    int64_t tmax = 0;
+    for (int s = 0; s < c->n_seq; ++s) tmax = std::max<int64_t>(tmax, c->seq_lens[s]);
+    if (mask_ld < tmax) return fail(LKV_ERR_CONTRACT, "cache_from_trace: mask length mismatch");  // model.cpp:300
+    for (int s = 0; s < c->n_seq; ++s)
+        if (c->seq_lens[s] > 4096 * 1024) return fail(LKV_ERR_UNSUPPORTED, "cache_from_trace supports t <= 4M rows");
+    const EvictWs w = evict_layout(c, 1);
+    if ((st = check_ws(ws, ws_bytes, w.total))) return st;
+    memset(p, 0, sizeof *p);
+    p->seq = make_seq(c);
+    p->masks = masks;
+    p->mask_ld = mask_ld;
+    p->chunk_cnt = at<uint32_t>(ws, w.chunk_out);
+    p->err = at<ErrWord>(ws, w.err);
+    p->row_bytes = c->head_dim * (c->dtype == LKV_F32 ? 4 : 2);
+    return LKV_OK;
+}
+
+lkv_status lkv_mask_counts(const lkv_cache_desc* c, const int32_t* masks, int64_t mask_ld, int32_t* counts, void* ws,
+                           size_t ws_bytes, lkv_stream_t stream) {
+    TraceParams p;
+    lkv_status st = trace_params(c, masks, mask_ld, ws, ws_bytes, &p);
+    if (st) return st;
+    if (!counts) return fail(LKV_ERR_CONTRACT, "mask_counts: counts is null");
+    p.counts = counts;
+    LKV_CUDA(launch_trace_counts(p, (int)n_heads_of(c), (cudaStream_t)stream), "mask counts");
+    return LKV_OK;
+}
+
+lkv_status lkv_cache_from_trace(const lkv_cache_desc* c, const int32_t* masks, int64_t mask_ld,
+                                const lkv_ragged_desc* out, void* ws, size_t ws_bytes, lkv_stream_t stream) {
+    TraceParams p;
+    lkv_status st = trace_params(c, masks, mask_ld, ws, ws_bytes, &p);
+    if (st) return st;
+    if ((st = check_cache(c, true))) return st;
+    if ((st = check_ragged(out, n_heads_of(c), c->head_dim, c->dtype, true))) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    p.counts = out->lens;
+    p.offsets = out->offsets;
+    p.capacity = out->capacity_rows;
+    p.out_pos = out->positions;
+    p.keys = c->keys;
+    p.values = c->values;
+    p.out_keys = out->keys;
+    p.out_values = out->values;
+    p.gather = 1;
+    LKV_CUDA(launch_trace_counts(p, (int)n_heads_of(c), s), "mask counts");
+    LKV_CUDA(launch_offsets(out->lens, (int)n_heads_of(c), out->decode_slack, out->offsets, s), "offsets");
+    LKV_CUDA(launch_trace_emit(p, s), "cache_from_trace emit");
+    return LKV_OK;
+}
+
+// score -> budget -> top-k -> compact on ONE stream as one programmatic-dependent-launch chain:
+//   K2 budgets (1 CTA, triggers its dependents at once) -> K1 scorer (PDL: runs on the other SMs
+//   while K2 solves; every K1 CTA waits for K2 before it completes) -> K3 plan -> K3+K4 emit (each
+//   waits for its predecessor).  No side stream, no flag: K2 is resident before K1 launches, so
+//   every wait makes progress on any SM partitioning, and the chain is graph-capturable.
 static lkv_status evict_impl(const lkv_cache_desc* c, const lkv_scorer_desc* s, const double* logits, int n,
                              int head_begin, bool shard, double R, int32_t mode, const lkv_ragged_desc* out,
                              float* scores_out, double* ratios_out, int32_t* budgets_out, void* ws, size_t ws_bytes,
@@ -572,60 +626,26 @@ static lkv_status evict_impl(const lkv_cache_desc* c, const lkv_scorer_desc* s, 
     int32_t* budgets = budgets_out ? budgets_out : at<int32_t>(ws, w.budgets);
     double* ratios = ratios_out ? ratios_out : at<double>(ws, w.ratios);
     float* scores = scores_out ? scores_out : at<float>(ws, w.scores);
-    // K2 (one CTA, latency-bound fp64) runs on a side stream concurrently with K1,
-    // which leaves one SM free for it; K3 waits for both.
-    cudaStream_t side = side_stream();
-    if (!side) return fail(LKV_ERR_CUDA, "side stream creation failed");
-    cudaEvent_t fork = nullptr, join = nullptr;
-    LKV_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming), "event");
-    LKV_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming), "event");
-    struct Ev {
-        cudaEvent_t a, b;
-        ~Ev() {
-            cudaEventDestroy(a);
-            cudaEventDestroy(b);
-        }
-    } guard{fork, join};
-    // timing knobs (profiles/k2_join_ab.sh): K2 before K1 on one stream / the event join instead of the flag
-    static const bool serial_k2 = getenv("LKV_SERIAL_K2") != nullptr;
-    static const bool event_join = getenv("LKV_K2_EVENT_JOIN") != nullptr;
-    if (serial_k2) side = strm;
-    // a captured graph would bake one epoch into every replay: captures keep the event join
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    LKV_CUDA(cudaStreamIsCapturing(strm, &cap), "capture status");
-    const bool use_flag = !serial_k2 && !event_join && cap == cudaStreamCaptureStatusNone;
-    static std::atomic<uint32_t> g_epoch{0};
-    uint32_t epoch = 0;
-    if (use_flag) {
-        do epoch = ++g_epoch;
-        while (epoch == 0);
-    }
-    LKV_CUDA(cudaEventRecord(fork, strm), "event record");
-    LKV_CUDA(cudaStreamWaitEvent(side, fork, 0), "stream wait");
+    // the tcgen05 scorer fuses top-k pass 1 (the histogram) into its epilogue: clear it before
+    // K2 (a memset between K2 and K1 would break the launch chain)
+    const bool tc = score_tc_supported(c->dtype, c->head_dim, s->hidden, s->input);
+    uint32_t* hist = at<uint32_t>(ws, w.hist);
+    if (tc) LKV_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 2048 * (size_t)n_heads_of(c), strm), "hist clear");
     if (shard)
         st = lkv_budgets_shard(logits, n, R, mode, c->seq_lens, c->n_seq, out->decode_slack, head_begin,
                                c->n_layers * c->n_kv_heads, ratios, at<int32_t>(ws, w.budgets_all), budgets,
-                               out->offsets, ws, ws_bytes, (lkv_stream_t)side);
+                               out->offsets, ws, ws_bytes, (lkv_stream_t)strm);
     else
         st = lkv_budgets(logits, n, R, mode, c->seq_lens, c->n_seq, out->decode_slack, ratios, budgets, out->offsets,
-                         ws, ws_bytes, (lkv_stream_t)side);
+                         ws, ws_bytes, (lkv_stream_t)strm);
     if (st) return st;
-    // the plan kernel waits for this flag (no event join: K1 -> plan -> emit stay one PDL chain)
-    if (use_flag) LKV_CUDA(launch_flag(at<uint32_t>(ws, w.k2_flag), epoch, side), "K2 flag");
-    LKV_CUDA(cudaEventRecord(join, side), "event record");
-    bool hist_made = false;  // the tcgen05 scorer fuses top-k pass 1 (the histogram) into its epilogue
-    if ((st = run_score(c, s, scores, strm, /*sms_reserved=*/1, at<uint32_t>(ws, w.hist), at<ErrWord>(ws, w.err),
-                        &hist_made)))
+    // K1 leaves one SM to K2.  The SIMT scorer (fp32 inputs) is launched normally: it runs after K2
+    // and the histogram kernel of the select reads the budgets.
+    bool hist_made = false;
+    if ((st = run_score(c, s, scores, strm, /*sms_reserved=*/tc ? 1 : 0, hist, at<ErrWord>(ws, w.err), &hist_made,
+                        /*clear_hist=*/false, /*pdl=*/tc)))
         return st;
-    // without the fused histogram, select_hist_kernel reads the budgets before the plan kernel's
-    // flag wait: join the side stream first on that path
-    if (!hist_made) epoch = 0;
-    if (event_join || !epoch) LKV_CUDA(cudaStreamWaitEvent(strm, join, 0), "stream wait");
-    st = run_select(c, scores, budgets, out, ws, w, true, strm, hist_made, 0, 0, epoch);
-    // the caller's later work on `strm` must still see K2 complete (ratios / budgets / offsets
-    // outputs): join the side stream after the emit -- off the K1 -> plan -> emit path
-    if (epoch && !st) LKV_CUDA(cudaStreamWaitEvent(strm, join, 0), "stream wait");
-    return st;
+    return run_select(c, scores, budgets, out, ws, w, true, strm, hist_made);
 }
 
 lkv_status lkv_evict(const lkv_cache_desc* c, const lkv_scorer_desc* s, const double* logits, double R, int32_t mode,
@@ -673,10 +693,10 @@ lkv_status lkv_evict_shard(const lkv_cache_desc* c, const lkv_scorer_desc* s, co
 //                 chunks are still uploading (PCIe is full duplex).
 // The D2H ranges need the ragged offsets on the host: K2 runs first on the side stream and
 // its offsets are read back once (all K uploads are already queued, so the wait is hidden).
-lkv_status lkv_evict_host(const lkv_cache_desc* hc, void* dev_keys, void* dev_values, const lkv_scorer_desc* s,
-                          const double* logits, double R, int32_t mode, const lkv_ragged_desc* out,
-                          const lkv_ragged_desc* host_out, int32_t layers_per_chunk, void* ws, size_t ws_bytes,
-                          lkv_stream_t stream) {
+static lkv_status evict_host_impl(const lkv_cache_desc* hc, void* dev_keys, void* dev_values, const lkv_scorer_desc* s,
+                                  const double* logits, int32_t n_logits, int32_t head_begin, bool shard, double R,
+                                  int32_t mode, const lkv_ragged_desc* out, const lkv_ragged_desc* host_out,
+                                  int32_t layers_per_chunk, void* ws, size_t ws_bytes, lkv_stream_t stream) {
     lkv_status st = check_cache(hc, true);
     if (st) return st;
     if ((st = check_scorer(s, hc))) return st;
@@ -698,7 +718,7 @@ lkv_status lkv_evict_host(const lkv_cache_desc* hc, void* dev_keys, void* dev_va
             return fail(LKV_ERR_CONTRACT, "host_out buffers must be pinned host memory");
     }
     const char* v_dev_alias = static_cast<const char*>(pa.devicePointer);
-    const int n = hc->n_layers * hc->n_kv_heads;
+    const int n = n_logits;
     const EvictWs w = evict_layout(hc, n);
     if ((st = check_ws(ws, ws_bytes, w.total))) return st;
     cudaStream_t strm = (cudaStream_t)stream;
@@ -731,8 +751,13 @@ lkv_status lkv_evict_host(const lkv_cache_desc* hc, void* dev_keys, void* dev_va
     LKV_CUDA(cudaStreamWaitEvent(cs, start, 0), "stream wait");
     LKV_CUDA(cudaStreamWaitEvent(ds, start, 0), "stream wait");
     // K2 on the side stream; its offsets go to the host when the compacted cache is copied back
-    st = lkv_budgets(logits, n, R, mode, hc->seq_lens, hc->n_seq, out->decode_slack, at<double>(ws, w.ratios), budgets,
-                     out->offsets, ws, ws_bytes, (lkv_stream_t)side);
+    if (shard)
+        st = lkv_budgets_shard(logits, n, R, mode, hc->seq_lens, hc->n_seq, out->decode_slack, head_begin,
+                               hc->n_layers * hc->n_kv_heads, at<double>(ws, w.ratios), at<int32_t>(ws, w.budgets_all),
+                               budgets, out->offsets, ws, ws_bytes, (lkv_stream_t)side);
+    else
+        st = lkv_budgets(logits, n, R, mode, hc->seq_lens, hc->n_seq, out->decode_slack, at<double>(ws, w.ratios),
+                         budgets, out->offsets, ws, ws_bytes, (lkv_stream_t)side);
     if (st) return st;
     const int64_t n_heads = n_heads_of(hc);
     if (host_out)
@@ -834,6 +859,26 @@ lkv_status lkv_evict_host(const lkv_cache_desc* hc, void* dev_keys, void* dev_va
         LKV_CUDA(cudaStreamWaitEvent(strm, back, 0), "stream wait");
     }
     return LKV_OK;
+}
+
+lkv_status lkv_evict_host(const lkv_cache_desc* hc, void* dev_keys, void* dev_values, const lkv_scorer_desc* s,
+                          const double* logits, double R, int32_t mode, const lkv_ragged_desc* out,
+                          const lkv_ragged_desc* host_out, int32_t layers_per_chunk, void* ws, size_t ws_bytes,
+                          lkv_stream_t stream) {
+    if (!hc) return fail(LKV_ERR_CONTRACT, "cache descriptor is null");
+    return evict_host_impl(hc, dev_keys, dev_values, s, logits, hc->n_layers * hc->n_kv_heads, 0, false, R, mode, out,
+                           host_out, layers_per_chunk, ws, ws_bytes, stream);
+}
+
+lkv_status lkv_evict_host_shard(const lkv_cache_desc* hc, void* dev_keys, void* dev_values, const lkv_scorer_desc* s,
+                                const double* logits, int32_t n_logits, int32_t head_begin, double R, int32_t mode,
+                                const lkv_ragged_desc* out, const lkv_ragged_desc* host_out, int32_t layers_per_chunk,
+                                void* ws, size_t ws_bytes, lkv_stream_t stream) {
+    if (!hc) return fail(LKV_ERR_CONTRACT, "cache descriptor is null");
+    if (n_logits < 1 || head_begin < 0 || (int64_t)head_begin + (int64_t)hc->n_layers * hc->n_kv_heads > n_logits)
+        return fail(LKV_ERR_CONTRACT, "evict_host_shard: the shard's heads must lie inside the n_logits global heads");
+    return evict_host_impl(hc, dev_keys, dev_values, s, logits, n_logits, head_begin, true, R, mode, out, host_out,
+                           layers_per_chunk, ws, ws_bytes, stream);
 }
 
 // ---- Soft-TopK (training) -------------------------------------------------
@@ -1015,8 +1060,11 @@ size_t lkv_decode_workspace_bytes(const lkv_ragged_desc* r, int32_t G) {
     return decode_layout(r, G).total;
 }
 
-lkv_status lkv_decode_plan(const lkv_ragged_desc* r, void* ws, size_t ws_bytes, lkv_stream_t stream) {
+lkv_status lkv_decode_plan_ex(const lkv_ragged_desc* r, int32_t rows_per_item, void* ws, size_t ws_bytes,
+                              lkv_stream_t stream) {
     if (!r || !r->offsets || r->n_heads < 1) return fail(LKV_ERR_CONTRACT, "bad ragged descriptor");
+    if (rows_per_item != 0 && (rows_per_item < kDecMinCh || rows_per_item > 1024 || rows_per_item % 64))
+        return fail(LKV_ERR_CONTRACT, "decode plan: rows_per_item must be 0 or a multiple of 64 in [128, 1024]");
     const DecodeWs w = decode_layout(r, 1);
     lkv_status st = check_ws(ws, ws_bytes, w.items + sizeof(DecodeItem) * (size_t)w.max_items);
     if (st) return st;
@@ -1024,9 +1072,28 @@ lkv_status lkv_decode_plan(const lkv_ragged_desc* r, void* ws, size_t ws_bytes, 
     // the combine bound assumes the largest group (16)
     LKV_CUDA(launch_decode_plan(r->offsets, r->n_heads, 1, 1, at<DecodeItem>(ws, w.items), at<int32_t>(ws, w.item_base),
                                 at<int32_t>(ws, w.layer_begin), at<int32_t>(ws, w.n_items), at<int32_t>(ws, w.ch),
-                                8 * num_sms(), 16, (cudaStream_t)stream),
+                                8 * num_sms(), 16, rows_per_item, (cudaStream_t)stream),
              "decode plan");
     return LKV_OK;
+}
+
+lkv_status lkv_decode_plan_info(const lkv_ragged_desc* r, const void* ws, int32_t* n_items, int32_t* rows_per_item,
+                                lkv_stream_t stream) {
+    if (!r || !ws) return fail(LKV_ERR_CONTRACT, "decode plan info: null argument");
+    const DecodeWs w = decode_layout(r, 1);  // the plan words do not depend on G
+    int32_t v[2] = {0, 0};
+    LKV_CUDA(cudaMemcpyAsync(&v[0], static_cast<const char*>(ws) + w.n_items, 4, cudaMemcpyDeviceToHost,
+                             (cudaStream_t)stream), "plan info");
+    LKV_CUDA(cudaMemcpyAsync(&v[1], static_cast<const char*>(ws) + w.ch, 4, cudaMemcpyDeviceToHost, (cudaStream_t)stream),
+             "plan info");
+    LKV_CUDA(cudaStreamSynchronize((cudaStream_t)stream), "plan info");
+    if (n_items) *n_items = v[0];
+    if (rows_per_item) *rows_per_item = v[1];
+    return LKV_OK;
+}
+
+lkv_status lkv_decode_plan(const lkv_ragged_desc* r, void* ws, size_t ws_bytes, lkv_stream_t stream) {
+    return lkv_decode_plan_ex(r, 0, ws, ws_bytes, stream);
 }
 
 lkv_status lkv_decode_step(const lkv_ragged_desc* r, int32_t n_seq, int32_t n_layers, int32_t n_kv_heads,
@@ -1278,10 +1345,12 @@ size_t lkv_model_workspace_bytes(const lkv_model_desc* m, int32_t n_seq, const l
     return model_ws(model_geom(m), n_seq, r, m).total;
 }
 
-lkv_status lkv_model_plan(const lkv_model_desc* m, const lkv_ragged_desc* r, int32_t n_seq, void* ws, size_t ws_bytes,
-                          lkv_stream_t stream) {
+lkv_status lkv_model_plan_ex(const lkv_model_desc* m, const lkv_ragged_desc* r, int32_t n_seq, int32_t rows_per_item,
+                             void* ws, size_t ws_bytes, lkv_stream_t stream) {
     lkv_status st = check_model(m);
     if (st || (st = check_model_cache(m, r, n_seq))) return st;
+    if (rows_per_item != 0 && (rows_per_item < kDecMinCh || rows_per_item > 1024 || rows_per_item % 64))
+        return fail(LKV_ERR_CONTRACT, "model plan: rows_per_item must be 0 or a multiple of 64 in [128, 1024]");
     const ModelGeom g = model_geom(m);
     const ModelWs w = model_ws(g, n_seq, r, m);
     if ((st = check_ws(ws, ws_bytes, w.total))) return st;
@@ -1292,10 +1361,15 @@ lkv_status lkv_model_plan(const lkv_model_desc* m, const lkv_ragged_desc* r, int
                                 at<int32_t>(ws, w.dec.item_base), at<int32_t>(ws, w.dec.layer_begin),
                                 at<int32_t>(ws, w.dec.n_items), at<int32_t>(ws, w.dec.ch),
                                 g.dtype == LKV_BF16 ? -decode_resident_ctas(g.Hq / g.H, num_sms()) : 4 * num_sms(),
-                                g.Hq / g.H, s),
+                                g.Hq / g.H, rows_per_item, s),
              "decode plan");
     LKV_CUDA(launch_rope_table(m->max_seq_len, g.D, m->rope_base, 0, at<float2>(ws, w.rope), s), "rope table");
     return LKV_OK;
+}
+
+lkv_status lkv_model_plan(const lkv_model_desc* m, const lkv_ragged_desc* r, int32_t n_seq, void* ws, size_t ws_bytes,
+                          lkv_stream_t stream) {
+    return lkv_model_plan_ex(m, r, n_seq, 0, ws, ws_bytes, stream);
 }
 
 lkv_status lkv_model_decode_step(const lkv_model_desc* m, const void* weights, const lkv_ragged_desc* r, int32_t n_seq,
@@ -1380,8 +1454,7 @@ lkv_status lkv_model_decode_step(const lkv_model_desc* m, const void* weights, c
     dp.part_o = at<float>(ws, w.dec.part_o);
     dp.new_len = at<int32_t>(ws, w.dec.new_len);
     dp.err = err;
-    static const bool no_early = getenv("LKV_NO_EARLY_KV") != nullptr;  // A/B knob (profiles/knob_combine.sh)
-    dp.early_kv = g.dtype == LKV_BF16 && !no_early ? 1 : 0;  // the step's first launch (embed) is fully serialised
+    dp.early_kv = g.dtype == LKV_BF16 ? 1 : 0;  // the step's first launch (embed) is fully serialised
     CUtensorMap mk, mv;
     if (g.dtype == LKV_BF16) {
         if ((st = make_map_bf16(&mk, r->keys, 128, (uint64_t)r->capacity_rows, 64))) return st;
@@ -1406,21 +1479,20 @@ lkv_status lkv_model_decode_step(const lkv_model_desc* m, const void* weights, c
     gp.norm_eps = (float)m->norm_eps;
     gp.act_next = act_h;
     auto normed = [&](GemvParams& q) { q.ss_in = ss; };
-    static const int mx = getenv("LKV_MODEL_EXPT") ? atoi(getenv("LKV_MODEL_EXPT")) : 0;  // timing knobs
     for (int l = 0; l < g.L; ++l) {
         const unsigned char* lw = wb + g.layer0 + (size_t)l * g.layer_stride;
-        if (!(mx & 4)) LKV_CUDA(gemv(g.qkv, lw + g.o_qkv, EPI_QKV, act_h, g.dm + 2 * g.dkv, normed), "qkv");
+        LKV_CUDA(gemv(g.qkv, lw + g.o_qkv, EPI_QKV, act_h, g.dm + 2 * g.dkv, normed), "qkv");
         dp.layer0 = l;
         dp.item_lo = lbeg + l;
         dp.item_hi = lbeg + l + 1;
-        if (!(mx & 2)) LKV_CUDA(launch_decode(dp, g.dtype, &mk, &mv, sms, s), "attention");
+        LKV_CUDA(launch_decode(dp, g.dtype, &mk, &mv, sms, s), "attention");
         const float* g_mlp = norm_gain(l, true);
-        if (!(mx & 8)) LKV_CUDA(gemv(g.wo, lw + g.o_wo, EPI_RESID, at<void>(ws, w.act_attn), g.dm,
+        LKV_CUDA(gemv(g.wo, lw + g.o_wo, EPI_RESID, at<void>(ws, w.act_attn), g.dm,
                       [&](GemvParams& q) { q.gain_next = g_mlp; }),
                  "wo");
-        if (!(mx & 16)) LKV_CUDA(gemv(g.gu, lw + g.o_gu, EPI_SWIGLU, act_h, g.ff, normed), "gate/up");
+        LKV_CUDA(gemv(g.gu, lw + g.o_gu, EPI_SWIGLU, act_h, g.ff, normed), "gate/up");
         const float* g_next = norm_gain(l + 1, false);
-        if (!(mx & 32)) LKV_CUDA(gemv(g.down, lw + g.o_down, EPI_RESID, at<void>(ws, w.act_ff), g.dm,
+        LKV_CUDA(gemv(g.down, lw + g.o_down, EPI_RESID, at<void>(ws, w.act_ff), g.dm,
                       [&](GemvParams& q) { q.gain_next = g_next; }),
                  "down");
     }

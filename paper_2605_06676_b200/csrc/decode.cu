@@ -27,14 +27,8 @@ namespace lkv_dev {
 
 constexpr int kDecMaxCh = 1024;  // largest work item (rows); the plan picks 128..1024 per cache
 constexpr int kDecStageRows = 64;   // rows per pipeline stage
-#ifndef LKV_DEC_STAGES
-#define LKV_DEC_STAGES 2
-#endif
-#ifndef LKV_DEC_PER_SM
-#define LKV_DEC_PER_SM 2
-#endif
-constexpr int kDecStages = LKV_DEC_STAGES;  // x 32 KB per CTA
-constexpr int kDecPerSm = LKV_DEC_PER_SM;   // resident CTAs per SM
+constexpr int kDecStages = 2;       // x 32 KB per CTA
+constexpr int kDecPerSm = 2;        // resident CTAs per SM
 constexpr int kDecConsumers = 4;    // consumer warps (16 rows of a stage each)
 constexpr int kDecThreads = (kDecConsumers + 1) * 32;
 
@@ -54,7 +48,7 @@ constexpr int kPlanMaxLayers = 256;   // layers the one-wave policy tracks
 __global__ void __launch_bounds__(1024) decode_plan_kernel(const int64_t* offsets, int n_seq, int n_layers, int n_kv,
                                                            DecodeItem* items, int32_t* item_base,
                                                            int32_t* layer_begin, int32_t* n_items, int32_t* ch_out,
-                                                           int target_items, int G) {
+                                                           int target_items, int G, int force_ch) {
     __shared__ uint32_t s_scan[33];
     __shared__ int32_t s_carry;
     __shared__ unsigned long long s_cnt[4];
@@ -74,7 +68,9 @@ __global__ void __launch_bounds__(1024) decode_plan_kernel(const int64_t* offset
     }
     __syncthreads();
     int ch = 128;
-    if (target_items < 0 && n_layers <= kPlanMaxLayers) {
+    if (force_ch > 0) {
+        ch = force_ch;  // the caller fixes the work-item size (tests; profiling of one shape)
+    } else if (target_items < 0 && n_layers <= kPlanMaxLayers) {
         // one-wave policy (per-layer launches, target = -slots): the smallest ch (a multiple of 64)
         // whose busiest layer has no more items than the launch has resident CTAs, so no layer's
         // attention runs a second, mostly idle wave
@@ -694,9 +690,9 @@ __global__ void __launch_bounds__(kCombCols * kCombSlices) decode_combine_kernel
 // ---- host launchers ---------------------------------------------------------------------------------
 cudaError_t launch_decode_plan(const int64_t* offsets, int n_seq, int n_layers, int n_kv, DecodeItem* items,
                                int32_t* item_base, int32_t* layer_begin, int32_t* n_items, int32_t* ch,
-                               int target_items, int G, cudaStream_t stream) {
+                               int target_items, int G, int force_ch, cudaStream_t stream) {
     decode_plan_kernel<<<1, 1024, 0, stream>>>(offsets, n_seq, n_layers, n_kv, items, item_base, layer_begin,
-                                               n_items, ch, target_items, G);
+                                               n_items, ch, target_items, G, force_ch);
     note_launches(1);
     return cudaGetLastError();
 }
@@ -731,8 +727,6 @@ cudaError_t launch_decode(const DecodeParams& p, int dtype, const CUtensorMap* m
         const int grid = min(p.max_items, per_sm * num_sms);
         e = launch_pdl(kern, dim3(grid), dim3(kDecThreads), smem, stream, p, *mk, *mv);
         if (e != cudaSuccess) return e;
-        static const bool no_comb = getenv("LKV_NO_COMBINE") != nullptr;  // timing knob (profiles/model_knobs.sh)
-        if (no_comb) return cudaGetLastError();
         const dim3 cgrid(p.n_seq * p.q_layers * p.n_kv_heads, (p.G * p.head_dim + kCombCols - 1) / kCombCols);
         // few heads (a per-layer launch): split each head's chunks over 4 thread slices
         if (cgrid.x * cgrid.y < (unsigned)num_sms)

@@ -43,6 +43,9 @@ struct ScoreParams {
     float* scores;
     uint32_t* hist;  // nullable: fused top-11-bit histogram per head (tcgen05 path; zeroed by the caller)
     ErrWord* err;
+    // 1: launched as the programmatic-dependent secondary of K2 on the same stream (lkv_evict):
+    // it starts while K2 runs and waits for K2 before completing
+    int32_t pdl;
     int32_t tile_base[LKV_MAX_SEQ + 1];
 };
 cudaError_t launch_score_simt(ScoreParams p, int dtype, int num_sms, cudaStream_t stream);
@@ -74,14 +77,8 @@ struct SelectParams {
     int32_t gather;
     int32_t hist_ready;  // the scorer already produced `hist` (fused pass 1)
     ErrWord* err;
-    // non-null: budgets / offsets come from K2 on a side stream with no event join; the plan
-    // kernel waits (bounded) until *k2_flag == k2_epoch, which launch_flag stores after K2
-    const uint32_t* k2_flag;
-    uint32_t k2_epoch;
     int32_t chunk_base[LKV_MAX_SEQ + 1];
 };
-// one-thread kernel: *flag = epoch (release, gpu scope) once every earlier op of the stream is done
-cudaError_t launch_flag(uint32_t* flag, uint32_t epoch, cudaStream_t stream);
 struct CompactParams {
     SeqTable seq;
     const int64_t* offsets;
@@ -95,6 +92,27 @@ struct CompactParams {
     ErrWord* err;
 };
 cudaError_t launch_select(SelectParams p, int n_heads, cudaStream_t stream);
+// cache_from_trace by a device mask scan (model.cpp:289-315)
+struct TraceParams {
+    SeqTable seq;
+    const int32_t* masks;  // [n_heads][mask_ld], nonzero = keep
+    int64_t mask_ld;
+    uint32_t* chunk_cnt;   // [chunks] (workspace): counts, then exclusive bases within the head
+    int32_t* counts;       // [n_heads] kept rows per head (the ragged lens)
+    const int64_t* offsets;
+    int64_t capacity;
+    int32_t* out_pos;
+    const void* keys;
+    const void* values;
+    void* out_keys;
+    void* out_values;
+    int32_t row_bytes;
+    int32_t gather;
+    ErrWord* err;
+    int32_t chunk_base[LKV_MAX_SEQ + 1];
+};
+cudaError_t launch_trace_counts(TraceParams p, int n_heads, cudaStream_t stream);
+cudaError_t launch_trace_emit(TraceParams p, cudaStream_t stream);
 cudaError_t launch_compact(const CompactParams& p, int n_heads, cudaStream_t stream);
 // ---- decode.cu (K5)
 // Packed activation layout read by the weight-streaming GEMV (model.cu): the bf16 B operand of
@@ -143,10 +161,11 @@ struct DecodeParams {
     int32_t early_kv;
 };
 // target_items > 0: the largest power-of-two ch giving at least that many items per layer;
-// target_items < 0: the smallest ch (multiple of 64) whose busiest layer fits -target_items items
+// target_items < 0: the smallest ch (multiple of 64) whose busiest layer fits -target_items items;
+// force_ch > 0 overrides both (a multiple of 64 in [kDecMinCh, 1024])
 cudaError_t launch_decode_plan(const int64_t* offsets, int n_seq, int n_layers, int n_kv, DecodeItem* items,
                                int32_t* item_base, int32_t* layer_begin, int32_t* n_items, int32_t* ch,
-                               int target_items, int G, cudaStream_t stream);
+                               int target_items, int G, int force_ch, cudaStream_t stream);
 constexpr int kDecMinCh = 128;  // smallest work item the plan may choose (workspace sizing)
 cudaError_t launch_decode(const DecodeParams& p, int dtype, const CUtensorMap* mk, const CUtensorMap* mv, int num_sms,
                           cudaStream_t stream);

@@ -42,36 +42,12 @@ namespace lkv_dev {
 constexpr int kWsCols = 64;                    // output columns per unit (4 m16 tiles)
 constexpr int kWsK = 128;                      // k per unit (8 k16 steps)
 constexpr int kWsUnitBytes = kWsCols * kWsK * 2;  // 16 KB of bf16
-#ifndef LKV_WS_STAGES
-#define LKV_WS_STAGES 4
-#endif
-#ifndef LKV_WS_PER_SM
-#define LKV_WS_PER_SM 2
-#endif
-constexpr int kWsStages = LKV_WS_STAGES;
+constexpr int kWsStages = 4;
 constexpr int kWsConsumers = 4;
 constexpr int kWsThreads = (kWsConsumers + 1) * 32;
-constexpr int kWsPerSm = LKV_WS_PER_SM;
+constexpr int kWsPerSm = 2;
 constexpr int kYPad = 17;                      // y[64][17]: columns x batch (B <= 16)
 constexpr int kWsMaxSplit = 1024;              // CTAs sharing one column group (<= KU + 1; K <= 130k)
-#ifndef LKV_GEMV_SPLIT
-#define LKV_GEMV_SPLIT 1  // cluster split-K for narrow matrices (0: stream-K everywhere, for A/B)
-#endif
-#ifndef LKV_GEMV_EXPT
-#define LKV_GEMV_EXPT 0  // profiles/gemv_bench.cu bisection knobs: 1 no mma, 2 no fix-up, 4 no epilogue, 8 trace
-#endif
-#if LKV_GEMV_EXPT & 8
-__device__ unsigned long long g_gemv_trace[512][8];
-__device__ __forceinline__ unsigned long long gtime() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-#define GTRACE(i) \
-    if ((LKV_GEMV_EXPT & 8) && threadIdx.x == 0) g_gemv_trace[blockIdx.x][i] = gtime()
-#else
-#define GTRACE(i)
-#endif
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
@@ -243,7 +219,6 @@ __device__ __forceinline__ void ws_consume(const GemvParams& p, int64_t u0, int6
     const int tid = threadIdx.x;  // 0..127
     const int64_t U = (int64_t)p.NG * p.KU;
     const int P = gridDim.x, c = blockIdx.x;
-    GTRACE(0);
     const int g = lane >> 2, cq = (lane & 3) * 2;
     int64_t u = u0;
     const int ng_first = (int)(u0 / p.KU);
@@ -270,7 +245,6 @@ __device__ __forceinline__ void ws_consume(const GemvParams& p, int64_t u0, int6
 #pragma unroll
                 for (int t = 0; t < 4; ++t) {
                     const uint4 a = *reinterpret_cast<const uint4*>(stg + ((ks * 4 + t) * 32 + lane) * 16);
-                    if (LKV_GEMV_EXPT & 1) { acc[t][0][0] += __uint_as_float(a.x); continue; }
 #pragma unroll
                     for (int bt = 0; bt < NBT; ++bt) mma_16816(acc[t][bt], a, bf[bt].x, bf[bt].y);
                 }
@@ -282,7 +256,6 @@ __device__ __forceinline__ void ws_consume(const GemvParams& p, int64_t u0, int6
                 ph ^= 1;
             }
         }
-        GTRACE(1);
         // ---- cross-warp reduction (fixed order) -> y[64][b]
         constexpr int BW = NBT * 8;
 #pragma unroll
@@ -306,7 +279,7 @@ __device__ __forceinline__ void ws_consume(const GemvParams& p, int64_t u0, int6
         }
         named_sync(1, kWsConsumers * 32);
         if constexpr (SPLIT) break;  // one column group per CTA: reduced across the cluster by the caller
-        if (!whole && !(LKV_GEMV_EXPT & 2)) {
+        if (!whole) {
             // stream-K fix-up: partial -> global slot; the last CTA of the group sums in CTA order
             const int slot = 2 * c + (ng == ng_first ? 0 : 1);
             float* mine = p.part + (size_t)slot * kWsCols * 16;
@@ -326,7 +299,6 @@ __device__ __forceinline__ void ws_consume(const GemvParams& p, int64_t u0, int6
                 *s_last = last;
             }
             named_sync(1, kWsConsumers * 32);
-            GTRACE(2);
             if (!*s_last) continue;
             // slot of every contributing CTA computed once (one 64-bit division each), then each
             // thread streams its two float4 of every partial with the loads of 4 CTAs in flight --
@@ -355,10 +327,8 @@ __device__ __forceinline__ void ws_consume(const GemvParams& p, int64_t u0, int6
             }
             named_sync(1, kWsConsumers * 32);
         }
-        GTRACE(3);
-        if (!(LKV_GEMV_EXPT & 4)) gemv_epilogue<__nv_bfloat16>(p, ng, y, tid, kWsConsumers * 32);
+        gemv_epilogue<__nv_bfloat16>(p, ng, y, tid, kWsConsumers * 32);
         named_sync(1, kWsConsumers * 32);
-        GTRACE(4);
     }
 }
 
@@ -376,7 +346,6 @@ __global__ void __launch_bounds__(kWsThreads, kWsPerSm) wstream_gemv_kernel(cons
     int* s_slot = s_last + 4;  // [kWsMaxSplit]: partial slots of the CTAs sharing a column group
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    GTRACE(5);
     const int64_t U = (int64_t)p.NG * p.KU;
     const int P = gridDim.x, c = blockIdx.x;
     int64_t u0, u1;
@@ -536,7 +505,7 @@ cudaError_t launch_gemv(const GemvParams& p, int dtype, int num_sms, cudaStream_
         // beat stream-K; QKV at S = 3 was slower, odd cluster sizes pack poorly)
         int S = 1;
         while (S < 8 && (int64_t)p.NG * S * 2 <= cap && S * 2 <= p.KU) S *= 2;
-        if (S >= 2 && (int64_t)p.NG * S * 5 >= cap * 4 && LKV_GEMV_SPLIT) {
+        if (S >= 2 && (int64_t)p.NG * S * 5 >= cap * 4) {
             GemvParams q = p;
             q.split = S;
             auto kern = q.nbt == 1 ? wstream_gemv_kernel<1, true> : wstream_gemv_kernel<2, true>;

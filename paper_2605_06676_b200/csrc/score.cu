@@ -24,7 +24,7 @@ __device__ __forceinline__ float act_f32(int act, float h) {
 
 // Epilogue activations on the MUFU path (approximations far inside the 1e-2 bf16 bar):
 //  GELU-erf: gelu(h) = h * Phi(h) = 0.5 (h + |h| erf(|h|/sqrt2)); erf by Abramowitz-Stegun
-//            7.1.28 (one rcp, default) or 7.1.26 (rcp + ex2).  f() returns 2*gelu; w2 is
+//            7.1.28 (one rcp).  f() returns 2*gelu; w2 is
 //            pre-scaled by 0.5.
 //  SiLU:     h / (1 + e^{-h}) (tensor.cpp:371-378) with ex2 + rcp.
 __device__ __forceinline__ float rcp_approx(float x) {
@@ -39,26 +39,9 @@ __device__ __forceinline__ float ex2_approx(float x) {
 }
 template <int ACT>
 struct EpiAct;
-#ifndef LKV_GELU_AS
-#define LKV_GELU_AS 28
-#endif
 template <>
 struct EpiAct<LKV_ACT_GELU_ERF> {
     static constexpr float kW2Scale = 0.5f;
-#if LKV_GELU_AS == 26
-    __device__ __forceinline__ static float f(float h) {
-        const float ah = fabsf(h);
-        const float t = rcp_approx(fmaf(0.3275911f * 0.70710678118654752f, ah, 1.0f));
-        float p = fmaf(1.061405429f, t, -1.453152027f);
-        p = fmaf(p, t, 1.421413741f);
-        p = fmaf(p, t, -0.284496736f);
-        p = fmaf(p, t, 0.254829592f);
-        p *= t;
-        const float e = ex2_approx(h * h * -0.72134752044448170f);  // e^{-h^2/2}
-        const float erf_abs = fmaf(-p, e, 1.0f);
-        return fmaf(ah, erf_abs, h);
-    }
-#else
     // Abramowitz-Stegun 7.1.28: erf(u) = 1 - (1 + a1 u + ... + a6 u^6)^-16, |error| <= 3e-7
     // (1.7e-6 in fp32); u = |h|/sqrt2 folded into the coefficients.  One MUFU (rcp).
     __device__ __forceinline__ static float f(float h) {
@@ -76,7 +59,6 @@ struct EpiAct<LKV_ACT_GELU_ERF> {
         const float r = rcp_approx(y);
         return fmaf(-ah, r, h + ah);  // 2 gelu(h) = h + |h| erf(|h|/sqrt2)
     }
-#endif
 };
 template <>
 struct EpiAct<LKV_ACT_SILU> {
@@ -207,9 +189,6 @@ __device__ __forceinline__ TileInfo decode_tile(const ScoreParams& p, int tile, 
 // tcgen05 kernel
 // ============================================================================
 constexpr int kTcRows = 128;  // UMMA M
-#ifndef LKV_SCORE_EPI
-#define LKV_SCORE_EPI 4
-#endif
 // Epilogue groups of 4 warps (one TMEM lane quarter each); group g drains accumulator
 // stage g, i.e. every E-th tile.  Warps 0..3: TMA producer, MMA issuer, TMEM allocator, spare.
 constexpr int kHistBins = 2048;  // top 11 key bits: the first radix digit of the top-k (select.cu)
@@ -222,7 +201,7 @@ struct TcCfg {
     static constexpr int kW = NBOX * kWBox;
     static constexpr int kStages = (NBOX == 2) ? (N <= 64 ? 5 : 4) : 2;
     // [k;v] tiles (NBOX = 4) leave room for two epilogue groups only
-    static constexpr int kEpi = (NBOX == 2) ? LKV_SCORE_EPI : 2;
+    static constexpr int kEpi = (NBOX == 2) ? 4 : 2;
     static constexpr int kThreads = 128 + 128 * kEpi;
     static constexpr int kEpiChunk = kEpi > 2 ? 16 : 32;  // TMEM columns per tcgen05.ld (register budget)
     static constexpr int kAcc = kEpi * N;  // accumulator columns: one N-wide stage per epilogue group
@@ -259,29 +238,10 @@ __global__ void __launch_bounds__(TcCfg<N, NBOX>::kThreads, 1)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
 
-    // Tile schedule.  LKV_SCORE_RR == 0: one contiguous range per CTA (tiles of a head and
-    // heads of a layer stay together).  LKV_SCORE_RR == g > 0: groups of g tiles dealt
-    // round-robin, so all CTAs stream through the same region of the cache at once.
-#ifndef LKV_SCORE_RR
-#define LKV_SCORE_RR 0
-#endif
-    constexpr int RR = LKV_SCORE_RR;
-    constexpr int RRd = RR > 0 ? RR : 1;
-    int n_local;
-    int t_begin = 0;
-    if (RR == 0) {
-        t_begin = (int)((int64_t)total_tiles * blockIdx.x / gridDim.x);
-        n_local = (int)((int64_t)total_tiles * (blockIdx.x + 1) / gridDim.x) - t_begin;
-    } else {
-        const int n_chunks = (total_tiles + RRd - 1) / RRd;
-        const int mine = (int)blockIdx.x < n_chunks ? (n_chunks - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-        n_local = mine * RRd;
-        if (mine && (n_chunks - 1) % (int)gridDim.x == (int)blockIdx.x) n_local -= n_chunks * RRd - total_tiles;
-    }
-    auto tile_of = [&](int i) -> int {
-        if (RR == 0) return t_begin + i;
-        return ((i / RRd) * (int)gridDim.x + (int)blockIdx.x) * RRd + (i % RRd);
-    };
+    // Tile schedule: one contiguous range of (seq, head, 128-row tile) per CTA, so the tiles of
+    // a head and the heads of a scorer stay together (weights and histogram flushes amortised).
+    const int t_begin = (int)((int64_t)total_tiles * blockIdx.x / gridDim.x);
+    const int n_local = (int)((int64_t)total_tiles * (blockIdx.x + 1) / gridDim.x) - t_begin;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
@@ -313,10 +273,10 @@ __global__ void __launch_bounds__(TcCfg<N, NBOX>::kThreads, 1)
             const uint64_t pol_stream = l2_policy_evict_first();
             const uint64_t pol_keep = l2_policy_evict_last();
             int cur = -1, wloads = 0;
-            TileCursor cur_t = cursor_at(p, tile_of(0), kTcRows);
+            TileCursor cur_t = cursor_at(p, t_begin, kTcRows);
             for (int i = 0; i < n_local; ++i) {
-                if (RR == 0 && i > 0) cursor_next(p, cur_t, kTcRows);
-                const TileInfo ti = RR == 0 ? cursor_info(p, cur_t, kTcRows) : decode_tile(p, tile_of(i), kTcRows);
+                if (i > 0) cursor_next(p, cur_t, kTcRows);
+                const TileInfo ti = cursor_info(p, cur_t, kTcRows);
                 if (ti.scorer != cur) {
                     if (wloads > 0) mbar_wait(wempty, (wloads - 1) & 1);
                     mbar_arrive_expect_tx(wfull, Cfg::kW);
@@ -347,10 +307,10 @@ __global__ void __launch_bounds__(TcCfg<N, NBOX>::kThreads, 1)
             const uint32_t a_base = smem_u32(sA);
             const uint32_t w_base = smem_u32(sW);
             int cur = -1, wuses = 0;
-            TileCursor cur_t = cursor_at(p, tile_of(0), kTcRows);
+            TileCursor cur_t = cursor_at(p, t_begin, kTcRows);
             for (int i = 0; i < n_local; ++i) {
-                if (RR == 0 && i > 0) cursor_next(p, cur_t, kTcRows);
-                const TileInfo ti = RR == 0 ? cursor_info(p, cur_t, kTcRows) : decode_tile(p, tile_of(i), kTcRows);
+                if (i > 0) cursor_next(p, cur_t, kTcRows);
+                const TileInfo ti = cursor_info(p, cur_t, kTcRows);
                 if (ti.scorer != cur) {
                     if (wuses > 0) umma_commit(wempty);  // old weights free once prior MMAs retire
                     mbar_wait(wfull, wuses & 1);
@@ -398,11 +358,11 @@ __global__ void __launch_bounds__(TcCfg<N, NBOX>::kThreads, 1)
             named_bar_sync(1 + grp, 128);
         };
         int cur = -1, cur_head = -1;
-        TileCursor cur_t = cursor_at(p, tile_of(grp), kTcRows);
+        TileCursor cur_t = cursor_at(p, t_begin + grp, kTcRows);
         for (int i = grp; i < n_local; i += kEpi) {
-            if (RR == 0 && i > grp)
+            if (i > grp)
                 for (int k = 0; k < kEpi; ++k) cursor_next(p, cur_t, kTcRows);
-            const TileInfo ti = RR == 0 ? cursor_info(p, cur_t, kTcRows) : decode_tile(p, tile_of(i), kTcRows);
+            const TileInfo ti = cursor_info(p, cur_t, kTcRows);
             if (p.hist && ti.head != cur_head) {
                 if (cur_head >= 0) flush_hist(cur_head);
                 else named_bar_sync(1 + grp, 128);  // zeroing complete
@@ -462,6 +422,11 @@ __global__ void __launch_bounds__(TcCfg<N, NBOX>::kThreads, 1)
         tc_fence_after();
         tmem_dealloc(tmem_base, Cfg::kTmemCols);
     }
+    // Launched as the PDL secondary of K2 (lkv_evict): no CTA of this grid may complete before
+    // K2 has, so the select kernels behind this one (which wait for this grid) see the budgets
+    // and offsets.  K2 is resident before this grid launches (it triggers at its start), so the
+    // wait always makes progress.  A no-op for a normal launch.
+    pdl_wait();
 }
 
 // ============================================================================
@@ -584,7 +549,11 @@ static cudaError_t launch_tc_inst(const ScoreParams& p, const CUtensorMap& mk, c
     auto kern = score_tc_kernel<N, NBOX, ACT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
     if (e != cudaSuccess) return e;
-    kern<<<grid, Cfg::kThreads, Cfg::kSmem, stream>>>(p, mk, mv, mw, tiles);
+    if (p.pdl)
+        e = launch_pdl(kern, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmem, stream, p, mk, mv, mw, tiles);
+    else
+        kern<<<grid, Cfg::kThreads, Cfg::kSmem, stream>>>(p, mk, mv, mw, tiles);
+    if (e != cudaSuccess) return e;
     note_launches(1);
     return cudaGetLastError();
 }

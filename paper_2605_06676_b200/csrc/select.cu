@@ -154,28 +154,6 @@ __global__ void __launch_bounds__(kPlanThreads, 2) select_plan_kernel(const __gr
     uint32_t* s_ckey = plan_dyn + kCandCap;
     __shared__ uint32_t s_scan[33];
     __shared__ uint32_t s_bin, s_above, s_ncand;
-    if (p.k2_flag) {  // K2 ran on a side stream: wait for its flag instead of an event join
-        __shared__ int s_k2_late;
-        if (threadIdx.x == 0) {
-            uint64_t t0, t1;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-            uint32_t v;
-            s_k2_late = 0;
-            for (;;) {
-                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.k2_flag) : "memory");
-                if (v == p.k2_epoch) break;
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-                if (t1 - t0 > 2000000000ull) {  // 2 s: never in practice (K2 takes ~0.1 ms); no hang
-                    latch_error(p.err, LKV_ERR_CUDA, -1);
-                    s_k2_late = 1;
-                    break;
-                }
-                __nanosleep(200);
-            }
-        }
-        __syncthreads();
-        if (s_k2_late) return;
-    }
     const int head = blockIdx.x;
     const int s_idx = head_seq(p.seq, head);
     const int t = p.seq.len[s_idx];
@@ -380,32 +358,9 @@ __global__ void __launch_bounds__(kPlanThreads, 2) select_plan_kernel(const __gr
 }
 
 // ---- row gather (16-byte vectors) ----------------------------------------------------------
+constexpr int kGatherUnroll = 8;  // 16-byte loads in flight per thread and tensor
 // 2^log2_units 16-byte vectors per row (head_dim * elem / 16); lanes walk (row, vector)
 // pairs so a warp moves whole rows with coalesced 16-byte accesses.
-__device__ __forceinline__ void gather_rows(const uint4* __restrict__ src, uint4* __restrict__ dst,
-                                            const int32_t* rows /*smem*/, int n_rows, int log2_units, int tid,
-                                            int nthreads) {
-    const int units = 1 << log2_units;
-    const int total = n_rows << log2_units;
-    int u = tid;
-#ifndef LKV_GATHER_UNROLL
-#define LKV_GATHER_UNROLL 8
-#endif
-    constexpr int U = LKV_GATHER_UNROLL;
-    for (; u + (U - 1) * nthreads < total; u += U * nthreads) {
-        uint4 v[U];
-#pragma unroll
-        for (int k = 0; k < U; ++k) {
-            const int uu = u + k * nthreads;
-            v[k] = __ldg(src + ((size_t)rows[uu >> log2_units] << log2_units) + (uu & (units - 1)));
-        }
-#pragma unroll
-        for (int k = 0; k < U; ++k) __stcs(dst + u + k * nthreads, v[k]);
-    }
-    for (; u < total; u += nthreads)
-        __stcs(dst + u, __ldg(src + ((size_t)rows[u >> log2_units] << log2_units) + (u & (units - 1))));
-}
-
 // K and V rows of the same kept positions in one loop: twice the loads in flight per thread
 __device__ __forceinline__ void gather_rows_kv(const uint4* __restrict__ ks, const uint4* __restrict__ vs,
                                                uint4* __restrict__ kd, uint4* __restrict__ vd,
@@ -414,7 +369,7 @@ __device__ __forceinline__ void gather_rows_kv(const uint4* __restrict__ ks, con
     const int units = 1 << log2_units;
     const int total = n_rows << log2_units;
     int u = tid;
-    constexpr int U = LKV_GATHER_UNROLL;
+    constexpr int U = kGatherUnroll;
     for (; u + (U - 1) * nthreads < total; u += U * nthreads) {
         uint4 a[U], b[U];
 #pragma unroll
@@ -438,10 +393,7 @@ __device__ __forceinline__ void gather_rows_kv(const uint4* __restrict__ ks, con
 }
 
 // ---- S5 --------------------------------------------------------------------------
-#ifndef LKV_EMIT_MINB
-#define LKV_EMIT_MINB 1
-#endif
-__global__ void __launch_bounds__(kSelThreads, LKV_EMIT_MINB) select_emit_kernel(const __grid_constant__ SelectParams p) {
+__global__ void __launch_bounds__(kSelThreads) select_emit_kernel(const __grid_constant__ SelectParams p) {
     pdl_wait();
     __shared__ int32_t s_pos[kChunk];
     __shared__ uint32_t s_scan[kSelThreads / 32 + 1];
@@ -504,8 +456,12 @@ __global__ void __launch_bounds__(kSelThreads, LKV_EMIT_MINB) select_emit_kernel
 
 constexpr int kCompactRows = 256;
 
+// A position outside [0, t) (or a head whose rows overrun its capacity) is a contract_error, as
+// the reference's bounds checks raise (model.cpp:298-312, evictsim.cpp:104-109): it is latched in
+// the caller's workspace and the offending rows are not written (never silently replaced).
 __global__ void __launch_bounds__(256) compact_kernel(const __grid_constant__ CompactParams p) {
     __shared__ int32_t s_pos[kCompactRows];
+    __shared__ int s_bad;
     const int head = blockIdx.y;
     const int r0 = blockIdx.x * kCompactRows;
     const int len = p.lens[head];
@@ -513,25 +469,162 @@ __global__ void __launch_bounds__(256) compact_kernel(const __grid_constant__ Co
     const int n = min(kCompactRows, len - r0);
     const int t = p.seq.len[head_seq(p.seq, head)];
     const int64_t obase = p.offsets[head] + r0;
-    if (p.offsets[head] + len > p.offsets[head + 1]) {
+    if (len < 0 || p.offsets[head] + len > p.offsets[head + 1]) {
         if (threadIdx.x == 0) latch_error(p.err, LKV_ERR_CONTRACT, head);
         return;
     }
+    if (threadIdx.x == 0) s_bad = 0;
+    __syncthreads();
     for (int i = threadIdx.x; i < n; i += 256) {
-        int32_t pos = p.positions[obase + i];
-        if (pos < 0 || pos >= t) {
-            latch_error(p.err, LKV_ERR_CONTRACT, head);
-            pos = 0;
-        }
+        const int32_t pos = p.positions[obase + i];
+        if (pos < 0 || pos >= t) s_bad = 1;
         s_pos[i] = pos;
     }
     __syncthreads();
+    if (s_bad) {
+        if (threadIdx.x == 0) latch_error(p.err, LKV_ERR_CONTRACT, head);
+        return;
+    }
     const int lu = 31 - __clz(p.row_bytes / 16);
     const size_t head_row0 = (size_t)head * p.seq.T;
-    gather_rows(static_cast<const uint4*>(p.keys) + (head_row0 << lu), static_cast<uint4*>(p.out_keys) + (obase << lu),
-                s_pos, n, lu, threadIdx.x, 256);
-    gather_rows(static_cast<const uint4*>(p.values) + (head_row0 << lu),
-                static_cast<uint4*>(p.out_values) + (obase << lu), s_pos, n, lu, threadIdx.x, 256);
+    gather_rows_kv(static_cast<const uint4*>(p.keys) + (head_row0 << lu),
+                   static_cast<const uint4*>(p.values) + (head_row0 << lu), static_cast<uint4*>(p.out_keys) + (obase << lu),
+                   static_cast<uint4*>(p.out_values) + (obase << lu), s_pos, n, lu, threadIdx.x, 256);
+}
+
+// ---- cache_from_trace on the device: compaction by a mask scan (model.cpp:289-315) -------------
+// Row j of head i is kept iff masks[i * mask_ld + j] != 0 (j < t), ascending.  Three passes over
+// 4096-row chunks: count, per-head chunk scan (-> lens), emit (positions + 16-byte row gather).
+__device__ __forceinline__ ChunkInfo trace_chunk(const TraceParams& p, int chunk) {
+    int s = 0;
+    while (s + 1 < p.seq.n_seq && p.chunk_base[s + 1] <= chunk) ++s;
+    const int t = p.seq.len[s];
+    const int cph = (t + kChunk - 1) / kChunk;
+    const int local = chunk - p.chunk_base[s];
+    const int hs = local / cph;
+    ChunkInfo ci;
+    ci.c = local - hs * cph;
+    ci.head = s * p.seq.n_layers * p.seq.n_kv_heads + hs;
+    ci.cbase = chunk - ci.c;
+    ci.t = t;
+    ci.c0 = ci.c * kChunk;
+    ci.n = min(kChunk, t - ci.c0);
+    return ci;
+}
+
+__device__ __forceinline__ uint32_t trace_keep16(const TraceParams& p, const ChunkInfo& ci, int j0) {
+    const int32_t* m = p.masks + (size_t)ci.head * p.mask_ld + ci.c0;
+    uint32_t keep = 0;
+    if (j0 + kPerThread <= ci.n && (reinterpret_cast<uintptr_t>(m + j0) & 15) == 0) {
+        const int4* v = reinterpret_cast<const int4*>(m + j0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int4 x = __ldg(v + q);
+            keep |= uint32_t(x.x != 0) << (4 * q) | uint32_t(x.y != 0) << (4 * q + 1) |
+                    uint32_t(x.z != 0) << (4 * q + 2) | uint32_t(x.w != 0) << (4 * q + 3);
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < kPerThread; ++q) keep |= uint32_t(j0 + q < ci.n && __ldg(m + j0 + q) != 0) << q;
+    }
+    return keep;
+}
+
+__global__ void __launch_bounds__(kSelThreads) trace_count_kernel(const __grid_constant__ TraceParams p) {
+    __shared__ uint32_t s_scan[kSelThreads / 32 + 1];
+    const ChunkInfo ci = trace_chunk(p, blockIdx.x);
+    const uint32_t n = __popc(trace_keep16(p, ci, threadIdx.x * kPerThread));
+    uint32_t tot;
+    block_exclusive_scan<kSelThreads>(n, s_scan, &tot);
+    if (threadIdx.x == 0) p.chunk_cnt[blockIdx.x] = tot;
+}
+
+// one CTA per head: chunk counts -> exclusive chunk bases (in place), head total -> counts
+__global__ void __launch_bounds__(kSelThreads) trace_scan_kernel(const __grid_constant__ TraceParams p) {
+    __shared__ uint32_t s_scan[kSelThreads / 32 + 1];
+    const int head = blockIdx.x;
+    const int s_idx = head_seq(p.seq, head);
+    const int t = p.seq.len[s_idx];
+    const int cph = (t + kChunk - 1) / kChunk;
+    const int hs = head - s_idx * p.seq.n_layers * p.seq.n_kv_heads;
+    uint32_t* cc = p.chunk_cnt + p.chunk_base[s_idx] + hs * cph;
+    constexpr int kPer = kMaxChunksPerHead / kSelThreads;
+    uint32_t v[kPer], local = 0;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+        const int c = threadIdx.x * kPer + q;
+        v[q] = c < cph ? cc[c] : 0u;
+        local += v[q];
+    }
+    uint32_t tot;
+    uint32_t run = block_exclusive_scan<kSelThreads>(local, s_scan, &tot);
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+        const int c = threadIdx.x * kPer + q;
+        if (c < cph) cc[c] = run;
+        run += v[q];
+    }
+    if (threadIdx.x == 0) p.counts[head] = (int32_t)tot;
+}
+
+__global__ void __launch_bounds__(kSelThreads) trace_emit_kernel(const __grid_constant__ TraceParams p) {
+    __shared__ int32_t s_pos[kChunk];
+    __shared__ uint32_t s_scan[kSelThreads / 32 + 1];
+    const ChunkInfo ci = trace_chunk(p, blockIdx.x);
+    const int64_t o0 = p.offsets[ci.head], o1 = p.offsets[ci.head + 1];
+    const int32_t len = p.counts[ci.head];
+    if (o0 < 0 || o0 + len > o1 || o1 > p.capacity) {  // the ragged cache cannot hold this head
+        if (threadIdx.x == 0 && ci.c == 0) latch_error(p.err, LKV_ERR_CONTRACT, ci.head);
+        return;
+    }
+    const int j0 = threadIdx.x * kPerThread;
+    const uint32_t keep = trace_keep16(p, ci, j0);
+    uint32_t tot;
+    uint32_t slot = block_exclusive_scan<kSelThreads>(__popc(keep), s_scan, &tot);
+    const int64_t obase = o0 + p.chunk_cnt[blockIdx.x];
+    uint32_t k = keep;
+    while (k) {
+        const int q = __ffs(k) - 1;
+        k &= k - 1;
+        const int32_t pos = ci.c0 + j0 + q;
+        p.out_pos[obase + slot] = pos;
+        s_pos[slot] = pos;
+        ++slot;
+    }
+    if (!p.gather || tot == 0) return;
+    __syncthreads();
+    const int lu = 31 - __clz(p.row_bytes / 16);
+    const size_t head_row0 = (size_t)ci.head * p.seq.T;
+    gather_rows_kv(static_cast<const uint4*>(p.keys) + (head_row0 << lu),
+                   static_cast<const uint4*>(p.values) + (head_row0 << lu), static_cast<uint4*>(p.out_keys) + (obase << lu),
+                   static_cast<uint4*>(p.out_values) + (obase << lu), s_pos, (int)tot, lu, threadIdx.x, kSelThreads);
+}
+
+static int trace_total_chunks(TraceParams& p) {
+    int64_t acc = 0;
+    for (int s = 0; s < p.seq.n_seq; ++s) {
+        p.chunk_base[s] = (int32_t)acc;
+        acc += (int64_t)p.seq.n_layers * p.seq.n_kv_heads * ((p.seq.len[s] + kChunk - 1) / kChunk);
+    }
+    p.chunk_base[p.seq.n_seq] = (int32_t)acc;
+    return (int)acc;
+}
+
+cudaError_t launch_trace_counts(TraceParams p, int n_heads, cudaStream_t stream) {
+    const int chunks = trace_total_chunks(p);
+    if (chunks == 0) return cudaSuccess;
+    trace_count_kernel<<<chunks, kSelThreads, 0, stream>>>(p);
+    trace_scan_kernel<<<n_heads, kSelThreads, 0, stream>>>(p);
+    note_launches(2);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_trace_emit(TraceParams p, cudaStream_t stream) {
+    const int chunks = trace_total_chunks(p);
+    if (chunks == 0) return cudaSuccess;
+    trace_emit_kernel<<<chunks, kSelThreads, 0, stream>>>(p);
+    note_launches(1);
+    return cudaGetLastError();
 }
 
 // ---- host launchers --------------------------------------------------------------------------
@@ -561,16 +654,6 @@ cudaError_t launch_select(SelectParams p, int n_heads, cudaStream_t stream) {
     if ((e = launch_pdl(select_plan_kernel, dim3(n_heads), dim3(kPlanThreads), kPlanSmem, stream, p)) != cudaSuccess) return e;
     if ((e = launch_pdl(select_emit_kernel, dim3(chunks), dim3(kSelThreads), 0, stream, p)) != cudaSuccess) return e;
     note_launches(2);
-    return cudaGetLastError();
-}
-
-__global__ void flag_kernel(uint32_t* flag, uint32_t epoch) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(epoch) : "memory");
-}
-
-cudaError_t launch_flag(uint32_t* flag, uint32_t epoch, cudaStream_t stream) {
-    flag_kernel<<<1, 1, 0, stream>>>(flag, epoch);
-    note_launches(1);
     return cudaGetLastError();
 }
 

@@ -296,27 +296,30 @@ size_t esize(Precision p) { return p == Precision::bf16 ? 2 : 4; }
 KvCache cache_from_trace(const KvTrace& tr, const std::vector<std::vector<int>>& hard_masks, Precision prec) {
     const int heads = tr.n_layers * tr.n_kv_heads;
     if ((int)hard_masks.size() != heads) throw contract_error("cache_from_trace: one mask per head required");
-    DenseUpload du = upload_trace(tr, prec);
-    std::vector<int32_t> counts((size_t)heads), positions;
+    std::vector<int32_t> masks((size_t)heads * tr.t);
     for (int h = 0; h < heads; ++h) {
         const auto& m = hard_masks[(size_t)h];
         if ((int)m.size() != tr.t) throw contract_error("cache_from_trace: mask length mismatch");
-        for (int j = 0; j < tr.t; ++j)
-            if (m[(size_t)j]) {
-                positions.push_back(j);
-                ++counts[(size_t)h];
-            }
+        std::copy(m.begin(), m.end(), masks.begin() + (size_t)h * tr.t);
     }
-    const int64_t rows = (int64_t)positions.size();
-    Dev B = upload(counts.data(), counts.size());
+    DenseUpload du = upload_trace(tr, prec);
+    Dev M = upload(masks.data(), masks.size());
+    Workspace ws(lkv_workspace_bytes(&du.desc, 1));
+    // device mask scan: counts size the ragged cache, then compaction + 16-byte row gather
+    Dev cnt(sizeof(int32_t) * (size_t)heads);
+    check(lkv_mask_counts(&du.desc, M.as<int32_t>(), tr.t, cnt.as<int32_t>(), ws.ptr(), ws.bytes, (lkv_stream_t)stream()),
+          "cache_from_trace");
+    int64_t rows = 0;
+    for (int32_t c : download<int32_t>(cnt, (size_t)heads)) rows += c;
     Dev offs(sizeof(int64_t) * ((size_t)heads + 1));
-    check(lkv_ragged_offsets(B.as<int32_t>(), heads, 0, offs.as<int64_t>(), (lkv_stream_t)stream()), "cache_from_trace");
-    Dev lens = upload(counts.data(), counts.size());
-    Dev rp = upload(positions.data(), positions.size() ? positions.size() : 1);
+    Dev lens(sizeof(int32_t) * (size_t)heads);
+    Dev rp(sizeof(int32_t) * (size_t)(rows ? rows : 1));
     Dev rk(esize(prec) * (size_t)(rows ? rows : 1) * tr.head_dim), rv(esize(prec) * (size_t)(rows ? rows : 1) * tr.head_dim);
     lkv_ragged_desc r{heads, tr.head_dim, dtype_of(prec), 0, rows, offs.as<int64_t>(), lens.as<int32_t>(), rk.p, rv.p,
                       rp.as<int32_t>()};
-    check(lkv_compact(&du.desc, &r, (lkv_stream_t)stream()), "cache_from_trace");
+    check(lkv_cache_from_trace(&du.desc, M.as<int32_t>(), tr.t, &r, ws.ptr(), ws.bytes, (lkv_stream_t)stream()),
+          "cache_from_trace");
+    ws.status("cache_from_trace");
     return download_ragged(tr, offs, lens, rk, rv, rp, prec);
 }
 

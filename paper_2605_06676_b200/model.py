@@ -97,9 +97,9 @@ class DecodeModel:
         self.cache = None
         self.ws = None
 
-    def bind(self, cache: RaggedCache) -> None:
+    def bind(self, cache: RaggedCache, rows_per_item: int = 0) -> None:
         """Attach a compacted cache (after every eviction): plans the per-layer attention
-        work and builds the RoPE table."""
+        work (rows_per_item 0: one wave per layer; else fixed) and builds the RoPE table."""
         if cache.n_seq > MODEL_MAX_SEQ:
             raise ValueError(f"at most {MODEL_MAX_SEQ} sequences per decode batch")
         rd = cache.desc()
@@ -108,8 +108,8 @@ class DecodeModel:
             _check(1)
         self.cache = cache
         self.ws = Workspace(nbytes, device=self.device)
-        _check(lib().lkv_model_plan(C.byref(self.desc), C.byref(rd), cache.n_seq, C.c_void_p(self.ws.ptr),
-                                    self.ws.nbytes, _stream()))
+        _check(lib().lkv_model_plan_ex(C.byref(self.desc), C.byref(rd), cache.n_seq, int(rows_per_item),
+                                       C.c_void_p(self.ws.ptr), self.ws.nbytes, _stream()))
         self._rd = rd
 
     def step(self, tokens: torch.Tensor, logits: torch.Tensor | None = None, check: bool = True) -> torch.Tensor:

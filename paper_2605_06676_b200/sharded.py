@@ -189,6 +189,32 @@ class ShardEvictor:
                                      _ptr(self.ratios), _ptr(self.budgets), C.c_void_p(self.ws.ptr), self.ws.nbytes,
                                      _stream(stream)))
 
+    def launch_host(self, logits: torch.Tensor, host_keys: torch.Tensor, host_values: torch.Tensor,
+                    host_out: RaggedCache | None = None, layers_per_chunk: int = 1, stream=None) -> None:
+        """lkv_evict_host_shard: this rank's layers held in pinned host memory, K streamed into the
+        evictor's device K buffer chunk by chunk, kept V rows gathered over PCIe, the compacted shard
+        copied back into `host_out` (pinned, same capacity) when given."""
+        if logits.numel() != self.n_logits or logits.dtype != torch.float64:
+            raise ContractError("evict_host_shard needs the full fp64 logit vector (gather_logits)")
+        if not (host_keys.is_pinned() and host_values.is_pinned()):
+            raise ContractError("host K/V must be pinned (torch pin_memory)")
+        if tuple(host_keys.shape) != self.cache.shape or host_keys.dtype != self.cache.keys.dtype:
+            raise ContractError("host K/V must match the shard's cache shape and dtype")
+        hd = _abi.CacheDesc(*[getattr(self._cd, f) for f, _ in _abi.CacheDesc._fields_])
+        hd.keys, hd.values = host_keys.data_ptr(), host_values.data_ptr()
+        dev_v = self.cache.values.data_ptr() if self.scorers.input == _abi.SCORER_KV else None
+        ho = host_out.desc() if host_out is not None else None
+        _check(lib().lkv_evict_host_shard(C.byref(hd), C.c_void_p(self.cache.keys.data_ptr()),
+                                          C.c_void_p(dev_v) if dev_v else None, C.byref(self._sd), _ptr(logits),
+                                          self.n_logits, self.head_begin, self.R, self.mode, C.byref(self._rd),
+                                          C.byref(ho) if ho is not None else None, layers_per_chunk,
+                                          C.c_void_p(self.ws.ptr), self.ws.nbytes, _stream(stream)))
+
+    def host_result_buffer(self) -> RaggedCache:
+        r = self.ragged
+        return RaggedCache(r.n_seq, r.n_layers, r.n_kv_heads, r.head_dim, r.dtype, r.capacity_rows, r.decode_slack,
+                           device="cpu", pinned=True)
+
     def run(self, logits: torch.Tensor) -> RaggedCache:
         self.launch(logits)
         self.ws.status()

@@ -48,7 +48,7 @@ def test_tensor_core_and_tma_instructions_present():
 
 def test_status_names_and_version():
     L = lkv.lib()
-    assert L.lkv_abi_version() == 1
+    assert L.lkv_abi_version() == 2
     assert L.lkv_status_name(3) == b"budget_error"
     assert L.lkv_status_name(1) == b"contract_error"
 

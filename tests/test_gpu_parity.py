@@ -597,7 +597,7 @@ def test_evict_is_deterministic():
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("ratio", [0.05, 0.25])
+@pytest.mark.parametrize("ratio", [0.05, 0.10, 0.25])
 def test_config3_full_size_properties(ratio):
     """C3 at full size (t = 131072, 256 heads): exact totals, top-b property with the
     lowest-index tie rule, rows equal the dense rows at the kept positions."""
@@ -608,7 +608,7 @@ def test_config3_full_size_properties(ratio):
     res = lkv.evict(cache, scorers, logits, ratio, lkv.BUDGET_EXACT, keep_scores=True)
     n, T = cfg.n_layers * cfg.n_kv_heads, cfg.max_tokens
     b = res.budgets.reshape(-1)
-    assert int(b.sum()) == {0.05: 1677722, 0.25: 8388608}[ratio]
+    assert int(b.sum()) == {0.05: 1677722, 0.10: 3355443, 0.25: 8388608}[ratio]
     want_b = O.freeze_budgets_exact(O.allocate_budgets(logits.cpu().numpy(), ratio), ratio, T)
     assert (b.cpu().numpy() == want_b).all()
     scores = res.scores.reshape(n, T)
@@ -628,6 +628,142 @@ def test_config3_full_size_properties(ratio):
         assert torch.equal(res.cache.values[offs[h]:offs[h] + bh], Vd[h][p])
         if h % 61 == 0:
             assert (p.cpu().numpy() == O.select_positions_f32(scores[h].cpu().numpy(), bh)).all()
+
+
+@pytest.mark.slow
+def test_config3_headline_full_parity():
+    """The bench's headline workload, C3 at full size (t = 131072, 32 x 8 heads, R = 0.15, exact
+    budgets, one lkv_evict): budgets bit-exact (total 5,033,165); EVERY head's kept positions
+    bit-exact against the oracle's stable-sort top-k on the device scores; every kept K/V row equal
+    to the dense row; K1 scores within 1e-2 of the fp64 oracle on 8 full heads spread over the
+    layers; then decode over that cache with the bench's 1024-row work items, checked against the
+    fp64 oracle on sampled heads (the largest heads included)."""
+    cfg = synth.CONFIGS[3]
+    cache = synth.make_cache(cfg)
+    scorers = synth.make_scorers(cfg)
+    logits = synth.make_logits(cfg)
+    res = lkv.evict(cache, scorers, logits, 0.15, lkv.BUDGET_EXACT, decode_slack=4, keep_scores=True)
+    n, T, D = cfg.n_layers * cfg.n_kv_heads, cfg.max_tokens, cfg.head_dim
+    b = res.budgets.reshape(-1).cpu().numpy()
+    assert int(b.sum()) == 5033165
+    want_b = O.freeze_budgets_exact(O.allocate_budgets(logits.cpu().numpy(), 0.15), 0.15, T)
+    assert (b == want_b).all()
+    rc = res.cache
+    offs = rc.offsets.cpu().numpy()
+    assert (rc.lens.cpu().numpy() == b).all()
+    scores = res.scores.reshape(n, T).cpu().numpy()
+    pos_all = rc.positions.cpu().numpy()
+    Kd = cache.keys.reshape(n, T, D)
+    Vd = cache.values.reshape(n, T, D)
+    for h in range(n):
+        bh = int(b[h])
+        p = pos_all[offs[h]:offs[h] + bh]
+        assert (p == O.select_positions_f32(scores[h], bh)).all(), h
+        pt = torch.from_numpy(p.astype(np.int64)).to(DEV)
+        assert torch.equal(rc.keys[offs[h]:offs[h] + bh], Kd[h][pt]), h
+        assert torch.equal(rc.values[offs[h]:offs[h] + bh], Vd[h][pt]), h
+    # K1 scores at full length on 8 heads (layers 0, 4, ..., 28; head l % 8)
+    w1 = w_np(scorers.w1)
+    for l in range(0, cfg.n_layers, 4):
+        h = l * cfg.n_kv_heads + (l % cfg.n_kv_heads)
+        ref = O.token_scores(to_np(Kd[h]), None, w1[l], w_np(scorers.b1[l]), w_np(scorers.w2[l]), act=O.GELU_ERF)
+        assert rel_gap(scores[h], ref) <= 1e-2, h
+    # decode with the measured work-item size (all layers per launch, ch = 1024)
+    G = cfg.n_q_heads // cfg.n_kv_heads
+    rc.tokens_seen.fill_(T)
+    lkv.decode_plan(rc, G, rows_per_item=1024)
+    assert lkv.decode_plan_info(rc)[1] == 1024
+    del res, scores
+    for st in range(2):
+        q, k, v = synth.make_decode_inputs(cfg, st)
+        out = lkv.decode_step(rc, q, k, v)
+    heads = sorted(set([int(np.argmax(b)), int(np.argmin(b))] + list(range(0, n, 23))))
+    _check_decode_heads(rc, q, out, cfg.n_kv_heads, heads, 1e-2)
+
+
+def _check_decode_heads(rc, q, out, n_kv, heads, tol):
+    """fp64 oracle over the device's cache for the listed flat heads (n_seq == 1)."""
+    _, L, Hq, D = q.shape
+    G = Hq // n_kv
+    scale = 1.0 / math.sqrt(D)
+    qn = q.detach().to(torch.float64).cpu().numpy()
+    on = out.detach().to(torch.float64).cpu().numpy()
+    offs = rc.offsets.cpu().numpy()
+    lens = rc.lens.cpu().numpy()
+    for h in heads:
+        l, kvh = divmod(h, n_kv)
+        o, ln = int(offs[h]), int(lens[h])
+        want = O.decode_attention(qn[0, l, kvh * G:(kvh + 1) * G], to_np(rc.keys[o:o + ln]), to_np(rc.values[o:o + ln]),
+                                  scale)
+        assert rel_gap(on[0, l, kvh * G:(kvh + 1) * G], want) <= tol, h
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("rows_per_item", [0, 1024, 192])
+def test_config2_full_size_decode_work_items(rows_per_item):
+    """Decode over the full evicted C2 cache with the work-item size the bench measures (the
+    automatic all-layer plan picks 1024 rows here) and two forced sizes, against the fp64 oracle on
+    every head."""
+    cfg = synth.CONFIGS[2]
+    cache = synth.make_cache(cfg)
+    res = lkv.evict(cache, synth.make_scorers(cfg), synth.make_logits(cfg), cfg.ratio, lkv.BUDGET_EXACT,
+                    decode_slack=8)
+    del cache
+    rc = res.cache
+    rc.tokens_seen.fill_(cfg.max_tokens)
+    G = cfg.n_q_heads // cfg.n_kv_heads
+    lkv.decode_plan(rc, G, rows_per_item=rows_per_item)
+    n_items, ch = lkv.decode_plan_info(rc)
+    assert ch == (rows_per_item or 1024)
+    assert n_items >= rc.n_heads
+    for st in range(3):
+        q, k, v = synth.make_decode_inputs(cfg, st)
+        out = lkv.decode_step(rc, q, k, v)
+    want = _decode_oracle(rc, q, cfg.n_kv_heads, 1.0 / math.sqrt(cfg.head_dim))
+    assert rel_gap(out.to(torch.float64).cpu().numpy(), want) <= 1e-2
+
+
+def test_compact_rejects_out_of_range_positions():
+    """lkv_compact: a position outside [0, t) is a contract_error, latched in the workspace; the
+    head's rows are not written (never replaced by another row)."""
+    torch.manual_seed(3)
+    K = torch.randn(1, 1, 2, 64, 128, device=DEV).to(torch.bfloat16)
+    cache = lkv.DenseCache(K, K.clone(), [64])
+    rc = lkv.RaggedCache(1, 1, 2, 128, torch.bfloat16, 8, 0)
+    rc.offsets.copy_(torch.tensor([0, 4, 8], dtype=torch.int64))
+    rc.lens.fill_(4)
+    rc.positions.copy_(torch.tensor([0, 5, 9, 63, 1, 2, 64, 3], dtype=torch.int32))
+    rc.keys.fill_(7.0)
+    with pytest.raises(lkv.ContractError):
+        lkv.compact(cache, rc)
+    assert torch.equal(rc.keys[:4], K[0, 0, 0][[0, 5, 9, 63]])
+    assert bool((rc.keys[4:] == 7.0).all())  # head 1 (position 64 >= t) untouched
+    rc.positions[6] = 4
+    lkv.compact(cache, rc)
+    assert torch.equal(rc.keys[4:], K[0, 0, 1][[1, 2, 4, 3]])
+
+
+def test_cache_from_trace_capacity_and_ragged_lengths():
+    """Device mask scan over ragged sequences (t_s < max_tokens, heads longer than one 4096-row
+    chunk): counts, offsets (with decode slack), positions and rows exact."""
+    torch.manual_seed(4)
+    T = 9000
+    K = torch.randn(2, 1, 2, T, 128, device=DEV).to(torch.bfloat16)
+    V = torch.randn(2, 1, 2, T, 128, device=DEV).to(torch.bfloat16)
+    cache = lkv.DenseCache(K, V, [T, 5000])
+    masks = (torch.rand(4, T, device=DEV) < 0.2).to(torch.int32)
+    masks[2:, 5000:] = 1  # past t_s: never kept
+    rc = lkv.cache_from_trace(cache, masks, decode_slack=3)
+    m = masks.cpu().numpy()
+    offs = rc.offsets.cpu().numpy()
+    Kn, Vn = to_np(K).reshape(4, T, 128), to_np(V).reshape(4, T, 128)
+    for h in range(4):
+        t = T if h < 2 else 5000
+        want = np.nonzero(m[h, :t])[0]
+        k, v, p = rc.head(h)
+        assert (p.cpu().numpy() == want).all()
+        assert offs[h + 1] - offs[h] == len(want) + 3
+        assert (to_np(k) == Kn[h, want]).all() and (to_np(v) == Vn[h, want]).all()
 
 
 # ---------------------------------------------------------------------------------------------
@@ -691,9 +827,9 @@ def test_layerwise_prefill_equals_one_shot_eviction():
 
 @pytest.mark.gpu
 def test_evict_graph_replay_matches_eager():
-    """lkv_evict captured in a CUDA graph (the K2 -> plan hand-off then uses the event join, not the
-    per-call epoch flag) and replayed gives the eager result, also after the logits change between
-    replays (budgets re-solved inside the graph)."""
+    """lkv_evict captured in a CUDA graph (its K2 -> K1 -> plan -> emit programmatic-dependent
+    chain is captured as such) and replayed gives the eager result, also after the logits change
+    between replays (budgets re-solved inside the graph)."""
     cfg = synth.CONFIGS[2]
     cache = synth.make_cache(cfg, n_layers=2, max_tokens=8192)
     scorers = synth.make_scorers(cfg, n_layers=2)

@@ -80,7 +80,7 @@ def _ragged(cfg, seqs, dtype, slack, t):
     return rc, rounded
 
 
-def _run(cfg, P, dtype, n_seq, t, steps, seed, tol, slack=None):
+def _run(cfg, P, dtype, n_seq, t, steps, seed, tol, slack=None, rows_per_item=0):
     torch.manual_seed(seed)
     Pd = _round(P, dtype)
     seqs = _caches(cfg, Pd, n_seq, t, seed)
@@ -90,7 +90,9 @@ def _run(cfg, P, dtype, n_seq, t, steps, seed, tol, slack=None):
     dm = M.DecodeModel(M.ModelConfig(**{k: getattr(cfg, k) for k in ("n_layers", "n_query_heads", "n_kv_heads",
                                                                       "head_dim", "vocab_size", "max_seq_len",
                                                                       "mlp_hidden")}), P, dtype=dtype)
-    dm.bind(rc)
+    dm.bind(rc, rows_per_item=rows_per_item)
+    if rows_per_item:
+        assert lkv.decode_plan_info(rc, dm.ws)[1] == rows_per_item
     rng = np.random.default_rng(seed + 1)
     for step in range(steps):
         toks = rng.integers(0, cfg.vocab_size, n_seq)
@@ -141,12 +143,15 @@ def test_model_decode_bf16(n_seq):
     _run(cfg, P, torch.bfloat16, n_seq=n_seq, t=200 if n_seq < 9 else 64, steps=2, seed=10 + n_seq, tol=1e-2)
 
 
-def test_model_decode_bf16_gqa8_long_cache():
-    """G=8, caches long enough for several 1024-row attention chunks per head."""
+@pytest.mark.parametrize("rows_per_item", [0, 512, 1024, 192])
+def test_model_decode_bf16_gqa8_long_cache(rows_per_item):
+    """G=8, ~1500-row heads: the one-wave plan (0 picks the smallest 64-multiple that fits one
+    wave, 128 rows for these four heads) and forced 512 / 1024 / 192-row work items, i.e. heads
+    spanning 1-3 large chunks and the multi-slice combine."""
     cfg = OM.ModelConfig(n_layers=1, n_query_heads=16, n_kv_heads=2, head_dim=128, vocab_size=300,
                          max_seq_len=4096, mlp_hidden=512)
     P = OM.random_params(cfg, 12, norm_jitter=0.1)
-    _run(cfg, P, torch.bfloat16, n_seq=2, t=3000, steps=2, seed=13, tol=1e-2, slack=5)
+    _run(cfg, P, torch.bfloat16, n_seq=2, t=3000, steps=2, seed=13, tol=1e-2, slack=5, rows_per_item=rows_per_item)
 
 
 def test_model_decode_deterministic_and_graph():

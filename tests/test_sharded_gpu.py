@@ -100,3 +100,33 @@ def test_nccl_comm_single_rank():
         assert torch.equal(sharded.gather_logits(comm, plan, lg), lg)
     finally:
         comm.close()
+
+
+@pytest.mark.parametrize("world,rank", [(4, 1), (4, 3)])
+def test_host_shard_equals_device_shard(world, rank):
+    """lkv_evict_host_shard (the rank's layers in pinned host memory, K streamed in, kept V gathered
+    over PCIe, compacted shard copied back) == lkv_evict_shard on the device copy, bit for bit."""
+    cfg = synth.CONFIGS[2]
+    L, T = 8, 5000
+    cache = synth.make_cache(cfg, n_layers=L, max_tokens=T)
+    scorers = synth.make_scorers(cfg, n_layers=L)
+    logits = synth.make_logits(cfg, n_layers=L)
+    plan = sharded.ShardPlan(L, cfg.n_kv_heads, world)
+    l0, l1 = plan.layers[rank]
+    lc, ls = _local(cache, scorers, l0, l1)
+    ev = sharded.ShardEvictor(lc, ls, plan, rank, cfg.ratio, lkv.BUDGET_EXACT, decode_slack=2)
+    dev = ev.run(logits)
+    want = [x.clone() for x in (dev.offsets, dev.lens, dev.positions, dev.keys, dev.values)]
+    hk, hv = lc.keys.cpu().pin_memory(), lc.values.cpu().pin_memory()
+    ho = ev.host_result_buffer()
+    for _ in range(2):
+        ev.launch_host(logits, hk, hv, ho, layers_per_chunk=1)
+        torch.cuda.synchronize()
+        ev.ws.status()
+        assert torch.equal(ho.offsets, want[0].cpu()) and torch.equal(ho.lens, want[1].cpu())
+        offs, lens = want[0].cpu().tolist(), want[1].cpu().tolist()
+        for h in range(len(lens)):
+            o, n = offs[h], lens[h]
+            assert torch.equal(ho.positions[o:o + n], want[2][o:o + n].cpu())
+            assert torch.equal(ho.keys[o:o + n], want[3][o:o + n].cpu())
+            assert torch.equal(ho.values[o:o + n], want[4][o:o + n].cpu())
