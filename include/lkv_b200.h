@@ -74,7 +74,7 @@ typedef enum lkv_status {
     LKV_ERR_NCCL = 8             /* NCCL missing or a collective failed (multi-GPU plumbing only) */
 } lkv_status;
 
-typedef enum lkv_dtype { LKV_F32 = 0, LKV_BF16 = 1 } lkv_dtype;
+typedef enum lkv_dtype { LKV_F32 = 0, LKV_BF16 = 1, LKV_F64 = 2 /* gather-only: lkv_compact / cache_from_trace */ } lkv_dtype;
 typedef enum lkv_activation { LKV_ACT_SILU = 0, LKV_ACT_GELU_ERF = 1 } lkv_activation;
 typedef enum lkv_scorer_input {
     LKV_SCORER_K = 1,  /* x = k            (BASELINE.json configs: head_dim -> hidden -> 1) */
@@ -327,6 +327,67 @@ lkv_status lkv_masked_attention_bwd(const lkv_attn_desc* attn, const void* q, co
                                     const float* mask, const void* out, const float* lse, const void* d_out,
                                     float* dq, float* dk, float* dv, float* dmask, void* workspace,
                                     size_t workspace_bytes, lkv_stream_t stream);
+
+/* ---- fp64 reference-precision operators --------------------------------------------- */
+/* The reference computes in float64 (tensor.hpp:3).  These device operators back the
+ * declaration-compatible C++ API (include/lkv/ headers), which keeps the reference's signatures and
+ * precision: the LKV-H solve with its outputs (lambda, split m, density, permutation), the LKV-T
+ * scorer, top-b selection on fp64 scores, and the toy GQA model's forward / decode operators.
+ * Each output element is computed in an order independent of the number of rows in the call, so
+ * a t-row prefill and a one-row decode agree bit for bit.  All row-major, device pointers. */
+
+/* soft_topk_forward (soft_topk.hpp:60, soft_topk.cpp:111-164) with the reference's exact solve
+ * (solve_threshold :58-109): values [n], density [n], permutation [n] (stable descending order of
+ * x), lambda, split_m, clamped_k (each nullable but values).  Device-side errors latch: k outside
+ * (0, n) -> BUDGET, non-finite -> NUMERIC, |x/tau| > 1e300 (n >= 2) -> OVERFLOW_GUARD, no bracket
+ * -> NUMERIC. */
+lkv_status lkv_soft_topk_exact(const double* x, int32_t n, double k, double tau, double* values, double* density,
+                               int32_t* permutation, double* lambda, int32_t* split_m, double* clamped_k,
+                               void* workspace, size_t workspace_bytes, lkv_stream_t stream);
+/* C[M x N] (+)= A[M x K] B[K x N] (matmul, tensor.cpp:276-297); accumulate: C + (A B). */
+lkv_status lkv_f64_gemm(int32_t M, int32_t N, int32_t K, const double* A, int64_t lda, const double* B, int64_t ldb,
+                        double* C, int64_t ldc, int32_t accumulate, lkv_stream_t stream);
+/* out = x * gain / sqrt(mean(x^2) + eps) per row (rmsnorm, model.cpp:48-53) */
+lkv_status lkv_f64_rmsnorm(int32_t rows, int32_t cols, const double* x, int64_t ldx, const double* gain, double eps,
+                           double* out, int64_t ldo, lkv_stream_t stream);
+/* rotary pairs of every head of row r at position pos0 + r, in place (rope, tensor.cpp:586-623) */
+lkv_status lkv_f64_rope(int32_t rows, int32_t n_heads, int32_t head_dim, double* x, int64_t ldx, int32_t pos0,
+                        double base, lkv_stream_t stream);
+/* masked_attention_dense (attention.cpp:46-94) for n_q_heads query heads at once, query head h
+ * reading kv head h / group; p_raw / p [n_q_heads][n_q][t] and renorm [n_q_heads][n_q] nullable
+ * (AttentionSaved).  A row whose masked mass vanishes -> DEGENERATE_MASK (latched). */
+typedef struct lkv_f64_attn_desc {
+    int32_t n_q_heads, group, n_q, t, head_dim;
+    int32_t causal, query_pos_offset, self_always_retained;
+    double scale;
+    const double* q;  int64_t ldq;    /* row r, head h at q[r * ldq + h * head_dim] */
+    const double* k;  const double* v; int64_t ldkv;
+    const double* mask; int64_t mask_ld; /* nullable; kv head g's mask at mask[g * mask_ld + j] */
+    double* out;      int64_t ldo;
+    double* p_raw;    double* p;       double* renorm;
+} lkv_f64_attn_desc;
+lkv_status lkv_f64_attention(const lkv_f64_attn_desc* attn, void* workspace, size_t workspace_bytes,
+                             lkv_stream_t stream);
+/* out = silu(gate) * up (model.cpp:112-115) */
+lkv_status lkv_f64_swiglu(int64_t n, const double* gate, const double* up, double* out, lkv_stream_t stream);
+/* out[r] = table[tokens[r]] (embedding_rows); a token outside [0, vocab) -> CONTRACT (latched) */
+lkv_status lkv_f64_embed(const int32_t* tokens, int32_t n, const double* table, int32_t d_model, int32_t vocab,
+                         double* out, void* workspace, size_t workspace_bytes, lkv_stream_t stream);
+/* [t][n_heads * head_dim] (row stride ldx) -> head-major [n_heads][out_rows][head_dim] */
+lkv_status lkv_f64_split_heads(int32_t t, int32_t n_heads, int32_t head_dim, const double* x, int64_t ldx, double* out,
+                               int64_t out_rows, lkv_stream_t stream);
+/* token_scores (policy.cpp:131-136): u = act(x W1 + b1) . w2, x = [k ; v] (input KV) or k;
+ * W1 [in][hidden] as the reference stores it.  A non-finite score -> NUMERIC (latched). */
+lkv_status lkv_f64_token_scores(int32_t t, int32_t head_dim, int32_t input, const double* keys, int64_t ldk,
+                                const double* values, int64_t ldv, const double* w1, const double* b1, const double* w2,
+                                int32_t hidden, int32_t activation, double* u, void* workspace, size_t workspace_bytes,
+                                lkv_stream_t stream);
+/* hard_topk / inference_select (soft_topk.cpp:191-201) on fp64 scores [n_heads][ld], one budget
+ * per head: the budgets[h] largest of the first t scores (ties -> lowest index, -0.0 == +0.0),
+ * positions written ascending at out->offsets[h], out->lens[h] = budgets[h].  Budget outside
+ * [0, t] -> BUDGET, NaN -> NUMERIC (latched).  Rows are gathered by lkv_compact (LKV_F64). */
+lkv_status lkv_f64_select(const double* scores, int32_t n_heads, int32_t t, int64_t ld, const int32_t* budgets,
+                          const lkv_ragged_desc* out, void* workspace, size_t workspace_bytes, lkv_stream_t stream);
 
 /* ---- K/V production for layer-by-layer prefill (the step before the path) -------- */
 /* cos/sin table [t_max][head_dim/2] of float2 (cos, sin) for positions pos_offset + p,

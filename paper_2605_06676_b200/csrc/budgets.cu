@@ -186,9 +186,13 @@ __global__ void __launch_bounds__(kBudgetThreads, 1) budgets_kernel(const Budget
     __syncthreads();
 
     // -- load + validate (solve_threshold :61-64: first offending element decides)
+    // (soft_topk_forward solves on x / tau, soft_topk.cpp:140-143; the unscaled scores stay in
+    // `rem` for the output permutation, which sorts them, :152-156)
     for (int i = tid; i < n; i += kBudgetThreads) {
-        const double v = p.logits[i];
+        const double raw = p.logits[i];
+        const double v = p.soft ? raw / p.tau : raw;
         x[i] = v;
+        if (p.soft) rem[i] = raw;
         if (!isfinite(v) || fabs(v) > 1e300) atomicMin(&s_first_bad, i);
     }
     __syncthreads();
@@ -203,8 +207,8 @@ __global__ void __launch_bounds__(kBudgetThreads, 1) budgets_kernel(const Budget
         if (s_first_bad != INT_MAX) return;
     }
 
-    // -- k = R * n, clamp_budget (:27-33)
-    const double k = p.R * n;
+    // -- k = R * n (allocate_budgets, policy.cpp:118) or given (soft_topk_forward), clamp_budget (:27-33)
+    const double k = p.soft ? p.k_abs : p.R * n;
     if (tid == 0) {
         if (!(k > 0.0) || !(k < (double)n)) {
             latch_error(p.err, LKV_ERR_BUDGET, 0);
@@ -219,8 +223,20 @@ __global__ void __launch_bounds__(kBudgetThreads, 1) budgets_kernel(const Budget
     const double kc = s_kc;
 
     if (n == 1) {  // soft_topk_forward :119-131: the single output is the clamped budget
-        if (tid == 0) r[0] = kc;
+        if (tid == 0) {
+            r[0] = kc;
+            if (p.soft) {
+                const double z = kc >= 0.5 ? -log(2.0 * (1.0 - kc)) : log(2.0 * kc);
+                if (p.lambda_out) *p.lambda_out = rem[0] / p.tau - z;
+                if (p.m_out) *p.m_out = kc >= 0.5 ? 1 : 0;
+                if (p.kc_out) *p.kc_out = kc;
+                if (p.density_out) p.density_out[0] = std_max(0.5 * exp(-fabs(z)), DBL_MIN);
+                if (p.perm_out) p.perm_out[0] = 0;
+                if (p.ratios_out) p.ratios_out[0] = kc;
+            }
+        }
         __syncthreads();
+        if (p.soft) return;
     } else {
         // -- stable descending sort in rank form: ties keep input order
         for (int i = tid; i < n; i += kBudgetThreads) {
@@ -291,6 +307,7 @@ __global__ void __launch_bounds__(kBudgetThreads, 1) budgets_kernel(const Budget
         } else if (tid == 0) {
             const int m = s_first_ok;
             s_lambda = candidate_lambda(m, n, kc, l1[m], l2[m]);
+            s_best_m = m;
         }
         __syncthreads();
         if (s_fail) return;
@@ -313,6 +330,24 @@ __global__ void __launch_bounds__(kBudgetThreads, 1) budgets_kernel(const Budget
         }
         __syncthreads();
         if (s_fail) return;
+        if (p.soft) {  // soft_topk_forward's remaining outputs (:139-156)
+            if (tid == 0) {
+                if (p.lambda_out) *p.lambda_out = lambda;
+                if (p.m_out) *p.m_out = s_best_m;
+                if (p.kc_out) *p.kc_out = kc;
+            }
+            for (int i = tid; i < n; i += kBudgetThreads) {
+                if (p.ratios_out) p.ratios_out[i] = r[i];
+                if (p.density_out) p.density_out[i] = std_max(0.5 * exp(-fabs(x[i] - lambda)), DBL_MIN);
+                if (p.perm_out) {  // stable descending order of the unscaled scores
+                    const double xi = rem[i];
+                    int rank = 0;
+                    for (int j = 0; j < n; ++j) rank += (rem[j] > xi) || (rem[j] == xi && j < i);
+                    p.perm_out[rank] = i;
+                }
+            }
+            return;
+        }
     }
     freeze_and_offsets(p, r, rem, fl, delta, &s_sum, &s_carry, s_scan);
 }

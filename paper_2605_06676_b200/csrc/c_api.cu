@@ -46,6 +46,8 @@ lkv_status cuda_fail(cudaError_t e, const char* where) {
         if (e_ != cudaSuccess) return cuda_fail(e_, where); \
     } while (0)
 
+int elem_bytes(int dtype) { return dtype == LKV_F64 ? 8 : dtype == LKV_F32 ? 4 : 2; }
+
 int num_sms() {
     int dev = 0, n = 0;
     cudaGetDevice(&dev);
@@ -111,10 +113,10 @@ lkv_status check_cache(const lkv_cache_desc* c, bool need_kv) {
     if (c->n_layers < 1 || c->n_kv_heads < 1) return fail(LKV_ERR_CONTRACT, "n_layers and n_kv_heads must be >= 1");
     if (c->head_dim < 8 || c->head_dim % 8) return fail(LKV_ERR_CONTRACT, "head_dim must be a positive multiple of 8");
     {
-        const int units = c->head_dim * (c->dtype == LKV_F32 ? 4 : 2) / 16;
+        const int units = c->head_dim * elem_bytes(c->dtype) / 16;
         if (units & (units - 1)) return fail(LKV_ERR_UNSUPPORTED, "row bytes must be a power-of-two multiple of 16");
     }
-    if (c->dtype != LKV_F32 && c->dtype != LKV_BF16) return fail(LKV_ERR_CONTRACT, "unknown dtype");
+    if (c->dtype != LKV_F32 && c->dtype != LKV_BF16 && c->dtype != LKV_F64) return fail(LKV_ERR_CONTRACT, "unknown dtype");
     if (c->max_tokens < 1) return fail(LKV_ERR_CONTRACT, "max_tokens must be >= 1");
     if (!c->seq_lens) return fail(LKV_ERR_CONTRACT, "seq_lens (host) is null");
     for (int s = 0; s < c->n_seq; ++s)
@@ -189,6 +191,7 @@ lkv_status check_ws(void* ws, size_t have, size_t need) {
 
 lkv_status check_scorer(const lkv_scorer_desc* s, const lkv_cache_desc* c) {
     if (!s) return fail(LKV_ERR_CONTRACT, "scorer descriptor is null");
+    if (c->dtype == LKV_F64) return fail(LKV_ERR_UNSUPPORTED, "fp64 caches are scored by lkv_f64_token_scores");
     if (s->input != LKV_SCORER_K && s->input != LKV_SCORER_KV) return fail(LKV_ERR_CONTRACT, "scorer input must be K or KV");
     if (s->activation != LKV_ACT_SILU && s->activation != LKV_ACT_GELU_ERF) return fail(LKV_ERR_CONTRACT, "unknown activation");
     if (s->hidden < 1 || s->hidden > 256) return fail(LKV_ERR_CONTRACT, "scorer hidden must lie in [1, 256]");
@@ -283,7 +286,7 @@ lkv_status run_select(const lkv_cache_desc* c, const float* scores, const int32_
     p.values = c->values;
     p.out_keys = out->keys;
     p.out_values = out->values;
-    p.row_bytes = c->head_dim * (c->dtype == LKV_F32 ? 4 : 2);
+    p.row_bytes = c->head_dim * elem_bytes(c->dtype);
     p.gather = gather ? 1 : 0;
     p.hist_ready = hist_ready ? 1 : 0;
     p.err = at<ErrWord>(ws, w.err);
@@ -523,6 +526,7 @@ lkv_status lkv_select(const lkv_cache_desc* c, const float* scores, const int32_
                       int32_t gather, void* ws, size_t ws_bytes, lkv_stream_t stream) {
     lkv_status st = check_cache(c, gather != 0);
     if (st) return st;
+    if (c->dtype == LKV_F64) return fail(LKV_ERR_UNSUPPORTED, "fp64 scores are selected by lkv_f64_select");
     if ((st = check_ragged(out, n_heads_of(c), c->head_dim, c->dtype, gather != 0))) return st;
     if (!scores || !budgets) return fail(LKV_ERR_CONTRACT, "scores/budgets are null");
     const EvictWs w = evict_layout(c, 1);
@@ -546,7 +550,7 @@ lkv_status lkv_compact(const lkv_cache_desc* c, const lkv_ragged_desc* out, void
     p.values = c->values;
     p.out_keys = out->keys;
     p.out_values = out->values;
-    p.row_bytes = c->head_dim * (c->dtype == LKV_F32 ? 4 : 2);
+    p.row_bytes = c->head_dim * elem_bytes(c->dtype);
     p.err = at<ErrWord>(ws, 0);  // out-of-range positions / overrun heads -> contract_error
     LKV_CUDA(launch_compact(p, (int)n_heads_of(c), (cudaStream_t)stream), "compact");
     return LKV_OK;
@@ -570,7 +574,7 @@ static lkv_status trace_params(const lkv_cache_desc* c, const int32_t* masks, in
     p->mask_ld = mask_ld;
     p->chunk_cnt = at<uint32_t>(ws, w.chunk_out);
     p->err = at<ErrWord>(ws, w.err);
-    p->row_bytes = c->head_dim * (c->dtype == LKV_F32 ? 4 : 2);
+    p->row_bytes = c->head_dim * elem_bytes(c->dtype);
     return LKV_OK;
 }
 
@@ -724,7 +728,7 @@ static lkv_status evict_host_impl(const lkv_cache_desc* hc, void* dev_keys, void
     cudaStream_t strm = (cudaStream_t)stream;
     cudaStream_t side = side_stream(), cs = copy_stream(), ds = d2h_stream();
     if (!side || !cs || !ds) return fail(LKV_ERR_CUDA, "helper stream creation failed");
-    const size_t esz = hc->dtype == LKV_F32 ? 4 : 2;
+    const size_t esz = elem_bytes(hc->dtype);
     const size_t rowb = (size_t)hc->head_dim * esz;
     const size_t head_bytes = (size_t)hc->max_tokens * rowb;
     const int H = hc->n_kv_heads, L = hc->n_layers;
@@ -1154,6 +1158,152 @@ lkv_status lkv_decode_step(const lkv_ragged_desc* r, int32_t n_seq, int32_t n_la
         if ((st = make_map_bf16(&mv, r->values, 128, (uint64_t)r->capacity_rows, 64))) return st;
     }
     LKV_CUDA(launch_decode(p, r->dtype, &mk, &mv, num_sms(), (cudaStream_t)stream), "decode");
+    return LKV_OK;
+}
+
+// ---- fp64 reference-precision operators (the declaration-compatible include/lkv API) ------------
+lkv_status lkv_soft_topk_exact(const double* x, int32_t n, double k, double tau, double* values, double* density,
+                               int32_t* permutation, double* lambda, int32_t* split_m, double* clamped_k, void* ws,
+                               size_t ws_bytes, lkv_stream_t stream) {
+    if (!(tau > 0.0)) return fail(LKV_ERR_CONTRACT, "soft_topk_forward: tau must be positive");  // soft_topk.cpp:112
+    if (n < 1) return fail(LKV_ERR_CONTRACT, "soft_topk_forward: empty scores");               // :114
+    if (n > 3072) return fail(LKV_ERR_UNSUPPORTED, "soft_topk_exact: n <= 3072");
+    if (!x || !values) return fail(LKV_ERR_CONTRACT, "soft_topk_exact: null buffer");
+    lkv_status st = check_ws(ws, ws_bytes, sizeof(ErrWord));
+    if (st) return st;
+    BudgetParams p;
+    memset(&p, 0, sizeof p);
+    p.logits = x;
+    p.n = n;
+    p.mode = LKV_BUDGET_FLOOR;
+    p.n_seq = 1;
+    p.seq_len[0] = 1;
+    p.soft = 1;
+    p.k_abs = k;
+    p.tau = tau;
+    p.ratios_out = values;
+    p.density_out = density;
+    p.perm_out = permutation;
+    p.lambda_out = lambda;
+    p.m_out = split_m;
+    p.kc_out = clamped_k;
+    p.err = at<ErrWord>(ws, 0);
+    LKV_CUDA(launch_budgets(p, (cudaStream_t)stream), "soft topk exact");
+    return LKV_OK;
+}
+
+lkv_status lkv_f64_gemm(int32_t M, int32_t N, int32_t K, const double* A, int64_t lda, const double* B, int64_t ldb,
+                        double* C, int64_t ldc, int32_t accumulate, lkv_stream_t stream) {
+    if (M < 0 || N < 0 || K < 1 || !A || !B || !C || lda < K || ldb < N || ldc < N)
+        return fail(LKV_ERR_CONTRACT, "f64 gemm: bad extents");
+    F64GemmParams p{M, N, K, A, lda, B, ldb, C, ldc, accumulate ? 1 : 0};
+    LKV_CUDA(launch_f64_gemm(p, (cudaStream_t)stream), "f64 gemm");
+    return LKV_OK;
+}
+
+lkv_status lkv_f64_rmsnorm(int32_t rows, int32_t cols, const double* x, int64_t ldx, const double* gain, double eps,
+                           double* out, int64_t ldo, lkv_stream_t stream) {
+    if (rows < 0 || cols < 1 || !x || !gain || !out || ldx < cols || ldo < cols || !(eps > 0.0))
+        return fail(LKV_ERR_CONTRACT, "f64 rmsnorm: bad arguments");
+    LKV_CUDA(launch_f64_rmsnorm(rows, cols, x, ldx, gain, eps, out, ldo, (cudaStream_t)stream), "f64 rmsnorm");
+    return LKV_OK;
+}
+
+lkv_status lkv_f64_rope(int32_t rows, int32_t n_heads, int32_t head_dim, double* x, int64_t ldx, int32_t pos0,
+                        double base, lkv_stream_t stream) {
+    if (head_dim % 2) return fail(LKV_ERR_CONTRACT, "rope: last dim must be even");  // tensor.cpp:588
+    if (rows < 0 || n_heads < 1 || head_dim < 2 || !x || ldx < (int64_t)n_heads * head_dim || pos0 < 0 || !(base > 0.0))
+        return fail(LKV_ERR_CONTRACT, "f64 rope: bad arguments");
+    LKV_CUDA(launch_f64_rope(rows, n_heads, head_dim, x, ldx, pos0, base, (cudaStream_t)stream), "f64 rope");
+    return LKV_OK;
+}
+
+lkv_status lkv_f64_attention(const lkv_f64_attn_desc* a, void* ws, size_t ws_bytes, lkv_stream_t stream) {
+    if (!a) return fail(LKV_ERR_CONTRACT, "attention descriptor is null");
+    if (a->n_q_heads < 1 || a->n_q < 1 || a->t < 1 || a->head_dim < 1 || a->group < 1)
+        return fail(LKV_ERR_CONTRACT, "attention: empty extents");  // attention.cpp:34
+    if (a->head_dim > 256) return fail(LKV_ERR_UNSUPPORTED, "f64 attention: head_dim <= 256");
+    if (a->causal && a->query_pos_offset + 1 < 1) return fail(LKV_ERR_CONTRACT, "attention: first query row admits no key");
+    if (!a->q || !a->k || !a->v || !a->out) return fail(LKV_ERR_CONTRACT, "attention: null buffer");
+    lkv_status st = check_ws(ws, ws_bytes, sizeof(ErrWord));
+    if (st) return st;
+    F64AttnParams p;
+    memset(&p, 0, sizeof p);
+    p.n_qh = a->n_q_heads;
+    p.G = a->group;
+    p.n_q = a->n_q;
+    p.t = a->t;
+    p.d = a->head_dim;
+    p.q = a->q;
+    p.ldq = a->ldq;
+    p.k = a->k;
+    p.v = a->v;
+    p.ldk = a->ldkv;
+    p.mask = a->mask;
+    p.mask_ld = a->mask_ld;
+    p.causal = a->causal;
+    p.qpo = a->query_pos_offset;
+    p.self_keep = a->self_always_retained;
+    p.scale = a->scale;
+    p.out = a->out;
+    p.ldo = a->ldo;
+    p.p_raw = a->p_raw;
+    p.p = a->p;
+    p.renorm = a->renorm;
+    p.err = at<ErrWord>(ws, 0);
+    LKV_CUDA(launch_f64_attention(p, (cudaStream_t)stream), "f64 attention");
+    return LKV_OK;
+}
+
+lkv_status lkv_f64_swiglu(int64_t n, const double* gate, const double* up, double* out, lkv_stream_t stream) {
+    if (n < 0 || !gate || !up || !out) return fail(LKV_ERR_CONTRACT, "f64 swiglu: bad arguments");
+    LKV_CUDA(launch_f64_swiglu(n, gate, up, out, (cudaStream_t)stream), "f64 swiglu");
+    return LKV_OK;
+}
+
+lkv_status lkv_f64_embed(const int32_t* tokens, int32_t n, const double* table, int32_t d_model, int32_t vocab,
+                         double* out, void* ws, size_t ws_bytes, lkv_stream_t stream) {
+    if (n < 0 || d_model < 1 || vocab < 1 || !tokens || !table || !out) return fail(LKV_ERR_CONTRACT, "f64 embed: bad arguments");
+    lkv_status st = check_ws(ws, ws_bytes, sizeof(ErrWord));
+    if (st) return st;
+    LKV_CUDA(launch_f64_embed(tokens, n, table, d_model, vocab, out, at<ErrWord>(ws, 0), (cudaStream_t)stream), "f64 embed");
+    return LKV_OK;
+}
+
+lkv_status lkv_f64_split_heads(int32_t t, int32_t n_heads, int32_t head_dim, const double* x, int64_t ldx, double* out,
+                               int64_t out_rows, lkv_stream_t stream) {
+    if (t < 0 || n_heads < 1 || head_dim < 1 || !x || !out || ldx < (int64_t)n_heads * head_dim || out_rows < t)
+        return fail(LKV_ERR_CONTRACT, "f64 split_heads: bad arguments");
+    LKV_CUDA(launch_f64_split_heads(t, n_heads, head_dim, x, ldx, out, out_rows, (cudaStream_t)stream), "f64 split");
+    return LKV_OK;
+}
+
+lkv_status lkv_f64_token_scores(int32_t t, int32_t head_dim, int32_t input, const double* keys, int64_t ldk,
+                                const double* values, int64_t ldv, const double* w1, const double* b1, const double* w2,
+                                int32_t hidden, int32_t activation, double* u, void* ws, size_t ws_bytes,
+                                lkv_stream_t stream) {
+    if (input != LKV_SCORER_K && input != LKV_SCORER_KV) return fail(LKV_ERR_CONTRACT, "scorer input must be K or KV");
+    if (activation != LKV_ACT_SILU && activation != LKV_ACT_GELU_ERF) return fail(LKV_ERR_CONTRACT, "unknown activation");
+    if (t < 0 || head_dim < 1 || hidden < 1 || !keys || !w1 || !b1 || !w2 || !u || ldk < head_dim ||
+        (input == LKV_SCORER_KV && (!values || ldv < head_dim)))
+        return fail(LKV_ERR_CONTRACT, "token_scores: bad arguments");
+    if (f64_scorer_smem(input * head_dim, hidden) > 200 * 1024) return fail(LKV_ERR_UNSUPPORTED, "f64 scorer too large");
+    lkv_status st = check_ws(ws, ws_bytes, sizeof(ErrWord));
+    if (st) return st;
+    F64ScorerParams p{t, head_dim, input, hidden, activation, keys, ldk, values, ldv, w1, b1, w2, u, at<ErrWord>(ws, 0)};
+    LKV_CUDA(launch_f64_scorer(p, (cudaStream_t)stream), "f64 scorer");
+    return LKV_OK;
+}
+
+lkv_status lkv_f64_select(const double* scores, int32_t n_heads, int32_t t, int64_t ld, const int32_t* budgets,
+                          const lkv_ragged_desc* out, void* ws, size_t ws_bytes, lkv_stream_t stream) {
+    if (!scores || !budgets || !out || !out->offsets || !out->lens || !out->positions || n_heads < 1 || t < 0 || ld < t)
+        return fail(LKV_ERR_CONTRACT, "f64 select: bad arguments");
+    if (out->n_heads != n_heads) return fail(LKV_ERR_CONTRACT, "ragged n_heads mismatch");
+    lkv_status st = check_ws(ws, ws_bytes, sizeof(ErrWord));
+    if (st) return st;
+    F64SelectParams p{t, ld, scores, budgets, out->offsets, out->positions, out->lens, at<ErrWord>(ws, 0)};
+    LKV_CUDA(launch_f64_select(p, n_heads, (cudaStream_t)stream), "f64 select");
     return LKV_OK;
 }
 

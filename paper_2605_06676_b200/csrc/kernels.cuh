@@ -27,6 +27,15 @@ struct BudgetParams {
     int32_t local_begin;
     int32_t local_count;
     int32_t* budgets_local_out;
+    // soft = 1: soft_topk_forward / solve_threshold (soft_topk.cpp:58-164) with k and tau given:
+    // the solve runs on logits / tau, values go to ratios_out, nothing is frozen
+    int32_t soft;
+    double k_abs, tau;
+    double* lambda_out;
+    int32_t* m_out;
+    double* kc_out;
+    double* density_out;
+    int32_t* perm_out;
     int32_t seq_len[LKV_MAX_SEQ];
 };
 cudaError_t launch_budgets(const BudgetParams& p, cudaStream_t stream);
@@ -266,6 +275,70 @@ cudaError_t launch_embed(const void* tok_embed, int dtype, const int32_t* tokens
 cudaError_t launch_pack_weight(const void* src, int dtype, int K, int cols, int col_mode, int col_off, int NG, int KU,
                                void* dst, cudaStream_t stream);
 cudaError_t launch_to_f32(const void* src, int dtype, int n, float* dst, cudaStream_t stream);
+// ---- f64.cu (reference-precision operators behind include/lkv/*.hpp)
+struct F64GemmParams {
+    int32_t M, N, K;
+    const double* A;
+    int64_t lda;
+    const double* B;
+    int64_t ldb;
+    double* C;
+    int64_t ldc;
+    int32_t accumulate;  // C = C + A B (the sum is formed first, then added)
+};
+struct F64AttnParams {
+    int32_t n_qh, G, n_q, t, d;  // query heads (kv head = h / G), query rows, keys, head width (<= 256)
+    const double* q;             // row r, head h at q[r * ldq + h * d]
+    int64_t ldq;
+    const double* k;             // key j of kv head g at k[j * ldk + g * d]
+    const double* v;
+    int64_t ldk;
+    const double* mask;          // nullable; kv head g's mask at mask[g * mask_ld + j]
+    int64_t mask_ld;
+    int32_t causal, qpo, self_keep;
+    double scale;
+    double* out;                 // row r, head h at out[r * ldo + h * d]
+    int64_t ldo;
+    double* p_raw;               // nullable [n_qh][n_q][t]
+    double* p;                   // nullable [n_qh][n_q][t]
+    double* renorm;              // nullable [n_qh][n_q]
+    ErrWord* err;
+};
+struct F64ScorerParams {
+    int32_t t, d, in_mode, hidden, act;
+    const double* k;
+    int64_t ldk;
+    const double* v;
+    int64_t ldv;
+    const double* w1;  // [in][hidden] (the reference layout, policy.hpp:25)
+    const double* b1;
+    const double* w2;
+    double* u;
+    ErrWord* err;
+};
+struct F64SelectParams {
+    int32_t t;
+    int64_t ld;
+    const double* scores;    // [n_heads][ld]
+    const int32_t* budgets;  // [n_heads]
+    const int64_t* offsets;  // [n_heads + 1]
+    int32_t* positions;
+    int32_t* lens;
+    ErrWord* err;
+};
+cudaError_t launch_f64_gemm(const F64GemmParams& p, cudaStream_t s);
+cudaError_t launch_f64_rmsnorm(int rows, int cols, const double* x, int64_t ldx, const double* gain, double eps,
+                               double* out, int64_t ldo, cudaStream_t s);
+cudaError_t launch_f64_rope(int rows, int n_heads, int d, double* x, int64_t ldx, int pos0, double base, cudaStream_t s);
+cudaError_t launch_f64_attention(const F64AttnParams& p, cudaStream_t s);
+cudaError_t launch_f64_swiglu(int64_t n, const double* gate, const double* up, double* out, cudaStream_t s);
+cudaError_t launch_f64_embed(const int32_t* tokens, int n, const double* table, int dm, int vocab, double* out,
+                             ErrWord* err, cudaStream_t s);
+cudaError_t launch_f64_split_heads(int t, int H, int d, const double* x, int64_t ldx, double* out, int64_t T,
+                                   cudaStream_t s);
+size_t f64_scorer_smem(int in, int hidden);
+cudaError_t launch_f64_scorer(const F64ScorerParams& p, cudaStream_t s);
+cudaError_t launch_f64_select(const F64SelectParams& p, int n_heads, cudaStream_t s);
 // ---- rope.cu (layer-by-layer prefill: K/V production)
 cudaError_t launch_rope_table(int t_max, int head_dim, double base, int pos_offset, float2* cs, cudaStream_t stream);
 cudaError_t launch_rope_pack(const void* k_lin, const void* v_lin, int n_seq, int t_max, const int32_t* seq_lens,
