@@ -30,7 +30,9 @@ EXPORTED = [
     "lkv_comm_init", "lkv_comm_destroy", "lkv_comm_size", "lkv_comm_rank", "lkv_comm_allgatherv", "lkv_comm_gatherv",
     "lkv_attn_workspace_bytes", "lkv_masked_attention_fwd", "lkv_masked_attention_bwd", "lkv_soft_topk_fwd",
     "lkv_soft_topk_vjp", "lkv_evict_budgets", "lkv_mask_counts", "lkv_cache_from_trace", "lkv_decode_plan_ex",
-    "lkv_model_plan_ex", "lkv_decode_plan_info", "lkv_evict_host_shard",
+    "lkv_model_plan_ex", "lkv_decode_plan_info", "lkv_evict_host_shard", "lkv_soft_topk_exact", "lkv_f64_gemm",
+    "lkv_f64_rmsnorm", "lkv_f64_rope", "lkv_f64_attention", "lkv_f64_swiglu", "lkv_f64_embed", "lkv_f64_split_heads",
+    "lkv_f64_token_scores", "lkv_f64_select",
 ]
 
 
@@ -56,6 +58,15 @@ class AttnDesc(C.Structure):
     _fields_ = [("batch", C.c_int32), ("n_q_heads", C.c_int32), ("n_kv_heads", C.c_int32), ("t_q", C.c_int32),
                 ("t_k", C.c_int32), ("head_dim", C.c_int32), ("dtype", C.c_int32), ("causal", C.c_int32),
                 ("query_pos_offset", C.c_int32), ("self_always_retained", C.c_int32), ("scale", C.c_double)]
+
+
+class F64AttnDesc(C.Structure):
+    _fields_ = [("n_q_heads", C.c_int32), ("group", C.c_int32), ("n_q", C.c_int32), ("t", C.c_int32),
+                ("head_dim", C.c_int32), ("causal", C.c_int32), ("query_pos_offset", C.c_int32),
+                ("self_always_retained", C.c_int32), ("scale", C.c_double), ("q", C.c_void_p), ("ldq", C.c_int64),
+                ("k", C.c_void_p), ("v", C.c_void_p), ("ldkv", C.c_int64), ("mask", C.c_void_p),
+                ("mask_ld", C.c_int64), ("out", C.c_void_p), ("ldo", C.c_int64), ("p_raw", C.c_void_p),
+                ("p", C.c_void_p), ("renorm", C.c_void_p)]
 
 
 class ModelDesc(C.Structure):
@@ -108,6 +119,19 @@ def load():
     L.lkv_evict_host_shard.argtypes = [P(CacheDesc), vp, vp, P(ScorerDesc), vp, i32, i32, dbl, i32, P(RaggedDesc),
                                        P(RaggedDesc), i32, vp, sz, vp]
     L.lkv_evict_host_shard.restype = C.c_int
+    L.lkv_soft_topk_exact.argtypes = [vp, i32, dbl, dbl, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+    L.lkv_f64_gemm.argtypes = [i32, i32, i32, vp, i64, vp, i64, vp, i64, i32, vp]
+    L.lkv_f64_rmsnorm.argtypes = [i32, i32, vp, i64, vp, dbl, vp, i64, vp]
+    L.lkv_f64_rope.argtypes = [i32, i32, i32, vp, i64, i32, dbl, vp]
+    L.lkv_f64_attention.argtypes = [P(F64AttnDesc), vp, sz, vp]
+    L.lkv_f64_swiglu.argtypes = [i64, vp, vp, vp, vp]
+    L.lkv_f64_embed.argtypes = [vp, i32, vp, i32, i32, vp, vp, sz, vp]
+    L.lkv_f64_split_heads.argtypes = [i32, i32, i32, vp, i64, vp, i64, vp]
+    L.lkv_f64_token_scores.argtypes = [i32, i32, i32, vp, i64, vp, i64, vp, vp, vp, i32, i32, vp, vp, sz, vp]
+    L.lkv_f64_select.argtypes = [vp, i32, i32, i64, vp, P(RaggedDesc), vp, sz, vp]
+    for name in ["lkv_soft_topk_exact", "lkv_f64_gemm", "lkv_f64_rmsnorm", "lkv_f64_rope", "lkv_f64_attention",
+                 "lkv_f64_swiglu", "lkv_f64_embed", "lkv_f64_split_heads", "lkv_f64_token_scores", "lkv_f64_select"]:
+        getattr(L, name).restype = C.c_int
     L.lkv_rope_table.argtypes = [i32, i32, dbl, i32, vp, vp]
     L.lkv_rope_pack.argtypes = [vp, vp, P(CacheDesc), vp, vp, vp, vp]
     L.lkv_decode_workspace_bytes.restype = sz
