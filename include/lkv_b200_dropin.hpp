@@ -161,8 +161,15 @@ struct LkvParams {
     std::vector<Mlp2> token_scorers;      // one per (l, h): 2 d_head -> d_head -> 1
 };
 LkvParams load_lkv_params(const std::string& path);
-// policy.cpp:106-108 -- the LKV-H logits (fp64 host setup, once per checkpoint)
+// policy.cpp:106-108 -- the LKV-H logits (fp64 scorer on the device)
 std::vector<double> head_scores(const LkvParams& params);
+// the reference's tensor container (container.cpp:45-137): 8-byte LE metadata length, JSON
+// metadata, f64 / f32 payloads; every tensor comes back as fp64
+struct ContainerTensor {
+    std::vector<int> shape;
+    std::vector<double> v;
+};
+std::vector<std::pair<std::string, ContainerTensor>> read_container(const std::string& path);
 
 // ---- training-time operators -----------------------------------------------
 // soft_topk.hpp:36-44 / :60-67 -- values sum to the clamped k; the saved density terms feed the VJP.

@@ -31,7 +31,7 @@ _REF_PATH = os.path.join(_HERE, "_ref", "liblkv_ref.so")
 _FAST_PATH = os.path.join(_HERE, "liblkv_oracle_fast.so")
 
 OK, CONTRACT, NUMERIC, BUDGET, OVERFLOW_GUARD, DEGENERATE_MASK = range(6)
-F32, BF16 = 0, 1
+F32, BF16, F64 = 0, 1, 2
 SILU, GELU_ERF = 0, 1
 
 
@@ -257,7 +257,10 @@ def token_scores(keys, values, w1, b1, w2, act: int = SILU, dtype: int | None = 
             dtype = BF16
         else:
             dtype = F32
-            keys = np.ascontiguousarray(keys, dtype=np.float32)
+    if dtype == F32:
+        keys = np.ascontiguousarray(keys, dtype=np.float32)
+    elif dtype == F64:
+        keys = np.ascontiguousarray(keys, dtype=np.float64)
     t, d = keys.shape
     in_mode = 1
     vptr = None

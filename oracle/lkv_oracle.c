@@ -567,6 +567,7 @@ int lkvo_freeze_budgets_exact(const double* ratios, int n, double target_ratio, 
 }
 
 static inline double widen(int dtype, const void* p, int64_t i) {
+    if (dtype == LKVO_F64) return ((const double*)p)[i];
     if (dtype == LKVO_F32) return (double)((const float*)p)[i];
     uint32_t bits = (uint32_t)((const uint16_t*)p)[i] << 16;
     float f;

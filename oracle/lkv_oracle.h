@@ -36,7 +36,7 @@ enum {
     LKVO_DEGENERATE_MASK = 5
 };
 
-enum { LKVO_F32 = 0, LKVO_BF16 = 1 };
+enum { LKVO_F32 = 0, LKVO_BF16 = 1, LKVO_F64 = 2 /* fp64 inputs (the reference API's own precision) */ };
 enum { LKVO_SILU = 0, LKVO_GELU_ERF = 1 };
 
 /* ---- rng.hpp:11-66 (mt19937_64 + hand-rolled conversions) -------------- */

@@ -22,6 +22,7 @@
 #pragma GCC visibility push(default)  // the reference API is exported from the -fvisibility=hidden library
 #endif
 #include "../../include/lkv/attention.hpp"
+#include "../../include/lkv/checkpoint.hpp"
 #include "../../include/lkv/errors.hpp"
 #include "../../include/lkv/evictsim.hpp"
 #include "../../include/lkv/policy.hpp"
@@ -29,6 +30,7 @@
 #include "../../include/lkv/soft_topk.hpp"
 #include "../../include/lkv/tensor.hpp"
 #include "../../include/lkv_b200.h"
+#include "../../include/lkv_b200_dropin.hpp"
 
 namespace lkv {
 
@@ -1184,6 +1186,114 @@ std::pair<KvCache, SimReport> prefill_with_eviction(const ModelWeights& weights,
     rep.kv_bytes_compressed = mr.compressed_bytes;
     rep.reduction = mr.reduction_factor;
     return {std::move(cache), std::move(rep)};
+}
+
+// ============================ checkpoint.hpp ====================================================
+namespace {
+constexpr double kCkptVersion = 1.0;  // checkpoint.cpp:12
+
+// container writer (container.cpp:45-76): u64 LE metadata length, compact JSON object of
+// {"name": {"dtype": "f64", "shape": [...], "byte_offset": o, "byte_length": n}} in entry order,
+// then the f64 payloads back to back
+void write_container(const std::string& path, const std::vector<std::pair<std::string, const Tensor*>>& entries) {
+    std::string meta = "{";
+    uint64_t off = 0;
+    for (size_t i = 0; i < entries.size(); ++i) {
+        const Tensor& t = *entries[i].second;
+        if (!t.defined()) throw contract_error("container: undefined tensor " + entries[i].first);
+        for (size_t j = 0; j < i; ++j)
+            if (entries[j].first == entries[i].first) throw contract_error("container: duplicate tensor name " + entries[i].first);
+        std::string shape = "[";
+        for (size_t d = 0; d < t.shape().size(); ++d) shape += (d ? "," : "") + std::to_string(t.shape()[d]);
+        shape += "]";
+        const uint64_t len = t.numel() * 8;
+        meta += (i ? ",\"" : "\"") + entries[i].first + "\":{\"dtype\":\"f64\",\"shape\":" + shape +
+                ",\"byte_offset\":" + std::to_string(off) + ",\"byte_length\":" + std::to_string(len) + "}";
+        off += len;
+    }
+    meta += "}";
+    FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) throw contract_error("container: cannot open for writing: " + path);
+    unsigned char hdr[8];
+    for (int i = 0; i < 8; ++i) hdr[i] = static_cast<unsigned char>((uint64_t)meta.size() >> (8 * i));
+    bool ok = std::fwrite(hdr, 1, 8, f) == 8 && std::fwrite(meta.data(), 1, meta.size(), f) == meta.size();
+    for (const auto& e : entries)
+        ok = ok && std::fwrite(e.second->data(), 8, e.second->numel(), f) == e.second->numel();
+    ok = (std::fclose(f) == 0) && ok;
+    if (!ok) throw contract_error("container: write failed: " + path);
+}
+
+std::vector<std::pair<std::string, b200::ContainerTensor>> read(const std::string& path) {
+    try {
+        return b200::read_container(path);
+    } catch (const b200::contract_error& e) {
+        throw contract_error(std::string(e.what()).substr(10));  // same "contract: " taxonomy
+    }
+}
+const b200::ContainerTensor& at(const std::vector<std::pair<std::string, b200::ContainerTensor>>& c,
+                                const std::string& name) {
+    for (const auto& e : c)
+        if (e.first == name) return e.second;
+    throw contract_error("container: missing tensor " + name);
+}
+}  // namespace
+
+void save_model(const std::string& path, const ModelWeights& weights) {  // checkpoint.cpp:16-29
+    const ModelConfig& c = weights.config;
+    Tensor meta = make({9}, {kCkptVersion, (double)c.n_layers, (double)c.n_query_heads, (double)c.n_kv_heads,
+                             (double)c.head_dim, (double)c.vocab_size, (double)c.max_seq_len, (double)c.mlp_hidden,
+                             weights.frozen ? 1.0 : 0.0});
+    std::vector<std::pair<std::string, const Tensor*>> e{{"__meta", &meta}};
+    for (auto& nt : const_cast<ModelWeights&>(weights).named_params()) e.emplace_back(nt.first, nt.second);
+    write_container(path, e);
+}
+
+ModelWeights load_model(const std::string& path) {  // checkpoint.cpp:31-52
+    const auto c = read(path);
+    const auto& meta = at(c, "__meta");
+    if (meta.v.size() != 9 || meta.v[0] != kCkptVersion) throw contract_error("model checkpoint: unsupported metadata");
+    ModelConfig cfg;
+    cfg.n_layers = (int)meta.v[1];
+    cfg.n_query_heads = (int)meta.v[2];
+    cfg.n_kv_heads = (int)meta.v[3];
+    cfg.head_dim = (int)meta.v[4];
+    cfg.vocab_size = (int)meta.v[5];
+    cfg.max_seq_len = (int)meta.v[6];
+    cfg.mlp_hidden = (int)meta.v[7];
+    ModelWeights w = init_model(cfg);
+    for (auto& nt : w.named_params()) {
+        const auto& t = at(c, nt.first);
+        if (t.shape != nt.second->shape()) throw contract_error("model checkpoint: shape mismatch for " + nt.first);
+        *nt.second = make(t.shape, t.v);
+    }
+    w.frozen = meta.v[8] != 0.0;
+    return w;
+}
+
+void save_lkv_params(const std::string& path, const LkvParams& params) {  // checkpoint.cpp:54-65
+    Tensor meta = make({5}, {kCkptVersion, (double)params.n_layers, (double)params.n_kv_heads, (double)params.d_e,
+                             (double)params.d_head});
+    std::vector<std::pair<std::string, const Tensor*>> e{{"__meta", &meta}};
+    for (auto& nt : const_cast<LkvParams&>(params).named_params()) e.emplace_back(nt.first, nt.second);
+    write_container(path, e);
+}
+
+LkvParams load_lkv_params(const std::string& path) {  // checkpoint.cpp:67-86
+    const auto c = read(path);
+    const auto& meta = at(c, "__meta");
+    if (meta.v.size() != 5 || meta.v[0] != kCkptVersion) throw contract_error("policy checkpoint: unsupported metadata");
+    ModelConfig cfg;
+    cfg.n_layers = (int)meta.v[1];
+    cfg.n_kv_heads = (int)meta.v[2];
+    cfg.head_dim = (int)meta.v[4];
+    cfg.n_query_heads = cfg.n_kv_heads;
+    LkvParams p = init_lkv_params(cfg, 0, (int)meta.v[3]);
+    for (auto& nt : p.named_params()) {
+        const auto& t = at(c, nt.first);
+        if (t.shape != nt.second->shape()) throw contract_error("policy checkpoint: shape mismatch for " + nt.first);
+        *nt.second = make(t.shape, t.v);
+    }
+    return p;
 }
 
 }  // namespace lkv

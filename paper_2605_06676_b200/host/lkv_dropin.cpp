@@ -661,12 +661,10 @@ std::vector<MetaRec> parse_meta(const std::string& js) {
     return out;
 }
 
-struct Loaded {
-    std::vector<int> shape;
-    std::vector<double> v;
-};
+using Loaded = ContainerTensor;
+}  // namespace
 
-std::vector<std::pair<std::string, Loaded>> load_container(const std::string& path) {
+std::vector<std::pair<std::string, ContainerTensor>> read_container(const std::string& path) {
     FILE* f = std::fopen(path.c_str(), "rb");
     if (!f) throw contract_error("container: cannot open: " + path);
     std::string raw;
@@ -706,6 +704,7 @@ std::vector<std::pair<std::string, Loaded>> load_container(const std::string& pa
     return out;
 }
 
+namespace {
 const Loaded& entry(const std::vector<std::pair<std::string, Loaded>>& c, const std::string& name) {
     for (const auto& e : c)
         if (e.first == name) return e.second;
@@ -722,7 +721,7 @@ Mlp2 mlp_of(const std::vector<std::pair<std::string, Loaded>>& c, const std::str
 }  // namespace
 
 LkvParams load_lkv_params(const std::string& path) {
-    const auto c = load_container(path);
+    const auto c = read_container(path);
     const Loaded& meta = entry(c, "__meta");
     if (meta.v.size() != 5 || meta.v[0] != 1.0) throw contract_error("policy checkpoint: unsupported metadata");
     LkvParams p;
@@ -740,23 +739,20 @@ LkvParams load_lkv_params(const std::string& path) {
     return p;
 }
 
-std::vector<double> head_scores(const LkvParams& p) {
+std::vector<double> head_scores(const LkvParams& p) {  // policy.cpp:106-108 on the device (fp64 scorer)
     const int n = p.n_layers * p.n_kv_heads, de = p.d_e, hid = p.head_predictor.hidden;
-    std::vector<double> out((size_t)n, 0.0), h((size_t)hid);
-    for (int r = 0; r < n; ++r) {
-        std::fill(h.begin(), h.end(), 0.0);
-        for (int i = 0; i < de; ++i) {
-            const double x = p.head_embeddings[(size_t)r * de + i];
-            for (int j = 0; j < hid; ++j) h[(size_t)j] += x * p.head_predictor.w1[(size_t)i * hid + j];
-        }
-        double s = 0.0;
-        for (int j = 0; j < hid; ++j) {
-            const double v = h[(size_t)j] + p.head_predictor.b1[(size_t)j];
-            s += v / (1.0 + std::exp(-v)) * p.head_predictor.w2[(size_t)j];
-        }
-        out[(size_t)r] = s;
-    }
-    return out;
+    if ((int)p.head_embeddings.size() != n * de) throw contract_error("head_scores: embedding table size mismatch");
+    Dev E = upload(p.head_embeddings.data(), p.head_embeddings.size());
+    Dev W1 = upload(p.head_predictor.w1.data(), p.head_predictor.w1.size());
+    Dev B1 = upload(p.head_predictor.b1.data(), p.head_predictor.b1.size());
+    Dev W2 = upload(p.head_predictor.w2.data(), p.head_predictor.w2.size());
+    Dev U(sizeof(double) * (size_t)n);
+    Workspace ws(256);
+    check(lkv_f64_token_scores(n, de, LKV_SCORER_K, E.as<double>(), de, nullptr, 0, W1.as<double>(), B1.as<double>(),
+                               W2.as<double>(), hid, LKV_ACT_SILU, U.as<double>(), ws.ptr(), ws.bytes, (lkv_stream_t)stream()),
+          "head_scores");
+    ws.status("head_scores");
+    return download<double>(U, (size_t)n);
 }
 
 // ---- evictsim.cpp:56-81 (accounting) ------------------------------------------------------------------------

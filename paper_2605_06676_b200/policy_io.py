@@ -8,9 +8,9 @@ then the payloads back to back (f64, or f32 widened to f64 on load).  The policy
 `head_predictor.{w1,b1,w2}` (d_e -> d_e/2 -> 1) and `token_scorers.<i>.{w1,b1,w2}`
 (2 d_head -> d_head -> 1, one per (layer, kv head), policy.hpp:34-47).
 
-`head_scores` (policy.cpp:106-108) is policy setup -- L*H scalars computed once per
-checkpoint -- and is evaluated here in fp64 with the reference's formula, so the LKV-H
-logits handed to the device K2 kernel are the reference's own to the last few ulps.
+`head_scores` (policy.cpp:106-108) runs the head predictor on the device in fp64
+(lkv_f64_token_scores: silu(E W1 + b1) w2, mlp2_forward policy.cpp:30-34), so the LKV-H logits
+handed to K2 are the reference's own to the last few ulps.
 """
 from __future__ import annotations
 
@@ -103,11 +103,28 @@ def load_lkv_params(path: str) -> LkvParams:
     return p
 
 
-def head_scores(p: LkvParams) -> np.ndarray:
-    """policy.cpp:106-108: silu(E W1 + b1) w2 (mlp2_forward, policy.cpp:30-34), fp64."""
-    h = p.head_embeddings @ p.head_predictor.w1 + p.head_predictor.b1
-    h = h / (1.0 + np.exp(-h))
-    return h @ p.head_predictor.w2
+def head_scores(p: LkvParams, device="cuda"):
+    """policy.cpp:106-108: silu(E W1 + b1) w2 (mlp2_forward, policy.cpp:30-34), fp64 on the
+    device (lkv_f64_token_scores).  Returns a device fp64 tensor [L*H]."""
+    import ctypes as C
+
+    import torch
+
+    from . import SCORER_K, Workspace, _check, _ptr, _stream, lib
+
+    def dev(a):
+        return torch.tensor(np.ascontiguousarray(a, dtype=np.float64), device=device)
+
+    E, W1, B1, W2 = (dev(x) for x in (p.head_embeddings, p.head_predictor.w1, p.head_predictor.b1,
+                                      p.head_predictor.w2))
+    n, de = E.shape
+    hidden = W1.shape[1]
+    u = torch.empty(n, dtype=torch.float64, device=device)
+    ws = Workspace(256, device=device)
+    _check(lib().lkv_f64_token_scores(n, de, SCORER_K, _ptr(E), de, None, 0, _ptr(W1), _ptr(B1), _ptr(W2), hidden,
+                                      SILU, _ptr(u), C.c_void_p(ws.ptr), ws.nbytes, _stream()))
+    ws.status()
+    return u
 
 
 def scorers_from_params(p: LkvParams, dtype=None, device="cuda") -> Scorers:
@@ -154,7 +171,7 @@ def export_budgets(checkpoint: str, ratio: float, t: int, out_dir: str, device="
     from . import BUDGET_FLOOR, budgets as device_budgets
 
     p = load_lkv_params(checkpoint)
-    logits = torch.tensor(head_scores(p), dtype=torch.float64, device=device)
+    logits = head_scores(p, device=device)
     ratios, b = device_budgets(logits, ratio, [max(int(t), 1)], BUDGET_FLOOR)
     os.makedirs(out_dir, exist_ok=True)
     p1 = os.path.join(out_dir, "budgets.csv")

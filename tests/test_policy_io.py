@@ -25,19 +25,24 @@ def test_load_reference_checkpoint(name, L, H, d, de):
     # init_mlp2 (policy.cpp:18-28): b1 = 0, w1 ~ N(0, 1/in)
     assert all((m.b1 == 0).all() for m in p.token_scorers)
     assert abs(np.std(np.concatenate([m.w1.ravel() for m in p.token_scorers])) - 1 / np.sqrt(2 * d)) < 0.1 / np.sqrt(d)
-    # the LKV-H logits equal the reference's own load_lkv_params + head_scores
+    # the oracle's mlp2 on the loaded tables equals the reference's own load_lkv_params + head_scores
     want = np.load(os.path.join(G, f"head_scores_{name}.npy"))
-    got = policy_io.head_scores(p)
+    got = O.token_scores(p.head_embeddings, None, p.head_predictor.w1, p.head_predictor.b1, p.head_predictor.w2, act=O.SILU, dtype=O.F64)
     assert np.max(np.abs(got - want)) <= 1e-12 * max(1.0, np.max(np.abs(want)))
     # parameter count fixture (policy.cpp:289-299): 2d*d + d + d per scorer
     assert sum(m.w1.size + m.b1.size + m.w2.size for m in p.token_scorers) == L * H * (2 * d * d + 2 * d)
 
 
-def test_budgets_from_checkpoint_are_the_references():
-    p = policy_io.load_lkv_params(os.path.join(G, "lkv_params_desk.bin"))
-    logits = np.load(os.path.join(G, "head_scores_desk.npy"))
-    r = O.allocate_budgets(policy_io.head_scores(p), 0.15)
-    assert np.allclose(r, O.allocate_budgets(logits, 0.15), rtol=1e-12, atol=0)
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["desk", "l2h4d128"])
+def test_device_head_scores_are_the_references(name):
+    """The LKV-H logits computed on the B200 (fp64) equal the reference's own head_scores."""
+    p = policy_io.load_lkv_params(os.path.join(G, f"lkv_params_{name}.bin"))
+    want = np.load(os.path.join(G, f"head_scores_{name}.npy"))
+    got = policy_io.head_scores(p).cpu().numpy()
+    assert np.max(np.abs(got - want)) <= 1e-12 * max(1.0, np.max(np.abs(want)))
+    r = O.allocate_budgets(got, 0.15)
+    assert np.allclose(r, O.allocate_budgets(want, 0.15), rtol=1e-12, atol=0)
 
 
 def test_container_validation(tmp_path):

@@ -79,3 +79,28 @@ def test_reference_test_cases_pass_on_b200(suite):
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
     m = re.search(r"test cases: (\d+) \| (\d+) passed \| 0 failed", r.stdout)
     assert m and int(m.group(1)) > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["desk", "l2h4d128"])
+def test_checkpoint_api_ingests_reference_policy(name, tmp_path):
+    """lkv::load_lkv_params on a checkpoint written by the reference's own save path, LKV-H logits
+    by lkv::head_scores on the B200 == the reference's head_scores; save/load round trips; the
+    device budgets from them == the CPU oracle's freeze of the reference's logits."""
+    import numpy as np
+
+    import oracle as O
+
+    binp = os.path.join(ROOT, "paper_2605_06676_b200", "build", "test_checkpoint_api")
+    if not os.path.exists(binp):
+        subprocess.check_call(["make", "-s", "test_api"], cwd=os.path.join(ROOT, "paper_2605_06676_b200"))
+    g = os.path.join(ROOT, "tests", "golden")
+    r = subprocess.run([binp, os.path.join(g, f"lkv_params_{name}.bin"), str(tmp_path)], capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    got = np.array([float(l.split()[2]) for l in r.stdout.splitlines() if l.startswith("score ")])
+    want = np.load(os.path.join(g, f"head_scores_{name}.npy"))
+    assert got.shape == want.shape
+    assert np.max(np.abs(got - want)) <= 1e-12 * max(1.0, np.max(np.abs(want)))
+    b = np.array([int(l.split()[2]) for l in r.stdout.splitlines() if l.startswith("budget ")])
+    assert (b == O.freeze_budgets(O.allocate_budgets(want, 0.15), 1000)).all()
