@@ -14,6 +14,7 @@
 #include "lkv/attention.hpp"
 #include "lkv/checkpoint.hpp"
 #include "lkv/errors.hpp"
+#include "lkv/evictsim.hpp"
 #include "lkv/model.hpp"
 #include "lkv/policy.hpp"
 #include "lkv/soft_topk.hpp"
@@ -283,6 +284,43 @@ int ref_decode_steps(void* h, const int32_t* lens, const int64_t* row_off, const
             }
         }
         *tokens_seen_out = cache.tokens_seen;
+    });
+}
+
+// prefill_with_eviction (evictsim.cpp:95-238) with a learned selection policy whose LkvParams come
+// from init_lkv_params(config, lkv_seed) (policy.cpp:84-100), or a baseline select kind
+// (0 learned, 1 random, 2 recency, 3 sink_recent, 4 attn_window).  Outputs the compacted cache:
+// lens [L*H], row offsets = exclusive scan of lens, keys/values [rows][d], positions [rows]; and
+// report = {scoring_ops, peak_kv_values, kv_bytes_full, kv_bytes_compressed}.
+int ref_prefill_with_eviction(void* h, const int32_t* tokens, int t, const int32_t* budgets, int select_kind,
+                              unsigned long long lkv_seed, unsigned long long seed, int32_t* lens, double* keys,
+                              double* values, int32_t* positions, double* report) {
+    return guarded([&] {
+        const lkv::ModelWeights& w = *static_cast<lkv::ModelWeights*>(h);
+        const lkv::ModelConfig& c = w.config;
+        lkv::LkvParams params = lkv::init_lkv_params(c, lkv_seed);
+        lkv::EvictionPolicy pol;
+        pol.budget = lkv::BudgetKind::uniform;
+        const lkv::SelectKind kinds[] = {lkv::SelectKind::learned, lkv::SelectKind::random, lkv::SelectKind::recency,
+                                         lkv::SelectKind::sink_recent, lkv::SelectKind::attn_window};
+        pol.select = kinds[select_kind];
+        pol.params = &params;
+        const int n = c.total_kv_heads(), d = c.head_dim;
+        auto [cache, rep] = lkv::prefill_with_eviction(w, std::vector<int>(tokens, tokens + t),
+                                                       std::vector<int>(budgets, budgets + n), pol, seed);
+        size_t row = 0;
+        for (int i = 0; i < n; ++i) {
+            const lkv::HeadCache& hc = cache.heads[(size_t)i];
+            lens[i] = hc.retained();
+            std::memcpy(keys + row * d, hc.keys.data(), sizeof(double) * hc.keys.size());
+            std::memcpy(values + row * d, hc.values.data(), sizeof(double) * hc.values.size());
+            std::memcpy(positions + row, hc.retained_positions.data(), sizeof(int32_t) * (size_t)hc.retained());
+            row += (size_t)hc.retained();
+        }
+        report[0] = (double)rep.scoring_ops;
+        report[1] = (double)rep.peak_kv_values;
+        report[2] = rep.kv_bytes_full;
+        report[3] = rep.kv_bytes_compressed;
     });
 }
 

@@ -125,7 +125,7 @@ def test_export_budgets_from_reference_checkpoint(tmp_path):
     ck = os.path.join(G, "lkv_params_l2h4d128.bin")
     p1, p2 = policy_io.export_budgets(ck, 0.15, 1000, str(tmp_path))
     p = policy_io.load_lkv_params(ck)
-    scores = policy_io.head_scores(p)
+    scores = policy_io.head_scores(p).cpu().numpy()
     want_ratios = O.allocate_budgets(scores, 0.15)
     assert open(p1).read() == policy_io.budget_table_csv(want_ratios, p.n_layers, p.n_kv_heads)
     if O.ref_lib() is not None:
