@@ -31,6 +31,19 @@ constexpr int kMaxChunksPerHead = 1024;           // t <= 4M rows per head
 
 enum : uint32_t { kModeNormal = 0, kModeNone = 1, kModeAll = 2 };
 
+// key <-> float for the float-domain compares (f32_key's inverse on keys of real floats)
+constexpr uint32_t kKeyNegInf = 0x007fffffu;  // f32_key(-inf)
+constexpr uint32_t kKeyPosInf = 0xff800000u;  // f32_key(+inf)
+__device__ __forceinline__ float key_to_f32(uint32_t k) {
+    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+// the largest float below f (f != -0.0, f finite or +inf)
+__device__ __forceinline__ float float_below(float f) {
+    const uint32_t u = __float_as_uint(f);
+    if (u == 0u) return __uint_as_float(0x80000001u);  // +0.0 -> -denorm_min
+    return __uint_as_float((u & 0x80000000u) ? u + 1u : u - 1u);
+}
+
 
 
 struct ChunkInfo {
@@ -188,65 +201,69 @@ __global__ void __launch_bounds__(kPlanThreads, 2) select_plan_kernel(const __gr
         find_bin_from_top<kPlanThreads>(cnt, 2048, (uint32_t)b, s_scan, &s_bin, &s_above);
         const uint32_t bin1 = s_bin;
         uint32_t rem = (uint32_t)b - s_above;
-        // S3
+        // S3 in the float domain.  The bin's keys [bin1 << 21, ((bin1 + 1) << 21) - 1] are a float
+        // interval, so a row lies above the bin iff x > g_thr and inside it iff x >= lo_f and not
+        // above -- two compares per row, no key transform (IEEE compares treat -0.0 == +0.0, as the
+        // key does; NaN was rejected by K1).  Rows above are counted per warp with one reduction
+        // per chunk; the in-bin rows are appended (position + key) warp-aggregated.
         const float* sc = p.scores + (size_t)head * p.seq.T;
         uint32_t* cand = p.cands + (size_t)head * p.seq.T;  // overflow past kCandCap
-        // 16-byte loads when every head's scores are 16-byte aligned: branch-free (the address
-        // clamped into the head's row stride, rows >= t masked) so a batch's loads are all issued
-        // before the first use
+        const uint32_t lo_key = bin1 << 21;
+        const uint64_t hi1 = ((uint64_t)bin1 + 1) << 21;  // the first key above the bin
+        const float lo_f = lo_key <= kKeyNegInf ? -INFINITY : key_to_f32(lo_key);
+        const float g_thr = hi1 > kKeyPosInf ? INFINITY : float_below(key_to_f32((uint32_t)hi1));
         const int T = p.seq.T;
+        const int full = t / kChunk;  // chunks whose 4096 rows are all inside the head
+        // 16-byte loads when every head's scores are 16-byte aligned: branch-free (the address
+        // clamped into the head's row stride) so a batch's loads are all issued before the first use
         const bool vec = ((reinterpret_cast<uintptr_t>(sc)) & 15) == 0 && (T & 3) == 0;
         for (int c0 = 0; c0 < cph; c0 += kPlanBatch) {
-            uint32_t k[kPlanBatch][kPlanRows], valid[kPlanBatch];
+            float v[kPlanBatch][kPlanRows];
             if (vec) {
-                float4 f[kPlanBatch][2];
 #pragma unroll
                 for (int u = 0; u < kPlanBatch; ++u)
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         const int r = min((c0 + u) * kChunk + tid * kPlanRows + 4 * h, T - 4);
-                        f[u][h] = __ldg(reinterpret_cast<const float4*>(sc + r));
+                        const float4 f = __ldg(reinterpret_cast<const float4*>(sc + r));
+                        v[u][4 * h + 0] = f.x;
+                        v[u][4 * h + 1] = f.y;
+                        v[u][4 * h + 2] = f.z;
+                        v[u][4 * h + 3] = f.w;
                     }
-#pragma unroll
-                for (int u = 0; u < kPlanBatch; ++u) {
-                    const int r = (c0 + u) * kChunk + tid * kPlanRows;
-                    valid[u] = 0;
-#pragma unroll
-                    for (int q = 0; q < kPlanRows; ++q) valid[u] |= uint32_t(c0 + u < cph && r + q < t) << q;
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        k[u][4 * h + 0] = f32_key(f[u][h].x);
-                        k[u][4 * h + 1] = f32_key(f[u][h].y);
-                        k[u][4 * h + 2] = f32_key(f[u][h].z);
-                        k[u][4 * h + 3] = f32_key(f[u][h].w);
-                    }
-                }
             } else {
 #pragma unroll
                 for (int u = 0; u < kPlanBatch; ++u) {
-                    valid[u] = 0;
                     const int r = (c0 + u) * kChunk + tid * kPlanRows;
 #pragma unroll
-                    for (int q = 0; q < kPlanRows; ++q) {
-                        const bool ok = c0 + u < cph && r + q < t;
-                        k[u][q] = ok ? f32_key(__ldg(sc + r + q)) : 0u;
-                        valid[u] |= uint32_t(ok) << q;
-                    }
+                    for (int q = 0; q < kPlanRows; ++q) v[u][q] = r + q < t ? __ldg(sc + r + q) : -INFINITY;
                 }
             }
 #pragma unroll
             for (int u = 0; u < kPlanBatch; ++u) {
-                if (c0 + u >= cph) break;
-                uint32_t gt = 0, cm = 0;  // rows above bin1; bit mask of the rows inside it
+                const int c = c0 + u;
+                if (c >= cph) break;
+                const int r0 = c * kChunk + tid * kPlanRows;
+                uint32_t gt = 0, cm = 0;  // rows above the bin; bit mask of the rows inside it
+                if (c < full) {
 #pragma unroll
-                for (int q = 0; q < kPlanRows; ++q) {
-                    const uint32_t d = k[u][q] >> 21;
-                    const bool v = valid[u] >> q & 1u;
-                    gt += v && d > bin1;
-                    cm |= uint32_t(v && d == bin1) << q;
+                    for (int q = 0; q < kPlanRows; ++q) {
+                        const bool above = v[u][q] > g_thr;
+                        gt += above;
+                        cm |= uint32_t(!above && v[u][q] >= lo_f) << q;
+                    }
+                } else {  // the head's last, partial chunk
+#pragma unroll
+                    for (int q = 0; q < kPlanRows; ++q) {
+                        const bool ok = r0 + q < t;
+                        const bool above = ok && v[u][q] > g_thr;
+                        gt += above;
+                        cm |= uint32_t(ok && !above && v[u][q] >= lo_f) << q;
+                    }
                 }
                 const uint32_t wgt = __reduce_add_sync(0xffffffffu, gt);
-                if (lane == 0 && wgt) atomicAdd(&c_gt[c0 + u], wgt);
+                if (lane == 0 && wgt) atomicAdd(&c_gt[c], wgt);
+                if (!__any_sync(0xffffffffu, cm)) continue;
                 // warp-aggregated append of the in-bin rows (position and key)
                 const uint32_t nc = __popc(cm);
                 uint32_t incl = nc;
@@ -256,25 +273,23 @@ __global__ void __launch_bounds__(kPlanThreads, 2) select_plan_kernel(const __gr
                     if (lane >= o) incl += y;
                 }
                 const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
-                if (wtot) {
-                    uint32_t base = 0;
-                    if (lane == 31) base = atomicAdd(&s_ncand, wtot);
-                    base = __shfl_sync(0xffffffffu, base, 31) + incl - nc;
-                    const uint32_t r0 = (uint32_t)((c0 + u) * kChunk + tid * kPlanRows);
-                    while (cm) {  // only the rows inside the bin (a few % of them)
-                        const int q = __ffs(cm) - 1;
-                        cm &= cm - 1;
-                        uint32_t key = k[u][0];
+                uint32_t base = 0;
+                if (lane == 31) base = atomicAdd(&s_ncand, wtot);
+                base = __shfl_sync(0xffffffffu, base, 31) + incl - nc;
+                while (cm) {  // only the rows inside the bin (a few % of them)
+                    const int q = __ffs(cm) - 1;
+                    cm &= cm - 1;
+                    float x = v[u][0];
 #pragma unroll
-                        for (int z = 1; z < kPlanRows; ++z) key = q == z ? k[u][z] : key;  // no local-memory indexing
-                        if (base < kCandCap) {
-                            s_cpos[base] = r0 + q;
-                            s_ckey[base] = key;
-                        } else {
-                            cand[base - kCandCap] = r0 + q;
-                        }
-                        ++base;
+                    for (int z = 1; z < kPlanRows; ++z) x = q == z ? v[u][z] : x;  // no local-memory indexing
+                    const uint32_t key = f32_key(x);
+                    if (base < kCandCap) {
+                        s_cpos[base] = (uint32_t)(r0 + q);
+                        s_ckey[base] = key;
+                    } else {
+                        cand[base - kCandCap] = (uint32_t)(r0 + q);
                     }
+                    ++base;
                 }
             }
         }

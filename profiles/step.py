@@ -35,5 +35,6 @@ q, k, v = synth.make_decode_inputs(cfg, 0)
 for _ in range(a.decode):
     lkv.decode_step(rc, q, k, v, check=False)
 torch.cuda.synchronize()
-rc._decode_ws.status()
+if rc._decode_ws is not None:
+    rc._decode_ws.status()
 print("OK")
