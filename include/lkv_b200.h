@@ -401,6 +401,16 @@ lkv_status lkv_rope_table(int32_t t_max, int32_t head_dim, double base, int32_t 
 lkv_status lkv_rope_pack(const void* k_lin, const void* v_lin, const lkv_cache_desc* layer, const void* table,
                          void* k_out, void* v_out, lkv_stream_t stream);
 
+/* One layer's K/V production on tcgen05 tensor cores (evictsim.cpp:133-145): [k | v] = h Wkv with
+ * RoPE (K only, at the absolute positions of `table`, lkv_rope_table) and the token-major ->
+ * head-major pack fused into the GEMM epilogue, written straight into the dense layer k_out /
+ * v_out [n_seq][n_kv_heads][max_tokens][head_dim] that lkv_score / lkv_select read (the
+ * rope_pack round trip disappears).  h: [n_seq][max_tokens][d_model] bf16 (the attention-normed
+ * hidden states); wkv_t: [2 * n_kv_heads * head_dim][d_model] bf16 = [Wk | Wv] transposed (K
+ * output columns first).  bf16, head_dim 128, d_model % 64 == 0; fp32 accumulation. */
+lkv_status lkv_kv_project(const void* h, int32_t d_model, const void* wkv_t, const lkv_cache_desc* layer,
+                          const void* table, void* k_out, void* v_out, lkv_stream_t stream);
+
 /* ---- K5: decode over the ragged cache ------------------------------------------- */
 /* lkv_decode_plan splits every head's capacity into work items of 128..1024 rows (once
  * per eviction, after offsets are final).  lkv_decode_step then runs one decode

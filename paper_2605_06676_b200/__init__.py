@@ -314,7 +314,8 @@ def select(cache: DenseCache, scores: torch.Tensor, budgets_: torch.Tensor, deco
     _check(lib().lkv_ragged_offsets(_ptr(b), cache.n_heads, decode_slack, _ptr(rc.offsets), _stream()))
     ws = ws or _workspace_for(cache, 1)
     cd, rd = cache.desc(), rc.desc()
-    _check(lib().lkv_select(C.byref(cd), _ptr(scores.contiguous()), _ptr(b), C.byref(rd), 1 if gather else 0,
+    scores = scores.contiguous()  # keep every temporary alive across the call (stream-ordered reuse)
+    _check(lib().lkv_select(C.byref(cd), _ptr(scores), _ptr(b), C.byref(rd), 1 if gather else 0,
                             C.c_void_p(ws.ptr), ws.nbytes, _stream()))
     ws.status()
     rc.tokens_seen.copy_(torch.tensor(cache.seq_lens, dtype=torch.int32))
@@ -503,8 +504,11 @@ def decode_step(ragged: RaggedCache, q: torch.Tensor, new_k: torch.Tensor, new_v
     scale = scale if scale is not None else 1.0 / math.sqrt(D)
     rd = ragged.desc()
     ws = ragged._decode_ws
-    _check(lib().lkv_decode_step(C.byref(rd), n_seq, L, H, Hq, _ptr(q.contiguous()), _ptr(new_k.contiguous()),
-                                 _ptr(new_v.contiguous()), _ptr(ragged.tokens_seen), _ptr(out), float(scale),
+    # bind the contiguous copies first: a temporary freed inside the argument list could be handed
+    # to the next .contiguous() of the same call before the kernel reads it
+    q, new_k, new_v = q.contiguous(), new_k.contiguous(), new_v.contiguous()
+    _check(lib().lkv_decode_step(C.byref(rd), n_seq, L, H, Hq, _ptr(q), _ptr(new_k),
+                                 _ptr(new_v), _ptr(ragged.tokens_seen), _ptr(out), float(scale),
                                  C.c_void_p(ws.ptr), ws.nbytes, _stream()))
     if check:
         ws.status()

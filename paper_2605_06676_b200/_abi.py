@@ -32,7 +32,7 @@ EXPORTED = [
     "lkv_soft_topk_vjp", "lkv_evict_budgets", "lkv_mask_counts", "lkv_cache_from_trace", "lkv_decode_plan_ex",
     "lkv_model_plan_ex", "lkv_decode_plan_info", "lkv_evict_host_shard", "lkv_soft_topk_exact", "lkv_f64_gemm",
     "lkv_f64_rmsnorm", "lkv_f64_rope", "lkv_f64_attention", "lkv_f64_swiglu", "lkv_f64_embed", "lkv_f64_split_heads",
-    "lkv_f64_token_scores", "lkv_f64_select",
+    "lkv_f64_token_scores", "lkv_f64_select", "lkv_kv_project",
 ]
 
 
@@ -132,6 +132,8 @@ def load():
     for name in ["lkv_soft_topk_exact", "lkv_f64_gemm", "lkv_f64_rmsnorm", "lkv_f64_rope", "lkv_f64_attention",
                  "lkv_f64_swiglu", "lkv_f64_embed", "lkv_f64_split_heads", "lkv_f64_token_scores", "lkv_f64_select"]:
         getattr(L, name).restype = C.c_int
+    L.lkv_kv_project.argtypes = [vp, i32, vp, P(CacheDesc), vp, vp, vp, vp]
+    L.lkv_kv_project.restype = C.c_int
     L.lkv_rope_table.argtypes = [i32, i32, dbl, i32, vp, vp]
     L.lkv_rope_pack.argtypes = [vp, vp, P(CacheDesc), vp, vp, vp, vp]
     L.lkv_decode_workspace_bytes.restype = sz

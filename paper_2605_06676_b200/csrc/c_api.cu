@@ -1059,6 +1059,37 @@ lkv_status lkv_rope_pack(const void* k_lin, const void* v_lin, const lkv_cache_d
     return LKV_OK;
 }
 
+lkv_status lkv_kv_project(const void* h, int32_t d_model, const void* wkv_t, const lkv_cache_desc* layer,
+                          const void* table, void* k_out, void* v_out, lkv_stream_t stream) {
+    lkv_status st = check_cache(layer, false);
+    if (st) return st;
+    if (layer->n_layers != 1) return fail(LKV_ERR_CONTRACT, "kv_project: one layer per call");
+    if (layer->dtype != LKV_BF16 || layer->head_dim != 128)
+        return fail(LKV_ERR_UNSUPPORTED, "kv_project: bf16 and head_dim 128 (tcgen05 tiles)");
+    if (d_model < 64 || d_model % 64) return fail(LKV_ERR_UNSUPPORTED, "kv_project: d_model must be a multiple of 64");
+    if (!h || !wkv_t || !table || !k_out || !v_out) return fail(LKV_ERR_CONTRACT, "kv_project: null buffer");
+    if ((reinterpret_cast<uintptr_t>(k_out) | reinterpret_cast<uintptr_t>(v_out) |
+         reinterpret_cast<uintptr_t>(table)) & 15)
+        return fail(LKV_ERR_CONTRACT, "kv_project: outputs and table must be 16-byte aligned");
+    KvProjParams p;
+    memset(&p, 0, sizeof p);
+    p.T = (int32_t)layer->max_tokens;
+    p.H = layer->n_kv_heads;
+    p.D = layer->head_dim;
+    p.M = layer->n_seq * p.T;
+    p.N = 2 * p.H * p.D;
+    p.K = d_model;
+    p.table = static_cast<const float2*>(table);
+    p.k_out = k_out;
+    p.v_out = v_out;
+    if (p.N % 256) return fail(LKV_ERR_UNSUPPORTED, "kv_project: 2 * n_kv_heads * head_dim must be a multiple of 256");
+    CUtensorMap ma, mb;
+    if ((st = make_map_bf16(&ma, h, (uint64_t)d_model, (uint64_t)p.M, 128))) return st;
+    if ((st = make_map_bf16(&mb, wkv_t, (uint64_t)d_model, (uint64_t)p.N, 256))) return st;
+    LKV_CUDA(launch_kv_project(p, ma, mb, num_sms(), (cudaStream_t)stream), "kv project");
+    return LKV_OK;
+}
+
 size_t lkv_decode_workspace_bytes(const lkv_ragged_desc* r, int32_t G) {
     if (!r || G < 1) return 0;
     return decode_layout(r, G).total;

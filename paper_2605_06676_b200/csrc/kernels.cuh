@@ -339,6 +339,17 @@ cudaError_t launch_f64_split_heads(int t, int H, int d, const double* x, int64_t
 size_t f64_scorer_smem(int in, int hidden);
 cudaError_t launch_f64_scorer(const F64ScorerParams& p, cudaStream_t s);
 cudaError_t launch_f64_select(const F64SelectParams& p, int n_heads, cudaStream_t s);
+// ---- kvproj.cu (layer-by-layer prefill: K/V projections on tcgen05 with RoPE + pack fused)
+struct KvProjParams {
+    int32_t M, N, K;        // M = n_seq * T token rows, N = 2 * H * D, K = d_model
+    int32_t T, H, D;
+    const float2* table;    // [T][D / 2] (cos, sin) at absolute positions (lkv_rope_table)
+    void* k_out;            // [n_seq][H][T][D] bf16
+    void* v_out;
+};
+cudaError_t launch_kv_project(const KvProjParams& p, const CUtensorMap& ma, const CUtensorMap& mb, int num_sms,
+                              cudaStream_t stream);
+size_t kv_project_smem();
 // ---- rope.cu (layer-by-layer prefill: K/V production)
 cudaError_t launch_rope_table(int t_max, int head_dim, double base, int pos_offset, float2* cs, cudaStream_t stream);
 cudaError_t launch_rope_pack(const void* k_lin, const void* v_lin, int n_seq, int t_max, const int32_t* seq_lens,

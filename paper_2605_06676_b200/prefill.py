@@ -4,9 +4,10 @@ The reference computes one layer's K/V over the full prefix, scores and compacts
 per KV head, then moves on, so the peak KV footprint is ONE full-length layer plus the
 compressed earlier layers (the peak accounting of evictsim.cpp:157-159).  Here, per layer:
 
-  k_lin, v_lin = x @ Wk, x @ Wv     (caller's projections: plain cuBLAS GEMMs)
-  lkv_rope_pack                     (RoPE at absolute positions + token-major -> head-major,
-                                     into ONE reusable dense layer buffer)
+  lkv_kv_project                    (h [Wk | Wv] on tcgen05 with RoPE at absolute positions and
+                                     the token-major -> head-major pack fused in the epilogue,
+                                     into ONE reusable dense layer buffer; ingest_layer_hidden)
+  or, for projections computed elsewhere, lkv_rope_pack (ingest_layer)
   lkv_score + lkv_select(gather)    (per sequence, with that layer's slice of the budgets that
                                      lkv_budgets solved once over ALL L*H logits)
 
@@ -63,6 +64,20 @@ class LayerwisePrefill:
                                  _ptr(self.ratios), _ptr(self.budgets), _ptr(self.ragged.offsets),
                                  C.c_void_p(self._bws.ptr), self._bws.nbytes, s))
 
+    def ingest_layer_hidden(self, l: int, h: torch.Tensor, wkv_t: torch.Tensor) -> None:
+        """Produce layer `l`'s K/V from the attention-normed hidden states h [n_seq, max_tokens,
+        d_model] and the transposed [Wk | Wv] weights wkv_t [2 * H * D, d_model] (kv_weights())
+        with lkv_kv_project (tcgen05 GEMM, RoPE + head-major pack fused), then score, select and
+        compact it."""
+        S, H, D, T = self.S, self.H, self.D, self.T
+        if h.dim() != 3 or h.shape[:2] != (S, T) or h.dtype != self.dtype or wkv_t.shape != (2 * H * D, h.shape[2]):
+            raise ContractError("h must be [n_seq, max_tokens, d_model] and wkv_t [2 * H * D, d_model]")
+        ld = self.layer.desc()
+        h, wkv_t = h.contiguous(), wkv_t.contiguous()  # alive across the call
+        _check(lib().lkv_kv_project(_ptr(h), h.shape[2], _ptr(wkv_t), C.byref(ld),
+                                    _ptr(self.table), _ptr(self.k_layer), _ptr(self.v_layer), _stream()))
+        self._score_select(l)
+
     def ingest_layer(self, l: int, k_lin: torch.Tensor, v_lin: torch.Tensor) -> None:
         """Rope, score, select and compact layer `l` from its projections
         k_lin / v_lin [n_seq, max_tokens, n_kv_heads * head_dim] (post-GEMM, pre-RoPE)."""
@@ -74,6 +89,12 @@ class LayerwisePrefill:
         ld = self.layer.desc()
         _check(lib().lkv_rope_pack(_ptr(k_lin), _ptr(v_lin), C.byref(ld), _ptr(self.table), _ptr(self.k_layer),
                                    _ptr(self.v_layer), s))
+        self._score_select(l)
+
+    def _score_select(self, l: int) -> None:
+        S, H, D, T = self.S, self.H, self.D, self.T
+        s = _stream()
+        ld = self.layer.desc()
         sc = self.scorers
         in_dim = sc.w1.shape[1]
         hidden = sc.w1.shape[2]
@@ -116,6 +137,25 @@ def rope_table(max_tokens: int, head_dim: int, base: float = 10000.0, pos_offset
     return t
 
 
+def kv_weights(wk: torch.Tensor, wv: torch.Tensor) -> torch.Tensor:
+    """[Wk | Wv] (reference layout x W, [d_model, H * D] each) -> the transposed, concatenated
+    [2 * H * D, d_model] operand lkv_kv_project reads (K-major for the UMMA B operand)."""
+    return torch.cat([wk, wv], dim=1).t().contiguous()
+
+
+def kv_project(h: torch.Tensor, wkv_t: torch.Tensor, table: torch.Tensor, seq_lens, n_kv_heads: int,
+               head_dim: int = 128):
+    """h [n_seq, T, d_model] bf16 -> (K roped, V) dense layer [n_seq, 1, H, T, D] (lkv_kv_project)."""
+    S, T, dm = h.shape
+    k_out = torch.empty(S, 1, n_kv_heads, T, head_dim, dtype=h.dtype, device=h.device)
+    v_out = torch.empty_like(k_out)
+    layer = DenseCache(k_out, v_out, list(seq_lens))
+    h, wkv_t = h.contiguous(), wkv_t.contiguous()  # alive across the call
+    _check(lib().lkv_kv_project(_ptr(h), dm, _ptr(wkv_t), C.byref(layer.desc()), _ptr(table),
+                                _ptr(k_out), _ptr(v_out), _stream()))
+    return k_out, v_out
+
+
 def rope_pack(k_lin: torch.Tensor, v_lin: torch.Tensor, table: torch.Tensor, seq_lens, n_kv_heads: int):
     """[n_seq, T, H*D] projections -> (K roped, V) dense layer [n_seq, 1, H, T, D]."""
     S, T, HD = k_lin.shape
@@ -123,6 +163,9 @@ def rope_pack(k_lin: torch.Tensor, v_lin: torch.Tensor, table: torch.Tensor, seq
     k_out = torch.empty(S, 1, n_kv_heads, T, D, dtype=k_lin.dtype, device=k_lin.device)
     v_out = torch.empty_like(k_out)
     layer = DenseCache(k_out, v_out, list(seq_lens))
-    _check(lib().lkv_rope_pack(_ptr(k_lin.contiguous()), _ptr(v_lin.contiguous()), C.byref(layer.desc()), _ptr(table),
+    # both contiguous copies alive across the call: two temporaries freed inside one argument list
+    # can share a caching-allocator block (the second copy overwrote the first, K came out as V)
+    k_lin, v_lin = k_lin.contiguous(), v_lin.contiguous()
+    _check(lib().lkv_rope_pack(_ptr(k_lin), _ptr(v_lin), C.byref(layer.desc()), _ptr(table),
                                _ptr(k_out), _ptr(v_out), _stream()))
     return k_out, v_out

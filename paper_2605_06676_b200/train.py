@@ -70,7 +70,8 @@ def masked_attention_bwd(q, k, v, mask, out, lse, d_out, causal=True, scale=None
     dk = torch.empty(k.shape, dtype=torch.float32, device=q.device)
     dv = torch.empty(k.shape, dtype=torch.float32, device=q.device)
     dm = torch.empty(k.shape[:3], dtype=torch.float32, device=q.device) if m is not None else None
-    _check(lib().lkv_masked_attention_bwd(C.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(m), _ptr(out.contiguous()),
+    out = out.contiguous()
+    _check(lib().lkv_masked_attention_bwd(C.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(m), _ptr(out),
                                           _ptr(lse), _ptr(d_out), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(dm),
                                           C.c_void_p(ws.ptr), ws.nbytes, _stream()))
     if check:

@@ -792,6 +792,82 @@ def test_rope_pack_matches_fp64_rope():  # tensor.cpp:586-623 convention, absolu
         assert torch.equal(v[:, 0].transpose(1, 2).reshape(S, T, H * D)[1, :450], v_lin[1, :450])
 
 
+@pytest.mark.parametrize("S,T,H,dm", [(2, 300, 2, 256), (1, 1024, 8, 512), (3, 129, 4, 64),
+                                     (1, 20000, 8, 256), (2, 9000, 4, 1024)])  # the last two: many tiles per CTA
+def test_kv_project_matches_fp64_projection_and_rope(S, T, H, dm):
+    """lkv_kv_project (tcgen05 GEMM, RoPE + head-major pack in the epilogue) vs the fp64 oracle of
+    evictsim.cpp:133-145: k = rope(h Wk) at absolute positions, v = h Wv, on the same bf16 inputs;
+    bf16 bar 1e-2 (observed ~3e-3: fp32 accumulation, one bf16 rounding of the output).  Token
+    counts off the 128-row tile, several heads per 256-column tile."""
+    from paper_2605_06676_b200 import prefill
+
+    torch.manual_seed(S * 1000 + T)
+    D = 128
+    h = (torch.randn(S, T, dm, device=DEV) * 0.5).to(torch.bfloat16)
+    wk = (torch.randn(dm, H * D, device=DEV) / math.sqrt(dm)).to(torch.bfloat16)
+    wv = (torch.randn(dm, H * D, device=DEV) / math.sqrt(dm)).to(torch.bfloat16)
+    tab = prefill.rope_table(T, D)
+    k, v = prefill.kv_project(h, prefill.kv_weights(wk, wv), tab, [T] * S, H)
+    hd = h.double().cpu().numpy()
+    kl = (hd @ wk.double().cpu().numpy()).reshape(S, T, H, D)
+    vl = (hd @ wv.double().cpu().numpy()).reshape(S, T, H, D)
+    pos = np.arange(T)[:, None]
+    th = pos * (10000.0 ** (-2.0 * np.arange(D // 2) / D))[None, :]
+    a, b = kl[..., 0::2], kl[..., 1::2]
+    want_k = np.empty_like(kl)
+    want_k[..., 0::2] = a * np.cos(th)[None, :, None, :] - b * np.sin(th)[None, :, None, :]
+    want_k[..., 1::2] = a * np.sin(th)[None, :, None, :] + b * np.cos(th)[None, :, None, :]
+    got_k = k.double().cpu().numpy()[:, 0].transpose(0, 2, 1, 3)
+    got_v = v.double().cpu().numpy()[:, 0].transpose(0, 2, 1, 3)
+    assert rel_gap(got_k, want_k) <= 1e-2
+    assert rel_gap(got_v, vl) <= 1e-2
+
+
+def test_layerwise_prefill_from_hidden_states_equals_one_shot():
+    """Layer-by-layer prefill fed by lkv_kv_project (ingest_layer_hidden) == one lkv_evict over the
+    dense cache that the same kernel produces layer by layer: budgets, offsets, positions and rows
+    bit-exact."""
+    from paper_2605_06676_b200 import prefill
+
+    cfg = synth.CONFIGS[2]
+    S, L, H, D, T, dm = 1, 3, 8, 128, 2000, 512
+    torch.manual_seed(77)
+    hs = [(torch.randn(S, T, dm, device=DEV) * 0.5).to(torch.bfloat16) for _ in range(L)]
+    ws = [prefill.kv_weights((torch.randn(dm, H * D, device=DEV) / math.sqrt(dm)).to(torch.bfloat16),
+                             (torch.randn(dm, H * D, device=DEV) / math.sqrt(dm)).to(torch.bfloat16)) for _ in range(L)]
+    scorers = synth.make_scorers(cfg, n_layers=L)
+    logits = synth.make_logits(cfg, n_layers=L)
+    pf = prefill.LayerwisePrefill(S, L, H, D, T, [T], scorers, logits, cfg.ratio, lkv.BUDGET_EXACT, decode_slack=2)
+    for l in range(L):
+        pf.ingest_layer_hidden(l, hs[l], ws[l])
+    rc = pf.finish()
+    tab = prefill.rope_table(T, D)
+    K = torch.empty(S, L, H, T, D, dtype=torch.bfloat16, device=DEV)
+    V = torch.empty_like(K)
+    for l in range(L):
+        k, v = prefill.kv_project(hs[l], ws[l], tab, [T], H)
+        K[:, l], V[:, l] = k[:, 0], v[:, 0]
+    ref = lkv.evict(lkv.DenseCache(K, V, [T]), scorers, logits, cfg.ratio, lkv.BUDGET_EXACT, decode_slack=2)
+    assert torch.equal(rc.offsets, ref.cache.offsets) and torch.equal(rc.lens, ref.cache.lens)
+    for i in range(L * H):
+        assert all(torch.equal(a, b) for a, b in zip(rc.head(i), ref.cache.head(i))), i
+
+
+def test_rope_pack_noncontiguous_views():
+    """rope_pack on strided views (k and v slices of one [T, 2HD] projection): each gets its own
+    contiguous copy for the duration of the call (two temporaries freed inside one argument list
+    used to share a caching-allocator block, so K came out as rope(V))."""
+    from paper_2605_06676_b200 import prefill
+
+    torch.manual_seed(43)
+    S, T, H, D = 1, 700, 2, 128
+    kv = torch.randn(S, T, 2 * H * D, device=DEV).to(torch.bfloat16)
+    tab = prefill.rope_table(T, D)
+    k1, v1 = prefill.rope_pack(kv[..., :H * D], kv[..., H * D:], tab, [T], H)
+    k2, v2 = prefill.rope_pack(kv[..., :H * D].contiguous(), kv[..., H * D:].contiguous(), tab, [T], H)
+    assert torch.equal(k1, k2) and torch.equal(v1, v2)
+
+
 def test_layerwise_prefill_equals_one_shot_eviction():
     """Per-layer rope + score + select into one ragged cache == one lkv_evict over the whole
     dense cache; peak KV = one dense layer + the compressed earlier layers (evictsim.cpp:157-159)."""
