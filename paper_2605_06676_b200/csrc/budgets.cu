@@ -249,20 +249,57 @@ __global__ void __launch_bounds__(kBudgetThreads, 1) budgets_kernel(const Budget
             xs[rank] = xi;
         }
         __syncthreads();
-        // -- log prefix sums of e^{-x} (thread 0) and log suffix sums of e^{x} (warp 1) (:74-82)
-        if (tid == 0) {
-            double acc = -CUDART_INF;
-            l1[0] = acc;
-            for (int m = 1; m <= n; ++m) {
-                acc = logaddexp_ref(acc, -xs[m - 1]);
-                l1[m] = acc;
+        // -- log prefix sums of e^{-x} and log suffix sums of e^{x} (:74-82) as two parallel
+        //    log-sum-exp scans: each thread folds a contiguous segment of the sorted scores, a
+        //    Hillis-Steele scan combines the segment totals (log2(1024) rounds), and each thread
+        //    completes its segment.  The reference folds left to right in one chain; a scan
+        //    associates differently, so l1 / l2 may differ from it in the last few ulps (ratios stay
+        //    within 1e-13 relative; budgets bit-exact -- tests/test_gpu_parity.py), at ~15 steps of
+        //    latency instead of n.
+        {
+            // scratch for the segment totals: r and the fl / delta pair are written only later (rem
+            // holds the unscaled scores of a soft_topk_forward call)
+            double* sa = r;
+            double* sb = reinterpret_cast<double*>(fl);
+            const int per = (n + kBudgetThreads - 1) / kBudgetThreads;
+            const int i0 = min(n, tid * per), i1 = min(n, i0 + per);
+            double a = -CUDART_INF, b = -CUDART_INF;
+            for (int i = i0; i < i1; ++i) {  // local inclusive prefix of e^{-x}
+                a = logaddexp_ref(a, -xs[i]);
+                l1[i + 1] = a;
             }
-        } else if (tid == 32) {
-            double acc = -CUDART_INF;
-            l2[n] = acc;
-            for (int m = n - 1; m >= 0; --m) {
-                acc = logaddexp_ref(acc, xs[m]);
-                l2[m] = acc;
+            for (int i = i1 - 1; i >= i0; --i) {  // local inclusive suffix of e^{x}
+                b = logaddexp_ref(b, xs[i]);
+                l2[i] = b;
+            }
+            const int nt = (n + per - 1) / per;  // threads that own a segment (<= kBudgetThreads)
+            if (tid < nt) {
+                sa[tid] = a;
+                sb[tid] = b;
+            }
+            __syncthreads();
+            for (int off = 1; off < nt; off <<= 1) {
+                double na = 0.0, nb = 0.0;
+                if (tid < nt) {
+                    na = tid >= off ? logaddexp_ref(sa[tid - off], sa[tid]) : sa[tid];
+                    nb = tid + off < nt ? logaddexp_ref(sb[tid], sb[tid + off]) : sb[tid];
+                }
+                __syncthreads();
+                if (tid < nt) {
+                    sa[tid] = na;
+                    sb[tid] = nb;
+                }
+                __syncthreads();
+            }
+            const double pre = (tid > 0 && tid <= nt) ? sa[tid - 1] : -CUDART_INF;  // segments before mine
+            const double suf = tid + 1 < nt ? sb[tid + 1] : -CUDART_INF;           // segments after mine
+            for (int i = i0; i < i1; ++i) {
+                l1[i + 1] = logaddexp_ref(pre, l1[i + 1]);
+                l2[i] = logaddexp_ref(suf, l2[i]);
+            }
+            if (tid == 0) {
+                l1[0] = -CUDART_INF;
+                l2[n] = -CUDART_INF;
             }
         }
         __syncthreads();

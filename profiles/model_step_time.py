@@ -28,6 +28,8 @@ def main():
     ap.add_argument("--vocab", type=int, default=128256)
     ap.add_argument("--t", type=int, default=32768)
     ap.add_argument("--eager", action="store_true", help="eager steps, no graph (for ncu launch lists)")
+    ap.add_argument("--rows-per-item", type=int, default=0,
+                    help="per-layer attention work-item rows (0: the one-wave plan)")
     a = ap.parse_args()
     torch.manual_seed(0)
     cfg = M.ModelConfig(n_layers=32, n_query_heads=32, n_kv_heads=8, head_dim=128, vocab_size=a.vocab,
@@ -60,7 +62,7 @@ def main():
     del cache
     torch.cuda.empty_cache()
     rc = res.cache
-    model.bind(rc)
+    model.bind(rc, rows_per_item=a.rows_per_item)
     tokens = torch.randint(0, cfg.vocab_size, (a.n_seq,), dtype=torch.int32, device="cuda")
     logits = torch.empty(a.n_seq, cfg.vocab_size, dtype=torch.float32, device="cuda")
     model.step(tokens, logits)  # eager step, error-checked
