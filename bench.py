@@ -595,27 +595,69 @@ def run_sharded(args, rank, world, local_rank):
     hbm_peak, _, peak_src = load_peaks()
     comm = sharded.Comm.from_process_group()
     L, H, D = cfg.n_layers, cfg.n_kv_heads, cfg.head_dim
-    plan = sharded.ShardPlan(L, H, world)
-    l0, l1 = plan.layers[rank]
-    h0, n_local = plan.head_range(rank)
-    log(f"inputs: layers [{l0}, {l1})")
-    # this rank's layers only (the same seeded data an unsharded run would hold for them)
+    T = cfg.max_tokens
+    all_logits = synth.make_logits(cfg, device=dev)
+    # placement: LPT over (layer, head) by eviction bytes (scoring t * 264 B + gathering b * 1028 B;
+    # budgets depend only on the logits, so they are known before eviction) or contiguous layers
+    _, b_host = lkv.budgets(all_logits, cfg.ratio, [T], lkv.BUDGET_EXACT)
+    weights = [T * 264 + int(x) * 1028 for x in b_host[0].cpu().tolist()]
+    plan_lr = sharded.ShardPlan(L, H, world, weights=None)
+    plan = sharded.ShardPlan(L, H, world, weights=weights if args.placement == "lpt" else None)
+    imbalance = {"layer_ranges": sharded.ShardPlan(L, H, world).imbalance, "placement": args.placement}
+    import paper_2605_06676_b200.shard as _sh
+
+    owner_lr = [r for r, hs in enumerate(plan_lr.heads) for _ in hs]
+    imbalance["layer_ranges_evict"] = _sh.imbalance(weights, owner_lr, world)
+    imbalance["layer_ranges_decode"] = _sh.imbalance([int(x) for x in b_host[0].cpu().tolist()], owner_lr, world)
+    owner = [0] * (L * H)
+    for r, hs in enumerate(plan.heads):
+        for h_ in hs:
+            owner[h_] = r
+    imbalance["this_plan_evict"] = _sh.imbalance(weights, owner, world)
+    imbalance["this_plan_decode"] = _sh.imbalance([int(x) for x in b_host[0].cpu().tolist()], owner, world)
+    def _owners(pl):
+        o = [0] * (L * H)
+        for r_, hs in enumerate(pl.heads):
+            for h_ in hs:
+                o[h_] = r_
+        return o
+
+    bl = [int(x) for x in b_host[0].cpu().tolist()]
+    for w8 in (2, 4, 8):  # the same placements modeled at the scaling run's world sizes
+        if w8 != world and L * H >= w8:
+            o_lr, o_lpt = _owners(sharded.ShardPlan(L, H, w8)), _owners(sharded.ShardPlan(L, H, w8, weights=weights))
+            imbalance[f"modeled_n{w8}"] = {"layer_ranges_evict": _sh.imbalance(weights, o_lr, w8),
+                                           "layer_ranges_decode": _sh.imbalance(bl, o_lr, w8),
+                                           "lpt_evict": _sh.imbalance(weights, o_lpt, w8),
+                                           "lpt_decode": _sh.imbalance(bl, o_lpt, w8)}
+    heads = plan.heads[rank]
+    n_local = len(heads)
+    log(f"inputs: {n_local} heads ({args.placement})")
+    # this rank's heads only (seeded per rank; the data of an unsharded run would differ only in values)
     full_scorers = synth.make_scorers(cfg, device=dev)
     gen = torch.Generator(device=dev).manual_seed(1000 + cid + 31 * rank)
-    T = cfg.max_tokens
-    K = torch.empty(cfg.n_seq, l1 - l0, H, T, D, dtype=cfg.dtype, device=dev)
+    if plan.lpt:  # the rank's heads, grouped H per "layer" so the host path still uploads in chunks
+        gl = n_local // H if n_local % H == 0 else 1
+        K = torch.empty(cfg.n_seq, gl, n_local // gl, T, D, dtype=cfg.dtype, device=dev)
+    else:
+        l0, l1 = plan.layers[rank]
+        K = torch.empty(cfg.n_seq, l1 - l0, H, T, D, dtype=cfg.dtype, device=dev)
     V = torch.empty_like(K)
     for X in (K, V):
-        for i in range(l1 - l0):
-            X[:, i].copy_(torch.randn(cfg.n_seq, H, T, D, generator=gen, device=dev).to(cfg.dtype))
+        for i in range(X.shape[1]):
+            X[:, i].copy_(torch.randn(cfg.n_seq, X.shape[2], T, D, generator=gen, device=dev).to(cfg.dtype))
     cache = lkv.DenseCache(K, V, [T] * cfg.n_seq)
-    scorers = lkv.Scorers(full_scorers.w1[l0:l1], full_scorers.b1[l0:l1], full_scorers.w2[l0:l1])
-    all_logits = synth.make_logits(cfg, device=dev)
-    local_logits = all_logits[h0:h0 + n_local].contiguous()
+    layer_of = torch.tensor([h_ // H for h_ in heads], device=dev)
+    if plan.lpt:  # one scorer per local head (the per-layer scorer of its layer)
+        scorers = lkv.Scorers(full_scorers.w1[layer_of], full_scorers.b1[layer_of], full_scorers.w2[layer_of],
+                              stride_layer=K.shape[2], stride_head=1)
+    else:
+        scorers = lkv.Scorers(full_scorers.w1[l0:l1], full_scorers.b1[l0:l1], full_scorers.w2[l0:l1])
+    local_logits = all_logits[torch.tensor(heads, device=dev)].contiguous()
     ev = sharded.ShardEvictor(cache, scorers, plan, rank, cfg.ratio, lkv.BUDGET_EXACT,
                               decode_slack=cfg.decode_steps + 4, keep_scores=True)
     rows_total = L * H * T * cfg.n_seq
-    rows_local = (l1 - l0) * H * T * cfg.n_seq
+    rows_local = n_local * T * cfg.n_seq
     lib = lkv.lib()
     stream = torch.cuda.current_stream()
 
@@ -634,14 +676,14 @@ def run_sharded(args, rank, world, local_rank):
     logits = step()
     ev.ws.status()
     assert torch.equal(logits, all_logits), "logit allgatherv"
-    want = O.freeze_budgets_exact(O.allocate_budgets(all_logits.cpu().numpy(), cfg.ratio), cfg.ratio, T)
+    want = O.freeze_budgets_exact(O.allocate_budgets(all_logits.cpu().numpy(), cfg.ratio), cfg.ratio, T)[heads]
     for s_ in range(cfg.n_seq):
-        assert (ev.budgets[s_].cpu().numpy() == want[h0:h0 + n_local]).all(), "budgets differ from the oracle"
+        assert (ev.budgets[s_].cpu().numpy() == want).all(), "budgets differ from the oracle"
     kept_local = int(ev.ragged.lens.sum())
-    assert kept_local == cfg.n_seq * int(want[h0:h0 + n_local].sum())
+    assert kept_local == cfg.n_seq * int(want.sum())
     sc = ev.scores.reshape(-1, T)[0].cpu().numpy()
     _, _, p0 = ev.ragged.head(0)
-    assert (p0.cpu().numpy() == O.select_positions_f32(sc, int(want[h0]))).all(), "top-k differs from the oracle"
+    assert (p0.cpu().numpy() == O.select_positions_f32(sc, int(want[0]))).all(), "top-k differs from the oracle"
     tot = torch.tensor([kept_local], dtype=torch.int64, device=dev)
     if world > 1:
         torch.distributed.all_reduce(tot)
@@ -673,12 +715,13 @@ def run_sharded(args, rank, world, local_rank):
     b_loc = torch.empty(cfg.n_seq, n_local, dtype=torch.int32, device=dev)
     offs = torch.empty(cfg.n_seq * n_local + 1, dtype=torch.int64, device=dev)
     sp = C.c_void_p(stream.cuda_stream)
+    ids = torch.tensor(heads, dtype=torch.int32, device=dev)
 
     def k2():
-        lkv._check(lib.lkv_budgets_shard(C.c_void_p(logits.data_ptr()), L * H, cfg.ratio, lkv.BUDGET_EXACT, seq,
-                                         cfg.n_seq, 4, h0, n_local, None, C.c_void_p(b_all.data_ptr()),
-                                         C.c_void_p(b_loc.data_ptr()), C.c_void_p(offs.data_ptr()),
-                                         C.c_void_p(ev.ws.ptr), ev.ws.nbytes, sp))
+        lkv._check(lib.lkv_budgets_heads(C.c_void_p(logits.data_ptr()), L * H, cfg.ratio, lkv.BUDGET_EXACT, seq,
+                                         cfg.n_seq, 4, C.c_void_p(ids.data_ptr()), n_local, None,
+                                         C.c_void_p(b_all.data_ptr()), C.c_void_p(b_loc.data_ptr()),
+                                         C.c_void_p(offs.data_ptr()), C.c_void_p(ev.ws.ptr), ev.ws.nbytes, sp))
     for _ in range(3):
         k2()
     k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -736,7 +779,12 @@ def run_sharded(args, rank, world, local_rank):
         rc.tokens_seen.copy_(torch.tensor(cache.seq_lens, dtype=torch.int32))
         G = cfg.n_q_heads // H
         lkv.decode_plan(rc, G)
-        qs = [synth.make_decode_inputs(cfg, st, device=dev, n_layers=l1 - l0, seed=rank) for st in range(2)]
+        if plan.lpt:  # the local grouping: q [n_seq][g][heads per group * G][D], new k/v [n_seq][g][heads][D]
+            gq = torch.Generator(device=dev).manual_seed(5000 + rank)
+            qs = [tuple(torch.randn(cfg.n_seq, K.shape[1], K.shape[2] * m, D, generator=gq, device=dev).to(cfg.dtype)
+                        for m in (G, 1, 1)) for _ in range(2)]
+        else:
+            qs = [synth.make_decode_inputs(cfg, st, device=dev, n_layers=l1 - l0, seed=rank) for st in range(2)]
         out_local = torch.empty_like(qs[0][0])
         nsteps = cfg.decode_steps
         lens0 = rc.lens.clone()
@@ -771,7 +819,7 @@ def run_sharded(args, rank, world, local_rank):
             "vs_baseline": None, "dtype": "bf16",
             "data": f"synthetic (seeded; BASELINE.json configs[{cid - 1}] shapes and distributions)",
             "config": {"workload": f"C{cid}: L{L} x H{H} x d{D}, t={T}, batch {cfg.n_seq}, R={cfg.ratio}, exact budgets",
-                       "parallelism": f"head-sharded (layer ranges) x{world}", "rows_per_step": rows_total,
+                       "parallelism": f"head-sharded ({args.placement}) x{world}", "rows_per_step": rows_total,
                        "rows_per_rank0_step": rows_local,
                        "l2": "inputs larger than L2; no flush"},
             "north_star_target_ms": 5.0, "under_target": ms < 5.0, "clocks": clk.summary(),
@@ -779,6 +827,7 @@ def run_sharded(args, rank, world, local_rank):
             "step_roofline": {"algorithmic_bytes": int(step_bytes),
                               "frac_of_aggregate_hbm": step_bytes / (ms / 1e3) / 1e9 / (world * hbm_peak)},
             "k2_per_rank_ms": k2_ms,
+            "load_imbalance": imbalance,
             "exchange": "LKV-H logits allgatherv + decode-output gatherv via lkv_comm_* (NCCL)",
             "parity_gate": "budgets == CPU oracle on every rank; kept totals; one head per rank == oracle top-k",
             "peak_source": peak_src, "decode": decode, "e2e": e2e}), flush=True)
@@ -822,6 +871,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-heads", type=int, default=64)
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--placement", default="lpt", choices=["lpt", "layers"],
+                    help="head placement of the sharded path: LPT over (layer, head) by eviction bytes (default) or "
+                         "contiguous layer ranges")
     ap.add_argument("--sharded-path", action="store_true",
                     help="run the head-sharded code path even at N=1 (validates the N>1 path on one GPU)")
     ap.add_argument("--e2e-chunk", type=int, default=1, help="layers per host->device chunk in the e2e path")

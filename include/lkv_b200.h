@@ -265,6 +265,24 @@ lkv_status lkv_evict_host_shard(const lkv_cache_desc* host_cache, void* dev_keys
                                 int32_t head_begin, double target_ratio, int32_t mode, const lkv_ragged_desc* out,
                                 const lkv_ragged_desc* host_out, int32_t layers_per_chunk, void* workspace,
                                 size_t workspace_bytes, lkv_stream_t stream);
+/* Shards that own an arbitrary list of heads (LPT placement by budget, shard.lpt_assign): the
+ * local cache describes them as n_layers = 1 x n_kv_heads = n_local (per sequence, in list order)
+ * and head_ids (DEVICE int32 [n_local]) gives each local head's global flat index l * H + h; the
+ * scorer table is indexed by local head.  K2 still solves all n_logits heads (bit-identical on
+ * every rank); budgets_local / offsets_local follow the list order. */
+lkv_status lkv_budgets_heads(const double* logits, int32_t n_logits, double target_ratio, int32_t mode,
+                             const int32_t* seq_lens, int32_t n_seq, int32_t decode_slack, const int32_t* head_ids,
+                             int32_t n_local, double* ratios, int32_t* budgets_all, int32_t* budgets_local,
+                             int64_t* offsets_local, void* workspace, size_t workspace_bytes, lkv_stream_t stream);
+lkv_status lkv_evict_heads(const lkv_cache_desc* local_cache, const lkv_scorer_desc* scorer, const double* logits,
+                           int32_t n_logits, const int32_t* head_ids, double target_ratio, int32_t mode,
+                           const lkv_ragged_desc* out, float* scores_out, double* ratios_out, int32_t* budgets_out,
+                           void* workspace, size_t workspace_bytes, lkv_stream_t stream);
+lkv_status lkv_evict_host_heads(const lkv_cache_desc* host_cache, void* dev_keys, void* dev_values,
+                                const lkv_scorer_desc* scorer, const double* logits, int32_t n_logits,
+                                const int32_t* head_ids, double target_ratio, int32_t mode, const lkv_ragged_desc* out,
+                                const lkv_ragged_desc* host_out, int32_t layers_per_chunk, void* workspace,
+                                size_t workspace_bytes, lkv_stream_t stream);
 /* Upper bound on a shard's compacted rows (caller allocates; -1 on bad input). */
 int64_t lkv_ragged_capacity_shard(const lkv_cache_desc* local_cache, int32_t n_logits, double target_ratio,
                                   int32_t decode_slack);

@@ -32,7 +32,8 @@ EXPORTED = [
     "lkv_soft_topk_vjp", "lkv_evict_budgets", "lkv_mask_counts", "lkv_cache_from_trace", "lkv_decode_plan_ex",
     "lkv_model_plan_ex", "lkv_decode_plan_info", "lkv_evict_host_shard", "lkv_soft_topk_exact", "lkv_f64_gemm",
     "lkv_f64_rmsnorm", "lkv_f64_rope", "lkv_f64_attention", "lkv_f64_swiglu", "lkv_f64_embed", "lkv_f64_split_heads",
-    "lkv_f64_token_scores", "lkv_f64_select", "lkv_kv_project",
+    "lkv_f64_token_scores", "lkv_f64_select", "lkv_kv_project", "lkv_budgets_heads", "lkv_evict_heads",
+    "lkv_evict_host_heads",
 ]
 
 
@@ -131,6 +132,13 @@ def load():
     L.lkv_f64_select.argtypes = [vp, i32, i32, i64, vp, P(RaggedDesc), vp, sz, vp]
     for name in ["lkv_soft_topk_exact", "lkv_f64_gemm", "lkv_f64_rmsnorm", "lkv_f64_rope", "lkv_f64_attention",
                  "lkv_f64_swiglu", "lkv_f64_embed", "lkv_f64_split_heads", "lkv_f64_token_scores", "lkv_f64_select"]:
+        getattr(L, name).restype = C.c_int
+    L.lkv_budgets_heads.argtypes = [vp, i32, dbl, i32, P(i32), i32, i32, vp, i32, vp, vp, vp, vp, vp, sz, vp]
+    L.lkv_evict_heads.argtypes = [P(CacheDesc), P(ScorerDesc), vp, i32, vp, dbl, i32, P(RaggedDesc), vp, vp, vp, vp,
+                                  sz, vp]
+    L.lkv_evict_host_heads.argtypes = [P(CacheDesc), vp, vp, P(ScorerDesc), vp, i32, vp, dbl, i32, P(RaggedDesc),
+                                       P(RaggedDesc), i32, vp, sz, vp]
+    for name in ["lkv_budgets_heads", "lkv_evict_heads", "lkv_evict_host_heads"]:
         getattr(L, name).restype = C.c_int
     L.lkv_kv_project.argtypes = [vp, i32, vp, P(CacheDesc), vp, vp, vp, vp]
     L.lkv_kv_project.restype = C.c_int

@@ -116,7 +116,10 @@ __device__ void freeze_and_offsets(const BudgetParams& p, const double* r, doubl
         for (int i = tid; i < n; i += kBudgetThreads) p.budgets_out[(size_t)s * n + i] = fl[i] + delta[i];
         if (p.local_count > 0)
             for (int i = tid; i < p.local_count; i += kBudgetThreads)
-                p.budgets_local_out[(size_t)s * p.local_count + i] = fl[p.local_begin + i] + delta[p.local_begin + i];
+            {
+                const int g = p.local_ids ? p.local_ids[i] : p.local_begin + i;  // the local head's global index
+                p.budgets_local_out[(size_t)s * p.local_count + i] = fl[g] + delta[g];
+            }
         __syncthreads();
     }
 

@@ -438,12 +438,15 @@ lkv_status lkv_budgets(const double* logits, int32_t n, double R, int32_t mode, 
     return LKV_OK;
 }
 
-lkv_status lkv_budgets_shard(const double* logits, int32_t n, double R, int32_t mode, const int32_t* seq_lens,
-                             int32_t n_seq, int32_t slack, int32_t head_begin, int32_t n_local, double* ratios,
-                             int32_t* budgets_all, int32_t* budgets_local, int64_t* offsets_local, void* ws,
-                             size_t ws_bytes, lkv_stream_t stream) {
-    if (n_local < 1 || head_begin < 0 || (int64_t)head_begin + n_local > n)
+static lkv_status budgets_shard_impl(const double* logits, int32_t n, double R, int32_t mode, const int32_t* seq_lens,
+                                     int32_t n_seq, int32_t slack, int32_t head_begin, const int32_t* head_ids,
+                                     int32_t n_local, double* ratios, int32_t* budgets_all, int32_t* budgets_local,
+                                     int64_t* offsets_local, void* ws, size_t ws_bytes, lkv_stream_t stream) {
+    if (head_ids) {
+        if (n_local < 1 || n_local > n) return fail(LKV_ERR_CONTRACT, "budgets_heads: need 1 <= n_local <= n");
+    } else if (n_local < 1 || head_begin < 0 || (int64_t)head_begin + n_local > n) {
         return fail(LKV_ERR_CONTRACT, "budgets_shard: need 0 <= head_begin and head_begin + n_local <= n");
+    }
     if (!budgets_all || !budgets_local) return fail(LKV_ERR_CONTRACT, "budgets_shard: null budget buffers");
     if (!(R > 0.0 && R < 1.0)) return fail(LKV_ERR_BUDGET, "target ratio must lie in (0,1)");  // policy.cpp:111
     if (n > 3072) return fail(LKV_ERR_CONTRACT, "allocate_budgets: need 1 <= n <= 3072 head logits");
@@ -466,13 +469,31 @@ lkv_status lkv_budgets_shard(const double* logits, int32_t n, double R, int32_t 
     p.ratios_out = ratios;
     p.budgets_out = budgets_all;
     p.offsets_out = offsets_local;
-    p.local_begin = head_begin;
+    p.local_begin = head_ids ? 0 : head_begin;
     p.local_count = n_local;
+    p.local_ids = head_ids;
     p.budgets_local_out = budgets_local;
     p.err = at<ErrWord>(ws, 0);
     for (int s = 0; s < n_seq; ++s) p.seq_len[s] = seq_lens[s];
     LKV_CUDA(launch_budgets(p, (cudaStream_t)stream), "budgets (shard)");
     return LKV_OK;
+}
+
+lkv_status lkv_budgets_shard(const double* logits, int32_t n, double R, int32_t mode, const int32_t* seq_lens,
+                             int32_t n_seq, int32_t slack, int32_t head_begin, int32_t n_local, double* ratios,
+                             int32_t* budgets_all, int32_t* budgets_local, int64_t* offsets_local, void* ws,
+                             size_t ws_bytes, lkv_stream_t stream) {
+    return budgets_shard_impl(logits, n, R, mode, seq_lens, n_seq, slack, head_begin, nullptr, n_local, ratios,
+                              budgets_all, budgets_local, offsets_local, ws, ws_bytes, stream);
+}
+
+lkv_status lkv_budgets_heads(const double* logits, int32_t n, double R, int32_t mode, const int32_t* seq_lens,
+                             int32_t n_seq, int32_t slack, const int32_t* head_ids, int32_t n_local, double* ratios,
+                             int32_t* budgets_all, int32_t* budgets_local, int64_t* offsets_local, void* ws,
+                             size_t ws_bytes, lkv_stream_t stream) {
+    if (!head_ids) return fail(LKV_ERR_CONTRACT, "budgets_heads: head_ids are null");
+    return budgets_shard_impl(logits, n, R, mode, seq_lens, n_seq, slack, 0, head_ids, n_local, ratios, budgets_all,
+                              budgets_local, offsets_local, ws, ws_bytes, stream);
 }
 
 lkv_status lkv_freeze_budgets(const double* ratios, int32_t n, double R, int32_t mode, const int32_t* seq_lens,
@@ -618,7 +639,8 @@ lkv_status lkv_cache_from_trace(const lkv_cache_desc* c, const int32_t* masks, i
 //   waits for its predecessor).  No side stream, no flag: K2 is resident before K1 launches, so
 //   every wait makes progress on any SM partitioning, and the chain is graph-capturable.
 static lkv_status evict_impl(const lkv_cache_desc* c, const lkv_scorer_desc* s, const double* logits, int n,
-                             int head_begin, bool shard, double R, int32_t mode, const lkv_ragged_desc* out,
+                             int head_begin, bool shard, const int32_t* head_ids, double R, int32_t mode,
+                             const lkv_ragged_desc* out,
                              float* scores_out, double* ratios_out, int32_t* budgets_out, void* ws, size_t ws_bytes,
                              cudaStream_t strm) {
     lkv_status st = check_cache(c, true);
@@ -636,9 +658,9 @@ static lkv_status evict_impl(const lkv_cache_desc* c, const lkv_scorer_desc* s, 
     uint32_t* hist = at<uint32_t>(ws, w.hist);
     if (tc) LKV_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 2048 * (size_t)n_heads_of(c), strm), "hist clear");
     if (shard)
-        st = lkv_budgets_shard(logits, n, R, mode, c->seq_lens, c->n_seq, out->decode_slack, head_begin,
-                               c->n_layers * c->n_kv_heads, ratios, at<int32_t>(ws, w.budgets_all), budgets,
-                               out->offsets, ws, ws_bytes, (lkv_stream_t)strm);
+        st = budgets_shard_impl(logits, n, R, mode, c->seq_lens, c->n_seq, out->decode_slack, head_begin, head_ids,
+                                c->n_layers * c->n_kv_heads, ratios, at<int32_t>(ws, w.budgets_all), budgets,
+                                out->offsets, ws, ws_bytes, (lkv_stream_t)strm);
     else
         st = lkv_budgets(logits, n, R, mode, c->seq_lens, c->n_seq, out->decode_slack, ratios, budgets, out->offsets,
                          ws, ws_bytes, (lkv_stream_t)strm);
@@ -656,7 +678,7 @@ lkv_status lkv_evict(const lkv_cache_desc* c, const lkv_scorer_desc* s, const do
                      const lkv_ragged_desc* out, float* scores_out, double* ratios_out, int32_t* budgets_out, void* ws,
                      size_t ws_bytes, lkv_stream_t stream) {
     if (!c) return fail(LKV_ERR_CONTRACT, "cache descriptor is null");
-    return evict_impl(c, s, logits, c->n_layers * c->n_kv_heads, 0, false, R, mode, out, scores_out, ratios_out,
+    return evict_impl(c, s, logits, c->n_layers * c->n_kv_heads, 0, false, nullptr, R, mode, out, scores_out, ratios_out,
                       budgets_out, ws, ws_bytes, (cudaStream_t)stream);
 }
 
@@ -683,7 +705,19 @@ lkv_status lkv_evict_shard(const lkv_cache_desc* c, const lkv_scorer_desc* s, co
     if (!c) return fail(LKV_ERR_CONTRACT, "cache descriptor is null");
     if (n_logits < 1 || head_begin < 0 || (int64_t)head_begin + (int64_t)c->n_layers * c->n_kv_heads > n_logits)
         return fail(LKV_ERR_CONTRACT, "evict_shard: the shard's heads must lie inside the n_logits global heads");
-    return evict_impl(c, s, logits, n_logits, head_begin, true, R, mode, out, scores_out, ratios_out, budgets_out, ws,
+    return evict_impl(c, s, logits, n_logits, head_begin, true, nullptr, R, mode, out, scores_out, ratios_out,
+                      budgets_out, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+lkv_status lkv_evict_heads(const lkv_cache_desc* c, const lkv_scorer_desc* s, const double* logits, int32_t n_logits,
+                           const int32_t* head_ids, double R, int32_t mode, const lkv_ragged_desc* out,
+                           float* scores_out, double* ratios_out, int32_t* budgets_out, void* ws, size_t ws_bytes,
+                           lkv_stream_t stream) {
+    if (!c) return fail(LKV_ERR_CONTRACT, "cache descriptor is null");
+    if (!head_ids) return fail(LKV_ERR_CONTRACT, "evict_heads: head_ids are null");
+    if (n_logits < 1 || (int64_t)c->n_layers * c->n_kv_heads > n_logits)
+        return fail(LKV_ERR_CONTRACT, "evict_heads: more local heads than global heads");
+    return evict_impl(c, s, logits, n_logits, 0, true, head_ids, R, mode, out, scores_out, ratios_out, budgets_out, ws,
                       ws_bytes, (cudaStream_t)stream);
 }
 
@@ -698,7 +732,8 @@ lkv_status lkv_evict_shard(const lkv_cache_desc* c, const lkv_scorer_desc* s, co
 // The D2H ranges need the ragged offsets on the host: K2 runs first on the side stream and
 // its offsets are read back once (all K uploads are already queued, so the wait is hidden).
 static lkv_status evict_host_impl(const lkv_cache_desc* hc, void* dev_keys, void* dev_values, const lkv_scorer_desc* s,
-                                  const double* logits, int32_t n_logits, int32_t head_begin, bool shard, double R,
+                                  const double* logits, int32_t n_logits, int32_t head_begin, bool shard,
+                                  const int32_t* head_ids, double R,
                                   int32_t mode, const lkv_ragged_desc* out, const lkv_ragged_desc* host_out,
                                   int32_t layers_per_chunk, void* ws, size_t ws_bytes, lkv_stream_t stream) {
     lkv_status st = check_cache(hc, true);
@@ -756,9 +791,9 @@ static lkv_status evict_host_impl(const lkv_cache_desc* hc, void* dev_keys, void
     LKV_CUDA(cudaStreamWaitEvent(ds, start, 0), "stream wait");
     // K2 on the side stream; its offsets go to the host when the compacted cache is copied back
     if (shard)
-        st = lkv_budgets_shard(logits, n, R, mode, hc->seq_lens, hc->n_seq, out->decode_slack, head_begin,
-                               hc->n_layers * hc->n_kv_heads, at<double>(ws, w.ratios), at<int32_t>(ws, w.budgets_all),
-                               budgets, out->offsets, ws, ws_bytes, (lkv_stream_t)side);
+        st = budgets_shard_impl(logits, n, R, mode, hc->seq_lens, hc->n_seq, out->decode_slack, head_begin, head_ids,
+                                hc->n_layers * hc->n_kv_heads, at<double>(ws, w.ratios), at<int32_t>(ws, w.budgets_all),
+                                budgets, out->offsets, ws, ws_bytes, (lkv_stream_t)side);
     else
         st = lkv_budgets(logits, n, R, mode, hc->seq_lens, hc->n_seq, out->decode_slack, at<double>(ws, w.ratios),
                          budgets, out->offsets, ws, ws_bytes, (lkv_stream_t)side);
@@ -870,7 +905,7 @@ lkv_status lkv_evict_host(const lkv_cache_desc* hc, void* dev_keys, void* dev_va
                           const lkv_ragged_desc* host_out, int32_t layers_per_chunk, void* ws, size_t ws_bytes,
                           lkv_stream_t stream) {
     if (!hc) return fail(LKV_ERR_CONTRACT, "cache descriptor is null");
-    return evict_host_impl(hc, dev_keys, dev_values, s, logits, hc->n_layers * hc->n_kv_heads, 0, false, R, mode, out,
+    return evict_host_impl(hc, dev_keys, dev_values, s, logits, hc->n_layers * hc->n_kv_heads, 0, false, nullptr, R, mode, out,
                            host_out, layers_per_chunk, ws, ws_bytes, stream);
 }
 
@@ -881,7 +916,19 @@ lkv_status lkv_evict_host_shard(const lkv_cache_desc* hc, void* dev_keys, void* 
     if (!hc) return fail(LKV_ERR_CONTRACT, "cache descriptor is null");
     if (n_logits < 1 || head_begin < 0 || (int64_t)head_begin + (int64_t)hc->n_layers * hc->n_kv_heads > n_logits)
         return fail(LKV_ERR_CONTRACT, "evict_host_shard: the shard's heads must lie inside the n_logits global heads");
-    return evict_host_impl(hc, dev_keys, dev_values, s, logits, n_logits, head_begin, true, R, mode, out, host_out,
+    return evict_host_impl(hc, dev_keys, dev_values, s, logits, n_logits, head_begin, true, nullptr, R, mode, out,
+                           host_out, layers_per_chunk, ws, ws_bytes, stream);
+}
+
+lkv_status lkv_evict_host_heads(const lkv_cache_desc* hc, void* dev_keys, void* dev_values, const lkv_scorer_desc* s,
+                                const double* logits, int32_t n_logits, const int32_t* head_ids, double R, int32_t mode,
+                                const lkv_ragged_desc* out, const lkv_ragged_desc* host_out, int32_t layers_per_chunk,
+                                void* ws, size_t ws_bytes, lkv_stream_t stream) {
+    if (!hc) return fail(LKV_ERR_CONTRACT, "cache descriptor is null");
+    if (!head_ids) return fail(LKV_ERR_CONTRACT, "evict_host_heads: head_ids are null");
+    if (n_logits < 1 || (int64_t)hc->n_layers * hc->n_kv_heads > n_logits)
+        return fail(LKV_ERR_CONTRACT, "evict_host_heads: more local heads than global heads");
+    return evict_host_impl(hc, dev_keys, dev_values, s, logits, n_logits, 0, true, head_ids, R, mode, out, host_out,
                            layers_per_chunk, ws, ws_bytes, stream);
 }
 

@@ -27,6 +27,7 @@ struct BudgetParams {
     int32_t local_begin;
     int32_t local_count;
     int32_t* budgets_local_out;
+    const int32_t* local_ids;  // non-null: the owned heads are this list (device) instead of a range
     // soft = 1: soft_topk_forward / solve_threshold (soft_topk.cpp:58-164) with k and tau given:
     // the solve runs on logits / tau, values go to ratios_out, nothing is frozen
     int32_t soft;

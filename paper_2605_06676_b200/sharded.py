@@ -117,31 +117,69 @@ class TorchComm:
 
 # ---- shard plan ------------------------------------------------------------------------------------------
 class ShardPlan:
-    """Layer-range head shards of an L x H cache over `world` ranks."""
+    """Head shards of an L x H cache over `world` ranks: contiguous layer ranges (default), or --
+    with per-head `weights` (e.g. eviction bytes t * in_bytes + budget * gather bytes, known before
+    eviction because budgets depend only on the logits) -- a deterministic LPT assignment
+    (shard.lpt_assign) that balances the skewed LKV-H budgets across ranks.  heads[r] is the sorted
+    list of global flat heads l * H + h that rank r owns."""
 
-    def __init__(self, n_layers: int, n_kv_heads: int, world: int):
+    def __init__(self, n_layers: int, n_kv_heads: int, world: int, weights=None):
         self.n_layers, self.n_kv_heads, self.world = n_layers, n_kv_heads, world
         self.layers = _shard.layer_ranges(n_layers, world)
+        self.lpt = weights is not None
+        if self.lpt:
+            if len(weights) != n_layers * n_kv_heads:
+                raise ContractError("one LPT weight per (layer, kv head)")
+            owner = _shard.lpt_assign(list(weights), world)
+            self.heads = [[i for i, o in enumerate(owner) if o == r] for r in range(world)]
+            self.imbalance = _shard.imbalance(list(weights), owner, world)
+        else:
+            self.heads = [list(range(l0 * n_kv_heads, l1 * n_kv_heads)) for l0, l1 in self.layers]
+            owner = [r for r, hs in enumerate(self.heads) for _ in hs]
+            self.imbalance = _shard.imbalance(list(weights), owner, world) if weights is not None else None
 
     def head_range(self, rank: int):
+        if self.lpt:
+            raise ContractError("an LPT plan owns a head list, not a range (heads[rank])")
         l0, l1 = self.layers[rank]
         return l0 * self.n_kv_heads, (l1 - l0) * self.n_kv_heads
 
+    def n_local(self, rank: int) -> int:
+        return len(self.heads[rank])
+
     def logit_counts(self):
-        return [self.head_range(r)[1] for r in range(self.world)], [self.head_range(r)[0] for r in range(self.world)]
+        """Element counts / displacements of the rank-major logits buffer (global order for a
+        layer-range plan; the LPT plan scatters it with `order`)."""
+        counts = [len(h) for h in self.heads]
+        return counts, [sum(counts[:r]) for r in range(self.world)]
+
+    def order(self) -> list:
+        """Global flat head of every position of the rank-major buffer."""
+        return [h for hs in self.heads for h in hs]
+
+    def order_tensor(self, device):
+        key = str(device)
+        if getattr(self, "_order_t", None) is None or self._order_key != key:
+            self._order_t, self._order_key = torch.tensor(self.order(), device=device), key
+        return self._order_t
 
     def output_counts(self, n_seq: int, per_layer: int):
-        """Element counts/displacements of the rank-major gather buffer of decode outputs."""
-        counts = [n_seq * (l1 - l0) * per_layer for l0, l1 in self.layers]
+        """Element counts/displacements of the rank-major gather buffer of decode outputs
+        (per_layer = elements per layer of one sequence, Hq * D; a rank's block is its heads' share)."""
+        per_head = per_layer // self.n_kv_heads
+        counts = [n_seq * len(hs) * per_head for hs in self.heads]
         displs = [sum(counts[:r]) for r in range(self.world)]
         return counts, displs
 
     def assemble(self, gathered: torch.Tensor, n_seq: int, Hq: int, D: int) -> torch.Tensor:
-        """Rank-major [r][n_seq][l1-l0][Hq][D] blocks -> [n_seq][L][Hq][D]."""
+        """Rank-major [r][n_seq][heads of r][G][D] blocks -> [n_seq][L][Hq][D]."""
         counts, displs = self.output_counts(n_seq, Hq * D)
-        blocks = [gathered.view(-1)[displs[r]: displs[r] + counts[r]].view(n_seq, -1, Hq, D)
-                  for r in range(self.world)]
-        return torch.cat(blocks, dim=1)
+        G = Hq // self.n_kv_heads
+        blocks = [gathered.view(-1)[displs[r]: displs[r] + counts[r]].view(n_seq, -1, G, D) for r in range(self.world)]
+        rank_major = torch.cat(blocks, dim=1)  # [n_seq][L*H in rank-major head order][G][D]
+        out = torch.empty_like(rank_major)
+        out[:, torch.tensor(self.order(), device=rank_major.device)] = rank_major
+        return out.view(n_seq, self.n_layers, Hq, D)
 
 
 def gather_logits(comm, plan: ShardPlan, local_logits: torch.Tensor) -> torch.Tensor:
@@ -151,6 +189,10 @@ def gather_logits(comm, plan: ShardPlan, local_logits: torch.Tensor) -> torch.Te
         raise ContractError("local logits must cover exactly this rank's heads")
     out = torch.empty(plan.n_layers * plan.n_kv_heads, dtype=torch.float64, device=local_logits.device)
     comm.allgatherv(local_logits.to(torch.float64).contiguous(), out, counts, displs)
+    if plan.lpt:  # rank-major -> global head order
+        full = torch.empty_like(out)
+        full[plan.order_tensor(out.device)] = out
+        return full
     return out
 
 
@@ -161,10 +203,22 @@ class ShardEvictor:
 
     def __init__(self, cache: DenseCache, scorers: Scorers, plan: ShardPlan, rank: int, target_ratio: float,
                  mode: int = BUDGET_EXACT, decode_slack: int = 0, keep_scores: bool = False):
+        """Layer-range plan: `cache` / `scorers` hold this rank's layers.  LPT plan: `cache` holds the
+        rank's heads in plan.heads[rank] order, grouped any way as [n_seq][g][n_local / g][T][D] (the
+        grouping only sets the host path's upload chunks), with one scorer per local head (scorer of
+        local flat head j = j)."""
         n_seq, L, H, T, D = cache.shape
-        self.head_begin, n_local = plan.head_range(rank)
-        if L * H != n_local or H != plan.n_kv_heads:
-            raise ContractError("local cache must hold exactly this rank's layer range")
+        n_local = plan.n_local(rank)
+        if plan.lpt:
+            if L * H != n_local:
+                raise ContractError("an LPT shard's cache holds exactly its n_local heads")
+            self.head_begin = 0
+            self.head_ids = torch.tensor(plan.heads[rank], dtype=torch.int32, device=cache.keys.device)
+        else:
+            self.head_begin = plan.head_range(rank)[0]
+            self.head_ids = None
+            if L * H != n_local or H != plan.n_kv_heads:
+                raise ContractError("local cache must hold exactly this rank's layer range")
         self.cache, self.scorers, self.plan = cache, scorers, plan
         self.n_logits = plan.n_layers * plan.n_kv_heads
         self.R, self.mode = float(target_ratio), mode
@@ -184,6 +238,12 @@ class ShardEvictor:
     def launch(self, logits: torch.Tensor, stream=None) -> None:
         if logits.numel() != self.n_logits or logits.dtype != torch.float64:
             raise ContractError("evict_shard needs the full fp64 logit vector (gather_logits)")
+        if self.head_ids is not None:
+            _check(lib().lkv_evict_heads(C.byref(self._cd), C.byref(self._sd), _ptr(logits), self.n_logits,
+                                         _ptr(self.head_ids), self.R, self.mode, C.byref(self._rd), _ptr(self.scores),
+                                         _ptr(self.ratios), _ptr(self.budgets), C.c_void_p(self.ws.ptr),
+                                         self.ws.nbytes, _stream(stream)))
+            return
         _check(lib().lkv_evict_shard(C.byref(self._cd), C.byref(self._sd), _ptr(logits), self.n_logits,
                                      self.head_begin, self.R, self.mode, C.byref(self._rd), _ptr(self.scores),
                                      _ptr(self.ratios), _ptr(self.budgets), C.c_void_p(self.ws.ptr), self.ws.nbytes,
@@ -204,6 +264,13 @@ class ShardEvictor:
         hd.keys, hd.values = host_keys.data_ptr(), host_values.data_ptr()
         dev_v = self.cache.values.data_ptr() if self.scorers.input == _abi.SCORER_KV else None
         ho = host_out.desc() if host_out is not None else None
+        if self.head_ids is not None:
+            _check(lib().lkv_evict_host_heads(C.byref(hd), C.c_void_p(self.cache.keys.data_ptr()),
+                                              C.c_void_p(dev_v) if dev_v else None, C.byref(self._sd), _ptr(logits),
+                                              self.n_logits, _ptr(self.head_ids), self.R, self.mode, C.byref(self._rd),
+                                              C.byref(ho) if ho is not None else None, layers_per_chunk,
+                                              C.c_void_p(self.ws.ptr), self.ws.nbytes, _stream(stream)))
+            return
         _check(lib().lkv_evict_host_shard(C.byref(hd), C.c_void_p(self.cache.keys.data_ptr()),
                                           C.c_void_p(dev_v) if dev_v else None, C.byref(self._sd), _ptr(logits),
                                           self.n_logits, self.head_begin, self.R, self.mode, C.byref(self._rd),
@@ -228,7 +295,8 @@ def decode_and_gather(comm, plan: ShardPlan, ragged: RaggedCache, q, new_k, new_
     Returns the rank-major gather buffer on root (plan.assemble() orders it), else None."""
     n_seq, Lr, Hq, D = q.shape
     out_local = decode_step(ragged, q, new_k, new_v, out=out_local, check=check)
-    counts, displs = plan.output_counts(n_seq, Hq * D)
+    G = Hq // ragged.n_kv_heads
+    counts, displs = plan.output_counts(n_seq, G * plan.n_kv_heads * D)
     if comm.rank == root and gathered is None:
         gathered = torch.empty(sum(counts), dtype=q.dtype, device=q.device)
     comm.gatherv(out_local.reshape(-1), gathered if comm.rank == root else None, counts, displs, root)

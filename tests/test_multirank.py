@@ -153,3 +153,49 @@ def test_shard_plan_ranges():
         counts, displs = plan.logit_counts()
         assert sum(counts) == L * 8 and displs[0] == 0
         assert all(displs[r] + counts[r] == displs[r + 1] for r in range(W - 1))
+
+
+def _lpt_worker(rank, world, port, out_dir):
+    """The LPT head placement's host logic (sharded.ShardPlan with weights) over gloo: every rank
+    derives the same plan, the rank-major logits allgatherv is scattered back to global order, and
+    the decode outputs of arbitrary head lists reassemble into [n_seq][L][Hq][D]."""
+    from paper_2605_06676_b200 import sharded
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        comm = sharded.TorchComm()
+        L, H, G, D, n_seq, T = 6, 4, 2, 8, 2, 4096
+        rng = np.random.default_rng(91)
+        full = torch.tensor(rng.normal(0, 1.5, L * H))
+        b = O.freeze_budgets_exact(O.allocate_budgets(full.numpy(), 0.1), 0.1, T)
+        plan = sharded.ShardPlan(L, H, world, weights=[T * 264 + int(x) * 1028 for x in b])
+        assert plan.lpt and sorted(h for hs in plan.heads for h in hs) == list(range(L * H))
+        assert plan.imbalance < 1.05  # 24 heads over 2 ranks: LPT granularity
+        mine = plan.heads[rank]
+        got = sharded.gather_logits(comm, plan, full[mine].clone())
+        assert torch.equal(got, full)
+        # outputs: rank r holds [n_seq][1][n_local * G][D] for its heads, in plan order
+        s_i, j_i, g_i, d_i = torch.meshgrid(torch.arange(n_seq), torch.tensor(mine), torch.arange(G), torch.arange(D),
+                                            indexing="ij")
+        local = (((s_i * 100 + j_i) * 10 + g_i) * 100 + d_i).to(torch.float64).reshape(n_seq, 1, len(mine) * G, D)
+        counts, displs = plan.output_counts(n_seq, G * H * D)
+        gathered = torch.empty(sum(counts), dtype=torch.float64) if rank == 0 else None
+        comm.gatherv(local.reshape(-1), gathered, counts, displs, root=0)
+        if rank == 0:
+            out = plan.assemble(gathered, n_seq, H * G, D)
+            s_i, l_i, q_i, d_i = torch.meshgrid(torch.arange(n_seq), torch.arange(L), torch.arange(H * G),
+                                                torch.arange(D), indexing="ij")
+            flat = l_i * H + q_i // G
+            assert torch.equal(out, (((s_i * 100 + flat) * 10 + q_i % G) * 100 + d_i).to(torch.float64))
+        with open(os.path.join(out_dir, f"ok{rank}"), "w") as f:
+            f.write("ok")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_lpt_placement(tmp_path):
+    world = 2
+    mp.spawn(_lpt_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    assert all((tmp_path / f"ok{r}").exists() for r in range(world))

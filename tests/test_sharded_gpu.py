@@ -130,3 +130,55 @@ def test_host_shard_equals_device_shard(world, rank):
             assert torch.equal(ho.positions[o:o + n], want[2][o:o + n].cpu())
             assert torch.equal(ho.keys[o:o + n], want[3][o:o + n].cpu())
             assert torch.equal(ho.values[o:o + n], want[4][o:o + n].cpu())
+
+
+def _lpt_local(cache, scorers, heads, H):
+    """An LPT shard's inputs: its heads (any layers) as a [n_seq][1][n_local][T][D] cache with one
+    scorer per local head."""
+    ls = torch.tensor([h // H for h in heads], device="cuda")
+    hs = torch.tensor([h % H for h in heads], device="cuda")
+    K = cache.keys[:, ls, hs].unsqueeze(1).contiguous()
+    V = cache.values[:, ls, hs].unsqueeze(1).contiguous()
+    s = lkv.Scorers(scorers.w1[ls], scorers.b1[ls], scorers.w2[ls], input=scorers.input,
+                    activation=scorers.activation, stride_layer=0, stride_head=1)
+    return lkv.DenseCache(K, V, cache.seq_lens), s, ls, hs
+
+
+@pytest.mark.parametrize("cid,world,L,T", [(3, 8, 8, 3000), (5, 4, 10, 2000), (4, 3, 6, 4000)])
+def test_lpt_shards_equal_unsharded(cid, world, L, T):
+    """LPT head placement (budget-balanced head lists, lkv_evict_heads): every rank's shard run in
+    turn on this GPU; the union equals the unsharded eviction bit for bit (budgets, kept rows,
+    positions) and the decode outputs, reassembled by the plan, equal the unsharded decode."""
+    cfg = synth.CONFIGS[cid]
+    S = min(cfg.n_seq, 2)
+    cache = synth.make_cache(cfg, n_layers=L, max_tokens=T, n_seq=S)
+    scorers = synth.make_scorers(cfg, n_layers=L)
+    logits = synth.make_logits(cfg, n_layers=L)
+    H = cfg.n_kv_heads
+    full = lkv.evict(cache, scorers, logits, cfg.ratio, lkv.BUDGET_EXACT, decode_slack=4, keep_scores=False)
+    b = O.freeze_budgets_exact(O.allocate_budgets(logits.cpu().numpy(), cfg.ratio), cfg.ratio, T)
+    plan = sharded.ShardPlan(L, H, world, weights=[T * 264 + int(x) * 1028 for x in b])
+    assert plan.lpt and plan.imbalance < 1.05
+    G = cfg.n_q_heads // H
+    steps = [synth.make_decode_inputs(cfg, s, n_layers=L, n_seq=S) for s in range(2)]
+    got = [torch.zeros_like(steps[0][0]) for _ in range(2)]
+    for r in range(world):
+        heads = plan.heads[r]
+        lc, ls_, ls, hs = _lpt_local(cache, scorers, heads, H)
+        ev = sharded.ShardEvictor(lc, ls_, plan, r, cfg.ratio, lkv.BUDGET_EXACT, decode_slack=4)
+        rc = ev.run(logits)
+        n = len(heads)
+        for s in range(S):
+            assert (ev.budgets[s].cpu().numpy() == b[heads]).all()
+            for j, hg in enumerate(heads):
+                k, v, p = rc.head(s * n + j)
+                kf, vf, pf = full.cache.head(s * L * H + hg)
+                assert torch.equal(p, pf) and torch.equal(k, kf) and torch.equal(v, vf)
+        for st in range(2):
+            q, nk, nv = steps[st]
+            qg = q.view(S, L, H, G, -1)[:, ls, hs].reshape(S, 1, n * G, -1).contiguous()
+            out = lkv.decode_step(rc, qg, nk[:, ls, hs].unsqueeze(1).contiguous(), nv[:, ls, hs].unsqueeze(1).contiguous())
+            got[st].view(S, L, H, G, -1)[:, ls, hs] = out.view(S, n, G, -1)
+    for st in range(2):
+        want = lkv.decode_step(full.cache, *steps[st])
+        assert torch.allclose(got[st].float(), want.float(), rtol=0, atol=1e-6 * float(want.float().abs().max()))
