@@ -144,48 +144,93 @@ __device__ void find_bin_from_top(const uint32_t* cnt /*smem*/, int nbins, uint3
     __syncthreads();
 }
 
-// ---- S2-S4 fused: one CTA per head -------------------------------------------------------------
-// S2: the bin holding the b-th largest key, from the histogram K1 (or S1) built.  S3: one pass over
-// the head's scores (4 rows per thread per 4096-row chunk, 8 chunks of loads in flight): rows
-// above that bin are counted per chunk in shared memory, rows inside it appended to the head's
-// candidate list (warp-aggregated).  S4: radix-select the remaining 21 bits over the candidates
-// -> exact threshold key T and the number of T-equal rows still needed, then the per-chunk output
-// offsets by a chunk scan.  No global round trip between the phases (they were three launches).
-constexpr int kPlanThreads = 512;   // 2 CTAs / SM: one wave for a few hundred heads
-constexpr int kPlanRows = kChunk / kPlanThreads;  // 8 rows of a chunk per thread (two float4)
-constexpr int kPlanBatch = 4;       // chunks of loads in flight per thread
-constexpr int kCandCap = 8192;      // candidates kept in shared memory (the rest go to the global list)
+// ---- S2-S4 fused: one thread-block cluster per head ----------------------------------------------
+// A head's chunks are split over the `cs` CTAs of a cluster (contiguous chunk ranges) while the
+// grid still fits the resident slots, so a handful of heads (one rank's share of a head-sharded
+// run) still use every SM; a few hundred heads run one CTA each.  Per CTA:
+//   S2  the bin holding the b-th largest key, from the histogram K1 (or S1) built (every CTA of
+//       the cluster derives the same bin).
+//   S3  one pass over its chunks' scores in the float domain (the next step's loads in flight while
+//       a step is processed): rows above the bin counted per chunk (one warp reduction per chunk),
+//       rows inside it appended (position + key, warp-aggregated slots) and histogrammed on the
+//       next 11 key bits on the spot.
+//   S4  the cluster's histograms summed over distributed shared memory -> T's second digit; one
+//       sweep over the candidates: digit above it -> above T (per-chunk counts), equal -> the last
+//       10-bit histogram and a short list -> exact threshold key T and the number of T-equal rows
+//       still needed; the short list settles the per-chunk counts.  Per-chunk output offsets: a
+//       local chunk scan plus the cluster prefix of the lower ranks' totals (DSMEM).
+// No global round trip between the phases and no inter-CTA spin (cluster barriers only).
+constexpr int kPlanThreads = 512;
+constexpr int kPlanBatch = 2;                     // chunks per step (one per half of the CTA)
+constexpr int kPlanRows = kChunk * kPlanBatch / kPlanThreads;  // 16 contiguous rows of a chunk per thread
+constexpr int kCandCap = 8192;                    // candidates per CTA in shared memory (rest: global)
+constexpr int kPlanMaxCs = 8;                     // portable cluster size
+constexpr int kPlanList = 512;                    // candidates sharing T's second digit (else a re-sweep)
 constexpr size_t kPlanSmem = 2 * sizeof(uint32_t) * kCandCap;  // dynamic: positions + keys
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cluster_size() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t dsmem_ld_u32(const uint32_t* local, uint32_t rank) {
+    uint32_t v;
+    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(dsmem_map(smem_u32(local), rank)) : "memory");
+    return v;
+}
+
+// sum the cluster's `nbins`-bin histograms `mine` (every rank's copy) into `out` (local)
+__device__ __forceinline__ void cluster_hist_sum(const uint32_t* mine, uint32_t* out, int nbins, uint32_t cs) {
+    cluster_sync_all();  // every rank's histogram complete
+    for (int i = threadIdx.x; i < nbins; i += kPlanThreads) {
+        uint32_t v = 0;
+        for (uint32_t r = 0; r < cs; ++r) v += dsmem_ld_u32(mine + i, r);
+        out[i] = v;
+    }
+    cluster_sync_all();  // every rank done reading `mine` (it is reused next)
+}
 
 __global__ void __launch_bounds__(kPlanThreads, 2) select_plan_kernel(const __grid_constant__ SelectParams p) {
     pdl_wait();
-    __shared__ uint32_t cnt[2048];
+    __shared__ uint32_t cnt[2048];   // local histogram (read by the cluster)
+    __shared__ uint32_t cnt2[2048];  // the cluster's sum
     __shared__ uint32_t c_gt[kMaxChunksPerHead];
     __shared__ uint32_t c_eq[kMaxChunksPerHead];
     extern __shared__ uint32_t plan_dyn[];
     uint32_t* s_cpos = plan_dyn;
     uint32_t* s_ckey = plan_dyn + kCandCap;
     __shared__ uint32_t s_scan[33];
-    __shared__ uint32_t s_bin, s_above, s_ncand;
-    const int head = blockIdx.x;
+    __shared__ uint32_t s_bin, s_above, s_ncand, s_nlist;
+    __shared__ uint32_t s_lpos[kPlanList], s_lkey[kPlanList];  // candidates in T's 11-bit digit
+    __shared__ uint32_t s_tot[2];    // this rank's equal-to-T and kept totals (read by higher ranks)
+    const uint32_t cs = cluster_size(), crank = cluster_rank();
+    const int head = blockIdx.x / cs;
     const int s_idx = head_seq(p.seq, head);
     const int t = p.seq.len[s_idx];
     const int b = p.budgets[head];
     HeadSel* st = p.state + head;
-    if (b < 0 || b > t) {  // budget outside [0, t] (hard_topk, soft_topk.cpp:193)
-        if (threadIdx.x == 0) latch_error(p.err, LKV_ERR_BUDGET, head);
+    if (b < 0 || b > t) {  // budget outside [0, t] (hard_topk, soft_topk.cpp:193); uniform over the cluster
+        if (threadIdx.x == 0 && crank == 0) latch_error(p.err, LKV_ERR_BUDGET, head);
         return;
     }
     const int cph = (t + kChunk - 1) / kChunk;
+    const int c_lo = (int)((int64_t)cph * crank / cs), c_hi = (int)((int64_t)cph * (crank + 1) / cs);
+    const int nch = c_hi - c_lo;
     const int hs = head - s_idx * p.seq.n_layers * p.seq.n_kv_heads;
     const int cbase = p.chunk_base[s_idx] + hs * cph;
     const uint32_t mode = b == 0 ? kModeNone : (b == t ? kModeAll : kModeNormal);
     const int tid = threadIdx.x, lane = tid & 31;
-    for (int c = tid; c < cph; c += kPlanThreads) {
+    for (int c = tid; c < nch; c += kPlanThreads) {
         c_gt[c] = 0;
         c_eq[c] = 0;
     }
     if (tid == 0) s_ncand = 0;
+    for (int i = tid; i < 2048; i += kPlanThreads) cnt[i] = 0;  // pass-A histogram, filled during S3
     uint32_t key_t = 0, need_eq = 0;
     if (mode == kModeNormal) {
         // S2
@@ -195,19 +240,18 @@ __global__ void __launch_bounds__(kPlanThreads, 2) select_plan_kernel(const __gr
 #pragma unroll
             for (int q = 0; q < 2048 / kPlanThreads; ++q) hv[q] = gh[tid + q * kPlanThreads];
 #pragma unroll
-            for (int q = 0; q < 2048 / kPlanThreads; ++q) cnt[tid + q * kPlanThreads] = hv[q];
+            for (int q = 0; q < 2048 / kPlanThreads; ++q) cnt2[tid + q * kPlanThreads] = hv[q];
         }
         __syncthreads();
-        find_bin_from_top<kPlanThreads>(cnt, 2048, (uint32_t)b, s_scan, &s_bin, &s_above);
+        find_bin_from_top<kPlanThreads>(cnt2, 2048, (uint32_t)b, s_scan, &s_bin, &s_above);
         const uint32_t bin1 = s_bin;
         uint32_t rem = (uint32_t)b - s_above;
         // S3 in the float domain.  The bin's keys [bin1 << 21, ((bin1 + 1) << 21) - 1] are a float
         // interval, so a row lies above the bin iff x > g_thr and inside it iff x >= lo_f and not
         // above -- two compares per row, no key transform (IEEE compares treat -0.0 == +0.0, as the
-        // key does; NaN was rejected by K1).  Rows above are counted per warp with one reduction
-        // per chunk; the in-bin rows are appended (position + key) warp-aggregated.
+        // key does; NaN was rejected by K1).
         const float* sc = p.scores + (size_t)head * p.seq.T;
-        uint32_t* cand = p.cands + (size_t)head * p.seq.T;  // overflow past kCandCap
+        uint32_t* cand = p.cands + (size_t)head * p.seq.T + (size_t)c_lo * kChunk;  // overflow past kCandCap
         const uint32_t lo_key = bin1 << 21;
         const uint64_t hi1 = ((uint64_t)bin1 + 1) << 21;  // the first key above the bin
         const float lo_f = lo_key <= kKeyNegInf ? -INFINITY : key_to_f32(lo_key);
@@ -217,54 +261,55 @@ __global__ void __launch_bounds__(kPlanThreads, 2) select_plan_kernel(const __gr
         // 16-byte loads when every head's scores are 16-byte aligned: branch-free (the address
         // clamped into the head's row stride) so a batch's loads are all issued before the first use
         const bool vec = ((reinterpret_cast<uintptr_t>(sc)) & 15) == 0 && (T & 3) == 0;
-        for (int c0 = 0; c0 < cph; c0 += kPlanBatch) {
-            float v[kPlanBatch][kPlanRows];
+        // the loads of step i + 1 are issued before step i is processed (two register buffers)
+        // a step covers kPlanBatch chunks, the CTA's halves one chunk each: thread tid reads rows
+        // [j0, j0 + 16) of chunk c0 + u (u = tid / 256), four 16-byte loads
+        const int u = tid / (kChunk / kPlanRows), j0 = (tid % (kChunk / kPlanRows)) * kPlanRows;
+        auto load = [&](float (&v)[kPlanRows], int c0) {
+            if (c0 + u >= c_hi) return;  // warp-uniform; process() skips it too
             if (vec) {
 #pragma unroll
-                for (int u = 0; u < kPlanBatch; ++u)
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int r = min((c0 + u) * kChunk + tid * kPlanRows + 4 * h, T - 4);
-                        const float4 f = __ldg(reinterpret_cast<const float4*>(sc + r));
-                        v[u][4 * h + 0] = f.x;
-                        v[u][4 * h + 1] = f.y;
-                        v[u][4 * h + 2] = f.z;
-                        v[u][4 * h + 3] = f.w;
-                    }
-            } else {
-#pragma unroll
-                for (int u = 0; u < kPlanBatch; ++u) {
-                    const int r = (c0 + u) * kChunk + tid * kPlanRows;
-#pragma unroll
-                    for (int q = 0; q < kPlanRows; ++q) v[u][q] = r + q < t ? __ldg(sc + r + q) : -INFINITY;
+                for (int h = 0; h < kPlanRows / 4; ++h) {
+                    const int r = min((c0 + u) * kChunk + j0 + 4 * h, T - 4);
+                    const float4 f = __ldg(reinterpret_cast<const float4*>(sc + r));
+                    v[4 * h + 0] = f.x;
+                    v[4 * h + 1] = f.y;
+                    v[4 * h + 2] = f.z;
+                    v[4 * h + 3] = f.w;
                 }
-            }
+            } else {
+                const int r = (c0 + u) * kChunk + j0;
 #pragma unroll
-            for (int u = 0; u < kPlanBatch; ++u) {
-                const int c = c0 + u;
-                if (c >= cph) break;
-                const int r0 = c * kChunk + tid * kPlanRows;
+                for (int q = 0; q < kPlanRows; ++q) v[q] = r + q < t ? __ldg(sc + r + q) : -INFINITY;
+            }
+        };
+        // rows above the bin counted per chunk (one warp reduction); rows inside it appended
+        // (warp-aggregated slots) with their key, and counted in the pass-A histogram
+        auto process = [&](const float (&v)[kPlanRows], int c0) {
+            {
+                const int c = c0 + u;  // warp-uniform
+                if (c >= c_hi) return;
+                const int r0 = c * kChunk + j0;
                 uint32_t gt = 0, cm = 0;  // rows above the bin; bit mask of the rows inside it
                 if (c < full) {
 #pragma unroll
                     for (int q = 0; q < kPlanRows; ++q) {
-                        const bool above = v[u][q] > g_thr;
+                        const bool above = v[q] > g_thr;
                         gt += above;
-                        cm |= uint32_t(!above && v[u][q] >= lo_f) << q;
+                        cm |= uint32_t(!above && v[q] >= lo_f) << q;
                     }
                 } else {  // the head's last, partial chunk
 #pragma unroll
                     for (int q = 0; q < kPlanRows; ++q) {
                         const bool ok = r0 + q < t;
-                        const bool above = ok && v[u][q] > g_thr;
+                        const bool above = ok && v[q] > g_thr;
                         gt += above;
-                        cm |= uint32_t(ok && !above && v[u][q] >= lo_f) << q;
+                        cm |= uint32_t(ok && !above && v[q] >= lo_f) << q;
                     }
                 }
                 const uint32_t wgt = __reduce_add_sync(0xffffffffu, gt);
-                if (lane == 0 && wgt) atomicAdd(&c_gt[c], wgt);
-                if (!__any_sync(0xffffffffu, cm)) continue;
-                // warp-aggregated append of the in-bin rows (position and key)
+                if (lane == 0 && wgt) atomicAdd(&c_gt[c - c_lo], wgt);
+                if (!__any_sync(0xffffffffu, cm)) return;
                 const uint32_t nc = __popc(cm);
                 uint32_t incl = nc;
 #pragma unroll
@@ -272,17 +317,16 @@ __global__ void __launch_bounds__(kPlanThreads, 2) select_plan_kernel(const __gr
                     const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
                     if (lane >= o) incl += y;
                 }
-                const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
                 uint32_t base = 0;
-                if (lane == 31) base = atomicAdd(&s_ncand, wtot);
+                if (lane == 31) base = atomicAdd(&s_ncand, incl);
                 base = __shfl_sync(0xffffffffu, base, 31) + incl - nc;
                 while (cm) {  // only the rows inside the bin (a few % of them)
                     const int q = __ffs(cm) - 1;
                     cm &= cm - 1;
-                    float x = v[u][0];
-#pragma unroll
-                    for (int z = 1; z < kPlanRows; ++z) x = q == z ? v[u][z] : x;  // no local-memory indexing
-                    const uint32_t key = f32_key(x);
+                    // the row's score again (an L1 hit: its line was just loaded) instead of a
+                    // 16-way register select
+                    const uint32_t key = f32_key(__ldg(sc + r0 + q));
+                    atomicAdd(&cnt[(key >> 10) & 2047u], 1u);  // S4 pass A, fused
                     if (base < kCandCap) {
                         s_cpos[base] = (uint32_t)(r0 + q);
                         s_ckey[base] = key;
@@ -292,84 +336,139 @@ __global__ void __launch_bounds__(kPlanThreads, 2) select_plan_kernel(const __gr
                     ++base;
                 }
             }
+        };
+        {
+            float va[kPlanRows], vb[kPlanRows];
+            int c0 = c_lo;
+            if (c0 < c_hi) load(va, c0);
+            while (c0 < c_hi) {
+                if (c0 + kPlanBatch < c_hi) load(vb, c0 + kPlanBatch);
+                process(va, c0);
+                c0 += kPlanBatch;
+                if (c0 >= c_hi) break;
+                if (c0 + kPlanBatch < c_hi) load(va, c0 + kPlanBatch);
+                process(vb, c0);
+                c0 += kPlanBatch;
+            }
         }
         __syncthreads();
         const uint32_t n_cand = s_ncand;
         auto cand_key = [&](uint32_t i) -> uint32_t {
             return i < kCandCap ? s_ckey[i] : f32_key(sc[cand[i - kCandCap]]);
         };
-        // S4 pass A: key bits [10, 21) among the candidates
-        for (int i = tid; i < 2048; i += kPlanThreads) cnt[i] = 0;
-        __syncthreads();
-        for (uint32_t i = tid; i < n_cand; i += kPlanThreads) atomicAdd(&cnt[(cand_key(i) >> 10) & 2047u], 1u);
-        __syncthreads();
-        find_bin_from_top<kPlanThreads>(cnt, 2048, rem, s_scan, &s_bin, &s_above);
+        // S4 pass A (histogram of key bits [10, 21) built during S3): the digit of T
+        cluster_hist_sum(cnt, cnt2, 2048, cs);
+        find_bin_from_top<kPlanThreads>(cnt2, 2048, rem, s_scan, &s_bin, &s_above);
         const uint32_t binA = s_bin;
         rem -= s_above;
-        // pass B: key bits [0, 10) among candidates in binA
+        // pass B, one sweep over the candidates: digit above binA -> above T, counted per chunk (one
+        // atomic per (warp, chunk)); digit == binA -> low-10-bit histogram and the short list of
+        // rows whose order against T is still open
         for (int i = tid; i < 1024; i += kPlanThreads) cnt[i] = 0;
+        if (tid == 0) s_nlist = 0;
         __syncthreads();
-        for (uint32_t i = tid; i < n_cand; i += kPlanThreads) {
-            const uint32_t kk = cand_key(i);
-            if (((kk >> 10) & 2047u) == binA) atomicAdd(&cnt[kk & 1023u], 1u);
-        }
-        __syncthreads();
-        find_bin_from_top<kPlanThreads>(cnt, 1024, rem, s_scan, &s_bin, &s_above);
-        key_t = (bin1 << 21) | (binA << 10) | s_bin;
-        need_eq = rem - s_above;
-        // per chunk: candidates strictly above T, and equal to T (the list is roughly in chunk
-        // order, so lanes mostly agree on the chunk: one atomic per (warp, chunk, kind))
         for (uint32_t i0 = 0; i0 < n_cand; i0 += kPlanThreads) {
             const uint32_t i = i0 + tid;
-            int kind = -1;  // 0: above T, 1: equal to T
+            bool above = false;
             uint32_t ch = 0;
             if (i < n_cand) {
                 const uint32_t pos = i < kCandCap ? s_cpos[i] : cand[i - kCandCap];
                 const uint32_t kk = cand_key(i);
-                ch = pos / kChunk;
-                kind = kk > key_t ? 0 : (kk == key_t ? 1 : -1);
+                const uint32_t d = (kk >> 10) & 2047u;
+                ch = pos / kChunk - c_lo;
+                above = d > binA;
+                if (d == binA) {
+                    atomicAdd(&cnt[kk & 1023u], 1u);
+                    const uint32_t j = atomicAdd(&s_nlist, 1u);
+                    if (j < kPlanList) {
+                        s_lpos[j] = pos;
+                        s_lkey[j] = kk;
+                    }
+                }
             }
-            const uint32_t grp = __match_any_sync(0xffffffffu, kind < 0 ? 0xffffffffu : (ch << 1) | (uint32_t)kind);
-            if (kind >= 0 && lane == __ffs(grp) - 1) atomicAdd(kind ? &c_eq[ch] : &c_gt[ch], (uint32_t)__popc(grp));
+            const uint32_t grp = __match_any_sync(0xffffffffu, above ? ch : 0xffffffffu);
+            if (above && lane == __ffs(grp) - 1) atomicAdd(&c_gt[ch], (uint32_t)__popc(grp));
+        }
+        cluster_hist_sum(cnt, cnt2, 1024, cs);
+        find_bin_from_top<kPlanThreads>(cnt2, 1024, rem, s_scan, &s_bin, &s_above);
+        key_t = (bin1 << 21) | (binA << 10) | s_bin;
+        need_eq = rem - s_above;
+        // the open rows: above T or equal to T, per chunk (the list, or -- when it overflowed -- the
+        // candidates again)
+        const uint32_t n_list = s_nlist;
+        const bool listed = n_list <= (uint32_t)kPlanList;
+        const uint32_t n_open = listed ? n_list : n_cand;
+        for (uint32_t i = tid; i < n_open; i += kPlanThreads) {
+            uint32_t pos, kk;
+            if (listed) {
+                pos = s_lpos[i];
+                kk = s_lkey[i];
+            } else {
+                pos = i < kCandCap ? s_cpos[i] : cand[i - kCandCap];
+                kk = cand_key(i);
+                if (((kk >> 10) & 2047u) != binA) continue;
+            }
+            const uint32_t ch = pos / kChunk - c_lo;
+            if (kk > key_t) atomicAdd(&c_gt[ch], 1u);
+            else if (kk == key_t) atomicAdd(&c_eq[ch], 1u);
         }
     }
     __syncthreads();
-    // chunk scan (cph <= 1024): eq_before and out_base in index order, two chunks per thread
-    uint32_t gt2[2] = {0, 0}, eq2[2] = {0, 0};
+    // chunk scan over this rank's chunks (eq_before and out_base in index order), offset by the
+    // lower ranks' totals
+    constexpr int kPer = kMaxChunksPerHead / kPlanThreads;
+    uint32_t gtv[kPer], eqv[kPer], eq_loc = 0;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int c = tid * 2 + h;
-        if (c < cph) {
-            if (mode == kModeAll) gt2[h] = (uint32_t)min(kChunk, t - c * kChunk);
-            else if (mode == kModeNormal) gt2[h] = c_gt[c];
-            eq2[h] = c_eq[c];
+    for (int h = 0; h < kPer; ++h) {
+        const int c = tid * kPer + h;
+        gtv[h] = eqv[h] = 0;
+        if (c < nch) {
+            if (mode == kModeAll) gtv[h] = (uint32_t)min(kChunk, t - (c_lo + c) * kChunk);
+            else if (mode == kModeNormal) gtv[h] = c_gt[c];
+            eqv[h] = c_eq[c];
         }
+        eq_loc += eqv[h];
     }
-    uint32_t tot;
-    const uint32_t eqb0 = block_exclusive_scan<kPlanThreads>(eq2[0] + eq2[1], s_scan, &tot);
-    uint32_t kept2[2], eqb2[2] = {eqb0, eqb0 + eq2[0]};
+    uint32_t eq_tot;
+    uint32_t eqb = block_exclusive_scan<kPlanThreads>(eq_loc, s_scan, &eq_tot);
+    if (tid == 0) s_tot[0] = eq_tot;
+    cluster_sync_all();
+    uint32_t eq_base = 0;
+    for (uint32_t r = 0; r < crank; ++r) eq_base += dsmem_ld_u32(&s_tot[0], r);
+    eqb += eq_base;
+    uint32_t keptv[kPer], eqbv[kPer], kept_loc = 0;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        uint32_t take = 0;
-        if (need_eq > eqb2[h]) take = min(need_eq - eqb2[h], eq2[h]);
-        kept2[h] = gt2[h] + take;
+    for (int h = 0; h < kPer; ++h) {
+        eqbv[h] = eqb;
+        const uint32_t take = need_eq > eqb ? min(need_eq - eqb, eqv[h]) : 0u;
+        keptv[h] = gtv[h] + take;
+        kept_loc += keptv[h];
+        eqb += eqv[h];
     }
-    const uint32_t ob0 = block_exclusive_scan<kPlanThreads>(kept2[0] + kept2[1], s_scan, &tot);
+    uint32_t kept_tot;
+    uint32_t ob = block_exclusive_scan<kPlanThreads>(kept_loc, s_scan, &kept_tot);
+    if (tid == 0) s_tot[1] = kept_tot;
+    cluster_sync_all();
+    uint32_t out_base = 0;
+    for (uint32_t r = 0; r < crank; ++r) out_base += dsmem_ld_u32(&s_tot[1], r);
+    ob += out_base;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int c = tid * 2 + h;
-        if (c < cph) {
-            p.chunk_out[cbase + c] = ob0 + (h ? kept2[0] : 0u);
-            p.chunk_eqb[cbase + c] = eqb2[h];
+    for (int h = 0; h < kPer; ++h) {
+        const int c = tid * kPer + h;
+        if (c < nch) {
+            p.chunk_out[cbase + c_lo + c] = ob;
+            p.chunk_eqb[cbase + c_lo + c] = eqbv[h];
         }
+        ob += keptv[h];
     }
-    if (tid == 0) {
+    if (tid == 0 && crank == cs - 1) {
         st->mode = mode;
         st->key_t = key_t;
         st->need_eq = need_eq;
         p.out_lens[head] = b;
-        if (tot != (uint32_t)b) latch_error(p.err, LKV_ERR_NUMERIC, head);  // internal consistency
+        if (out_base + kept_tot != (uint32_t)b) latch_error(p.err, LKV_ERR_NUMERIC, head);  // internal consistency
     }
+    cluster_sync_all();  // no rank exits while another may still read its shared memory
 }
 
 // ---- row gather (16-byte vectors) ----------------------------------------------------------
@@ -666,7 +765,16 @@ cudaError_t launch_select(SelectParams p, int n_heads, cudaStream_t stream) {
     const cudaError_t attr =
         cudaFuncSetAttribute(select_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPlanSmem);
     if (attr != cudaSuccess) return attr;
-    if ((e = launch_pdl(select_plan_kernel, dim3(n_heads), dim3(kPlanThreads), kPlanSmem, stream, p)) != cudaSuccess) return e;
+    // cluster size: split heads while the grid still fits the resident slots (2 CTAs / SM), never
+    // below one chunk per CTA (cs <= the longest head's chunk count), at most the portable 8
+    int dev = 0, sms = 148, max_cph = 1;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    for (int s = 0; s < p.seq.n_seq; ++s) max_cph = max(max_cph, (p.seq.len[s] + kChunk - 1) / kChunk);
+    int cs = 1;
+    while (cs < kPlanMaxCs && 2 * cs <= max_cph && (int64_t)n_heads * cs * 2 <= 2 * (int64_t)sms) cs *= 2;
+    if ((e = launch_pdl_cluster(select_plan_kernel, dim3(n_heads * cs), dim3(kPlanThreads), kPlanSmem, stream, cs,
+                                p)) != cudaSuccess)
+        return e;
     if ((e = launch_pdl(select_emit_kernel, dim3(chunks), dim3(kSelThreads), 0, stream, p)) != cudaSuccess) return e;
     note_launches(2);
     return cudaGetLastError();

@@ -21,10 +21,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--evict", type=int, default=3)
 ap.add_argument("--decode", type=int, default=3)
 ap.add_argument("--config", type=int, default=2)
+ap.add_argument("--n-layers", type=int, default=0, help="fewer layers (e.g. one rank's share of a head-sharded run)")
 a = ap.parse_args()
 cfg = synth.CONFIGS[a.config]
-cache = synth.make_cache(cfg)
-ev = lkv.Evictor(cache, synth.make_scorers(cfg), synth.make_logits(cfg), cfg.ratio, lkv.BUDGET_EXACT,
+cache = synth.make_cache(cfg, n_layers=a.n_layers or None)
+L = a.n_layers or cfg.n_layers
+ev = lkv.Evictor(cache, synth.make_scorers(cfg, n_layers=L), synth.make_logits(cfg, n_layers=L), cfg.ratio, lkv.BUDGET_EXACT,
                  decode_slack=a.decode + 8)
 for _ in range(a.evict):
     ev.launch()
