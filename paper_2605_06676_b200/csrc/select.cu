@@ -184,15 +184,25 @@ __device__ __forceinline__ uint32_t dsmem_ld_u32(const uint32_t* local, uint32_t
     return v;
 }
 
+// cluster barrier; a plain CTA barrier when the cluster is this CTA alone (no cluster-scope fences)
+__device__ __forceinline__ void plan_sync(uint32_t cs) {
+    if (cs == 1) __syncthreads();
+    else cluster_sync_all();
+}
+
 // sum the cluster's `nbins`-bin histograms `mine` (every rank's copy) into `out` (local)
 __device__ __forceinline__ void cluster_hist_sum(const uint32_t* mine, uint32_t* out, int nbins, uint32_t cs) {
-    cluster_sync_all();  // every rank's histogram complete
-    for (int i = threadIdx.x; i < nbins; i += kPlanThreads) {
-        uint32_t v = 0;
-        for (uint32_t r = 0; r < cs; ++r) v += dsmem_ld_u32(mine + i, r);
-        out[i] = v;
+    plan_sync(cs);  // every rank's histogram complete
+    if (cs == 1) {
+        for (int i = threadIdx.x; i < nbins; i += kPlanThreads) out[i] = mine[i];
+    } else {
+        for (int i = threadIdx.x; i < nbins; i += kPlanThreads) {
+            uint32_t v = 0;
+            for (uint32_t r = 0; r < cs; ++r) v += dsmem_ld_u32(mine + i, r);
+            out[i] = v;
+        }
     }
-    cluster_sync_all();  // every rank done reading `mine` (it is reused next)
+    plan_sync(cs);  // every rank done reading `mine` (it is reused next)
 }
 
 __global__ void __launch_bounds__(kPlanThreads, 2) select_plan_kernel(const __grid_constant__ SelectParams p) {
@@ -323,9 +333,16 @@ __global__ void __launch_bounds__(kPlanThreads, 2) select_plan_kernel(const __gr
                 while (cm) {  // only the rows inside the bin (a few % of them)
                     const int q = __ffs(cm) - 1;
                     cm &= cm - 1;
-                    // the row's score again (an L1 hit: its line was just loaded) instead of a
-                    // 16-way register select
-                    const uint32_t key = f32_key(__ldg(sc + r0 + q));
+                    // v[q] by a 4-level select tree on the bits of q (registers cannot be indexed;
+                    // re-reading the row from memory stalls on L2 when L1 has evicted the line)
+                    float h8[8], h4[4], h2[2];
+#pragma unroll
+                    for (int z = 0; z < 8; ++z) h8[z] = (q & 8) ? v[z + 8] : v[z];
+#pragma unroll
+                    for (int z = 0; z < 4; ++z) h4[z] = (q & 4) ? h8[z + 4] : h8[z];
+#pragma unroll
+                    for (int z = 0; z < 2; ++z) h2[z] = (q & 2) ? h4[z + 2] : h4[z];
+                    const uint32_t key = f32_key((q & 1) ? h2[1] : h2[0]);
                     atomicAdd(&cnt[(key >> 10) & 2047u], 1u);  // S4 pass A, fused
                     if (base < kCandCap) {
                         s_cpos[base] = (uint32_t)(r0 + q);
@@ -386,8 +403,15 @@ __global__ void __launch_bounds__(kPlanThreads, 2) select_plan_kernel(const __gr
                     }
                 }
             }
-            const uint32_t grp = __match_any_sync(0xffffffffu, above ? ch : 0xffffffffu);
-            if (above && lane == __ffs(grp) - 1) atomicAdd(&c_gt[ch], (uint32_t)__popc(grp));
+            // the list is in append order, mostly one chunk per warp: one atomic when all lanes
+            // agree, else one per lane
+            const uint32_t ch0 = __shfl_sync(0xffffffffu, ch, 0);
+            if (__all_sync(0xffffffffu, ch == ch0)) {
+                const uint32_t na = __popc(__ballot_sync(0xffffffffu, above));
+                if (lane == 0 && na) atomicAdd(&c_gt[ch0], na);
+            } else if (above) {
+                atomicAdd(&c_gt[ch], 1u);
+            }
         }
         cluster_hist_sum(cnt, cnt2, 1024, cs);
         find_bin_from_top<kPlanThreads>(cnt2, 1024, rem, s_scan, &s_bin, &s_above);
@@ -432,7 +456,7 @@ __global__ void __launch_bounds__(kPlanThreads, 2) select_plan_kernel(const __gr
     uint32_t eq_tot;
     uint32_t eqb = block_exclusive_scan<kPlanThreads>(eq_loc, s_scan, &eq_tot);
     if (tid == 0) s_tot[0] = eq_tot;
-    cluster_sync_all();
+    plan_sync(cs);
     uint32_t eq_base = 0;
     for (uint32_t r = 0; r < crank; ++r) eq_base += dsmem_ld_u32(&s_tot[0], r);
     eqb += eq_base;
@@ -448,7 +472,7 @@ __global__ void __launch_bounds__(kPlanThreads, 2) select_plan_kernel(const __gr
     uint32_t kept_tot;
     uint32_t ob = block_exclusive_scan<kPlanThreads>(kept_loc, s_scan, &kept_tot);
     if (tid == 0) s_tot[1] = kept_tot;
-    cluster_sync_all();
+    plan_sync(cs);
     uint32_t out_base = 0;
     for (uint32_t r = 0; r < crank; ++r) out_base += dsmem_ld_u32(&s_tot[1], r);
     ob += out_base;
@@ -468,7 +492,7 @@ __global__ void __launch_bounds__(kPlanThreads, 2) select_plan_kernel(const __gr
         p.out_lens[head] = b;
         if (out_base + kept_tot != (uint32_t)b) latch_error(p.err, LKV_ERR_NUMERIC, head);  // internal consistency
     }
-    cluster_sync_all();  // no rank exits while another may still read its shared memory
+    if (cs > 1) cluster_sync_all();  // no rank exits while another may still read its shared memory
 }
 
 // ---- row gather (16-byte vectors) ----------------------------------------------------------
