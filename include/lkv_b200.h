@@ -266,10 +266,11 @@ lkv_status lkv_evict_host_shard(const lkv_cache_desc* host_cache, void* dev_keys
                                 const lkv_ragged_desc* host_out, int32_t layers_per_chunk, void* workspace,
                                 size_t workspace_bytes, lkv_stream_t stream);
 /* Shards that own an arbitrary list of heads (LPT placement by budget, shard.lpt_assign): the
- * local cache describes them as n_layers = 1 x n_kv_heads = n_local (per sequence, in list order)
- * and head_ids (DEVICE int32 [n_local]) gives each local head's global flat index l * H + h; the
- * scorer table is indexed by local head.  K2 still solves all n_logits heads (bit-identical on
- * every rank); budgets_local / offsets_local follow the list order. */
+ * local cache holds them per sequence in list order, grouped any way as n_layers x n_kv_heads =
+ * n_local (e.g. groups of H, so lkv_evict_host_heads still uploads per group), and head_ids
+ * (DEVICE int32 [n_local]) gives local head j = l * n_kv_heads + h its global flat index; the scorer
+ * table is indexed by local head (stride_layer = n_kv_heads, stride_head = 1).  K2 still solves all
+ * n_logits heads (bit-identical on every rank); budgets_local / offsets_local follow the list order. */
 lkv_status lkv_budgets_heads(const double* logits, int32_t n_logits, double target_ratio, int32_t mode,
                              const int32_t* seq_lens, int32_t n_seq, int32_t decode_slack, const int32_t* head_ids,
                              int32_t n_local, double* ratios, int32_t* budgets_all, int32_t* budgets_local,
