@@ -1132,7 +1132,7 @@ lkv_status lkv_kv_project(const void* h, int32_t d_model, const void* wkv_t, con
     if (p.N % 256) return fail(LKV_ERR_UNSUPPORTED, "kv_project: 2 * n_kv_heads * head_dim must be a multiple of 256");
     CUtensorMap ma, mb;
     if ((st = make_map_bf16(&ma, h, (uint64_t)d_model, (uint64_t)p.M, 128))) return st;
-    if ((st = make_map_bf16(&mb, wkv_t, (uint64_t)d_model, (uint64_t)p.N, 256))) return st;
+    if ((st = make_map_bf16(&mb, wkv_t, (uint64_t)d_model, (uint64_t)p.N, 128))) return st;  // a CTA's half of N
     LKV_CUDA(launch_kv_project(p, ma, mb, num_sms(), (cudaStream_t)stream), "kv project");
     return LKV_OK;
 }
