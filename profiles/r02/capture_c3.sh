@@ -21,4 +21,5 @@ cap select_plan 1 $S
 cap select_emit 1 $S
 cap budgets 1 $S
 cap decode_attn 1 $S
+cap kv_project 0 python profiles/kvproj_time.py
 ls $P
