@@ -44,6 +44,8 @@ def test_tensor_core_and_tma_instructions_present():
     assert "UTCHMMA" in sass  # tcgen05.mma (scorer)
     assert "UTMALDG" in sass  # TMA tile loads
     assert "LDTM" in sass     # tcgen05.ld (TMEM epilogue)
+    # the K/V projection runs on CTA pairs: tcgen05.mma.cta_group::2, 2-SM TMA, multicast commit
+    assert "UTCHMMA.2CTA" in sass and "UTMALDG.2D.2CTA" in sass and "UTCBAR.2CTA.MULTICAST" in sass
 
 
 def test_status_names_and_version():

@@ -795,7 +795,7 @@ def test_rope_pack_matches_fp64_rope():  # tensor.cpp:586-623 convention, absolu
 @pytest.mark.parametrize("S,T,H,dm", [(2, 300, 2, 256), (1, 1024, 8, 512), (3, 129, 4, 64),
                                      (1, 20000, 8, 256), (2, 9000, 4, 1024)])  # the last two: many tiles per CTA
 def test_kv_project_matches_fp64_projection_and_rope(S, T, H, dm):
-    """lkv_kv_project (tcgen05 GEMM, RoPE + head-major pack in the epilogue) vs the fp64 oracle of
+    """lkv_kv_project (tcgen05 GEMM on CTA pairs, RoPE + head-major pack in the epilogue) vs the fp64 oracle of
     evictsim.cpp:133-145: k = rope(h Wk) at absolute positions, v = h Wv, on the same bf16 inputs;
     bf16 bar 1e-2 (observed ~3e-3: fp32 accumulation, one bf16 rounding of the output).  Token
     counts off the 128-row tile, several heads per 256-column tile."""
