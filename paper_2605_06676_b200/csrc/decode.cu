@@ -593,6 +593,18 @@ __global__ void __launch_bounds__(kCombCols * kCombSlices) decode_combine_kernel
         const float* pm = p.part_m + (size_t)base * G;
         const float* pl = p.part_l + (size_t)base * G;
         const float* po = p.part_o + (size_t)base * G * D;
+        static_assert(kCombSlices == 1 || kCombSlices == 4, "combine slices");
+        constexpr int S = kCombSlices;
+        const int col = threadIdx.x % kCombCols, sl = threadIdx.x / kCombCols;
+        const int e = blockIdx.y * kCombCols + col;
+        // the first block of this thread's partial outputs is requested now, together with phase
+        // 1's maxima and sums (one memory round trip instead of two before the sums can start)
+        float v[16];
+        if (e < G * D) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+                if (sl + k * S < nch) v[k] = po[(size_t)(sl + k * S) * G * D + e];
+        }
         // phase 1: all (chunk, g) maxima and sums in parallel -> shared memory
         float* s_m = s_w;                       // [nch * G] (reused for the weights below)
         __shared__ float s_l[kCombMaxChunks / 4];
@@ -631,36 +643,28 @@ __global__ void __launch_bounds__(kCombCols * kCombSlices) decode_combine_kernel
         // grid.y tiles the G*D outputs.  Chunk c is summed into partial c % 4 and the four partials
         // are added in order, whether one thread holds all four (kCombSlices = 1) or slice sl of
         // the threads holds partial sl (kCombSlices = 4): the result does not depend on the launch
-        // shape.  A thread's 16 chunk loads of a block are in flight together.
-        static_assert(kCombSlices == 1 || kCombSlices == 4, "combine slices");
-        constexpr int S = kCombSlices;
+        // shape.  A thread's 16 chunk loads of a block are in flight together (the first block's
+        // since before phase 1).
         __shared__ float s_part[S][kCombCols];
-        const int col = threadIdx.x % kCombCols, sl = threadIdx.x / kCombCols;
-        const int e = blockIdx.y * kCombCols + col;
         const int g = min(e, G * D - 1) / D;
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
         if (e < G * D) {
             int c = sl;
-            for (; c + 15 * S < nch; c += 16 * S) {
-                float v[16];
+            for (;;) {
+                const bool whole = c + 15 * S < nch;
 #pragma unroll
-                for (int k = 0; k < 16; ++k) v[k] = po[(size_t)(c + k * S) * G * D + e];
+                for (int k = 0; k < 16; ++k)
+                    if (whole || c + k * S < nch) {
+                        float& a = acc[S == 4 ? 0 : (k & 3)];
+                        a = fmaf(v[k], s_w[(c + k * S) * G + g], a);
+                    }
+                if (!whole) break;
+                c += 16 * S;
+                if (c >= nch) break;
 #pragma unroll
-                for (int k = 0; k < 16; ++k) {
-                    float& a = acc[S == 4 ? 0 : (k & 3)];
-                    a = fmaf(v[k], s_w[(c + k * S) * G + g], a);
-                }
+                for (int k = 0; k < 16; ++k)
+                    if (c + k * S < nch) v[k] = po[(size_t)(c + k * S) * G * D + e];
             }
-            float v[16];
-#pragma unroll
-            for (int k = 0; k < 16; ++k)
-                if (c + k * S < nch) v[k] = po[(size_t)(c + k * S) * G * D + e];
-#pragma unroll
-            for (int k = 0; k < 16; ++k)
-                if (c + k * S < nch) {
-                    float& a = acc[S == 4 ? 0 : (k & 3)];
-                    a = fmaf(v[k], s_w[(c + k * S) * G + g], a);
-                }
         }
         float sum;
         if constexpr (S == 4) {
