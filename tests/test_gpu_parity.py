@@ -239,6 +239,32 @@ def test_select_adversarial_ties(t):
         _select_case(scores, [t] * len(heads), [b] * len(heads))
 
 
+def test_select_cluster_split_ragged():
+    """Few heads (6) over ragged sequences (t = 5000 and 40000): the plan splits each head over a
+    4-CTA cluster, so the short heads' clusters have CTAs without chunks; budgets 0, t, t - 1, 1 and
+    interior ones, heavy ties in one head.  Indices and gathered rows vs the oracle."""
+    torch.manual_seed(77)
+    T, lens, D = 40000, [5000, 40000], 8
+    K = torch.randn(2, 1, 3, T, D, device=DEV)
+    V = torch.randn(2, 1, 3, T, D, device=DEV)
+    scores = torch.randn(2, 1, 3, T)
+    scores[1, 0, 2] = torch.randint(0, 4, (T,)).float()  # ties across every CTA of the cluster
+    cache = lkv.DenseCache(K, V, lens)
+    budgets = [[0, 5000, 1234], [1, 39999, 6000]]
+    rc = lkv.select(cache, scores.to(DEV), torch.tensor(budgets, dtype=torch.int32, device=DEV).reshape(-1),
+                    decode_slack=3)
+    offs, pos, ln = rc.offsets.cpu().numpy(), rc.positions.cpu().numpy(), rc.lens.cpu().numpy()
+    rk, Kn = to_np(rc.keys), to_np(K)
+    for s in range(2):
+        for h in range(3):
+            i, t, b = s * 3 + h, lens[s], budgets[s][h]
+            want = O.select_positions_f32(scores[s, 0, h, :t].numpy(), b)
+            assert ln[i] == b
+            assert (pos[offs[i]:offs[i] + b] == want).all(), (s, h)
+            if b:
+                assert (rk[offs[i]:offs[i] + b] == Kn[s, 0, h, want]).all()
+
+
 def test_select_extreme_values():
     t = 5000
     s = torch.randn(4, t)
