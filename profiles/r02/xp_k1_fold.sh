@@ -1,4 +1,4 @@
-# b1 folded into the MMA (fold) vs the committed epilogue bias add (v728): parity, then within-box timing
+# candidate build (fold = the working tree, e.g. Estrin) vs the committed (v728): parity, then within-box timing
 L=paper_2605_06676_b200
 cp $L/liblkv_b200_fold.so $L/liblkv_b200.so
 timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "score or config3 or evict or kv_project or layerwise" > gpurun_out/fold_tests.log 2>&1; echo tests=$?; tail -1 gpurun_out/fold_tests.log
