@@ -27,7 +27,8 @@ namespace lkv_dev {
 
 constexpr int kDecMaxCh = 1024;  // largest work item (rows); the plan picks 128..1024 per cache
 constexpr int kDecStageRows = 64;   // rows per pipeline stage
-constexpr int kDecStages = 2;       // x 32 KB per CTA
+constexpr int kDecStages = 2;       // x 32 KB per CTA (all-layer launches and G > 4)
+constexpr int kDecStagesLayer = 3;  // per-layer launches at G <= 4: the whole one-wave item in flight
 constexpr int kDecPerSm = 2;        // resident CTAs per SM
 constexpr int kDecConsumers = 4;    // consumer warps (16 rows of a stage each)
 constexpr int kDecThreads = (kDecConsumers + 1) * 32;
@@ -209,16 +210,16 @@ __device__ __forceinline__ uint32_t sw_off(int row, int q) {
 // ---- bf16 attention kernel (tensor cores) ------------------------------------------------------
 // HI: the group has more than 8 query heads, so rows 8..15 of the m16 fragments are live.
 // For G <= 8 those rows are zero padding: their accumulators are never kept in registers.
-template <bool HI>
+template <bool HI, int ST>
 __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
     decode_attn_bf16_kernel(const __grid_constant__ DecodeParams p, const __grid_constant__ CUtensorMap tmap_k,
                             const __grid_constant__ CUtensorMap tmap_v) {
     constexpr int kStageBytes = 2 * kDecStageRows * 256;  // K + V, 64 rows x 256 B each
     extern __shared__ unsigned char smem_dyn[];
     unsigned char* smem = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);  // aligned, still a __shared__ pointer
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kDecStages * kStageBytes);
-    uint64_t* empty = full + kDecStages;
-    float* red = reinterpret_cast<float*>(empty + kDecStages);  // [consumers][G][D + 2]
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * kStageBytes);
+    uint64_t* empty = full + ST;
+    float* red = reinterpret_cast<float*>(empty + ST);  // [consumers][G][D + 2]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int G = p.G;
@@ -231,7 +232,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
     const int it_lo = *p.item_lo, it_hi = *p.item_hi;
     const int ch = *p.ch;
     if (threadIdx.x == 0) {
-        for (int i = 0; i < kDecStages; ++i) {
+        for (int i = 0; i < ST; ++i) {
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], kDecConsumers);
         }
@@ -263,7 +264,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
                     tma_load_2d(dst + kDecStageRows * 128, &tmap_k, &full[st], 64, y, pol);
                     tma_load_2d(dst + 2 * kDecStageRows * 128, &tmap_v, &full[st], 0, y, pol);
                     tma_load_2d(dst + 3 * kDecStageRows * 128, &tmap_v, &full[st], 64, y, pol);
-                    if (++st == kDecStages) {
+                    if (++st == ST) {
                         st = 0;
                         ph ^= 1;
                     }
@@ -423,7 +424,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecPerSm)
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[st]);
-            if (++st == kDecStages) {
+            if (++st == ST) {
                 st = 0;
                 ph ^= 1;
             }
@@ -701,14 +702,23 @@ cudaError_t launch_decode_plan(const int64_t* offsets, int n_seq, int n_layers, 
     return cudaGetLastError();
 }
 
-size_t decode_bf16_smem(int G) {
-    return 1024 + kDecStages * (2 * kDecStageRows * 256) + 2 * kDecStages * 8 + (size_t)kDecConsumers * G * (128 + 2) * 4;
+size_t decode_bf16_smem(int G, int stages) {
+    return 1024 + stages * (2 * kDecStageRows * 256) + 2 * stages * 8 + (size_t)kDecConsumers * G * (128 + 2) * 4;
+}
+// a per-layer launch (the model step) of a G <= 4 group keeps its whole one-wave work item in
+// flight (3 stages, still 2 CTAs per SM); all-layer launches stream long items through 2 stages
+static int decode_stages(int q_layers, int G) { return (q_layers == 1 && G <= 4) ? kDecStagesLayer : kDecStages; }
+static void (*decode_bf16_kern(int G, int stages))(DecodeParams, CUtensorMap, CUtensorMap) {
+    if (G > 8) return decode_attn_bf16_kernel<true, kDecStages>;
+    return stages == kDecStagesLayer ? decode_attn_bf16_kernel<false, kDecStagesLayer>
+                                     : decode_attn_bf16_kernel<false, kDecStages>;
 }
 
 // resident CTAs of one bf16 decode launch (its persistent grid size): the one-wave plan target
-int decode_resident_ctas(int G, int num_sms) {
-    auto kern = G > 8 ? decode_attn_bf16_kernel<true> : decode_attn_bf16_kernel<false>;
-    const size_t smem = decode_bf16_smem(G);
+int decode_resident_ctas(int G, int num_sms) {  // of a per-layer launch (the model step's plan)
+    const int stages = decode_stages(1, G);
+    auto kern = decode_bf16_kern(G, stages);
+    const size_t smem = decode_bf16_smem(G, stages);
     int per_sm = 0;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDecThreads, smem) != cudaSuccess)
@@ -720,8 +730,9 @@ cudaError_t launch_decode(const DecodeParams& p, int dtype, const CUtensorMap* m
                           cudaStream_t stream) {
     if (p.max_items == 0) return cudaSuccess;
     if (dtype == LKV_BF16) {
-        const size_t smem = decode_bf16_smem(p.G);
-        auto kern = p.G > 8 ? decode_attn_bf16_kernel<true> : decode_attn_bf16_kernel<false>;
+        const int stages = decode_stages(p.q_layers, p.G);
+        const size_t smem = decode_bf16_smem(p.G, stages);
+        auto kern = decode_bf16_kern(p.G, stages);
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         int per_sm = 0;
