@@ -593,7 +593,7 @@ def run_sharded(args, rank, world, local_rank):
     if args.ratio:
         cfg = synth.Config(**{**cfg.__dict__, "ratio": args.ratio})
     hbm_peak, _, peak_src = load_peaks()
-    comm = sharded.Comm.from_process_group()
+    comm = sharded.TorchComm() if args.validate_one_gpu else sharded.Comm.from_process_group()
     L, H, D = cfg.n_layers, cfg.n_kv_heads, cfg.head_dim
     T = cfg.max_tokens
     all_logits = synth.make_logits(cfg, device=dev)
@@ -828,7 +828,10 @@ def run_sharded(args, rank, world, local_rank):
                               "frac_of_aggregate_hbm": step_bytes / (ms / 1e3) / 1e9 / (world * hbm_peak)},
             "k2_per_rank_ms": k2_ms,
             "load_imbalance": imbalance,
-            "exchange": "LKV-H logits allgatherv + decode-output gatherv via lkv_comm_* (NCCL)",
+            "exchange": ("LKV-H logits allgatherv + decode-output gatherv via gloo host collectives "
+                         "(--validate-one-gpu: every rank on GPU 0; a logic check, NOT a scaling number)"
+                         if args.validate_one_gpu else
+                         "LKV-H logits allgatherv + decode-output gatherv via lkv_comm_* (NCCL)"),
             "parity_gate": "budgets == CPU oracle on every rank; kept totals; one head per rank == oracle top-k",
             "peak_source": peak_src, "decode": decode, "e2e": e2e}), flush=True)
     comm.close()
@@ -877,6 +880,9 @@ def main():
     ap.add_argument("--sharded-path", action="store_true",
                     help="run the head-sharded code path even at N=1 (validates the N>1 path on one GPU)")
     ap.add_argument("--e2e-chunk", type=int, default=1, help="layers per host->device chunk in the e2e path")
+    ap.add_argument("--validate-one-gpu", action="store_true",
+                    help="logic check of the N-rank sharded path with every rank on GPU 0 and gloo host collectives "
+                         "instead of NCCL (no rank's kernels wait on another's); its timings are not scaling numbers")
     ap.add_argument("--shard", default="heads", choices=["batch", "heads"],
                     help="heads (default): the config's cache split by layer range over the GPUs (strong scaling, "
                          "NCCL logits/outputs exchange); batch: one sequence per GPU (weak scaling)")
@@ -893,11 +899,16 @@ def main():
         sys.exit(spawn(args.gpus))
     if args.gpus != world:
         log(f"--gpus {args.gpus} but WORLD_SIZE={world}: running {world} rank(s)")
+    if args.validate_one_gpu:
+        local_rank = 0
     if world > 1:
         import torch
 
         torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        if args.validate_one_gpu:
+            torch.distributed.init_process_group("gloo")
+        else:
+            torch.distributed.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
     try:
         if args.shard == "heads" and (world > 1 or args.sharded_path):
             run_sharded(args, rank, world, local_rank)

@@ -94,15 +94,20 @@ class TorchComm:
         self.dist, self.group = dist, group
         self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
 
+    def close(self):
+        pass
+
     def allgatherv(self, send, recv, counts, displs, stream=None):
         m = max(int(c) for c in counts)
-        pad = torch.zeros(m, dtype=recv.dtype, device=recv.device)
-        pad[: int(counts[self.rank])] = send.reshape(-1)[: int(counts[self.rank])]
+        # gloo exchanges host tensors: device data is staged through the host
+        host = self.dist.get_backend(self.group) == "gloo"
+        pad = torch.zeros(m, dtype=recv.dtype, device="cpu" if host else recv.device)
+        pad[: int(counts[self.rank])] = send.reshape(-1)[: int(counts[self.rank])].to(pad.device)
         parts = [torch.zeros_like(pad) for _ in range(self.world)]
         self.dist.all_gather(parts, pad, group=self.group)
         flat = recv.view(-1)
         for r in range(self.world):
-            flat[int(displs[r]): int(displs[r]) + int(counts[r])] = parts[r][: int(counts[r])]
+            flat[int(displs[r]): int(displs[r]) + int(counts[r])] = parts[r][: int(counts[r])].to(flat.device)
 
     def gatherv(self, send, recv, counts, displs, root=0, stream=None):
         tmp = torch.empty(int(sum(int(c) for c in counts)), dtype=send.dtype, device=send.device)
