@@ -2,12 +2,13 @@
 
     python profiles/prefill_time.py [--t 32768] [--reps 5]
 
-Per layer: the K/V projections (plain cuBLAS GEMMs x @ Wk, x @ Wv, as the model computes them),
-then lkv_rope_pack (RoPE at absolute positions + token-major -> head-major) and the per-layer
+Per layer (unfused form): the K/V projections (plain cuBLAS GEMMs x @ Wk, x @ Wv), then lkv_rope_pack (RoPE at absolute positions + token-major -> head-major) and the per-layer
 score/select into the one global ragged cache.  Reports the eviction-side time per layer (rope_pack
 + score + select, device-timed), rope_pack alone with its HBM GB/s (algorithmic bytes: read the
 two projections, write the two roped layers = 4 * T * H * D * 2 B), and the peak KV footprint
-versus the full cache (the evictsim.cpp:157-159 accounting).
+versus the full cache (the evictsim.cpp:157-159 accounting).  Fused form: hidden states ->
+lkv_kv_project (K/V GEMM on CTA pairs with RoPE + pack in the epilogue) -> score/select, all 32
+layers (ingest_layer_hidden), device-timed end to end.
 """
 import argparse
 import json
@@ -76,7 +77,29 @@ def main():
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6545.9
     full_kv = L * H * T * D * 2 * 2
+    # the fused path: hidden states -> lkv_kv_project (2-SM tcgen05 GEMM + RoPE + pack) -> score/select
+    wkv_t = prefill.kv_weights(wk, wv)
+    pf2 = prefill.LayerwisePrefill(1, L, H, D, T, [T], scorers, logits, cfg.ratio, lkv.BUDGET_EXACT, decode_slack=4)
+    for l in range(L):  # warm
+        pf2.ingest_layer_hidden(l, x, wkv_t)
+    pf2.finish()
+    tot_fused = 0.0
+    for _ in range(a.reps):
+        pf2 = prefill.LayerwisePrefill(1, L, H, D, T, [T], scorers, logits, cfg.ratio, lkv.BUDGET_EXACT,
+                                       decode_slack=4)
+        torch.cuda.synchronize()
+        ev[0].record()
+        for l in range(L):
+            pf2.ingest_layer_hidden(l, x, wkv_t)
+        ev[1].record()
+        torch.cuda.synchronize()
+        tot_fused += ev[0].elapsed_time(ev[1])
+        pf2.finish()
+    assert torch.equal(pf2.ragged.lens, pf.ragged.lens)
     print(json.dumps({
+        "fused_prefill_ms_all_layers": tot_fused / a.reps,
+        "fused_prefill_ms_per_layer": tot_fused / a.reps / L,
+        "unfused_ms_all_layers": (tot_gemm + tot_evict) / a.reps,
         "what": "layer-by-layer prefill eviction, C2 geometry (L32 H8 d128), bf16, R=0.15",
         "t": T, "evict_ms_per_layer": tot_evict / n, "evict_ms_all_layers": tot_evict / a.reps,
         "kv_gemms_ms_per_layer": tot_gemm / n,
