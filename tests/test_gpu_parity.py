@@ -819,7 +819,8 @@ def test_rope_pack_matches_fp64_rope():  # tensor.cpp:586-623 convention, absolu
 
 
 @pytest.mark.parametrize("S,T,H,dm", [(2, 300, 2, 256), (1, 1024, 8, 512), (3, 129, 4, 64),
-                                     (1, 20000, 8, 256), (2, 9000, 4, 1024)])  # the last two: many tiles per CTA
+                                     (1, 20000, 8, 256), (2, 9000, 4, 1024),  # these two: many tiles per pair
+                                     (1, 100, 1, 64), (1, 256, 1, 128)])  # one 256-row pair tile: partial / exact
 def test_kv_project_matches_fp64_projection_and_rope(S, T, H, dm):
     """lkv_kv_project (tcgen05 GEMM on CTA pairs, RoPE + head-major pack in the epilogue) vs the fp64 oracle of
     evictsim.cpp:133-145: k = rope(h Wk) at absolute positions, v = h Wv, on the same bf16 inputs;
