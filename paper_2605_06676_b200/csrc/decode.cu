@@ -598,14 +598,17 @@ __global__ void __launch_bounds__(kCombCols * kCombSlices) decode_combine_kernel
         constexpr int S = kCombSlices;
         const int col = threadIdx.x % kCombCols, sl = threadIdx.x / kCombCols;
         const int e = blockIdx.y * kCombCols + col;
-        // the first block of this thread's partial outputs is requested now, together with phase
-        // 1's maxima and sums (one memory round trip instead of two before the sums can start)
+        // per-layer launches (S = 4, a few heads): the first block of this thread's partial outputs
+        // is requested now, together with phase 1's maxima and sums (one memory round trip fewer on
+        // the step's critical path); all-layer launches keep their registers for occupancy
         float v[16];
-        if (e < G * D) {
+        auto load_block = [&](int c) {
 #pragma unroll
             for (int k = 0; k < 16; ++k)
-                if (sl + k * S < nch) v[k] = po[(size_t)(sl + k * S) * G * D + e];
-        }
+                if (c + k * S < nch) v[k] = po[(size_t)(c + k * S) * G * D + e];
+        };
+        if constexpr (S == 4)
+            if (e < G * D) load_block(sl);
         // phase 1: all (chunk, g) maxima and sums in parallel -> shared memory
         float* s_m = s_w;                       // [nch * G] (reused for the weights below)
         __shared__ float s_l[kCombMaxChunks / 4];
@@ -651,6 +654,7 @@ __global__ void __launch_bounds__(kCombCols * kCombSlices) decode_combine_kernel
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
         if (e < G * D) {
             int c = sl;
+            if constexpr (S != 4) load_block(c);
             for (;;) {
                 const bool whole = c + 15 * S < nch;
 #pragma unroll
@@ -662,9 +666,7 @@ __global__ void __launch_bounds__(kCombCols * kCombSlices) decode_combine_kernel
                 if (!whole) break;
                 c += 16 * S;
                 if (c >= nch) break;
-#pragma unroll
-                for (int k = 0; k < 16; ++k)
-                    if (c + k * S < nch) v[k] = po[(size_t)(c + k * S) * G * D + e];
+                load_block(c);
             }
         }
         float sum;
