@@ -190,8 +190,7 @@ __device__ __forceinline__ TileInfo decode_tile(const ScoreParams& p, int tile, 
 // ============================================================================
 constexpr int kTcRows = 128;  // UMMA M
 // Epilogue groups of 4 warps (one TMEM lane quarter each); group g drains accumulator
-// stage g, i.e. every E-th tile.  Warps 0..3: TMA producer, MMA issuer, TMEM allocator, bias-operand
-// builder (kFoldBias; else spare).
+// stage g, i.e. every E-th tile.  Warps 0..3: TMA producer, MMA issuer, TMEM allocator, spare.
 constexpr int kHistBins = 2048;  // top 11 key bits: the first radix digit of the top-k (select.cu)
 
 template <int N, int NBOX>
@@ -208,15 +207,7 @@ struct TcCfg {
     static constexpr int kAcc = kEpi * N;  // accumulator columns: one N-wide stage per epilogue group
     static constexpr int kTmemCols = (kAcc <= 32) ? 32 : (kAcc <= 64) ? 64 : (kAcc <= 128) ? 128 : (kAcc <= 256) ? 256 : 512;
     static_assert(kAcc <= 512, "TMEM holds 512 fp32 columns");
-    // b1 folded into the MMA as one more K=16 step: A = a ones column block (one 8-row swizzle atom,
-    // replicated by SBO = 0), B = b1 split exactly into three bf16 columns (hi + mid + lo) per hidden
-    // unit, built by the spare warp 3 for every scorer.  Takes the bias add out of the epilogue,
-    // whose FMA pipe bounds K1 (profiles/r02/k1_gelu_experiments.txt); only where it fits.
-    static constexpr int kBias = N * 128;  // the bias operand: N rows x one 128-byte swizzle row
-    static constexpr int kSmemBase = kStages * kAStage + kW + 256 + 2 * kEpi * N * 4 + kEpi * kHistBins * 4 + 1024;
-    static constexpr bool kFoldBias = kSmemBase + 1024 + kBias <= 227 * 1024;
-    static constexpr int kExtra = kFoldBias ? 1024 + kBias : 0;
-    static constexpr int kSmem = kSmemBase + kExtra;
+    static constexpr int kSmem = kStages * kAStage + kW + 256 + 2 * kEpi * N * 4 + kEpi * kHistBins * 4 + 1024;
     static_assert(kSmem <= 227 * 1024, "shared memory budget");
 };
 
@@ -233,18 +224,15 @@ __global__ void __launch_bounds__(TcCfg<N, NBOX>::kThreads, 1)
     unsigned char* smem = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);  // aligned, still a __shared__ pointer
     unsigned char* sA = smem;
     unsigned char* sW = smem + S * Cfg::kAStage;
-    unsigned char* sOnes = sW + Cfg::kW;        // (kFoldBias) 1 KB: the ones column block
-    unsigned char* sBias = sOnes + 1024;        // (kFoldBias) [N][128 B]: b1 hi / mid / lo
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sW + Cfg::kW + Cfg::kExtra);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sW + Cfg::kW);
     uint64_t* full = bars;              // [S]
     uint64_t* empty = bars + S;         // [S]
     uint64_t* tfull = bars + 2 * S;           // [kEpi]
     uint64_t* tempty = bars + 2 * S + kEpi;   // [kEpi]
     uint64_t* wfull = bars + 2 * S + 2 * kEpi;
     uint64_t* wempty = wfull + 1;
-    uint64_t* bfull = wempty + 1;  // (kFoldBias) the scorer's bias operand is built
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
-    float* sEpi = reinterpret_cast<float*>(sW + Cfg::kW + Cfg::kExtra + 256);  // [kEpi groups][b1 | w2][N]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wempty + 1);
+    float* sEpi = reinterpret_cast<float*>(sW + Cfg::kW + 256);  // [kEpi groups][b1 | w2][N]
     uint32_t* sHist = reinterpret_cast<uint32_t*>(sEpi + 2 * kEpi * N);  // [kEpi groups][kHistBins]
 
     const int warp = threadIdx.x >> 5;
@@ -266,7 +254,6 @@ __global__ void __launch_bounds__(TcCfg<N, NBOX>::kThreads, 1)
         }
         mbar_init(wfull, 1);
         mbar_init(wempty, 1);
-        mbar_init(bfull, 1);
         fence_barrier_init();
     }
     if (warp == 0 && lane == 0) {
@@ -275,16 +262,6 @@ __global__ void __launch_bounds__(TcCfg<N, NBOX>::kThreads, 1)
         tma_prefetch_desc(&tmap_w);
     }
     if (warp == 2) tmem_alloc(tmem_slot, Cfg::kTmemCols);
-    if (Cfg::kFoldBias && warp == 3) {
-        // the ones block: 8 rows x 128 B, logical 16-byte chunk 0 = (1, 1, 1, 0, ...) bf16, stored
-        // at physical chunk (0 ^ row) by the 128-byte swizzle; every other chunk zero
-        for (int e = lane; e < 64; e += 32) {
-            const int r = e >> 3, pc = e & 7;
-            const uint4 v = pc == r ? make_uint4(0x3F803F80u, 0x00003F80u, 0u, 0u) : make_uint4(0u, 0u, 0u, 0u);
-            *reinterpret_cast<uint4*>(sOnes + r * 128 + pc * 16) = v;
-        }
-        fence_proxy_async_smem();
-    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -337,7 +314,6 @@ __global__ void __launch_bounds__(TcCfg<N, NBOX>::kThreads, 1)
                 if (ti.scorer != cur) {
                     if (wuses > 0) umma_commit(wempty);  // old weights free once prior MMAs retire
                     mbar_wait(wfull, wuses & 1);
-                    if constexpr (Cfg::kFoldBias) mbar_wait(bfull, wuses & 1);
                     cur = ti.scorer;
                     ++wuses;
                 }
@@ -355,42 +331,8 @@ __global__ void __launch_bounds__(TcCfg<N, NBOX>::kThreads, 1)
                     const uint64_t bdesc = umma_desc_sw128(w_base + box * Cfg::kWBox + within * 32);
                     umma_bf16(d_tmem, adesc, bdesc, idesc, kk > 0 ? 1u : 0u);
                 }
-                if constexpr (Cfg::kFoldBias)  // + ones x (b1 hi, mid, lo): SBO 0 repeats the 8-row atom
-                    umma_bf16(d_tmem, umma_desc_sw128(smem_u32(sOnes)) & ~(uint64_t(0x3FFFu) << 32),
-                              umma_desc_sw128(smem_u32(sBias)), idesc, 1u);
                 umma_commit(&empty[st]);   // smem slot free when these MMAs retire
                 umma_commit(&tfull[acc]);  // accumulator ready
-            }
-        }
-    } else if (warp == 3) {
-        // ===================== bias operand builder (kFoldBias) =====================
-        if constexpr (Cfg::kFoldBias) {
-            int cur = -1, bl = 0;
-            TileCursor cur_t = cursor_at(p, t_begin, kTcRows);
-            for (int i = 0; i < n_local; ++i) {
-                if (i > 0) cursor_next(p, cur_t, kTcRows);
-                const TileInfo ti = cursor_info(p, cur_t, kTcRows);
-                if (ti.scorer == cur) continue;
-                if (bl > 0) mbar_wait(wempty, (bl - 1) & 1);  // the previous scorer's MMAs retired
-                // row n, logical chunk 0 = (hi, mid, lo, 0, ...) with hi + mid + lo == b1[n] exactly
-                for (int n = lane; n < N; n += 32) {
-                    const float b = p.b1[(size_t)ti.scorer * N + n];
-                    const __nv_bfloat16 hi = __float2bfloat16_rn(b);
-                    const float r1 = b - __bfloat162float(hi);
-                    const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
-                    const __nv_bfloat16 lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
-                    const uint32_t w0 = (uint32_t)__bfloat16_as_ushort(hi) | ((uint32_t)__bfloat16_as_ushort(mid) << 16);
-                    const uint32_t w1 = (uint32_t)__bfloat16_as_ushort(lo);
-#pragma unroll
-                    for (int pc = 0; pc < 8; ++pc)
-                        *reinterpret_cast<uint4*>(sBias + n * 128 + pc * 16) =
-                            pc == (n & 7) ? make_uint4(w0, w1, 0u, 0u) : make_uint4(0u, 0u, 0u, 0u);
-                }
-                fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(bfull);
-                cur = ti.scorer;
-                ++bl;
             }
         }
     } else if (warp >= 4) {
@@ -455,12 +397,8 @@ __global__ void __launch_bounds__(TcCfg<N, NBOX>::kThreads, 1)
                 for (int q = 0; q < kEpiChunk; q += 4) {
                     const float4 bb = *reinterpret_cast<const float4*>(s_b1 + c * kEpiChunk + q);
                     const float4 ww = *reinterpret_cast<const float4*>(s_w2 + c * kEpiChunk + q);
-                    float2 h0 = f2(__uint_as_float(r[q + 0]), __uint_as_float(r[q + 1]));
-                    float2 h1 = f2(__uint_as_float(r[q + 2]), __uint_as_float(r[q + 3]));
-                    if constexpr (!Cfg::kFoldBias) {
-                        h0 = __fadd2_rn(h0, f2(bb.x, bb.y));
-                        h1 = __fadd2_rn(h1, f2(bb.z, bb.w));
-                    }
+                    const float2 h0 = __fadd2_rn(f2(__uint_as_float(r[q + 0]), __uint_as_float(r[q + 1])), f2(bb.x, bb.y));
+                    const float2 h1 = __fadd2_rn(f2(__uint_as_float(r[q + 2]), __uint_as_float(r[q + 3])), f2(bb.z, bb.w));
                     s2 = __ffma2_rn(EpiAct2<ACT>::f(h0), f2(ww.x, ww.y), s2);
                     s2 = __ffma2_rn(EpiAct2<ACT>::f(h1), f2(ww.z, ww.w), s2);
                 }
