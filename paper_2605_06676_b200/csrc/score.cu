@@ -37,44 +37,18 @@ __device__ __forceinline__ float ex2_approx(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
-template <int ACT>
-struct EpiAct;
-template <>
-struct EpiAct<LKV_ACT_GELU_ERF> {
-    static constexpr float kW2Scale = 0.5f;
-    // Abramowitz-Stegun 7.1.28: erf(u) = 1 - (1 + a1 u + ... + a6 u^6)^-16, |error| <= 3e-7
-    // (1.7e-6 in fp32); u = |h|/sqrt2 folded into the coefficients.  One MUFU (rcp).
-    __device__ __forceinline__ static float f(float h) {
-        const float ah = fabsf(h);
-        float y = fmaf(5.382975000e-06f, ah, 4.889063564e-05f);
-        y = fmaf(y, ah, 3.800357500e-05f);
-        y = fmaf(y, ah, 3.277626324e-03f);
-        y = fmaf(y, ah, 2.114100615e-02f);
-        y = fmaf(y, ah, 4.986734697e-02f);
-        y = fmaf(y, ah, 1.0f);
-        y *= y;
-        y *= y;
-        y *= y;
-        y *= y;  // y^16 (inf for large |h| -> r = 0 -> erf = 1)
-        const float r = rcp_approx(y);
-        return fmaf(-ah, r, h + ah);  // 2 gelu(h) = h + |h| erf(|h|/sqrt2)
-    }
-};
-template <>
-struct EpiAct<LKV_ACT_SILU> {
-    static constexpr float kW2Scale = 1.0f;
-    __device__ __forceinline__ static float f(float h) {
-        return h * rcp_approx(1.0f + ex2_approx(h * -1.4426950408889634f));
-    }
-};
-// Packed-pair forms (sm_100 FFMA2/FMUL2/FADD2): the epilogue is issue-bound, so two
-// accumulator columns go through every FP32 instruction at once; MUFU stays scalar.
+// Packed-pair forms (sm_100 FFMA2/FMUL2/FADD2): the epilogue bounds K1 on the FMA pipe, so two
+// accumulator columns go through every FP32 instruction at once (scalar FFMA measured 17% slower
+// on K1, profiles/r02/k1_gelu_experiments.txt); MUFU stays scalar.
 __device__ __forceinline__ float2 f2(float x, float y) { return make_float2(x, y); }
 __device__ __forceinline__ float2 abs2(float2 v) { return make_float2(fabsf(v.x), fabsf(v.y)); }
 template <int ACT>
 struct EpiAct2;
 template <>
-struct EpiAct2<LKV_ACT_GELU_ERF> {  // 2 gelu(h), A&S 7.1.28 (see EpiAct)
+struct EpiAct2<LKV_ACT_GELU_ERF> {  // 2 gelu(h)
+    // Abramowitz-Stegun 7.1.28: erf(u) = 1 - (1 + a1 u + ... + a6 u^6)^-16, |error| <= 3e-7
+    // (1.7e-6 in fp32); u = |h|/sqrt2 folded into the coefficients.  One MUFU (rcp) per element;
+    // returns 2 gelu(h) = h + |h| erf(|h|/sqrt2), w2 pre-scaled by 0.5.
     static constexpr float kW2Scale = 0.5f;
     __device__ __forceinline__ static float2 f(float2 h) {
         const float2 ah = abs2(h);
