@@ -48,6 +48,7 @@ constexpr int kWsThreads = (kWsConsumers + 1) * 32;
 constexpr int kWsPerSm = 2;
 constexpr int kYPad = 17;                      // y[64][17]: columns x batch (B <= 16)
 constexpr int kWsMaxSplit = 1024;              // CTAs sharing one column group (<= KU + 1; K <= 130k)
+constexpr int kWsMaxCluster = 8;               // split-K cluster size bound (launch_gemv)
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
@@ -379,22 +380,62 @@ __global__ void __launch_bounds__(kWsThreads, kWsPerSm) wstream_gemv_kernel(cons
         ws_consume<NBT, SPLIT>(p, u0, u1, smem, full, empty, red, y, s_last, s_slot, st, ph);
     }
     if constexpr (SPLIT) {
-        // every thread of every CTA in the cluster (the producer warp too) joins both barriers
-        cluster_sync_all();
-        const int S = p.split;
-        if (rank == 0 && warp < kWsConsumers) {
-            const int tid = threadIdx.x;
-            const uint32_t ybase = smem_u32(&y[0][0]);
-            for (int e = tid; e < kWsCols * 16; e += kWsConsumers * 32) {
-                const int n = e >> 4, b = e & 15;
-                float v = y[n][b];
-                for (int r = 1; r < S; ++r) v += dsmem_ld(dsmem_map(ybase + (uint32_t)(n * kYPad + b) * 4u, r));
-                y[n][b] = v;
-            }
-            named_sync(1, kWsConsumers * 32);
-            gemv_epilogue<__nv_bfloat16>(p, c / S, y, tid, kWsConsumers * 32);
+        // Rank 0 sums the cluster's partial products (DSMEM, rank order) and runs the epilogue.  Only
+        // the live batch columns are summed, with every peer's load in flight at once.  A residual
+        // epilogue of <= 2 batch rows (Wo, down at decode batch sizes) is inlined: its x / gain loads
+        // are issued before the cluster barrier and the group's sum of squares is a warp reduction.
+        // Peers leave as soon as rank 0 has read their partials (split arrive / wait), freeing their
+        // slots for the next kernel's CTAs while rank 0 finishes the epilogue.
+        const int S = p.split, B = p.B, ngc = c / S;
+        const int tid = threadIdx.x;
+        const bool resid_fast = p.epi == EPI_RESID && !p.ss_in && B * kWsCols <= kWsConsumers * 32;
+        const int nl = tid & (kWsCols - 1), bb = tid >> 6, n = ngc * kWsCols + nl;
+        const bool mine = rank == 0 && warp < kWsConsumers && tid < B * kWsCols && n < p.N;
+        float xr = 0.f, gr = 0.f;
+        if (resid_fast && mine) {
+            xr = p.x[(size_t)bb * p.N + n];
+            if (p.gain_next) gr = __ldg(p.gain_next + n);
         }
-        cluster_sync_all();  // peers stay resident until rank 0 has read their partials
+        cluster_sync_all();  // every thread of every CTA in the cluster (the producer warp too)
+        if (rank == 0 && warp < kWsConsumers) {
+            const uint32_t ybase = smem_u32(&y[0][0]);
+            for (int e = tid; e < kWsCols * B; e += kWsConsumers * 32) {
+                const int en = e & (kWsCols - 1), eb = e >> 6;
+                const uint32_t a = ybase + (uint32_t)(en * kYPad + eb) * 4u;
+                float t[kWsMaxCluster];
+#pragma unroll
+                for (int r = 1; r < kWsMaxCluster; ++r)
+                    if (r < S) t[r] = dsmem_ld(dsmem_map(a, r));
+                float v = y[en][eb];
+#pragma unroll
+                for (int r = 1; r < kWsMaxCluster; ++r)
+                    if (r < S) v += t[r];
+                y[en][eb] = v;
+            }
+        }
+        __syncwarp();
+        cluster_arrive();  // rank 0's consumers: after their peer reads; everyone else: now
+        if (rank == 0 && warp < kWsConsumers) {
+            if (resid_fast) {
+                float v = 0.f;
+                if (mine) {
+                    v = xr + y[nl][bb];
+                    p.x[(size_t)bb * p.N + n] = v;
+                    if (p.gain_next) store_norm_act<__nv_bfloat16>(p.act_next, bb, n, p.N, p.nbt, v * gr);
+                }
+                // the group's sum of squares: warp w holds columns [32 (w & 1), +32) of batch row w / 2
+                float q = v * v;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+                if (lane == 0) red[warp] = q;
+                named_sync(1, kWsConsumers * 32);
+                if (tid < B) p.ss_part[(size_t)ngc * B + tid] = red[2 * tid] + red[2 * tid + 1];
+            } else {
+                named_sync(1, kWsConsumers * 32);
+                gemv_epilogue<__nv_bfloat16>(p, ngc, y, tid, kWsConsumers * 32);
+            }
+        }
+        cluster_wait();  // peers stay resident until rank 0 has read their partials
     }
 }
 
@@ -502,7 +543,8 @@ cudaError_t launch_gemv(const GemvParams& p, int dtype, int num_sms, cudaStream_
         const size_t smem = wstream_smem(p.nbt);
         // narrow matrices: cluster split-K with S CTAs per column group, S a power of two <= 8, used
         // when the NG * S CTAs still fill >= 80% of the one-wave slots (measured: Wo / down at S = 4
-        // beat stream-K; QKV at S = 3 was slower, odd cluster sizes pack poorly)
+        // beat stream-K; QKV at S = 3 was slower, also with the faster cluster reduction --
+        // profiles/r02/xp_qkv_split.sh: +35 us per step)
         int S = 1;
         while (S < 8 && (int64_t)p.NG * S * 2 <= cap && S * 2 <= p.KU) S *= 2;
         if (S >= 2 && (int64_t)p.NG * S * 5 >= cap * 4) {

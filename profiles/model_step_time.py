@@ -21,6 +21,21 @@ import paper_2605_06676_b200 as lkv  # noqa: E402
 from paper_2605_06676_b200 import model as M, synth  # noqa: E402
 
 
+def trace_replay(g, path):
+    """One replay with the experiment build's per-CTA (kind, entry, wait released, exit) records."""
+    import ctypes
+    import numpy as np
+    lib = ctypes.CDLL(lkv._abi.LIB_PATH)
+    lib.lkv_xp_trace.restype = ctypes.c_int32
+    lib.lkv_xp_trace(None, 0)
+    g.replay()
+    torch.cuda.synchronize()
+    rec = np.zeros(1 << 20, dtype=[("kind", "<u4"), ("cta", "<u4")] + [(f"t{i}", "<u8") for i in range(6)])
+    n = lib.lkv_xp_trace(rec.ctypes.data_as(ctypes.c_void_p), 1 << 20)
+    np.save(path, rec[:n])
+    print("trace records", n)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n-seq", type=int, default=1)
@@ -28,6 +43,8 @@ def main():
     ap.add_argument("--vocab", type=int, default=128256)
     ap.add_argument("--t", type=int, default=32768)
     ap.add_argument("--eager", action="store_true", help="eager steps, no graph (for ncu launch lists)")
+    ap.add_argument("--trace", default="",
+                    help="experiment builds with LKV_XP_TRACE: write one replay's per-CTA timeline here")
     ap.add_argument("--rows-per-item", type=int, default=0,
                     help="per-layer attention work-item rows (0: the one-wave plan)")
     a = ap.parse_args()
@@ -86,6 +103,8 @@ def main():
     torch.cuda.synchronize()
     model.ws.status()
     ms = e0.elapsed_time(e1) / a.steps
+    if a.trace:
+        trace_replay(g, a.trace)
     kv_rows = float(lens0.double().sum()) + 1.5 * a.steps * rc.n_heads + 3 * rc.n_heads
     kv_bytes = kv_rows * 2 * cfg.head_dim * 2
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
