@@ -77,19 +77,32 @@ __device__ __forceinline__ void store_norm_act(void* act, int b, int n, int dm, 
     else static_cast<float*>(act)[(size_t)b * dm + n] = v;
 }
 
+// Per-CTA values every epilogue of the launch shares, computed once by the consumers right after
+// griddepcontrol.wait (before the first unit), so no epilogue -- and no mid-stream group epilogue --
+// waits on their loads: the 1 / rms of the consumed activations' rmsnorm (model.cpp:48-53) and the
+// step position of each batch row (RoPE, EPI_QKV).
+__shared__ float ws_inv_rms[16];
+__shared__ int ws_pos[16];
+__device__ __forceinline__ void gemv_prologue(const GemvParams& p, int tid, int nthr) {
+    const int B = p.B, warp = tid >> 5, lane = tid & 31;
+    if (p.ss_in) {  // sum over the producer's per-group sums of squares: lanes stride, fixed-order tree
+        const int ngx = (p.norm_dm + 63) / 64;
+        for (int b = warp; b < B; b += nthr >> 5) {
+            float s = 0.f;
+            for (int gi = lane; gi < ngx; gi += 32) s += p.ss_in[(size_t)gi * B + b];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (lane == 0) ws_inv_rms[b] = 1.f / sqrtf(s / (float)p.norm_dm + p.norm_eps);
+        }
+    }
+    if (p.epi == EPI_QKV && tid < B) ws_pos[tid] = min(max(p.tokens_seen[tid], 0), p.max_seq - 1);
+}
+
 template <typename T>
 __device__ void gemv_epilogue(const GemvParams& p, int ng, float (*y)[kYPad], int tid, int nthr) {
     const int B = p.B;
-    if (p.ss_in) {  // rmsnorm (model.cpp:48-53) of the consumed activations: W^T (x g / rms) = (W^T x g) / rms
-        __shared__ float s_inv[16];
-        if (tid < B) {
-            const int ngx = (p.norm_dm + 63) / 64;
-            float s = 0.f;
-            for (int gi = 0; gi < ngx; ++gi) s += p.ss_in[(size_t)gi * B + tid];
-            s_inv[tid] = 1.f / sqrtf(s / (float)p.norm_dm + p.norm_eps);
-        }
-        named_sync(1, nthr);
-        for (int e = tid; e < kWsCols * B; e += nthr) y[e & 63][e >> 6] *= s_inv[e >> 6];
+    if (p.ss_in) {  // rmsnorm of the consumed activations: W^T (x g / rms) = (W^T x g) / rms
+        for (int e = tid; e < kWsCols * B; e += nthr) y[e & 63][e >> 6] *= ws_inv_rms[e >> 6];
         named_sync(1, nthr);
     }
     if (p.epi == EPI_QKV) {
@@ -110,7 +123,7 @@ __device__ void gemv_epilogue(const GemvParams& p, int ng, float (*y)[kYPad], in
                 dst = p.v_out, col = n - p.dm - p.dkv, ld = p.dkv, rot = false;
             }
             if (rot) {  // rope_row (model.cpp:38-46): pair j of the head, theta = pos * base^(-2j/d)
-                const int pos = min(max(p.tokens_seen[b], 0), p.max_seq - 1);
+                const int pos = ws_pos[b];
                 const float2 cs = p.rope[(size_t)pos * (D / 2) + (col % D) / 2];
                 const float r0 = a * cs.x - c * cs.y, r1 = a * cs.y + c * cs.x;
                 a = r0;
@@ -377,6 +390,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsPerSm) wstream_gemv_kernel(cons
         if constexpr (!SPLIT) return;
     } else {
         pdl_wait();
+        gemv_prologue(p, threadIdx.x, kWsConsumers * 32);  // ordered before every epilogue by its named barriers
         ws_consume<NBT, SPLIT>(p, u0, u1, smem, full, empty, red, y, s_last, s_slot, st, ph);
     }
     if constexpr (SPLIT) {
@@ -442,6 +456,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsPerSm) wstream_gemv_kernel(cons
 // ---- fp32 SIMT GEMV (correctness configs): one 64-thread block per column group ------------------
 __global__ void __launch_bounds__(64) gemv_f32_kernel(const __grid_constant__ GemvParams p) {
     pdl_wait();
+    gemv_prologue(p, threadIdx.x, 64);
     __shared__ float y[kWsCols][kYPad];
     const int ng = blockIdx.x, nl = threadIdx.x;
     const int ldw = p.NG * kWsCols;
@@ -557,7 +572,19 @@ cudaError_t launch_gemv(const GemvParams& p, int dtype, int num_sms, cudaStream_
             note_launches(1);
             return e;
         }
-        const int grid = (int)(U < cap ? U : cap);
+        int grid = (int)(U < cap ? U : cap);
+        // group-aligned stream-K grids: every column group split evenly over S CTAs (NG * S CTAs,
+        // >= 90% of the slots), or every CTA holding k whole groups (NG / k CTAs, >= 75%): no CTA's
+        // range crosses a group boundary, so no CTA pauses its weight stream for a mid-stream
+        // fix-up (Llama-3-8B step, profiles/r02/xp_align.sh: QKV 296 -> 288 CTAs, gate/up 296 ->
+        // 224, 3.136 -> 2.979 ms on the same box)
+        if (p.NG <= cap) {
+            const int64_t g2 = (int64_t)p.NG * (cap / p.NG);
+            if (g2 * 10 >= cap * 9 && g2 <= U) grid = (int)g2;
+        } else {
+            const int k = (int)((p.NG + cap - 1) / cap);
+            if (p.NG % k == 0 && (int64_t)(p.NG / k) * 4 >= cap * 3) grid = p.NG / k;
+        }
         auto kern = p.nbt == 1 ? wstream_gemv_kernel<1, false> : wstream_gemv_kernel<2, false>;
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
