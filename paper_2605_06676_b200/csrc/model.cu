@@ -77,25 +77,52 @@ __device__ __forceinline__ void store_norm_act(void* act, int b, int n, int dm, 
     else static_cast<float*>(act)[(size_t)b * dm + n] = v;
 }
 
-// Per-CTA values every epilogue of the launch shares, computed once by the consumers right after
-// griddepcontrol.wait (before the first unit), so no epilogue -- and no mid-stream group epilogue --
-// waits on their loads: the 1 / rms of the consumed activations' rmsnorm (model.cpp:48-53) and the
-// step position of each batch row (RoPE, EPI_QKV).
+// Per-CTA values every epilogue of the launch shares, computed once per CTA: the 1 / rms of the
+// consumed activations' rmsnorm (model.cpp:48-53) and the step position of each batch row (RoPE,
+// EPI_QKV).  The consumers issue the loads right after griddepcontrol.wait and finish the sums
+// after their first group's units (the loads fly under the MMAs), so neither the stream's start nor
+// any group epilogue waits on them.  Fast path: a warp per batch row (B <= 4 with the 4 consumer
+// warps), <= 128 producer groups (four loads per lane); otherwise the sums run synchronously in the
+// finish step.
 __shared__ float ws_inv_rms[16];
 __shared__ int ws_pos[16];
-__device__ __forceinline__ void gemv_prologue(const GemvParams& p, int tid, int nthr) {
+struct ProRegs {
+    float v[4];
+    int pos;
+};
+__device__ __forceinline__ bool prologue_fast(const GemvParams& p, int nthr) {
+    return p.B * 32 <= nthr && p.norm_dm <= 128 * 64;
+}
+__device__ __forceinline__ ProRegs gemv_prologue_issue(const GemvParams& p, int tid, int nthr) {
+    ProRegs r = {{0.f, 0.f, 0.f, 0.f}, 0};
+    const int warp = tid >> 5, lane = tid & 31;
+    if (p.ss_in && prologue_fast(p, nthr) && warp < p.B) {
+        const int ngx = (p.norm_dm + 63) / 64;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (lane + 32 * k < ngx) r.v[k] = p.ss_in[(size_t)(lane + 32 * k) * p.B + warp];
+    }
+    if (p.epi == EPI_QKV && tid < p.B) r.pos = p.tokens_seen[tid];
+    return r;
+}
+__device__ __forceinline__ void gemv_prologue_finish(const GemvParams& p, const ProRegs& r, int tid, int nthr) {
     const int B = p.B, warp = tid >> 5, lane = tid & 31;
-    if (p.ss_in) {  // sum over the producer's per-group sums of squares: lanes stride, fixed-order tree
+    if (p.ss_in) {  // lanes stride over the producer's per-group sums of squares, fixed-order tree
         const int ngx = (p.norm_dm + 63) / 64;
         for (int b = warp; b < B; b += nthr >> 5) {
-            float s = 0.f;
-            for (int gi = lane; gi < ngx; gi += 32) s += p.ss_in[(size_t)gi * B + b];
+            float s;
+            if (prologue_fast(p, nthr)) {
+                s = ((r.v[0] + r.v[1]) + r.v[2]) + r.v[3];
+            } else {
+                s = 0.f;
+                for (int gi = lane; gi < ngx; gi += 32) s += p.ss_in[(size_t)gi * B + b];
+            }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
             if (lane == 0) ws_inv_rms[b] = 1.f / sqrtf(s / (float)p.norm_dm + p.norm_eps);
         }
     }
-    if (p.epi == EPI_QKV && tid < B) ws_pos[tid] = min(max(p.tokens_seen[tid], 0), p.max_seq - 1);
+    if (p.epi == EPI_QKV && tid < B) ws_pos[tid] = min(max(r.pos, 0), p.max_seq - 1);
 }
 
 template <typename T>
@@ -236,6 +263,8 @@ __device__ __forceinline__ void ws_consume(const GemvParams& p, int64_t u0, int6
     const int g = lane >> 2, cq = (lane & 3) * 2;
     int64_t u = u0;
     const int ng_first = (int)(u0 / p.KU);
+    const ProRegs pro = gemv_prologue_issue(p, tid, kWsConsumers * 32);
+    bool pro_done = false;
     while (u < u1) {
         const int ng = (int)(u / p.KU);
         const int64_t gbeg = (int64_t)ng * p.KU, gend = gbeg + p.KU;
@@ -269,6 +298,10 @@ __device__ __forceinline__ void ws_consume(const GemvParams& p, int64_t u0, int6
                 st = 0;
                 ph ^= 1;
             }
+        }
+        if (!pro_done) {  // ordered before every epilogue by the named barriers below
+            gemv_prologue_finish(p, pro, tid, kWsConsumers * 32);
+            pro_done = true;
         }
         // ---- cross-warp reduction (fixed order) -> y[64][b]
         constexpr int BW = NBT * 8;
@@ -390,7 +423,6 @@ __global__ void __launch_bounds__(kWsThreads, kWsPerSm) wstream_gemv_kernel(cons
         if constexpr (!SPLIT) return;
     } else {
         pdl_wait();
-        gemv_prologue(p, threadIdx.x, kWsConsumers * 32);  // ordered before every epilogue by its named barriers
         ws_consume<NBT, SPLIT>(p, u0, u1, smem, full, empty, red, y, s_last, s_slot, st, ph);
     }
     if constexpr (SPLIT) {
@@ -456,7 +488,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsPerSm) wstream_gemv_kernel(cons
 // ---- fp32 SIMT GEMV (correctness configs): one 64-thread block per column group ------------------
 __global__ void __launch_bounds__(64) gemv_f32_kernel(const __grid_constant__ GemvParams p) {
     pdl_wait();
-    gemv_prologue(p, threadIdx.x, 64);
+    gemv_prologue_finish(p, gemv_prologue_issue(p, threadIdx.x, 64), threadIdx.x, 64);
     __shared__ float y[kWsCols][kYPad];
     const int ng = blockIdx.x, nl = threadIdx.x;
     const int ldw = p.NG * kWsCols;
