@@ -1683,6 +1683,7 @@ lkv_status lkv_model_decode_step(const lkv_model_desc* m, const void* weights, c
     dp.new_len = at<int32_t>(ws, w.dec.new_len);
     dp.err = err;
     dp.early_kv = g.dtype == LKV_BF16 ? 1 : 0;  // the step's first launch (embed) is fully serialised
+    dp.lens_deferred = 1;                        // advanced by the lm_head GEMV below
     CUtensorMap mk, mv;
     if (g.dtype == LKV_BF16) {
         if ((st = make_map_bf16(&mk, r->keys, 128, (uint64_t)r->capacity_rows, 64))) return st;
@@ -1735,6 +1736,10 @@ lkv_status lkv_model_decode_step(const lkv_model_desc* m, const void* weights, c
         q.act = act_h;
         q.epi = EPI_F32;
         q.ss_in = ss;  // final_norm's 1 / rms
+        q.lens_inc = r->lens;  // the step's deferred bookkeeping: every head + 1 row, every sequence + 1 token
+        q.n_lens = dp.n_heads;
+        q.seen_inc = tokens_seen;
+        q.n_seen = B;
         LKV_CUDA(launch_gemv(q, g.dtype, sms, s), "lm_head");
     }
     return LKV_OK;

@@ -575,7 +575,6 @@ __global__ void __launch_bounds__(kCombCols * kCombSlices) decode_combine_kernel
                                                                                 int single_chunk_done) {
     constexpr int kCombThreads = kCombCols * kCombSlices;
     pdl_trigger();  // the next GEMV may start streaming its weights
-    pdl_wait();
     __shared__ float s_w[kCombMaxChunks];  // [c * G + g] weight exp2(m_c - M_g) / L_g
     __shared__ float s_M[16], s_L[16];
     // blockIdx.x enumerates this launch's heads layer-major (as the plan does)
@@ -584,13 +583,16 @@ __global__ void __launch_bounds__(kCombCols * kCombSlices) decode_combine_kernel
     const int js = jr / p.n_kv_heads;
     const int head = (js * p.n_layers + p.layer0 + jl) * p.n_kv_heads + (jr - js * p.n_kv_heads);
     const int D = p.head_dim, G = p.G;
-    // the length the attention kernel saw: lens[head] itself is advanced below by the y = 0 CTA
-    // while other CTAs of the head may not have started (so it is never read here)
-    const int len_new = p.new_len[head];
-    const int ch = *p.ch;
+    const int ch = *p.ch;                  // the plan's (written before the step)
+    const int base = p.item_base[head];
+    // the length the attention kernel saw.  lens_deferred: lens is not written during the step, so
+    // it is read before the wait.  Otherwise lens[head] is advanced below by the y = 0 CTA while
+    // other CTAs of the head may not have started, so the attention kernel's copy is read.
+    int len_new = p.lens_deferred ? p.lens[head] + 1 : 0;
+    pdl_wait();
+    if (!p.lens_deferred) len_new = p.new_len[head];
     const int nch = (len_new + ch - 1) / ch;
     if (!(single_chunk_done && nch == 1) && nch * G <= kCombMaxChunks) {
-        const int base = p.item_base[head];
         const float* pm = p.part_m + (size_t)base * G;
         const float* pl = p.part_l + (size_t)base * G;
         const float* po = p.part_o + (size_t)base * G * D;
@@ -685,7 +687,7 @@ __global__ void __launch_bounds__(kCombCols * kCombSlices) decode_combine_kernel
     } else if (nch * G > kCombMaxChunks && threadIdx.x == 0 && blockIdx.y == 0) {
         latch_error(p.err, LKV_ERR_UNSUPPORTED, head);
     }
-    if (threadIdx.x == 0 && blockIdx.y == 0) {
+    if (!p.lens_deferred && threadIdx.x == 0 && blockIdx.y == 0) {
         p.lens[head] = len_new;
         // tokens_seen advances once per step, after the last layer's append (the position of
         // every layer's new row is the step's starting tokens_seen, model.cpp:218,246)

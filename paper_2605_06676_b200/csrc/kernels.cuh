@@ -169,6 +169,10 @@ struct DecodeParams {
     // writes these heads' rows or lens: the model step's per-layer launches, whose step starts
     // with a fully serialised launch (lkv_model_step).
     int32_t early_kv;
+    // 1: lens / tokens_seen are advanced by the step's last kernel (lkv_model_decode_step's lm_head
+    // GEMV), not by the combine: nothing writes lens while the step's layers run, so the combine
+    // reads a head's length and work-item range before griddepcontrol.wait
+    int32_t lens_deferred;
 };
 // target_items > 0: the largest power-of-two ch giving at least that many items per layer;
 // target_items < 0: the smallest ch (multiple of 64) whose busiest layer fits -target_items items;
@@ -266,6 +270,12 @@ struct GemvParams {
     int32_t nbt_out, ff;
     // EPI_F32
     float* f_out;
+    // step bookkeeping (the model step's last GEMV, CTA 0, after griddepcontrol.wait): lens[i] += 1
+    // for i < n_lens, tokens_seen[s] += 1 for s < n_seen (DecodeParams::lens_deferred)
+    int32_t* lens_inc;
+    int32_t n_lens;
+    int32_t* seen_inc;
+    int32_t n_seen;
 };
 cudaError_t launch_gemv(const GemvParams& p, int dtype, int num_sms, cudaStream_t stream);
 size_t gemv_max_grid(int num_sms);

@@ -84,6 +84,15 @@ __device__ __forceinline__ void store_norm_act(void* act, int b, int n, int dm, 
 // any group epilogue waits on them.  Fast path: a warp per batch row (B <= 4 with the 4 consumer
 // warps), <= 128 producer groups (four loads per lane); otherwise the sums run synchronously in the
 // finish step.
+// the decode step's deferred cache bookkeeping (DecodeParams::lens_deferred): every head of the step
+// gained one row and every sequence one token; run by CTA 0 of the step's last GEMV, whose wait
+// implies every layer's attention and combine have completed
+__device__ __forceinline__ void gemv_step_bookkeeping(const GemvParams& p, int tid, int nthr) {
+    if (blockIdx.x != 0) return;
+    for (int i = tid; i < p.n_lens; i += nthr) p.lens_inc[i] += 1;
+    for (int i = tid; i < p.n_seen; i += nthr) p.seen_inc[i] += 1;
+}
+
 __shared__ float ws_inv_rms[16];
 __shared__ int ws_pos[16];
 struct ProRegs {
@@ -264,6 +273,7 @@ __device__ __forceinline__ void ws_consume(const GemvParams& p, int64_t u0, int6
     int64_t u = u0;
     const int ng_first = (int)(u0 / p.KU);
     const ProRegs pro = gemv_prologue_issue(p, tid, kWsConsumers * 32);
+    if (p.n_lens | p.n_seen) gemv_step_bookkeeping(p, tid, kWsConsumers * 32);
     bool pro_done = false;
     while (u < u1) {
         const int ng = (int)(u / p.KU);
@@ -489,6 +499,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsPerSm) wstream_gemv_kernel(cons
 __global__ void __launch_bounds__(64) gemv_f32_kernel(const __grid_constant__ GemvParams p) {
     pdl_wait();
     gemv_prologue_finish(p, gemv_prologue_issue(p, threadIdx.x, 64), threadIdx.x, 64);
+    if (p.n_lens | p.n_seen) gemv_step_bookkeeping(p, threadIdx.x, 64);
     __shared__ float y[kWsCols][kYPad];
     const int ng = blockIdx.x, nl = threadIdx.x;
     const int ldw = p.NG * kWsCols;
