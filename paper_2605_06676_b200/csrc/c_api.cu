@@ -1637,6 +1637,10 @@ lkv_status lkv_model_decode_step(const lkv_model_desc* m, const void* weights, c
     gp.nbt_out = gp.nbt;
     gp.act_out = at<void>(ws, w.act_ff);
     gp.ff = g.ff;
+    // each GEMV CTA also warms the 4 weight units after its ring's first stages in L2 before
+    // griddepcontrol.wait (profiles/r02/xp_l2ahead*.sh: -0.3% per step; 8 units slower; Wo alone
+    // slower, every GEMV but Wo no better than none)
+    gp.l2_ahead = 4;
     auto gemv = [&](const MatGeom& mg, const unsigned char* wp, int epi, const void* act, int n_real,
                     auto&& tweak) -> cudaError_t {
         GemvParams q = gp;

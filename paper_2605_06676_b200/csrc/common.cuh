@@ -236,6 +236,12 @@ __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint3
         : "memory");
 }
 
+// 1-D bulk prefetch global -> L2 (no destination, no completion): warms lines a later read uses.
+// bytes and the address must be multiples of 16.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* gsrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gsrc), "r"(bytes) : "memory");
+}
+
 // the same with a thread-block cluster of `cluster_x` CTAs along x
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl_cluster(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,

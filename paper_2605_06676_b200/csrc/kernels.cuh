@@ -274,6 +274,9 @@ struct GemvParams {
     // for i < n_lens, tokens_seen[s] += 1 for s < n_seen (DecodeParams::lens_deferred)
     int32_t* lens_inc;
     int32_t n_lens;
+    // bf16: weight units past the ring's first stages that each CTA prefetches into L2 before
+    // griddepcontrol.wait (for a GEMV behind kernels that leave HBM idle: Wo behind the attention)
+    int32_t l2_ahead;
     int32_t* seen_inc;
     int32_t n_seen;
 };

@@ -242,6 +242,10 @@ __device__ __forceinline__ void ws_produce(const GemvParams& p, int64_t u0, int6
             bulk_g2s(smem + st * kStage + kWsUnitBytes, asrc + (size_t)(u % p.KU) * kActBytes, kActBytes, &full[st],
                      pol_a);
         if (i == npre - 1) {
+            // the next p.l2_ahead units after the ring's into L2 too, while the previous kernel finishes
+            if (fresh)
+                for (int64_t j = npre; j < n && j < npre + p.l2_ahead; ++j)
+                    bulk_prefetch_l2(wsrc + (size_t)(u0 + j) * kWsUnitBytes, kWsUnitBytes);
             gate();
             for (int j = 0; j < npre; ++j) {
                 const int sj = (st0 + j) % kWsStages;
