@@ -393,6 +393,89 @@ __device__ __forceinline__ void ws_consume(const GemvParams& p, int64_t u0, int6
     }
 }
 
+// The split-K cluster's tail (after every CTA's units): rank 0 sums the partial products and runs
+// the epilogue.  KE: outputs per consumer thread (1 when B <= 2, 8 up to B = 16).
+template <int KE>
+__device__ __forceinline__ void ws_split_tail(const GemvParams& p, int c, int rank, float (*y)[kYPad], float* red) {
+    constexpr int kE = KE;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // Rank 0 sums the cluster's partial products (DSMEM, rank order) and runs the epilogue.  Only
+    // the live batch columns are summed, every peer load of a thread's (up to 8) outputs in
+    // flight at once.  The residual epilogue (Wo, down) is inlined: its x / gain loads are
+    // issued before the cluster barrier and the group's sums of squares are warp reductions
+    // (element e = tid + 128 k: a warp holds 32 columns of one batch row).  Peers leave as soon
+    // as rank 0 has read their partials (split arrive / wait), freeing their slots for the
+    // next kernel's CTAs while rank 0 finishes the epilogue.
+    const int S = p.split, B = p.B, ngc = c / S;
+    const int tid = threadIdx.x;
+    const bool lead = rank == 0 && warp < kWsConsumers;
+    const bool resid_fast = p.epi == EPI_RESID && !p.ss_in;
+    float xr[kE], gr[kE];
+#pragma unroll
+    for (int k = 0; k < kE; ++k) {
+        xr[k] = gr[k] = 0.f;
+        const int e = tid + k * kWsConsumers * 32, n = ngc * kWsCols + (e & (kWsCols - 1));
+        if (resid_fast && lead && e < B * kWsCols && n < p.N) {
+            xr[k] = p.x[(size_t)(e >> 6) * p.N + n];
+            if (p.gain_next) gr[k] = __ldg(p.gain_next + n);
+        }
+    }
+    cluster_sync_all();  // every thread of every CTA in the cluster (the producer warp too)
+    if (lead) {
+        const uint32_t ybase = smem_u32(&y[0][0]);
+        float t[kE][kWsMaxCluster];
+#pragma unroll
+        for (int k = 0; k < kE; ++k) {
+            const int e = tid + k * kWsConsumers * 32;
+            if (e < B * kWsCols) {
+                const uint32_t a = ybase + (uint32_t)((e & (kWsCols - 1)) * kYPad + (e >> 6)) * 4u;
+#pragma unroll
+                for (int r = 1; r < kWsMaxCluster; ++r)
+                    if (r < S) t[k][r] = dsmem_ld(dsmem_map(a, r));
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kE; ++k) {
+            const int e = tid + k * kWsConsumers * 32;
+            if (e < B * kWsCols) {
+                float v = y[e & (kWsCols - 1)][e >> 6];
+#pragma unroll
+                for (int r = 1; r < kWsMaxCluster; ++r)
+                    if (r < S) v += t[k][r];
+                y[e & (kWsCols - 1)][e >> 6] = v;
+            }
+        }
+    }
+    __syncwarp();
+    cluster_arrive();  // rank 0's consumers: after their peer reads; everyone else: now
+    if (lead) {
+        if (resid_fast) {
+#pragma unroll
+            for (int k = 0; k < kE; ++k) {
+                const int e = tid + k * kWsConsumers * 32;  // warp-uniform row e >> 6
+                if (e >= B * kWsCols) break;
+                const int nl = e & (kWsCols - 1), bb = e >> 6, n = ngc * kWsCols + nl;
+                float v = 0.f;
+                if (n < p.N) {
+                    v = xr[k] + y[nl][bb];
+                    p.x[(size_t)bb * p.N + n] = v;
+                    if (p.gain_next) store_norm_act<__nv_bfloat16>(p.act_next, bb, n, p.N, p.nbt, v * gr[k]);
+                }
+                float q = v * v;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+                if (lane == 0) red[2 * bb + (nl >> 5)] = q;
+            }
+            named_sync(1, kWsConsumers * 32);
+            if (tid < B) p.ss_part[(size_t)ngc * B + tid] = red[2 * tid] + red[2 * tid + 1];
+        } else {
+            named_sync(1, kWsConsumers * 32);
+            gemv_epilogue<__nv_bfloat16>(p, ngc, y, tid, kWsConsumers * 32);
+        }
+    }
+    cluster_wait();  // peers stay resident until rank 0 has read their partials
+}
+
 template <int NBT, bool SPLIT>
 __global__ void __launch_bounds__(kWsThreads, kWsPerSm) wstream_gemv_kernel(const __grid_constant__ GemvParams p) {
     constexpr int kActBytes = 8 * NBT * 256;  // 8 k16 steps x NBT tiles x 32 lanes x 8 B
@@ -440,62 +523,9 @@ __global__ void __launch_bounds__(kWsThreads, kWsPerSm) wstream_gemv_kernel(cons
         ws_consume<NBT, SPLIT>(p, u0, u1, smem, full, empty, red, y, s_last, s_slot, st, ph);
     }
     if constexpr (SPLIT) {
-        // Rank 0 sums the cluster's partial products (DSMEM, rank order) and runs the epilogue.  Only
-        // the live batch columns are summed, with every peer's load in flight at once.  A residual
-        // epilogue of <= 2 batch rows (Wo, down at decode batch sizes) is inlined: its x / gain loads
-        // are issued before the cluster barrier and the group's sum of squares is a warp reduction.
-        // Peers leave as soon as rank 0 has read their partials (split arrive / wait), freeing their
-        // slots for the next kernel's CTAs while rank 0 finishes the epilogue.
-        const int S = p.split, B = p.B, ngc = c / S;
-        const int tid = threadIdx.x;
-        const bool resid_fast = p.epi == EPI_RESID && !p.ss_in && B * kWsCols <= kWsConsumers * 32;
-        const int nl = tid & (kWsCols - 1), bb = tid >> 6, n = ngc * kWsCols + nl;
-        const bool mine = rank == 0 && warp < kWsConsumers && tid < B * kWsCols && n < p.N;
-        float xr = 0.f, gr = 0.f;
-        if (resid_fast && mine) {
-            xr = p.x[(size_t)bb * p.N + n];
-            if (p.gain_next) gr = __ldg(p.gain_next + n);
-        }
-        cluster_sync_all();  // every thread of every CTA in the cluster (the producer warp too)
-        if (rank == 0 && warp < kWsConsumers) {
-            const uint32_t ybase = smem_u32(&y[0][0]);
-            for (int e = tid; e < kWsCols * B; e += kWsConsumers * 32) {
-                const int en = e & (kWsCols - 1), eb = e >> 6;
-                const uint32_t a = ybase + (uint32_t)(en * kYPad + eb) * 4u;
-                float t[kWsMaxCluster];
-#pragma unroll
-                for (int r = 1; r < kWsMaxCluster; ++r)
-                    if (r < S) t[r] = dsmem_ld(dsmem_map(a, r));
-                float v = y[en][eb];
-#pragma unroll
-                for (int r = 1; r < kWsMaxCluster; ++r)
-                    if (r < S) v += t[r];
-                y[en][eb] = v;
-            }
-        }
-        __syncwarp();
-        cluster_arrive();  // rank 0's consumers: after their peer reads; everyone else: now
-        if (rank == 0 && warp < kWsConsumers) {
-            if (resid_fast) {
-                float v = 0.f;
-                if (mine) {
-                    v = xr + y[nl][bb];
-                    p.x[(size_t)bb * p.N + n] = v;
-                    if (p.gain_next) store_norm_act<__nv_bfloat16>(p.act_next, bb, n, p.N, p.nbt, v * gr);
-                }
-                // the group's sum of squares: warp w holds columns [32 (w & 1), +32) of batch row w / 2
-                float q = v * v;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
-                if (lane == 0) red[warp] = q;
-                named_sync(1, kWsConsumers * 32);
-                if (tid < B) p.ss_part[(size_t)ngc * B + tid] = red[2 * tid] + red[2 * tid + 1];
-            } else {
-                named_sync(1, kWsConsumers * 32);
-                gemv_epilogue<__nv_bfloat16>(p, ngc, y, tid, kWsConsumers * 32);
-            }
-        }
-        cluster_wait();  // peers stay resident until rank 0 has read their partials
+        // B <= 2 batch rows: one output per thread (the decode step's common case, fewest registers)
+        if (p.B * kWsCols <= kWsConsumers * 32) ws_split_tail<1>(p, c, rank, y, red);
+        else ws_split_tail<kWsCols * 16 / (kWsConsumers * 32)>(p, c, rank, y, red);
     }
 }
 
