@@ -1,0 +1,13 @@
+# same-box A/B of the model step (n_seq 1 and 16): the split-K merge inside the attention kernel
+# (last-arriving item, partials bulk-copied into its free ring; no combine launch) (fm) vs the
+# combine kernel (base); GPU tests of the decode paths on fm first
+L=paper_2605_06676_b200
+cp $L/liblkv_b200_fm.so $L/liblkv_b200.so
+python -m pytest tests/test_model_decode.py tests/test_gpu_parity.py -q -m gpu -k "decode or model" 2>&1 | tail -2
+for r in 1 2; do for v in base fm; do
+  cp $L/liblkv_b200_$v.so $L/liblkv_b200.so
+  echo "$v n1 $(python profiles/model_step_time.py --steps 50 2>/dev/null | tail -1 | grep -o '"ms_per_step": [0-9.]*')"
+  echo "$v n16 $(python profiles/model_step_time.py --steps 20 --n-seq 16 2>/dev/null | tail -1 | grep -o '"ms_per_step": [0-9.]*')"
+  echo "$v bench-decode $(python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu --no-sweep 2>/dev/null | tail -1 | grep -o '"decode[^}]*}' | head -c 300)"
+done; done
+cp $L/liblkv_b200_fm.so $L/liblkv_b200.so
