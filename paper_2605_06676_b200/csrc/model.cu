@@ -634,12 +634,12 @@ cudaError_t launch_gemv(const GemvParams& p, int dtype, int num_sms, cudaStream_
         const int64_t cap = (int64_t)kWsPerSm * num_sms;
         const size_t smem = wstream_smem(p.nbt);
         // narrow matrices: cluster split-K with S CTAs per column group, S a power of two <= 8, used
-        // when the NG * S CTAs still fill >= 80% of the one-wave slots (measured: Wo / down at S = 4
-        // beat stream-K; QKV at S = 3 was slower, also with the faster cluster reduction --
-        // profiles/r02/xp_qkv_split.sh: +35 us per step)
+        // when the NG * S CTAs still fill >= 60% of the one-wave slots (measured on the Llama-3-8B
+        // step: Wo / down at S = 4 beat stream-K; QKV at S = 2 (192 CTAs) beats the group-aligned
+        // stream-K by 2% of the step, S = 3 is 3% slower -- profiles/r02/xp_qkv_cluster.sh)
         int S = 1;
         while (S < 8 && (int64_t)p.NG * S * 2 <= cap && S * 2 <= p.KU) S *= 2;
-        if (S >= 2 && (int64_t)p.NG * S * 5 >= cap * 4) {
+        if (S >= 2 && (int64_t)p.NG * S * 5 >= cap * 3) {
             GemvParams q = p;
             q.split = S;
             auto kern = q.nbt == 1 ? wstream_gemv_kernel<1, true> : wstream_gemv_kernel<2, true>;
