@@ -576,7 +576,6 @@ __global__ void __launch_bounds__(kCombCols * kCombSlices) decode_combine_kernel
     constexpr int kCombThreads = kCombCols * kCombSlices;
     pdl_trigger();  // the next GEMV may start streaming its weights
     __shared__ float s_w[kCombMaxChunks];  // [c * G + g] weight exp2(m_c - M_g) / L_g
-    __shared__ float s_M[16], s_L[16];
     // blockIdx.x enumerates this launch's heads layer-major (as the plan does)
     const int per_layer = p.n_seq * p.n_kv_heads;
     const int jl = blockIdx.x / per_layer, jr = blockIdx.x - jl * per_layer;
@@ -611,37 +610,29 @@ __global__ void __launch_bounds__(kCombCols * kCombSlices) decode_combine_kernel
         };
         if constexpr (S == 4)
             if (e < G * D) load_block(sl);
-        // phase 1: all (chunk, g) maxima and sums in parallel -> shared memory
-        float* s_m = s_w;                       // [nch * G] (reused for the weights below)
-        __shared__ float s_l[kCombMaxChunks / 4];
-        const bool l_in_smem = nch * G <= kCombMaxChunks / 4;
-        for (int i = threadIdx.x; i < nch * G; i += kCombThreads) {
-            s_m[i] = pm[i];
-            if (l_in_smem) s_l[i] = pl[i];
-        }
-        __syncthreads();
+        // weights: one warp per query head g reads its (chunk) maxima and sums straight from the
+        // partials (lanes stride over chunks), reduces M and L by the xor tree, and writes
+        // exp2(m_c - M) / L for its chunks -- one CTA barrier before the weighted sums
         {
             const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-            for (int g = warp; g < G; g += kCombThreads / 32) {  // one warp per query head
-                float M = -INFINITY;
-                for (int c = lane; c < nch; c += 32) M = fmaxf(M, s_m[c * G + g]);
+            for (int g = warp; g < G; g += kCombThreads / 32) {
+                float m0 = -INFINITY, l0 = 0.f;  // this lane's first chunk (nch <= 32: the only one)
+                if (lane < nch) {
+                    m0 = pm[lane * G + g];
+                    l0 = pl[lane * G + g];
+                }
+                float M = m0;
+                for (int c = lane + 32; c < nch; c += 32) M = fmaxf(M, pm[c * G + g]);
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
                 float L = 0.f;
-                for (int c = lane; c < nch; c += 32)
-                    L += (l_in_smem ? s_l[c * G + g] : pl[c * G + g]) * exp2f(s_m[c * G + g] - M);
+                if (lane < nch) L += l0 * exp2f(m0 - M);
+                for (int c = lane + 32; c < nch; c += 32) L += pl[c * G + g] * exp2f(pm[c * G + g] - M);
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
-                if (lane == 0) {
-                    s_M[g] = M;
-                    s_L[g] = L;
-                }
+                if (lane < nch) s_w[lane * G + g] = exp2f(m0 - M) / L;
+                for (int c = lane + 32; c < nch; c += 32) s_w[c * G + g] = exp2f(pm[c * G + g] - M) / L;
             }
-        }
-        __syncthreads();
-        for (int i = threadIdx.x; i < nch * G; i += kCombThreads) {
-            const int g = i % G;
-            s_w[i] = exp2f(s_m[i] - s_M[g]) / s_L[g];
         }
         __syncthreads();
         const HeadCoord hc = head_coord(p, head);
