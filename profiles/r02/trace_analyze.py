@@ -9,7 +9,7 @@ import sys
 
 import numpy as np
 
-NAMES = {0: "qkv", 100: "attn", 101: "comb", 17: "wo|down", 2: "gate/up", 3: "lm_head"}
+NAMES = {0: "qkv", 16: "qkv", 100: "attn", 101: "comb", 17: "wo|down", 2: "gate/up", 3: "lm_head"}
 
 
 def main(path):
@@ -21,16 +21,17 @@ def main(path):
     for k in np.unique(kind):
         rk = r[kind == k]
         rk = rk[np.argsort(rk["t0"], kind="stable")]
-        n_l = {0: 32, 100: 32, 101: 32, 17: 64, 2: 32, 3: 1}[int(k)]
+        n_l = {0: 32, 16: 32, 100: 32, 101: 32, 17: 64, 2: 32, 3: 1}[int(k)]
         per = len(rk) // n_l
         launches[int(k)] = [rk[i * per:(i + 1) * per] for i in range(n_l)]
         print(f"{NAMES[int(k)]:8s} launches {n_l} CTAs/launch {per} (records {len(rk)})")
     seq = []
     for l in range(32):
         wo, down = launches[17][2 * l], launches[17][2 * l + 1]
-        seq.append([("qkv", launches[0][l]), ("attn", launches[100][l]), ("comb", launches[101][l]), ("wo", wo),
+        qkv = launches[0] if 0 in launches else launches[16]  # stream-K or split-K cluster
+        seq.append([("qkv", qkv[l]), ("attn", launches[100][l]), ("comb", launches[101][l]), ("wo", wo),
                     ("gate/up", launches[2][l]), ("down", down)])
-    t_start = min(x["t0"].min() for x in launches[0][0:1])
+    t_start = seq[0][0][1]["t0"].min()
     t_end = launches[3][0]["t5"].max()
     print(f"step (first qkv entry -> lm_head exit): {(t_end - t_start) / 1e3:.1f} us")
     rows = {}
