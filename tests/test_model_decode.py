@@ -154,6 +154,18 @@ def test_model_decode_bf16_gqa8_long_cache(rows_per_item):
     _run(cfg, P, torch.bfloat16, n_seq=2, t=3000, steps=2, seed=13, tol=1e-2, slack=5, rows_per_item=rows_per_item)
 
 
+@pytest.mark.parametrize("n_seq", [1, 5, 16])
+def test_model_decode_bf16_wide_gemv_paths(n_seq):
+    """d_model 2048, G = 4, mlp 14336: the launch rules the Llama-3-8B step takes -- QKV (48 column
+    groups) and Wo / down (32) as split-K clusters with the DSMEM tail (one output per thread at
+    n_seq 1, eight at 5 and 16, two batch tiles at 16), gate/up (448 groups) as a group-aligned
+    stream-K grid of 224 CTAs holding two whole groups each, lm_head as stream-K with fix-ups."""
+    cfg = OM.ModelConfig(n_layers=2, n_query_heads=16, n_kv_heads=4, head_dim=128, vocab_size=1000, max_seq_len=512,
+                         mlp_hidden=14336)
+    P = OM.random_params(cfg, 31, norm_jitter=0.1)
+    _run(cfg, P, torch.bfloat16, n_seq=n_seq, t=96 if n_seq < 9 else 48, steps=2, seed=40 + n_seq, tol=1e-2)
+
+
 def test_model_decode_deterministic_and_graph():
     """Two identical steps are bit-identical (stream-K partials summed in CTA order), and a
     CUDA-graph replay equals the eager step."""
