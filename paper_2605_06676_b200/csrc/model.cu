@@ -42,7 +42,10 @@ namespace lkv_dev {
 constexpr int kWsCols = 64;                    // output columns per unit (4 m16 tiles)
 constexpr int kWsK = 128;                      // k per unit (8 k16 steps)
 constexpr int kWsUnitBytes = kWsCols * kWsK * 2;  // 16 KB of bf16
-constexpr int kWsStages = 4;
+// ring depth: 5 stages with one batch tile (2 CTAs per SM still fit; n_seq 4 -0.3%, n_seq 1 equal,
+// profiles/r02/xp_ws_stages.sh), 4 with two
+template <int NBT>
+constexpr int ws_stages() { return NBT == 1 ? 5 : 4; }
 constexpr int kWsConsumers = 4;
 constexpr int kWsThreads = (kWsConsumers + 1) * 32;
 constexpr int kWsPerSm = 2;
@@ -231,10 +234,10 @@ __device__ __forceinline__ void ws_produce(const GemvParams& p, int64_t u0, int6
     const unsigned char* wsrc = static_cast<const unsigned char*>(p.w);
     const unsigned char* asrc = static_cast<const unsigned char*>(p.act);
     const int64_t n = u1 - u0;
-    const int npre = (int)(n < kWsStages ? n : kWsStages);
+    const int npre = (int)(n < ws_stages<NBT>() ? n : ws_stages<NBT>());
     const int st0 = st;
     for (int64_t i = 0; i < n; ++i) {
-        if (!(fresh && i < kWsStages)) mbar_wait(&empty[st], ph ^ 1);
+        if (!(fresh && i < ws_stages<NBT>())) mbar_wait(&empty[st], ph ^ 1);
         mbar_arrive_expect_tx(&full[st], kStage);
         const int64_t u = u0 + i;
         bulk_g2s(smem + st * kStage, wsrc + (size_t)u * kWsUnitBytes, kWsUnitBytes, &full[st], pol_w);
@@ -248,12 +251,12 @@ __device__ __forceinline__ void ws_produce(const GemvParams& p, int64_t u0, int6
                     bulk_prefetch_l2(wsrc + (size_t)(u0 + j) * kWsUnitBytes, kWsUnitBytes);
             gate();
             for (int j = 0; j < npre; ++j) {
-                const int sj = (st0 + j) % kWsStages;
+                const int sj = (st0 + j) % ws_stages<NBT>();
                 bulk_g2s(smem + sj * kStage + kWsUnitBytes, asrc + (size_t)((u0 + j) % p.KU) * kActBytes, kActBytes,
                          &full[sj], pol_a);
             }
         }
-        if (++st == kWsStages) {
+        if (++st == ws_stages<NBT>()) {
             st = 0;
             ph ^= 1;
         }
@@ -308,7 +311,7 @@ __device__ __forceinline__ void ws_consume(const GemvParams& p, int64_t u0, int6
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[st]);
-            if (++st == kWsStages) {
+            if (++st == ws_stages<NBT>()) {
                 st = 0;
                 ph ^= 1;
             }
@@ -482,9 +485,9 @@ __global__ void __launch_bounds__(kWsThreads, kWsPerSm) wstream_gemv_kernel(cons
     constexpr int kStage = kWsUnitBytes + kActBytes;
     extern __shared__ unsigned char smem_raw[];
     unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);  // aligned, still a __shared__ pointer
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kWsStages * kStage);
-    uint64_t* empty = full + kWsStages;
-    float* red = reinterpret_cast<float*>(empty + kWsStages);  // [4][64][NBT * 8]
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + ws_stages<NBT>() * kStage);
+    uint64_t* empty = full + ws_stages<NBT>();
+    float* red = reinterpret_cast<float*>(empty + ws_stages<NBT>());  // [4][64][NBT * 8]
     float(*y)[kYPad] = reinterpret_cast<float(*)[kYPad]>(red + kWsConsumers * kWsCols * NBT * 8);
     int* s_last = reinterpret_cast<int*>(y + kWsCols);
     int* s_slot = s_last + 4;  // [kWsMaxSplit]: partial slots of the CTAs sharing a column group
@@ -504,7 +507,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsPerSm) wstream_gemv_kernel(cons
         u1 = unit_begin(c + 1, U, P);
     }
     if (threadIdx.x == 0) {
-        for (int i = 0; i < kWsStages; ++i) {
+        for (int i = 0; i < ws_stages<NBT>(); ++i) {
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], kWsConsumers);
         }
@@ -624,7 +627,8 @@ size_t gemv_max_grid(int num_sms) { return (size_t)kWsPerSm * num_sms; }
 
 static size_t wstream_smem(int nbt) {
     const size_t stage = kWsUnitBytes + 8 * nbt * 256;
-    return 128 + kWsStages * stage + 2 * kWsStages * 8 + (size_t)kWsConsumers * kWsCols * nbt * 8 * 4 +
+    const int stages = nbt == 1 ? ws_stages<1>() : ws_stages<2>();
+    return 128 + stages * stage + 2 * stages * 8 + (size_t)kWsConsumers * kWsCols * nbt * 8 * 4 +
            (size_t)kWsCols * kYPad * 4 + 16 + 4 * kWsMaxSplit;
 }
 
