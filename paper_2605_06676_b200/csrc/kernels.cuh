@@ -274,11 +274,11 @@ struct GemvParams {
     // for i < n_lens, tokens_seen[s] += 1 for s < n_seen (DecodeParams::lens_deferred)
     int32_t* lens_inc;
     int32_t n_lens;
-    // bf16: weight units past the ring's first stages that each CTA prefetches into L2 before
-    // griddepcontrol.wait (for a GEMV behind kernels that leave HBM idle: Wo behind the attention)
-    int32_t l2_ahead;
     int32_t* seen_inc;
     int32_t n_seen;
+    // bf16: weight units past the ring's first stages that each CTA prefetches into L2 before
+    // griddepcontrol.wait (4 in the model step; more, or whole matrices, measured slower)
+    int32_t l2_ahead;
 };
 cudaError_t launch_gemv(const GemvParams& p, int dtype, int num_sms, cudaStream_t stream);
 size_t gemv_max_grid(int num_sms);
