@@ -80,13 +80,6 @@ __device__ __forceinline__ void store_norm_act(void* act, int b, int n, int dm, 
     else static_cast<float*>(act)[(size_t)b * dm + n] = v;
 }
 
-// Per-CTA values every epilogue of the launch shares, computed once per CTA: the 1 / rms of the
-// consumed activations' rmsnorm (model.cpp:48-53) and the step position of each batch row (RoPE,
-// EPI_QKV).  The consumers issue the loads right after griddepcontrol.wait and finish the sums
-// after their first group's units (the loads fly under the MMAs), so neither the stream's start nor
-// any group epilogue waits on them.  Fast path: a warp per batch row (B <= 4 with the 4 consumer
-// warps), <= 128 producer groups (four loads per lane); otherwise the sums run synchronously in the
-// finish step.
 // the decode step's deferred cache bookkeeping (DecodeParams::lens_deferred): every head of the step
 // gained one row and every sequence one token; run by CTA 0 of the step's last GEMV, whose wait
 // implies every layer's attention and combine have completed
@@ -96,6 +89,13 @@ __device__ __forceinline__ void gemv_step_bookkeeping(const GemvParams& p, int t
     for (int i = tid; i < p.n_seen; i += nthr) p.seen_inc[i] += 1;
 }
 
+// Per-CTA values every epilogue of the launch shares, computed once per CTA: the 1 / rms of the
+// consumed activations' rmsnorm (model.cpp:48-53) and the step position of each batch row (RoPE,
+// EPI_QKV).  The consumers issue the loads right after griddepcontrol.wait and finish the sums
+// after their first group's units (the loads fly under the MMAs), so neither the stream's start nor
+// any group epilogue waits on them.  Fast path: a warp per batch row (B <= 4 with the 4 consumer
+// warps), <= 128 producer groups (four loads per lane); otherwise the sums run synchronously in the
+// finish step.
 __shared__ float ws_inv_rms[16];
 __shared__ int ws_pos[16];
 struct ProRegs {
