@@ -12,14 +12,17 @@
 //    128 k, stored in the register-fragment order of mma.m16n8k16 (A = W^T): one lds.128 per
 //    lane per 16x16 tile, no ldmatrix, no bank conflicts; units of a matrix form one contiguous
 //    stream [column group][k-unit];
-//  * a persistent grid (2 CTAs / SM) splits the unit stream EVENLY (stream-K): CTA c owns units
-//    [c U / P, (c+1) U / P), so every SM streams the same number of bytes whatever the shape;
+//  * one wave of CTAs (2 per SM) splits the units evenly, so every SM streams about the same
+//    bytes whatever the shape: narrow matrices as split-K thread-block clusters (S CTAs per
+//    column group, partials summed by rank 0 over DSMEM), the rest as stream-K (CTA c owns units
+//    [c U / P, (c+1) U / P)) on a grid aligned to column groups where one fits (S CTAs per group,
+//    or k whole groups per CTA), so that no CTA stops its stream for a mid-stream fix-up;
 //  * one producer thread moves each unit (plus the matching 2-4 KB slice of the packed
-//    activations) with a 1-D bulk TMA copy into a 4-stage mbarrier ring; the first stages'
-//    WEIGHT copies are issued before griddepcontrol.wait, i.e. while the previous kernel of
-//    the step is still finishing (PDL);
+//    activations) with a 1-D bulk TMA copy into a 5-stage (one batch tile) / 4-stage mbarrier
+//    ring; the first stages' WEIGHT copies, and 4 more units into L2, are issued before
+//    griddepcontrol.wait, i.e. while the previous kernel of the step is still finishing (PDL);
 //  * 4 consumer warps split each unit's 8 k-steps, accumulate on tensor cores (fp32), and
-//    reduce across warps in fixed order; a column group cut by a CTA boundary is finished by
+//    reduce across warps in fixed order; a column group shared by stream-K CTAs is finished by
 //    the last-arriving CTA, which sums the partials in CTA order (deterministic);
 //  * the epilogue is fused: RoPE + scatter into q / new k / new v (QKV), residual add + the
 //    group's sum of squares + x * gain of the next rmsnorm written as the next GEMV's packed
